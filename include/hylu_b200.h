@@ -1,0 +1,132 @@
+/* hylu_b200.h — C ABI of the B200-native HYLU numeric factorization / solve.
+ *
+ * The reference (arxiv/paper_2509_07690, Python package ``polylu``) exposes a pure
+ * Python API and ships no numeric/solve code; each entry
+ * point below replaces one SPEC operation and is bound by the ctypes layer in
+ * paper_2509_07690_b200/device.py, which presents the SPEC Python signatures:
+ *
+ *   hy_upload_symbolic            <- SymbolicStructure/PivotScale/Ordering upload
+ *                                    (outputs of SPEC.md:155,165,175-223)
+ *   hy_factorize                  <- factorize(A, ps, ord, sym, opts)
+ *   hy_refactorize                <- refactorize(A_new, prior, opts)
+ *   hy_solve                      <- solve(A, factors, ps, ord, b) w/o refinement
+ *                                    (forward/backward substitution)
+ *   hy_refactorize_solve_batched  <- B x [refactorize -> solve] sharing one symbolic
+ *                                    (BASELINE config 4; SURVEY §3 call stack 3)
+ *
+ * Conventions: plain pointers and sizes; device pointers are prefixed d_; every
+ * call is asynchronous on the given CUDA stream (0 = legacy default stream).
+ * Return codes map 1:1 to the reference exception classes (errors.py):
+ *   HY_OK 0, HY_DIMENSION_MISMATCH 1 (DimensionMismatch, errors.py:32),
+ *   HY_ZERO_DIAGONAL 2 (ZeroDiagonal, :52), HY_CYCLE_DETECTED 3 (CycleDetected, :56),
+ *   HY_NUMERIC_BREAKDOWN 4 (NumericBreakdown, :60), HY_PATTERN_MISMATCH 5
+ *   (PatternMismatch, :64), HY_CUDA_ERROR 10, HY_INVALID_ARGUMENT 11.
+ * NumericBreakdown is detected on the device: it is reported through the
+ * factors' status word (read it after synchronizing the stream).
+ * No C++ exception crosses the ABI.  A handle is bound to one device and is
+ * not re-entrant; use one handle per GPU.
+ */
+#ifndef HYLU_B200_H
+#define HYLU_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  HY_OK = 0,
+  HY_DIMENSION_MISMATCH = 1,
+  HY_ZERO_DIAGONAL = 2,
+  HY_CYCLE_DETECTED = 3,
+  HY_NUMERIC_BREAKDOWN = 4,
+  HY_PATTERN_MISMATCH = 5,
+  HY_CUDA_ERROR = 10,
+  HY_INVALID_ARGUMENT = 11
+};
+
+/* KernelMode (config.py:11-16) */
+enum { HY_ROWROW = 0, HY_SUPROW = 1, HY_SUPSUP = 2 };
+
+typedef struct hy_handle hy_handle;
+
+/* Host arrays describing the symbolic structure in node layout:
+ * node u spans factor rows [node_first[u], node_first[u+1]); its ascending column
+ * list is cols[colptr[u] .. colptr[u+1]) with L width nl[u]; its values are a
+ * dense row-major (rows x width) block at valoff[u].  Everything is copied to the
+ * device once; the host arrays may be freed after the call returns. */
+typedef struct {
+  int64_t n;            /* dimension */
+  int64_t nnodes;
+  int64_t nnz;          /* nnz(A) */
+  int32_t kernel_mode;  /* HY_ROWROW / HY_SUPROW / HY_SUPSUP (max tier) */
+  const int64_t *node_first;   /* [nnodes+1] */
+  const int8_t *node_kind;     /* [nnodes] 0 = standalone row, 1 = supernode */
+  const int64_t *colptr;       /* [nnodes+1] */
+  const int32_t *cols;         /* [colptr[nnodes]] */
+  const int64_t *nl;           /* [nnodes] */
+  const int64_t *valoff;       /* [nnodes+1] */
+  const int64_t *dep_ptr;      /* [nnodes+1] */
+  const int32_t *deps;         /* ascending source nodes per node */
+  const int64_t *level_ptr;    /* [nlevels+1] factorization / forward-solve levels */
+  const int32_t *level_nodes;
+  int64_t nlevels;
+  const int64_t *ulevel_ptr;   /* [nulevels+1] backward-solve levels */
+  const int32_t *ulevel_nodes;
+  int64_t nulevels;
+  const int64_t *a_row_ptr;    /* [n+1] CSR row pointer of A (original rows) */
+  const int64_t *a_col_idx;    /* [nnz]  (pattern check only) */
+  const int64_t *mrow_src;     /* [n] original row feeding M row i */
+  const int32_t *colpos;       /* [nnz] position of each A entry in its node's column list */
+  const double *scale;         /* [nnz] dr[row]*dc[col] */
+  const double *dr;            /* [n] */
+  const double *dc;            /* [n] */
+  const int64_t *perm;         /* [n] symmetric ordering, perm[k] = index at position k */
+} hy_symbolic_desc;
+
+/* NumericFactors on the device.  All buffers are caller-owned
+ * device memory (torch tensors in the Python layer). */
+typedef struct {
+  double *d_values;        /* [stored values] node layout */
+  int32_t *d_inner_perm;   /* [n] block-relative pivot order per supernode row */
+  double *d_anorm;         /* [1] */
+  int32_t *d_status;       /* [4]: [0] perturbation count, [1] breakdown row + 1 (0 = none),
+                                   [2] log overflow flag, [3] reserved */
+  int64_t *d_pert_rows;    /* [pert_cap] factor rows where perturbation fired */
+  double *d_pert_vals;     /* [pert_cap] original pivot values */
+  int64_t pert_cap;
+} hy_factors;
+
+int hy_create(int device, hy_handle **out);
+void hy_destroy(hy_handle *h);
+const char *hy_last_error(void);
+
+int hy_upload_symbolic(hy_handle *h, const hy_symbolic_desc *desc);
+/* Number of doubles a hy_factors.d_values buffer needs. */
+int64_t hy_stored_values(const hy_handle *h);
+
+int hy_factorize(hy_handle *h, const double *d_avals, double eps, hy_factors *out,
+                 uintptr_t stream);
+int hy_refactorize(hy_handle *h, const double *d_avals, double eps, const hy_factors *prior,
+                   hy_factors *out, uintptr_t stream);
+int hy_solve(hy_handle *h, const hy_factors *f, const double *d_b, double *d_x,
+             uintptr_t stream);
+
+/* Batched refactorize + solve of B instances sharing the uploaded symbolic
+ * structure and the prior's inner_perm / anorm.  d_vals [B][nnz], d_b / d_x [B][n]
+ * (row-major), d_npert [B] receives each instance's perturbation count.  The
+ * handle owns the interleaved factor workspace (grown on demand). */
+int hy_refactorize_solve_batched(hy_handle *h, int64_t B, const double *d_vals,
+                                 const double *d_b, double *d_x, double eps,
+                                 const hy_factors *prior, int32_t *d_npert, uintptr_t stream);
+/* Copy instance b's factor values from the last batched call into node layout. */
+int hy_batched_factor_values(hy_handle *h, int64_t b, double *d_out, uintptr_t stream);
+
+/* Number of kernel launches issued by this handle since creation (bench evidence). */
+int64_t hy_launch_count(const hy_handle *h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

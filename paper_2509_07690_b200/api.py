@@ -1,0 +1,292 @@
+"""Public API mirroring the reference's SPEC entry points (drop-in surface).
+
+| SPEC operation                                     | here                               |
+|----------------------------------------------------|------------------------------------|
+| static_pivot(A) -> PivotScale        SPEC.md:155   | ``static_pivot`` (reference code)  |
+| amd_order(pattern) -> Ordering       SPEC.md:165   | ``amd_order`` (reference code)     |
+| symbolic_factorize(A, ps, ord)       SPEC.md:175   | ``symbolic_factorize``             |
+| factorize(A, ps, ord, sym, opts)     SPEC.md:280   | ``factorize``  (device)            |
+| refactorize(A_new, prior, opts)      SPEC.md:340   | ``refactorize`` (device)           |
+| solve(A, factors, ps, ord, b, thr)   SPEC.md:489   | ``solve`` (device substitution +   |
+|                                                    |  automatic refinement)|
+| (BASELINE config 4, no SPEC name)                  | ``refactorize_solve_batched``      |
+
+``analyze`` (not a reference name) = static_pivot → ordering → symbolic_factorize.
+Errors are the reference's own classes (``polylu.errors``).  The device path has
+no CPU fallback: without a CUDA device or the built library these raise.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import preprocess as _pp
+from ._ref import KernelMode, SolverConfig, errors, matrix as _refmatrix
+from .analysis import Analysis, analyze, value_map
+from .symbolic import SymbolicStructure, symbolic_from_pattern
+
+static_pivot = _pp.static_pivot
+PivotScale = _pp.PivotScale
+Ordering = _pp.Ordering
+
+
+def amd_order(ap, ai):
+    return _pp.amd_order(ap, ai)
+
+
+def symbolic_factorize(A, ps, order, config=None, kernel_override=None, threads=1):
+    """SPEC.md:175-183 (+ detect_supernodes, select_kernel, build_task_graph, levels)."""
+    mp, mc, _ = _pp.m_pattern(A, ps, order)
+    return symbolic_from_pattern(A.n, mp, mc, config, kernel_override, threads)
+
+
+@dataclass
+class FactorOptions:
+    """SPEC.md:273-276.  ``threads`` has no effect on the device (kept for the API);
+    ``device`` selects the GPU."""
+    kernel_override: object = None
+    perturbation_epsilon: float = 1e-8
+    threads: int = 1
+    pivot_tolerance: object = None
+    device: int = 0
+
+    def __post_init__(self):
+        if not (0.0 <= self.perturbation_epsilon < 1.0):
+            raise ValueError("perturbation_epsilon must lie in [0, 1)")
+
+
+@dataclass
+class RefinementReport:
+    """SPEC.md:454-457."""
+    iterations: int = 0
+    backward_errors: list = field(default_factory=list)
+    converged: bool = True
+
+
+@dataclass
+class NumericFactors:
+    """SPEC.md:266-271, resident on the device in node layout."""
+    symbolic: SymbolicStructure
+    values: object            # torch.float64 CUDA tensor [stored]
+    inner_perm: object        # torch.int32 CUDA tensor [n]
+    anorm: float
+    perturbed: list
+    _bufs: dict = field(repr=False, default=None)
+    _desc: object = field(repr=False, default=None)
+    _ctx: object = field(repr=False, default=None)
+
+    def host_values(self):
+        return self.values.cpu().numpy()
+
+    def host_inner_perm(self):
+        return self.inner_perm.cpu().numpy().astype(np.int64)
+
+    def l_values(self):
+        """Per-row L values aligned with ``symbolic.l_pattern()`` (SPEC layout view)."""
+        return [v for v, _ in self._row_views()]
+
+    def u_values(self):
+        return [v for _, v in self._row_views()]
+
+    def _row_views(self):
+        s = self.symbolic
+        F = self.host_values()
+        out = []
+        for i in range(s.n):
+            u = int(s.node_of[i])
+            t = i - int(s.node_first[u])
+            W = int(s.colptr[u + 1] - s.colptr[u])
+            d = int(s.nl[u]) + t
+            row = F[s.valoff[u] + t * W: s.valoff[u] + (t + 1) * W]
+            out.append((row[:d], row[d:]))
+        return out
+
+
+# --------------------------------------------------------------------------- contexts
+def _context(an, device=0):
+    ctxs = an.__dict__.setdefault("_device_ctx", {})
+    if device not in ctxs:
+        from .device import DeviceContext
+        ctxs[device] = DeviceContext(an, device)
+    return ctxs[device]
+
+
+def _analysis_for(A, ps, order, sym, config=None):
+    an = getattr(sym, "_analysis", None)
+    if an is None or an.pivot_scale is not ps or an.ordering is not order:
+        vm = value_map(A, ps, order, sym)
+        an = Analysis(A, ps, order, sym, vm, config or SolverConfig(), {})
+        sym._analysis = an
+    return an
+
+
+def _check_pattern(an, A):
+    if A.n != an.A.n:
+        raise errors.DimensionMismatch("matrix dimension %d differs from analyzed %d" % (A.n, an.A.n))
+    if (A.nnz != an.A.nnz or not np.array_equal(A.row_ptr, an.A.row_ptr)
+            or not np.array_equal(A.col_idx, an.A.col_idx)):
+        raise errors.PatternMismatch("refactorization input pattern differs from the analyzed pattern")
+
+
+def _apply_mode(an, opts):
+    if opts.kernel_override is None:
+        return
+    mode = opts.kernel_override
+    mode = KernelMode.parse(mode) if isinstance(mode, str) else KernelMode(mode)
+    if mode != an.symbolic.kernel_mode:
+        raise ValueError("kernel_override must be fixed at analyze time "
+                         "(analyze(..., kernel_override=...)); got %s for a %s analysis"
+                         % (mode.name, an.symbolic.kernel_mode.name))
+
+
+def _finish(ctx, an, bufs, desc, check_breakdown=True):
+    st = bufs["status"].cpu().numpy()
+    npert = int(st[0])
+    if check_breakdown and st[1] != 0:
+        raise errors.NumericBreakdown("zero pivot at factor row %d with perturbation disabled"
+                                      % (int(st[1]) - 1))
+    k = min(npert, int(desc.pert_cap))
+    rows = bufs["pert_rows"][:k].cpu().numpy()
+    vals = bufs["pert_vals"][:k].cpu().numpy()
+    o = np.argsort(rows, kind="stable")
+    pert = list(zip(rows[o].tolist(), vals[o].tolist()))
+    anorm = float(bufs["anorm"].cpu().item())
+    return NumericFactors(an.symbolic, bufs["values"], bufs["inner_perm"], anorm, pert,
+                          bufs, desc, ctx)
+
+
+def factorize_analysis(an, values=None, opts=None, stream=None):
+    """factorize on an ``Analysis`` (values default to the analyzed A's)."""
+    import torch
+    opts = opts or FactorOptions()
+    _apply_mode(an, opts)
+    ctx = _context(an, opts.device)
+    vals = an.A.values if values is None else values
+    d_vals = vals if isinstance(vals, torch.Tensor) else torch.from_numpy(
+        np.ascontiguousarray(vals, np.float64)).to(ctx.device)
+    bufs, desc = ctx.alloc_factors()
+    from .device import check
+    check(ctx.lib.hy_factorize(ctx.h, d_vals.data_ptr(), float(opts.perturbation_epsilon),
+                               desc, ctx.stream_handle(stream)))
+    return _finish(ctx, an, bufs, desc)
+
+
+def factorize(A, ps, order=None, sym=None, opts=None):
+    """SPEC.md:280-288.  Also accepts ``factorize(analysis, opts=...)``."""
+    if isinstance(A, Analysis):
+        return factorize_analysis(A, None, ps if isinstance(ps, FactorOptions) else opts)
+    an = _analysis_for(A, ps, order, sym)
+    if A is not an.A:
+        _check_pattern(an, A)
+    return factorize_analysis(an, A.values, opts)
+
+
+def refactorize(A_new, prior, opts=None, stream=None):
+    """reuse PivotScale, Ordering, symbolic, schedule, inner_perm, anorm."""
+    import torch
+    from .device import check
+    opts = opts or FactorOptions()
+    ctx = prior._ctx
+    an = ctx.analysis
+    if isinstance(A_new, torch.Tensor):
+        d_vals = A_new
+    else:
+        _check_pattern(an, A_new)
+        d_vals = torch.from_numpy(np.ascontiguousarray(A_new.values)).to(ctx.device)
+    bufs, desc = ctx.alloc_factors()
+    check(ctx.lib.hy_refactorize(ctx.h, d_vals.data_ptr(), float(opts.perturbation_epsilon),
+                                 prior._desc, desc, ctx.stream_handle(stream)))
+    return _finish(ctx, an, bufs, desc)
+
+
+def substitute(factors, b, stream=None):
+    """Forward/backward substitution with scaling and permutations (no refinement)."""
+    import torch
+    from .device import check
+    ctx = factors._ctx
+    d_b = b if isinstance(b, torch.Tensor) else torch.from_numpy(
+        np.ascontiguousarray(b, np.float64)).to(ctx.device)
+    if d_b.shape != (ctx.n,):
+        raise errors.DimensionMismatch("b must have length %d" % ctx.n)
+    d_x = torch.empty(ctx.n, dtype=torch.float64, device=ctx.device)
+    check(ctx.lib.hy_solve(ctx.h, factors._desc, d_b.data_ptr(), d_x.data_ptr(),
+                           ctx.stream_handle(stream)))
+    return d_x
+
+
+def solve(A, factors, ps=None, order=None, b=None, threads=1, config=None):
+    """SPEC.md:489-497 (+ automatic iterative_refinement when perturbation fired,
+    SPEC.md:499-507; residual and backward error in original coordinates)."""
+    b = np.ascontiguousarray(b, np.float64)
+    if b.shape != (A.n,):
+        raise errors.DimensionMismatch("b must have length %d" % A.n)
+    x = substitute(factors, b).cpu().numpy()
+    report = RefinementReport()
+    if factors.perturbed:
+        cfg = config or SolverConfig()
+        errs = [_refmatrix.backward_error(A, x, b)]
+        it = 0
+        converged = errs[-1] <= cfg.refine_tolerance
+        while not converged and it < cfg.max_refine_iters:
+            r = b - _refmatrix.spmv(A, x)
+            xn = x + substitute(factors, r).cpu().numpy()
+            e = _refmatrix.backward_error(A, xn, b)
+            it += 1
+            if e > cfg.refine_stagnation_factor * errs[-1]:
+                if e < errs[-1]:
+                    x = xn
+                    errs.append(e)
+                break
+            x = xn
+            errs.append(e)
+            converged = e <= cfg.refine_tolerance
+        report = RefinementReport(it, errs, bool(converged))
+    return x, report
+
+
+class BatchedRefactorizer:
+    """B x [refactorize → solve] sharing one symbolic structure on one GPU
+    (BASELINE config 4).  Reuses ``prior``'s inner_perm and anorm."""
+
+    def __init__(self, prior, eps=1e-8):
+        self.prior = prior
+        self.ctx = prior._ctx
+        self.eps = eps
+
+    def run(self, d_vals, d_rhs, d_x=None, d_npert=None, stream=None):
+        import torch
+        from .device import check
+        B = d_vals.shape[0]
+        if d_vals.shape[1] != self.ctx.nnz or d_rhs.shape != (B, self.ctx.n):
+            raise errors.DimensionMismatch("batched values/rhs shapes do not match the analysis")
+        if d_x is None:
+            d_x = torch.empty((B, self.ctx.n), dtype=torch.float64, device=self.ctx.device)
+        if d_npert is None:
+            d_npert = torch.empty(B, dtype=torch.int32, device=self.ctx.device)
+        check(self.ctx.lib.hy_refactorize_solve_batched(
+            self.ctx.h, B, d_vals.data_ptr(), d_rhs.data_ptr(), d_x.data_ptr(), float(self.eps),
+            self.prior._desc, d_npert.data_ptr(), self.ctx.stream_handle(stream)))
+        return d_x, d_npert
+
+    def factor_values(self, b, stream=None):
+        import torch
+        from .device import check
+        out = torch.empty(self.ctx.stored, dtype=torch.float64, device=self.ctx.device)
+        check(self.ctx.lib.hy_batched_factor_values(self.ctx.h, b, out.data_ptr(),
+                                                    self.ctx.stream_handle(stream)))
+        return out
+
+
+def refactorize_solve_batched(values, prior, rhs, opts=None):
+    """Host-facing batched call: values [B, nnz], rhs [B, n] (numpy or CUDA tensors)
+    → (x [B, n] numpy, perturbation counts [B])."""
+    import torch
+    opts = opts or FactorOptions()
+    br = BatchedRefactorizer(prior, opts.perturbation_epsilon)
+    dev = br.ctx.device
+    dv = values if isinstance(values, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(values)).to(dev)
+    dr = rhs if isinstance(rhs, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(rhs)).to(dev)
+    x, npert = br.run(dv, dr)
+    return x.cpu().numpy(), npert.cpu().numpy()

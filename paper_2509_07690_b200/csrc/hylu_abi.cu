@@ -1,0 +1,362 @@
+// hylu_abi.cu — the extern "C" boundary (include/hylu_b200.h): handle, one-time
+// symbolic upload, level plans, and the launch sequences for factorize /
+// refactorize / solve / batched refactorize+solve.
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "hylu_b200.h"
+#include "hylu_common.cuh"
+
+namespace hy {
+// kernels (hylu_factor.cu / hylu_batch.cu)
+__global__ void k_anorm(const double *, const double *, int64_t, double *);
+__global__ void k_rows(DevSym, CallP, const int32_t *, int);
+__global__ void k_sn(DevSym, CallP, const int32_t *);
+size_t sn_smem_bytes();
+__global__ void k_bhat(DevSym, const int32_t *, const double *, double *);
+__global__ void k_xout(DevSym, const double *, double *);
+__global__ void k_fwd(DevSym, const double *, const int32_t *, int, double *);
+__global__ void k_bwd(DevSym, const double *, const int32_t *, int, double *);
+__global__ void k_batch_factor(DevSym, BatchP, const int32_t *, int, int);
+__global__ void k_batch_bhat(DevSym, const int32_t *, const double *, double *, int64_t);
+__global__ void k_batch_xout(DevSym, const double *, double *, int64_t);
+__global__ void k_batch_fwd(DevSym, const double *, int64_t, const int32_t *, int, int, double *);
+__global__ void k_batch_bwd(DevSym, const double *, int64_t, const int32_t *, int, int, double *);
+__global__ void k_batch_extract(const double *, int64_t, int64_t, double *);
+}  // namespace hy
+
+using namespace hy;
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string &msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(x)                                                                              \
+  do {                                                                                     \
+    cudaError_t _e = (x);                                                                  \
+    if (_e != cudaSuccess)                                                                 \
+      return fail(HY_CUDA_ERROR, std::string(#x) + ": " + cudaGetErrorString(_e));         \
+  } while (0)
+
+// Per level: standalone-row nodes and supernode nodes, in level order.
+struct Plan {
+  std::vector<int64_t> rptr, sptr;  // [nlev+1] offsets into the concatenated lists
+  int32_t *d_rows = nullptr, *d_sns = nullptr;
+  int nlev = 0;
+  // batched: all nodes per level
+  std::vector<int64_t> aptr;
+  int32_t *d_all = nullptr;
+};
+
+struct hy_handle {
+  int device = 0;
+  DevSym S{};
+  std::vector<void *> allocs;
+  Plan fplan, bplan;
+  int64_t stored = 0;
+  bool uploaded = false;
+  double *d_y = nullptr;          // single-solve workspace [n]
+  double *d_bf = nullptr;         // batched factor workspace
+  int64_t bf_cap = 0;             // doubles
+  double *d_by = nullptr;         // batched solve workspace
+  int64_t by_cap = 0;
+  int64_t last_B = 0;
+  int64_t launches = 0;
+  size_t sn_smem = 0;
+};
+
+template <class T>
+static int upload(hy_handle *h, T **dst, const T *src, int64_t count) {
+  *dst = nullptr;
+  if (count <= 0) return HY_OK;
+  CK(cudaMalloc((void **)dst, sizeof(T) * count));
+  h->allocs.push_back(*dst);
+  if (src) CK(cudaMemcpy(*dst, src, sizeof(T) * count, cudaMemcpyHostToDevice));
+  return HY_OK;
+}
+
+#define UP(dst, src, cnt)                              \
+  do {                                                 \
+    int _r = upload(h, dst, src, (int64_t)(cnt));      \
+    if (_r) return _r;                                 \
+  } while (0)
+
+static int build_plan(hy_handle *h, Plan &pl, const int64_t *lptr, const int32_t *lnodes,
+                      int64_t nlev, const int8_t *kind) {
+  pl.nlev = (int)nlev;
+  pl.rptr.assign(nlev + 1, 0);
+  pl.sptr.assign(nlev + 1, 0);
+  pl.aptr.assign(nlev + 1, 0);
+  std::vector<int32_t> rows, sns, all;
+  for (int64_t l = 0; l < nlev; ++l) {
+    for (int64_t k = lptr[l]; k < lptr[l + 1]; ++k) {
+      const int32_t u = lnodes[k];
+      (kind[u] ? sns : rows).push_back(u);
+      all.push_back(u);
+    }
+    pl.rptr[l + 1] = (int64_t)rows.size();
+    pl.sptr[l + 1] = (int64_t)sns.size();
+    pl.aptr[l + 1] = (int64_t)all.size();
+  }
+  UP(&pl.d_rows, rows.data(), rows.size());
+  UP(&pl.d_sns, sns.data(), sns.size());
+  UP(&pl.d_all, all.data(), all.size());
+  return HY_OK;
+}
+
+extern "C" {
+
+const char *hy_last_error(void) { return g_err.c_str(); }
+
+int hy_create(int device, hy_handle **out) {
+  if (!out) return fail(HY_INVALID_ARGUMENT, "null output handle");
+  CK(cudaSetDevice(device));
+  hy_handle *h = new hy_handle();
+  h->device = device;
+  h->sn_smem = sn_smem_bytes();
+  cudaError_t e = cudaFuncSetAttribute(k_sn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)h->sn_smem);
+  if (e != cudaSuccess) {
+    delete h;
+    return fail(HY_CUDA_ERROR, std::string("cudaFuncSetAttribute(k_sn): ") + cudaGetErrorString(e));
+  }
+  *out = h;
+  return HY_OK;
+}
+
+void hy_destroy(hy_handle *h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  for (void *p : h->allocs) cudaFree(p);
+  if (h->d_bf) cudaFree(h->d_bf);
+  if (h->d_by) cudaFree(h->d_by);
+  delete h;
+}
+
+int64_t hy_stored_values(const hy_handle *h) { return h ? h->stored : -1; }
+int64_t hy_launch_count(const hy_handle *h) { return h ? h->launches : -1; }
+
+int hy_upload_symbolic(hy_handle *h, const hy_symbolic_desc *d) {
+  if (!h || !d) return fail(HY_INVALID_ARGUMENT, "null handle/descriptor");
+  if (h->uploaded) return fail(HY_INVALID_ARGUMENT, "symbolic already uploaded to this handle");
+  if (d->n <= 0 || d->nnodes <= 0 || d->n > INT32_MAX)
+    return fail(HY_DIMENSION_MISMATCH, "invalid dimension");
+  if (d->kernel_mode < 0 || d->kernel_mode > 2) return fail(HY_INVALID_ARGUMENT, "bad kernel_mode");
+  CK(cudaSetDevice(h->device));
+  const int64_t n = d->n, nn = d->nnodes, nnz = d->nnz;
+  // validate node structure (host side, cheap): rows partition [0,n), deps point backward
+  if (d->node_first[0] != 0 || d->node_first[nn] != n)
+    return fail(HY_DIMENSION_MISMATCH, "node rows do not partition [0, n)");
+  for (int64_t u = 0; u < nn; ++u) {
+    const int64_t s = d->node_first[u + 1] - d->node_first[u];
+    if (s <= 0 || s > 64) return fail(HY_INVALID_ARGUMENT, "node row count outside [1, 64]");
+    if (d->nl[u] < 0 || d->nl[u] > d->colptr[u + 1] - d->colptr[u])
+      return fail(HY_INVALID_ARGUMENT, "bad L width");
+    for (int64_t k = d->dep_ptr[u]; k < d->dep_ptr[u + 1]; ++k)
+      if (d->deps[k] >= u || d->deps[k] < 0)
+        return fail(HY_CYCLE_DETECTED, "dependency does not point to a lower node");
+  }
+  DevSym &S = h->S;
+  S.n = (int32_t)n;
+  S.nn = (int32_t)nn;
+  S.mode = d->kernel_mode;
+  S.nnz = nnz;
+  int64_t *p64;
+  int32_t *p32;
+  UP(&p64, d->node_first, nn + 1); S.first = p64;
+  int8_t *p8;
+  UP(&p8, d->node_kind, nn); S.kind = p8;
+  UP(&p64, d->colptr, nn + 1); S.colptr = p64;
+  UP(&p32, d->cols, d->colptr[nn]); S.cols = p32;
+  std::vector<int32_t> nl32(nn), node_of(n);
+  for (int64_t u = 0; u < nn; ++u) {
+    nl32[u] = (int32_t)d->nl[u];
+    for (int64_t r = d->node_first[u]; r < d->node_first[u + 1]; ++r) node_of[r] = (int32_t)u;
+  }
+  UP(&p32, nl32.data(), nn); S.nl = p32;
+  UP(&p64, d->valoff, nn + 1); S.valoff = p64;
+  UP(&p64, d->dep_ptr, nn + 1); S.dptr = p64;
+  UP(&p32, d->deps, d->dep_ptr[nn]); S.deps = p32;
+  UP(&p32, node_of.data(), n); S.node_of = p32;
+  UP(&p64, d->a_row_ptr, n + 1); S.a_ptr = p64;
+  UP(&p64, d->mrow_src, n); S.mrow_src = p64;
+  UP(&p32, d->colpos, nnz); S.colpos = p32;
+  double *pd;
+  UP(&pd, d->scale, nnz); S.scale = pd;
+  UP(&pd, d->dr, n); S.dr = pd;
+  UP(&pd, d->dc, n); S.dc = pd;
+  UP(&p64, d->perm, n); S.perm = p64;
+  UP(&h->d_y, (const double *)nullptr, n);
+  h->stored = d->valoff[nn];
+  int rc = build_plan(h, h->fplan, d->level_ptr, d->level_nodes, d->nlevels, d->node_kind);
+  if (rc) return rc;
+  rc = build_plan(h, h->bplan, d->ulevel_ptr, d->ulevel_nodes, d->nulevels, d->node_kind);
+  if (rc) return rc;
+  h->uploaded = true;
+  return HY_OK;
+}
+
+static int run_factor(hy_handle *h, const double *d_avals, double eps, const hy_factors *prior,
+                      hy_factors *out, cudaStream_t st) {
+  if (!h || !h->uploaded) return fail(HY_INVALID_ARGUMENT, "symbolic not uploaded");
+  if (!d_avals || !out || !out->d_values || !out->d_inner_perm || !out->d_anorm || !out->d_status)
+    return fail(HY_INVALID_ARGUMENT, "null buffer");
+  if (eps < 0.0 || eps >= 1.0) return fail(HY_INVALID_ARGUMENT, "perturbation_epsilon outside [0,1)");
+  CK(cudaSetDevice(h->device));
+  CK(cudaMemsetAsync(out->d_status, 0, 4 * sizeof(int32_t), st));
+  CallP P{};
+  P.F = out->d_values;
+  P.A = d_avals;
+  P.iperm = out->d_inner_perm;
+  P.anorm = out->d_anorm;
+  P.eps = eps;
+  P.status = out->d_status;
+  P.pert_rows = out->d_pert_rows;
+  P.pert_vals = out->d_pert_vals;
+  P.pert_cap = out->d_pert_rows && out->d_pert_vals ? out->pert_cap : 0;
+  if (prior) {
+    P.refactor = 1;
+    P.iperm_prior = prior->d_inner_perm;
+    if (prior->d_anorm != out->d_anorm)
+      CK(cudaMemcpyAsync(out->d_anorm, prior->d_anorm, sizeof(double), cudaMemcpyDeviceToDevice, st));
+    if (prior->d_inner_perm != out->d_inner_perm)
+      CK(cudaMemcpyAsync(out->d_inner_perm, prior->d_inner_perm, sizeof(int32_t) * h->S.n,
+                         cudaMemcpyDeviceToDevice, st));
+  } else {
+    P.refactor = 0;
+    P.iperm_prior = nullptr;
+    CK(cudaMemsetAsync(out->d_inner_perm, 0, sizeof(int32_t) * h->S.n, st));
+    CK(cudaMemsetAsync(out->d_anorm, 0, sizeof(double), st));
+    k_anorm<<<296, 256, 0, st>>>(d_avals, h->S.scale, h->S.nnz, out->d_anorm);
+    h->launches++;
+  }
+  const Plan &pl = h->fplan;
+  for (int l = 0; l < pl.nlev; ++l) {
+    const int nr = (int)(pl.rptr[l + 1] - pl.rptr[l]);
+    const int ns = (int)(pl.sptr[l + 1] - pl.sptr[l]);
+    if (nr) {
+      k_rows<<<(nr + 3) / 4, 128, 0, st>>>(h->S, P, pl.d_rows + pl.rptr[l], nr);
+      h->launches++;
+    }
+    if (ns) {
+      k_sn<<<ns, 256, h->sn_smem, st>>>(h->S, P, pl.d_sns + pl.sptr[l]);
+      h->launches++;
+    }
+  }
+  CK(cudaGetLastError());
+  return HY_OK;
+}
+
+int hy_factorize(hy_handle *h, const double *d_avals, double eps, hy_factors *out,
+                 uintptr_t stream) {
+  return run_factor(h, d_avals, eps, nullptr, out, (cudaStream_t)stream);
+}
+
+int hy_refactorize(hy_handle *h, const double *d_avals, double eps, const hy_factors *prior,
+                   hy_factors *out, uintptr_t stream) {
+  if (!prior || !prior->d_inner_perm || !prior->d_anorm)
+    return fail(HY_INVALID_ARGUMENT, "refactorize needs prior factors");
+  return run_factor(h, d_avals, eps, prior, out, (cudaStream_t)stream);
+}
+
+int hy_solve(hy_handle *h, const hy_factors *f, const double *d_b, double *d_x, uintptr_t stream) {
+  if (!h || !h->uploaded) return fail(HY_INVALID_ARGUMENT, "symbolic not uploaded");
+  if (!f || !f->d_values || !d_b || !d_x) return fail(HY_INVALID_ARGUMENT, "null buffer");
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n = h->S.n;
+  k_bhat<<<(n + 255) / 256, 256, 0, st>>>(h->S, f->d_inner_perm, d_b, h->d_y);
+  h->launches++;
+  for (int l = 0; l < h->fplan.nlev; ++l) {
+    const int c = (int)(h->fplan.aptr[l + 1] - h->fplan.aptr[l]);
+    k_fwd<<<(c + 3) / 4, 128, 0, st>>>(h->S, f->d_values, h->fplan.d_all + h->fplan.aptr[l], c, h->d_y);
+    h->launches++;
+  }
+  for (int l = 0; l < h->bplan.nlev; ++l) {
+    const int c = (int)(h->bplan.aptr[l + 1] - h->bplan.aptr[l]);
+    k_bwd<<<(c + 3) / 4, 128, 0, st>>>(h->S, f->d_values, h->bplan.d_all + h->bplan.aptr[l], c, h->d_y);
+    h->launches++;
+  }
+  k_xout<<<(n + 255) / 256, 256, 0, st>>>(h->S, h->d_y, d_x);
+  h->launches++;
+  CK(cudaGetLastError());
+  return HY_OK;
+}
+
+int hy_refactorize_solve_batched(hy_handle *h, int64_t B, const double *d_vals, const double *d_b,
+                                 double *d_x, double eps, const hy_factors *prior, int32_t *d_npert,
+                                 uintptr_t stream) {
+  if (!h || !h->uploaded) return fail(HY_INVALID_ARGUMENT, "symbolic not uploaded");
+  if (B <= 0 || !d_vals || !d_b || !d_x || !prior || !d_npert)
+    return fail(HY_INVALID_ARGUMENT, "null buffer or empty batch");
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int G = (int)((B + 31) / 32);
+  const int64_t need = (int64_t)G * 32 * h->stored;
+  if (need > h->bf_cap) {
+    if (h->d_bf) CK(cudaFree(h->d_bf));
+    h->d_bf = nullptr;
+    CK(cudaMalloc((void **)&h->d_bf, sizeof(double) * need));
+    h->bf_cap = need;
+  }
+  const int64_t needy = (int64_t)G * 32 * h->S.n;
+  if (needy > h->by_cap) {
+    if (h->d_by) CK(cudaFree(h->d_by));
+    h->d_by = nullptr;
+    CK(cudaMalloc((void **)&h->d_by, sizeof(double) * needy));
+    h->by_cap = needy;
+  }
+  h->last_B = B;
+  // prior anorm lives on the device: fetch it once (tiny, synchronous on this stream)
+  double anorm = 0.0;
+  CK(cudaMemcpyAsync(&anorm, prior->d_anorm, sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  CK(cudaMemsetAsync(d_npert, 0, sizeof(int32_t) * B, st));
+  BatchP P{h->d_bf, d_vals, prior->d_inner_perm, eps * anorm, d_npert, B, h->stored};
+  const Plan &pl = h->fplan;
+  for (int l = 0; l < pl.nlev; ++l) {
+    const int c = (int)(pl.aptr[l + 1] - pl.aptr[l]);
+    const int64_t tasks = (int64_t)c * G;
+    k_batch_factor<<<(unsigned)((tasks + 3) / 4), 128, 0, st>>>(h->S, P, pl.d_all + pl.aptr[l], c, G);
+    h->launches++;
+  }
+  dim3 tg((h->S.n + 31) / 32, G);
+  k_batch_bhat<<<tg, 256, 0, st>>>(h->S, prior->d_inner_perm, d_b, h->d_by, B);
+  h->launches++;
+  for (int l = 0; l < pl.nlev; ++l) {
+    const int c = (int)(pl.aptr[l + 1] - pl.aptr[l]);
+    const int64_t tasks = (int64_t)c * G;
+    k_batch_fwd<<<(unsigned)((tasks + 3) / 4), 128, 0, st>>>(h->S, h->d_bf, h->stored,
+                                                           pl.d_all + pl.aptr[l], c, G, h->d_by);
+    h->launches++;
+  }
+  const Plan &bp = h->bplan;
+  for (int l = 0; l < bp.nlev; ++l) {
+    const int c = (int)(bp.aptr[l + 1] - bp.aptr[l]);
+    const int64_t tasks = (int64_t)c * G;
+    k_batch_bwd<<<(unsigned)((tasks + 3) / 4), 128, 0, st>>>(h->S, h->d_bf, h->stored,
+                                                           bp.d_all + bp.aptr[l], c, G, h->d_by);
+    h->launches++;
+  }
+  k_batch_xout<<<tg, 256, 0, st>>>(h->S, h->d_by, d_x, B);
+  h->launches++;
+  CK(cudaGetLastError());
+  return HY_OK;
+}
+
+int hy_batched_factor_values(hy_handle *h, int64_t b, double *d_out, uintptr_t stream) {
+  if (!h || !h->d_bf || b < 0 || b >= h->last_B || !d_out)
+    return fail(HY_INVALID_ARGUMENT, "no batched factors for this index");
+  CK(cudaSetDevice(h->device));
+  k_batch_extract<<<296, 256, 0, (cudaStream_t)stream>>>(h->d_bf, h->stored, b, d_out);
+  h->launches++;
+  CK(cudaGetLastError());
+  return HY_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,97 @@
+// hylu_common.cuh — shared device structures and helpers for the sm_100a kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define HY_FULL 0xffffffffu
+
+namespace hy {
+
+// Symbolic structure resident on the device (uploaded once by hy_upload_symbolic).
+struct DevSym {
+  int32_t n, nn, mode;
+  int64_t nnz;
+  const int64_t *first;     // [nn+1]
+  const int8_t *kind;       // [nn]
+  const int64_t *colptr;    // [nn+1]
+  const int32_t *cols;      // [colptr[nn]]
+  const int32_t *nl;        // [nn]
+  const int64_t *valoff;    // [nn+1]
+  const int64_t *dptr;      // [nn+1]
+  const int32_t *deps;
+  const int32_t *node_of;   // [n]
+  const int64_t *a_ptr;     // [n+1]
+  const int64_t *mrow_src;  // [n]
+  const int32_t *colpos;    // [nnz]
+  const double *scale;      // [nnz]
+  const double *dr, *dc;    // [n]
+  const int64_t *perm;      // [n]
+};
+
+// Per-call parameters (single-instance path).
+struct CallP {
+  double *F;                 // factor values (node layout)
+  const double *A;           // A values [nnz]
+  int32_t *iperm;            // inner_perm [n] (written on factorize, read on refactorize)
+  const int32_t *iperm_prior;
+  const double *anorm;       // [1]
+  double eps;
+  int refactor;
+  int32_t *status;           // [4]
+  int64_t *pert_rows;
+  double *pert_vals;
+  int64_t pert_cap;
+};
+
+// Per-call parameters (batched path).
+struct BatchP {
+  double *BF;            // interleaved factor workspace [G][stored][32]
+  const double *A;       // [B][nnz]
+  const int32_t *iperm;  // prior inner_perm [n]
+  double thr;            // eps * prior anorm
+  int32_t *npert;        // [B]
+  int64_t B;
+  int64_t stored;
+};
+
+__device__ __forceinline__ int lower_bound_i32(const int32_t *c, int lo, int hi, int key) {
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (c[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// pivot_perturb: |p| < thr -> sign(p)*thr (sign(0) = +).
+__device__ __forceinline__ double perturb(double p, double thr, bool &fired) {
+  fired = fabs(p) < thr;
+  if (fired) return p < 0.0 ? -thr : thr;
+  return p;
+}
+
+__device__ __forceinline__ void log_pivot(const CallP &P, int64_t row, double orig, bool fired,
+                                          double thr) {
+  if (fired) {
+    int k = atomicAdd(&P.status[0], 1);
+    if (k < P.pert_cap) {
+      P.pert_rows[k] = row;
+      P.pert_vals[k] = orig;
+    } else {
+      P.status[2] = 1;
+    }
+  }
+  if (thr == 0.0 && orig == 0.0) atomicCAS(&P.status[1], 0, (int)(row + 1));
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(HY_FULL, v, o);
+  return v;
+}
+
+// atomic max for non-negative doubles (bit patterns order like unsigned ints)
+__device__ __forceinline__ void atomic_max_nonneg(double *addr, double v) {
+  atomicMax(reinterpret_cast<unsigned long long *>(addr), (unsigned long long)__double_as_longlong(v));
+}
+
+}  // namespace hy

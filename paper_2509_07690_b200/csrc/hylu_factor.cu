@@ -1,0 +1,501 @@
+// hylu_factor.cu — single-instance numeric factorization and triangular solve
+// kernels for sm_100a (one factorization per GPU).
+//
+// Execution: the elimination DAG is level-scheduled (SPEC.md:215-223 levels; the
+// bulk mode of SPEC.md:397-405 on the device).  Per level two kernels run:
+//   k_rows  — one warp per standalone-row node: scatter its M row into a
+//             shared-memory accumulator, apply row-row and
+//             sup-row updates in ascending source order, perturb
+//             the pivot, write the row once.
+//   k_sn    — one CTA per supernode node: scatter, external updates (row-row per
+//             source row in ROWROW mode, TRSM + GEMM otherwise),
+//             then the in-supernode dense LU with block-restricted pivoting
+//             (SPEC.md:320-328).
+// Solve: per-level forward (unit L) and backward (U) substitution kernels.
+#include "hylu_common.cuh"
+
+namespace hy {
+
+// ============================================================================ anorm
+__global__ void k_anorm(const double *__restrict__ A, const double *__restrict__ scale, int64_t nnz,
+                        double *out) {
+  double m = 0.0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x)
+    m = fmax(m, fabs(A[e] * scale[e]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(HY_FULL, m, o));
+  if ((threadIdx.x & 31) == 0 && m > 0.0) atomic_max_nonneg(out, m);
+}
+
+// ============================================================================ rows
+constexpr int RW_WARPS = 4;
+constexpr int CAPW = 512;
+
+struct RowSmem {
+  double w[CAPW];
+  int32_t c[CAPW];
+  double x[64];
+};
+
+__device__ void row_task(const DevSym &S, const CallP &P, int u, RowSmem &sm, int lane) {
+  const int64_t i = S.first[u];
+  const int64_t c0 = S.colptr[u];
+  const int W = (int)(S.colptr[u + 1] - c0);
+  const int L = S.nl[u];
+  double *F = P.F;
+  double *Fu = F + S.valoff[u];
+  const bool inSm = W <= CAPW;
+  double *w = inSm ? sm.w : Fu;
+  const int32_t *tc = inSm ? sm.c : S.cols + c0;
+  for (int q = lane; q < W; q += 32) {
+    w[q] = 0.0;
+    if (inSm) sm.c[q] = S.cols[c0 + q];
+  }
+  __syncwarp();
+  {
+    const int64_t a = S.mrow_src[i];
+    for (int64_t e = S.a_ptr[a] + lane; e < S.a_ptr[a + 1]; e += 32)
+      w[S.colpos[e]] = P.A[e] * S.scale[e];
+  }
+  __syncwarp();
+  int p = 0;
+  while (p < L) {
+    const int j = tc[p];
+    const int v = S.node_of[j];
+    const int vf = (int)S.first[v];
+    const int64_t vc0 = S.colptr[v];
+    const int vW = (int)(S.colptr[v + 1] - vc0);
+    const int vnl = S.nl[v];
+    const int32_t *vc = S.cols + vc0;
+    const double *vb = F + S.valoff[v];
+    if (S.kind[v] == 0 || S.mode == 0) {
+      // ---- row-row: source row j
+      const int tj = j - vf;
+      const double *srow = vb + (int64_t)tj * vW;
+      const int sd = vnl + tj;
+      const double l = w[p] / srow[sd];
+      __syncwarp();
+      if (lane == 0) w[p] = l;
+      if (l != 0.0) {
+        for (int q = sd + 1 + lane; q < vW; q += 32) {
+          const int pos = lower_bound_i32(tc, p + 1, W, vc[q]);
+          w[pos] -= l * srow[q];
+        }
+      }
+      __syncwarp();
+      p++;
+    } else {
+      // ---- sup-row: TRSV with the source's upper block, then GEMV over its panel
+      const int vs = (int)(S.first[v + 1] - vf);
+      const int t0 = j - vf;
+      const int m = vs - t0;
+      for (int t = lane; t < vs; t += 32) sm.x[t] = (t >= t0) ? w[p + t - t0] : 0.0;
+      __syncwarp();
+      for (int t = t0; t < vs; ++t) {
+        const double *ur = vb + (int64_t)t * vW + vnl;
+        const double xt = sm.x[t] / ur[t];
+        __syncwarp();
+        if (lane == 0) sm.x[t] = xt;
+        if (xt != 0.0)
+          for (int t2 = t + 1 + lane; t2 < vs; t2 += 32) sm.x[t2] -= xt * ur[t2];
+        __syncwarp();
+      }
+      for (int t = t0 + lane; t < vs; t += 32) w[p + t - t0] = sm.x[t];
+      for (int q = vnl + vs + lane; q < vW; q += 32) {
+        double acc = 0.0;
+        for (int t = t0; t < vs; ++t) acc += sm.x[t] * vb[(int64_t)t * vW + q];
+        const int pos = lower_bound_i32(tc, p + m, W, vc[q]);
+        w[pos] -= acc;
+      }
+      __syncwarp();
+      p += m;
+    }
+  }
+  if (lane == 0) {
+    const double piv = w[L];
+    const double thr = P.eps * P.anorm[0];
+    bool fired;
+    w[L] = perturb(piv, thr, fired);
+    log_pivot(P, i, piv, fired, thr);
+  }
+  __syncwarp();
+  if (inSm)
+    for (int q = lane; q < W; q += 32) Fu[q] = w[q];
+}
+
+__global__ void __launch_bounds__(RW_WARPS * 32) k_rows(DevSym S, CallP P, const int32_t *nodes,
+                                                        int count) {
+  __shared__ RowSmem sm[RW_WARPS];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int idx = blockIdx.x * RW_WARPS + warp;
+  if (idx >= count) return;
+  row_task(S, P, nodes[idx], sm[warp], lane);
+}
+
+// ============================================================================ supernodes
+constexpr int SN_THREADS = 256;
+constexpr int SMAX = 64;
+constexpr int LDX = SMAX + 1;
+constexpr int TILE = 64;
+constexpr int CAPC = 8192;
+constexpr int SPOS = 2048;
+
+struct SnSmem {
+  double X[SMAX * LDX];   // multipliers / diagonal block LU
+  double U[SMAX * LDX];   // source diagonal block
+  double T[SMAX * LDX];   // GEMM / panel tile
+  int32_t spos[SPOS];
+  int32_t tcols[CAPC];
+  double lm[SMAX];
+  int32_t perm[SMAX];
+  int32_t pinv[SMAX];
+  int32_t piv_row;
+};
+
+// positions of source columns vc[qa..qa+cnt) in the target column list tc[lo..W), -1 if absent
+__device__ __forceinline__ void map_cols(const int32_t *vc, int qa, int cnt, const int32_t *tc,
+                                         int lo, int W, int32_t *out) {
+  for (int q = threadIdx.x; q < cnt; q += blockDim.x) {
+    const int k = vc[qa + q];
+    const int pos = lower_bound_i32(tc, lo, W, k);
+    out[q] = (pos < W && tc[pos] == k) ? pos : -1;
+  }
+}
+
+__global__ void __launch_bounds__(SN_THREADS, 1) k_sn(DevSym S, CallP P, const int32_t *nodes) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SnSmem &sm = *reinterpret_cast<SnSmem *>(smem_raw);
+  const int u = nodes[blockIdx.x];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = SN_THREADS / 32;
+  const int r = (int)S.first[u];
+  const int s = (int)(S.first[u + 1] - r);
+  const int64_t c0 = S.colptr[u];
+  const int W = (int)(S.colptr[u + 1] - c0);
+  const int L = S.nl[u];
+  double *F = P.F;
+  double *Pm = F + S.valoff[u];
+  const bool colsSm = W <= CAPC;
+  const int32_t *tc = colsSm ? sm.tcols : S.cols + c0;
+  const double thr = P.eps * P.anorm[0];
+
+  if (colsSm)
+    for (int q = tid; q < W; q += SN_THREADS) sm.tcols[q] = S.cols[c0 + q];
+  if (tid < s) {
+    if (P.refactor) {
+      const int t = P.iperm_prior[r + tid];
+      sm.pinv[t] = tid;
+      P.iperm[r + tid] = t;
+    } else {
+      sm.pinv[tid] = tid;
+    }
+  }
+  for (int64_t q = tid; q < (int64_t)s * W; q += SN_THREADS) Pm[q] = 0.0;
+  __syncthreads();
+  for (int t = warp; t < s; t += nwarps) {
+    const int64_t a = S.mrow_src[r + t];
+    double *row = Pm + (int64_t)sm.pinv[t] * W;
+    for (int64_t e = S.a_ptr[a] + lane; e < S.a_ptr[a + 1]; e += 32)
+      row[S.colpos[e]] = P.A[e] * S.scale[e];
+  }
+  __syncthreads();
+
+  // ------------------------------------------------------------ external updates
+  for (int64_t di = S.dptr[u]; di < S.dptr[u + 1]; ++di) {
+    const int v = S.deps[di];
+    const int vf = (int)S.first[v];
+    const int vs = (int)(S.first[v + 1] - vf);
+    const int64_t vc0 = S.colptr[v];
+    const int vW = (int)(S.colptr[v + 1] - vc0);
+    const int vnl = S.nl[v];
+    const int32_t *vc = S.cols + vc0;
+    const double *vb = F + S.valoff[v];
+    if (S.kind[v] == 0 || S.mode == 0) {
+      for (int tj = 0; tj < vs; ++tj) {
+        const int j = vf + tj;
+        const int pj = lower_bound_i32(tc, 0, L, j);
+        if (pj >= L || tc[pj] != j) continue;  // uniform
+        const double *srow = vb + (int64_t)tj * vW;
+        const int sd = vnl + tj;
+        if (tid < s) {
+          const double l = Pm[(int64_t)tid * W + pj] / srow[sd];
+          Pm[(int64_t)tid * W + pj] = l;
+          sm.lm[tid] = l;
+        }
+        for (int qa = sd + 1; qa < vW; qa += SPOS) {
+          const int cnt = min(SPOS, vW - qa);
+          __syncthreads();
+          map_cols(vc, qa, cnt, tc, pj + 1, W, sm.spos);
+          __syncthreads();
+          for (int idx = tid; idx < s * cnt; idx += SN_THREADS) {
+            const int t = idx / cnt, q = idx - t * cnt;
+            const double l = sm.lm[t];
+            if (l != 0.0) Pm[(int64_t)t * W + sm.spos[q]] -= l * srow[qa + q];
+          }
+        }
+        __syncthreads();
+      }
+    } else {
+      // block update: X = W_b U_bb^-1 (TRSM), W_panel -= X U_panel (GEMM)
+      __syncthreads();
+      map_cols(vc, vnl, vs, tc, 0, W, sm.spos);
+      __syncthreads();
+      for (int idx = tid; idx < s * vs; idx += SN_THREADS) {
+        const int t = idx / vs, tt = idx - t * vs;
+        const int ps = sm.spos[tt];
+        sm.X[t * LDX + tt] = ps >= 0 ? Pm[(int64_t)t * W + ps] : 0.0;
+      }
+      for (int idx = tid; idx < vs * vs; idx += SN_THREADS) {
+        const int tt = idx / vs, t2 = idx - tt * vs;
+        sm.U[tt * LDX + t2] = t2 >= tt ? vb[(int64_t)tt * vW + vnl + t2] : 0.0;
+      }
+      __syncthreads();
+      for (int tt = 0; tt < vs; ++tt) {
+        if (tid < s) sm.X[tid * LDX + tt] /= sm.U[tt * LDX + tt];
+        __syncthreads();
+        const int rem = vs - tt - 1;
+        for (int idx = tid; idx < s * rem; idx += SN_THREADS) {
+          const int t = idx / rem, t2 = tt + 1 + idx - t * rem;
+          sm.X[t * LDX + t2] -= sm.X[t * LDX + tt] * sm.U[tt * LDX + t2];
+        }
+        __syncthreads();
+      }
+      for (int idx = tid; idx < s * vs; idx += SN_THREADS) {
+        const int t = idx / vs, tt = idx - t * vs;
+        const int ps = sm.spos[tt];
+        if (ps >= 0) Pm[(int64_t)t * W + ps] = sm.X[t * LDX + tt];
+      }
+      // GEMM over the source panel, 64-column tiles, 4x4 outputs per thread
+      const int tr = tid >> 4, tcl = tid & 15;
+      for (int qa = vnl + vs; qa < vW; qa += TILE) {
+        const int nq = min(TILE, vW - qa);
+        __syncthreads();
+        for (int idx = tid; idx < vs * TILE; idx += SN_THREADS) {
+          const int tt = idx / TILE, c = idx - tt * TILE;
+          sm.T[tt * LDX + c] = c < nq ? vb[(int64_t)tt * vW + qa + c] : 0.0;
+        }
+        map_cols(vc, qa, nq, tc, 0, W, sm.spos);
+        __syncthreads();
+        double acc[4][4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+        for (int tt = 0; tt < vs; ++tt) {
+          double xv[4], tv[4];
+#pragma unroll
+          for (int a = 0; a < 4; ++a) xv[a] = sm.X[(tr + 16 * a) * LDX + tt];
+#pragma unroll
+          for (int b = 0; b < 4; ++b) tv[b] = sm.T[tt * LDX + tcl + 16 * b];
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) acc[a][b] = fma(xv[a], tv[b], acc[a][b]);
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          const int t = tr + 16 * a;
+          if (t < s) {
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              const int c = tcl + 16 * b;
+              if (c < nq) Pm[(int64_t)t * W + sm.spos[c]] -= acc[a][b];
+            }
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+
+  // ------------------------------------------------------------ internal LU
+  __syncthreads();
+  for (int idx = tid; idx < s * s; idx += SN_THREADS) {
+    const int t = idx / s, tt = idx - t * s;
+    sm.X[t * LDX + tt] = Pm[(int64_t)t * W + L + tt];
+  }
+  if (tid < s) sm.perm[tid] = tid;
+  __syncthreads();
+  for (int t = 0; t < s; ++t) {
+    if (!P.refactor && warp == 0) {
+      // pivot search over rows t..s-1 of column t: max |.|, lowest index on ties
+      double best = -1.0;
+      int bi = s;
+      for (int q = t + lane; q < s; q += 32) {
+        const double a = fabs(sm.X[q * LDX + t]);
+        if (a > best) { best = a; bi = q; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(HY_FULL, best, o);
+        const int oi = __shfl_xor_sync(HY_FULL, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (bi != t && bi < s) {
+        for (int c = lane; c < s; c += 32) {
+          const double tmp = sm.X[t * LDX + c];
+          sm.X[t * LDX + c] = sm.X[bi * LDX + c];
+          sm.X[bi * LDX + c] = tmp;
+        }
+        if (lane == 0) {
+          const int tp = sm.perm[t];
+          sm.perm[t] = sm.perm[bi];
+          sm.perm[bi] = tp;
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      const double piv = sm.X[t * LDX + t];
+      bool fired;
+      sm.X[t * LDX + t] = perturb(piv, thr, fired);
+      log_pivot(P, r + t, piv, fired, thr);
+    }
+    __syncthreads();
+    const double pv = sm.X[t * LDX + t];
+    for (int q = t + 1 + tid; q < s; q += SN_THREADS) sm.X[q * LDX + t] /= pv;
+    __syncthreads();
+    const int rem = s - t - 1;
+    for (int idx = tid; idx < rem * rem; idx += SN_THREADS) {
+      const int q = t + 1 + idx / rem, c = t + 1 + idx % rem;
+      sm.X[q * LDX + c] -= sm.X[q * LDX + t] * sm.X[t * LDX + c];
+    }
+    __syncthreads();
+  }
+  // permute the L-union part by tiles (in place, tile read fully before written)
+  for (int ca = 0; ca < L; ca += TILE) {
+    const int nq = min(TILE, L - ca);
+    for (int idx = tid; idx < s * nq; idx += SN_THREADS) {
+      const int t = idx / nq, c = idx - t * nq;
+      sm.T[t * LDX + c] = Pm[(int64_t)sm.perm[t] * W + ca + c];
+    }
+    __syncthreads();
+    for (int idx = tid; idx < s * nq; idx += SN_THREADS) {
+      const int t = idx / nq, c = idx - t * nq;
+      Pm[(int64_t)t * W + ca + c] = sm.T[t * LDX + c];
+    }
+    __syncthreads();
+  }
+  // panel: permute + U_panel = L_bb^-1 (P panel), rank-1 steps (t ascending per entry)
+  for (int ca = L + s; ca < W; ca += TILE) {
+    const int nq = min(TILE, W - ca);
+    for (int idx = tid; idx < s * nq; idx += SN_THREADS) {
+      const int t = idx / nq, c = idx - t * nq;
+      sm.T[t * LDX + c] = Pm[(int64_t)sm.perm[t] * W + ca + c];
+    }
+    __syncthreads();
+    for (int tt = 0; tt + 1 < s; ++tt) {
+      const int rem = s - tt - 1;
+      for (int idx = tid; idx < rem * nq; idx += SN_THREADS) {
+        const int q = tt + 1 + idx / nq, c = idx % nq;
+        sm.T[q * LDX + c] -= sm.X[q * LDX + tt] * sm.T[tt * LDX + c];
+      }
+      __syncthreads();
+    }
+    for (int idx = tid; idx < s * nq; idx += SN_THREADS) {
+      const int t = idx / nq, c = idx - t * nq;
+      Pm[(int64_t)t * W + ca + c] = sm.T[t * LDX + c];
+    }
+    __syncthreads();
+  }
+  for (int idx = tid; idx < s * s; idx += SN_THREADS) {
+    const int t = idx / s, tt = idx - t * s;
+    Pm[(int64_t)t * W + L + tt] = sm.X[t * LDX + tt];
+  }
+  if (!P.refactor && tid < s) P.iperm[r + tid] = sm.perm[tid];
+}
+
+size_t sn_smem_bytes() { return sizeof(SnSmem); }
+
+// ============================================================================ solve
+// b_hat[i] = dr[a] * b[a], a = original row feeding factor row i (inner_perm applied)
+__global__ void k_bhat(DevSym S, const int32_t *iperm, const double *b, double *y) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < S.n; i += gridDim.x * blockDim.x) {
+    const int u = S.node_of[i];
+    int src = i;
+    if (S.kind[u] == 1) src = (int)S.first[u] + iperm[i];
+    const int64_t a = S.mrow_src[src];
+    y[i] = S.dr[a] * b[a];
+  }
+}
+
+__global__ void k_xout(DevSym S, const double *z, double *x) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < S.n; k += gridDim.x * blockDim.x) {
+    const int64_t c = S.perm[k];
+    x[c] = S.dc[c] * z[k];
+  }
+}
+
+// forward substitution, one warp per node (supernode rows: external dot products
+// by all lanes, then the in-block unit-lower solve)
+__global__ void k_fwd(DevSym S, const double *F, const int32_t *nodes, int count, double *y) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int idx = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (idx >= count) return;
+  const int u = nodes[idx];
+  const int r = (int)S.first[u];
+  const int s = (int)(S.first[u + 1] - r);
+  const int64_t c0 = S.colptr[u];
+  const int W = (int)(S.colptr[u + 1] - c0);
+  const int L = S.nl[u];
+  const double *Fu = F + S.valoff[u];
+  const int32_t *cc = S.cols + c0;
+  double mine0 = 0.0, mine1 = 0.0;  // lane t / t+32 row partials
+  for (int t = 0; t < s; ++t) {
+    const double *row = Fu + (int64_t)t * W;
+    double acc = 0.0;
+    for (int p = lane; p < L; p += 32) acc += row[p] * y[cc[p]];
+    acc = warp_sum(acc);
+    if (lane == (t & 31)) {
+      if (t < 32) mine0 = y[r + t] - acc; else mine1 = y[r + t] - acc;
+    }
+  }
+  // in-block: y_t -= sum_{tt<t} L[t][tt] y_tt
+  for (int tt = 0; tt < s; ++tt) {
+    const double ytt = __shfl_sync(HY_FULL, tt < 32 ? mine0 : mine1, tt & 31);
+    const int t0 = lane, t1 = lane + 32;
+    if (t0 > tt && t0 < s) mine0 -= Fu[(int64_t)t0 * W + L + tt] * ytt;
+    if (t1 > tt && t1 < s) mine1 -= Fu[(int64_t)t1 * W + L + tt] * ytt;
+  }
+  if (lane < s) y[r + lane] = mine0;
+  if (lane + 32 < s) y[r + lane + 32] = mine1;
+}
+
+__global__ void k_bwd(DevSym S, const double *F, const int32_t *nodes, int count, double *y) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int idx = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (idx >= count) return;
+  const int u = nodes[idx];
+  const int r = (int)S.first[u];
+  const int s = (int)(S.first[u + 1] - r);
+  const int64_t c0 = S.colptr[u];
+  const int W = (int)(S.colptr[u + 1] - c0);
+  const int L = S.nl[u];
+  const double *Fu = F + S.valoff[u];
+  const int32_t *cc = S.cols + c0;
+  double mine0 = 0.0, mine1 = 0.0;
+  for (int t = 0; t < s; ++t) {
+    const double *row = Fu + (int64_t)t * W;
+    double acc = 0.0;
+    for (int p = L + s + lane; p < W; p += 32) acc += row[p] * y[cc[p]];
+    acc = warp_sum(acc);
+    if (lane == (t & 31)) {
+      if (t < 32) mine0 = y[r + t] - acc; else mine1 = y[r + t] - acc;
+    }
+  }
+  for (int tt = s - 1; tt >= 0; --tt) {
+    // finalize z_tt
+    const double d = Fu[(int64_t)tt * W + L + tt];
+    if (lane == (tt & 31)) {
+      if (tt < 32) mine0 /= d; else mine1 /= d;
+    }
+    const double ztt = __shfl_sync(HY_FULL, tt < 32 ? mine0 : mine1, tt & 31);
+    const int t0 = lane, t1 = lane + 32;
+    if (t0 < tt) mine0 -= Fu[(int64_t)t0 * W + L + tt] * ztt;
+    if (t1 < tt) mine1 -= Fu[(int64_t)t1 * W + L + tt] * ztt;
+  }
+  if (lane < s) y[r + lane] = mine0;
+  if (lane + 32 < s) y[r + lane + 32] = mine1;
+}
+
+}  // namespace hy

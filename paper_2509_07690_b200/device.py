@@ -1,0 +1,182 @@
+"""ctypes binding of ``lib/libhylu_b200.so`` (C ABI: ``include/hylu_b200.h``).
+
+PyTorch is used only for device memory and streams: every buffer handed to the
+library is a CUDA tensor's ``data_ptr()``.  There is no CPU fallback: if the
+library or a CUDA device is missing, constructing a ``DeviceContext`` raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from ._ref import errors
+
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libhylu_b200.so")
+_lib = None
+
+HY_CODES = {
+    1: errors.DimensionMismatch,
+    2: errors.ZeroDiagonal,
+    3: errors.CycleDetected,
+    4: errors.NumericBreakdown,
+    5: errors.PatternMismatch,
+}
+
+
+class DeviceError(RuntimeError):
+    """CUDA / ABI failure (HY_CUDA_ERROR, HY_INVALID_ARGUMENT)."""
+
+
+class SymbolicDesc(ctypes.Structure):
+    _fields_ = [
+        ("n", ctypes.c_int64), ("nnodes", ctypes.c_int64), ("nnz", ctypes.c_int64),
+        ("kernel_mode", ctypes.c_int32),
+        ("node_first", ctypes.c_void_p), ("node_kind", ctypes.c_void_p),
+        ("colptr", ctypes.c_void_p), ("cols", ctypes.c_void_p), ("nl", ctypes.c_void_p),
+        ("valoff", ctypes.c_void_p), ("dep_ptr", ctypes.c_void_p), ("deps", ctypes.c_void_p),
+        ("level_ptr", ctypes.c_void_p), ("level_nodes", ctypes.c_void_p), ("nlevels", ctypes.c_int64),
+        ("ulevel_ptr", ctypes.c_void_p), ("ulevel_nodes", ctypes.c_void_p), ("nulevels", ctypes.c_int64),
+        ("a_row_ptr", ctypes.c_void_p), ("a_col_idx", ctypes.c_void_p), ("mrow_src", ctypes.c_void_p),
+        ("colpos", ctypes.c_void_p), ("scale", ctypes.c_void_p), ("dr", ctypes.c_void_p),
+        ("dc", ctypes.c_void_p), ("perm", ctypes.c_void_p),
+    ]
+
+
+class FactorsDesc(ctypes.Structure):
+    _fields_ = [
+        ("d_values", ctypes.c_void_p), ("d_inner_perm", ctypes.c_void_p), ("d_anorm", ctypes.c_void_p),
+        ("d_status", ctypes.c_void_p), ("d_pert_rows", ctypes.c_void_p), ("d_pert_vals", ctypes.c_void_p),
+        ("pert_cap", ctypes.c_int64),
+    ]
+
+
+def library():
+    """Load the CUDA library (building it in-tree first if it is absent)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        from . import build
+        build.build_cuda()
+    lib = ctypes.CDLL(_LIB_PATH)
+    vp, i64, u = ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint64
+    lib.hy_create.argtypes = [ctypes.c_int, ctypes.POINTER(vp)]
+    lib.hy_destroy.argtypes = [vp]
+    lib.hy_destroy.restype = None
+    lib.hy_last_error.restype = ctypes.c_char_p
+    lib.hy_upload_symbolic.argtypes = [vp, ctypes.POINTER(SymbolicDesc)]
+    lib.hy_stored_values.argtypes = [vp]
+    lib.hy_stored_values.restype = i64
+    lib.hy_launch_count.argtypes = [vp]
+    lib.hy_launch_count.restype = i64
+    lib.hy_factorize.argtypes = [vp, vp, ctypes.c_double, ctypes.POINTER(FactorsDesc), u]
+    lib.hy_refactorize.argtypes = [vp, vp, ctypes.c_double, ctypes.POINTER(FactorsDesc),
+                                   ctypes.POINTER(FactorsDesc), u]
+    lib.hy_solve.argtypes = [vp, ctypes.POINTER(FactorsDesc), vp, vp, u]
+    lib.hy_refactorize_solve_batched.argtypes = [vp, i64, vp, vp, vp, ctypes.c_double,
+                                                 ctypes.POINTER(FactorsDesc), vp, u]
+    lib.hy_batched_factor_values.argtypes = [vp, i64, vp, u]
+    _lib = lib
+    return lib
+
+
+def check(rc):
+    if rc == 0:
+        return
+    msg = library().hy_last_error().decode(errors="replace")
+    if rc in HY_CODES:
+        raise HY_CODES[rc](msg)
+    raise DeviceError("hylu_b200 error %d: %s" % (rc, msg))
+
+
+def _ptr(a):
+    return ctypes.c_void_p(a.ctypes.data) if a is not None else None
+
+
+class DeviceContext:
+    """One handle = one device + one uploaded symbolic structure."""
+
+    def __init__(self, analysis, device=0):
+        import torch
+        if not torch.cuda.is_available():
+            raise DeviceError("no CUDA device: the hylu_b200 path has no CPU fallback")
+        self.torch = torch
+        self.device = torch.device("cuda", device)
+        self.lib = library()
+        self.analysis = analysis
+        h = ctypes.c_void_p()
+        check(self.lib.hy_create(device, ctypes.byref(h)))
+        self.h = h
+        s = analysis.symbolic
+        A = analysis.A
+        vm = analysis.vmap
+        ps = analysis.pivot_scale
+        keep = dict(
+            node_first=np.ascontiguousarray(s.node_first, np.int64),
+            node_kind=np.ascontiguousarray(s.node_kind, np.int8),
+            colptr=np.ascontiguousarray(s.colptr, np.int64),
+            cols=np.ascontiguousarray(s.cols, np.int32),
+            nl=np.ascontiguousarray(s.nl, np.int64),
+            valoff=np.ascontiguousarray(s.valoff, np.int64),
+            dep_ptr=np.ascontiguousarray(s.dep_ptr, np.int64),
+            deps=np.ascontiguousarray(s.deps, np.int32),
+            level_ptr=np.ascontiguousarray(s.level_ptr, np.int64),
+            level_nodes=np.ascontiguousarray(s.level_nodes, np.int32),
+            ulevel_ptr=np.ascontiguousarray(s.ulevel_ptr, np.int64),
+            ulevel_nodes=np.ascontiguousarray(s.ulevel_nodes, np.int32),
+            a_row_ptr=np.ascontiguousarray(A.row_ptr, np.int64),
+            a_col_idx=np.ascontiguousarray(A.col_idx, np.int64),
+            mrow_src=np.ascontiguousarray(vm.mrow_src, np.int64),
+            colpos=np.ascontiguousarray(vm.colpos, np.int32),
+            scale=np.ascontiguousarray(vm.scale, np.float64),
+            dr=np.ascontiguousarray(ps.dr, np.float64),
+            dc=np.ascontiguousarray(ps.dc, np.float64),
+            perm=np.ascontiguousarray(analysis.ordering.perm, np.int64),
+        )
+        d = SymbolicDesc()
+        d.n, d.nnodes, d.nnz = s.n, s.nnodes, A.nnz
+        d.kernel_mode = int(s.kernel_mode)
+        for k, v in keep.items():
+            setattr(d, k, v.ctypes.data)
+        d.nlevels = len(s.level_ptr) - 1
+        d.nulevels = len(s.ulevel_ptr) - 1
+        with torch.cuda.device(self.device):
+            check(self.lib.hy_upload_symbolic(self.h, ctypes.byref(d)))
+        self.stored = int(self.lib.hy_stored_values(self.h))
+        self.n = s.n
+        self.nnz = A.nnz
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                self.lib.hy_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def stream_handle(self, stream=None):
+        t = self.torch
+        st = stream if stream is not None else t.cuda.current_stream(self.device)
+        return ctypes.c_uint64(st.cuda_stream)
+
+    def alloc_factors(self, pert_cap=1024):
+        t = self.torch
+        dev = self.device
+        bufs = dict(
+            values=t.empty(self.stored, dtype=t.float64, device=dev),
+            inner_perm=t.zeros(self.n, dtype=t.int32, device=dev),
+            anorm=t.zeros(1, dtype=t.float64, device=dev),
+            status=t.zeros(4, dtype=t.int32, device=dev),
+            pert_rows=t.zeros(pert_cap, dtype=t.int64, device=dev),
+            pert_vals=t.zeros(pert_cap, dtype=t.float64, device=dev),
+        )
+        desc = FactorsDesc(bufs["values"].data_ptr(), bufs["inner_perm"].data_ptr(),
+                           bufs["anorm"].data_ptr(), bufs["status"].data_ptr(),
+                           bufs["pert_rows"].data_ptr(), bufs["pert_vals"].data_ptr(), pert_cap)
+        return bufs, desc
+
+    def launches(self):
+        return int(self.lib.hy_launch_count(self.h))
