@@ -120,6 +120,12 @@ int hy_solve(hy_handle *h, const hy_factors *f, const double *d_b, double *d_x,
 int hy_refactorize_solve_batched(hy_handle *h, int64_t B, const double *d_vals,
                                  const double *d_b, double *d_x, double eps,
                                  const hy_factors *prior, int32_t *d_npert, uintptr_t stream);
+/* The two phases of hy_refactorize_solve_batched (same semantics), exposed so a
+ * caller can time them separately.  hy_solve_batched uses the factors of the last
+ * hy_refactorize_batched call on this handle (same B). */
+int hy_refactorize_batched(hy_handle *h, int64_t B, const double *d_vals, double eps,
+                           const hy_factors *prior, int32_t *d_npert, uintptr_t stream);
+int hy_solve_batched(hy_handle *h, int64_t B, const double *d_b, double *d_x, uintptr_t stream);
 /* Copy instance b's factor values from the last batched call into node layout. */
 int hy_batched_factor_values(hy_handle *h, int64_t b, double *d_out, uintptr_t stream);
 

@@ -66,6 +66,7 @@ struct hy_handle {
   double *d_by = nullptr;         // batched solve workspace
   int64_t by_cap = 0;
   int64_t last_B = 0;
+  const int32_t *last_iperm = nullptr;
   int64_t launches = 0;
   size_t sn_smem = 0;
 };
@@ -288,14 +289,7 @@ int hy_solve(hy_handle *h, const hy_factors *f, const double *d_b, double *d_x, 
   return HY_OK;
 }
 
-int hy_refactorize_solve_batched(hy_handle *h, int64_t B, const double *d_vals, const double *d_b,
-                                 double *d_x, double eps, const hy_factors *prior, int32_t *d_npert,
-                                 uintptr_t stream) {
-  if (!h || !h->uploaded) return fail(HY_INVALID_ARGUMENT, "symbolic not uploaded");
-  if (B <= 0 || !d_vals || !d_b || !d_x || !prior || !d_npert)
-    return fail(HY_INVALID_ARGUMENT, "null buffer or empty batch");
-  CK(cudaSetDevice(h->device));
-  cudaStream_t st = (cudaStream_t)stream;
+static int batch_prepare(hy_handle *h, int64_t B) {
   const int G = (int)((B + 31) / 32);
   const int64_t need = (int64_t)G * 32 * h->stored;
   if (need > h->bf_cap) {
@@ -311,13 +305,24 @@ int hy_refactorize_solve_batched(hy_handle *h, int64_t B, const double *d_vals, 
     CK(cudaMalloc((void **)&h->d_by, sizeof(double) * needy));
     h->by_cap = needy;
   }
+  return HY_OK;
+}
+
+int hy_refactorize_batched(hy_handle *h, int64_t B, const double *d_vals, double eps,
+                           const hy_factors *prior, int32_t *d_npert, uintptr_t stream) {
+  if (!h || !h->uploaded) return fail(HY_INVALID_ARGUMENT, "symbolic not uploaded");
+  if (B <= 0 || !d_vals || !prior || !d_npert)
+    return fail(HY_INVALID_ARGUMENT, "null buffer or empty batch");
+  if (eps < 0.0 || eps >= 1.0) return fail(HY_INVALID_ARGUMENT, "perturbation_epsilon outside [0,1)");
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = batch_prepare(h, B);
+  if (rc) return rc;
   h->last_B = B;
-  // prior anorm lives on the device: fetch it once (tiny, synchronous on this stream)
-  double anorm = 0.0;
-  CK(cudaMemcpyAsync(&anorm, prior->d_anorm, sizeof(double), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
+  h->last_iperm = prior->d_inner_perm;
   CK(cudaMemsetAsync(d_npert, 0, sizeof(int32_t) * B, st));
-  BatchP P{h->d_bf, d_vals, prior->d_inner_perm, eps * anorm, d_npert, B, h->stored};
+  const int G = (int)((B + 31) / 32);
+  BatchP P{h->d_bf, d_vals, prior->d_inner_perm, prior->d_anorm, eps, d_npert, B, h->stored};
   const Plan &pl = h->fplan;
   for (int l = 0; l < pl.nlev; ++l) {
     const int c = (int)(pl.aptr[l + 1] - pl.aptr[l]);
@@ -325,8 +330,20 @@ int hy_refactorize_solve_batched(hy_handle *h, int64_t B, const double *d_vals, 
     k_batch_factor<<<(unsigned)((tasks + 3) / 4), 128, 0, st>>>(h->S, P, pl.d_all + pl.aptr[l], c, G);
     h->launches++;
   }
+  CK(cudaGetLastError());
+  return HY_OK;
+}
+
+int hy_solve_batched(hy_handle *h, int64_t B, const double *d_b, double *d_x, uintptr_t stream) {
+  if (!h || !h->uploaded || B != h->last_B || !h->d_bf)
+    return fail(HY_INVALID_ARGUMENT, "no batched factors of this batch size");
+  if (!d_b || !d_x) return fail(HY_INVALID_ARGUMENT, "null buffer");
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int G = (int)((B + 31) / 32);
+  const Plan &pl = h->fplan;
   dim3 tg((h->S.n + 31) / 32, G);
-  k_batch_bhat<<<tg, 256, 0, st>>>(h->S, prior->d_inner_perm, d_b, h->d_by, B);
+  k_batch_bhat<<<tg, 256, 0, st>>>(h->S, h->last_iperm, d_b, h->d_by, B);
   h->launches++;
   for (int l = 0; l < pl.nlev; ++l) {
     const int c = (int)(pl.aptr[l + 1] - pl.aptr[l]);
@@ -347,6 +364,14 @@ int hy_refactorize_solve_batched(hy_handle *h, int64_t B, const double *d_vals, 
   h->launches++;
   CK(cudaGetLastError());
   return HY_OK;
+}
+
+int hy_refactorize_solve_batched(hy_handle *h, int64_t B, const double *d_vals, const double *d_b,
+                                 double *d_x, double eps, const hy_factors *prior, int32_t *d_npert,
+                                 uintptr_t stream) {
+  int rc = hy_refactorize_batched(h, B, d_vals, eps, prior, d_npert, stream);
+  if (rc) return rc;
+  return hy_solve_batched(h, B, d_b, d_x, stream);
 }
 
 int hy_batched_factor_values(hy_handle *h, int64_t b, double *d_out, uintptr_t stream) {

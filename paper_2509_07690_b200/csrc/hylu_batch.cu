@@ -40,6 +40,7 @@ __global__ void __launch_bounds__(BW * 32) k_batch_factor(DevSym S, BatchP P, co
     for (int q = lane; q < W; q += 32) tcs[warp][q] = S.cols[c0 + q];
   double *gbase = P.BF + (int64_t)g * P.stored * 32;
   const double *Ab = P.A + (int64_t)g * 32 * S.nnz;
+  const double thr = P.eps * P.anorm[0];
   const int nlive = (int)(P.B - (int64_t)g * 32 < 32 ? P.B - (int64_t)g * 32 : 32);
   __syncwarp();
   for (int t = 0; t < s; ++t) {
@@ -81,7 +82,7 @@ __global__ void __launch_bounds__(BW * 32) k_batch_factor(DevSym S, BatchP P, co
     double *dp = w + (int64_t)Lt * 32 + lane;
     const double piv = *dp;
     bool fired;
-    *dp = perturb(piv, P.thr, fired);
+    *dp = perturb(piv, thr, fired);
     if (fired && live) atomicAdd(&P.npert[b], 1);
     __syncwarp();
   }

@@ -48,7 +48,8 @@ struct BatchP {
   double *BF;            // interleaved factor workspace [G][stored][32]
   const double *A;       // [B][nnz]
   const int32_t *iperm;  // prior inner_perm [n]
-  double thr;            // eps * prior anorm
+  const double *anorm;   // prior anorm [1] (device)
+  double eps;
   int32_t *npert;        // [B]
   int64_t B;
   int64_t stored;

@@ -78,6 +78,9 @@ def library():
     lib.hy_solve.argtypes = [vp, ctypes.POINTER(FactorsDesc), vp, vp, u]
     lib.hy_refactorize_solve_batched.argtypes = [vp, i64, vp, vp, vp, ctypes.c_double,
                                                  ctypes.POINTER(FactorsDesc), vp, u]
+    lib.hy_refactorize_batched.argtypes = [vp, i64, vp, ctypes.c_double,
+                                           ctypes.POINTER(FactorsDesc), vp, u]
+    lib.hy_solve_batched.argtypes = [vp, i64, vp, vp, u]
     lib.hy_batched_factor_values.argtypes = [vp, i64, vp, u]
     _lib = lib
     return lib

@@ -159,8 +159,7 @@ def _dominant_diag(n, row_ptr, col_idx, offvals):
     diag = col_idx == rows
     vals = np.empty(len(col_idx))
     vals[~diag] = offvals
-    rs = np.zeros(n)
-    np.add.at(rs, rows[~diag], np.abs(offvals))
+    rs = np.bincount(rows[~diag], weights=np.abs(offvals), minlength=n)
     vals[diag] = np.where(rs > 0, 1.1 * rs, 1.0)
     return vals, diag
 
@@ -179,39 +178,60 @@ def circuit(n=200000, n_hubs=5, hub_nnz=2000, seed=SEEDS["c1"]):
                    {"n": n, "hubs": n_hubs, "hub_nnz": hub_nnz, "seed": seed})
 
 
-def batch_instance(A0, diag_mask, b_index, seed):
-    """Values and rhs of instance ``b_index`` of the c4 batch.
+class BatchValues:
+    """Per-instance values/rhs of the c4 batch (pattern work done once).
 
-    rng = default_rng(seed + 1 + b): off-diagonals x (1+U[-0.2,0.2]) (CSR order),
-    diagonal reset to 1.1 x row abs-sum, then rhs~U[-1,1] from the same stream.
-    """
-    rng = np.random.default_rng(seed + 1 + b_index)
-    n = A0.n
-    off = A0.values[~diag_mask] * (1.0 + rng.uniform(-0.2, 0.2, int((~diag_mask).sum())))
-    vals, _ = _dominant_diag(n, A0.row_ptr, A0.col_idx, off)
-    rhs = rng.uniform(-1.0, 1.0, n)
-    return vals, rhs
+    Instance b: rng = default_rng(seed + 1 + b); off-diagonals x (1+U[-0.2,0.2])
+    (CSR order), diagonal reset to 1.1 x row abs-sum (1.0 for an empty row), then
+    rhs~U[-1,1] from the same stream."""
+
+    def __init__(self, A0, seed):
+        n = A0.n
+        self.n, self.nnz, self.seed = n, A0.nnz, seed
+        rows = np.repeat(np.arange(n), np.diff(A0.row_ptr))
+        self.diag = A0.col_idx == rows
+        self.off_rows = rows[~self.diag]
+        self.base_off = np.asarray(A0.values)[~self.diag]
+
+    def instance(self, b, vals_out=None, rhs_out=None):
+        rng = np.random.default_rng(self.seed + 1 + b)
+        off = self.base_off * (1.0 + rng.uniform(-0.2, 0.2, len(self.base_off)))
+        vals = np.empty(self.nnz) if vals_out is None else vals_out
+        vals[~self.diag] = off
+        rs = np.bincount(self.off_rows, weights=np.abs(off), minlength=self.n)
+        vals[self.diag] = np.where(rs > 0, 1.1 * rs, 1.0)
+        rhs = rng.uniform(-1.0, 1.0, self.n) if rhs_out is None else rhs_out
+        if rhs_out is not None:
+            rhs[:] = rng.uniform(-1.0, 1.0, self.n)
+        return vals, rhs
+
+    def fill(self, indices, vals, rhs, threads=8):
+        """Generate instances ``indices`` into vals[len, nnz] / rhs[len, n] (threaded)."""
+        from concurrent.futures import ThreadPoolExecutor
+        idx = list(indices)
+
+        def work(t):
+            self.instance(idx[t], vals[t], rhs[t])
+
+        with ThreadPoolExecutor(max(1, threads)) as ex:
+            list(ex.map(work, range(len(idx))))
 
 
-def circuit_batch(batch=4096, n=20000, n_hubs=3, hub_nnz=2000, seed=SEEDS["c4"], instances=None):
+def circuit_batch(batch=4096, n=20000, n_hubs=3, hub_nnz=2000, seed=SEEDS["c4"], instances=None,
+                  threads=8):
     """c4: base pattern/values = circuit(n, n_hubs, hub_nnz, seed); instance b per
-    ``batch_instance``.  ``instances`` restricts generation to a subset of indices
-    (the parity tests and the CPU baseline sample use a few)."""
+    ``BatchValues``; ``A0`` carries instance 0's values (analyzed once).
+    ``instances`` restricts generation to a subset of indices."""
     base = circuit(n, n_hubs, hub_nnz, seed)
-    A = base.A
-    rows = np.repeat(np.arange(n), np.diff(A.row_ptr))
-    diag = A.col_idx == rows
-    idx = range(batch) if instances is None else instances
-    vals = np.empty((len(idx), A.nnz))
+    gen = BatchValues(base.A, seed)
+    idx = list(range(batch)) if instances is None else list(instances)
+    vals = np.empty((len(idx), base.A.nnz))
     rhs = np.empty((len(idx), n))
-    for t, bi in enumerate(idx):
-        vals[t], rhs[t] = batch_instance(A, diag, bi, seed)
-    A0 = A.with_values(vals[0]) if (instances is None or 0 in list(idx)) else A
-    if instances is not None and 0 not in list(idx):
-        v0, _ = batch_instance(A, diag, 0, seed)
-        A0 = A.with_values(v0)
+    gen.fill(idx, vals, rhs, threads)
+    v0 = vals[idx.index(0)] if 0 in idx else gen.instance(0)[0]
+    A0 = base.A.with_values(v0)
     return BatchProblem("c4_batch_%dx%d" % (len(idx), n), A0, vals, rhs, "amd",
-                        {"n": n, "batch": batch, "instances": list(idx), "seed": seed})
+                        {"n": n, "batch": batch, "instances": idx, "seed": seed, "gen": gen})
 
 
 # --------------------------------------------------------------------------- c2
