@@ -113,6 +113,29 @@ int hy_refactorize(hy_handle *h, const double *d_avals, double eps, const hy_fac
 int hy_solve(hy_handle *h, const hy_factors *f, const double *d_b, double *d_x,
              uintptr_t stream);
 
+/* Row programs for the batched path (built on the host by schedule.py for a given
+ * prior inner_perm).  Must be uploaded before the
+ * batched calls, and must match the inner_perm of the prior they are used with. */
+typedef struct {
+  int64_t nsteps, nrel, nhubrows, nlev, nhpos, npred;
+  const int64_t *row_ptr;   /* [n+1] */
+  const int32_t *st_p;      /* [nsteps] */
+  const int32_t *st_j;
+  const int64_t *st_src;
+  const int32_t *st_cnt;
+  const int64_t *st_rel;
+  const int32_t *rel;       /* [nrel] */
+  const uint8_t *node_hub;  /* [nnodes] */
+  const int64_t *hrow_lev;  /* [nhubrows+1] */
+  const int64_t *lev_ptr;   /* [nlev+1] */
+  const int32_t *hpos;      /* [nhpos] */
+  const int64_t *hdiv;      /* [nhpos] */
+  const int64_t *hpp;       /* [nhpos+1] */
+  const int32_t *pred_p;    /* [npred] */
+  const int64_t *pred_u;    /* [npred] */
+} hy_row_programs;
+int hy_upload_row_programs(hy_handle *h, const hy_row_programs *progs);
+
 /* Batched refactorize + solve of B instances sharing the uploaded symbolic
  * structure and the prior's inner_perm / anorm.  d_vals [B][nnz], d_b / d_x [B][n]
  * (row-major), d_npert [B] receives each instance's perturbation count.  The
@@ -124,7 +147,10 @@ int hy_refactorize_solve_batched(hy_handle *h, int64_t B, const double *d_vals,
  * caller can time them separately.  hy_solve_batched uses the factors of the last
  * hy_refactorize_batched call on this handle (same B). */
 int hy_refactorize_batched(hy_handle *h, int64_t B, const double *d_vals, double eps,
-                           const hy_factors *prior, int32_t *d_npert, uintptr_t stream);
+                           const hy_factors *prior, int32_t *d_npert, const double *d_b_fuse,
+                           uintptr_t stream);
+/* d_b == NULL: use the forward substitution fused into the last
+ * hy_refactorize_batched(..., d_b_fuse != NULL) call (only the backward pass runs). */
 int hy_solve_batched(hy_handle *h, int64_t B, const double *d_b, double *d_x, uintptr_t stream);
 /* Copy instance b's factor values from the last batched call into node layout. */
 int hy_batched_factor_values(hy_handle *h, int64_t b, double *d_out, uintptr_t stream);

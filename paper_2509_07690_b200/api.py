@@ -250,10 +250,14 @@ class BatchedRefactorizer:
     """B x [refactorize → solve] sharing one symbolic structure on one GPU
     (BASELINE config 4).  Reuses ``prior``'s inner_perm and anorm."""
 
-    def __init__(self, prior, eps=1e-8):
+    def __init__(self, prior, eps=1e-8, hub_steps=None):
+        from .schedule import HUB_STEPS, build_programs
         self.prior = prior
         self.ctx = prior._ctx
         self.eps = eps
+        self.programs = build_programs(self.ctx.analysis, prior.host_inner_perm(),
+                                       HUB_STEPS if hub_steps is None else hub_steps)
+        self.ctx.upload_programs(self.programs)
 
     def run(self, d_vals, d_rhs, d_x=None, d_npert=None, stream=None):
         import torch
@@ -265,9 +269,11 @@ class BatchedRefactorizer:
             d_x = torch.empty((B, self.ctx.n), dtype=torch.float64, device=self.ctx.device)
         if d_npert is None:
             d_npert = torch.empty(B, dtype=torch.int32, device=self.ctx.device)
-        check(self.ctx.lib.hy_refactorize_solve_batched(
-            self.ctx.h, B, d_vals.data_ptr(), d_rhs.data_ptr(), d_x.data_ptr(), float(self.eps),
-            self.prior._desc, d_npert.data_ptr(), self.ctx.stream_handle(stream)))
+        sh = self.ctx.stream_handle(stream)
+        check(self.ctx.lib.hy_refactorize_batched(
+            self.ctx.h, B, d_vals.data_ptr(), float(self.eps), self.prior._desc, d_npert.data_ptr(),
+            d_rhs.data_ptr(), sh))
+        check(self.ctx.lib.hy_solve_batched(self.ctx.h, B, None, d_x.data_ptr(), sh))
         return d_x, d_npert
 
     def factor_values(self, b, stream=None):
@@ -279,12 +285,12 @@ class BatchedRefactorizer:
         return out
 
 
-def refactorize_solve_batched(values, prior, rhs, opts=None):
+def refactorize_solve_batched(values, prior, rhs, opts=None, hub_steps=None):
     """Host-facing batched call: values [B, nnz], rhs [B, n] (numpy or CUDA tensors)
     → (x [B, n] numpy, perturbation counts [B])."""
     import torch
     opts = opts or FactorOptions()
-    br = BatchedRefactorizer(prior, opts.perturbation_epsilon)
+    br = BatchedRefactorizer(prior, opts.perturbation_epsilon, hub_steps)
     dev = br.ctx.device
     dv = values if isinstance(values, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(values)).to(dev)
     dr = rhs if isinstance(rhs, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(rhs)).to(dev)

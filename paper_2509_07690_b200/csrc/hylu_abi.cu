@@ -19,7 +19,8 @@ __global__ void k_bhat(DevSym, const int32_t *, const double *, double *);
 __global__ void k_xout(DevSym, const double *, double *);
 __global__ void k_fwd(DevSym, const double *, const int32_t *, int, double *);
 __global__ void k_bwd(DevSym, const double *, const int32_t *, int, double *);
-__global__ void k_batch_factor(DevSym, BatchP, const int32_t *, int, int);
+__global__ void k_bt_rows(DevSym, BatchP, DevProg, const int32_t *, int, int, const double *, double *);
+__global__ void k_bt_hub(DevSym, BatchP, DevProg, const int32_t *, int, int, const double *, double *);
 __global__ void k_batch_bhat(DevSym, const int32_t *, const double *, double *, int64_t);
 __global__ void k_batch_xout(DevSym, const double *, double *, int64_t);
 __global__ void k_batch_fwd(DevSym, const double *, int64_t, const int32_t *, int, int, double *);
@@ -67,6 +68,13 @@ struct hy_handle {
   int64_t by_cap = 0;
   int64_t last_B = 0;
   const int32_t *last_iperm = nullptr;
+  bool last_fused = false;
+  // batched row programs (schedule.py), built per prior inner_perm
+  DevProg prog{};
+  bool prog_ok = false;
+  std::vector<void *> prog_allocs;
+  std::vector<int64_t> bl_rptr, bl_hptr;   // per level: non-hub / hub node offsets
+  int32_t *d_bl_rows = nullptr, *d_bl_hubs = nullptr;
   int64_t launches = 0;
   size_t sn_smem = 0;
 };
@@ -110,6 +118,22 @@ static int build_plan(hy_handle *h, Plan &pl, const int64_t *lptr, const int32_t
   return HY_OK;
 }
 
+template <class T>
+static int upload_prog(hy_handle *h, T **dst, const T *src, int64_t count) {
+  *dst = nullptr;
+  if (count <= 0) return HY_OK;
+  CK(cudaMalloc((void **)dst, sizeof(T) * count));
+  h->prog_allocs.push_back(*dst);
+  CK(cudaMemcpy(*dst, src, sizeof(T) * count, cudaMemcpyHostToDevice));
+  return HY_OK;
+}
+
+#define UPP(dst, src, cnt)                                 \
+  do {                                                     \
+    int _r = upload_prog(h, dst, src, (int64_t)(cnt));     \
+    if (_r) return _r;                                     \
+  } while (0)
+
 extern "C" {
 
 const char *hy_last_error(void) { return g_err.c_str(); }
@@ -134,6 +158,7 @@ void hy_destroy(hy_handle *h) {
   if (!h) return;
   cudaSetDevice(h->device);
   for (void *p : h->allocs) cudaFree(p);
+  for (void *p : h->prog_allocs) cudaFree(p);
   if (h->d_bf) cudaFree(h->d_bf);
   if (h->d_by) cudaFree(h->d_by);
   delete h;
@@ -289,6 +314,62 @@ int hy_solve(hy_handle *h, const hy_factors *f, const double *d_b, double *d_x, 
   return HY_OK;
 }
 
+int hy_upload_row_programs(hy_handle *h, const hy_row_programs *d) {
+  if (!h || !h->uploaded || !d) return fail(HY_INVALID_ARGUMENT, "symbolic not uploaded / null");
+  CK(cudaSetDevice(h->device));
+  CK(cudaDeviceSynchronize());
+  for (void *p : h->prog_allocs) cudaFree(p);
+  h->prog_allocs.clear();
+  h->prog_ok = false;
+  const int64_t n = h->S.n, nn = h->S.nn;
+  DevProg &R = h->prog;
+  int64_t *p64;
+  int32_t *p32;
+  UPP(&p64, d->row_ptr, n + 1); R.row_ptr = p64;
+  UPP(&p32, d->st_p, d->nsteps); R.st_p = p32;
+  UPP(&p32, d->st_j, d->nsteps); R.st_j = p32;
+  UPP(&p64, d->st_src, d->nsteps); R.st_src = p64;
+  UPP(&p32, d->st_cnt, d->nsteps); R.st_cnt = p32;
+  UPP(&p64, d->st_rel, d->nsteps); R.st_rel = p64;
+  UPP(&p32, d->rel, d->nrel); R.rel = p32;
+  std::vector<int32_t> hub_base(nn, -1);
+  std::vector<int64_t> first(nn + 1);
+  CK(cudaMemcpy(first.data(), h->S.first, sizeof(int64_t) * (nn + 1), cudaMemcpyDeviceToHost));
+  int32_t hr = 0;
+  for (int64_t u = 0; u < nn; ++u)
+    if (d->node_hub[u]) {
+      hub_base[u] = hr;
+      hr += (int32_t)(first[u + 1] - first[u]);
+    }
+  if (hr != d->nhubrows) return fail(HY_INVALID_ARGUMENT, "hub row count mismatch");
+  UPP(&p32, hub_base.data(), nn); R.hub_base = p32;
+  UPP(&p64, d->hrow_lev, d->nhubrows + 1); R.hrow_lev = p64;
+  UPP(&p64, d->lev_ptr, d->nlev + 1); R.lev_ptr = p64;
+  UPP(&p32, d->hpos, d->nhpos); R.hpos = p32;
+  UPP(&p64, d->hdiv, d->nhpos); R.hdiv = p64;
+  UPP(&p64, d->hpp, d->nhpos + 1); R.hpp = p64;
+  UPP(&p32, d->pred_p, d->npred); R.pred_p = p32;
+  UPP(&p64, d->pred_u, d->npred); R.pred_u = p64;
+  // per level split: non-hub nodes / hub nodes
+  const Plan &pl = h->fplan;
+  std::vector<int32_t> all(pl.aptr[pl.nlev]);
+  if (!all.empty())
+    CK(cudaMemcpy(all.data(), pl.d_all, sizeof(int32_t) * all.size(), cudaMemcpyDeviceToHost));
+  std::vector<int32_t> rows, hubs;
+  h->bl_rptr.assign(pl.nlev + 1, 0);
+  h->bl_hptr.assign(pl.nlev + 1, 0);
+  for (int l = 0; l < pl.nlev; ++l) {
+    for (int64_t k = pl.aptr[l]; k < pl.aptr[l + 1]; ++k)
+      (d->node_hub[all[k]] ? hubs : rows).push_back(all[k]);
+    h->bl_rptr[l + 1] = (int64_t)rows.size();
+    h->bl_hptr[l + 1] = (int64_t)hubs.size();
+  }
+  UPP(&h->d_bl_rows, rows.data(), rows.size());
+  UPP(&h->d_bl_hubs, hubs.data(), hubs.size());
+  h->prog_ok = true;
+  return HY_OK;
+}
+
 static int batch_prepare(hy_handle *h, int64_t B) {
   const int G = (int)((B + 31) / 32);
   const int64_t need = (int64_t)G * 32 * h->stored;
@@ -309,10 +390,12 @@ static int batch_prepare(hy_handle *h, int64_t B) {
 }
 
 int hy_refactorize_batched(hy_handle *h, int64_t B, const double *d_vals, double eps,
-                           const hy_factors *prior, int32_t *d_npert, uintptr_t stream) {
+                           const hy_factors *prior, int32_t *d_npert, const double *d_b_fuse,
+                           uintptr_t stream) {
   if (!h || !h->uploaded) return fail(HY_INVALID_ARGUMENT, "symbolic not uploaded");
   if (B <= 0 || !d_vals || !prior || !d_npert)
     return fail(HY_INVALID_ARGUMENT, "null buffer or empty batch");
+  if (!h->prog_ok) return fail(HY_INVALID_ARGUMENT, "row programs not uploaded");
   if (eps < 0.0 || eps >= 1.0) return fail(HY_INVALID_ARGUMENT, "perturbation_epsilon outside [0,1)");
   CK(cudaSetDevice(h->device));
   cudaStream_t st = (cudaStream_t)stream;
@@ -323,12 +406,21 @@ int hy_refactorize_batched(hy_handle *h, int64_t B, const double *d_vals, double
   CK(cudaMemsetAsync(d_npert, 0, sizeof(int32_t) * B, st));
   const int G = (int)((B + 31) / 32);
   BatchP P{h->d_bf, d_vals, prior->d_inner_perm, prior->d_anorm, eps, d_npert, B, h->stored};
-  const Plan &pl = h->fplan;
-  for (int l = 0; l < pl.nlev; ++l) {
-    const int c = (int)(pl.aptr[l + 1] - pl.aptr[l]);
-    const int64_t tasks = (int64_t)c * G;
-    k_batch_factor<<<(unsigned)((tasks + 3) / 4), 128, 0, st>>>(h->S, P, pl.d_all + pl.aptr[l], c, G);
-    h->launches++;
+  h->last_fused = d_b_fuse != nullptr;
+  for (int l = 0; l < h->fplan.nlev; ++l) {
+    const int nr = (int)(h->bl_rptr[l + 1] - h->bl_rptr[l]);
+    const int nh = (int)(h->bl_hptr[l + 1] - h->bl_hptr[l]);
+    if (nr) {
+      const int64_t tasks = (int64_t)nr * G;
+      k_bt_rows<<<(unsigned)((tasks + 3) / 4), 128, 0, st>>>(h->S, P, h->prog, h->d_bl_rows + h->bl_rptr[l],
+                                                             nr, G, d_b_fuse, h->d_by);
+      h->launches++;
+    }
+    if (nh) {
+      k_bt_hub<<<(unsigned)(nh * G), 256, 0, st>>>(h->S, P, h->prog, h->d_bl_hubs + h->bl_hptr[l], nh, G,
+                                                  d_b_fuse, h->d_by);
+      h->launches++;
+    }
   }
   CK(cudaGetLastError());
   return HY_OK;
@@ -337,12 +429,15 @@ int hy_refactorize_batched(hy_handle *h, int64_t B, const double *d_vals, double
 int hy_solve_batched(hy_handle *h, int64_t B, const double *d_b, double *d_x, uintptr_t stream) {
   if (!h || !h->uploaded || B != h->last_B || !h->d_bf)
     return fail(HY_INVALID_ARGUMENT, "no batched factors of this batch size");
-  if (!d_b || !d_x) return fail(HY_INVALID_ARGUMENT, "null buffer");
+  if (!d_x) return fail(HY_INVALID_ARGUMENT, "null buffer");
+  if (!d_b && !h->last_fused)
+    return fail(HY_INVALID_ARGUMENT, "d_b == NULL needs a refactorization with a fused rhs");
   CK(cudaSetDevice(h->device));
   cudaStream_t st = (cudaStream_t)stream;
   const int G = (int)((B + 31) / 32);
   const Plan &pl = h->fplan;
   dim3 tg((h->S.n + 31) / 32, G);
+  if (d_b) {
   k_batch_bhat<<<tg, 256, 0, st>>>(h->S, h->last_iperm, d_b, h->d_by, B);
   h->launches++;
   for (int l = 0; l < pl.nlev; ++l) {
@@ -351,6 +446,7 @@ int hy_solve_batched(hy_handle *h, int64_t B, const double *d_b, double *d_x, ui
     k_batch_fwd<<<(unsigned)((tasks + 3) / 4), 128, 0, st>>>(h->S, h->d_bf, h->stored,
                                                            pl.d_all + pl.aptr[l], c, G, h->d_by);
     h->launches++;
+  }
   }
   const Plan &bp = h->bplan;
   for (int l = 0; l < bp.nlev; ++l) {
@@ -369,9 +465,9 @@ int hy_solve_batched(hy_handle *h, int64_t B, const double *d_b, double *d_x, ui
 int hy_refactorize_solve_batched(hy_handle *h, int64_t B, const double *d_vals, const double *d_b,
                                  double *d_x, double eps, const hy_factors *prior, int32_t *d_npert,
                                  uintptr_t stream) {
-  int rc = hy_refactorize_batched(h, B, d_vals, eps, prior, d_npert, stream);
+  int rc = hy_refactorize_batched(h, B, d_vals, eps, prior, d_npert, d_b, stream);
   if (rc) return rc;
-  return hy_solve_batched(h, B, d_b, d_x, stream);
+  return hy_solve_batched(h, B, nullptr, d_x, stream);
 }
 
 int hy_batched_factor_values(hy_handle *h, int64_t b, double *d_out, uintptr_t stream) {

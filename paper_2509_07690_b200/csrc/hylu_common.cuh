@@ -55,6 +55,25 @@ struct BatchP {
   int64_t stored;
 };
 
+// Row programs (schedule.py) resident on the device.
+struct DevProg {
+  const int64_t *row_ptr;   // [n+1]
+  const int32_t *st_p;
+  const int32_t *st_j;
+  const int64_t *st_src;
+  const int32_t *st_cnt;
+  const int64_t *st_rel;
+  const int32_t *rel;
+  const int32_t *hub_base;  // [nn] first hub-row index of a hub node, -1 otherwise
+  const int64_t *hrow_lev;
+  const int64_t *lev_ptr;
+  const int32_t *hpos;
+  const int64_t *hdiv;
+  const int64_t *hpp;
+  const int32_t *pred_p;
+  const int64_t *pred_u;
+};
+
 __device__ __forceinline__ int lower_bound_i32(const int32_t *c, int lo, int hi, int key) {
   while (lo < hi) {
     int mid = (lo + hi) >> 1;

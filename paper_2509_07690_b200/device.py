@@ -53,6 +53,18 @@ class FactorsDesc(ctypes.Structure):
     ]
 
 
+class ProgramsDesc(ctypes.Structure):
+    _fields_ = [
+        ("nsteps", ctypes.c_int64), ("nrel", ctypes.c_int64), ("nhubrows", ctypes.c_int64),
+        ("nlev", ctypes.c_int64), ("nhpos", ctypes.c_int64), ("npred", ctypes.c_int64),
+        ("row_ptr", ctypes.c_void_p), ("st_p", ctypes.c_void_p), ("st_j", ctypes.c_void_p),
+        ("st_src", ctypes.c_void_p), ("st_cnt", ctypes.c_void_p), ("st_rel", ctypes.c_void_p),
+        ("rel", ctypes.c_void_p), ("node_hub", ctypes.c_void_p), ("hrow_lev", ctypes.c_void_p),
+        ("lev_ptr", ctypes.c_void_p), ("hpos", ctypes.c_void_p), ("hdiv", ctypes.c_void_p),
+        ("hpp", ctypes.c_void_p), ("pred_p", ctypes.c_void_p), ("pred_u", ctypes.c_void_p),
+    ]
+
+
 def library():
     """Load the CUDA library (building it in-tree first if it is absent)."""
     global _lib
@@ -79,7 +91,8 @@ def library():
     lib.hy_refactorize_solve_batched.argtypes = [vp, i64, vp, vp, vp, ctypes.c_double,
                                                  ctypes.POINTER(FactorsDesc), vp, u]
     lib.hy_refactorize_batched.argtypes = [vp, i64, vp, ctypes.c_double,
-                                           ctypes.POINTER(FactorsDesc), vp, u]
+                                           ctypes.POINTER(FactorsDesc), vp, vp, u]
+    lib.hy_upload_row_programs.argtypes = [vp, ctypes.POINTER(ProgramsDesc)]
     lib.hy_solve_batched.argtypes = [vp, i64, vp, vp, u]
     lib.hy_batched_factor_values.argtypes = [vp, i64, vp, u]
     _lib = lib
@@ -180,6 +193,22 @@ class DeviceContext:
                            bufs["anorm"].data_ptr(), bufs["status"].data_ptr(),
                            bufs["pert_rows"].data_ptr(), bufs["pert_vals"].data_ptr(), pert_cap)
         return bufs, desc
+
+    def upload_programs(self, progs):
+        """Upload schedule.RowPrograms (built for a prior inner_perm)."""
+        arrs = {k: np.ascontiguousarray(getattr(progs, k)) for k in (
+            "row_ptr", "st_p", "st_j", "st_src", "st_cnt", "st_rel", "rel", "node_hub", "hrow_lev",
+            "lev_ptr", "hpos", "hdiv", "hpp", "pred_p", "pred_u")}
+        d = ProgramsDesc()
+        d.nsteps, d.nrel = len(progs.st_p), len(progs.rel)
+        d.nhubrows = len(progs.hrow_lev) - 1
+        d.nlev = len(progs.lev_ptr) - 1
+        d.nhpos, d.npred = len(progs.hpos), len(progs.pred_p)
+        for k, v in arrs.items():
+            setattr(d, k, v.ctypes.data if v.size else None)
+        with self.torch.cuda.device(self.device):
+            check(self.lib.hy_upload_row_programs(self.h, ctypes.byref(d)))
+        self._programs = arrs
 
     def launches(self):
         return int(self.lib.hy_launch_count(self.h))

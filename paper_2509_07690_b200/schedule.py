@@ -1,0 +1,269 @@
+"""Host-built device schedules ("row programs") — uploaded once, shared by every
+instance of a batch and by every refactorization.
+
+Up-looking row i applies, for each L position p in ascending
+order, the source row j = cols[p]: l = w[p] / U(j,j); w[pos(k)] -= l·U(j,k).  The
+program of a factor row lists only the *structurally nonzero* steps (L positions
+reached by A's pattern or by an earlier step — union padding inside supernodes
+and never-filled positions have l = 0 exactly and are skipped, which leaves every
+stored value unchanged) together with the target positions ``rel`` of every
+U(j, >j) entry, so the device never searches column lists.
+
+Rows with many steps (circuit hub rows: 7k–27k L entries, but only ~80–90
+dependency levels inside the row) get a *pull* program instead: positions are
+grouped by intra-row level, and each position gathers its contributions
+w[p] = m[p] − Σ_s l_s·U_s(col p) in ascending step order (the same operation
+order as the sequential push loop), so a whole CTA works on one row.
+
+Supernode rows use the fixed pivot order of a prior factorization (refactorize
+semantics), so programs are built per prior ``inner_perm``.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+from numba import njit
+
+HUB_STEPS = 384
+
+
+@njit(cache=True)
+def _programs(n, first, kind, colptr, cols, nl, valoff, node_of, a_ptr, mrow_src, colpos, iperm,
+              hub_steps):
+    nn = len(kind)
+    # upper bounds for allocation: steps <= sum of L widths incl. in-block parts
+    max_steps = 0
+    for u in range(nn):
+        s = first[u + 1] - first[u]
+        max_steps += s * nl[u] + s * (s - 1) // 2
+    st_p = np.empty(max_steps, np.int32)
+    st_j = np.empty(max_steps, np.int32)
+    st_src = np.empty(max_steps, np.int64)
+    st_cnt = np.empty(max_steps, np.int32)
+    st_rel = np.empty(max_steps, np.int64)
+    row_ptr = np.zeros(n + 1, np.int64)
+    cap_rel = 1 << 20
+    rel = np.empty(cap_rel, np.int32)
+    nrel = 0
+    nst = 0
+    pos_of = np.full(n, -1, np.int64)
+    nz = np.zeros(1, np.uint8)
+    maxW = 0
+    for u in range(nn):
+        maxW = max(maxW, colptr[u + 1] - colptr[u])
+    nz = np.zeros(maxW, np.uint8)
+    node_hub = np.zeros(nn, np.uint8)
+    for u in range(nn):
+        r = first[u]
+        s = first[u + 1] - r
+        c0 = colptr[u]
+        W = colptr[u + 1] - c0
+        L = nl[u]
+        for q in range(W):
+            pos_of[cols[c0 + q]] = q
+        for t in range(s):
+            i = r + t
+            nz[:W] = 0
+            src_row = r + iperm[i] if kind[u] == 1 else r
+            a = mrow_src[src_row]
+            for e in range(a_ptr[a], a_ptr[a + 1]):
+                nz[colpos[e]] = 1
+            Lt = L + t
+            for p in range(Lt):
+                if nz[p] == 0:
+                    continue
+                j = cols[c0 + p]
+                v = node_of[j]
+                tj = j - first[v]
+                vc0 = colptr[v]
+                vW = colptr[v + 1] - vc0
+                sd = nl[v] + tj
+                cnt = vW - sd - 1
+                if nrel + cnt > cap_rel:
+                    cap_rel = max(2 * cap_rel, nrel + cnt)
+                    tmp = np.empty(cap_rel, np.int32)
+                    tmp[:nrel] = rel[:nrel]
+                    rel = tmp
+                st_p[nst] = p
+                st_j[nst] = j
+                st_src[nst] = valoff[v] + tj * vW + sd
+                st_cnt[nst] = cnt
+                st_rel[nst] = nrel
+                for q in range(sd + 1, vW):
+                    tp = pos_of[cols[vc0 + q]]
+                    rel[nrel] = tp
+                    nz[tp] = 1
+                    nrel += 1
+                nst += 1
+            row_ptr[i + 1] = nst
+            if row_ptr[i + 1] - row_ptr[i] > hub_steps:
+                node_hub[u] = 1
+        for q in range(W):
+            pos_of[cols[c0 + q]] = -1
+    return (row_ptr, st_p[:nst].copy(), st_j[:nst].copy(), st_src[:nst].copy(),
+            st_cnt[:nst].copy(), st_rel[:nst].copy(), rel[:nrel].copy(), node_hub)
+
+
+@njit(cache=True)
+def _pull(n, first, colptr, nl, valoff, a_ptr, mrow_src, colpos, kind, iperm, hub_nodes, row_ptr,
+          st_p, st_src, st_cnt, st_rel, rel):
+    """Pull programs for every row of the hub nodes.
+
+    Per hub row (in node order): positions grouped by intra-row level; per position
+    its contributions (multiplier position, U value offset) in ascending step order
+    and its kind: >=0 → L position (divide by the value at that offset),
+    -1 → U position, -2 → pivot."""
+    nrows = 0
+    for k in range(len(hub_nodes)):
+        u = hub_nodes[k]
+        nrows += first[u + 1] - first[u]
+    hrow_lev = np.zeros(nrows + 1, np.int64)      # offsets into lev_ptr
+    lev_ptr_l = [np.int64(0)]
+    pos_l = []
+    div_l = []
+    pp_l = [np.int64(0)]
+    pred_p_l = []
+    pred_u_l = []
+    hr = 0
+    nlev_tot = 0
+    for k in range(len(hub_nodes)):
+        u = hub_nodes[k]
+        r = first[u]
+        s = first[u + 1] - r
+        W = colptr[u + 1] - colptr[u]
+        L = nl[u]
+        for t in range(s):
+            i = r + t
+            Lt = L + t
+            level = np.full(W, -1, np.int64)
+            npred = np.zeros(W, np.int64)
+            step_at = np.full(W, -1, np.int64)
+            src_row = r + iperm[i] if kind[u] == 1 else r
+            a = mrow_src[src_row]
+            for e in range(a_ptr[a], a_ptr[a + 1]):
+                level[colpos[e]] = 0
+            for st in range(row_ptr[i], row_ptr[i + 1]):
+                p = st_p[st]
+                step_at[p] = st
+                lp = level[p]
+                for q in range(st_cnt[st]):
+                    tp = rel[st_rel[st] + q]
+                    npred[tp] += 1
+                    if lp + 1 > level[tp]:
+                        level[tp] = lp + 1
+            maxl = level.max()
+            # positions by level (structurally nonzero ones only)
+            cnt = np.zeros(maxl + 2, np.int64)
+            for p in range(W):
+                if level[p] >= 0:
+                    cnt[level[p] + 1] += 1
+            for l in range(maxl + 1):
+                cnt[l + 1] += cnt[l]
+            order = np.empty(cnt[maxl + 1], np.int64)
+            fillp = cnt[:maxl + 1].copy()
+            for p in range(W):
+                if level[p] >= 0:
+                    order[fillp[level[p]]] = p
+                    fillp[level[p]] += 1
+            # pred lists per position (ascending step order)
+            pstart = np.zeros(W + 1, np.int64)
+            for p in range(W):
+                pstart[p + 1] = pstart[p] + npred[p]
+            pp = np.empty(pstart[W], np.int32)
+            pu = np.empty(pstart[W], np.int64)
+            fill2 = pstart[:W].copy()
+            for st in range(row_ptr[i], row_ptr[i + 1]):
+                p = st_p[st]
+                for q in range(st_cnt[st]):
+                    tp = rel[st_rel[st] + q]
+                    pp[fill2[tp]] = p
+                    pu[fill2[tp]] = st_src[st] + 1 + q
+                    fill2[tp] += 1
+            for l in range(maxl + 1):
+                lev_ptr_l.append(lev_ptr_l[-1] + (cnt[l + 1] - cnt[l]))
+            nlev_tot += maxl + 1
+            hrow_lev[hr + 1] = nlev_tot
+            for x in range(len(order)):
+                p = order[x]
+                pos_l.append(np.int32(p))
+                if p < Lt:
+                    div_l.append(st_src[step_at[p]])
+                elif p == Lt:
+                    div_l.append(np.int64(-2))
+                else:
+                    div_l.append(np.int64(-1))
+                for y in range(pstart[p], pstart[p + 1]):
+                    pred_p_l.append(pp[y])
+                    pred_u_l.append(pu[y])
+                pp_l.append(pp_l[-1] + (pstart[p + 1] - pstart[p]))
+            hr += 1
+    lev_ptr = np.empty(len(lev_ptr_l), np.int64)
+    for x in range(len(lev_ptr_l)):
+        lev_ptr[x] = lev_ptr_l[x]
+    hpos = np.empty(len(pos_l), np.int32)
+    hdiv = np.empty(len(div_l), np.int64)
+    for x in range(len(pos_l)):
+        hpos[x] = pos_l[x]
+        hdiv[x] = div_l[x]
+    hpp = np.empty(len(pp_l), np.int64)
+    for x in range(len(pp_l)):
+        hpp[x] = pp_l[x]
+    pred_p = np.empty(len(pred_p_l), np.int32)
+    pred_u = np.empty(len(pred_u_l), np.int64)
+    for x in range(len(pred_p_l)):
+        pred_p[x] = pred_p_l[x]
+        pred_u[x] = pred_u_l[x]
+    return hrow_lev, lev_ptr, hpos, hdiv, hpp, pred_p, pred_u
+
+
+@dataclass
+class RowPrograms:
+    row_ptr: np.ndarray     # int64[n+1] steps of factor row i
+    st_p: np.ndarray        # int32 multiplier position in the target row
+    st_j: np.ndarray        # int32 source row (forward-solve coupling)
+    st_src: np.ndarray      # int64 offset of U(j,j) in node storage
+    st_cnt: np.ndarray      # int32 number of U(j,>j) entries
+    st_rel: np.ndarray      # int64 offset into rel
+    rel: np.ndarray         # int32 target positions of U(j,>j) entries
+    node_hub: np.ndarray    # uint8[nn]
+    hub_nodes: np.ndarray   # int32
+    hrow_lev: np.ndarray    # int64[nhubrows+1] -> lev_ptr index
+    lev_ptr: np.ndarray     # int64 -> hpos index
+    hpos: np.ndarray        # int32 positions in level order
+    hdiv: np.ndarray        # int64 per position: diag offset (L), -1 (U), -2 (pivot)
+    hpp: np.ndarray         # int64[len(hpos)+1] -> pred index
+    pred_p: np.ndarray      # int32
+    pred_u: np.ndarray      # int64
+
+    @property
+    def nsteps(self):
+        return len(self.st_p)
+
+    def nbytes(self):
+        return sum(getattr(self, k).nbytes for k in self.__dataclass_fields__)
+
+
+def build_programs(an, inner_perm, hub_steps=HUB_STEPS):
+    s = an.symbolic
+    vm = an.vmap
+    ip = np.ascontiguousarray(inner_perm, np.int64)
+    (row_ptr, st_p, st_j, st_src, st_cnt, st_rel, rel, node_hub) = _programs(
+        s.n, s.node_first, s.node_kind, s.colptr, s.cols, s.nl, s.valoff, s.node_of,
+        an.A.row_ptr, vm.mrow_src, vm.colpos, ip, hub_steps)
+    hub_nodes = np.flatnonzero(node_hub).astype(np.int32)
+    if len(hub_nodes):
+        hrow_lev, lev_ptr, hpos, hdiv, hpp, pred_p, pred_u = _pull(
+            s.n, s.node_first, s.colptr, s.nl, s.valoff, an.A.row_ptr, vm.mrow_src, vm.colpos,
+            s.node_kind, ip, hub_nodes.astype(np.int64), row_ptr, st_p, st_src, st_cnt, st_rel, rel)
+    else:
+        hrow_lev = np.zeros(1, np.int64)
+        lev_ptr = np.zeros(1, np.int64)
+        hpos = np.zeros(0, np.int32)
+        hdiv = np.zeros(0, np.int64)
+        hpp = np.zeros(1, np.int64)
+        pred_p = np.zeros(0, np.int32)
+        pred_u = np.zeros(0, np.int64)
+    return RowPrograms(row_ptr, st_p, st_j, st_src, st_cnt, st_rel, rel, node_hub, hub_nodes,
+                       hrow_lev, lev_ptr, hpos, hdiv, hpp, pred_p, pred_u)

@@ -64,13 +64,14 @@ def test_refactorize_matches_oracle(name):
     assert np.array_equal(f1.host_values(), f0.host_values())
 
 
-def test_batched_matches_oracle():
-    bp = gen.config("c4", "small")
+@pytest.mark.parametrize("hub_steps", [384, 6])
+def test_batched_matches_oracle(hub_steps):
+    bp = gen.circuit_batch(40, 2000, 2, 200)
     an = an_mod.analyze(bp.A0, SolverConfig(ordering="amd"))
     on = _oracle()
     prior = api.factorize_analysis(an)
     oprior = on.factorize(an)
-    X, npert = api.refactorize_solve_batched(bp.values, prior, bp.rhs)
+    X, npert = api.refactorize_solve_batched(bp.values, prior, bp.rhs, hub_steps=hub_steps)
     Xo, npo = on.refactor_solve_batch(an, oprior, bp.values, bp.rhs)
     assert _rel(X, Xo) <= 1e-9
     assert np.array_equal(npert, npo)
@@ -78,3 +79,20 @@ def test_batched_matches_oracle():
         A = bp.A0.with_values(bp.values[b])
         res = np.linalg.norm(refmatrix.spmv(A, X[b]) - bp.rhs[b]) / np.linalg.norm(bp.rhs[b])
         assert res <= RES_TOL
+
+
+def test_batched_factor_values_match_oracle():
+    bp = gen.circuit_batch(33, 2000, 2, 200)   # a partial last group
+    an = an_mod.analyze(bp.A0, SolverConfig(ordering="amd"))
+    on = _oracle()
+    prior = api.factorize_analysis(an)
+    oprior = on.factorize(an)
+    br = api.BatchedRefactorizer(prior, hub_steps=20)
+    import torch
+    dv = torch.from_numpy(bp.values).cuda()
+    dr = torch.from_numpy(bp.rhs).cuda()
+    br.run(dv, dr)
+    for b in (0, 17, 32):
+        ref = on.factorize(an, bp.values[b], prior=oprior)
+        got = br.factor_values(b).cpu().numpy()
+        assert _rel(got, ref.values) <= LU_RTOL
