@@ -117,7 +117,7 @@ int hy_solve(hy_handle *h, const hy_factors *f, const double *d_b, double *d_x,
  * prior inner_perm).  Must be uploaded before the
  * batched calls, and must match the inner_perm of the prior they are used with. */
 typedef struct {
-  int64_t nsteps, nrel, nhubrows, nlev, nhpos, npred;
+  int64_t nsteps, nrel, nhubrows, nlev, nhpos, npred, nwi, nsp, max_slots;
   const int64_t *row_ptr;   /* [n+1] */
   const int32_t *st_p;      /* [nsteps] */
   const int32_t *st_j;
@@ -133,6 +133,16 @@ typedef struct {
   const int64_t *hpp;       /* [nhpos+1] */
   const int32_t *pred_p;    /* [npred] */
   const int64_t *pred_u;    /* [npred] */
+  const int64_t *lev_wi;    /* [nlev+1] gather work items per intra-row level */
+  const int32_t *wi_x;      /* [nwi] */
+  const int64_t *wi_y0;
+  const int64_t *wi_y1;
+  const int32_t *wi_slot;
+  const int64_t *lev_sp;    /* [nlev+1] split positions per intra-row level */
+  const int32_t *sp_x;      /* [nsp] */
+  const int32_t *sp_s0;
+  const int32_t *sp_n;
+  const int32_t *level_ws;  /* [nlevels] widest non-hub node per factorization level */
 } hy_row_programs;
 int hy_upload_row_programs(hy_handle *h, const hy_row_programs *progs);
 

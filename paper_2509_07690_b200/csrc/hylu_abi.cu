@@ -19,8 +19,10 @@ __global__ void k_bhat(DevSym, const int32_t *, const double *, double *);
 __global__ void k_xout(DevSym, const double *, double *);
 __global__ void k_fwd(DevSym, const double *, const int32_t *, int, double *);
 __global__ void k_bwd(DevSym, const double *, const int32_t *, int, double *);
-__global__ void k_bt_rows(DevSym, BatchP, DevProg, const int32_t *, int, int, const double *, double *);
-__global__ void k_bt_hub(DevSym, BatchP, DevProg, const int32_t *, int, int, const double *, double *);
+__global__ void k_bt_pipe(DevSym, BatchP, DevProg, const int32_t *, int, int, const double *, double *, int *,
+                          int *, int, const int32_t *, int);
+__global__ void k_bt_hub(DevSym, BatchP, DevProg, const int32_t *, int, int, const double *, double *,
+                         double *, int);
 __global__ void k_batch_bhat(DevSym, const int32_t *, const double *, double *, int64_t);
 __global__ void k_batch_xout(DevSym, const double *, double *, int64_t);
 __global__ void k_batch_fwd(DevSym, const double *, int64_t, const int32_t *, int, int, double *);
@@ -74,6 +76,17 @@ struct hy_handle {
   bool prog_ok = false;
   std::vector<void *> prog_allocs;
   std::vector<int64_t> bl_rptr, bl_hptr;   // per level: non-hub / hub node offsets
+  std::vector<int32_t> level_ws;           // per level: widest non-hub node
+  int max_slots = 0;
+  int *d_flags = nullptr;                  // [nn * G] completion epochs
+  int64_t flags_cap = 0;
+  int *d_counters = nullptr;               // one claim counter (int64) per launch of a call
+  int counters_cap = 0;
+  int epoch = 0;
+  int32_t *d_node_level = nullptr;
+  int pipe_blocks = 0;
+  double *d_scratch = nullptr;             // hub partial sums
+  int64_t scratch_cap = 0;
   int32_t *d_bl_rows = nullptr, *d_bl_hubs = nullptr;
   int64_t launches = 0;
   size_t sn_smem = 0;
@@ -160,6 +173,9 @@ void hy_destroy(hy_handle *h) {
   for (void *p : h->allocs) cudaFree(p);
   for (void *p : h->prog_allocs) cudaFree(p);
   if (h->d_bf) cudaFree(h->d_bf);
+  if (h->d_scratch) cudaFree(h->d_scratch);
+  if (h->d_flags) cudaFree(h->d_flags);
+  if (h->d_counters) cudaFree(h->d_counters);
   if (h->d_by) cudaFree(h->d_by);
   delete h;
 }
@@ -223,6 +239,12 @@ int hy_upload_symbolic(hy_handle *h, const hy_symbolic_desc *d) {
   if (rc) return rc;
   rc = build_plan(h, h->bplan, d->ulevel_ptr, d->ulevel_nodes, d->nulevels, d->node_kind);
   if (rc) return rc;
+  {
+    std::vector<int32_t> lev(nn, 0);
+    for (int64_t l = 0; l < d->nlevels; ++l)
+      for (int64_t k = d->level_ptr[l]; k < d->level_ptr[l + 1]; ++k) lev[d->level_nodes[k]] = (int32_t)l;
+    UP(&h->d_node_level, lev.data(), nn);
+  }
   h->uploaded = true;
   return HY_OK;
 }
@@ -350,6 +372,17 @@ int hy_upload_row_programs(hy_handle *h, const hy_row_programs *d) {
   UPP(&p64, d->hpp, d->nhpos + 1); R.hpp = p64;
   UPP(&p32, d->pred_p, d->npred); R.pred_p = p32;
   UPP(&p64, d->pred_u, d->npred); R.pred_u = p64;
+  UPP(&p64, d->lev_wi, d->nlev + 1); R.lev_wi = p64;
+  UPP(&p32, d->wi_x, d->nwi); R.wi_x = p32;
+  UPP(&p64, d->wi_y0, d->nwi); R.wi_y0 = p64;
+  UPP(&p64, d->wi_y1, d->nwi); R.wi_y1 = p64;
+  UPP(&p32, d->wi_slot, d->nwi); R.wi_slot = p32;
+  UPP(&p64, d->lev_sp, d->nlev + 1); R.lev_sp = p64;
+  UPP(&p32, d->sp_x, d->nsp); R.sp_x = p32;
+  UPP(&p32, d->sp_s0, d->nsp); R.sp_s0 = p32;
+  UPP(&p32, d->sp_n, d->nsp); R.sp_n = p32;
+  h->max_slots = (int)d->max_slots;
+  h->level_ws.assign(d->level_ws, d->level_ws + h->fplan.nlev);
   // per level split: non-hub nodes / hub nodes
   const Plan &pl = h->fplan;
   std::vector<int32_t> all(pl.aptr[pl.nlev]);
@@ -407,20 +440,65 @@ int hy_refactorize_batched(hy_handle *h, int64_t B, const double *d_vals, double
   const int G = (int)((B + 31) / 32);
   BatchP P{h->d_bf, d_vals, prior->d_inner_perm, prior->d_anorm, eps, d_npert, B, h->stored};
   h->last_fused = d_b_fuse != nullptr;
-  for (int l = 0; l < h->fplan.nlev; ++l) {
-    const int nr = (int)(h->bl_rptr[l + 1] - h->bl_rptr[l]);
-    const int nh = (int)(h->bl_hptr[l + 1] - h->bl_hptr[l]);
+  const int64_t nflags = (int64_t)h->S.nn * G;
+  if (nflags > h->flags_cap) {
+    if (h->d_flags) CK(cudaFree(h->d_flags));
+    h->d_flags = nullptr;
+    CK(cudaMalloc((void **)&h->d_flags, sizeof(int) * nflags));
+    CK(cudaMemset(h->d_flags, 0, sizeof(int) * nflags));
+    h->flags_cap = nflags;
+    h->epoch = 0;
+  }
+  const int nl = h->fplan.nlev;
+  if (h->counters_cap < nl + 1) {
+    if (h->d_counters) CK(cudaFree(h->d_counters));
+    CK(cudaMalloc((void **)&h->d_counters, sizeof(long long) * (nl + 1)));
+    h->counters_cap = nl + 1;
+  }
+  CK(cudaMemsetAsync(h->d_counters, 0, sizeof(long long) * (nl + 1), st));
+  h->epoch++;
+  if (h->pipe_blocks == 0) {
+    int per_sm = 0, sms = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bt_pipe, 128, 0));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
+    h->pipe_blocks = per_sm * sms;
+  }
+  // segments: maximal level runs without hub nodes -> one persistent launch each;
+  // hub levels -> one CTA per (hub node, group)
+  int l = 0;
+  while (l < nl) {
+    if (h->bl_hptr[l + 1] > h->bl_hptr[l]) {
+      const int nh = (int)(h->bl_hptr[l + 1] - h->bl_hptr[l]);
+      const int64_t need = (int64_t)nh * G * (h->max_slots > 0 ? h->max_slots : 1) * 32;
+      if (need > h->scratch_cap) {
+        if (h->d_scratch) CK(cudaFree(h->d_scratch));
+        h->d_scratch = nullptr;
+        CK(cudaMalloc((void **)&h->d_scratch, sizeof(double) * need));
+        h->scratch_cap = need;
+      }
+      k_bt_hub<<<(unsigned)(nh * G), 512, 0, st>>>(h->S, P, h->prog, h->d_bl_hubs + h->bl_hptr[l], nh, G,
+                                                  d_b_fuse, h->d_by, h->d_scratch, h->max_slots);
+      h->launches++;
+      const int nr = (int)(h->bl_rptr[l + 1] - h->bl_rptr[l]);
+      if (nr) {
+        k_bt_pipe<<<h->pipe_blocks, 128, 0, st>>>(h->S, P, h->prog, h->d_bl_rows + h->bl_rptr[l], nr, G,
+                                                   d_b_fuse, h->d_by, (int *)((long long *)h->d_counters + l),
+                                                   h->d_flags, h->epoch, h->d_node_level, l);
+        h->launches++;
+      }
+      ++l;
+      continue;
+    }
+    int l1 = l;
+    while (l1 < nl && h->bl_hptr[l1 + 1] == h->bl_hptr[l1]) ++l1;
+    const int nr = (int)(h->bl_rptr[l1] - h->bl_rptr[l]);
     if (nr) {
-      const int64_t tasks = (int64_t)nr * G;
-      k_bt_rows<<<(unsigned)((tasks + 3) / 4), 128, 0, st>>>(h->S, P, h->prog, h->d_bl_rows + h->bl_rptr[l],
-                                                             nr, G, d_b_fuse, h->d_by);
+      k_bt_pipe<<<h->pipe_blocks, 128, 0, st>>>(h->S, P, h->prog, h->d_bl_rows + h->bl_rptr[l], nr, G,
+                                                 d_b_fuse, h->d_by, (int *)((long long *)h->d_counters + l),
+                                                 h->d_flags, h->epoch, h->d_node_level, l);
       h->launches++;
     }
-    if (nh) {
-      k_bt_hub<<<(unsigned)(nh * G), 256, 0, st>>>(h->S, P, h->prog, h->d_bl_hubs + h->bl_hptr[l], nh, G,
-                                                  d_b_fuse, h->d_by);
-      h->launches++;
-    }
+    l = l1;
   }
   CK(cudaGetLastError());
   return HY_OK;

@@ -15,23 +15,79 @@
 
 namespace hy {
 
-constexpr int BW = 4;          // warps per block (row kernel)
-constexpr int WS = 32;         // rows with W <= WS keep their accumulator in shared memory
-constexpr int HUB_THREADS = 256;
+constexpr int BW = 4;            // warps per block (bwd / fwd kernels)
+constexpr int HUB_THREADS = 512;
+
+// Apply the row-program steps [s0, s1) to the accumulator w (lane-offset pointer,
+// stride 32), software-pipelined: the next step's scalars, its U(j,j) and y_j are
+// loaded while the current step runs.  Returns the fused forward-substitution
+// accumulator.  Target positions inside one step are distinct (a source row's
+// columns are distinct), so each group of 8 updates loads all targets first.
+template <typename WPtr>
+__device__ __forceinline__ double run_steps(const DevProg &R, int64_t s0, int64_t s1, WPtr w,
+                                            const double *gb, const double *yb, double yacc) {
+  if (s0 >= s1) return yacc;
+  int p = R.st_p[s0];
+  int64_t src = R.st_src[s0];
+  int cnt = R.st_cnt[s0];
+  int64_t ro = R.st_rel[s0];
+  double d = gb[src * 32];
+  double yj = yb[(int64_t)R.st_j[s0] * 32];
+  for (int64_t st = s0; st < s1; ++st) {
+    int pn = 0, cn = 0;
+    int64_t sn = 0, rn = 0;
+    double dn = 1.0, yn = 0.0;
+    if (st + 1 < s1) {
+      pn = R.st_p[st + 1];
+      sn = R.st_src[st + 1];
+      cn = R.st_cnt[st + 1];
+      rn = R.st_rel[st + 1];
+      dn = gb[sn * 32];
+      yn = yb[(int64_t)R.st_j[st + 1] * 32];
+    }
+    const int32_t *rl = R.rel + ro;
+    const double *us = gb + (src + 1) * 32;
+    const double l = w[p * 32] / d;
+    w[p * 32] = l;
+    yacc -= l * yj;
+    int q = 0;
+    for (; q + 8 <= cnt; q += 8) {
+      int t[8];
+      double u[8], a[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        t[k] = rl[q + k];
+        u[k] = us[(q + k) * 32];
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) a[k] = w[t[k] * 32];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) w[t[k] * 32] = a[k] - l * u[k];
+    }
+    for (; q < cnt; ++q) {
+      const int tq = rl[q];
+      w[tq * 32] -= l * us[q * 32];
+    }
+    p = pn; src = sn; cnt = cn; ro = rn; d = dn; yj = yn;
+  }
+  return yacc;
+}
 
 // ---------------------------------------------------------------------------
-// Row kernel: one warp per (non-hub node, group of 32 instances), lane = instance.
-// Executes the node's row programs (structural steps only, precomputed target
-// positions), fuses the forward substitution y_i = b̂_i − Σ_s l_s y_{j_s}.
-__global__ void __launch_bounds__(BW * 32) k_bt_rows(DevSym S, BatchP P, DevProg R,
-                                                     const int32_t *nodes, int count, int G,
-                                                     const double *rhs, double *Y) {
-  __shared__ double wsm[BW][WS * 32];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t task = (int64_t)blockIdx.x * BW + warp;
-  if (task >= (int64_t)count * G) return;
-  const int u = nodes[task / G];
-  const int g = (int)(task % G);
+// Dependency flags: flag[node * G + g] == epoch once (node, group) is complete.
+__device__ __forceinline__ int ld_acquire(const int *p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int *p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// One (node, group) task: up-looking rows in order, lane = instance.
+__device__ __forceinline__ void bt_node(const DevSym &S, const BatchP &P, const DevProg &R, int u,
+                                        int g, const double *rhs, double *Y, double *wsm0, int ws,
+                                        int lane) {
   const int64_t b = (int64_t)g * 32 + lane;
   const bool live = b < P.B;
   const int nlive = (int)(P.B - (int64_t)g * 32 < 32 ? P.B - (int64_t)g * 32 : 32);
@@ -44,69 +100,107 @@ __global__ void __launch_bounds__(BW * 32) k_bt_rows(DevSym S, BatchP P, DevProg
   const double *gb = gb0 + lane;
   double *yb = Y + (int64_t)g * S.n * 32 + lane;
   const double *Ab = P.A + (int64_t)g * 32 * S.nnz;
-  const bool inSm = W <= WS;
+  const bool kindsn = S.kind[u] != 0;
+  const int64_t vbase = S.valoff[u];
   for (int t = 0; t < s; ++t) {
     const int i = r + t;
-    double *w0 = inSm ? wsm[warp] : gb0 + (S.valoff[u] + (int64_t)t * W) * 32;
-    double *w = w0 + lane;
-    for (int q = 0; q < W; ++q) w[q * 32] = 0.0;
-    const int srow = S.kind[u] ? r + P.iperm[i] : r;
+    const int64_t s0 = R.row_ptr[i], s1 = R.row_ptr[i + 1];
+    const bool inSm = (s1 > s0) && W <= ws;
+    double *grow = gb0 + (vbase + (int64_t)t * W) * 32;
+    double *w0 = inSm ? wsm0 : grow;
+    const int srow = kindsn ? r + P.iperm[i] : r;
     const int64_t a = S.mrow_src[srow];
     const int64_t e0 = S.a_ptr[a];
     const int k = (int)(S.a_ptr[a + 1] - e0);
-    __syncwarp();
-    for (int idx = lane; idx < nlive * k; idx += 32) {
-      const int inst = idx / k, e = idx - inst * k;
-      w0[S.colpos[e0 + e] * 32 + inst] = Ab[(int64_t)inst * S.nnz + e0 + e] * S.scale[e0 + e];
-    }
     double yacc = (live && rhs) ? S.dr[a] * rhs[b * S.n + a] : 0.0;
+    for (int q = 0; q < W; ++q) w0[q * 32 + lane] = 0.0;
     __syncwarp();
-    const int64_t s0 = R.row_ptr[i], s1 = R.row_ptr[i + 1];
-    for (int64_t st = s0; st < s1; ++st) {
-      const int p = R.st_p[st];
-      const int64_t src = R.st_src[st];
-      const int cnt = R.st_cnt[st];
-      const int32_t *rl = R.rel + R.st_rel[st];
-      const double d = gb[src * 32];
-      const double yj = yb[(int64_t)R.st_j[st] * 32];
-      const double l = w[p * 32] / d;
-      w[p * 32] = l;
-      yacc -= l * yj;
-      const double *us = gb + (src + 1) * 32;
-      int q = 0;
-      for (; q + 4 <= cnt; q += 4) {
-        const int t0 = rl[q], t1 = rl[q + 1], t2 = rl[q + 2], t3 = rl[q + 3];
-        const double u0 = us[(q + 0) * 32], u1 = us[(q + 1) * 32];
-        const double u2 = us[(q + 2) * 32], u3 = us[(q + 3) * 32];
-        w[t0 * 32] -= l * u0;
-        w[t1 * 32] -= l * u1;
-        w[t2 * 32] -= l * u2;
-        w[t3 * 32] -= l * u3;
-      }
-      for (; q < cnt; ++q) w[rl[q] * 32] -= l * us[q * 32];
+    for (int e = 0; e < k; ++e) {
+      const int pos = S.colpos[e0 + e];
+      const double sc = S.scale[e0 + e];
+      if (lane < nlive) w0[pos * 32 + lane] = Ab[(int64_t)lane * S.nnz + e0 + e] * sc;
     }
+    __syncwarp();
+    if (inSm)
+      yacc = run_steps(R, s0, s1, wsm0 + lane, gb, yb, yacc);
+    else
+      yacc = run_steps(R, s0, s1, grow + lane, gb, yb, yacc);
     const int Lt = L + t;
-    const double piv = w[Lt * 32];
+    const double piv = w0[Lt * 32 + lane];
     bool fired;
-    w[Lt * 32] = perturb(piv, thr, fired);
+    w0[Lt * 32 + lane] = perturb(piv, thr, fired);
     if (fired && live) atomicAdd(&P.npert[b], 1);
     yb[(int64_t)i * 32] = yacc;
-    if (inSm) {
-      double *dst = gb0 + (S.valoff[u] + (int64_t)t * W) * 32 + lane;
-      for (int q = 0; q < W; ++q) dst[q * 32] = w[q * 32];
-    }
+    if (inSm)
+      for (int q = 0; q < W; ++q) grow[q * 32 + lane] = w0[q * 32 + lane];
     __syncwarp();
   }
 }
 
+constexpr int PIPE_WARPS = 4;
+constexpr int PIPE_WS = 32;
+
+// Persistent, dependency-driven row kernel for a segment of levels without hub
+// nodes (the device form of SPEC's pipeline mode): warps claim
+// (node, group) tasks in level-major order from an atomic counter, wait on the
+// completion flags of the node's in-segment dependencies, run the task, then
+// publish its flag.  Claim order is topological and every claimed task is held by
+// a resident warp, so the earliest unfinished claimed task can always proceed.
+__global__ void __launch_bounds__(PIPE_WARPS * 32, 6)
+    k_bt_pipe(DevSym S, BatchP P, DevProg R, const int32_t *nodes, int count, int G,
+              const double *rhs, double *Y, int *counter, int *flags, int epoch,
+              const int32_t *node_level, int lev0) {
+  __shared__ __align__(16) double wsm[PIPE_WARPS][PIPE_WS * 32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t total = (int64_t)count * G;
+  for (;;) {
+    long long t = 0;
+    if (lane == 0) t = (long long)atomicAdd(reinterpret_cast<unsigned long long *>(counter), 1ull);
+    t = __shfl_sync(HY_FULL, t, 0);
+    if (t >= total) return;
+    const int u = nodes[t / G];
+    const int g = (int)(t % G);
+    for (int64_t k = S.dptr[u] + lane; k < S.dptr[u + 1]; k += 32) {
+      const int v = S.deps[k];
+      if (node_level[v] >= lev0) {
+        const int *f = flags + (int64_t)v * G + g;
+        while (ld_acquire(f) != epoch) __nanosleep(100);
+      }
+    }
+    __syncwarp();
+    __threadfence();
+    bt_node(S, P, R, u, g, rhs, Y, wsm[warp], PIPE_WS, lane);
+    __syncwarp();
+    __threadfence();
+    if (lane == 0) st_release(flags + (int64_t)u * G + g, epoch);
+  }
+}
+
 // ---------------------------------------------------------------------------
-// Hub kernel: one CTA per (hub node, group).  Pull programs: positions of a row are
-// processed level by level (intra-row dependency levels); each position gathers
-// its contributions in ascending step order.  Forward substitution fused with a
-// fixed-order cross-warp reduction.
+// Hub kernel: one CTA per (hub node, group).  Pull programs: the positions of a row
+// are processed level by level (intra-row dependency levels); a position gathers
+// its contributions (ascending step order) in work items of <= 64 terms; positions
+// with more terms are split and their partial sums combined in slot order, so the
+// result is deterministic.  Forward substitution is fused (fixed-order reduction).
+__device__ __forceinline__ void hub_finalize(const DevProg &R, const BatchP &P, int64_t x, int p,
+                                             double acc, double *w, const double *gb, double thr,
+                                             bool live, int64_t b) {
+  const int64_t kd = R.hdiv[x];
+  if (kd >= 0) {
+    acc = acc / gb[kd * 32];
+  } else if (kd == -2) {
+    bool fired;
+    const double piv = acc;
+    acc = perturb(piv, thr, fired);
+    if (fired && live) atomicAdd(&P.npert[b], 1);
+  }
+  w[p * 32] = acc;
+}
+
 __global__ void __launch_bounds__(HUB_THREADS) k_bt_hub(DevSym S, BatchP P, DevProg R,
                                                         const int32_t *nodes, int count, int G,
-                                                        const double *rhs, double *Y) {
+                                                        const double *rhs, double *Y,
+                                                        double *scratch, int max_slots) {
   __shared__ double red[HUB_THREADS / 32][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = HUB_THREADS / 32;
   const int task = blockIdx.x;
@@ -123,6 +217,7 @@ __global__ void __launch_bounds__(HUB_THREADS) k_bt_hub(DevSym S, BatchP P, DevP
   const double *gb = gb0 + lane;
   double *yb = Y + (int64_t)g * S.n * 32 + lane;
   const double *Ab = P.A + (int64_t)g * 32 * S.nnz;
+  double *scr = scratch + (size_t)blockIdx.x * max_slots * 32 + lane;
   const int hr0 = R.hub_base[u];
   for (int t = 0; t < s; ++t) {
     const int i = r + t;
@@ -141,32 +236,46 @@ __global__ void __launch_bounds__(HUB_THREADS) k_bt_hub(DevSym S, BatchP P, DevP
     __syncthreads();
     const int hr = hr0 + t;
     for (int64_t lev = R.hrow_lev[hr]; lev < R.hrow_lev[hr + 1]; ++lev) {
-      for (int64_t x = R.lev_ptr[lev] + warp; x < R.lev_ptr[lev + 1]; x += nw) {
+      for (int64_t it = R.lev_wi[lev] + warp; it < R.lev_wi[lev + 1]; it += nw) {
+        const int64_t x = R.wi_x[it];
         const int p = R.hpos[x];
-        double acc = w[p * 32];
-        const int64_t y0 = R.hpp[x], y1 = R.hpp[x + 1];
-        int64_t y = y0;
-        for (; y + 4 <= y1; y += 4) {
-          const double l0 = w[R.pred_p[y] * 32], l1 = w[R.pred_p[y + 1] * 32];
-          const double l2 = w[R.pred_p[y + 2] * 32], l3 = w[R.pred_p[y + 3] * 32];
-          const double v0 = gb[R.pred_u[y] * 32], v1 = gb[R.pred_u[y + 1] * 32];
-          const double v2 = gb[R.pred_u[y + 2] * 32], v3 = gb[R.pred_u[y + 3] * 32];
-          acc -= l0 * v0;
-          acc -= l1 * v1;
-          acc -= l2 * v2;
-          acc -= l3 * v3;
+        const int slot = R.wi_slot[it];
+        const int64_t y1 = R.wi_y1[it];
+        int64_t y = R.wi_y0[it];
+        double acc = slot < 0 ? w[p * 32] : 0.0;
+        for (; y + 8 <= y1; y += 8) {
+          int pp[8];
+          int64_t pu[8];
+          double lv[8], uv[8];
+#pragma unroll
+          for (int k2 = 0; k2 < 8; ++k2) {
+            pp[k2] = R.pred_p[y + k2];
+            pu[k2] = R.pred_u[y + k2];
+          }
+#pragma unroll
+          for (int k2 = 0; k2 < 8; ++k2) {
+            lv[k2] = w[pp[k2] * 32];
+            uv[k2] = gb[pu[k2] * 32];
+          }
+#pragma unroll
+          for (int k2 = 0; k2 < 8; ++k2) acc -= lv[k2] * uv[k2];
         }
         for (; y < y1; ++y) acc -= w[R.pred_p[y] * 32] * gb[R.pred_u[y] * 32];
-        const int64_t kd = R.hdiv[x];
-        if (kd >= 0) {
-          acc = acc / gb[kd * 32];
-        } else if (kd == -2) {
-          bool fired;
-          const double piv = acc;
-          acc = perturb(piv, thr, fired);
-          if (fired && live) atomicAdd(&P.npert[b], 1);
+        if (slot < 0)
+          hub_finalize(R, P, x, p, acc, w, gb, thr, live, b);
+        else
+          scr[(size_t)slot * 32] = acc;
+      }
+      if (R.lev_sp[lev + 1] > R.lev_sp[lev]) {
+        __syncthreads();
+        for (int64_t k2 = R.lev_sp[lev] + warp; k2 < R.lev_sp[lev + 1]; k2 += nw) {
+          const int64_t x = R.sp_x[k2];
+          const int p = R.hpos[x];
+          double acc = w[p * 32];
+          const int s0 = R.sp_s0[k2], ns = R.sp_n[k2];
+          for (int c = 0; c < ns; ++c) acc += scr[(size_t)(s0 + c) * 32];
+          hub_finalize(R, P, x, p, acc, w, gb, thr, live, b);
         }
-        w[p * 32] = acc;
       }
       __syncthreads();
     }

@@ -72,6 +72,15 @@ struct DevProg {
   const int64_t *hpp;
   const int32_t *pred_p;
   const int64_t *pred_u;
+  const int64_t *lev_wi;    // work items per intra-row level
+  const int32_t *wi_x;
+  const int64_t *wi_y0;
+  const int64_t *wi_y1;
+  const int32_t *wi_slot;
+  const int64_t *lev_sp;    // split positions per intra-row level
+  const int32_t *sp_x;
+  const int32_t *sp_s0;
+  const int32_t *sp_n;
 };
 
 __device__ __forceinline__ int lower_bound_i32(const int32_t *c, int lo, int hi, int key) {

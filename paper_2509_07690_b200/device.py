@@ -57,11 +57,16 @@ class ProgramsDesc(ctypes.Structure):
     _fields_ = [
         ("nsteps", ctypes.c_int64), ("nrel", ctypes.c_int64), ("nhubrows", ctypes.c_int64),
         ("nlev", ctypes.c_int64), ("nhpos", ctypes.c_int64), ("npred", ctypes.c_int64),
+        ("nwi", ctypes.c_int64), ("nsp", ctypes.c_int64), ("max_slots", ctypes.c_int64),
         ("row_ptr", ctypes.c_void_p), ("st_p", ctypes.c_void_p), ("st_j", ctypes.c_void_p),
         ("st_src", ctypes.c_void_p), ("st_cnt", ctypes.c_void_p), ("st_rel", ctypes.c_void_p),
         ("rel", ctypes.c_void_p), ("node_hub", ctypes.c_void_p), ("hrow_lev", ctypes.c_void_p),
         ("lev_ptr", ctypes.c_void_p), ("hpos", ctypes.c_void_p), ("hdiv", ctypes.c_void_p),
         ("hpp", ctypes.c_void_p), ("pred_p", ctypes.c_void_p), ("pred_u", ctypes.c_void_p),
+        ("lev_wi", ctypes.c_void_p), ("wi_x", ctypes.c_void_p), ("wi_y0", ctypes.c_void_p),
+        ("wi_y1", ctypes.c_void_p), ("wi_slot", ctypes.c_void_p), ("lev_sp", ctypes.c_void_p),
+        ("sp_x", ctypes.c_void_p), ("sp_s0", ctypes.c_void_p), ("sp_n", ctypes.c_void_p),
+        ("level_ws", ctypes.c_void_p),
     ]
 
 
@@ -198,12 +203,14 @@ class DeviceContext:
         """Upload schedule.RowPrograms (built for a prior inner_perm)."""
         arrs = {k: np.ascontiguousarray(getattr(progs, k)) for k in (
             "row_ptr", "st_p", "st_j", "st_src", "st_cnt", "st_rel", "rel", "node_hub", "hrow_lev",
-            "lev_ptr", "hpos", "hdiv", "hpp", "pred_p", "pred_u")}
+            "lev_ptr", "hpos", "hdiv", "hpp", "pred_p", "pred_u", "lev_wi", "wi_x", "wi_y0", "wi_y1",
+            "wi_slot", "lev_sp", "sp_x", "sp_s0", "sp_n", "level_ws")}
         d = ProgramsDesc()
         d.nsteps, d.nrel = len(progs.st_p), len(progs.rel)
         d.nhubrows = len(progs.hrow_lev) - 1
         d.nlev = len(progs.lev_ptr) - 1
         d.nhpos, d.npred = len(progs.hpos), len(progs.pred_p)
+        d.nwi, d.nsp, d.max_slots = len(progs.wi_x), len(progs.sp_x), progs.max_slots
         for k, v in arrs.items():
             setattr(d, k, v.ctypes.data if v.size else None)
         with self.torch.cuda.device(self.device):

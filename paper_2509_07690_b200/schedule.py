@@ -218,6 +218,72 @@ def _pull(n, first, colptr, nl, valoff, a_ptr, mrow_src, colpos, kind, iperm, hu
     return hrow_lev, lev_ptr, hpos, hdiv, hpp, pred_p, pred_u
 
 
+@njit(cache=True)
+def _chunks(hrow_lev, lev_ptr, hpp, ch):
+    """Per intra-row level, split the gather work into items of <= ch contributions.
+
+    Work item: (position x, pred range [y0, y1), slot); slot = -1 → the item holds the
+    whole position (finalize directly); slot >= 0 → partial sum into scratch slot.
+    Split positions: (x, first slot, slot count), combined in slot order."""
+    nlev = len(lev_ptr) - 1
+    wi_x_l = []
+    wi_y0_l = []
+    wi_y1_l = []
+    wi_slot_l = []
+    sp_x_l = []
+    sp_s0_l = []
+    sp_n_l = []
+    lev_wi = np.zeros(nlev + 1, np.int64)
+    lev_sp = np.zeros(nlev + 1, np.int64)
+    max_slots = 0
+    for lev in range(nlev):
+        slot = 0
+        for x in range(lev_ptr[lev], lev_ptr[lev + 1]):
+            y0 = hpp[x]
+            y1 = hpp[x + 1]
+            if y1 - y0 <= ch:
+                wi_x_l.append(np.int32(x))
+                wi_y0_l.append(y0)
+                wi_y1_l.append(y1)
+                wi_slot_l.append(np.int32(-1))
+            else:
+                nsl = 0
+                y = y0
+                while y < y1:
+                    wi_x_l.append(np.int32(x))
+                    wi_y0_l.append(y)
+                    wi_y1_l.append(min(y + ch, y1))
+                    wi_slot_l.append(np.int32(slot + nsl))
+                    nsl += 1
+                    y += ch
+                sp_x_l.append(np.int32(x))
+                sp_s0_l.append(np.int32(slot))
+                sp_n_l.append(np.int32(nsl))
+                slot += nsl
+        max_slots = max(max_slots, slot)
+        lev_wi[lev + 1] = len(wi_x_l)
+        lev_sp[lev + 1] = len(sp_x_l)
+    nwi = len(wi_x_l)
+    wi_x = np.empty(nwi, np.int32)
+    wi_y0 = np.empty(nwi, np.int64)
+    wi_y1 = np.empty(nwi, np.int64)
+    wi_slot = np.empty(nwi, np.int32)
+    for k in range(nwi):
+        wi_x[k] = wi_x_l[k]
+        wi_y0[k] = wi_y0_l[k]
+        wi_y1[k] = wi_y1_l[k]
+        wi_slot[k] = wi_slot_l[k]
+    nsp = len(sp_x_l)
+    sp_x = np.empty(nsp, np.int32)
+    sp_s0 = np.empty(nsp, np.int32)
+    sp_n = np.empty(nsp, np.int32)
+    for k in range(nsp):
+        sp_x[k] = sp_x_l[k]
+        sp_s0[k] = sp_s0_l[k]
+        sp_n[k] = sp_n_l[k]
+    return lev_wi, wi_x, wi_y0, wi_y1, wi_slot, lev_sp, sp_x, sp_s0, sp_n, max_slots
+
+
 @dataclass
 class RowPrograms:
     row_ptr: np.ndarray     # int64[n+1] steps of factor row i
@@ -236,16 +302,31 @@ class RowPrograms:
     hpp: np.ndarray         # int64[len(hpos)+1] -> pred index
     pred_p: np.ndarray      # int32
     pred_u: np.ndarray      # int64
+    lev_wi: np.ndarray      # int64[nlev+1] work items per intra-row level
+    wi_x: np.ndarray        # int32 position index (into hpos)
+    wi_y0: np.ndarray       # int64
+    wi_y1: np.ndarray       # int64
+    wi_slot: np.ndarray     # int32 (-1 = whole position)
+    lev_sp: np.ndarray      # int64[nlev+1] split positions per level
+    sp_x: np.ndarray        # int32
+    sp_s0: np.ndarray       # int32
+    sp_n: np.ndarray        # int32
+    max_slots: int
+    level_ws: np.ndarray    # int32[nlevels] max width of non-hub nodes per factor level
 
     @property
     def nsteps(self):
         return len(self.st_p)
 
     def nbytes(self):
-        return sum(getattr(self, k).nbytes for k in self.__dataclass_fields__)
+        return sum(getattr(self, k).nbytes for k in self.__dataclass_fields__
+                   if isinstance(getattr(self, k), np.ndarray))
 
 
-def build_programs(an, inner_perm, hub_steps=HUB_STEPS):
+HUB_CHUNK = 64
+
+
+def build_programs(an, inner_perm, hub_steps=HUB_STEPS, chunk=HUB_CHUNK):
     s = an.symbolic
     vm = an.vmap
     ip = np.ascontiguousarray(inner_perm, np.int64)
@@ -265,5 +346,14 @@ def build_programs(an, inner_perm, hub_steps=HUB_STEPS):
         hpp = np.zeros(1, np.int64)
         pred_p = np.zeros(0, np.int32)
         pred_u = np.zeros(0, np.int64)
+    (lev_wi, wi_x, wi_y0, wi_y1, wi_slot, lev_sp, sp_x, sp_s0, sp_n,
+     max_slots) = _chunks(hrow_lev, lev_ptr, hpp, chunk)
+    W = np.diff(s.colptr)
+    level_ws = np.zeros(len(s.level_ptr) - 1, np.int32)
+    for lv in range(len(level_ws)):
+        nodes = s.level_nodes[s.level_ptr[lv]:s.level_ptr[lv + 1]]
+        nodes = nodes[node_hub[nodes] == 0]
+        level_ws[lv] = int(W[nodes].max()) if len(nodes) else 0
     return RowPrograms(row_ptr, st_p, st_j, st_src, st_cnt, st_rel, rel, node_hub, hub_nodes,
-                       hrow_lev, lev_ptr, hpos, hdiv, hpp, pred_p, pred_u)
+                       hrow_lev, lev_ptr, hpos, hdiv, hpp, pred_p, pred_u, lev_wi, wi_x, wi_y0,
+                       wi_y1, wi_slot, lev_sp, sp_x, sp_s0, sp_n, int(max_slots), level_ws)
