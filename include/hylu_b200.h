@@ -134,12 +134,14 @@ typedef struct {
   const int32_t *pred_p;    /* [npred] */
   const int64_t *pred_u;    /* [npred] */
   const int64_t *lev_wi;    /* [nlev+1] gather work items per intra-row level */
-  const int32_t *wi_x;      /* [nwi] */
+  const int32_t *wi_p;      /* [nwi] target position */
+  const int64_t *wi_kd;     /* [nwi] finalize kind: diag offset / -1 U / -2 pivot */
   const int64_t *wi_y0;
   const int64_t *wi_y1;
   const int32_t *wi_slot;
   const int64_t *lev_sp;    /* [nlev+1] split positions per intra-row level */
-  const int32_t *sp_x;      /* [nsp] */
+  const int32_t *sp_p;      /* [nsp] */
+  const int64_t *sp_kd;
   const int32_t *sp_s0;
   const int32_t *sp_n;
   const int32_t *level_ws;  /* [nlevels] widest non-hub node per factorization level */
@@ -164,6 +166,10 @@ int hy_refactorize_batched(hy_handle *h, int64_t B, const double *d_vals, double
 int hy_solve_batched(hy_handle *h, int64_t B, const double *d_b, double *d_x, uintptr_t stream);
 /* Copy instance b's factor values from the last batched call into node layout. */
 int hy_batched_factor_values(hy_handle *h, int64_t b, double *d_out, uintptr_t stream);
+
+/* Tuning knobs: "group_batch" (claim-order batch of 32-instance groups in the
+ * batched pipeline kernel, default 4). */
+int hy_set_option(hy_handle *h, const char *name, int64_t value);
 
 /* Number of kernel launches issued by this handle since creation (bench evidence). */
 int64_t hy_launch_count(const hy_handle *h);

@@ -20,7 +20,7 @@ __global__ void k_xout(DevSym, const double *, double *);
 __global__ void k_fwd(DevSym, const double *, const int32_t *, int, double *);
 __global__ void k_bwd(DevSym, const double *, const int32_t *, int, double *);
 __global__ void k_bt_pipe(DevSym, BatchP, DevProg, const int32_t *, int, int, const double *, double *, int *,
-                          int *, int, const int32_t *, int);
+                          int *, int, const int32_t *, int, int);
 __global__ void k_bt_hub(DevSym, BatchP, DevProg, const int32_t *, int, int, const double *, double *,
                          double *, int);
 __global__ void k_batch_bhat(DevSym, const int32_t *, const double *, double *, int64_t);
@@ -85,6 +85,7 @@ struct hy_handle {
   int epoch = 0;
   int32_t *d_node_level = nullptr;
   int pipe_blocks = 0;
+  int gbatch = 4;                          // claim-order group batch (L2 locality)
   double *d_scratch = nullptr;             // hub partial sums
   int64_t scratch_cap = 0;
   int32_t *d_bl_rows = nullptr, *d_bl_hubs = nullptr;
@@ -182,6 +183,15 @@ void hy_destroy(hy_handle *h) {
 
 int64_t hy_stored_values(const hy_handle *h) { return h ? h->stored : -1; }
 int64_t hy_launch_count(const hy_handle *h) { return h ? h->launches : -1; }
+
+int hy_set_option(hy_handle *h, const char *name, int64_t value) {
+  if (!h || !name) return fail(HY_INVALID_ARGUMENT, "null handle/name");
+  if (std::string(name) == "group_batch" && value >= 1) {
+    h->gbatch = (int)value;
+    return HY_OK;
+  }
+  return fail(HY_INVALID_ARGUMENT, std::string("unknown option ") + name);
+}
 
 int hy_upload_symbolic(hy_handle *h, const hy_symbolic_desc *d) {
   if (!h || !d) return fail(HY_INVALID_ARGUMENT, "null handle/descriptor");
@@ -373,12 +383,14 @@ int hy_upload_row_programs(hy_handle *h, const hy_row_programs *d) {
   UPP(&p32, d->pred_p, d->npred); R.pred_p = p32;
   UPP(&p64, d->pred_u, d->npred); R.pred_u = p64;
   UPP(&p64, d->lev_wi, d->nlev + 1); R.lev_wi = p64;
-  UPP(&p32, d->wi_x, d->nwi); R.wi_x = p32;
+  UPP(&p32, d->wi_p, d->nwi); R.wi_p = p32;
+  UPP(&p64, d->wi_kd, d->nwi); R.wi_kd = p64;
   UPP(&p64, d->wi_y0, d->nwi); R.wi_y0 = p64;
   UPP(&p64, d->wi_y1, d->nwi); R.wi_y1 = p64;
   UPP(&p32, d->wi_slot, d->nwi); R.wi_slot = p32;
   UPP(&p64, d->lev_sp, d->nlev + 1); R.lev_sp = p64;
-  UPP(&p32, d->sp_x, d->nsp); R.sp_x = p32;
+  UPP(&p32, d->sp_p, d->nsp); R.sp_p = p32;
+  UPP(&p64, d->sp_kd, d->nsp); R.sp_kd = p64;
   UPP(&p32, d->sp_s0, d->nsp); R.sp_s0 = p32;
   UPP(&p32, d->sp_n, d->nsp); R.sp_n = p32;
   h->max_slots = (int)d->max_slots;
@@ -476,14 +488,14 @@ int hy_refactorize_batched(hy_handle *h, int64_t B, const double *d_vals, double
         CK(cudaMalloc((void **)&h->d_scratch, sizeof(double) * need));
         h->scratch_cap = need;
       }
-      k_bt_hub<<<(unsigned)(nh * G), 512, 0, st>>>(h->S, P, h->prog, h->d_bl_hubs + h->bl_hptr[l], nh, G,
+      k_bt_hub<<<(unsigned)(nh * G), 1024, 0, st>>>(h->S, P, h->prog, h->d_bl_hubs + h->bl_hptr[l], nh, G,
                                                   d_b_fuse, h->d_by, h->d_scratch, h->max_slots);
       h->launches++;
       const int nr = (int)(h->bl_rptr[l + 1] - h->bl_rptr[l]);
       if (nr) {
         k_bt_pipe<<<h->pipe_blocks, 128, 0, st>>>(h->S, P, h->prog, h->d_bl_rows + h->bl_rptr[l], nr, G,
                                                    d_b_fuse, h->d_by, (int *)((long long *)h->d_counters + l),
-                                                   h->d_flags, h->epoch, h->d_node_level, l);
+                                                   h->d_flags, h->epoch, h->d_node_level, l, h->gbatch);
         h->launches++;
       }
       ++l;
@@ -495,7 +507,7 @@ int hy_refactorize_batched(hy_handle *h, int64_t B, const double *d_vals, double
     if (nr) {
       k_bt_pipe<<<h->pipe_blocks, 128, 0, st>>>(h->S, P, h->prog, h->d_bl_rows + h->bl_rptr[l], nr, G,
                                                  d_b_fuse, h->d_by, (int *)((long long *)h->d_counters + l),
-                                                 h->d_flags, h->epoch, h->d_node_level, l);
+                                                 h->d_flags, h->epoch, h->d_node_level, l, h->gbatch);
       h->launches++;
     }
     l = l1;

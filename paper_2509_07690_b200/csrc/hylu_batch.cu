@@ -16,7 +16,7 @@
 namespace hy {
 
 constexpr int BW = 4;            // warps per block (bwd / fwd kernels)
-constexpr int HUB_THREADS = 512;
+constexpr int HUB_THREADS = 1024;
 
 // Apply the row-program steps [s0, s1) to the accumulator w (lane-offset pointer,
 // stride 32), software-pipelined: the next step's scalars, its U(j,j) and y_j are
@@ -115,10 +115,11 @@ __device__ __forceinline__ void bt_node(const DevSym &S, const BatchP &P, const 
     double yacc = (live && rhs) ? S.dr[a] * rhs[b * S.n + a] : 0.0;
     for (int q = 0; q < W; ++q) w0[q * 32 + lane] = 0.0;
     __syncwarp();
-    for (int e = 0; e < k; ++e) {
-      const int pos = S.colpos[e0 + e];
-      const double sc = S.scale[e0 + e];
-      if (lane < nlive) w0[pos * 32 + lane] = Ab[(int64_t)lane * S.nnz + e0 + e] * sc;
+    // scatter: lanes over (instance, entry) pairs, instance-major, so a pass reads
+    // the k contiguous entries of consecutive instances (few sectors per instance)
+    for (int idx = lane; idx < nlive * k; idx += 32) {
+      const int inst = idx / k, e = idx - inst * k;
+      w0[S.colpos[e0 + e] * 32 + inst] = Ab[(int64_t)inst * S.nnz + e0 + e] * S.scale[e0 + e];
     }
     __syncwarp();
     if (inSm)
@@ -149,7 +150,7 @@ constexpr int PIPE_WS = 32;
 __global__ void __launch_bounds__(PIPE_WARPS * 32, 6)
     k_bt_pipe(DevSym S, BatchP P, DevProg R, const int32_t *nodes, int count, int G,
               const double *rhs, double *Y, int *counter, int *flags, int epoch,
-              const int32_t *node_level, int lev0) {
+              const int32_t *node_level, int lev0, int gbatch) {
   __shared__ __align__(16) double wsm[PIPE_WARPS][PIPE_WS * 32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t total = (int64_t)count * G;
@@ -158,20 +159,25 @@ __global__ void __launch_bounds__(PIPE_WARPS * 32, 6)
     if (lane == 0) t = (long long)atomicAdd(reinterpret_cast<unsigned long long *>(counter), 1ull);
     t = __shfl_sync(HY_FULL, t, 0);
     if (t >= total) return;
-    const int u = nodes[t / G];
-    const int g = (int)(t % G);
-    for (int64_t k = S.dptr[u] + lane; k < S.dptr[u + 1]; k += 32) {
+    // claim order: group batches of `gbatch` groups; inside a batch level-major
+    // (node index), groups fastest — keeps a batch's freshly written rows in L2
+    const int64_t per_batch = (int64_t)count * gbatch;
+    const int64_t bt = t / per_batch, rr = t - bt * per_batch;
+    const int gb_lo = (int)(bt * gbatch);
+    const int gcount = (G - gb_lo) < gbatch ? (G - gb_lo) : gbatch;
+    const int u = nodes[rr / gcount];
+    const int g = gb_lo + (int)(rr % gcount);
+    // every lane acquires every in-segment dependency flag (orders its own loads)
+    for (int64_t k = S.dptr[u]; k < S.dptr[u + 1]; ++k) {
       const int v = S.deps[k];
       if (node_level[v] >= lev0) {
         const int *f = flags + (int64_t)v * G + g;
-        while (ld_acquire(f) != epoch) __nanosleep(100);
+        while (ld_acquire(f) != epoch) __nanosleep(64);
       }
     }
-    __syncwarp();
-    __threadfence();
     bt_node(S, P, R, u, g, rhs, Y, wsm[warp], PIPE_WS, lane);
-    __syncwarp();
     __threadfence();
+    __syncwarp();
     if (lane == 0) st_release(flags + (int64_t)u * G + g, epoch);
   }
 }
@@ -182,10 +188,9 @@ __global__ void __launch_bounds__(PIPE_WARPS * 32, 6)
 // its contributions (ascending step order) in work items of <= 64 terms; positions
 // with more terms are split and their partial sums combined in slot order, so the
 // result is deterministic.  Forward substitution is fused (fixed-order reduction).
-__device__ __forceinline__ void hub_finalize(const DevProg &R, const BatchP &P, int64_t x, int p,
-                                             double acc, double *w, const double *gb, double thr,
-                                             bool live, int64_t b) {
-  const int64_t kd = R.hdiv[x];
+__device__ __forceinline__ void hub_finalize(const BatchP &P, int64_t kd, int p, double acc,
+                                             double *w, const double *gb, double thr, bool live,
+                                             int64_t b) {
   if (kd >= 0) {
     acc = acc / gb[kd * 32];
   } else if (kd == -2) {
@@ -237,8 +242,7 @@ __global__ void __launch_bounds__(HUB_THREADS) k_bt_hub(DevSym S, BatchP P, DevP
     const int hr = hr0 + t;
     for (int64_t lev = R.hrow_lev[hr]; lev < R.hrow_lev[hr + 1]; ++lev) {
       for (int64_t it = R.lev_wi[lev] + warp; it < R.lev_wi[lev + 1]; it += nw) {
-        const int64_t x = R.wi_x[it];
-        const int p = R.hpos[x];
+        const int p = R.wi_p[it];
         const int slot = R.wi_slot[it];
         const int64_t y1 = R.wi_y1[it];
         int64_t y = R.wi_y0[it];
@@ -262,19 +266,18 @@ __global__ void __launch_bounds__(HUB_THREADS) k_bt_hub(DevSym S, BatchP P, DevP
         }
         for (; y < y1; ++y) acc -= w[R.pred_p[y] * 32] * gb[R.pred_u[y] * 32];
         if (slot < 0)
-          hub_finalize(R, P, x, p, acc, w, gb, thr, live, b);
+          hub_finalize(P, R.wi_kd[it], p, acc, w, gb, thr, live, b);
         else
           scr[(size_t)slot * 32] = acc;
       }
       if (R.lev_sp[lev + 1] > R.lev_sp[lev]) {
         __syncthreads();
         for (int64_t k2 = R.lev_sp[lev] + warp; k2 < R.lev_sp[lev + 1]; k2 += nw) {
-          const int64_t x = R.sp_x[k2];
-          const int p = R.hpos[x];
+          const int p = R.sp_p[k2];
           double acc = w[p * 32];
           const int s0 = R.sp_s0[k2], ns = R.sp_n[k2];
           for (int c = 0; c < ns; ++c) acc += scr[(size_t)(s0 + c) * 32];
-          hub_finalize(R, P, x, p, acc, w, gb, thr, live, b);
+          hub_finalize(P, R.sp_kd[k2], p, acc, w, gb, thr, live, b);
         }
       }
       __syncthreads();

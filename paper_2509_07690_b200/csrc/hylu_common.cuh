@@ -73,12 +73,14 @@ struct DevProg {
   const int32_t *pred_p;
   const int64_t *pred_u;
   const int64_t *lev_wi;    // work items per intra-row level
-  const int32_t *wi_x;
+  const int32_t *wi_p;
+  const int64_t *wi_kd;
   const int64_t *wi_y0;
   const int64_t *wi_y1;
   const int32_t *wi_slot;
   const int64_t *lev_sp;    // split positions per intra-row level
-  const int32_t *sp_x;
+  const int32_t *sp_p;
+  const int64_t *sp_kd;
   const int32_t *sp_s0;
   const int32_t *sp_n;
 };

@@ -63,9 +63,10 @@ class ProgramsDesc(ctypes.Structure):
         ("rel", ctypes.c_void_p), ("node_hub", ctypes.c_void_p), ("hrow_lev", ctypes.c_void_p),
         ("lev_ptr", ctypes.c_void_p), ("hpos", ctypes.c_void_p), ("hdiv", ctypes.c_void_p),
         ("hpp", ctypes.c_void_p), ("pred_p", ctypes.c_void_p), ("pred_u", ctypes.c_void_p),
-        ("lev_wi", ctypes.c_void_p), ("wi_x", ctypes.c_void_p), ("wi_y0", ctypes.c_void_p),
-        ("wi_y1", ctypes.c_void_p), ("wi_slot", ctypes.c_void_p), ("lev_sp", ctypes.c_void_p),
-        ("sp_x", ctypes.c_void_p), ("sp_s0", ctypes.c_void_p), ("sp_n", ctypes.c_void_p),
+        ("lev_wi", ctypes.c_void_p), ("wi_p", ctypes.c_void_p), ("wi_kd", ctypes.c_void_p),
+        ("wi_y0", ctypes.c_void_p), ("wi_y1", ctypes.c_void_p), ("wi_slot", ctypes.c_void_p),
+        ("lev_sp", ctypes.c_void_p), ("sp_p", ctypes.c_void_p), ("sp_kd", ctypes.c_void_p),
+        ("sp_s0", ctypes.c_void_p), ("sp_n", ctypes.c_void_p),
         ("level_ws", ctypes.c_void_p),
     ]
 
@@ -100,6 +101,7 @@ def library():
     lib.hy_upload_row_programs.argtypes = [vp, ctypes.POINTER(ProgramsDesc)]
     lib.hy_solve_batched.argtypes = [vp, i64, vp, vp, u]
     lib.hy_batched_factor_values.argtypes = [vp, i64, vp, u]
+    lib.hy_set_option.argtypes = [vp, ctypes.c_char_p, i64]
     _lib = lib
     return lib
 
@@ -203,19 +205,22 @@ class DeviceContext:
         """Upload schedule.RowPrograms (built for a prior inner_perm)."""
         arrs = {k: np.ascontiguousarray(getattr(progs, k)) for k in (
             "row_ptr", "st_p", "st_j", "st_src", "st_cnt", "st_rel", "rel", "node_hub", "hrow_lev",
-            "lev_ptr", "hpos", "hdiv", "hpp", "pred_p", "pred_u", "lev_wi", "wi_x", "wi_y0", "wi_y1",
-            "wi_slot", "lev_sp", "sp_x", "sp_s0", "sp_n", "level_ws")}
+            "lev_ptr", "hpos", "hdiv", "hpp", "pred_p", "pred_u", "lev_wi", "wi_p", "wi_kd", "wi_y0",
+            "wi_y1", "wi_slot", "lev_sp", "sp_p", "sp_kd", "sp_s0", "sp_n", "level_ws")}
         d = ProgramsDesc()
         d.nsteps, d.nrel = len(progs.st_p), len(progs.rel)
         d.nhubrows = len(progs.hrow_lev) - 1
         d.nlev = len(progs.lev_ptr) - 1
         d.nhpos, d.npred = len(progs.hpos), len(progs.pred_p)
-        d.nwi, d.nsp, d.max_slots = len(progs.wi_x), len(progs.sp_x), progs.max_slots
+        d.nwi, d.nsp, d.max_slots = len(progs.wi_p), len(progs.sp_p), progs.max_slots
         for k, v in arrs.items():
             setattr(d, k, v.ctypes.data if v.size else None)
         with self.torch.cuda.device(self.device):
             check(self.lib.hy_upload_row_programs(self.h, ctypes.byref(d)))
         self._programs = arrs
+
+    def set_option(self, name, value):
+        check(self.lib.hy_set_option(self.h, name.encode(), int(value)))
 
     def launches(self):
         return int(self.lib.hy_launch_count(self.h))

@@ -303,12 +303,14 @@ class RowPrograms:
     pred_p: np.ndarray      # int32
     pred_u: np.ndarray      # int64
     lev_wi: np.ndarray      # int64[nlev+1] work items per intra-row level
-    wi_x: np.ndarray        # int32 position index (into hpos)
+    wi_p: np.ndarray        # int32 target position of the work item
+    wi_kd: np.ndarray       # int64 finalize kind (hdiv of the position)
     wi_y0: np.ndarray       # int64
     wi_y1: np.ndarray       # int64
     wi_slot: np.ndarray     # int32 (-1 = whole position)
     lev_sp: np.ndarray      # int64[nlev+1] split positions per level
-    sp_x: np.ndarray        # int32
+    sp_p: np.ndarray        # int32
+    sp_kd: np.ndarray       # int64
     sp_s0: np.ndarray       # int32
     sp_n: np.ndarray        # int32
     max_slots: int
@@ -355,5 +357,7 @@ def build_programs(an, inner_perm, hub_steps=HUB_STEPS, chunk=HUB_CHUNK):
         nodes = nodes[node_hub[nodes] == 0]
         level_ws[lv] = int(W[nodes].max()) if len(nodes) else 0
     return RowPrograms(row_ptr, st_p, st_j, st_src, st_cnt, st_rel, rel, node_hub, hub_nodes,
-                       hrow_lev, lev_ptr, hpos, hdiv, hpp, pred_p, pred_u, lev_wi, wi_x, wi_y0,
-                       wi_y1, wi_slot, lev_sp, sp_x, sp_s0, sp_n, int(max_slots), level_ws)
+                       hrow_lev, lev_ptr, hpos, hdiv, hpp, pred_p, pred_u, lev_wi,
+                       hpos[wi_x].astype(np.int32), hdiv[wi_x].astype(np.int64), wi_y0, wi_y1, wi_slot,
+                       lev_sp, hpos[sp_x].astype(np.int32), hdiv[sp_x].astype(np.int64), sp_s0, sp_n,
+                       int(max_slots), level_ws)
