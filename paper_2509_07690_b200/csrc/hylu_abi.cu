@@ -15,6 +15,7 @@ __global__ void k_anorm(const double *, const double *, int64_t, double *);
 __global__ void k_rows(DevSym, CallP, const int32_t *, int);
 __global__ void k_sn(DevSym, CallP, const int32_t *);
 size_t sn_smem_bytes();
+size_t pipe_smem_bytes();
 __global__ void k_bhat(DevSym, const int32_t *, const double *, double *);
 __global__ void k_xout(DevSym, const double *, double *);
 __global__ void k_fwd(DevSym, const double *, const int32_t *, int, double *);
@@ -85,7 +86,7 @@ struct hy_handle {
   int epoch = 0;
   int32_t *d_node_level = nullptr;
   int pipe_blocks = 0;
-  int gbatch = 4;                          // claim-order group batch (L2 locality)
+  int gbatch = 1 << 20;                    // claim-order group batch (>= G: level-major)
   double *d_scratch = nullptr;             // hub partial sums
   int64_t scratch_cap = 0;
   int32_t *d_bl_rows = nullptr, *d_bl_hubs = nullptr;
@@ -163,6 +164,11 @@ int hy_create(int device, hy_handle **out) {
   if (e != cudaSuccess) {
     delete h;
     return fail(HY_CUDA_ERROR, std::string("cudaFuncSetAttribute(k_sn): ") + cudaGetErrorString(e));
+  }
+  e = cudaFuncSetAttribute(k_bt_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pipe_smem_bytes());
+  if (e != cudaSuccess) {
+    delete h;
+    return fail(HY_CUDA_ERROR, std::string("cudaFuncSetAttribute(k_bt_pipe): ") + cudaGetErrorString(e));
   }
   *out = h;
   return HY_OK;
@@ -471,7 +477,7 @@ int hy_refactorize_batched(hy_handle *h, int64_t B, const double *d_vals, double
   h->epoch++;
   if (h->pipe_blocks == 0) {
     int per_sm = 0, sms = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bt_pipe, 128, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bt_pipe, 128, pipe_smem_bytes()));
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
     h->pipe_blocks = per_sm * sms;
   }
@@ -493,7 +499,7 @@ int hy_refactorize_batched(hy_handle *h, int64_t B, const double *d_vals, double
       h->launches++;
       const int nr = (int)(h->bl_rptr[l + 1] - h->bl_rptr[l]);
       if (nr) {
-        k_bt_pipe<<<h->pipe_blocks, 128, 0, st>>>(h->S, P, h->prog, h->d_bl_rows + h->bl_rptr[l], nr, G,
+        k_bt_pipe<<<h->pipe_blocks, 128, pipe_smem_bytes(), st>>>(h->S, P, h->prog, h->d_bl_rows + h->bl_rptr[l], nr, G,
                                                    d_b_fuse, h->d_by, (int *)((long long *)h->d_counters + l),
                                                    h->d_flags, h->epoch, h->d_node_level, l, h->gbatch);
         h->launches++;
@@ -505,7 +511,7 @@ int hy_refactorize_batched(hy_handle *h, int64_t B, const double *d_vals, double
     while (l1 < nl && h->bl_hptr[l1 + 1] == h->bl_hptr[l1]) ++l1;
     const int nr = (int)(h->bl_rptr[l1] - h->bl_rptr[l]);
     if (nr) {
-      k_bt_pipe<<<h->pipe_blocks, 128, 0, st>>>(h->S, P, h->prog, h->d_bl_rows + h->bl_rptr[l], nr, G,
+      k_bt_pipe<<<h->pipe_blocks, 128, pipe_smem_bytes(), st>>>(h->S, P, h->prog, h->d_bl_rows + h->bl_rptr[l], nr, G,
                                                  d_b_fuse, h->d_by, (int *)((long long *)h->d_counters + l),
                                                  h->d_flags, h->epoch, h->d_node_level, l, h->gbatch);
       h->launches++;

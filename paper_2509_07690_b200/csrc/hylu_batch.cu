@@ -84,10 +84,97 @@ __device__ __forceinline__ void st_release(int *p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+constexpr int STAGE = 40;   // staged source values per warp (x32 lanes)
+
+__device__ __forceinline__ void cp_async8(double *smem_dst, const double *gsrc) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
+// Run the steps [s0, s1) of one row, staging each chunk of steps' source data
+// (U(j,j), y_j, U(j,>j)) in shared memory with cp.async first, so a chunk costs
+// one memory round trip instead of one per step.  Step metadata for up to 32
+// steps is loaded lane-parallel and broadcast with shuffles.
+template <typename WPtr>
+__device__ __forceinline__ double run_staged(const DevProg &R, int64_t s0, int64_t s1, WPtr w,
+                                             const double *gb, const double *yb, double yacc,
+                                             double *stage, int32_t *relbuf, int lane) {
+  int64_t st = s0;
+  while (st < s1) {
+    const bool have = st + lane < s1;
+    int mp = 0, mc = 0, mj = 0;
+    int64_t msrc = 0, mrel = 0;
+    if (have) {
+      mp = R.st_p[st + lane];
+      mc = R.st_cnt[st + lane];
+      msrc = R.st_src[st + lane];
+      mrel = R.st_rel[st + lane];
+      mj = R.st_j[st + lane];
+    }
+    const int sz = have ? mc + 2 : 0;
+    int incl = sz;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(HY_FULL, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const unsigned fit = __ballot_sync(HY_FULL, have && incl <= STAGE);
+    const int nin = __popc(fit);  // fit is a prefix mask (incl is monotone)
+    if (nin == 0) {
+      // a single step larger than the stage: direct loads
+      const int p0 = __shfl_sync(HY_FULL, mp, 0), c0 = __shfl_sync(HY_FULL, mc, 0);
+      const int64_t src0 = __shfl_sync(HY_FULL, msrc, 0), rel0 = __shfl_sync(HY_FULL, mrel, 0);
+      const int j0 = __shfl_sync(HY_FULL, mj, 0);
+      const double dd = gb[src0 * 32];
+      const double lv = w[p0 * 32] / dd;
+      w[p0 * 32] = lv;
+      yacc -= lv * yb[(int64_t)j0 * 32];
+      const double *us = gb + (src0 + 1) * 32;
+      for (int q = 0; q < c0; ++q) w[R.rel[rel0 + q] * 32] -= lv * us[q * 32];
+      st += 1;
+      continue;
+    }
+    // issue the chunk's copies (each lane copies its own instance)
+    for (int k = 0; k < nin; ++k) {
+      const int ck = __shfl_sync(HY_FULL, mc, k);
+      const int64_t sk = __shfl_sync(HY_FULL, msrc, k);
+      const int64_t rk = __shfl_sync(HY_FULL, mrel, k);
+      const int jk = __shfl_sync(HY_FULL, mj, k);
+      const int ok = __shfl_sync(HY_FULL, incl, k) - ck - 2;
+      cp_async8(stage + ok * 32 + lane, gb + sk * 32);
+      cp_async8(stage + (ok + 1) * 32 + lane, yb + (int64_t)jk * 32);
+      const double *us = gb + (sk + 1) * 32;
+      for (int q = 0; q < ck; ++q) cp_async8(stage + (ok + 2 + q) * 32 + lane, us + q * 32);
+      for (int q = lane; q < ck; q += 32) relbuf[ok + 2 + q] = R.rel[rk + q];
+    }
+    cp_async_wait_all();
+    __syncwarp();
+    for (int k = 0; k < nin; ++k) {
+      const int pk = __shfl_sync(HY_FULL, mp, k);
+      const int ck = __shfl_sync(HY_FULL, mc, k);
+      const int ok = __shfl_sync(HY_FULL, incl, k) - ck - 2;
+      const double d = stage[ok * 32 + lane];
+      const double yj = stage[(ok + 1) * 32 + lane];
+      const double l = w[pk * 32] / d;
+      w[pk * 32] = l;
+      yacc -= l * yj;
+      const double *uv = stage + (ok + 2) * 32 + lane;
+      const int32_t *rl = relbuf + ok + 2;
+      for (int q = 0; q < ck; ++q) w[rl[q] * 32] -= l * uv[q * 32];
+    }
+    __syncwarp();
+    st += nin;
+  }
+  return yacc;
+}
+
 // One (node, group) task: up-looking rows in order, lane = instance.
 __device__ __forceinline__ void bt_node(const DevSym &S, const BatchP &P, const DevProg &R, int u,
                                         int g, const double *rhs, double *Y, double *wsm0, int ws,
-                                        int lane) {
+                                        double *stage, int32_t *relbuf, int lane) {
   const int64_t b = (int64_t)g * 32 + lane;
   const bool live = b < P.B;
   const int nlive = (int)(P.B - (int64_t)g * 32 < 32 ? P.B - (int64_t)g * 32 : 32);
@@ -123,9 +210,9 @@ __device__ __forceinline__ void bt_node(const DevSym &S, const BatchP &P, const 
     }
     __syncwarp();
     if (inSm)
-      yacc = run_steps(R, s0, s1, wsm0 + lane, gb, yb, yacc);
+      yacc = run_staged(R, s0, s1, wsm0 + lane, gb, yb, yacc, stage, relbuf, lane);
     else
-      yacc = run_steps(R, s0, s1, grow + lane, gb, yb, yacc);
+      yacc = run_staged(R, s0, s1, grow + lane, gb, yb, yacc, stage, relbuf, lane);
     const int Lt = L + t;
     const double piv = w0[Lt * 32 + lane];
     bool fired;
@@ -140,6 +227,9 @@ __device__ __forceinline__ void bt_node(const DevSym &S, const BatchP &P, const 
 
 constexpr int PIPE_WARPS = 4;
 constexpr int PIPE_WS = 32;
+size_t pipe_smem_bytes() {
+  return (size_t)PIPE_WARPS * ((PIPE_WS + STAGE) * 32 * sizeof(double) + STAGE * sizeof(int32_t));
+}
 
 // Persistent, dependency-driven row kernel for a segment of levels without hub
 // nodes (the device form of SPEC's pipeline mode): warps claim
@@ -147,12 +237,16 @@ constexpr int PIPE_WS = 32;
 // completion flags of the node's in-segment dependencies, run the task, then
 // publish its flag.  Claim order is topological and every claimed task is held by
 // a resident warp, so the earliest unfinished claimed task can always proceed.
-__global__ void __launch_bounds__(PIPE_WARPS * 32, 6)
+__global__ void __launch_bounds__(PIPE_WARPS * 32, 3)
     k_bt_pipe(DevSym S, BatchP P, DevProg R, const int32_t *nodes, int count, int G,
               const double *rhs, double *Y, int *counter, int *flags, int epoch,
               const int32_t *node_level, int lev0, int gbatch) {
-  __shared__ __align__(16) double wsm[PIPE_WARPS][PIPE_WS * 32];
+  extern __shared__ __align__(16) double pipe_smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double *wsm_w = pipe_smem + (size_t)warp * (PIPE_WS + STAGE) * 32;
+  double *stg_w = wsm_w + PIPE_WS * 32;
+  int32_t *rlb_w = reinterpret_cast<int32_t *>(pipe_smem + (size_t)PIPE_WARPS * (PIPE_WS + STAGE) * 32) +
+                   warp * STAGE;
   const int64_t total = (int64_t)count * G;
   for (;;) {
     long long t = 0;
@@ -175,7 +269,7 @@ __global__ void __launch_bounds__(PIPE_WARPS * 32, 6)
         while (ld_acquire(f) != epoch) __nanosleep(64);
       }
     }
-    bt_node(S, P, R, u, g, rhs, Y, wsm[warp], PIPE_WS, lane);
+    bt_node(S, P, R, u, g, rhs, Y, wsm_w, PIPE_WS, stg_w, rlb_w, lane);
     __threadfence();
     __syncwarp();
     if (lane == 0) st_release(flags + (int64_t)u * G + g, epoch);
