@@ -15,13 +15,15 @@ __global__ void k_anorm(const double *, const double *, int64_t, double *);
 __global__ void k_rows(DevSym, CallP, const int32_t *, int);
 __global__ void k_sn(DevSym, CallP, const int32_t *);
 size_t sn_smem_bytes();
-size_t pipe_smem_bytes();
+size_t pipe_smem_bytes(bool staged);
 __global__ void k_bhat(DevSym, const int32_t *, const double *, double *);
 __global__ void k_xout(DevSym, const double *, double *);
 __global__ void k_fwd(DevSym, const double *, const int32_t *, int, double *);
 __global__ void k_bwd(DevSym, const double *, const int32_t *, int, double *);
+template <bool STAGED>
 __global__ void k_bt_pipe(DevSym, BatchP, DevProg, const int32_t *, int, int, const double *, double *, int *,
-                          int *, int, const int32_t *, int, int);
+                          int *, int, const int32_t *, int, const int64_t *, const int32_t *, const int64_t *,
+                          int);
 __global__ void k_bt_hub(DevSym, BatchP, DevProg, const int32_t *, int, int, const double *, double *,
                          double *, int);
 __global__ void k_batch_bhat(DevSym, const int32_t *, const double *, double *, int64_t);
@@ -86,7 +88,18 @@ struct hy_handle {
   int epoch = 0;
   int32_t *d_node_level = nullptr;
   int pipe_blocks = 0;
-  int gbatch = 1 << 20;                    // claim-order group batch (>= G: level-major)
+  int gbatch = 1 << 20;                    // unused (kept for hy_set_option compatibility)
+  int staged = 0;                          // stage row sources with cp.async (option "staged")
+  // diagonal claim order per (segment, G): pair prefix sums, (level<<16|group), level offsets
+  struct Seg {
+    int l0, l1;
+    int64_t *d_pstart = nullptr;
+    int32_t *d_plg = nullptr;
+    int64_t *d_lptr = nullptr;
+    int npairs = 0;
+  };
+  std::vector<Seg> segs;
+  int segs_G = -1;
   double *d_scratch = nullptr;             // hub partial sums
   int64_t scratch_cap = 0;
   int32_t *d_bl_rows = nullptr, *d_bl_hubs = nullptr;
@@ -165,7 +178,11 @@ int hy_create(int device, hy_handle **out) {
     delete h;
     return fail(HY_CUDA_ERROR, std::string("cudaFuncSetAttribute(k_sn): ") + cudaGetErrorString(e));
   }
-  e = cudaFuncSetAttribute(k_bt_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pipe_smem_bytes());
+  e = cudaFuncSetAttribute(k_bt_pipe<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)pipe_smem_bytes(true));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_bt_pipe<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)pipe_smem_bytes(false));
   if (e != cudaSuccess) {
     delete h;
     return fail(HY_CUDA_ERROR, std::string("cudaFuncSetAttribute(k_bt_pipe): ") + cudaGetErrorString(e));
@@ -182,6 +199,11 @@ void hy_destroy(hy_handle *h) {
   if (h->d_bf) cudaFree(h->d_bf);
   if (h->d_scratch) cudaFree(h->d_scratch);
   if (h->d_flags) cudaFree(h->d_flags);
+  for (auto &sg : h->segs) {
+    cudaFree(sg.d_pstart);
+    cudaFree(sg.d_plg);
+    cudaFree(sg.d_lptr);
+  }
   if (h->d_counters) cudaFree(h->d_counters);
   if (h->d_by) cudaFree(h->d_by);
   delete h;
@@ -194,6 +216,11 @@ int hy_set_option(hy_handle *h, const char *name, int64_t value) {
   if (!h || !name) return fail(HY_INVALID_ARGUMENT, "null handle/name");
   if (std::string(name) == "group_batch" && value >= 1) {
     h->gbatch = (int)value;
+    return HY_OK;
+  }
+  if (std::string(name) == "staged") {
+    h->staged = value != 0;
+    h->pipe_blocks = 0;
     return HY_OK;
   }
   return fail(HY_INVALID_ARGUMENT, std::string("unknown option ") + name);
@@ -440,6 +467,52 @@ static int batch_prepare(hy_handle *h, int64_t B) {
   return HY_OK;
 }
 
+static int build_segments(hy_handle *h, int G) {
+  for (auto &sg : h->segs) {
+    cudaFree(sg.d_pstart);
+    cudaFree(sg.d_plg);
+    cudaFree(sg.d_lptr);
+  }
+  h->segs.clear();
+  const int nl = h->fplan.nlev;
+  int l = 0;
+  while (l < nl) {
+    int l1 = l + 1;
+    if (h->bl_hptr[l + 1] == h->bl_hptr[l])
+      while (l1 < nl && h->bl_hptr[l1 + 1] == h->bl_hptr[l1]) ++l1;
+    hy_handle::Seg sg;
+    sg.l0 = l;
+    sg.l1 = l1;
+    const int L = l1 - l;
+    std::vector<int64_t> lptr(L + 1), pstart;
+    std::vector<int32_t> plg;
+    for (int k = 0; k <= L; ++k) lptr[k] = h->bl_rptr[l + k] - h->bl_rptr[l];
+    int64_t acc = 0;
+    for (int d = 0; d < G + L - 1; ++d) {
+      for (int k = (d - G + 1 > 0 ? d - G + 1 : 0); k <= (d < L - 1 ? d : L - 1); ++k) {
+        const int64_t c = lptr[k + 1] - lptr[k];
+        if (!c) continue;
+        pstart.push_back(acc);
+        plg.push_back((k << 16) | (d - k));
+        acc += c;
+      }
+    }
+    sg.npairs = (int)plg.size();
+    if (sg.npairs) {
+      CK(cudaMalloc((void **)&sg.d_pstart, sizeof(int64_t) * sg.npairs));
+      CK(cudaMalloc((void **)&sg.d_plg, sizeof(int32_t) * sg.npairs));
+      CK(cudaMemcpy(sg.d_pstart, pstart.data(), sizeof(int64_t) * sg.npairs, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(sg.d_plg, plg.data(), sizeof(int32_t) * sg.npairs, cudaMemcpyHostToDevice));
+    }
+    CK(cudaMalloc((void **)&sg.d_lptr, sizeof(int64_t) * (L + 1)));
+    CK(cudaMemcpy(sg.d_lptr, lptr.data(), sizeof(int64_t) * (L + 1), cudaMemcpyHostToDevice));
+    h->segs.push_back(sg);
+    l = l1;
+  }
+  h->segs_G = G;
+  return HY_OK;
+}
+
 int hy_refactorize_batched(hy_handle *h, int64_t B, const double *d_vals, double eps,
                            const hy_factors *prior, int32_t *d_npert, const double *d_b_fuse,
                            uintptr_t stream) {
@@ -477,14 +550,24 @@ int hy_refactorize_batched(hy_handle *h, int64_t B, const double *d_vals, double
   h->epoch++;
   if (h->pipe_blocks == 0) {
     int per_sm = 0, sms = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bt_pipe, 128, pipe_smem_bytes()));
+    if (h->staged)
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bt_pipe<true>, 128, pipe_smem_bytes(true)));
+    else
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bt_pipe<false>, 128,
+                                                       pipe_smem_bytes(false)));
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
     h->pipe_blocks = per_sm * sms;
   }
-  // segments: maximal level runs without hub nodes -> one persistent launch each;
-  // hub levels -> one CTA per (hub node, group)
-  int l = 0;
-  while (l < nl) {
+  // segments: maximal level runs without hub nodes -> one persistent launch each
+  // (diagonal claim order); hub levels -> one CTA per (hub node, group), then the
+  // level's non-hub nodes
+  if (h->segs_G != G) {
+    int rc2 = build_segments(h, G);
+    if (rc2) return rc2;
+  }
+  for (size_t si = 0; si < h->segs.size(); ++si) {
+    const hy_handle::Seg &sg = h->segs[si];
+    const int l = sg.l0;
     if (h->bl_hptr[l + 1] > h->bl_hptr[l]) {
       const int nh = (int)(h->bl_hptr[l + 1] - h->bl_hptr[l]);
       const int64_t need = (int64_t)nh * G * (h->max_slots > 0 ? h->max_slots : 1) * 32;
@@ -495,28 +578,23 @@ int hy_refactorize_batched(hy_handle *h, int64_t B, const double *d_vals, double
         h->scratch_cap = need;
       }
       k_bt_hub<<<(unsigned)(nh * G), 1024, 0, st>>>(h->S, P, h->prog, h->d_bl_hubs + h->bl_hptr[l], nh, G,
-                                                  d_b_fuse, h->d_by, h->d_scratch, h->max_slots);
-      h->launches++;
-      const int nr = (int)(h->bl_rptr[l + 1] - h->bl_rptr[l]);
-      if (nr) {
-        k_bt_pipe<<<h->pipe_blocks, 128, pipe_smem_bytes(), st>>>(h->S, P, h->prog, h->d_bl_rows + h->bl_rptr[l], nr, G,
-                                                   d_b_fuse, h->d_by, (int *)((long long *)h->d_counters + l),
-                                                   h->d_flags, h->epoch, h->d_node_level, l, h->gbatch);
-        h->launches++;
-      }
-      ++l;
-      continue;
-    }
-    int l1 = l;
-    while (l1 < nl && h->bl_hptr[l1 + 1] == h->bl_hptr[l1]) ++l1;
-    const int nr = (int)(h->bl_rptr[l1] - h->bl_rptr[l]);
-    if (nr) {
-      k_bt_pipe<<<h->pipe_blocks, 128, pipe_smem_bytes(), st>>>(h->S, P, h->prog, h->d_bl_rows + h->bl_rptr[l], nr, G,
-                                                 d_b_fuse, h->d_by, (int *)((long long *)h->d_counters + l),
-                                                 h->d_flags, h->epoch, h->d_node_level, l, h->gbatch);
+                                                   d_b_fuse, h->d_by, h->d_scratch, h->max_slots);
       h->launches++;
     }
-    l = l1;
+    const int nr = (int)(h->bl_rptr[sg.l1] - h->bl_rptr[l]);
+    if (nr && sg.npairs) {
+      if (h->staged)
+        k_bt_pipe<true><<<h->pipe_blocks, 128, pipe_smem_bytes(true), st>>>(
+            h->S, P, h->prog, h->d_bl_rows + h->bl_rptr[l], nr, G, d_b_fuse, h->d_by,
+            (int *)((long long *)h->d_counters + si), h->d_flags, h->epoch, h->d_node_level, l, sg.d_pstart,
+            sg.d_plg, sg.d_lptr, sg.npairs);
+      else
+        k_bt_pipe<false><<<h->pipe_blocks, 128, pipe_smem_bytes(false), st>>>(
+            h->S, P, h->prog, h->d_bl_rows + h->bl_rptr[l], nr, G, d_b_fuse, h->d_by,
+            (int *)((long long *)h->d_counters + si), h->d_flags, h->epoch, h->d_node_level, l, sg.d_pstart,
+            sg.d_plg, sg.d_lptr, sg.npairs);
+      h->launches++;
+    }
   }
   CK(cudaGetLastError());
   return HY_OK;

@@ -172,6 +172,7 @@ __device__ __forceinline__ double run_staged(const DevProg &R, int64_t s0, int64
 }
 
 // One (node, group) task: up-looking rows in order, lane = instance.
+template <bool STAGED>
 __device__ __forceinline__ void bt_node(const DevSym &S, const BatchP &P, const DevProg &R, int u,
                                         int g, const double *rhs, double *Y, double *wsm0, int ws,
                                         double *stage, int32_t *relbuf, int lane) {
@@ -209,10 +210,17 @@ __device__ __forceinline__ void bt_node(const DevSym &S, const BatchP &P, const 
       w0[S.colpos[e0 + e] * 32 + inst] = Ab[(int64_t)inst * S.nnz + e0 + e] * S.scale[e0 + e];
     }
     __syncwarp();
-    if (inSm)
-      yacc = run_staged(R, s0, s1, wsm0 + lane, gb, yb, yacc, stage, relbuf, lane);
-    else
-      yacc = run_staged(R, s0, s1, grow + lane, gb, yb, yacc, stage, relbuf, lane);
+    if (STAGED) {
+      if (inSm)
+        yacc = run_staged(R, s0, s1, wsm0 + lane, gb, yb, yacc, stage, relbuf, lane);
+      else
+        yacc = run_staged(R, s0, s1, grow + lane, gb, yb, yacc, stage, relbuf, lane);
+    } else {
+      if (inSm)
+        yacc = run_steps(R, s0, s1, wsm0 + lane, gb, yb, yacc);
+      else
+        yacc = run_steps(R, s0, s1, grow + lane, gb, yb, yacc);
+    }
     const int Lt = L + t;
     const double piv = w0[Lt * 32 + lane];
     bool fired;
@@ -227,8 +235,9 @@ __device__ __forceinline__ void bt_node(const DevSym &S, const BatchP &P, const 
 
 constexpr int PIPE_WARPS = 4;
 constexpr int PIPE_WS = 32;
-size_t pipe_smem_bytes() {
-  return (size_t)PIPE_WARPS * ((PIPE_WS + STAGE) * 32 * sizeof(double) + STAGE * sizeof(int32_t));
+size_t pipe_smem_bytes(bool staged) {
+  const int st = staged ? STAGE : 0;
+  return (size_t)PIPE_WARPS * ((PIPE_WS + st) * 32 * sizeof(double) + st * sizeof(int32_t));
 }
 
 // Persistent, dependency-driven row kernel for a segment of levels without hub
@@ -237,30 +246,38 @@ size_t pipe_smem_bytes() {
 // completion flags of the node's in-segment dependencies, run the task, then
 // publish its flag.  Claim order is topological and every claimed task is held by
 // a resident warp, so the earliest unfinished claimed task can always proceed.
-__global__ void __launch_bounds__(PIPE_WARPS * 32, 3)
+template <bool STAGED>
+__global__ void __launch_bounds__(PIPE_WARPS * 32, STAGED ? 3 : 6)
     k_bt_pipe(DevSym S, BatchP P, DevProg R, const int32_t *nodes, int count, int G,
               const double *rhs, double *Y, int *counter, int *flags, int epoch,
-              const int32_t *node_level, int lev0, int gbatch) {
+              const int32_t *node_level, int lev0, const int64_t *pair_start, const int32_t *pair_lg,
+              const int64_t *seg_lptr, int npairs) {
   extern __shared__ __align__(16) double pipe_smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double *wsm_w = pipe_smem + (size_t)warp * (PIPE_WS + STAGE) * 32;
+  constexpr int SG = STAGED ? STAGE : 0;
+  double *wsm_w = pipe_smem + (size_t)warp * (PIPE_WS + SG) * 32;
   double *stg_w = wsm_w + PIPE_WS * 32;
-  int32_t *rlb_w = reinterpret_cast<int32_t *>(pipe_smem + (size_t)PIPE_WARPS * (PIPE_WS + STAGE) * 32) +
-                   warp * STAGE;
+  int32_t *rlb_w = reinterpret_cast<int32_t *>(pipe_smem + (size_t)PIPE_WARPS * (PIPE_WS + SG) * 32) +
+                   warp * SG;
   const int64_t total = (int64_t)count * G;
+  (void)G;
   for (;;) {
     long long t = 0;
     if (lane == 0) t = (long long)atomicAdd(reinterpret_cast<unsigned long long *>(counter), 1ull);
     t = __shfl_sync(HY_FULL, t, 0);
     if (t >= total) return;
-    // claim order: group batches of `gbatch` groups; inside a batch level-major
-    // (node index), groups fastest — keeps a batch's freshly written rows in L2
-    const int64_t per_batch = (int64_t)count * gbatch;
-    const int64_t bt = t / per_batch, rr = t - bt * per_batch;
-    const int gb_lo = (int)(bt * gbatch);
-    const int gcount = (G - gb_lo) < gbatch ? (G - gb_lo) : gbatch;
-    const int u = nodes[rr / gcount];
-    const int g = gb_lo + (int)(rr % gcount);
+    // claim order: diagonal wavefront over (level, group) pairs — group g at level
+    // l is claimed with group g+1 at level l-1 — so the rows a task reads were
+    // written about one group-equivalent of work earlier (L2-resident), while each
+    // diagonal still holds ~one group's worth of independent tasks.
+    int lo = 0, hi = npairs;  // last k with pair_start[k] <= t
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (pair_start[mid] <= t) lo = mid; else hi = mid;
+    }
+    const int lg = pair_lg[lo];
+    const int lvl = lg >> 16, g = lg & 0xffff;
+    const int u = nodes[seg_lptr[lvl] + (t - pair_start[lo])];
     // every lane acquires every in-segment dependency flag (orders its own loads)
     for (int64_t k = S.dptr[u]; k < S.dptr[u + 1]; ++k) {
       const int v = S.deps[k];
@@ -269,12 +286,19 @@ __global__ void __launch_bounds__(PIPE_WARPS * 32, 3)
         while (ld_acquire(f) != epoch) __nanosleep(64);
       }
     }
-    bt_node(S, P, R, u, g, rhs, Y, wsm_w, PIPE_WS, stg_w, rlb_w, lane);
+    bt_node<STAGED>(S, P, R, u, g, rhs, Y, wsm_w, PIPE_WS, stg_w, rlb_w, lane);
     __threadfence();
     __syncwarp();
     if (lane == 0) st_release(flags + (int64_t)u * G + g, epoch);
   }
 }
+
+template __global__ void k_bt_pipe<false>(DevSym, BatchP, DevProg, const int32_t *, int, int,
+                                          const double *, double *, int *, int *, int, const int32_t *,
+                                          int, const int64_t *, const int32_t *, const int64_t *, int);
+template __global__ void k_bt_pipe<true>(DevSym, BatchP, DevProg, const int32_t *, int, int,
+                                         const double *, double *, int *, int *, int, const int32_t *,
+                                         int, const int64_t *, const int32_t *, const int64_t *, int);
 
 // ---------------------------------------------------------------------------
 // Hub kernel: one CTA per (hub node, group).  Pull programs: the positions of a row

@@ -24,8 +24,8 @@ dr = torch.from_numpy(rhs).cuda()
 x = torch.empty((B, 20000), dtype=torch.float64, device="cuda")
 npert = torch.empty(B, dtype=torch.int32, device="cuda")
 ctx = br.ctx
-for gb in [int(a) for a in sys.argv[1:]] or [1, 2, 4, 8, 16, 128]:
-    ctx.set_option("group_batch", gb)
+for gb in [int(a) for a in sys.argv[1:]] or [0, 1]:
+    ctx.set_option("staged", gb)
     for _ in range(2):
         br.run(dv, dr, x, npert)
     ts = []
@@ -39,4 +39,4 @@ for gb in [int(a) for a in sys.argv[1:]] or [1, 2, 4, 8, 16, 128]:
     xh = x[:2].cpu().numpy()
     res = max(np.linalg.norm(refmatrix.spmv(A0.with_values(vals[b]), xh[b]) - rhs[b]) / np.linalg.norm(rhs[b])
               for b in range(2))
-    print("group_batch %4d  ms %.3f (min %.3f)  inst/s %.0f  res %.1e" % (gb, np.median(ts), min(ts), B / min(ts) * 1e3, res), flush=True)
+    print("staged %4d  ms %.3f (min %.3f)  inst/s %.0f  res %.1e" % (gb, np.median(ts), min(ts), B / min(ts) * 1e3, res), flush=True)
