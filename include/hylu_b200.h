@@ -145,6 +145,8 @@ typedef struct {
   const int32_t *sp_s0;
   const int32_t *sp_n;
   const int32_t *level_ws;  /* [nlevels] widest non-hub node per factorization level */
+  const int64_t *node_rec;  /* [nnodes][4] valoff, dep0, first|rows<<32, width|nl<<32 */
+  const int64_t *row_rec;   /* [n][4] step0, A entry0, nsteps|nentries<<32, original row */
 } hy_row_programs;
 int hy_upload_row_programs(hy_handle *h, const hy_row_programs *progs);
 

@@ -21,11 +21,10 @@ __global__ void k_xout(DevSym, const double *, double *);
 __global__ void k_fwd(DevSym, const double *, const int32_t *, int, double *);
 __global__ void k_bwd(DevSym, const double *, const int32_t *, int, double *);
 template <bool STAGED>
-__global__ void k_bt_pipe(DevSym, BatchP, DevProg, const int32_t *, int, int, const double *, double *, int *,
-                          int *, int, const int32_t *, int, const int64_t *, const int32_t *, const int64_t *,
-                          int);
+__global__ void k_bt_pipe(DevSym, BatchP, DevProg, const int2 *, int64_t, const double *, double *, int *, int *,
+                          int, int);
 __global__ void k_bt_hub(DevSym, BatchP, DevProg, const int32_t *, int, int, const double *, double *,
-                         double *, int);
+                         double *, int, int *, int);
 __global__ void k_batch_bhat(DevSym, const int32_t *, const double *, double *, int64_t);
 __global__ void k_batch_xout(DevSym, const double *, double *, int64_t);
 __global__ void k_batch_fwd(DevSym, const double *, int64_t, const int32_t *, int, int, double *);
@@ -93,10 +92,8 @@ struct hy_handle {
   // diagonal claim order per (segment, G): pair prefix sums, (level<<16|group), level offsets
   struct Seg {
     int l0, l1;
-    int64_t *d_pstart = nullptr;
-    int32_t *d_plg = nullptr;
-    int64_t *d_lptr = nullptr;
-    int npairs = 0;
+    int2 *d_tasks = nullptr;   // (node, group) in diagonal claim order
+    int64_t ntasks = 0;
   };
   std::vector<Seg> segs;
   int segs_G = -1;
@@ -106,6 +103,8 @@ struct hy_handle {
   int64_t launches = 0;
   size_t sn_smem = 0;
 };
+
+static void free_segments(hy_handle *h);
 
 template <class T>
 static int upload(hy_handle *h, T **dst, const T *src, int64_t count) {
@@ -162,6 +161,46 @@ static int upload_prog(hy_handle *h, T **dst, const T *src, int64_t count) {
     if (_r) return _r;                                     \
   } while (0)
 
+static void free_segments(hy_handle *h) {
+  for (auto &sg : h->segs) cudaFree(sg.d_tasks);
+  h->segs.clear();
+}
+
+// Per hub-free level segment, the flat (node, group) task list in diagonal order:
+// group g at level l is listed with group g+1 at level l-1.
+static int build_segments(hy_handle *h, int G) {
+  free_segments(h);
+  const int nl = h->fplan.nlev;
+  std::vector<int32_t> rows(h->bl_rptr[nl]);
+  if (!rows.empty())
+    CK(cudaMemcpy(rows.data(), h->d_bl_rows, sizeof(int32_t) * rows.size(), cudaMemcpyDeviceToHost));
+  int l = 0;
+  while (l < nl) {
+    int l1 = l + 1;
+    if (h->bl_hptr[l + 1] == h->bl_hptr[l])
+      while (l1 < nl && h->bl_hptr[l1 + 1] == h->bl_hptr[l1]) ++l1;
+    hy_handle::Seg sg;
+    sg.l0 = l;
+    sg.l1 = l1;
+    const int L = l1 - l;
+    std::vector<int2> tasks;
+    tasks.reserve((size_t)(h->bl_rptr[l1] - h->bl_rptr[l]) * G);
+    for (int d = 0; d < G + L - 1; ++d)
+      for (int k = (d - G + 1 > 0 ? d - G + 1 : 0); k <= (d < L - 1 ? d : L - 1); ++k)
+        for (int64_t q = h->bl_rptr[l + k]; q < h->bl_rptr[l + k + 1]; ++q)
+          tasks.push_back(make_int2(rows[q], d - k));
+    sg.ntasks = (int64_t)tasks.size();
+    if (sg.ntasks) {
+      CK(cudaMalloc((void **)&sg.d_tasks, sizeof(int2) * sg.ntasks));
+      CK(cudaMemcpy(sg.d_tasks, tasks.data(), sizeof(int2) * sg.ntasks, cudaMemcpyHostToDevice));
+    }
+    h->segs.push_back(sg);
+    l = l1;
+  }
+  h->segs_G = G;
+  return HY_OK;
+}
+
 extern "C" {
 
 const char *hy_last_error(void) { return g_err.c_str(); }
@@ -199,11 +238,7 @@ void hy_destroy(hy_handle *h) {
   if (h->d_bf) cudaFree(h->d_bf);
   if (h->d_scratch) cudaFree(h->d_scratch);
   if (h->d_flags) cudaFree(h->d_flags);
-  for (auto &sg : h->segs) {
-    cudaFree(sg.d_pstart);
-    cudaFree(sg.d_plg);
-    cudaFree(sg.d_lptr);
-  }
+  free_segments(h);
   if (h->d_counters) cudaFree(h->d_counters);
   if (h->d_by) cudaFree(h->d_by);
   delete h;
@@ -426,6 +461,12 @@ int hy_upload_row_programs(hy_handle *h, const hy_row_programs *d) {
   UPP(&p64, d->sp_kd, d->nsp); R.sp_kd = p64;
   UPP(&p32, d->sp_s0, d->nsp); R.sp_s0 = p32;
   UPP(&p32, d->sp_n, d->nsp); R.sp_n = p32;
+  {
+    longlong4 *q;
+    UPP(&q, (const longlong4 *)d->node_rec, nn); R.node_rec = q;
+    UPP(&q, (const longlong4 *)d->row_rec, n); R.row_rec = q;
+  }
+  h->segs_G = -1;
   h->max_slots = (int)d->max_slots;
   h->level_ws.assign(d->level_ws, d->level_ws + h->fplan.nlev);
   // per level split: non-hub nodes / hub nodes
@@ -464,52 +505,6 @@ static int batch_prepare(hy_handle *h, int64_t B) {
     CK(cudaMalloc((void **)&h->d_by, sizeof(double) * needy));
     h->by_cap = needy;
   }
-  return HY_OK;
-}
-
-static int build_segments(hy_handle *h, int G) {
-  for (auto &sg : h->segs) {
-    cudaFree(sg.d_pstart);
-    cudaFree(sg.d_plg);
-    cudaFree(sg.d_lptr);
-  }
-  h->segs.clear();
-  const int nl = h->fplan.nlev;
-  int l = 0;
-  while (l < nl) {
-    int l1 = l + 1;
-    if (h->bl_hptr[l + 1] == h->bl_hptr[l])
-      while (l1 < nl && h->bl_hptr[l1 + 1] == h->bl_hptr[l1]) ++l1;
-    hy_handle::Seg sg;
-    sg.l0 = l;
-    sg.l1 = l1;
-    const int L = l1 - l;
-    std::vector<int64_t> lptr(L + 1), pstart;
-    std::vector<int32_t> plg;
-    for (int k = 0; k <= L; ++k) lptr[k] = h->bl_rptr[l + k] - h->bl_rptr[l];
-    int64_t acc = 0;
-    for (int d = 0; d < G + L - 1; ++d) {
-      for (int k = (d - G + 1 > 0 ? d - G + 1 : 0); k <= (d < L - 1 ? d : L - 1); ++k) {
-        const int64_t c = lptr[k + 1] - lptr[k];
-        if (!c) continue;
-        pstart.push_back(acc);
-        plg.push_back((k << 16) | (d - k));
-        acc += c;
-      }
-    }
-    sg.npairs = (int)plg.size();
-    if (sg.npairs) {
-      CK(cudaMalloc((void **)&sg.d_pstart, sizeof(int64_t) * sg.npairs));
-      CK(cudaMalloc((void **)&sg.d_plg, sizeof(int32_t) * sg.npairs));
-      CK(cudaMemcpy(sg.d_pstart, pstart.data(), sizeof(int64_t) * sg.npairs, cudaMemcpyHostToDevice));
-      CK(cudaMemcpy(sg.d_plg, plg.data(), sizeof(int32_t) * sg.npairs, cudaMemcpyHostToDevice));
-    }
-    CK(cudaMalloc((void **)&sg.d_lptr, sizeof(int64_t) * (L + 1)));
-    CK(cudaMemcpy(sg.d_lptr, lptr.data(), sizeof(int64_t) * (L + 1), cudaMemcpyHostToDevice));
-    h->segs.push_back(sg);
-    l = l1;
-  }
-  h->segs_G = G;
   return HY_OK;
 }
 
@@ -578,21 +573,18 @@ int hy_refactorize_batched(hy_handle *h, int64_t B, const double *d_vals, double
         h->scratch_cap = need;
       }
       k_bt_hub<<<(unsigned)(nh * G), 1024, 0, st>>>(h->S, P, h->prog, h->d_bl_hubs + h->bl_hptr[l], nh, G,
-                                                   d_b_fuse, h->d_by, h->d_scratch, h->max_slots);
+                                                   d_b_fuse, h->d_by, h->d_scratch, h->max_slots,
+                                                   h->d_flags, h->epoch);
       h->launches++;
     }
-    const int nr = (int)(h->bl_rptr[sg.l1] - h->bl_rptr[l]);
-    if (nr && sg.npairs) {
+    if (sg.ntasks) {
+      int *ctr = (int *)((long long *)h->d_counters + si);
       if (h->staged)
         k_bt_pipe<true><<<h->pipe_blocks, 128, pipe_smem_bytes(true), st>>>(
-            h->S, P, h->prog, h->d_bl_rows + h->bl_rptr[l], nr, G, d_b_fuse, h->d_by,
-            (int *)((long long *)h->d_counters + si), h->d_flags, h->epoch, h->d_node_level, l, sg.d_pstart,
-            sg.d_plg, sg.d_lptr, sg.npairs);
+            h->S, P, h->prog, sg.d_tasks, sg.ntasks, d_b_fuse, h->d_by, ctr, h->d_flags, h->epoch, G);
       else
         k_bt_pipe<false><<<h->pipe_blocks, 128, pipe_smem_bytes(false), st>>>(
-            h->S, P, h->prog, h->d_bl_rows + h->bl_rptr[l], nr, G, d_b_fuse, h->d_by,
-            (int *)((long long *)h->d_counters + si), h->d_flags, h->epoch, h->d_node_level, l, sg.d_pstart,
-            sg.d_plg, sg.d_lptr, sg.npairs);
+            h->S, P, h->prog, sg.d_tasks, sg.ntasks, d_b_fuse, h->d_by, ctr, h->d_flags, h->epoch, G);
       h->launches++;
     }
   }

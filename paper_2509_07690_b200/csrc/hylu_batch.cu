@@ -171,35 +171,37 @@ __device__ __forceinline__ double run_staged(const DevProg &R, int64_t s0, int64
   return yacc;
 }
 
-// One (node, group) task: up-looking rows in order, lane = instance.
+// One (node, group) task: up-looking rows in order, lane = instance.  All
+// per-node / per-row metadata comes from packed records (one load each).
 template <bool STAGED>
 __device__ __forceinline__ void bt_node(const DevSym &S, const BatchP &P, const DevProg &R, int u,
-                                        int g, const double *rhs, double *Y, double *wsm0, int ws,
-                                        double *stage, int32_t *relbuf, int lane) {
+                                        const longlong4 nr, int g, const double *rhs, double *Y,
+                                        double *wsm0, int ws, double *stage, int32_t *relbuf,
+                                        int lane) {
   const int64_t b = (int64_t)g * 32 + lane;
   const bool live = b < P.B;
   const int nlive = (int)(P.B - (int64_t)g * 32 < 32 ? P.B - (int64_t)g * 32 : 32);
   const double thr = P.eps * P.anorm[0];
-  const int r = (int)S.first[u];
-  const int s = (int)(S.first[u + 1] - r);
-  const int W = (int)(S.colptr[u + 1] - S.colptr[u]);
-  const int L = S.nl[u];
+  const int64_t vbase = nr.x;
+  const int r = (int)(nr.z & 0xffffffff);
+  const int s = (int)(nr.z >> 32);
+  const int W = (int)(nr.w & 0xffffffff);
+  const int L = (int)(nr.w >> 32);
   double *gb0 = P.BF + (int64_t)g * P.stored * 32;  // group base (no lane offset)
   const double *gb = gb0 + lane;
   double *yb = Y + (int64_t)g * S.n * 32 + lane;
   const double *Ab = P.A + (int64_t)g * 32 * S.nnz;
-  const bool kindsn = S.kind[u] != 0;
-  const int64_t vbase = S.valoff[u];
+  longlong4 rr = R.row_rec[r];
   for (int t = 0; t < s; ++t) {
     const int i = r + t;
-    const int64_t s0 = R.row_ptr[i], s1 = R.row_ptr[i + 1];
+    const int64_t s0 = rr.x, e0 = rr.y;
+    const int64_t s1 = s0 + (rr.z & 0xffffffff);
+    const int k = (int)(rr.z >> 32);
+    const int64_t a = rr.w;
+    if (t + 1 < s) rr = R.row_rec[i + 1];
     const bool inSm = (s1 > s0) && W <= ws;
     double *grow = gb0 + (vbase + (int64_t)t * W) * 32;
     double *w0 = inSm ? wsm0 : grow;
-    const int srow = kindsn ? r + P.iperm[i] : r;
-    const int64_t a = S.mrow_src[srow];
-    const int64_t e0 = S.a_ptr[a];
-    const int k = (int)(S.a_ptr[a + 1] - e0);
     double yacc = (live && rhs) ? S.dr[a] * rhs[b * S.n + a] : 0.0;
     for (int q = 0; q < W; ++q) w0[q * 32 + lane] = 0.0;
     __syncwarp();
@@ -248,10 +250,8 @@ size_t pipe_smem_bytes(bool staged) {
 // a resident warp, so the earliest unfinished claimed task can always proceed.
 template <bool STAGED>
 __global__ void __launch_bounds__(PIPE_WARPS * 32, STAGED ? 3 : 6)
-    k_bt_pipe(DevSym S, BatchP P, DevProg R, const int32_t *nodes, int count, int G,
-              const double *rhs, double *Y, int *counter, int *flags, int epoch,
-              const int32_t *node_level, int lev0, const int64_t *pair_start, const int32_t *pair_lg,
-              const int64_t *seg_lptr, int npairs) {
+    k_bt_pipe(DevSym S, BatchP P, DevProg R, const int2 *tasks, int64_t total, const double *rhs,
+              double *Y, int *counter, int *flags, int epoch, int G) {
   extern __shared__ __align__(16) double pipe_smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int SG = STAGED ? STAGE : 0;
@@ -259,46 +259,33 @@ __global__ void __launch_bounds__(PIPE_WARPS * 32, STAGED ? 3 : 6)
   double *stg_w = wsm_w + PIPE_WS * 32;
   int32_t *rlb_w = reinterpret_cast<int32_t *>(pipe_smem + (size_t)PIPE_WARPS * (PIPE_WS + SG) * 32) +
                    warp * SG;
-  const int64_t total = (int64_t)count * G;
-  (void)G;
   for (;;) {
     long long t = 0;
     if (lane == 0) t = (long long)atomicAdd(reinterpret_cast<unsigned long long *>(counter), 1ull);
     t = __shfl_sync(HY_FULL, t, 0);
     if (t >= total) return;
-    // claim order: diagonal wavefront over (level, group) pairs — group g at level
-    // l is claimed with group g+1 at level l-1 — so the rows a task reads were
-    // written about one group-equivalent of work earlier (L2-resident), while each
-    // diagonal still holds ~one group's worth of independent tasks.
-    int lo = 0, hi = npairs;  // last k with pair_start[k] <= t
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (pair_start[mid] <= t) lo = mid; else hi = mid;
+    const int2 tk = tasks[t];
+    const int u = tk.x, g = tk.y;
+    const longlong4 nr = R.node_rec[u];
+    // lanes poll the dependency flags in parallel (acquire); the warp barrier then
+    // orders every lane's subsequent loads after the producers' releases
+    const int64_t d0 = nr.y, d1 = S.dptr[u + 1];
+    for (int64_t k = d0 + lane; k < d1; k += 32) {
+      const int *f = flags + (int64_t)S.deps[k] * G + g;
+      while (ld_acquire(f) != epoch) __nanosleep(64);
     }
-    const int lg = pair_lg[lo];
-    const int lvl = lg >> 16, g = lg & 0xffff;
-    const int u = nodes[seg_lptr[lvl] + (t - pair_start[lo])];
-    // every lane acquires every in-segment dependency flag (orders its own loads)
-    for (int64_t k = S.dptr[u]; k < S.dptr[u + 1]; ++k) {
-      const int v = S.deps[k];
-      if (node_level[v] >= lev0) {
-        const int *f = flags + (int64_t)v * G + g;
-        while (ld_acquire(f) != epoch) __nanosleep(64);
-      }
-    }
-    bt_node<STAGED>(S, P, R, u, g, rhs, Y, wsm_w, PIPE_WS, stg_w, rlb_w, lane);
+    __syncwarp();
+    bt_node<STAGED>(S, P, R, u, nr, g, rhs, Y, wsm_w, PIPE_WS, stg_w, rlb_w, lane);
     __threadfence();
     __syncwarp();
     if (lane == 0) st_release(flags + (int64_t)u * G + g, epoch);
   }
 }
 
-template __global__ void k_bt_pipe<false>(DevSym, BatchP, DevProg, const int32_t *, int, int,
-                                          const double *, double *, int *, int *, int, const int32_t *,
-                                          int, const int64_t *, const int32_t *, const int64_t *, int);
-template __global__ void k_bt_pipe<true>(DevSym, BatchP, DevProg, const int32_t *, int, int,
-                                         const double *, double *, int *, int *, int, const int32_t *,
-                                         int, const int64_t *, const int32_t *, const int64_t *, int);
+template __global__ void k_bt_pipe<false>(DevSym, BatchP, DevProg, const int2 *, int64_t,
+                                          const double *, double *, int *, int *, int, int);
+template __global__ void k_bt_pipe<true>(DevSym, BatchP, DevProg, const int2 *, int64_t,
+                                         const double *, double *, int *, int *, int, int);
 
 // ---------------------------------------------------------------------------
 // Hub kernel: one CTA per (hub node, group).  Pull programs: the positions of a row
@@ -323,7 +310,8 @@ __device__ __forceinline__ void hub_finalize(const BatchP &P, int64_t kd, int p,
 __global__ void __launch_bounds__(HUB_THREADS) k_bt_hub(DevSym S, BatchP P, DevProg R,
                                                         const int32_t *nodes, int count, int G,
                                                         const double *rhs, double *Y,
-                                                        double *scratch, int max_slots) {
+                                                        double *scratch, int max_slots, int *flags,
+                                                        int epoch) {
   __shared__ double red[HUB_THREADS / 32][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = HUB_THREADS / 32;
   const int task = blockIdx.x;
@@ -412,6 +400,10 @@ __global__ void __launch_bounds__(HUB_THREADS) k_bt_hub(DevSym S, BatchP P, DevP
       yb[(int64_t)i * 32] = yacc;
     }
     __syncthreads();
+  }
+  if (flags && threadIdx.x == 0) {
+    __threadfence();
+    st_release(flags + (int64_t)u * G + g, epoch);
   }
 }
 

@@ -81,6 +81,8 @@ struct DevProg {
   const int64_t *lev_sp;    // split positions per intra-row level
   const int32_t *sp_p;
   const int64_t *sp_kd;
+  const longlong4 *node_rec;  // [nn]: valoff, dep0, first|rows<<32, W|L<<32
+  const longlong4 *row_rec;   // [n]: step0, a_e0, nsteps|k<<32, a
   const int32_t *sp_s0;
   const int32_t *sp_n;
 };

@@ -67,7 +67,7 @@ class ProgramsDesc(ctypes.Structure):
         ("wi_y0", ctypes.c_void_p), ("wi_y1", ctypes.c_void_p), ("wi_slot", ctypes.c_void_p),
         ("lev_sp", ctypes.c_void_p), ("sp_p", ctypes.c_void_p), ("sp_kd", ctypes.c_void_p),
         ("sp_s0", ctypes.c_void_p), ("sp_n", ctypes.c_void_p),
-        ("level_ws", ctypes.c_void_p),
+        ("level_ws", ctypes.c_void_p), ("node_rec", ctypes.c_void_p), ("row_rec", ctypes.c_void_p),
     ]
 
 
@@ -206,7 +206,8 @@ class DeviceContext:
         arrs = {k: np.ascontiguousarray(getattr(progs, k)) for k in (
             "row_ptr", "st_p", "st_j", "st_src", "st_cnt", "st_rel", "rel", "node_hub", "hrow_lev",
             "lev_ptr", "hpos", "hdiv", "hpp", "pred_p", "pred_u", "lev_wi", "wi_p", "wi_kd", "wi_y0",
-            "wi_y1", "wi_slot", "lev_sp", "sp_p", "sp_kd", "sp_s0", "sp_n", "level_ws")}
+            "wi_y1", "wi_slot", "lev_sp", "sp_p", "sp_kd", "sp_s0", "sp_n", "level_ws", "node_rec",
+            "row_rec")}
         d = ProgramsDesc()
         d.nsteps, d.nrel = len(progs.st_p), len(progs.rel)
         d.nhubrows = len(progs.hrow_lev) - 1

@@ -315,6 +315,8 @@ class RowPrograms:
     sp_n: np.ndarray        # int32
     max_slots: int
     level_ws: np.ndarray    # int32[nlevels] max width of non-hub nodes per factor level
+    node_rec: np.ndarray    # int64[nn, 4]: valoff, dep0, (first | rows<<32), (W | L<<32)
+    row_rec: np.ndarray     # int64[n, 4]: step0, a_e0, (nsteps | k<<32), a (original row)
 
     @property
     def nsteps(self):
@@ -351,6 +353,24 @@ def build_programs(an, inner_perm, hub_steps=HUB_STEPS, chunk=HUB_CHUNK):
     (lev_wi, wi_x, wi_y0, wi_y1, wi_slot, lev_sp, sp_x, sp_s0, sp_n,
      max_slots) = _chunks(hrow_lev, lev_ptr, hpp, chunk)
     W = np.diff(s.colptr)
+    rows = np.diff(s.node_first)
+    ndeps = np.diff(s.dep_ptr)
+    node_rec = np.zeros((s.nnodes, 4), np.int64)
+    node_rec[:, 0] = s.valoff[:-1]
+    node_rec[:, 1] = s.dep_ptr[:-1]
+    node_rec[:, 2] = s.node_first[:-1] | (rows.astype(np.int64) << 32)
+    node_rec[:, 3] = W | (s.nl.astype(np.int64) << 32)
+    del ndeps
+    # row records: physical row i of node u holds M row (first + iperm[i]) in supernodes
+    first_of = s.node_first[s.node_of]
+    src = np.where(s.node_kind[s.node_of] == 1, first_of + ip, np.arange(s.n))
+    a = vm.mrow_src[src]
+    row_rec = np.zeros((s.n, 4), np.int64)
+    row_rec[:, 0] = row_ptr[:-1]
+    row_rec[:, 1] = an.A.row_ptr[a]
+    k = an.A.row_ptr[a + 1] - an.A.row_ptr[a]
+    row_rec[:, 2] = (row_ptr[1:] - row_ptr[:-1]) | (k.astype(np.int64) << 32)
+    row_rec[:, 3] = a
     level_ws = np.zeros(len(s.level_ptr) - 1, np.int32)
     for lv in range(len(level_ws)):
         nodes = s.level_nodes[s.level_ptr[lv]:s.level_ptr[lv + 1]]
@@ -360,4 +380,4 @@ def build_programs(an, inner_perm, hub_steps=HUB_STEPS, chunk=HUB_CHUNK):
                        hrow_lev, lev_ptr, hpos, hdiv, hpp, pred_p, pred_u, lev_wi,
                        hpos[wi_x].astype(np.int32), hdiv[wi_x].astype(np.int64), wi_y0, wi_y1, wi_slot,
                        lev_sp, hpos[sp_x].astype(np.int32), hdiv[sp_x].astype(np.int64), sp_s0, sp_n,
-                       int(max_slots), level_ws)
+                       int(max_slots), level_ws, node_rec, row_rec)
