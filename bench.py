@@ -189,7 +189,8 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=dev)
     from paper_2509_07690_b200 import api
     threads = max(1, (os.cpu_count() or 8) // max(1, world))
-    lo, hi = rank * N_INST // world, (rank + 1) * N_INST // world
+    from paper_2509_07690_b200.sharding import shard_range
+    lo, hi = shard_range(N_INST, rank, world)
     B = hi - lo
     A0, bv, vals, rhs = make_problem(lo, hi, threads)
     an = analysis_for(A0)
