@@ -113,6 +113,28 @@ int hy_refactorize(hy_handle *h, const double *d_avals, double eps, const hy_fac
 int hy_solve(hy_handle *h, const hy_factors *f, const double *d_b, double *d_x,
              uintptr_t stream);
 
+/* Column-slab plan for supernode targets (schedule.build_slab_plan): one CTA per
+ * slab, slabs grouped by factorization level.  Optional: without it supernodes
+ * run the one-CTA-per-supernode kernel. */
+typedef struct {
+  int64_t nslabs, nitems, ndeps, nlevels;
+  const int32_t *sl_node;       /* [nslabs] target supernode */
+  const int32_t *sl_c0;         /* [nslabs] first column position */
+  const int32_t *sl_c1;         /* [nslabs] end column position */
+  const int8_t *sl_kind;        /* [nslabs] 0 L-region, 1 block, 2 panel */
+  const int64_t *it_ptr;        /* [nslabs+1] */
+  const int32_t *it_k;          /* [nitems] source index within the target's deps */
+  const int32_t *it_q0;         /* [nitems] beyond-block column range of the source */
+  const int32_t *it_q1;
+  const int8_t *it_own;         /* [nitems] slab owns the source's block columns */
+  const int32_t *dep_pb;        /* [ndeps] block position of each source in its target */
+  const int64_t *level_slab_ptr;/* [nlevels+1] */
+  const int32_t *level_smax;    /* [nlevels] max target rows */
+  const int32_t *level_mmax;    /* [nlevels] max source rows */
+  const int32_t *level_swmax;   /* [nlevels] max slab width */
+} hy_slab_plan;
+int hy_upload_slab_plan(hy_handle *h, const hy_slab_plan *plan);
+
 /* Row programs for the batched path (built on the host by schedule.py for a given
  * prior inner_perm).  Must be uploaded before the
  * batched calls, and must match the inner_perm of the prior they are used with. */

@@ -15,6 +15,21 @@ __global__ void k_anorm(const double *, const double *, int64_t, double *);
 __global__ void k_rows(DevSym, CallP, const int32_t *, int);
 __global__ void k_sn(DevSym, CallP, const int32_t *);
 size_t sn_smem_bytes();
+struct SlabDev {
+  const int32_t *sl_node;
+  const int32_t *sl_c0;
+  const int32_t *sl_c1;
+  const int8_t *sl_kind;
+  const int64_t *it_ptr;
+  const int32_t *it_k;
+  const int32_t *it_q0;
+  const int32_t *it_q1;
+  const int8_t *it_own;
+  const int32_t *dep_pb;
+};
+__global__ void k_slab(DevSym, CallP, SlabDev, int, int *, int *, int *, int, int, int, int);
+__global__ void k_lperm(DevSym, CallP, const int32_t *, int);
+size_t slab_smem_bytes(int, int, int);
 size_t pipe_smem_bytes(bool staged);
 __global__ void k_bhat(DevSym, const int32_t *, const double *, double *);
 __global__ void k_xout(DevSym, const double *, double *);
@@ -102,6 +117,16 @@ struct hy_handle {
   int32_t *d_bl_rows = nullptr, *d_bl_hubs = nullptr;
   int64_t launches = 0;
   size_t sn_smem = 0;
+  // slab plan for supernode targets (single-instance factorization)
+  bool slab_ok = false;
+  SlabDev slab{};
+  std::vector<void *> slab_allocs;
+  std::vector<int64_t> slab_lptr;          // slabs per level
+  std::vector<int32_t> slab_smax, slab_mmax, slab_swmax;
+  int *d_slab_counters = nullptr;          // one per level
+  int *d_dep_flags = nullptr;              // per dependency edge
+  int *d_lu_flags = nullptr;               // per node
+  int slab_epoch = 0;
 };
 
 static void free_segments(hy_handle *h);
@@ -201,6 +226,22 @@ static int build_segments(hy_handle *h, int G) {
   return HY_OK;
 }
 
+template <class T>
+static int upload_slab(hy_handle *h, T **dst, const T *src, int64_t count) {
+  *dst = nullptr;
+  if (count <= 0) return HY_OK;
+  CK(cudaMalloc((void **)dst, sizeof(T) * count));
+  h->slab_allocs.push_back(*dst);
+  if (src) CK(cudaMemcpy(*dst, src, sizeof(T) * count, cudaMemcpyHostToDevice));
+  return HY_OK;
+}
+
+#define UPS(dst, src, cnt)                                 \
+  do {                                                     \
+    int _r = upload_slab(h, dst, src, (int64_t)(cnt));     \
+    if (_r) return _r;                                     \
+  } while (0)
+
 extern "C" {
 
 const char *hy_last_error(void) { return g_err.c_str(); }
@@ -235,6 +276,7 @@ void hy_destroy(hy_handle *h) {
   cudaSetDevice(h->device);
   for (void *p : h->allocs) cudaFree(p);
   for (void *p : h->prog_allocs) cudaFree(p);
+  for (void *p : h->slab_allocs) cudaFree(p);
   if (h->d_bf) cudaFree(h->d_bf);
   if (h->d_scratch) cudaFree(h->d_scratch);
   if (h->d_flags) cudaFree(h->d_flags);
@@ -327,6 +369,48 @@ int hy_upload_symbolic(hy_handle *h, const hy_symbolic_desc *d) {
   return HY_OK;
 }
 
+int hy_upload_slab_plan(hy_handle *h, const hy_slab_plan *d) {
+  if (!h || !h->uploaded || !d) return fail(HY_INVALID_ARGUMENT, "symbolic not uploaded / null");
+  if (d->nlevels != h->fplan.nlev) return fail(HY_DIMENSION_MISMATCH, "slab plan level count mismatch");
+  CK(cudaSetDevice(h->device));
+  for (void *p : h->slab_allocs) cudaFree(p);
+  h->slab_allocs.clear();
+  SlabDev &D = h->slab;
+  int32_t *p32;
+  int8_t *p8;
+  int64_t *p64;
+  UPS(&p32, d->sl_node, d->nslabs); D.sl_node = p32;
+  UPS(&p32, d->sl_c0, d->nslabs); D.sl_c0 = p32;
+  UPS(&p32, d->sl_c1, d->nslabs); D.sl_c1 = p32;
+  UPS(&p8, d->sl_kind, d->nslabs); D.sl_kind = p8;
+  UPS(&p64, d->it_ptr, d->nslabs + 1); D.it_ptr = p64;
+  UPS(&p32, d->it_k, d->nitems); D.it_k = p32;
+  UPS(&p32, d->it_q0, d->nitems); D.it_q0 = p32;
+  UPS(&p32, d->it_q1, d->nitems); D.it_q1 = p32;
+  UPS(&p8, d->it_own, d->nitems); D.it_own = p8;
+  UPS(&p32, d->dep_pb, d->ndeps); D.dep_pb = p32;
+  h->slab_lptr.assign(d->level_slab_ptr, d->level_slab_ptr + d->nlevels + 1);
+  h->slab_smax.assign(d->level_smax, d->level_smax + d->nlevels);
+  h->slab_mmax.assign(d->level_mmax, d->level_mmax + d->nlevels);
+  h->slab_swmax.assign(d->level_swmax, d->level_swmax + d->nlevels);
+  UPS(&h->d_slab_counters, (const int *)nullptr, d->nlevels + 1);
+  UPS(&h->d_dep_flags, (const int *)nullptr, d->ndeps + 1);
+  UPS(&h->d_lu_flags, (const int *)nullptr, h->S.nn);
+  CK(cudaMemset(h->d_dep_flags, 0, sizeof(int) * (d->ndeps + 1)));
+  CK(cudaMemset(h->d_lu_flags, 0, sizeof(int) * h->S.nn));
+  size_t mx = 0;
+  for (int64_t l = 0; l < d->nlevels; ++l) {
+    if (d->level_slab_ptr[l + 1] == d->level_slab_ptr[l]) continue;
+    const size_t b = slab_smem_bytes(d->level_smax[l], d->level_mmax[l], d->level_swmax[l]);
+    if (b > mx) mx = b;
+  }
+  if (mx > 227 * 1024) return fail(HY_INVALID_ARGUMENT, "slab shared memory exceeds 227 KB");
+  if (mx) CK(cudaFuncSetAttribute(k_slab, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx));
+  h->slab_epoch = 0;
+  h->slab_ok = true;
+  return HY_OK;
+}
+
 static int run_factor(hy_handle *h, const double *d_avals, double eps, const hy_factors *prior,
                       hy_factors *out, cudaStream_t st) {
   if (!h || !h->uploaded) return fail(HY_INVALID_ARGUMENT, "symbolic not uploaded");
@@ -362,6 +446,10 @@ static int run_factor(hy_handle *h, const double *d_avals, double eps, const hy_
     h->launches++;
   }
   const Plan &pl = h->fplan;
+  if (h->slab_ok) {
+    h->slab_epoch++;
+    CK(cudaMemsetAsync(h->d_slab_counters, 0, sizeof(int) * (pl.nlev + 1), st));
+  }
   for (int l = 0; l < pl.nlev; ++l) {
     const int nr = (int)(pl.rptr[l + 1] - pl.rptr[l]);
     const int ns = (int)(pl.sptr[l + 1] - pl.sptr[l]);
@@ -369,7 +457,21 @@ static int run_factor(hy_handle *h, const double *d_avals, double eps, const hy_
       k_rows<<<(nr + 3) / 4, 128, 0, st>>>(h->S, P, pl.d_rows + pl.rptr[l], nr);
       h->launches++;
     }
-    if (ns) {
+    if (ns && h->slab_ok) {
+      const int nsl = (int)(h->slab_lptr[l + 1] - h->slab_lptr[l]);
+      const size_t smem = slab_smem_bytes(h->slab_smax[l], h->slab_mmax[l], h->slab_swmax[l]);
+      k_slab<<<nsl, 256, smem, st>>>(h->S, P, h->slab, (int)h->slab_lptr[l], h->d_slab_counters + l,
+                                     h->d_dep_flags, h->d_lu_flags, h->slab_epoch, h->slab_smax[l],
+                                     h->slab_mmax[l], h->slab_swmax[l]);
+      h->launches++;
+      if (!P.refactor) {
+        int maxL = 1;
+        dim3 g(ns, 4);
+        (void)maxL;
+        k_lperm<<<g, 256, 0, st>>>(h->S, P, pl.d_sns + pl.sptr[l], ns);
+        h->launches++;
+      }
+    } else if (ns) {
       k_sn<<<ns, 256, h->sn_smem, st>>>(h->S, P, pl.d_sns + pl.sptr[l]);
       h->launches++;
     }

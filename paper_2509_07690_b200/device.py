@@ -71,6 +71,19 @@ class ProgramsDesc(ctypes.Structure):
     ]
 
 
+class SlabPlanDesc(ctypes.Structure):
+    _fields_ = [
+        ("nslabs", ctypes.c_int64), ("nitems", ctypes.c_int64), ("ndeps", ctypes.c_int64),
+        ("nlevels", ctypes.c_int64),
+        ("sl_node", ctypes.c_void_p), ("sl_c0", ctypes.c_void_p), ("sl_c1", ctypes.c_void_p),
+        ("sl_kind", ctypes.c_void_p), ("it_ptr", ctypes.c_void_p), ("it_k", ctypes.c_void_p),
+        ("it_q0", ctypes.c_void_p), ("it_q1", ctypes.c_void_p), ("it_own", ctypes.c_void_p),
+        ("dep_pb", ctypes.c_void_p), ("level_slab_ptr", ctypes.c_void_p),
+        ("level_smax", ctypes.c_void_p), ("level_mmax", ctypes.c_void_p),
+        ("level_swmax", ctypes.c_void_p),
+    ]
+
+
 def library():
     """Load the CUDA library (building it in-tree first if it is absent)."""
     global _lib
@@ -102,6 +115,7 @@ def library():
     lib.hy_solve_batched.argtypes = [vp, i64, vp, vp, u]
     lib.hy_batched_factor_values.argtypes = [vp, i64, vp, u]
     lib.hy_set_option.argtypes = [vp, ctypes.c_char_p, i64]
+    lib.hy_upload_slab_plan.argtypes = [vp, ctypes.POINTER(SlabPlanDesc)]
     _lib = lib
     return lib
 
@@ -171,6 +185,43 @@ class DeviceContext:
         self.stored = int(self.lib.hy_stored_values(self.h))
         self.n = s.n
         self.nnz = A.nnz
+        if s.supernode_count:
+            self.upload_slab_plan()
+
+    def upload_slab_plan(self):
+        from . import schedule
+        s = self.analysis.symbolic
+        plan = getattr(s, "_slab_plan", None)
+        if plan is None:
+            plan = schedule.build_slab_plan(s)
+            s._slab_plan = plan
+        need = schedule.slab_level_smem(s, plan)
+        dep_pb = schedule._dep_block_pos(s.node_first, s.node_kind, s.colptr, s.cols, s.nl,
+                                         s.dep_ptr, s.deps)
+        arrs = dict(
+            sl_node=np.ascontiguousarray(plan.sl_node, np.int32),
+            sl_c0=np.ascontiguousarray(plan.sl_c0, np.int32),
+            sl_c1=np.ascontiguousarray(plan.sl_c1, np.int32),
+            sl_kind=np.ascontiguousarray(plan.sl_kind, np.int8),
+            it_ptr=np.ascontiguousarray(plan.it_ptr, np.int64),
+            it_k=np.ascontiguousarray(plan.it_k, np.int32),
+            it_q0=np.ascontiguousarray(plan.it_q0, np.int32),
+            it_q1=np.ascontiguousarray(plan.it_q1, np.int32),
+            it_own=np.ascontiguousarray(plan.it_own, np.int8),
+            dep_pb=np.ascontiguousarray(dep_pb, np.int32),
+            level_slab_ptr=np.ascontiguousarray(plan.level_slab_ptr, np.int64),
+            level_smax=np.ascontiguousarray(need[:, 0], np.int32),
+            level_mmax=np.ascontiguousarray(need[:, 1], np.int32),
+            level_swmax=np.ascontiguousarray(need[:, 2], np.int32),
+        )
+        d = SlabPlanDesc()
+        d.nslabs, d.nitems, d.ndeps = plan.nslabs, len(plan.it_k), len(dep_pb)
+        d.nlevels = len(plan.level_slab_ptr) - 1
+        for k, v in arrs.items():
+            setattr(d, k, v.ctypes.data if v.size else None)
+        with self.torch.cuda.device(self.device):
+            check(self.lib.hy_upload_slab_plan(self.h, ctypes.byref(d)))
+        self._slab_arrays = arrs
 
     def __del__(self):
         try:

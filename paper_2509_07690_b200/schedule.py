@@ -381,3 +381,230 @@ def build_programs(an, inner_perm, hub_steps=HUB_STEPS, chunk=HUB_CHUNK):
                        hpos[wi_x].astype(np.int32), hdiv[wi_x].astype(np.int64), wi_y0, wi_y1, wi_slot,
                        lev_sp, hpos[sp_x].astype(np.int32), hdiv[sp_x].astype(np.int64), sp_s0, sp_n,
                        int(max_slots), level_ws, node_rec, row_rec)
+
+
+# --------------------------------------------------------------------------- slab plan
+SLAB_BUDGET = 16384      # accumulator doubles per slab CTA (rows x columns), 128 KB
+SLAB_COLS = 2048         # column cap per slab
+
+
+@njit(cache=True)
+def _lower_bound(a, lo, hi, key):
+    while lo < hi:
+        mid = (lo + hi) >> 1
+        if a[mid] < key:
+            lo = mid + 1
+        else:
+            hi = mid
+    return lo
+
+
+@njit(cache=True)
+def _slab_plan(first, kind, colptr, cols, nl, dptr, deps, node_of, level, budget, cap):
+    """Column slabs of every supernode target and, per slab, the ascending list of
+    source steps that touch it (or whose block it owns).
+
+    A target's L-region slabs never split a source node's columns; the block slab
+    starts at the diagonal block.  Item = (dep index k, q0, q1, owner) where
+    [q0, q1) is the range of the source's beyond-block columns that land in the slab."""
+    nn = len(kind)
+    # pass 1: count slabs / items
+    sl_node_l = []
+    sl_c0_l = []
+    sl_c1_l = []
+    sl_kind_l = []
+    it_ptr_l = [np.int64(0)]
+    it_k_l = []
+    it_q0_l = []
+    it_q1_l = []
+    it_own_l = []
+    sn_slab0 = np.full(nn, -1, np.int64)
+    sn_nslab = np.zeros(nn, np.int64)
+    sn_bslab = np.full(nn, -1, np.int64)
+    for u in range(nn):
+        if kind[u] != 1:
+            continue
+        r = first[u]
+        s = first[u + 1] - r
+        c0 = colptr[u]
+        W = colptr[u + 1] - c0
+        L = nl[u]
+        sw = budget // s
+        if sw > cap:
+            sw = cap
+        if sw < 64:
+            sw = 64
+        base = len(sl_node_l)
+        sn_slab0[u] = base
+        # L-region slabs: pack node runs
+        p = 0
+        while p < L:
+            start = p
+            while p < L:
+                v = node_of[cols[c0 + p]]
+                q = p
+                while q < L and node_of[cols[c0 + q]] == v:
+                    q += 1
+                if q - start > sw and p > start:
+                    break
+                p = q
+                if p - start >= sw:
+                    break
+            sl_node_l.append(u)
+            sl_c0_l.append(start)
+            sl_c1_l.append(p)
+            sl_kind_l.append(0)
+        # block slab + panel slabs
+        p = L
+        first_u = True
+        while p < W:
+            e = min(W, p + sw)
+            sl_node_l.append(u)
+            sl_c0_l.append(p)
+            sl_c1_l.append(e)
+            if first_u:
+                sn_bslab[u] = len(sl_node_l) - 1
+                sl_kind_l.append(1)
+                first_u = False
+            else:
+                sl_kind_l.append(2)
+            p = e
+        ns = len(sl_node_l) - base
+        sn_nslab[u] = ns
+        # items per slab
+        for si in range(base, base + ns):
+            a0 = sl_c0_l[si]
+            a1 = sl_c1_l[si]
+            idlo = cols[c0 + a0]
+            idhi = cols[c0 + a1 - 1]
+            for k in range(dptr[u + 1] - dptr[u]):
+                v = deps[dptr[u] + k]
+                vf = first[v]
+                vs = first[v + 1] - vf
+                vc0 = colptr[v]
+                vW = colptr[v + 1] - vc0
+                pst = nl[v] + vs          # first beyond-block position in v's list
+                # block position of v in the target (owner test)
+                pb0 = _lower_bound(cols, c0, c0 + L, vf) - c0
+                own = 1 if (pb0 >= a0 and pb0 < a1) else 0
+                q0 = _lower_bound(cols, vc0 + pst, vc0 + vW, idlo) - vc0 - pst
+                q1 = _lower_bound(cols, vc0 + pst, vc0 + vW, idhi + 1) - vc0 - pst
+                if q1 > q0 or own:
+                    it_k_l.append(np.int32(k))
+                    it_q0_l.append(np.int32(q0))
+                    it_q1_l.append(np.int32(q1))
+                    it_own_l.append(np.int8(own))
+            it_ptr_l.append(np.int64(len(it_k_l)))
+    ns = len(sl_node_l)
+    sl_node = np.empty(ns, np.int32)
+    sl_c0 = np.empty(ns, np.int32)
+    sl_c1 = np.empty(ns, np.int32)
+    sl_kind = np.empty(ns, np.int8)
+    for x in range(ns):
+        sl_node[x] = sl_node_l[x]
+        sl_c0[x] = sl_c0_l[x]
+        sl_c1[x] = sl_c1_l[x]
+        sl_kind[x] = sl_kind_l[x]
+    it_ptr = np.empty(len(it_ptr_l), np.int64)
+    for x in range(len(it_ptr_l)):
+        it_ptr[x] = it_ptr_l[x]
+    ni = len(it_k_l)
+    it_k = np.empty(ni, np.int32)
+    it_q0 = np.empty(ni, np.int32)
+    it_q1 = np.empty(ni, np.int32)
+    it_own = np.empty(ni, np.int8)
+    for x in range(ni):
+        it_k[x] = it_k_l[x]
+        it_q0[x] = it_q0_l[x]
+        it_q1[x] = it_q1_l[x]
+        it_own[x] = it_own_l[x]
+    return sl_node, sl_c0, sl_c1, sl_kind, it_ptr, it_k, it_q0, it_q1, it_own, sn_slab0, sn_nslab, sn_bslab
+
+
+@dataclass
+class SlabPlan:
+    sl_node: np.ndarray
+    sl_c0: np.ndarray
+    sl_c1: np.ndarray
+    sl_kind: np.ndarray      # 0 L-region, 1 block (+ first panel part), 2 panel
+    it_ptr: np.ndarray
+    it_k: np.ndarray
+    it_q0: np.ndarray
+    it_q1: np.ndarray
+    it_own: np.ndarray
+    sn_slab0: np.ndarray
+    sn_nslab: np.ndarray
+    sn_bslab: np.ndarray
+    level_slab_ptr: np.ndarray   # slabs grouped by factorization level (slab ids are in level order)
+
+    @property
+    def nslabs(self):
+        return len(self.sl_node)
+
+
+def build_slab_plan(sym, budget=SLAB_BUDGET, cap=SLAB_COLS):
+    """Slabs in factorization-level order (so one launch per level covers a
+    contiguous slab-id range, targets ascending, slabs ascending within a target)."""
+    s = sym
+    (sl_node, sl_c0, sl_c1, sl_kind, it_ptr, it_k, it_q0, it_q1, it_own, sn_slab0, sn_nslab,
+     sn_bslab) = _slab_plan(s.node_first, s.node_kind, s.colptr, s.cols, s.nl, s.dep_ptr, s.deps,
+                            s.node_of, s.level, budget, cap)
+    # reorder slabs by (level, node, slab) — nodes ascending already; stable sort on level
+    lev = s.level[sl_node] if len(sl_node) else np.zeros(0, np.int64)
+    order = np.argsort(lev, kind="stable")
+    inv = np.empty_like(order)
+    inv[order] = np.arange(len(order))
+    cnt = np.diff(it_ptr)
+    new_ptr = np.zeros(len(order) + 1, np.int64)
+    np.cumsum(cnt[order], out=new_ptr[1:])
+    idx = np.concatenate([np.arange(it_ptr[o], it_ptr[o + 1]) for o in order]) if len(order) else \
+        np.zeros(0, np.int64)
+    nlev = len(s.level_ptr) - 1
+    lptr = np.zeros(nlev + 1, np.int64)
+    if len(lev):
+        np.add.at(lptr[1:], lev, 1)
+    np.cumsum(lptr, out=lptr)
+    has = sn_slab0 >= 0
+    sn_slab0 = sn_slab0.copy()
+    sn_bslab = sn_bslab.copy()
+    sn_slab0[has] = inv[sn_slab0[has]]
+    sn_bslab[has] = inv[sn_bslab[has]]
+    return SlabPlan(sl_node[order], sl_c0[order], sl_c1[order], sl_kind[order], new_ptr,
+                    it_k[idx], it_q0[idx], it_q1[idx], it_own[idx], sn_slab0, sn_nslab, sn_bslab,
+                    lptr)
+
+
+@njit(cache=True)
+def _dep_block_pos(first, kind, colptr, cols, nl, dptr, deps):
+    """Per dependency edge (u, v): position in u's column list of v's first present
+    block column, and the per-slab-level shared-memory needs."""
+    nd = dptr[len(kind)]
+    pb = np.empty(nd, np.int32)
+    for u in range(len(kind)):
+        c0 = colptr[u]
+        L = nl[u]
+        for k in range(dptr[u], dptr[u + 1]):
+            v = deps[k]
+            pb[k] = _lower_bound(cols, c0, c0 + L, first[v]) - c0
+    return pb
+
+
+def slab_level_smem(sym, plan):
+    """(Smax, Mmax, SWmax) per level for the slab launch's dynamic shared memory."""
+    s = sym
+    nlev = len(plan.level_slab_ptr) - 1
+    out = np.zeros((nlev, 3), np.int64)
+    rows = np.diff(s.node_first)
+    for lv in range(nlev):
+        a, b = plan.level_slab_ptr[lv], plan.level_slab_ptr[lv + 1]
+        if a == b:
+            continue
+        nodes = plan.sl_node[a:b]
+        sw = (plan.sl_c1[a:b] - plan.sl_c0[a:b])
+        mm = 1
+        for u in np.unique(nodes):
+            d = s.deps[s.dep_ptr[u]:s.dep_ptr[u + 1]]
+            if len(d):
+                mm = max(mm, int(rows[d].max()))
+        out[lv] = (int(rows[nodes].max()), mm, int(sw.max()))
+    return out
