@@ -132,6 +132,7 @@ typedef struct {
   const int32_t *level_smax;    /* [nlevels] max target rows */
   const int32_t *level_mmax;    /* [nlevels] max source rows */
   const int32_t *level_swmax;   /* [nlevels] max slab width */
+  const int32_t *level_accmax;  /* [nlevels] max rows x width of a slab accumulator */
 } hy_slab_plan;
 int hy_upload_slab_plan(hy_handle *h, const hy_slab_plan *plan);
 

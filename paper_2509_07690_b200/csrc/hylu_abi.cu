@@ -27,9 +27,9 @@ struct SlabDev {
   const int8_t *it_own;
   const int32_t *dep_pb;
 };
-__global__ void k_slab(DevSym, CallP, SlabDev, int, int *, int *, int *, int, int, int, int);
+__global__ void k_slab(DevSym, CallP, SlabDev, int, int *, int *, int *, int, int, int, int, int);
 __global__ void k_lperm(DevSym, CallP, const int32_t *, int);
-size_t slab_smem_bytes(int, int, int);
+size_t slab_smem_bytes(int, int, int, int);
 size_t pipe_smem_bytes(bool staged);
 __global__ void k_bhat(DevSym, const int32_t *, const double *, double *);
 __global__ void k_xout(DevSym, const double *, double *);
@@ -122,7 +122,7 @@ struct hy_handle {
   SlabDev slab{};
   std::vector<void *> slab_allocs;
   std::vector<int64_t> slab_lptr;          // slabs per level
-  std::vector<int32_t> slab_smax, slab_mmax, slab_swmax;
+  std::vector<int32_t> slab_smax, slab_mmax, slab_swmax, slab_accmax;
   int *d_slab_counters = nullptr;          // one per level
   int *d_dep_flags = nullptr;              // per dependency edge
   int *d_lu_flags = nullptr;               // per node
@@ -393,6 +393,7 @@ int hy_upload_slab_plan(hy_handle *h, const hy_slab_plan *d) {
   h->slab_smax.assign(d->level_smax, d->level_smax + d->nlevels);
   h->slab_mmax.assign(d->level_mmax, d->level_mmax + d->nlevels);
   h->slab_swmax.assign(d->level_swmax, d->level_swmax + d->nlevels);
+  h->slab_accmax.assign(d->level_accmax, d->level_accmax + d->nlevels);
   UPS(&h->d_slab_counters, (const int *)nullptr, d->nlevels + 1);
   UPS(&h->d_dep_flags, (const int *)nullptr, d->ndeps + 1);
   UPS(&h->d_lu_flags, (const int *)nullptr, h->S.nn);
@@ -401,7 +402,7 @@ int hy_upload_slab_plan(hy_handle *h, const hy_slab_plan *d) {
   size_t mx = 0;
   for (int64_t l = 0; l < d->nlevels; ++l) {
     if (d->level_slab_ptr[l + 1] == d->level_slab_ptr[l]) continue;
-    const size_t b = slab_smem_bytes(d->level_smax[l], d->level_mmax[l], d->level_swmax[l]);
+    const size_t b = slab_smem_bytes(d->level_smax[l], d->level_mmax[l], d->level_swmax[l], d->level_accmax[l]);
     if (b > mx) mx = b;
   }
   if (mx > 227 * 1024) return fail(HY_INVALID_ARGUMENT, "slab shared memory exceeds 227 KB");
@@ -459,10 +460,10 @@ static int run_factor(hy_handle *h, const double *d_avals, double eps, const hy_
     }
     if (ns && h->slab_ok) {
       const int nsl = (int)(h->slab_lptr[l + 1] - h->slab_lptr[l]);
-      const size_t smem = slab_smem_bytes(h->slab_smax[l], h->slab_mmax[l], h->slab_swmax[l]);
+      const size_t smem = slab_smem_bytes(h->slab_smax[l], h->slab_mmax[l], h->slab_swmax[l], h->slab_accmax[l]);
       k_slab<<<nsl, 256, smem, st>>>(h->S, P, h->slab, (int)h->slab_lptr[l], h->d_slab_counters + l,
                                      h->d_dep_flags, h->d_lu_flags, h->slab_epoch, h->slab_smax[l],
-                                     h->slab_mmax[l], h->slab_swmax[l]);
+                                     h->slab_mmax[l], h->slab_swmax[l], h->slab_accmax[l]);
       h->launches++;
       if (!P.refactor) {
         int maxL = 1;

@@ -50,7 +50,7 @@ __device__ __forceinline__ void st_rel(int *p, int v) {
 
 __global__ void __launch_bounds__(SLAB_THREADS, 1)
     k_slab(DevSym S, CallP P, SlabDev D, int slab_base, int *counter, int *dep_flags, int *lu_flags,
-           int epoch, int Smax, int Mmax, int SWmax) {
+           int epoch, int Smax, int Mmax, int SWmax, int ACCmax) {
   extern __shared__ __align__(16) double smd[];
   __shared__ int s_ticket;
   __shared__ int s_pinv[64];
@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(SLAB_THREADS, 1)
   double *F = P.F;
   double *Pm = F + S.valoff[u];
   double *acc = smd;                                         // s x sw (stride sw)
-  int32_t *tcol = reinterpret_cast<int32_t *>(acc + (size_t)Smax * SWmax);
+  int32_t *tcol = reinterpret_cast<int32_t *>(acc + (size_t)ACCmax);
   double *Xs = reinterpret_cast<double *>(tcol + ((SWmax + 1) & ~1));  // Smax x XLD
   double *Ut = Xs + (size_t)Smax * XLD;                      // max(Mmax, Smax) x XLD
   const double thr = P.eps * P.anorm[0];
@@ -359,9 +359,9 @@ __global__ void k_lperm(DevSym S, CallP P, const int32_t *sns, int count) {
   }
 }
 
-size_t slab_smem_bytes(int Smax, int Mmax, int SWmax) {
+size_t slab_smem_bytes(int Smax, int Mmax, int SWmax, int ACCmax) {
   const int urows = Mmax > Smax ? Mmax : Smax;
-  return (size_t)Smax * SWmax * sizeof(double) + (size_t)((SWmax + 1) & ~1) * sizeof(int32_t) +
+  return (size_t)ACCmax * sizeof(double) + (size_t)((SWmax + 1) & ~1) * sizeof(int32_t) +
          (size_t)(Smax + urows) * XLD * sizeof(double);
 }
 

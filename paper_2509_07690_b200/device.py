@@ -80,7 +80,7 @@ class SlabPlanDesc(ctypes.Structure):
         ("it_q0", ctypes.c_void_p), ("it_q1", ctypes.c_void_p), ("it_own", ctypes.c_void_p),
         ("dep_pb", ctypes.c_void_p), ("level_slab_ptr", ctypes.c_void_p),
         ("level_smax", ctypes.c_void_p), ("level_mmax", ctypes.c_void_p),
-        ("level_swmax", ctypes.c_void_p),
+        ("level_swmax", ctypes.c_void_p), ("level_accmax", ctypes.c_void_p),
     ]
 
 
@@ -213,6 +213,7 @@ class DeviceContext:
             level_smax=np.ascontiguousarray(need[:, 0], np.int32),
             level_mmax=np.ascontiguousarray(need[:, 1], np.int32),
             level_swmax=np.ascontiguousarray(need[:, 2], np.int32),
+            level_accmax=np.ascontiguousarray(need[:, 3], np.int32),
         )
         d = SlabPlanDesc()
         d.nslabs, d.nitems, d.ndeps = plan.nslabs, len(plan.it_k), len(dep_pb)

@@ -590,10 +590,10 @@ def _dep_block_pos(first, kind, colptr, cols, nl, dptr, deps):
 
 
 def slab_level_smem(sym, plan):
-    """(Smax, Mmax, SWmax) per level for the slab launch's dynamic shared memory."""
+    """(Smax, Mmax, SWmax, ACCmax) per level for the slab launch's shared memory."""
     s = sym
     nlev = len(plan.level_slab_ptr) - 1
-    out = np.zeros((nlev, 3), np.int64)
+    out = np.zeros((nlev, 4), np.int64)
     rows = np.diff(s.node_first)
     for lv in range(nlev):
         a, b = plan.level_slab_ptr[lv], plan.level_slab_ptr[lv + 1]
@@ -606,5 +606,5 @@ def slab_level_smem(sym, plan):
             d = s.deps[s.dep_ptr[u]:s.dep_ptr[u + 1]]
             if len(d):
                 mm = max(mm, int(rows[d].max()))
-        out[lv] = (int(rows[nodes].max()), mm, int(sw.max()))
+        out[lv] = (int(rows[nodes].max()), mm, int(sw.max()), int((rows[nodes] * sw).max()))
     return out
