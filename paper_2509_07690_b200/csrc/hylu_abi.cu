@@ -34,6 +34,16 @@ size_t pipe_smem_bytes(bool staged);
 __global__ void k_bhat(DevSym, const int32_t *, const double *, double *);
 __global__ void k_xout(DevSym, const double *, double *);
 __global__ void k_fwd(DevSym, const double *, const int32_t *, int, double *);
+struct SolveChunk {
+  int32_t node;
+  int32_t c0, c1;
+  int32_t slot;
+};
+__global__ void k_solve_part(DevSym, const double *, const SolveChunk *, int, const double *, double *, int);
+__global__ void k_fwd_fin(DevSym, const double *, const int32_t *, const int32_t *, const int32_t *, int,
+                          const double *, double *);
+__global__ void k_bwd_fin(DevSym, const double *, const int32_t *, const int32_t *, const int32_t *, int,
+                          const double *, double *);
 __global__ void k_bwd(DevSym, const double *, const int32_t *, int, double *);
 template <bool STAGED>
 __global__ void k_bt_pipe(DevSym, BatchP, DevProg, const int2 *, int64_t, const double *, double *, int *, int *,
@@ -73,11 +83,22 @@ struct Plan {
   int32_t *d_all = nullptr;
 };
 
+// Chunked-substitution plan for one direction: per level, chunk list and per-node
+// slot ranges (nodes in the same order as the level plan's d_all list).
+struct SolvePlan {
+  std::vector<int64_t> cptr;         // [nlev+1] chunk offsets
+  SolveChunk *d_chunks = nullptr;
+  int32_t *d_slot0 = nullptr, *d_nslot = nullptr;  // per node in level order
+  int64_t nslots = 0;
+};
+
 struct hy_handle {
   int device = 0;
   DevSym S{};
   std::vector<void *> allocs;
   Plan fplan, bplan;
+  SolvePlan fsolve, bsolve;
+  double *d_solve_scratch = nullptr;
   int64_t stored = 0;
   bool uploaded = false;
   double *d_y = nullptr;          // single-solve workspace [n]
@@ -360,6 +381,45 @@ int hy_upload_symbolic(hy_handle *h, const hy_symbolic_desc *d) {
   rc = build_plan(h, h->bplan, d->ulevel_ptr, d->ulevel_nodes, d->nulevels, d->node_kind);
   if (rc) return rc;
   {
+    // chunked substitution plans (forward: L part [0, L); backward: panel [L+s, W))
+    const int CH = 4096;
+    for (int dir = 0; dir < 2; ++dir) {
+      const int64_t *lp = dir == 0 ? d->level_ptr : d->ulevel_ptr;
+      const int32_t *ln = dir == 0 ? d->level_nodes : d->ulevel_nodes;
+      const int64_t nlev = dir == 0 ? d->nlevels : d->nulevels;
+      SolvePlan &sp = dir == 0 ? h->fsolve : h->bsolve;
+      std::vector<SolveChunk> chunks;
+      std::vector<int32_t> slot0, nslot;
+      sp.cptr.assign(nlev + 1, 0);
+      int64_t maxslots = 0;
+      for (int64_t l = 0; l < nlev; ++l) {
+        int32_t slot = 0;
+        for (int64_t k = lp[l]; k < lp[l + 1]; ++k) {
+          const int32_t u = ln[k];
+          const int64_t s = d->node_first[u + 1] - d->node_first[u];
+          const int64_t W = d->colptr[u + 1] - d->colptr[u];
+          const int64_t lo = dir == 0 ? 0 : d->nl[u] + s, hi = dir == 0 ? d->nl[u] : W;
+          slot0.push_back(slot);
+          int32_t ns = 0;
+          for (int64_t c = lo; c < hi; c += CH) {
+            chunks.push_back(SolveChunk{u, (int32_t)c, (int32_t)(c + CH < hi ? c + CH : hi), slot + ns});
+            ++ns;
+          }
+          nslot.push_back(ns);
+          slot += ns;
+        }
+        sp.cptr[l + 1] = (int64_t)chunks.size();
+        if (slot > maxslots) maxslots = slot;
+      }
+      sp.nslots = maxslots;
+      UP(&sp.d_chunks, chunks.data(), chunks.size());
+      UP(&sp.d_slot0, slot0.data(), slot0.size());
+      UP(&sp.d_nslot, nslot.data(), nslot.size());
+    }
+    const int64_t ns = (h->fsolve.nslots > h->bsolve.nslots ? h->fsolve.nslots : h->bsolve.nslots);
+    UP(&h->d_solve_scratch, (const double *)nullptr, (ns > 0 ? ns : 1) * 64);
+  }
+  {
     std::vector<int32_t> lev(nn, 0);
     for (int64_t l = 0; l < d->nlevels; ++l)
       for (int64_t k = d->level_ptr[l]; k < d->level_ptr[l + 1]; ++k) lev[d->level_nodes[k]] = (int32_t)l;
@@ -394,6 +454,23 @@ int hy_upload_slab_plan(hy_handle *h, const hy_slab_plan *d) {
   h->slab_mmax.assign(d->level_mmax, d->level_mmax + d->nlevels);
   h->slab_swmax.assign(d->level_swmax, d->level_swmax + d->nlevels);
   h->slab_accmax.assign(d->level_accmax, d->level_accmax + d->nlevels);
+  // re-split the factorization level plan: slab targets -> slab list, others -> rows
+  {
+    std::vector<uint8_t> isslab(h->S.nn, 0);
+    for (int64_t k = 0; k < d->nslabs; ++k) isslab[d->sl_node[k]] = 1;
+    Plan &pl = h->fplan;
+    std::vector<int32_t> all(pl.aptr[pl.nlev]);
+    if (!all.empty())
+      CK(cudaMemcpy(all.data(), pl.d_all, sizeof(int32_t) * all.size(), cudaMemcpyDeviceToHost));
+    std::vector<int32_t> rows, sns;
+    for (int l = 0; l < pl.nlev; ++l) {
+      for (int64_t k = pl.aptr[l]; k < pl.aptr[l + 1]; ++k) (isslab[all[k]] ? sns : rows).push_back(all[k]);
+      pl.rptr[l + 1] = (int64_t)rows.size();
+      pl.sptr[l + 1] = (int64_t)sns.size();
+    }
+    UPS(&pl.d_rows, rows.data(), rows.size());
+    UPS(&pl.d_sns, sns.data(), sns.size());
+  }
   UPS(&h->d_slab_counters, (const int *)nullptr, d->nlevels + 1);
   UPS(&h->d_dep_flags, (const int *)nullptr, d->ndeps + 1);
   UPS(&h->d_lu_flags, (const int *)nullptr, h->S.nn);
@@ -501,15 +578,27 @@ int hy_solve(hy_handle *h, const hy_factors *f, const double *d_b, double *d_x, 
   const int n = h->S.n;
   k_bhat<<<(n + 255) / 256, 256, 0, st>>>(h->S, f->d_inner_perm, d_b, h->d_y);
   h->launches++;
-  for (int l = 0; l < h->fplan.nlev; ++l) {
-    const int c = (int)(h->fplan.aptr[l + 1] - h->fplan.aptr[l]);
-    k_fwd<<<(c + 3) / 4, 128, 0, st>>>(h->S, f->d_values, h->fplan.d_all + h->fplan.aptr[l], c, h->d_y);
-    h->launches++;
-  }
-  for (int l = 0; l < h->bplan.nlev; ++l) {
-    const int c = (int)(h->bplan.aptr[l + 1] - h->bplan.aptr[l]);
-    k_bwd<<<(c + 3) / 4, 128, 0, st>>>(h->S, f->d_values, h->bplan.d_all + h->bplan.aptr[l], c, h->d_y);
-    h->launches++;
+  for (int dir = 0; dir < 2; ++dir) {
+    const Plan &pl = dir == 0 ? h->fplan : h->bplan;
+    const SolvePlan &sp = dir == 0 ? h->fsolve : h->bsolve;
+    for (int l = 0; l < pl.nlev; ++l) {
+      const int c = (int)(pl.aptr[l + 1] - pl.aptr[l]);
+      const int nch = (int)(sp.cptr[l + 1] - sp.cptr[l]);
+      if (nch) {
+        k_solve_part<<<nch, 256, 0, st>>>(h->S, f->d_values, sp.d_chunks + sp.cptr[l], nch, h->d_y,
+                                         h->d_solve_scratch, dir == 0);
+        h->launches++;
+      }
+      if (dir == 0)
+        k_fwd_fin<<<(c + 3) / 4, 128, 0, st>>>(h->S, f->d_values, pl.d_all + pl.aptr[l],
+                                               sp.d_slot0 + pl.aptr[l], sp.d_nslot + pl.aptr[l], c,
+                                               h->d_solve_scratch, h->d_y);
+      else
+        k_bwd_fin<<<(c + 3) / 4, 128, 0, st>>>(h->S, f->d_values, pl.d_all + pl.aptr[l],
+                                               sp.d_slot0 + pl.aptr[l], sp.d_nslot + pl.aptr[l], c,
+                                               h->d_solve_scratch, h->d_y);
+      h->launches++;
+    }
   }
   k_xout<<<(n + 255) / 256, 256, 0, st>>>(h->S, h->d_y, d_x);
   h->launches++;

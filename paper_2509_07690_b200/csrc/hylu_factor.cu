@@ -498,4 +498,109 @@ __global__ void k_bwd(DevSym S, const double *F, const int32_t *nodes, int count
   if (lane + 32 < s) y[r + lane + 32] = mine1;
 }
 
+// ---------------------------------------------------------------------------
+// Chunked substitution: per level, (node, column chunk) partial dot products of
+// every row of the node over its off-block part (L-union for forward, panel for
+// backward), written to a scratch slot; then one warp per node combines the chunk
+// partials in slot order and runs the in-block triangular solve.
+struct SolveChunk {
+  int32_t node;
+  int32_t c0, c1;     // column positions [c0, c1) within the node's list
+  int32_t slot;       // scratch slot (x 64 rows)
+};
+
+__global__ void k_solve_part(DevSym S, const double *F, const SolveChunk *ch, int count,
+                             const double *y, double *scratch, int fwd) {
+  const int j = blockIdx.x;
+  if (j >= count) return;
+  const SolveChunk c = ch[j];
+  const int u = c.node;
+  const int r = (int)S.first[u];
+  const int s = (int)(S.first[u + 1] - r);
+  const int64_t cp = S.colptr[u];
+  const int W = (int)(S.colptr[u + 1] - cp);
+  const double *Fu = F + S.valoff[u];
+  const int32_t *cc = S.cols + cp;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int t = warp; t < s; t += nw) {
+    const double *row = Fu + (int64_t)t * W;
+    double acc = 0.0;
+    for (int q = c.c0 + lane; q < c.c1; q += 32) acc += row[q] * y[cc[q]];
+    acc = warp_sum(acc);
+    if (lane == 0) scratch[(int64_t)c.slot * 64 + t] = acc;
+  }
+}
+
+// forward finish: y_t = y_t - sum(chunk partials) - sum_{tt<t} L[t][tt] y_tt
+__global__ void k_fwd_fin(DevSym S, const double *F, const int32_t *nodes, const int32_t *slot0,
+                          const int32_t *nslot, int count, const double *scratch, double *y) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int idx = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (idx >= count) return;
+  const int u = nodes[idx];
+  const int r = (int)S.first[u];
+  const int s = (int)(S.first[u + 1] - r);
+  const int W = (int)(S.colptr[u + 1] - S.colptr[u]);
+  const int L = S.nl[u];
+  const double *Fu = F + S.valoff[u];
+  const int a0 = slot0[idx], an = nslot[idx];
+  double mine0 = 0.0, mine1 = 0.0;
+  if (lane < s) {
+    double acc = y[r + lane];
+    for (int k = 0; k < an; ++k) acc -= scratch[(int64_t)(a0 + k) * 64 + lane];
+    mine0 = acc;
+  }
+  if (lane + 32 < s) {
+    double acc = y[r + lane + 32];
+    for (int k = 0; k < an; ++k) acc -= scratch[(int64_t)(a0 + k) * 64 + lane + 32];
+    mine1 = acc;
+  }
+  for (int tt = 0; tt < s; ++tt) {
+    const double ytt = __shfl_sync(HY_FULL, tt < 32 ? mine0 : mine1, tt & 31);
+    const int t0 = lane, t1 = lane + 32;
+    if (t0 > tt && t0 < s) mine0 -= Fu[(int64_t)t0 * W + L + tt] * ytt;
+    if (t1 > tt && t1 < s) mine1 -= Fu[(int64_t)t1 * W + L + tt] * ytt;
+  }
+  if (lane < s) y[r + lane] = mine0;
+  if (lane + 32 < s) y[r + lane + 32] = mine1;
+}
+
+// backward finish: z_t = (y_t - sum(partials) - sum_{tt>t} U[t][tt] z_tt) / U[t][t]
+__global__ void k_bwd_fin(DevSym S, const double *F, const int32_t *nodes, const int32_t *slot0,
+                          const int32_t *nslot, int count, const double *scratch, double *y) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int idx = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (idx >= count) return;
+  const int u = nodes[idx];
+  const int r = (int)S.first[u];
+  const int s = (int)(S.first[u + 1] - r);
+  const int W = (int)(S.colptr[u + 1] - S.colptr[u]);
+  const int L = S.nl[u];
+  const double *Fu = F + S.valoff[u];
+  const int a0 = slot0[idx], an = nslot[idx];
+  double mine0 = 0.0, mine1 = 0.0;
+  if (lane < s) {
+    double acc = y[r + lane];
+    for (int k = 0; k < an; ++k) acc -= scratch[(int64_t)(a0 + k) * 64 + lane];
+    mine0 = acc;
+  }
+  if (lane + 32 < s) {
+    double acc = y[r + lane + 32];
+    for (int k = 0; k < an; ++k) acc -= scratch[(int64_t)(a0 + k) * 64 + lane + 32];
+    mine1 = acc;
+  }
+  for (int tt = s - 1; tt >= 0; --tt) {
+    const double d = Fu[(int64_t)tt * W + L + tt];
+    if (lane == (tt & 31)) {
+      if (tt < 32) mine0 /= d; else mine1 /= d;
+    }
+    const double ztt = __shfl_sync(HY_FULL, tt < 32 ? mine0 : mine1, tt & 31);
+    const int t0 = lane, t1 = lane + 32;
+    if (t0 < tt) mine0 -= Fu[(int64_t)t0 * W + L + tt] * ztt;
+    if (t1 < tt) mine1 -= Fu[(int64_t)t1 * W + L + tt] * ztt;
+  }
+  if (lane < s) y[r + lane] = mine0;
+  if (lane + 32 < s) y[r + lane + 32] = mine1;
+}
+
 }  // namespace hy

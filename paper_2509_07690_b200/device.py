@@ -185,16 +185,19 @@ class DeviceContext:
         self.stored = int(self.lib.hy_stored_values(self.h))
         self.n = s.n
         self.nnz = A.nnz
-        if s.supernode_count:
+        from . import schedule as _sc
+        self.wide_row = int(os.environ.get("HYLU_WIDE_ROW", _sc.WIDE_ROW))
+        if _sc.slab_nodes(s, self.wide_row).any():
             self.upload_slab_plan()
 
     def upload_slab_plan(self):
         from . import schedule
         s = self.analysis.symbolic
         plan = getattr(s, "_slab_plan", None)
-        if plan is None:
-            plan = schedule.build_slab_plan(s)
+        if plan is None or getattr(s, "_slab_wide", None) != self.wide_row:
+            plan = schedule.build_slab_plan(s, wide_row=self.wide_row)
             s._slab_plan = plan
+            s._slab_wide = self.wide_row
         need = schedule.slab_level_smem(s, plan)
         dep_pb = schedule._dep_block_pos(s.node_first, s.node_kind, s.colptr, s.cols, s.nl,
                                          s.dep_ptr, s.deps)

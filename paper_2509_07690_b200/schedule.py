@@ -400,7 +400,7 @@ def _lower_bound(a, lo, hi, key):
 
 
 @njit(cache=True)
-def _slab_plan(first, kind, colptr, cols, nl, dptr, deps, node_of, level, budget, cap):
+def _slab_plan(first, kind, colptr, cols, nl, dptr, deps, node_of, level, budget, cap, slab_node):
     """Column slabs of every supernode target and, per slab, the ascending list of
     source steps that touch it (or whose block it owns).
 
@@ -422,7 +422,7 @@ def _slab_plan(first, kind, colptr, cols, nl, dptr, deps, node_of, level, budget
     sn_nslab = np.zeros(nn, np.int64)
     sn_bslab = np.full(nn, -1, np.int64)
     for u in range(nn):
-        if kind[u] != 1:
+        if slab_node[u] == 0:
             continue
         r = first[u]
         s = first[u + 1] - r
@@ -542,13 +542,27 @@ class SlabPlan:
         return len(self.sl_node)
 
 
-def build_slab_plan(sym, budget=SLAB_BUDGET, cap=SLAB_COLS):
+WIDE_ROW = 1024
+
+
+def slab_nodes(sym, wide_row=WIDE_ROW):
+    """Nodes processed by the slab kernel: every supernode and, in SUPROW/SUPSUP
+    modes, standalone rows wider than ``wide_row`` (their supernode sources are
+    sup-row updates, i.e. block updates of a 1-row target)."""
+    m = (sym.node_kind == 1).astype(np.uint8)
+    if int(sym.kernel_mode) >= 1:
+        m |= ((sym.node_kind == 0) & (np.diff(sym.colptr) > wide_row)).astype(np.uint8)
+    return m
+
+
+def build_slab_plan(sym, budget=SLAB_BUDGET, cap=SLAB_COLS, wide_row=WIDE_ROW):
     """Slabs in factorization-level order (so one launch per level covers a
     contiguous slab-id range, targets ascending, slabs ascending within a target)."""
     s = sym
+    mask = slab_nodes(s, wide_row)
     (sl_node, sl_c0, sl_c1, sl_kind, it_ptr, it_k, it_q0, it_q1, it_own, sn_slab0, sn_nslab,
      sn_bslab) = _slab_plan(s.node_first, s.node_kind, s.colptr, s.cols, s.nl, s.dep_ptr, s.deps,
-                            s.node_of, s.level, budget, cap)
+                            s.node_of, s.level, budget, cap, mask)
     # reorder slabs by (level, node, slab) — nodes ascending already; stable sort on level
     lev = s.level[sl_node] if len(sl_node) else np.zeros(0, np.int64)
     order = np.argsort(lev, kind="stable")

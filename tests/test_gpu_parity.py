@@ -47,6 +47,23 @@ def test_factorize_matches_oracle(name, mode):
     assert _rel(x, xo) <= 1e-9
 
 
+@pytest.mark.parametrize("name", ["c0", "c2", "c3"])
+@pytest.mark.parametrize("mode", [1, 2])
+def test_wide_rows_on_slab_path(name, mode, monkeypatch):
+    """Standalone rows routed to the column-slab kernel (tiny threshold, tiny slabs)."""
+    monkeypatch.setenv("HYLU_WIDE_ROW", "4")
+    p, an = _analysis(name, mode)
+    on = _oracle()
+    ref = on.factorize(an)
+    f = api.factorize_analysis(an)
+    assert np.array_equal(f.host_inner_perm(), ref.inner_perm)
+    assert _rel(f.host_values(), ref.values) <= LU_RTOL
+    x, _ = api.solve(p.A, f, b=p.b)
+    assert np.linalg.norm(refmatrix.spmv(p.A, x) - p.b) / np.linalg.norm(p.b) <= RES_TOL
+    f2 = api.refactorize(p.A, f)
+    assert np.array_equal(f2.host_values(), f.host_values())
+
+
 @pytest.mark.parametrize("name", ["c0", "c1", "c3"])
 def test_refactorize_matches_oracle(name):
     p, an = _analysis(name)
