@@ -136,6 +136,22 @@ typedef struct {
 } hy_slab_plan;
 int hy_upload_slab_plan(hy_handle *h, const hy_slab_plan *plan);
 
+/* Level fan-in plan (schedule.build_fanin_plan), used in SUPROW / SUPSUP modes:
+ * per level, the nodes to factor, their permutation / TRSM tiles, the dependency
+ * edges leaving the level (multiplier blocks) and the (target, column tile)
+ * update items with their source lists. */
+typedef struct {
+  int64_t nlevels, nsrc, ndeps;
+  const int64_t *lu_ptr;  const int32_t *lu_nodes;                 /* [nlevels+1], [nnodes] */
+  const int64_t *pt_ptr;  const int32_t *pt_node, *pt_c0, *pt_c1;  /* tiles */
+  const int64_t *xp_ptr;  const int64_t *xp_edge; const int32_t *xp_tgt;
+  const int64_t *lev_up;  const int32_t *up_t, *up_c0, *up_c1; const int64_t *up_ptr;
+  const int32_t *src_k, *src_q0, *src_q1;                          /* [nsrc] */
+  const int32_t *dep_pb;                                           /* [ndeps] */
+  const int32_t *level_smax, *level_mmax;                          /* [nlevels] */
+} hy_fanin_plan;
+int hy_upload_fanin_plan(hy_handle *h, const hy_fanin_plan *plan);
+
 /* Row programs for the batched path (built on the host by schedule.py for a given
  * prior inner_perm).  Must be uploaded before the
  * batched calls, and must match the inner_perm of the prior they are used with. */

@@ -30,6 +30,28 @@ struct SlabDev {
 __global__ void k_slab(DevSym, CallP, SlabDev, int, int *, int *, int *, int, int, int, int, int);
 __global__ void k_lperm(DevSym, CallP, const int32_t *, int);
 size_t slab_smem_bytes(int, int, int, int);
+struct FaninDev {
+  const int32_t *lu_nodes;
+  const int32_t *pt_node;
+  const int32_t *pt_c0;
+  const int32_t *pt_c1;
+  const int64_t *xp_edge;
+  const int32_t *xp_tgt;
+  const int32_t *up_t;
+  const int32_t *up_c0;
+  const int32_t *up_c1;
+  const int64_t *up_ptr;
+  const int32_t *src_k;
+  const int32_t *src_q0;
+  const int32_t *src_q1;
+  const int32_t *dep_pb;
+};
+__global__ void k_fi_scatter(DevSym, CallP);
+__global__ void k_fi_lu(DevSym, CallP, FaninDev, int);
+__global__ void k_fi_panel(DevSym, CallP, FaninDev, int);
+__global__ void k_fi_x(DevSym, CallP, FaninDev, int);
+__global__ void k_fi_upd(DevSym, CallP, FaninDev, int, int, int);
+size_t fi_upd_smem(int, int);
 size_t pipe_smem_bytes(bool staged);
 __global__ void k_bhat(DevSym, const int32_t *, const double *, double *);
 __global__ void k_xout(DevSym, const double *, double *);
@@ -148,6 +170,12 @@ struct hy_handle {
   int *d_dep_flags = nullptr;              // per dependency edge
   int *d_lu_flags = nullptr;               // per node
   int slab_epoch = 0;
+  // level fan-in plan (SUPROW / SUPSUP modes)
+  bool fanin_ok = false;
+  FaninDev fi{};
+  std::vector<void *> fi_allocs;
+  std::vector<int64_t> fi_lu, fi_pt, fi_xp, fi_up;   // per-level offsets
+  std::vector<int32_t> fi_smax, fi_mmax;
 };
 
 static void free_segments(hy_handle *h);
@@ -263,6 +291,22 @@ static int upload_slab(hy_handle *h, T **dst, const T *src, int64_t count) {
     if (_r) return _r;                                     \
   } while (0)
 
+template <class T>
+static int upload_fi(hy_handle *h, T **dst, const T *src, int64_t count) {
+  *dst = nullptr;
+  if (count <= 0) return HY_OK;
+  CK(cudaMalloc((void **)dst, sizeof(T) * count));
+  h->fi_allocs.push_back(*dst);
+  CK(cudaMemcpy(*dst, src, sizeof(T) * count, cudaMemcpyHostToDevice));
+  return HY_OK;
+}
+
+#define UPF(dst, src, cnt)                                 \
+  do {                                                     \
+    int _r = upload_fi(h, dst, src, (int64_t)(cnt));       \
+    if (_r) return _r;                                     \
+  } while (0)
+
 extern "C" {
 
 const char *hy_last_error(void) { return g_err.c_str(); }
@@ -298,6 +342,7 @@ void hy_destroy(hy_handle *h) {
   for (void *p : h->allocs) cudaFree(p);
   for (void *p : h->prog_allocs) cudaFree(p);
   for (void *p : h->slab_allocs) cudaFree(p);
+  for (void *p : h->fi_allocs) cudaFree(p);
   if (h->d_bf) cudaFree(h->d_bf);
   if (h->d_scratch) cudaFree(h->d_scratch);
   if (h->d_flags) cudaFree(h->d_flags);
@@ -489,6 +534,75 @@ int hy_upload_slab_plan(hy_handle *h, const hy_slab_plan *d) {
   return HY_OK;
 }
 
+int hy_upload_fanin_plan(hy_handle *h, const hy_fanin_plan *d) {
+  if (!h || !h->uploaded || !d) return fail(HY_INVALID_ARGUMENT, "symbolic not uploaded / null");
+  if (d->nlevels != h->fplan.nlev) return fail(HY_DIMENSION_MISMATCH, "fan-in plan level count mismatch");
+  CK(cudaSetDevice(h->device));
+  for (void *p : h->fi_allocs) cudaFree(p);
+  h->fi_allocs.clear();
+  const int64_t nl = d->nlevels;
+  FaninDev &D = h->fi;
+  int32_t *p32;
+  int64_t *p64;
+  UPF(&p32, d->lu_nodes, d->lu_ptr[nl]); D.lu_nodes = p32;
+  UPF(&p32, d->pt_node, d->pt_ptr[nl]); D.pt_node = p32;
+  UPF(&p32, d->pt_c0, d->pt_ptr[nl]); D.pt_c0 = p32;
+  UPF(&p32, d->pt_c1, d->pt_ptr[nl]); D.pt_c1 = p32;
+  UPF(&p64, d->xp_edge, d->xp_ptr[nl]); D.xp_edge = p64;
+  UPF(&p32, d->xp_tgt, d->xp_ptr[nl]); D.xp_tgt = p32;
+  UPF(&p32, d->up_t, d->lev_up[nl]); D.up_t = p32;
+  UPF(&p32, d->up_c0, d->lev_up[nl]); D.up_c0 = p32;
+  UPF(&p32, d->up_c1, d->lev_up[nl]); D.up_c1 = p32;
+  UPF(&p64, d->up_ptr, d->lev_up[nl] + 1); D.up_ptr = p64;
+  UPF(&p32, d->src_k, d->nsrc); D.src_k = p32;
+  UPF(&p32, d->src_q0, d->nsrc); D.src_q0 = p32;
+  UPF(&p32, d->src_q1, d->nsrc); D.src_q1 = p32;
+  UPF(&p32, d->dep_pb, d->ndeps); D.dep_pb = p32;
+  h->fi_lu.assign(d->lu_ptr, d->lu_ptr + nl + 1);
+  h->fi_pt.assign(d->pt_ptr, d->pt_ptr + nl + 1);
+  h->fi_xp.assign(d->xp_ptr, d->xp_ptr + nl + 1);
+  h->fi_up.assign(d->lev_up, d->lev_up + nl + 1);
+  h->fi_smax.assign(d->level_smax, d->level_smax + nl);
+  h->fi_mmax.assign(d->level_mmax, d->level_mmax + nl);
+  size_t mx = 0;
+  for (int64_t l = 0; l < nl; ++l) {
+    const size_t b = fi_upd_smem(h->fi_smax[l], h->fi_mmax[l]);
+    if (b > mx) mx = b;
+  }
+  CK(cudaFuncSetAttribute(k_fi_upd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx));
+  CK(cudaFuncSetAttribute(k_fi_panel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)(64 * 256 * sizeof(double))));
+  CK(cudaFuncSetAttribute(k_fi_x, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)(2 * 64 * 65 * sizeof(double))));
+  h->fanin_ok = true;
+  return HY_OK;
+}
+
+static int run_fanin(hy_handle *h, const CallP &P, cudaStream_t st) {
+  CK(cudaMemsetAsync(P.F, 0, sizeof(double) * h->stored, st));
+  k_fi_scatter<<<(h->S.n * 32 + 255) / 256, 256, 0, st>>>(h->S, P);
+  h->launches++;
+  for (int l = 0; l < h->fplan.nlev; ++l) {
+    const int nlu = (int)(h->fi_lu[l + 1] - h->fi_lu[l]);
+    const int npt = (int)(h->fi_pt[l + 1] - h->fi_pt[l]);
+    const int nxp = (int)(h->fi_xp[l + 1] - h->fi_xp[l]);
+    const int nup = (int)(h->fi_up[l + 1] - h->fi_up[l]);
+    if (nlu) { k_fi_lu<<<nlu, 256, 0, st>>>(h->S, P, h->fi, (int)h->fi_lu[l]); h->launches++; }
+    if (npt) {
+      k_fi_panel<<<npt, 256, 64 * 256 * sizeof(double), st>>>(h->S, P, h->fi, (int)h->fi_pt[l]);
+      h->launches++;
+    }
+    if (nxp) { k_fi_x<<<nxp, 256, 2 * 64 * 65 * sizeof(double), st>>>(h->S, P, h->fi, (int)h->fi_xp[l]); h->launches++; }
+    if (nup) {
+      k_fi_upd<<<nup, 256, fi_upd_smem(h->fi_smax[l], h->fi_mmax[l]), st>>>(
+          h->S, P, h->fi, (int)h->fi_up[l], h->fi_smax[l], h->fi_mmax[l]);
+      h->launches++;
+    }
+  }
+  CK(cudaGetLastError());
+  return HY_OK;
+}
+
 static int run_factor(hy_handle *h, const double *d_avals, double eps, const hy_factors *prior,
                       hy_factors *out, cudaStream_t st) {
   if (!h || !h->uploaded) return fail(HY_INVALID_ARGUMENT, "symbolic not uploaded");
@@ -523,6 +637,7 @@ static int run_factor(hy_handle *h, const double *d_avals, double eps, const hy_
     k_anorm<<<296, 256, 0, st>>>(d_avals, h->S.scale, h->S.nnz, out->d_anorm);
     h->launches++;
   }
+  if (h->fanin_ok && h->S.mode >= 1) return run_fanin(h, P, st);
   const Plan &pl = h->fplan;
   if (h->slab_ok) {
     h->slab_epoch++;

@@ -1,0 +1,355 @@
+// hylu_fanin.cu — level-synchronous fan-in supernodal factorization (SUPROW /
+// SUPSUP modes, single instance).
+//
+// Every node (supernode or standalone row) is a dense rows x W block in node
+// layout.  All A values are scattered once (k_fi_scatter).  Then, per level ℓ of
+// the elimination DAG:
+//   k_fi_lu    — each node finishing at ℓ has received every update: in-block LU
+//                with pivoting restricted to the diagonal block
+//                and pivot perturbation; standalone rows only
+//                perturb their pivot.
+//   k_fi_panel — row permutation of the node's other columns and the unit-lower
+//                TRSM of its panel (U_panel = L_bb⁻¹ P·panel), tile-parallel.
+//   k_fi_x     — for every edge (T, v) with v at level ℓ: the multiplier block
+//                X = T[:, blk_v] · U_vv⁻¹ (the sup-row / sup-sup TRSM with the
+//                source's upper, non-unit block), in place: these
+//                are T's final L values.
+//   k_fi_upd   — per (target T, 64-column tile): T[:, tile] -= Σ_v X_{T,v} ·
+//                U_v[:, tile] over the level's sources v of T, accumulated in
+//                shared memory (K-aggregated across sources) and written once.
+// Sources finishing at the same level never touch each other's block columns
+// (that would make one depend on the other), so all X blocks of a level are
+// independent, and each target column receives its updates in ascending level
+// order — the up-looking dependency order.  Supernode sources act as blocks in
+// these modes (sup-row for row targets, sup-sup for supernode targets); the
+// result differs from per-row application only in summation order.
+#include "hylu_common.cuh"
+
+namespace hy {
+
+struct FaninDev {
+  const int32_t *lu_nodes;   // nodes by level
+  const int32_t *pt_node;    // perm / TRSM tiles
+  const int32_t *pt_c0;
+  const int32_t *pt_c1;
+  const int64_t *xp_edge;    // X pairs: dependency edge index (target given by xp_tgt)
+  const int32_t *xp_tgt;
+  const int32_t *up_t;       // update items
+  const int32_t *up_c0;
+  const int32_t *up_c1;
+  const int64_t *up_ptr;
+  const int32_t *src_k;
+  const int32_t *src_q0;
+  const int32_t *src_q1;
+  const int32_t *dep_pb;
+};
+
+constexpr int FI_THREADS = 256;
+constexpr int FXLD = 65;
+
+// ---------------------------------------------------------------------------- scatter
+// warp per M row: physical row = inverse of the prior inner_perm on refactorize
+__global__ void k_fi_scatter(DevSym S, CallP P) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= S.n) return;
+  const int i = warp;
+  const int u = S.node_of[i];
+  const int r = (int)S.first[u];
+  const int s = (int)(S.first[u + 1] - r);
+  const int W = (int)(S.colptr[u + 1] - S.colptr[u]);
+  int t = i - r;
+  int prow = t;
+  if (P.refactor && s > 1) {
+    // physical row p holds M row r + iperm[r+p]; find p with iperm[r+p] == t
+    const int a0 = lane < s ? P.iperm_prior[r + lane] : -1;
+    const int a1 = lane + 32 < s ? P.iperm_prior[r + lane + 32] : -1;
+    const unsigned m0 = __ballot_sync(HY_FULL, a0 == t), m1 = __ballot_sync(HY_FULL, a1 == t);
+    prow = m0 ? __ffs(m0) - 1 : 32 + __ffs(m1) - 1;
+  }
+  double *row = P.F + S.valoff[u] + (int64_t)prow * W;
+  const int64_t a = S.mrow_src[i];
+  for (int64_t e = S.a_ptr[a] + lane; e < S.a_ptr[a + 1]; e += 32) row[S.colpos[e]] = P.A[e] * S.scale[e];
+}
+
+// ---------------------------------------------------------------------------- LU
+__global__ void __launch_bounds__(FI_THREADS) k_fi_lu(DevSym S, CallP P, FaninDev D, int base) {
+  __shared__ double B[64 * FXLD];
+  __shared__ int perm[64];
+  const int u = D.lu_nodes[base + blockIdx.x];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int r = (int)S.first[u];
+  const int s = (int)(S.first[u + 1] - r);
+  const int W = (int)(S.colptr[u + 1] - S.colptr[u]);
+  const int L = S.nl[u];
+  double *Pm = P.F + S.valoff[u];
+  const double thr = P.eps * P.anorm[0];
+  if (s == 1) {
+    if (tid == 0) {
+      const double piv = Pm[L];
+      bool fired;
+      Pm[L] = perturb(piv, thr, fired);
+      log_pivot(P, r, piv, fired, thr);
+      P.iperm[r] = 0;
+    }
+    return;
+  }
+  for (int idx = tid; idx < s * s; idx += FI_THREADS) {
+    const int t = idx / s, a = idx - t * s;
+    B[t * FXLD + a] = Pm[(int64_t)t * W + L + a];
+  }
+  if (tid < s) perm[tid] = tid;
+  __syncthreads();
+  for (int t = 0; t < s; ++t) {
+    if (!P.refactor && warp == 0) {
+      double best = -1.0;
+      int bi = s;
+      for (int q = t + lane; q < s; q += 32) {
+        const double av = fabs(B[q * FXLD + t]);
+        if (av > best) { best = av; bi = q; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(HY_FULL, best, o);
+        const int oi = __shfl_xor_sync(HY_FULL, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (bi != t && bi < s) {
+        for (int c = lane; c < s; c += 32) {
+          const double tmp = B[t * FXLD + c];
+          B[t * FXLD + c] = B[bi * FXLD + c];
+          B[bi * FXLD + c] = tmp;
+        }
+        if (lane == 0) {
+          const int tp = perm[t];
+          perm[t] = perm[bi];
+          perm[bi] = tp;
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      const double piv = B[t * FXLD + t];
+      bool fired;
+      B[t * FXLD + t] = perturb(piv, thr, fired);
+      log_pivot(P, r + t, piv, fired, thr);
+    }
+    __syncthreads();
+    const double pv = B[t * FXLD + t];
+    for (int q = t + 1 + tid; q < s; q += FI_THREADS) B[q * FXLD + t] /= pv;
+    __syncthreads();
+    const int rem = s - t - 1;
+    for (int idx = tid; idx < rem * rem; idx += FI_THREADS) {
+      const int q = t + 1 + idx / rem, c = t + 1 + idx % rem;
+      B[q * FXLD + c] -= B[q * FXLD + t] * B[t * FXLD + c];
+    }
+    __syncthreads();
+  }
+  for (int idx = tid; idx < s * s; idx += FI_THREADS) {
+    const int t = idx / s, a = idx - t * s;
+    Pm[(int64_t)t * W + L + a] = B[t * FXLD + a];
+  }
+  if (tid < s) P.iperm[r + tid] = P.refactor ? P.iperm_prior[r + tid] : perm[tid];
+}
+
+// ---------------------------------------------------------------------------- panel
+// Tile of node v's columns [c0, c1) outside the block: apply the pivot row
+// permutation (factorize only) and, for panel tiles, the unit-lower TRSM.
+__global__ void __launch_bounds__(FI_THREADS) k_fi_panel(DevSym S, CallP P, FaninDev D, int base) {
+  extern __shared__ __align__(16) double tl[];   // s x (c1-c0), stride PANEL
+  __shared__ double Lb[64 * FXLD];
+  __shared__ int perm[64];
+  __shared__ int ident;
+  const int j = base + blockIdx.x;
+  const int u = D.pt_node[j];
+  const int c0 = D.pt_c0[j], c1 = D.pt_c1[j];
+  const int tw = c1 - c0;
+  const int tid = threadIdx.x;
+  const int r = (int)S.first[u];
+  const int s = (int)(S.first[u + 1] - r);
+  const int W = (int)(S.colptr[u + 1] - S.colptr[u]);
+  const int L = S.nl[u];
+  double *Pm = P.F + S.valoff[u];
+  const bool panel = c0 >= L + s;
+  if (tid == 0) ident = 1;
+  __syncthreads();
+  if (tid < s) {
+    perm[tid] = P.refactor ? tid : P.iperm[r + tid];
+    if (perm[tid] != tid) ident = 0;
+  }
+  __syncthreads();
+  if (ident && !panel) return;
+  if (panel)
+    for (int idx = tid; idx < s * s; idx += FI_THREADS) {
+      const int t = idx / s, a = idx - t * s;
+      Lb[t * FXLD + a] = Pm[(int64_t)t * W + L + a];
+    }
+  for (int idx = tid; idx < s * tw; idx += FI_THREADS) {
+    const int t = idx / tw, c = idx - t * tw;
+    tl[idx] = Pm[(int64_t)perm[t] * W + c0 + c];
+  }
+  __syncthreads();
+  if (panel) {
+    for (int t = 0; t + 1 < s; ++t) {
+      const int rem = s - t - 1;
+      for (int idx = tid; idx < rem * tw; idx += FI_THREADS) {
+        const int q = t + 1 + idx / tw, c = idx % tw;
+        tl[q * tw + c] -= Lb[q * FXLD + t] * tl[t * tw + c];
+      }
+      __syncthreads();
+    }
+  }
+  for (int idx = tid; idx < s * tw; idx += FI_THREADS) {
+    const int t = idx / tw, c = idx - t * tw;
+    Pm[(int64_t)t * W + c0 + c] = tl[idx];
+  }
+}
+
+// ---------------------------------------------------------------------------- X blocks
+// X = T[:, pb0 .. pb0+m) · U_bb⁻¹ in place; 4 threads per target row.
+__global__ void __launch_bounds__(FI_THREADS) k_fi_x(DevSym S, CallP P, FaninDev D, int base) {
+  extern __shared__ __align__(16) double xsm[];
+  double *Ub = xsm;
+  double *Xt = xsm + 64 * FXLD;
+  const int j = base + blockIdx.x;
+  const int64_t dk = D.xp_edge[j];
+  const int T = D.xp_tgt[j];
+  const int v = S.deps[dk];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int r = (int)S.first[T];
+  const int s = (int)(S.first[T + 1] - r);
+  const int64_t tc0 = S.colptr[T];
+  const int W = (int)(S.colptr[T + 1] - tc0);
+  const int vf = (int)S.first[v];
+  const int vs = (int)(S.first[v + 1] - vf);
+  const int vW = (int)(S.colptr[v + 1] - S.colptr[v]);
+  const int vnl = S.nl[v];
+  const double *vb = P.F + S.valoff[v];
+  double *Pm = P.F + S.valoff[T];
+  const int pb0 = D.dep_pb[dk];
+  const int tb0 = S.cols[tc0 + pb0] - vf;
+  const int m = vs - tb0;
+  for (int idx = tid; idx < m * m; idx += FI_THREADS) {
+    const int a = idx / m, b2 = idx - a * m;
+    Ub[a * FXLD + b2] = b2 >= a ? vb[(int64_t)(tb0 + a) * vW + vnl + tb0 + b2] : 0.0;
+  }
+  for (int idx = tid; idx < s * m; idx += FI_THREADS) {
+    const int t = idx / m, a = idx - t * m;
+    Xt[t * FXLD + a] = Pm[(int64_t)t * W + pb0 + a];
+  }
+  __syncthreads();
+  {
+    const int t = tid >> 2, qd = tid & 3;
+    double *xr = Xt + t * FXLD;
+    const bool act = t < s;
+    for (int a = 0; a < m; ++a) {
+      double x = 0.0;
+      if (act && (a & 3) == qd) {
+        x = xr[a] / Ub[a * FXLD + a];
+        xr[a] = x;
+      }
+      x = __shfl_sync(HY_FULL, x, (lane & ~3) | (a & 3));
+      if (act && x != 0.0)
+        for (int b2 = a + 1 + ((qd - a - 1) & 3); b2 < m; b2 += 4) xr[b2] -= x * Ub[a * FXLD + b2];
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  for (int idx = tid; idx < s * m; idx += FI_THREADS) {
+    const int t = idx / m, a = idx - t * m;
+    Pm[(int64_t)t * W + pb0 + a] = Xt[t * FXLD + a];
+  }
+}
+
+// ---------------------------------------------------------------------------- updates
+constexpr int FI_TILE = 64;
+
+__global__ void __launch_bounds__(FI_THREADS) k_fi_upd(DevSym S, CallP P, FaninDev D, int base,
+                                                       int Smax, int Mmax) {
+  extern __shared__ __align__(16) double fs[];
+  __shared__ int tcol[FI_TILE];
+  __shared__ int spos[FI_TILE];
+  const int j = base + blockIdx.x;
+  const int T = D.up_t[j];
+  const int c0 = D.up_c0[j], c1 = D.up_c1[j];
+  const int tw = c1 - c0;
+  const int tid = threadIdx.x;
+  const int r = (int)S.first[T];
+  const int s = (int)(S.first[T + 1] - r);
+  const int64_t tc0 = S.colptr[T];
+  const int W = (int)(S.colptr[T + 1] - tc0);
+  double *Pm = P.F + S.valoff[T];
+  double *acc = fs;                          // s x FI_TILE
+  double *Xs = acc + (size_t)Smax * FI_TILE; // Smax x FXLD
+  double *Ut = Xs + (size_t)Smax * FXLD;     // Mmax x FXLD
+  for (int c = tid; c < tw; c += FI_THREADS) tcol[c] = S.cols[tc0 + c0 + c];
+  for (int idx = tid; idx < s * FI_TILE; idx += FI_THREADS) {
+    const int t = idx / FI_TILE, c = idx - t * FI_TILE;
+    acc[idx] = c < tw ? Pm[(int64_t)t * W + c0 + c] : 0.0;
+  }
+  const int tr = tid >> 4, tcl = tid & 15;
+  for (int64_t z = D.up_ptr[j]; z < D.up_ptr[j + 1]; ++z) {
+    const int64_t dk = S.dptr[T] + D.src_k[z];
+    const int q0 = D.src_q0[z], q1 = D.src_q1[z];
+    const int nq = q1 - q0;
+    const int v = S.deps[dk];
+    const int vf = (int)S.first[v];
+    const int vs = (int)(S.first[v + 1] - vf);
+    const int64_t vc0 = S.colptr[v];
+    const int vW = (int)(S.colptr[v + 1] - vc0);
+    const int vnl = S.nl[v];
+    const double *vb = P.F + S.valoff[v];
+    const int pb0 = D.dep_pb[dk];
+    const int tb0 = S.cols[tc0 + pb0] - vf;
+    const int m = vs - tb0;
+    const int qbase = vnl + vs + q0;
+    __syncthreads();
+    for (int idx = tid; idx < s * m; idx += FI_THREADS) {
+      const int t = idx / m, a = idx - t * m;
+      Xs[t * FXLD + a] = Pm[(int64_t)t * W + pb0 + a];
+    }
+    for (int idx = tid; idx < m * FI_TILE; idx += FI_THREADS) {
+      const int a = idx >> 6, c = idx & 63;
+      Ut[a * FXLD + c] = c < nq ? vb[(int64_t)(tb0 + a) * vW + qbase + c] : 0.0;
+    }
+    if (tid < nq) spos[tid] = lower_bound_i32(tcol, 0, tw, S.cols[vc0 + qbase + tid]);
+    __syncthreads();
+    double c4[4][4];
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) c4[x][y] = 0.0;
+    for (int a = 0; a < m; ++a) {
+      double xv[4], uv[4];
+#pragma unroll
+      for (int x = 0; x < 4; ++x) xv[x] = (tr + 16 * x < s) ? Xs[(tr + 16 * x) * FXLD + a] : 0.0;
+#pragma unroll
+      for (int y = 0; y < 4; ++y) uv[y] = Ut[a * FXLD + tcl + 16 * y];
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) c4[x][y] = fma(xv[x], uv[y], c4[x][y]);
+    }
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      const int t = tr + 16 * x;
+      if (t < s) {
+#pragma unroll
+        for (int y = 0; y < 4; ++y) {
+          const int c = tcl + 16 * y;
+          if (c < nq) acc[t * FI_TILE + spos[c]] -= c4[x][y];
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int idx = tid; idx < s * FI_TILE; idx += FI_THREADS) {
+    const int t = idx / FI_TILE, c = idx - t * FI_TILE;
+    if (c < tw) Pm[(int64_t)t * W + c0 + c] = acc[idx];
+  }
+}
+
+size_t fi_upd_smem(int Smax, int Mmax) {
+  return ((size_t)Smax * FI_TILE + (size_t)Smax * FXLD + (size_t)Mmax * FXLD) * sizeof(double);
+}
+
+}  // namespace hy

@@ -84,6 +84,20 @@ class SlabPlanDesc(ctypes.Structure):
     ]
 
 
+class FaninPlanDesc(ctypes.Structure):
+    _fields_ = [
+        ("nlevels", ctypes.c_int64), ("nsrc", ctypes.c_int64), ("ndeps", ctypes.c_int64),
+        ("lu_ptr", ctypes.c_void_p), ("lu_nodes", ctypes.c_void_p),
+        ("pt_ptr", ctypes.c_void_p), ("pt_node", ctypes.c_void_p), ("pt_c0", ctypes.c_void_p),
+        ("pt_c1", ctypes.c_void_p),
+        ("xp_ptr", ctypes.c_void_p), ("xp_edge", ctypes.c_void_p), ("xp_tgt", ctypes.c_void_p),
+        ("lev_up", ctypes.c_void_p), ("up_t", ctypes.c_void_p), ("up_c0", ctypes.c_void_p),
+        ("up_c1", ctypes.c_void_p), ("up_ptr", ctypes.c_void_p),
+        ("src_k", ctypes.c_void_p), ("src_q0", ctypes.c_void_p), ("src_q1", ctypes.c_void_p),
+        ("dep_pb", ctypes.c_void_p), ("level_smax", ctypes.c_void_p), ("level_mmax", ctypes.c_void_p),
+    ]
+
+
 def library():
     """Load the CUDA library (building it in-tree first if it is absent)."""
     global _lib
@@ -116,6 +130,7 @@ def library():
     lib.hy_batched_factor_values.argtypes = [vp, i64, vp, u]
     lib.hy_set_option.argtypes = [vp, ctypes.c_char_p, i64]
     lib.hy_upload_slab_plan.argtypes = [vp, ctypes.POINTER(SlabPlanDesc)]
+    lib.hy_upload_fanin_plan.argtypes = [vp, ctypes.POINTER(FaninPlanDesc)]
     _lib = lib
     return lib
 
@@ -187,8 +202,33 @@ class DeviceContext:
         self.nnz = A.nnz
         from . import schedule as _sc
         self.wide_row = int(os.environ.get("HYLU_WIDE_ROW", _sc.WIDE_ROW))
-        if _sc.slab_nodes(s, self.wide_row).any():
+        self.path = "fanin" if (int(s.kernel_mode) >= 1 and os.environ.get("HYLU_PATH", "fanin") == "fanin") \
+            else "rows"
+        if self.path == "fanin":
+            self.upload_fanin_plan()
+        elif _sc.slab_nodes(s, self.wide_row).any():
             self.upload_slab_plan()
+
+    def upload_fanin_plan(self):
+        from . import schedule
+        s = self.analysis.symbolic
+        plan = getattr(s, "_fanin_plan", None)
+        if plan is None:
+            plan = schedule.build_fanin_plan(s)
+            s._fanin_plan = plan
+        arrs = {k: np.ascontiguousarray(getattr(plan, k)) for k in (
+            "lu_ptr", "lu_nodes", "pt_ptr", "pt_node", "pt_c0", "pt_c1", "xp_ptr", "xp_edge", "xp_tgt",
+            "lev_up", "up_t", "up_c0", "up_c1", "up_ptr", "src_k", "src_q0", "src_q1", "dep_pb",
+            "level_smax", "level_mmax")}
+        arrs["lu_nodes"] = arrs["lu_nodes"].astype(np.int32)
+        arrs["xp_edge"] = arrs["xp_edge"].astype(np.int64)
+        d = FaninPlanDesc()
+        d.nlevels, d.nsrc, d.ndeps = plan.nlevels, len(plan.src_k), len(plan.dep_pb)
+        for k, v in arrs.items():
+            setattr(d, k, v.ctypes.data if v.size else None)
+        with self.torch.cuda.device(self.device):
+            check(self.lib.hy_upload_fanin_plan(self.h, ctypes.byref(d)))
+        self._fanin_arrays = arrs
 
     def upload_slab_plan(self):
         from . import schedule

@@ -622,3 +622,208 @@ def slab_level_smem(sym, plan):
                 mm = max(mm, int(rows[d].max()))
         out[lv] = (int(rows[nodes].max()), mm, int(sw.max()), int((rows[nodes] * sw).max()))
     return out
+
+
+# --------------------------------------------------------------------------- level fan-in plan
+FANIN_TILE = 64          # target columns per update tile
+PANEL_TILE = 256         # columns per permutation / TRSM tile
+
+
+@njit(cache=True)
+def _fanin_plan(first, kind, colptr, cols, nl, dptr, deps, level, nlev, tw, pw):
+    """Per level: LU nodes, perm/TRSM tiles, X pairs and update tiles.
+
+    Update item = (target T, tile [c0, c1)) with its source list (dep index k, q0, q1):
+    the sources of T that finish at this level and whose beyond-block columns meet
+    the tile ([q0, q1) indexes those columns)."""
+    nn = len(kind)
+    # ---- nodes by level (LU) and perm/TRSM tiles
+    lu_cnt = np.zeros(nlev + 1, np.int64)
+    for u in range(nn):
+        lu_cnt[level[u] + 1] += 1
+    lu_ptr = np.cumsum(lu_cnt)
+    lu_nodes = np.empty(nn, np.int32)
+    fillp = lu_ptr[:-1].copy()
+    for u in range(nn):
+        lu_nodes[fillp[level[u]]] = u
+        fillp[level[u]] += 1
+    pt_node_l = []
+    pt_c0_l = []
+    pt_c1_l = []
+    pt_ptr = np.zeros(nlev + 1, np.int64)
+    for lv in range(nlev):
+        for x in range(lu_ptr[lv], lu_ptr[lv + 1]):
+            u = lu_nodes[x]
+            s = first[u + 1] - first[u]
+            if s < 2:
+                continue
+            W = colptr[u + 1] - colptr[u]
+            L = nl[u]
+            c = 0
+            while c < L:
+                pt_node_l.append(u)
+                pt_c0_l.append(c)
+                pt_c1_l.append(min(L, c + pw))
+                c += pw
+            c = L + s
+            while c < W:
+                pt_node_l.append(u)
+                pt_c0_l.append(c)
+                pt_c1_l.append(min(W, c + pw))
+                c += pw
+        pt_ptr[lv + 1] = len(pt_node_l)
+    # ---- X pairs: dependency edges grouped by the source's level
+    nd = dptr[nn]
+    xp_cnt = np.zeros(nlev + 1, np.int64)
+    for u in range(nn):
+        for k in range(dptr[u], dptr[u + 1]):
+            xp_cnt[level[deps[k]] + 1] += 1
+    xp_ptr = np.cumsum(xp_cnt)
+    xp_edge = np.empty(nd, np.int64)
+    xp_tgt = np.empty(nd, np.int32)
+    fillx = xp_ptr[:-1].copy()
+    for u in range(nn):
+        for k in range(dptr[u], dptr[u + 1]):
+            lv = level[deps[k]]
+            xp_edge[fillx[lv]] = k
+            xp_tgt[fillx[lv]] = u
+            fillx[lv] += 1
+    # ---- update tiles: for each edge (grouped by source level, then target), walk the
+    # source's beyond-block columns tile by tile
+    up_t_l = []      # target
+    up_c0_l = []
+    up_c1_l = []
+    up_ptr_l = [np.int64(0)]   # per item: range into src lists
+    src_k_l = []
+    src_q0_l = []
+    src_q1_l = []
+    lev_up = np.zeros(nlev + 1, np.int64)
+    tmp_tile = np.empty(0, np.int64)
+    for lv in range(nlev):
+        x = xp_ptr[lv]
+        while x < xp_ptr[lv + 1]:
+            u = xp_tgt[x]
+            x1 = x
+            while x1 < xp_ptr[lv + 1] and xp_tgt[x1] == u:
+                x1 += 1
+            # edges x..x1 share target u; gather (tile, k, q0, q1) records
+            c0u = colptr[u]
+            W = colptr[u + 1] - c0u
+            ntile = (W + tw - 1) // tw
+            cnt = np.zeros(ntile, np.int64)
+            recs_t = []
+            recs_k = []
+            recs_q0 = []
+            recs_q1 = []
+            for e in range(x, x1):
+                k = xp_edge[e]
+                v = deps[k]
+                vs = first[v + 1] - first[v]
+                vc0 = colptr[v]
+                vW = colptr[v + 1] - vc0
+                pst = nl[v] + vs
+                q = pst
+                while q < vW:
+                    pos = _lower_bound(cols, c0u, c0u + W, cols[vc0 + q]) - c0u
+                    t = pos // tw
+                    hi_id = cols[c0u + min(W, (t + 1) * tw) - 1]
+                    qe = _lower_bound(cols, vc0 + q, vc0 + vW, hi_id + 1) - vc0
+                    recs_t.append(t)
+                    recs_k.append(k - dptr[u])
+                    recs_q0.append(q - pst)
+                    recs_q1.append(qe - pst)
+                    cnt[t] += 1
+                    q = qe
+            # emit items tile-ordered, sources in edge (ascending k) order
+            for t in range(ntile):
+                if cnt[t] == 0:
+                    continue
+                up_t_l.append(u)
+                up_c0_l.append(t * tw)
+                up_c1_l.append(min(W, (t + 1) * tw))
+                for z in range(len(recs_t)):
+                    if recs_t[z] == t:
+                        src_k_l.append(np.int32(recs_k[z]))
+                        src_q0_l.append(np.int32(recs_q0[z]))
+                        src_q1_l.append(np.int32(recs_q1[z]))
+                up_ptr_l.append(np.int64(len(src_k_l)))
+            x = x1
+        lev_up[lv + 1] = len(up_t_l)
+    nu = len(up_t_l)
+    up_t = np.empty(nu, np.int32)
+    up_c0 = np.empty(nu, np.int32)
+    up_c1 = np.empty(nu, np.int32)
+    for z in range(nu):
+        up_t[z] = up_t_l[z]
+        up_c0[z] = up_c0_l[z]
+        up_c1[z] = up_c1_l[z]
+    up_ptr = np.empty(len(up_ptr_l), np.int64)
+    for z in range(len(up_ptr_l)):
+        up_ptr[z] = up_ptr_l[z]
+    ns = len(src_k_l)
+    src_k = np.empty(ns, np.int32)
+    src_q0 = np.empty(ns, np.int32)
+    src_q1 = np.empty(ns, np.int32)
+    for z in range(ns):
+        src_k[z] = src_k_l[z]
+        src_q0[z] = src_q0_l[z]
+        src_q1[z] = src_q1_l[z]
+    npt = len(pt_node_l)
+    pt_node = np.empty(npt, np.int32)
+    pt_c0 = np.empty(npt, np.int32)
+    pt_c1 = np.empty(npt, np.int32)
+    for z in range(npt):
+        pt_node[z] = pt_node_l[z]
+        pt_c0[z] = pt_c0_l[z]
+        pt_c1[z] = pt_c1_l[z]
+    return (lu_ptr, lu_nodes, pt_ptr, pt_node, pt_c0, pt_c1, xp_ptr, xp_edge.astype(np.int64), xp_tgt,
+            lev_up, up_t, up_c0, up_c1, up_ptr, src_k, src_q0, src_q1)
+
+
+@dataclass
+class FaninPlan:
+    lu_ptr: np.ndarray
+    lu_nodes: np.ndarray
+    pt_ptr: np.ndarray
+    pt_node: np.ndarray
+    pt_c0: np.ndarray
+    pt_c1: np.ndarray
+    xp_ptr: np.ndarray
+    xp_edge: np.ndarray
+    xp_tgt: np.ndarray
+    lev_up: np.ndarray
+    up_t: np.ndarray
+    up_c0: np.ndarray
+    up_c1: np.ndarray
+    up_ptr: np.ndarray
+    src_k: np.ndarray
+    src_q0: np.ndarray
+    src_q1: np.ndarray
+    dep_pb: np.ndarray
+    level_smax: np.ndarray     # max target rows among update items of a level
+    level_mmax: np.ndarray     # max source rows of a level
+
+    @property
+    def nlevels(self):
+        return len(self.lu_ptr) - 1
+
+
+def build_fanin_plan(sym, tw=FANIN_TILE, pw=PANEL_TILE):
+    s = sym
+    nlev = len(s.level_ptr) - 1
+    out = _fanin_plan(s.node_first, s.node_kind, s.colptr, s.cols, s.nl, s.dep_ptr, s.deps,
+                      s.level, nlev, tw, pw)
+    dep_pb = _dep_block_pos(s.node_first, s.node_kind, s.colptr, s.cols, s.nl, s.dep_ptr, s.deps)
+    rows = np.diff(s.node_first)
+    lu_ptr, lu_nodes = out[0], out[1]
+    lev_up, up_t = out[9], out[10]
+    smax = np.ones(nlev, np.int32)
+    mmax = np.ones(nlev, np.int32)
+    for lv in range(nlev):
+        a, b = lev_up[lv], lev_up[lv + 1]
+        if b > a:
+            smax[lv] = int(rows[up_t[a:b]].max())
+        nodes = lu_nodes[lu_ptr[lv]:lu_ptr[lv + 1]]
+        if len(nodes):
+            mmax[lv] = int(rows[nodes].max())
+    return FaninPlan(*out, dep_pb, smax, mmax)

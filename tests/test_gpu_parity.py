@@ -50,8 +50,10 @@ def test_factorize_matches_oracle(name, mode):
 @pytest.mark.parametrize("name", ["c0", "c2", "c3"])
 @pytest.mark.parametrize("mode", [1, 2])
 def test_wide_rows_on_slab_path(name, mode, monkeypatch):
-    """Standalone rows routed to the column-slab kernel (tiny threshold, tiny slabs)."""
+    """Row/slab path in SUP modes with standalone rows routed to the column-slab
+    kernel (tiny threshold, tiny slabs)."""
     monkeypatch.setenv("HYLU_WIDE_ROW", "4")
+    monkeypatch.setenv("HYLU_PATH", "rows")
     p, an = _analysis(name, mode)
     on = _oracle()
     ref = on.factorize(an)
