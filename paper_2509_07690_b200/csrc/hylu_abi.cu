@@ -536,7 +536,6 @@ int hy_upload_slab_plan(hy_handle *h, const hy_slab_plan *d) {
 
 int hy_upload_fanin_plan(hy_handle *h, const hy_fanin_plan *d) {
   if (!h || !h->uploaded || !d) return fail(HY_INVALID_ARGUMENT, "symbolic not uploaded / null");
-  if (d->nlevels != h->fplan.nlev) return fail(HY_DIMENSION_MISMATCH, "fan-in plan level count mismatch");
   CK(cudaSetDevice(h->device));
   for (void *p : h->fi_allocs) cudaFree(p);
   h->fi_allocs.clear();
@@ -582,7 +581,8 @@ static int run_fanin(hy_handle *h, const CallP &P, cudaStream_t st) {
   CK(cudaMemsetAsync(P.F, 0, sizeof(double) * h->stored, st));
   k_fi_scatter<<<(h->S.n * 32 + 255) / 256, 256, 0, st>>>(h->S, P);
   h->launches++;
-  for (int l = 0; l < h->fplan.nlev; ++l) {
+  const int nfl = (int)h->fi_lu.size() - 1;
+  for (int l = 0; l < nfl; ++l) {
     const int nlu = (int)(h->fi_lu[l + 1] - h->fi_lu[l]);
     const int npt = (int)(h->fi_pt[l + 1] - h->fi_pt[l]);
     const int nxp = (int)(h->fi_xp[l + 1] - h->fi_xp[l]);

@@ -808,11 +808,39 @@ class FaninPlan:
         return len(self.lu_ptr) - 1
 
 
+@njit(cache=True)
+def _fanin_levels(first, colptr, cols, nl, dptr, deps, node_of):
+    """Longest-path levels over L edges (v -> u for u's L entries in v's columns) and
+    U edges (v -> w when v's beyond-block columns meet w's block): within a fan-in
+    level no source updates another source's block columns, and every node's
+    updates come from strictly lower levels.  Equal to the L levels for
+    structurally symmetric patterns."""
+    nn = len(nl)
+    lev = np.zeros(nn, np.int64)
+    for u in range(nn):                    # nodes in topological (index) order
+        for k in range(dptr[u], dptr[u + 1]):
+            v = deps[k]
+            if lev[v] + 1 > lev[u]:
+                lev[u] = lev[v] + 1
+        # push U edges forward: owners of u's beyond-block columns
+        s = first[u + 1] - first[u]
+        c0 = colptr[u]
+        last = -1
+        for q in range(c0 + nl[u] + s, colptr[u + 1]):
+            w = node_of[cols[q]]
+            if w != last:
+                if lev[u] + 1 > lev[w]:
+                    lev[w] = lev[u] + 1
+                last = w
+    return lev
+
+
 def build_fanin_plan(sym, tw=FANIN_TILE, pw=PANEL_TILE):
     s = sym
-    nlev = len(s.level_ptr) - 1
+    flev = _fanin_levels(s.node_first, s.colptr, s.cols, s.nl, s.dep_ptr, s.deps, s.node_of)
+    nlev = int(flev.max()) + 1
     out = _fanin_plan(s.node_first, s.node_kind, s.colptr, s.cols, s.nl, s.dep_ptr, s.deps,
-                      s.level, nlev, tw, pw)
+                      flev, nlev, tw, pw)
     dep_pb = _dep_block_pos(s.node_first, s.node_kind, s.colptr, s.cols, s.nl, s.dep_ptr, s.deps)
     rows = np.diff(s.node_first)
     lu_ptr, lu_nodes = out[0], out[1]

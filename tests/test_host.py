@@ -148,3 +148,83 @@ def test_c_abi_library_exports_every_header_symbol():
     assert len(names) >= 12
     for nm in sorted(names):
         assert hasattr(lib, nm), nm
+
+
+def _run_fanin_cpu(an, plan):
+    """CPU interpreter of the level fan-in plan (the device kernels' arithmetic)."""
+    s = an.symbolic
+    vm = an.vmap
+    A = an.A
+    F = np.zeros(s.stored_values)
+    thr = 1e-8 * on.anorm_kernel(A.values, vm.scale)
+    rows = np.diff(s.node_first)
+    W = np.diff(s.colptr)
+
+    def blk(u):
+        return F[s.valoff[u]:s.valoff[u] + rows[u] * W[u]].reshape(rows[u], W[u])
+
+    for i in range(s.n):
+        u = s.node_of[i]
+        a = vm.mrow_src[i]
+        e0, e1 = A.row_ptr[a], A.row_ptr[a + 1]
+        blk(u)[i - s.node_first[u], vm.colpos[e0:e1]] = A.values[e0:e1] * vm.scale[e0:e1]
+    iperm = np.zeros(s.n, np.int64)
+    for lv in range(plan.nlevels):
+        for u in plan.lu_nodes[plan.lu_ptr[lv]:plan.lu_ptr[lv + 1]]:
+            B = blk(u)
+            r, L, sr = s.node_first[u], s.nl[u], rows[u]
+            perm = np.arange(sr)
+            for t in range(sr):
+                p = t + int(np.argmax(np.abs(B[t:, L + t])))
+                if p != t:
+                    B[[t, p]] = B[[p, t]]
+                    perm[[t, p]] = perm[[p, t]]
+                if abs(B[t, L + t]) < thr:
+                    B[t, L + t] = thr if B[t, L + t] >= 0 else -thr
+                for q in range(t + 1, sr):
+                    B[q, L + t] /= B[t, L + t]
+                    B[q, L + t + 1:] -= B[q, L + t] * B[t, L + t + 1:]
+            iperm[r:r + sr] = perm
+        for x in range(plan.xp_ptr[lv], plan.xp_ptr[lv + 1]):
+            k = plan.xp_edge[x]
+            T = plan.xp_tgt[x]
+            v = s.deps[k]
+            Tb = blk(T)
+            pb0 = plan.dep_pb[k]
+            tb0 = s.node_cols(T)[pb0] - s.node_first[v]
+            m = rows[v] - tb0
+            Ub = blk(v)[tb0:, s.nl[v] + tb0:s.nl[v] + rows[v]]
+            X = Tb[:, pb0:pb0 + m].copy()
+            for a_ in range(m):
+                X[:, a_] /= Ub[a_, a_]
+                X[:, a_ + 1:] -= np.outer(X[:, a_], Ub[a_, a_ + 1:])
+            Tb[:, pb0:pb0 + m] = X
+        for it in range(plan.lev_up[lv], plan.lev_up[lv + 1]):
+            T = plan.up_t[it]
+            Tb = blk(T)
+            tcols = s.node_cols(T)
+            for z in range(plan.up_ptr[it], plan.up_ptr[it + 1]):
+                k = s.dep_ptr[T] + plan.src_k[z]
+                v = s.deps[k]
+                pb0 = plan.dep_pb[k]
+                tb0 = tcols[pb0] - s.node_first[v]
+                m = rows[v] - tb0
+                qb = s.nl[v] + rows[v]
+                q0, q1 = plan.src_q0[z], plan.src_q1[z]
+                vc = s.node_cols(v)[qb + q0:qb + q1]
+                pos = np.searchsorted(tcols, vc)
+                X = Tb[:, pb0:pb0 + m]
+                Tb[:, pos] -= X @ blk(v)[tb0:, qb + q0:qb + q1]
+    return F, iperm
+
+
+@pytest.mark.parametrize("name,mode", [("c0", None), ("c1", 1), ("c3", 2), ("c2", 1)])
+def test_fanin_plan_reproduces_oracle(name, mode):
+    p = gen.config(name, "small")
+    an = an_mod.analyze(p.A, SolverConfig(ordering=p.ordering), kernel_override=mode)
+    plan = schedule.build_fanin_plan(an.symbolic)
+    F, ip = _run_fanin_cpu(an, plan)
+    ref = on.factorize(an)
+    # the interpreter applies permutations to whole rows, like the device
+    assert np.array_equal(ip, ref.inner_perm)
+    assert np.abs(F - ref.values).max() <= 1e-11 * max(1.0, np.abs(ref.values).max())
