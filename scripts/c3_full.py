@@ -1,0 +1,49 @@
+"""c3 at full size (48^3 x 3, ND): factorize / refactorize / solve timings + residual."""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2509_07690_b200 import api, generators as gen, analysis as an_mod  # noqa: E402
+from paper_2509_07690_b200._ref import SolverConfig, matrix as refmatrix  # noqa: E402
+
+k = int(sys.argv[1]) if len(sys.argv) > 1 else 48
+t0 = time.perf_counter()
+p = gen.fem27(k)
+an = an_mod.analyze(p.A, SolverConfig(ordering="nd"))
+s = an.symbolic
+ta = time.perf_counter() - t0
+dv = torch.from_numpy(np.array(p.A.values)).cuda()
+db = torch.from_numpy(np.array(p.b)).cuda()
+t0 = time.perf_counter()
+f = api.factorize_analysis(an, dv)     # includes plan upload on first call
+torch.cuda.synchronize()
+tfirst = time.perf_counter() - t0
+
+
+def ev(fn, reps=2):
+    ts = []
+    out = None
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        out = fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return min(ts), out
+
+
+tf, f = ev(lambda: api.factorize_analysis(an, dv))
+tr, f2 = ev(lambda: api.refactorize(dv, f))
+ts, x = ev(lambda: api.substitute(f, db), 3)
+xh = x.cpu().numpy()
+res = float(np.linalg.norm(refmatrix.spmv(p.A, xh) - p.b) / np.linalg.norm(p.b))
+print(json.dumps(dict(config="c3_k%d" % k, n=s.n, nnz=p.A.nnz, fill=s.fill_nnz, flops=s.flops,
+                      stored=s.stored_values, levels=len(s.level_ptr) - 1, analyze_s=round(ta, 1),
+                      first_factor_s=round(tfirst, 1), factor_ms=tf, refactor_ms=tr, solve_ms=ts,
+                      gflops=s.flops / tf / 1e6, residual=res, npert=len(f.perturbed))), flush=True)
