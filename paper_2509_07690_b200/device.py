@@ -95,6 +95,7 @@ class FaninPlanDesc(ctypes.Structure):
         ("up_c1", ctypes.c_void_p), ("up_ptr", ctypes.c_void_p),
         ("src_k", ctypes.c_void_p), ("src_q0", ctypes.c_void_p), ("src_q1", ctypes.c_void_p),
         ("dep_pb", ctypes.c_void_p), ("level_smax", ctypes.c_void_p), ("level_mmax", ctypes.c_void_p),
+        ("src_v", ctypes.c_void_p), ("src_pb", ctypes.c_void_p), ("src_tb", ctypes.c_void_p),
     ]
 
 
@@ -221,6 +222,8 @@ class DeviceContext:
             "lev_up", "up_t", "up_c0", "up_c1", "up_ptr", "src_k", "src_q0", "src_q1", "dep_pb",
             "level_smax", "level_mmax")}
         arrs["lu_nodes"] = arrs["lu_nodes"].astype(np.int32)
+        sv, spb, stb = schedule.fanin_source_records(s, plan)
+        arrs["src_v"], arrs["src_pb"], arrs["src_tb"] = sv, spb, stb
         arrs["xp_edge"] = arrs["xp_edge"].astype(np.int64)
         d = FaninPlanDesc()
         d.nlevels, d.nsrc, d.ndeps = plan.nlevels, len(plan.src_k), len(plan.dep_pb)

@@ -855,3 +855,17 @@ def build_fanin_plan(sym, tw=FANIN_TILE, pw=PANEL_TILE):
         if len(nodes):
             mmax[lv] = int(rows[nodes].max())
     return FaninPlan(*out, dep_pb, smax, mmax)
+
+
+def fanin_source_records(sym, plan):
+    """Per update-source record: (source node v, block position pb0 in the target,
+    first present block row tb0) — static, so the device does no metadata chasing."""
+    s = sym
+    # target of each source record
+    cnt = np.diff(plan.up_ptr)
+    tgt = np.repeat(plan.up_t.astype(np.int64), cnt)
+    dk = s.dep_ptr[tgt] + plan.src_k
+    v = s.deps[dk].astype(np.int32)
+    pb0 = plan.dep_pb[dk].astype(np.int32)
+    tb0 = (s.cols[s.colptr[tgt] + pb0] - s.node_first[v]).astype(np.int32)
+    return v, pb0, tb0
