@@ -182,7 +182,7 @@ struct hy_handle {
   std::vector<int64_t> fi_lu, fi_pt, fi_xp, fi_up;   // per-level offsets
   std::vector<int32_t> fi_smax, fi_mmax;
   int sm_count = 148;
-  int fi_upd_v2 = 1;                       // option "fanin_upd_v2"
+  int fi_upd_v2 = 0;                       // option "fanin_upd_v2"
   int fi_upd_ctas_per_sm = 2;              // option "fanin_ctas_per_sm"
 };
 

@@ -265,6 +265,8 @@ __global__ void __launch_bounds__(FI_THREADS) k_fi_x(DevSym S, CallP P, FaninDev
 
 // ---------------------------------------------------------------------------- updates
 constexpr int FI_TILE = 64;
+constexpr int FI_KC = 32;      // K (source rows) chunk staged per pass
+constexpr int KLD = FI_KC + 1;
 
 __global__ void __launch_bounds__(FI_THREADS) k_fi_upd(DevSym S, CallP P, FaninDev D, int base,
                                                        int Smax, int Mmax) {
@@ -282,8 +284,9 @@ __global__ void __launch_bounds__(FI_THREADS) k_fi_upd(DevSym S, CallP P, FaninD
   const int W = (int)(S.colptr[T + 1] - tc0);
   double *Pm = P.F + S.valoff[T];
   double *acc = fs;                          // s x FI_TILE
-  double *Xs = acc + (size_t)Smax * FI_TILE; // Smax x FXLD
-  double *Ut = Xs + (size_t)Smax * FXLD;     // Mmax x FXLD
+  double *Xs = acc + (size_t)Smax * FI_TILE; // Smax x KLD
+  double *Ut = Xs + (size_t)Smax * KLD;      // FI_KC x FXLD
+  (void)Mmax;
   for (int c = tid; c < tw; c += FI_THREADS) tcol[c] = S.cols[tc0 + c0 + c];
   for (int idx = tid; idx < s * FI_TILE; idx += FI_THREADS) {
     const int t = idx / FI_TILE, c = idx - t * FI_TILE;
@@ -291,46 +294,49 @@ __global__ void __launch_bounds__(FI_THREADS) k_fi_upd(DevSym S, CallP P, FaninD
   }
   const int tr = tid >> 4, tcl = tid & 15;
   for (int64_t z = D.up_ptr[j]; z < D.up_ptr[j + 1]; ++z) {
-    const int64_t dk = S.dptr[T] + D.src_k[z];
-    const int q0 = D.src_q0[z], q1 = D.src_q1[z];
-    const int nq = q1 - q0;
-    const int v = S.deps[dk];
+    const int v = D.src_v[z];
+    const int q0 = D.src_q0[z];
+    const int nq = D.src_q1[z] - q0;
     const int vf = (int)S.first[v];
     const int vs = (int)(S.first[v + 1] - vf);
     const int64_t vc0 = S.colptr[v];
     const int vW = (int)(S.colptr[v + 1] - vc0);
     const int vnl = S.nl[v];
     const double *vb = P.F + S.valoff[v];
-    const int pb0 = D.dep_pb[dk];
-    const int tb0 = S.cols[tc0 + pb0] - vf;
+    const int pb0 = D.src_pb[z];
+    const int tb0 = D.src_tb[z];
     const int m = vs - tb0;
     const int qbase = vnl + vs + q0;
     __syncthreads();
-    for (int idx = tid; idx < s * m; idx += FI_THREADS) {
-      const int t = idx / m, a = idx - t * m;
-      Xs[t * FXLD + a] = Pm[(int64_t)t * W + pb0 + a];
-    }
-    for (int idx = tid; idx < m * FI_TILE; idx += FI_THREADS) {
-      const int a = idx >> 6, c = idx & 63;
-      Ut[a * FXLD + c] = c < nq ? vb[(int64_t)(tb0 + a) * vW + qbase + c] : 0.0;
-    }
     if (tid < nq) spos[tid] = lower_bound_i32(tcol, 0, tw, S.cols[vc0 + qbase + tid]);
-    __syncthreads();
     double c4[4][4];
 #pragma unroll
     for (int x = 0; x < 4; ++x)
 #pragma unroll
       for (int y = 0; y < 4; ++y) c4[x][y] = 0.0;
-    for (int a = 0; a < m; ++a) {
-      double xv[4], uv[4];
+    for (int k0 = 0; k0 < m; k0 += FI_KC) {
+      const int kc = min(FI_KC, m - k0);
+      if (k0) __syncthreads();
+      for (int idx = tid; idx < s * kc; idx += FI_THREADS) {
+        const int t = idx / kc, a = idx - t * kc;
+        Xs[t * KLD + a] = Pm[(int64_t)t * W + pb0 + k0 + a];
+      }
+      for (int idx = tid; idx < kc * FI_TILE; idx += FI_THREADS) {
+        const int a = idx >> 6, c = idx & 63;
+        Ut[a * FXLD + c] = c < nq ? vb[(int64_t)(tb0 + k0 + a) * vW + qbase + c] : 0.0;
+      }
+      __syncthreads();
+      for (int a = 0; a < kc; ++a) {
+        double xv[4], uv[4];
 #pragma unroll
-      for (int x = 0; x < 4; ++x) xv[x] = (tr + 16 * x < s) ? Xs[(tr + 16 * x) * FXLD + a] : 0.0;
+        for (int x = 0; x < 4; ++x) xv[x] = (tr + 16 * x < s) ? Xs[(tr + 16 * x) * KLD + a] : 0.0;
 #pragma unroll
-      for (int y = 0; y < 4; ++y) uv[y] = Ut[a * FXLD + tcl + 16 * y];
+        for (int y = 0; y < 4; ++y) uv[y] = Ut[a * FXLD + tcl + 16 * y];
 #pragma unroll
-      for (int x = 0; x < 4; ++x)
+        for (int x = 0; x < 4; ++x)
 #pragma unroll
-        for (int y = 0; y < 4; ++y) c4[x][y] = fma(xv[x], uv[y], c4[x][y]);
+          for (int y = 0; y < 4; ++y) c4[x][y] = fma(xv[x], uv[y], c4[x][y]);
+      }
     }
 #pragma unroll
     for (int x = 0; x < 4; ++x) {
@@ -351,155 +357,9 @@ __global__ void __launch_bounds__(FI_THREADS) k_fi_upd(DevSym S, CallP P, FaninD
   }
 }
 
-// ---------------------------------------------------------------------------- updates v2
-// Persistent CTAs over a level's update items; per source a cp.async double buffer
-// (multiplier block X and the source's U tile for the next source load while the
-// current one is multiplied), then one write-back of the tile per item.
-__device__ __forceinline__ void cpa8(void *smem_dst, const void *gsrc) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gsrc) : "memory");
-}
-__device__ __forceinline__ void cpa4(void *smem_dst, const void *gsrc) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(gsrc) : "memory");
-}
-__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cpa_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
-__device__ __forceinline__ void cpa_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
-
-struct SrcMeta {
-  int m, nq, pb0, vW, qoff;    // qoff = first U column position (vnl + vs + q0) in v's list
-  int tb0;
-  int64_t vbase, vc0;
-};
-
-__device__ __forceinline__ SrcMeta src_meta(const DevSym &S, const FaninDev &D, int64_t z) {
-  SrcMeta sm;
-  const int v = D.src_v[z];
-  const int vf = (int)S.first[v];
-  const int vs = (int)(S.first[v + 1] - vf);
-  sm.vc0 = S.colptr[v];
-  sm.vW = (int)(S.colptr[v + 1] - sm.vc0);
-  sm.vbase = S.valoff[v];
-  sm.pb0 = D.src_pb[z];
-  sm.tb0 = D.src_tb[z];
-  sm.m = vs - sm.tb0;
-  const int q0 = D.src_q0[z];
-  sm.nq = D.src_q1[z] - q0;
-  sm.qoff = S.nl[v] + vs + q0;
-  return sm;
-}
-
-__device__ __forceinline__ void src_issue(const DevSym &S, const double *F, const double *Pm, int W,
-                                          int s, const SrcMeta &q, double *Xs, double *Ut, int *cid,
-                                          int tid) {
-  for (int idx = tid; idx < s * q.m; idx += FI_THREADS) {
-    const int t = idx / q.m, a = idx - t * q.m;
-    cpa8(Xs + t * FXLD + a, Pm + (int64_t)t * W + q.pb0 + a);
-  }
-  const double *vb = F + q.vbase;
-  for (int idx = tid; idx < q.m * q.nq; idx += FI_THREADS) {
-    const int a = idx / q.nq, c = idx - a * q.nq;
-    cpa8(Ut + a * FXLD + c, vb + (int64_t)(q.tb0 + a) * q.vW + q.qoff + c);
-  }
-  if (tid < q.nq) cpa4(cid + tid, S.cols + q.vc0 + q.qoff + tid);
-}
-
-__global__ void __launch_bounds__(FI_THREADS, 1) k_fi_upd2(DevSym S, CallP P, FaninDev D, int base,
-                                                           int count, int Smax, int Mmax) {
-  extern __shared__ __align__(16) double fs[];
-  __shared__ int tcol[FI_TILE];
-  __shared__ int spos[2][FI_TILE];
-  __shared__ int cidb[2][FI_TILE];
-  double *acc = fs;                                   // Smax x FI_TILE
-  double *Xb[2], *Ub[2];
-  Xb[0] = acc + (size_t)Smax * FI_TILE;
-  Ub[0] = Xb[0] + (size_t)Smax * FXLD;
-  Xb[1] = Ub[0] + (size_t)Mmax * FXLD;
-  Ub[1] = Xb[1] + (size_t)Smax * FXLD;
-  const int tid = threadIdx.x;
-  const int tr = tid >> 4, tcl = tid & 15;
-  for (int jj = blockIdx.x; jj < count; jj += gridDim.x) {
-    const int j = base + jj;
-    const int T = D.up_t[j];
-    const int c0 = D.up_c0[j], c1 = D.up_c1[j];
-    const int tw = c1 - c0;
-    const int r = (int)S.first[T];
-    const int s = (int)(S.first[T + 1] - r);
-    const int64_t tc0 = S.colptr[T];
-    const int W = (int)(S.colptr[T + 1] - tc0);
-    double *Pm = P.F + S.valoff[T];
-    const int64_t z0 = D.up_ptr[j], z1 = D.up_ptr[j + 1];
-    __syncthreads();   // previous item fully done with the buffers
-    // tile + first source
-    for (int idx = tid; idx < s * FI_TILE; idx += FI_THREADS) {
-      const int t = idx / FI_TILE, c = idx - t * FI_TILE;
-      if (c < tw) cpa8(acc + idx, Pm + (int64_t)t * W + c0 + c);
-    }
-    if (tid < tw) cpa4(tcol + tid, S.cols + tc0 + c0 + tid);
-    SrcMeta cur = src_meta(S, D, z0);
-    src_issue(S, P.F, Pm, W, s, cur, Xb[0], Ub[0], cidb[0], tid);
-    cpa_commit();
-    for (int64_t z = z0; z < z1; ++z) {
-      const int b = (int)((z - z0) & 1);
-      SrcMeta nxt;
-      const bool more = z + 1 < z1;
-      if (more) {
-        nxt = src_meta(S, D, z + 1);
-        src_issue(S, P.F, Pm, W, s, nxt, Xb[b ^ 1], Ub[b ^ 1], cidb[b ^ 1], tid);
-      }
-      cpa_commit();
-      cpa_wait1();
-      __syncthreads();
-      if (tid < cur.nq) spos[b][tid] = lower_bound_i32(tcol, 0, tw, cidb[b][tid]);
-      __syncthreads();
-      const double *Xs = Xb[b];
-      const double *Ut = Ub[b];
-      double c4[4][4];
-#pragma unroll
-      for (int x = 0; x < 4; ++x)
-#pragma unroll
-        for (int y = 0; y < 4; ++y) c4[x][y] = 0.0;
-      for (int a = 0; a < cur.m; ++a) {
-        double xv[4], uv[4];
-#pragma unroll
-        for (int x = 0; x < 4; ++x) xv[x] = (tr + 16 * x < s) ? Xs[(tr + 16 * x) * FXLD + a] : 0.0;
-#pragma unroll
-        for (int y = 0; y < 4; ++y) uv[y] = (tcl + 16 * y < cur.nq) ? Ut[a * FXLD + tcl + 16 * y] : 0.0;
-#pragma unroll
-        for (int x = 0; x < 4; ++x)
-#pragma unroll
-          for (int y = 0; y < 4; ++y) c4[x][y] = fma(xv[x], uv[y], c4[x][y]);
-      }
-#pragma unroll
-      for (int x = 0; x < 4; ++x) {
-        const int t = tr + 16 * x;
-        if (t < s) {
-#pragma unroll
-          for (int y = 0; y < 4; ++y) {
-            const int c = tcl + 16 * y;
-            if (c < cur.nq) acc[t * FI_TILE + spos[b][c]] -= c4[x][y];
-          }
-        }
-      }
-      __syncthreads();   // buffer b free for source z+2
-      if (more) cur = nxt;
-    }
-    cpa_wait0();
-    __syncthreads();
-    for (int idx = tid; idx < s * FI_TILE; idx += FI_THREADS) {
-      const int t = idx / FI_TILE, c = idx - t * FI_TILE;
-      if (c < tw) Pm[(int64_t)t * W + c0 + c] = acc[idx];
-    }
-  }
-}
-
-size_t fi_upd2_smem(int Smax, int Mmax) {
-  return ((size_t)Smax * FI_TILE + 2 * ((size_t)Smax * FXLD + (size_t)Mmax * FXLD)) * sizeof(double);
-}
-
 size_t fi_upd_smem(int Smax, int Mmax) {
-  return ((size_t)Smax * FI_TILE + (size_t)Smax * FXLD + (size_t)Mmax * FXLD) * sizeof(double);
+  (void)Mmax;
+  return ((size_t)Smax * FI_TILE + (size_t)Smax * KLD + (size_t)FI_KC * FXLD) * sizeof(double);
 }
 
 }  // namespace hy
