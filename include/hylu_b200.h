@@ -210,8 +210,7 @@ int hy_solve_batched(hy_handle *h, int64_t B, const double *d_b, double *d_x, ui
 int hy_batched_factor_values(hy_handle *h, int64_t b, double *d_out, uintptr_t stream);
 
 /* Tuning knobs: "staged" (0/1: stage each row's source values in shared memory
- * with cp.async in the batched pipeline kernel, default 0); "fanin_upd_v2" (0/1:
- * persistent double-buffered fan-in update kernel, default 1); "fanin_ctas_per_sm". */
+ * with cp.async in the batched pipeline kernel, default 0). */
 int hy_set_option(hy_handle *h, const char *name, int64_t value);
 
 /* Number of kernel launches issued by this handle since creation (bench evidence). */

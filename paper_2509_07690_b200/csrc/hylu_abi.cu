@@ -50,8 +50,7 @@ struct FaninDev {
   const int32_t *src_tb;
 };
 __global__ void k_fi_scatter(DevSym, CallP);
-__global__ void k_fi_upd2(DevSym, CallP, FaninDev, int, int, int, int);
-size_t fi_upd2_smem(int, int);
+
 __global__ void k_fi_lu(DevSym, CallP, FaninDev, int);
 __global__ void k_fi_panel(DevSym, CallP, FaninDev, int);
 __global__ void k_fi_x(DevSym, CallP, FaninDev, int);
@@ -182,8 +181,7 @@ struct hy_handle {
   std::vector<int64_t> fi_lu, fi_pt, fi_xp, fi_up;   // per-level offsets
   std::vector<int32_t> fi_smax, fi_mmax;
   int sm_count = 148;
-  int fi_upd_v2 = 0;                       // option "fanin_upd_v2"
-  int fi_upd_ctas_per_sm = 2;              // option "fanin_ctas_per_sm"
+
 };
 
 static void free_segments(hy_handle *h);
@@ -367,14 +365,6 @@ int hy_set_option(hy_handle *h, const char *name, int64_t value) {
   if (!h || !name) return fail(HY_INVALID_ARGUMENT, "null handle/name");
   if (std::string(name) == "group_batch" && value >= 1) {
     h->gbatch = (int)value;
-    return HY_OK;
-  }
-  if (std::string(name) == "fanin_upd_v2") {
-    h->fi_upd_v2 = value != 0;
-    return HY_OK;
-  }
-  if (std::string(name) == "fanin_ctas_per_sm" && value >= 1) {
-    h->fi_upd_ctas_per_sm = (int)value;
     return HY_OK;
   }
   if (std::string(name) == "staged") {
@@ -588,12 +578,6 @@ int hy_upload_fanin_plan(hy_handle *h, const hy_fanin_plan *d) {
     if (b > mx) mx = b;
   }
   CK(cudaFuncSetAttribute(k_fi_upd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx));
-  size_t mx2 = 0;
-  for (int64_t l = 0; l < nl; ++l) {
-    const size_t b = fi_upd2_smem(h->fi_smax[l], h->fi_mmax[l]);
-    if (b > mx2) mx2 = b;
-  }
-  CK(cudaFuncSetAttribute(k_fi_upd2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx2));
   CK(cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, h->device));
   CK(cudaFuncSetAttribute(k_fi_panel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)(64 * 256 * sizeof(double))));
@@ -620,16 +604,8 @@ static int run_fanin(hy_handle *h, const CallP &P, cudaStream_t st) {
     }
     if (nxp) { k_fi_x<<<nxp, 256, 2 * 64 * 65 * sizeof(double), st>>>(h->S, P, h->fi, (int)h->fi_xp[l]); h->launches++; }
     if (nup) {
-      if (h->fi_upd_v2) {
-        const size_t sm2 = fi_upd2_smem(h->fi_smax[l], h->fi_mmax[l]);
-        const int per = sm2 > 110 * 1024 ? 1 : h->fi_upd_ctas_per_sm;
-        const int grid = nup < h->sm_count * per ? nup : h->sm_count * per;
-        k_fi_upd2<<<grid, 256, sm2, st>>>(h->S, P, h->fi, (int)h->fi_up[l], nup, h->fi_smax[l],
-                                          h->fi_mmax[l]);
-      } else {
-        k_fi_upd<<<nup, 256, fi_upd_smem(h->fi_smax[l], h->fi_mmax[l]), st>>>(
-            h->S, P, h->fi, (int)h->fi_up[l], h->fi_smax[l], h->fi_mmax[l]);
-      }
+      k_fi_upd<<<nup, 256, fi_upd_smem(h->fi_smax[l], h->fi_mmax[l]), st>>>(
+          h->S, P, h->fi, (int)h->fi_up[l], h->fi_smax[l], h->fi_mmax[l]);
       h->launches++;
     }
   }
