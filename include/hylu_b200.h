@@ -189,6 +189,9 @@ typedef struct {
   const int64_t *row_rec;   /* [n][4] step0, A entry0, nsteps|nentries<<32, original row */
 } hy_row_programs;
 int hy_upload_row_programs(hy_handle *h, const hy_row_programs *progs);
+/* Pull programs for standalone hub rows of the single-instance row path (ROWROW
+ * mode); built with hub detection restricted to standalone rows. */
+int hy_upload_hub_programs(hy_handle *h, const hy_row_programs *progs);
 
 /* Batched refactorize + solve of B instances sharing the uploaded symbolic
  * structure and the prior's inner_perm / anorm.  d_vals [B][nnz], d_b / d_x [B][n]

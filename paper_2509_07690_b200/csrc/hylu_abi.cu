@@ -29,6 +29,7 @@ struct SlabDev {
 };
 __global__ void k_slab(DevSym, CallP, SlabDev, int, int *, int *, int *, int, int, int, int, int);
 __global__ void k_lperm(DevSym, CallP, const int32_t *, int);
+__global__ void k_hub1(DevSym, CallP, DevProg, const int32_t *, double *, int);
 size_t slab_smem_bytes(int, int, int, int);
 struct FaninDev {
   const int32_t *lu_nodes;
@@ -181,6 +182,15 @@ struct hy_handle {
   std::vector<int64_t> fi_lu, fi_pt, fi_xp, fi_up;   // per-level offsets
   std::vector<int32_t> fi_smax, fi_mmax;
   int sm_count = 148;
+  // single-instance hub rows (ROWROW path): programs + per-level hub node lists
+  bool hub1_ok = false;
+  DevProg prog1{};
+  std::vector<void *> hub1_allocs;
+  std::vector<int64_t> hub1_ptr;
+  int32_t *d_hub1 = nullptr;
+  int hub1_slots = 0;
+  double *d_hub1_scratch = nullptr;
+  int64_t hub1_scratch_cap = 0;
 
 };
 
@@ -313,6 +323,21 @@ static int upload_fi(hy_handle *h, T **dst, const T *src, int64_t count) {
     if (_r) return _r;                                     \
   } while (0)
 
+template <class T>
+static int upload_h1(hy_handle *h, T **dst, const T *src, int64_t count) {
+  *dst = nullptr;
+  if (count <= 0) return HY_OK;
+  CK(cudaMalloc((void **)dst, sizeof(T) * count));
+  h->hub1_allocs.push_back(*dst);
+  CK(cudaMemcpy(*dst, src, sizeof(T) * count, cudaMemcpyHostToDevice));
+  return HY_OK;
+}
+#define UPH(dst, src, cnt)                                 \
+  do {                                                     \
+    int _r = upload_h1(h, dst, src, (int64_t)(cnt));       \
+    if (_r) return _r;                                     \
+  } while (0)
+
 extern "C" {
 
 const char *hy_last_error(void) { return g_err.c_str(); }
@@ -349,6 +374,8 @@ void hy_destroy(hy_handle *h) {
   for (void *p : h->prog_allocs) cudaFree(p);
   for (void *p : h->slab_allocs) cudaFree(p);
   for (void *p : h->fi_allocs) cudaFree(p);
+  for (void *p : h->hub1_allocs) cudaFree(p);
+  if (h->d_hub1_scratch) cudaFree(h->d_hub1_scratch);
   if (h->d_bf) cudaFree(h->d_bf);
   if (h->d_scratch) cudaFree(h->d_scratch);
   if (h->d_flags) cudaFree(h->d_flags);
@@ -613,6 +640,63 @@ static int run_fanin(hy_handle *h, const CallP &P, cudaStream_t st) {
   return HY_OK;
 }
 
+int hy_upload_hub_programs(hy_handle *h, const hy_row_programs *d) {
+  if (!h || !h->uploaded || !d) return fail(HY_INVALID_ARGUMENT, "symbolic not uploaded / null");
+  CK(cudaSetDevice(h->device));
+  for (void *p : h->hub1_allocs) cudaFree(p);
+  h->hub1_allocs.clear();
+  h->hub1_ok = false;
+  const int64_t nn = h->S.nn;
+  DevProg &R = h->prog1;
+  std::vector<int32_t> hub_base(nn, -1);
+  std::vector<int64_t> first(nn + 1);
+  CK(cudaMemcpy(first.data(), h->S.first, sizeof(int64_t) * (nn + 1), cudaMemcpyDeviceToHost));
+  int32_t hr = 0;
+  for (int64_t u = 0; u < nn; ++u)
+    if (d->node_hub[u]) {
+      if (first[u + 1] - first[u] != 1) return fail(HY_INVALID_ARGUMENT, "single-path hub must be a row");
+      hub_base[u] = hr++;
+    }
+  if (hr != d->nhubrows) return fail(HY_INVALID_ARGUMENT, "hub row count mismatch");
+  if (hr == 0) return HY_OK;
+  int32_t *p32;
+  int64_t *p64;
+  UPH(&p32, hub_base.data(), nn); R.hub_base = p32;
+  UPH(&p64, d->hrow_lev, d->nhubrows + 1); R.hrow_lev = p64;
+  UPH(&p64, d->lev_wi, d->nlev + 1); R.lev_wi = p64;
+  UPH(&p32, d->wi_p, d->nwi); R.wi_p = p32;
+  UPH(&p64, d->wi_kd, d->nwi); R.wi_kd = p64;
+  UPH(&p64, d->wi_y0, d->nwi); R.wi_y0 = p64;
+  UPH(&p64, d->wi_y1, d->nwi); R.wi_y1 = p64;
+  UPH(&p32, d->wi_slot, d->nwi); R.wi_slot = p32;
+  UPH(&p64, d->lev_sp, d->nlev + 1); R.lev_sp = p64;
+  UPH(&p32, d->sp_p, d->nsp); R.sp_p = p32;
+  UPH(&p64, d->sp_kd, d->nsp); R.sp_kd = p64;
+  UPH(&p32, d->sp_s0, d->nsp); R.sp_s0 = p32;
+  UPH(&p32, d->sp_n, d->nsp); R.sp_n = p32;
+  UPH(&p32, d->pred_p, d->npred); R.pred_p = p32;
+  UPH(&p64, d->pred_u, d->npred); R.pred_u = p64;
+  h->hub1_slots = (int)(d->max_slots > 0 ? d->max_slots : 1);
+  // per factorization level: hub rows out of the row list
+  Plan &pl = h->fplan;
+  std::vector<int32_t> rows(pl.rptr[pl.nlev]);
+  if (!rows.empty())
+    CK(cudaMemcpy(rows.data(), pl.d_rows, sizeof(int32_t) * rows.size(), cudaMemcpyDeviceToHost));
+  std::vector<int32_t> keep, hubs;
+  std::vector<int64_t> rptr(pl.nlev + 1, 0);
+  h->hub1_ptr.assign(pl.nlev + 1, 0);
+  for (int l = 0; l < pl.nlev; ++l) {
+    for (int64_t k = pl.rptr[l]; k < pl.rptr[l + 1]; ++k) (d->node_hub[rows[k]] ? hubs : keep).push_back(rows[k]);
+    rptr[l + 1] = (int64_t)keep.size();
+    h->hub1_ptr[l + 1] = (int64_t)hubs.size();
+  }
+  pl.rptr = rptr;
+  UPH(&pl.d_rows, keep.data(), keep.size());
+  UPH(&h->d_hub1, hubs.data(), hubs.size());
+  h->hub1_ok = true;
+  return HY_OK;
+}
+
 static int run_factor(hy_handle *h, const double *d_avals, double eps, const hy_factors *prior,
                       hy_factors *out, cudaStream_t st) {
   if (!h || !h->uploaded) return fail(HY_INVALID_ARGUMENT, "symbolic not uploaded");
@@ -658,6 +742,19 @@ static int run_factor(hy_handle *h, const double *d_avals, double eps, const hy_
     const int ns = (int)(pl.sptr[l + 1] - pl.sptr[l]);
     if (nr) {
       k_rows<<<(nr + 3) / 4, 128, 0, st>>>(h->S, P, pl.d_rows + pl.rptr[l], nr);
+      h->launches++;
+    }
+    const int nh1 = h->hub1_ok ? (int)(h->hub1_ptr[l + 1] - h->hub1_ptr[l]) : 0;
+    if (nh1) {
+      const int64_t need = (int64_t)nh1 * h->hub1_slots;
+      if (need > h->hub1_scratch_cap) {
+        if (h->d_hub1_scratch) CK(cudaFree(h->d_hub1_scratch));
+        h->d_hub1_scratch = nullptr;
+        CK(cudaMalloc((void **)&h->d_hub1_scratch, sizeof(double) * need));
+        h->hub1_scratch_cap = need;
+      }
+      k_hub1<<<nh1, 1024, 0, st>>>(h->S, P, h->prog1, h->d_hub1 + h->hub1_ptr[l], h->d_hub1_scratch,
+                                   h->hub1_slots);
       h->launches++;
     }
     if (ns && h->slab_ok) {

@@ -499,6 +499,74 @@ __global__ void k_bwd(DevSym S, const double *F, const int32_t *nodes, int count
 }
 
 // ---------------------------------------------------------------------------
+// Hub rows of the single-instance row path (ROWROW mode): one CTA per standalone
+// row with thousands of L entries.  Pull programs (schedule.py): positions grouped
+// by intra-row dependency level; a thread takes one <= 64-term work item (the
+// position's contributions in ascending step order, the same operation order as
+// the sequential row-row loop); longer positions are split into partial sums
+// combined in slot order.  The row lives in its own factor storage (L2-resident).
+constexpr int HUB1_THREADS = 1024;
+
+__device__ __forceinline__ void hub1_final(const CallP &P, int64_t kd, double *w, int p, double acc,
+                                           const double *F, double thr, int64_t row) {
+  if (kd >= 0) {
+    acc = acc / F[kd];
+  } else if (kd == -2) {
+    bool fired;
+    const double piv = acc;
+    acc = perturb(piv, thr, fired);
+    log_pivot(P, row, piv, fired, thr);
+  }
+  w[p] = acc;
+}
+
+__global__ void __launch_bounds__(HUB1_THREADS) k_hub1(DevSym S, CallP P, DevProg R,
+                                                       const int32_t *nodes, double *scratch,
+                                                       int max_slots) {
+  const int u = nodes[blockIdx.x];
+  const int tid = threadIdx.x;
+  const int64_t i = S.first[u];
+  const int W = (int)(S.colptr[u + 1] - S.colptr[u]);
+  double *F = P.F;
+  double *w = F + S.valoff[u];
+  double *scr = scratch + (size_t)blockIdx.x * max_slots;
+  const double thr = P.eps * P.anorm[0];
+  for (int q = tid; q < W; q += HUB1_THREADS) w[q] = 0.0;
+  __syncthreads();
+  {
+    const int64_t a = S.mrow_src[i];
+    for (int64_t e = S.a_ptr[a] + tid; e < S.a_ptr[a + 1]; e += HUB1_THREADS)
+      w[S.colpos[e]] = P.A[e] * S.scale[e];
+  }
+  __syncthreads();
+  const int hr = R.hub_base[u];
+  for (int64_t lev = R.hrow_lev[hr]; lev < R.hrow_lev[hr + 1]; ++lev) {
+    for (int64_t it = R.lev_wi[lev] + tid; it < R.lev_wi[lev + 1]; it += HUB1_THREADS) {
+      const int p = R.wi_p[it];
+      const int slot = R.wi_slot[it];
+      const int64_t y1 = R.wi_y1[it];
+      double acc = slot < 0 ? w[p] : 0.0;
+      for (int64_t y = R.wi_y0[it]; y < y1; ++y) acc -= w[R.pred_p[y]] * F[R.pred_u[y]];
+      if (slot < 0)
+        hub1_final(P, R.wi_kd[it], w, p, acc, F, thr, i);
+      else
+        scr[slot] = acc;
+    }
+    if (R.lev_sp[lev + 1] > R.lev_sp[lev]) {
+      __syncthreads();
+      for (int64_t k2 = R.lev_sp[lev] + tid; k2 < R.lev_sp[lev + 1]; k2 += HUB1_THREADS) {
+        const int p = R.sp_p[k2];
+        double acc = w[p];
+        const int s0 = R.sp_s0[k2], ns = R.sp_n[k2];
+        for (int c = 0; c < ns; ++c) acc += scr[s0 + c];
+        hub1_final(P, R.sp_kd[k2], w, p, acc, F, thr, i);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Chunked substitution: per level, (node, column chunk) partial dot products of
 // every row of the node over its off-block part (L-union for forward, panel for
 // backward), written to a scratch slot; then one warp per node combines the chunk

@@ -132,6 +132,7 @@ def library():
     lib.hy_set_option.argtypes = [vp, ctypes.c_char_p, i64]
     lib.hy_upload_slab_plan.argtypes = [vp, ctypes.POINTER(SlabPlanDesc)]
     lib.hy_upload_fanin_plan.argtypes = [vp, ctypes.POINTER(FaninPlanDesc)]
+    lib.hy_upload_hub_programs.argtypes = [vp, ctypes.POINTER(ProgramsDesc)]
     _lib = lib
     return lib
 
@@ -207,8 +208,20 @@ class DeviceContext:
             else "rows"
         if self.path == "fanin":
             self.upload_fanin_plan()
-        elif _sc.slab_nodes(s, self.wide_row).any():
-            self.upload_slab_plan()
+        else:
+            if _sc.slab_nodes(s, self.wide_row).any():
+                self.upload_slab_plan()
+            self.upload_hub_programs()
+
+    def upload_hub_programs(self):
+        """Pull programs for standalone hub rows of the row path (ROWROW mode)."""
+        from . import schedule
+        hub = int(os.environ.get("HYLU_HUB_STEPS", schedule.HUB_STEPS))
+        progs = schedule.build_programs(self.analysis, np.zeros(self.n, np.int64), hub,
+                                        standalone_only=True)
+        if not len(progs.hub_nodes):
+            return
+        self._desc_programs(progs, self.lib.hy_upload_hub_programs)
 
     def upload_fanin_plan(self):
         from . import schedule
@@ -301,6 +314,9 @@ class DeviceContext:
 
     def upload_programs(self, progs):
         """Upload schedule.RowPrograms (built for a prior inner_perm)."""
+        self._desc_programs(progs, self.lib.hy_upload_row_programs)
+
+    def _desc_programs(self, progs, fn):
         arrs = {k: np.ascontiguousarray(getattr(progs, k)) for k in (
             "row_ptr", "st_p", "st_j", "st_src", "st_cnt", "st_rel", "rel", "node_hub", "hrow_lev",
             "lev_ptr", "hpos", "hdiv", "hpp", "pred_p", "pred_u", "lev_wi", "wi_p", "wi_kd", "wi_y0",
@@ -315,8 +331,9 @@ class DeviceContext:
         for k, v in arrs.items():
             setattr(d, k, v.ctypes.data if v.size else None)
         with self.torch.cuda.device(self.device):
-            check(self.lib.hy_upload_row_programs(self.h, ctypes.byref(d)))
-        self._programs = arrs
+            check(fn(self.h, ctypes.byref(d)))
+        self._programs = getattr(self, "_programs", [])
+        self._programs.append(arrs)
 
     def set_option(self, name, value):
         check(self.lib.hy_set_option(self.h, name.encode(), int(value)))

@@ -31,7 +31,7 @@ HUB_STEPS = 384
 
 @njit(cache=True)
 def _programs(n, first, kind, colptr, cols, nl, valoff, node_of, a_ptr, mrow_src, colpos, iperm,
-              hub_steps):
+              hub_steps, standalone_only):
     nn = len(kind)
     # upper bounds for allocation: steps <= sum of L widths incl. in-block parts
     max_steps = 0
@@ -98,7 +98,7 @@ def _programs(n, first, kind, colptr, cols, nl, valoff, node_of, a_ptr, mrow_src
                     nrel += 1
                 nst += 1
             row_ptr[i + 1] = nst
-            if row_ptr[i + 1] - row_ptr[i] > hub_steps:
+            if row_ptr[i + 1] - row_ptr[i] > hub_steps and (kind[u] == 0 or not standalone_only):
                 node_hub[u] = 1
         for q in range(W):
             pos_of[cols[c0 + q]] = -1
@@ -330,13 +330,13 @@ class RowPrograms:
 HUB_CHUNK = 64
 
 
-def build_programs(an, inner_perm, hub_steps=HUB_STEPS, chunk=HUB_CHUNK):
+def build_programs(an, inner_perm, hub_steps=HUB_STEPS, chunk=HUB_CHUNK, standalone_only=False):
     s = an.symbolic
     vm = an.vmap
     ip = np.ascontiguousarray(inner_perm, np.int64)
     (row_ptr, st_p, st_j, st_src, st_cnt, st_rel, rel, node_hub) = _programs(
         s.n, s.node_first, s.node_kind, s.colptr, s.cols, s.nl, s.valoff, s.node_of,
-        an.A.row_ptr, vm.mrow_src, vm.colpos, ip, hub_steps)
+        an.A.row_ptr, vm.mrow_src, vm.colpos, ip, hub_steps, standalone_only)
     hub_nodes = np.flatnonzero(node_hub).astype(np.int32)
     if len(hub_nodes):
         hrow_lev, lev_ptr, hpos, hdiv, hpp, pred_p, pred_u = _pull(

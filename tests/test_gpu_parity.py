@@ -115,3 +115,20 @@ def test_batched_factor_values_match_oracle():
         ref = on.factorize(an, bp.values[b], prior=oprior)
         got = br.factor_values(b).cpu().numpy()
         assert _rel(got, ref.values) <= LU_RTOL
+
+
+@pytest.mark.parametrize("name", ["c1", "c0", "c3"])
+def test_single_path_hub_rows(name, monkeypatch):
+    """ROWROW row path with standalone rows above a tiny step threshold routed to the
+    single-instance pull kernel (k_hub1)."""
+    monkeypatch.setenv("HYLU_HUB_STEPS", "6")
+    p, an = _analysis(name, 0)
+    on = _oracle()
+    ref = on.factorize(an)
+    f = api.factorize_analysis(an)
+    assert np.array_equal(f.host_inner_perm(), ref.inner_perm)
+    assert _rel(f.host_values(), ref.values) <= LU_RTOL
+    f2 = api.refactorize(p.A, f)
+    assert np.array_equal(f2.host_values(), f.host_values())
+    x, _ = api.solve(p.A, f, b=p.b)
+    assert np.linalg.norm(refmatrix.spmv(p.A, x) - p.b) / np.linalg.norm(p.b) <= RES_TOL
