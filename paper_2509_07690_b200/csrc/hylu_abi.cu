@@ -74,7 +74,7 @@ __global__ void k_bwd_fin(DevSym, const double *, const int32_t *, const int32_t
 __global__ void k_bwd(DevSym, const double *, const int32_t *, int, double *);
 template <bool STAGED>
 __global__ void k_bt_pipe(DevSym, BatchP, DevProg, const int2 *, int64_t, const double *, double *, int *, int *,
-                          int, int);
+                          int, int, int);
 __global__ void k_bt_hub(DevSym, BatchP, DevProg, const int32_t *, int, int, const double *, double *,
                          double *, int, int *, int);
 __global__ void k_batch_bhat(DevSym, const int32_t *, const double *, double *, int64_t);
@@ -152,6 +152,8 @@ struct hy_handle {
   int pipe_blocks = 0;
   int gbatch = 1 << 20;                    // unused (kept for hy_set_option compatibility)
   int staged = 0;                          // stage row sources with cp.async (option "staged")
+  int nowait = 0;                          // timing experiment only: skip dependency waits
+  int skew = 1;                            // diagonal claim order: group g+1 runs `skew` levels behind g
   // diagonal claim order per (segment, G): pair prefix sums, (level<<16|group), level offsets
   struct Seg {
     int l0, l1;
@@ -275,10 +277,14 @@ static int build_segments(hy_handle *h, int G) {
     const int L = l1 - l;
     std::vector<int2> tasks;
     tasks.reserve((size_t)(h->bl_rptr[l1] - h->bl_rptr[l]) * G);
-    for (int d = 0; d < G + L - 1; ++d)
-      for (int k = (d - G + 1 > 0 ? d - G + 1 : 0); k <= (d < L - 1 ? d : L - 1); ++k)
-        for (int64_t q = h->bl_rptr[l + k]; q < h->bl_rptr[l + k + 1]; ++q)
-          tasks.push_back(make_int2(rows[q], d - k));
+    const int sk = h->skew;
+    for (int d = 0; d < sk * (G - 1) + L; ++d)
+      for (int k = 0; k < L && k <= d; ++k) {
+        if ((d - k) % sk) continue;
+        const int g = (d - k) / sk;
+        if (g >= G) continue;
+        for (int64_t q = h->bl_rptr[l + k]; q < h->bl_rptr[l + k + 1]; ++q) tasks.push_back(make_int2(rows[q], g));
+      }
     sg.ntasks = (int64_t)tasks.size();
     if (sg.ntasks) {
       CK(cudaMalloc((void **)&sg.d_tasks, sizeof(int2) * sg.ntasks));
@@ -392,6 +398,15 @@ int hy_set_option(hy_handle *h, const char *name, int64_t value) {
   if (!h || !name) return fail(HY_INVALID_ARGUMENT, "null handle/name");
   if (std::string(name) == "group_batch" && value >= 1) {
     h->gbatch = (int)value;
+    return HY_OK;
+  }
+  if (std::string(name) == "diagonal_skew" && value >= 1) {
+    h->skew = (int)value;
+    h->segs_G = -1;
+    return HY_OK;
+  }
+  if (std::string(name) == "nowait_experiment") {
+    h->nowait = value != 0;
     return HY_OK;
   }
   if (std::string(name) == "staged") {
@@ -995,10 +1010,10 @@ int hy_refactorize_batched(hy_handle *h, int64_t B, const double *d_vals, double
       int *ctr = (int *)((long long *)h->d_counters + si);
       if (h->staged)
         k_bt_pipe<true><<<h->pipe_blocks, 128, pipe_smem_bytes(true), st>>>(
-            h->S, P, h->prog, sg.d_tasks, sg.ntasks, d_b_fuse, h->d_by, ctr, h->d_flags, h->epoch, G);
+            h->S, P, h->prog, sg.d_tasks, sg.ntasks, d_b_fuse, h->d_by, ctr, h->d_flags, h->epoch, G, h->nowait);
       else
         k_bt_pipe<false><<<h->pipe_blocks, 128, pipe_smem_bytes(false), st>>>(
-            h->S, P, h->prog, sg.d_tasks, sg.ntasks, d_b_fuse, h->d_by, ctr, h->d_flags, h->epoch, G);
+            h->S, P, h->prog, sg.d_tasks, sg.ntasks, d_b_fuse, h->d_by, ctr, h->d_flags, h->epoch, G, h->nowait);
       h->launches++;
     }
   }

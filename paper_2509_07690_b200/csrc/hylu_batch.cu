@@ -251,7 +251,7 @@ size_t pipe_smem_bytes(bool staged) {
 template <bool STAGED>
 __global__ void __launch_bounds__(PIPE_WARPS * 32, STAGED ? 3 : 6)
     k_bt_pipe(DevSym S, BatchP P, DevProg R, const int2 *tasks, int64_t total, const double *rhs,
-              double *Y, int *counter, int *flags, int epoch, int G) {
+              double *Y, int *counter, int *flags, int epoch, int G, int nowait) {
   extern __shared__ __align__(16) double pipe_smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int SG = STAGED ? STAGE : 0;
@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(PIPE_WARPS * 32, STAGED ? 3 : 6)
     // lanes poll the dependency flags in parallel (acquire); the warp barrier then
     // orders every lane's subsequent loads after the producers' releases
     const int64_t d0 = nr.y, d1 = S.dptr[u + 1];
-    for (int64_t k = d0 + lane; k < d1; k += 32) {
+    for (int64_t k = d0 + lane; k < d1 && !nowait; k += 32) {
       const int *f = flags + (int64_t)S.deps[k] * G + g;
       while (ld_acquire(f) != epoch) __nanosleep(64);
     }
@@ -283,9 +283,9 @@ __global__ void __launch_bounds__(PIPE_WARPS * 32, STAGED ? 3 : 6)
 }
 
 template __global__ void k_bt_pipe<false>(DevSym, BatchP, DevProg, const int2 *, int64_t,
-                                          const double *, double *, int *, int *, int, int);
+                                          const double *, double *, int *, int *, int, int, int);
 template __global__ void k_bt_pipe<true>(DevSym, BatchP, DevProg, const int2 *, int64_t,
-                                         const double *, double *, int *, int *, int, int);
+                                         const double *, double *, int *, int *, int, int, int);
 
 // ---------------------------------------------------------------------------
 // Hub kernel: one CTA per (hub node, group).  Pull programs: the positions of a row

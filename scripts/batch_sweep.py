@@ -24,8 +24,9 @@ dr = torch.from_numpy(rhs).cuda()
 x = torch.empty((B, 20000), dtype=torch.float64, device="cuda")
 npert = torch.empty(B, dtype=torch.int32, device="cuda")
 ctx = br.ctx
+opt = os.environ.get("SWEEP_OPT", "staged")
 for gb in [int(a) for a in sys.argv[1:]] or [0, 1]:
-    ctx.set_option("staged", gb)
+    ctx.set_option(opt, gb)
     for _ in range(2):
         br.run(dv, dr, x, npert)
     ts = []
@@ -39,4 +40,4 @@ for gb in [int(a) for a in sys.argv[1:]] or [0, 1]:
     xh = x[:2].cpu().numpy()
     res = max(np.linalg.norm(refmatrix.spmv(A0.with_values(vals[b]), xh[b]) - rhs[b]) / np.linalg.norm(rhs[b])
               for b in range(2))
-    print("staged %4d  ms %.3f (min %.3f)  inst/s %.0f  res %.1e" % (gb, np.median(ts), min(ts), B / min(ts) * 1e3, res), flush=True)
+    print(opt + " %4d  ms %.3f (min %.3f)  inst/s %.0f  res %.1e" % (gb, np.median(ts), min(ts), B / min(ts) * 1e3, res), flush=True)
