@@ -309,49 +309,93 @@ __global__ void __launch_bounds__(FI_THREADS) k_fi_upd(DevSym S, CallP P, FaninD
     const int qbase = vnl + vs + q0;
     __syncthreads();
     if (tid < nq) spos[tid] = lower_bound_i32(tcol, 0, tw, S.cols[vc0 + qbase + tid]);
-    // DMMA: warp w owns output rows 8w..8w+7 and all eight 8-column blocks;
-    // mma.sync.m8n8k4 f64 fragments: A(8x4) one element per lane (row lane/4,
-    // col lane%4), B(4x8) one element (row lane%4, col lane/4), C(8x8) two
-    // elements (row lane/4, cols 2*(lane%4) + {0,1}).
-    const int warp = tid >> 5, lane = tid & 31;
-    const int arow = warp * 8 + (lane >> 2), kq = lane & 3;
-    const bool wact = warp * 8 < s;
+    // Large contractions (target >= 32 rows, source block >= 16) run on the FP64
+    // tensor cores: mma.sync.m8n8k4 f64 (DMMA), the 8x8 output tiles spread over
+    // the 8 warps; fragments: A(8x4) one element per lane (row lane/4, col lane%4),
+    // B(4x8) one element (row lane%4, col lane/4), C(8x8) two elements (row
+    // lane/4, cols 2*(lane%4)+{0,1}).  Smaller ones use 4x4 FFMA register tiles.
+    const bool dmma = s >= 32 && m >= 16;
+    const int warp = tid >> 5, lane = tid & 31, kq = lane & 3, lr = lane >> 2;
+    const int nrb = (s + 7) >> 3, ncb = (nq + 7) >> 3, ntile = nrb * ncb;
     double d[8][2];
+    double c4[4][4];
 #pragma unroll
-    for (int cb = 0; cb < 8; ++cb) d[cb][0] = d[cb][1] = 0.0;
+    for (int j2 = 0; j2 < 8; ++j2) d[j2][0] = d[j2][1] = 0.0;
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) c4[x][y] = 0.0;
     for (int k0 = 0; k0 < m; k0 += FI_KC) {
       const int kc = min(FI_KC, m - k0);
+      const int kc4 = (kc + 3) & ~3;
       if (k0) __syncthreads();
-      for (int idx = tid; idx < s * FI_KC; idx += FI_THREADS) {
-        const int t = idx / FI_KC, a = idx - t * FI_KC;
+      for (int idx = tid; idx < s * kc4; idx += FI_THREADS) {
+        const int t = idx / kc4, a = idx - t * kc4;
         Xs[t * KLD + a] = a < kc ? Pm[(int64_t)t * W + pb0 + k0 + a] : 0.0;
       }
-      for (int idx = tid; idx < FI_KC * FI_TILE; idx += FI_THREADS) {
+      for (int idx = tid; idx < kc4 * FI_TILE; idx += FI_THREADS) {
         const int a = idx >> 6, c = idx & 63;
         Ut[a * FXLD + c] = (c < nq && a < kc) ? vb[(int64_t)(tb0 + k0 + a) * vW + qbase + c] : 0.0;
       }
       __syncthreads();
-      if (wact) {
+      if (dmma) {
         for (int k = 0; k < kc; k += 4) {
-          const double av = arow < s ? Xs[arow * KLD + k + kq] : 0.0;
 #pragma unroll
-          for (int cb = 0; cb < 8; ++cb) {
-            const double bv = Ut[(k + kq) * FXLD + cb * 8 + (lane >> 2)];
-            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                         : "+d"(d[cb][0]), "+d"(d[cb][1])
-                         : "d"(av), "d"(bv));
+          for (int j2 = 0; j2 < 8; ++j2) {
+            const int ti = warp + 8 * j2;
+            if (ti < ntile) {
+              const int rb = ti / ncb, cb = ti - rb * ncb;
+              const int ar = rb * 8 + lr;
+              const double av = ar < s ? Xs[ar * KLD + k + kq] : 0.0;
+              const double bv = Ut[(k + kq) * FXLD + cb * 8 + lr];
+              asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                           : "+d"(d[j2][0]), "+d"(d[j2][1])
+                           : "d"(av), "d"(bv));
+            }
           }
+        }
+      } else {
+        for (int a = 0; a < kc; ++a) {
+          double xv[4], uv[4];
+#pragma unroll
+          for (int x = 0; x < 4; ++x) xv[x] = (tr + 16 * x < s) ? Xs[(tr + 16 * x) * KLD + a] : 0.0;
+#pragma unroll
+          for (int y = 0; y < 4; ++y) uv[y] = Ut[a * FXLD + tcl + 16 * y];
+#pragma unroll
+          for (int x = 0; x < 4; ++x)
+#pragma unroll
+            for (int y = 0; y < 4; ++y) c4[x][y] = fma(xv[x], uv[y], c4[x][y]);
         }
       }
     }
-    if (wact && arow < s) {
+    if (dmma) {
 #pragma unroll
-      for (int cb = 0; cb < 8; ++cb)
+      for (int j2 = 0; j2 < 8; ++j2) {
+        const int ti = warp + 8 * j2;
+        if (ti < ntile) {
+          const int rb = ti / ncb, cb = ti - rb * ncb;
+          const int t = rb * 8 + lr;
+          if (t < s) {
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int c = cb * 8 + kq * 2 + e;
-          if (c < nq) acc[arow * FI_TILE + spos[c]] -= d[cb][e];
+            for (int e = 0; e < 2; ++e) {
+              const int c = cb * 8 + kq * 2 + e;
+              if (c < nq) acc[t * FI_TILE + spos[c]] -= d[j2][e];
+            }
+          }
         }
+      }
+    } else {
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        const int t = tr + 16 * x;
+        if (t < s) {
+#pragma unroll
+          for (int y = 0; y < 4; ++y) {
+            const int c = tcl + 16 * y;
+            if (c < nq) acc[t * FI_TILE + spos[c]] -= c4[x][y];
+          }
+        }
+      }
     }
   }
   __syncthreads();
