@@ -150,6 +150,7 @@ typedef struct {
   const int32_t *dep_pb;                                           /* [ndeps] */
   const int32_t *level_smax, *level_mmax;                          /* [nlevels] */
   const int32_t *src_v, *src_pb, *src_tb;   /* [nsrc] source node, block position, first block row */
+  const int64_t *lev_up_big;                /* [nlevels] first item routed to the DMMA kernel */
 } hy_fanin_plan;
 int hy_upload_fanin_plan(hy_handle *h, const hy_fanin_plan *plan);
 
@@ -213,7 +214,8 @@ int hy_solve_batched(hy_handle *h, int64_t B, const double *d_b, double *d_x, ui
 int hy_batched_factor_values(hy_handle *h, int64_t b, double *d_out, uintptr_t stream);
 
 /* Tuning knobs: "staged" (0/1: stage each row's source values in shared memory
- * with cp.async in the batched pipeline kernel, default 0). */
+ * with cp.async in the batched pipeline kernel, default 0); "fanin_dmma" (0/1:
+ * route update items of targets with >= 32 rows to the DMMA kernel, default 1). */
 int hy_set_option(hy_handle *h, const char *name, int64_t value);
 
 /* Number of kernel launches issued by this handle since creation (bench evidence). */

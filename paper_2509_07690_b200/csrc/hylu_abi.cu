@@ -56,6 +56,7 @@ __global__ void k_fi_lu(DevSym, CallP, FaninDev, int);
 __global__ void k_fi_panel(DevSym, CallP, FaninDev, int);
 __global__ void k_fi_x(DevSym, CallP, FaninDev, int);
 __global__ void k_fi_upd(DevSym, CallP, FaninDev, int, int, int);
+__global__ void k_fi_upd_mma(DevSym, CallP, FaninDev, int, int, int);
 size_t fi_upd_smem(int, int);
 size_t pipe_smem_bytes(bool staged);
 __global__ void k_bhat(DevSym, const int32_t *, const double *, double *);
@@ -182,6 +183,8 @@ struct hy_handle {
   FaninDev fi{};
   std::vector<void *> fi_allocs;
   std::vector<int64_t> fi_lu, fi_pt, fi_xp, fi_up;   // per-level offsets
+  std::vector<int64_t> fi_upbig;                     // per level: first DMMA-routed item
+  int fi_mma = 1;                                    // option "fanin_dmma"
   std::vector<int32_t> fi_smax, fi_mmax;
   int sm_count = 148;
   // single-instance hub rows (ROWROW path): programs + per-level hub node lists
@@ -400,6 +403,10 @@ int hy_set_option(hy_handle *h, const char *name, int64_t value) {
     h->gbatch = (int)value;
     return HY_OK;
   }
+  if (std::string(name) == "fanin_dmma") {
+    h->fi_mma = value != 0;
+    return HY_OK;
+  }
   if (std::string(name) == "diagonal_skew" && value >= 1) {
     h->skew = (int)value;
     h->segs_G = -1;
@@ -612,6 +619,7 @@ int hy_upload_fanin_plan(hy_handle *h, const hy_fanin_plan *d) {
   h->fi_pt.assign(d->pt_ptr, d->pt_ptr + nl + 1);
   h->fi_xp.assign(d->xp_ptr, d->xp_ptr + nl + 1);
   h->fi_up.assign(d->lev_up, d->lev_up + nl + 1);
+  h->fi_upbig.assign(d->lev_up_big, d->lev_up_big + nl);
   h->fi_smax.assign(d->level_smax, d->level_smax + nl);
   h->fi_mmax.assign(d->level_mmax, d->level_mmax + nl);
   size_t mx = 0;
@@ -620,6 +628,7 @@ int hy_upload_fanin_plan(hy_handle *h, const hy_fanin_plan *d) {
     if (b > mx) mx = b;
   }
   CK(cudaFuncSetAttribute(k_fi_upd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx));
+  CK(cudaFuncSetAttribute(k_fi_upd_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx));
   CK(cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, h->device));
   CK(cudaFuncSetAttribute(k_fi_panel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)(64 * 256 * sizeof(double))));
@@ -646,9 +655,17 @@ static int run_fanin(hy_handle *h, const CallP &P, cudaStream_t st) {
     }
     if (nxp) { k_fi_x<<<nxp, 256, 2 * 64 * 65 * sizeof(double), st>>>(h->S, P, h->fi, (int)h->fi_xp[l]); h->launches++; }
     if (nup) {
-      k_fi_upd<<<nup, 256, fi_upd_smem(h->fi_smax[l], h->fi_mmax[l]), st>>>(
-          h->S, P, h->fi, (int)h->fi_up[l], h->fi_smax[l], h->fi_mmax[l]);
-      h->launches++;
+      const size_t sm = fi_upd_smem(h->fi_smax[l], h->fi_mmax[l]);
+      const int split = h->fi_mma ? (int)h->fi_upbig[l] : (int)h->fi_up[l + 1];
+      const int nsm = split - (int)h->fi_up[l], nbig = (int)h->fi_up[l + 1] - split;
+      if (nsm) {
+        k_fi_upd<<<nsm, 256, sm, st>>>(h->S, P, h->fi, (int)h->fi_up[l], h->fi_smax[l], h->fi_mmax[l]);
+        h->launches++;
+      }
+      if (nbig) {
+        k_fi_upd_mma<<<nbig, 256, sm, st>>>(h->S, P, h->fi, split, h->fi_smax[l], h->fi_mmax[l]);
+        h->launches++;
+      }
     }
   }
   CK(cudaGetLastError());

@@ -309,22 +309,105 @@ __global__ void __launch_bounds__(FI_THREADS) k_fi_upd(DevSym S, CallP P, FaninD
     const int qbase = vnl + vs + q0;
     __syncthreads();
     if (tid < nq) spos[tid] = lower_bound_i32(tcol, 0, tw, S.cols[vc0 + qbase + tid]);
+    double c4[4][4];
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) c4[x][y] = 0.0;
+    for (int k0 = 0; k0 < m; k0 += FI_KC) {
+      const int kc = min(FI_KC, m - k0);
+      if (k0) __syncthreads();
+      for (int idx = tid; idx < s * kc; idx += FI_THREADS) {
+        const int t = idx / kc, a = idx - t * kc;
+        Xs[t * KLD + a] = Pm[(int64_t)t * W + pb0 + k0 + a];
+      }
+      for (int idx = tid; idx < kc * FI_TILE; idx += FI_THREADS) {
+        const int a = idx >> 6, c = idx & 63;
+        Ut[a * FXLD + c] = c < nq ? vb[(int64_t)(tb0 + k0 + a) * vW + qbase + c] : 0.0;
+      }
+      __syncthreads();
+      for (int a = 0; a < kc; ++a) {
+        double xv[4], uv[4];
+#pragma unroll
+        for (int x = 0; x < 4; ++x) xv[x] = (tr + 16 * x < s) ? Xs[(tr + 16 * x) * KLD + a] : 0.0;
+#pragma unroll
+        for (int y = 0; y < 4; ++y) uv[y] = Ut[a * FXLD + tcl + 16 * y];
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y) c4[x][y] = fma(xv[x], uv[y], c4[x][y]);
+      }
+    }
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      const int t = tr + 16 * x;
+      if (t < s) {
+#pragma unroll
+        for (int y = 0; y < 4; ++y) {
+          const int c = tcl + 16 * y;
+          if (c < nq) acc[t * FI_TILE + spos[c]] -= c4[x][y];
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int idx = tid; idx < s * FI_TILE; idx += FI_THREADS) {
+    const int t = idx / FI_TILE, c = idx - t * FI_TILE;
+    if (c < tw) Pm[(int64_t)t * W + c0 + c] = acc[idx];
+  }
+}
+
+__global__ void __launch_bounds__(FI_THREADS) k_fi_upd_mma(DevSym S, CallP P, FaninDev D, int base,
+                                                       int Smax, int Mmax) {
+  extern __shared__ __align__(16) double fs[];
+  __shared__ int tcol[FI_TILE];
+  __shared__ int spos[FI_TILE];
+  const int j = base + blockIdx.x;
+  const int T = D.up_t[j];
+  const int c0 = D.up_c0[j], c1 = D.up_c1[j];
+  const int tw = c1 - c0;
+  const int tid = threadIdx.x;
+  const int r = (int)S.first[T];
+  const int s = (int)(S.first[T + 1] - r);
+  const int64_t tc0 = S.colptr[T];
+  const int W = (int)(S.colptr[T + 1] - tc0);
+  double *Pm = P.F + S.valoff[T];
+  double *acc = fs;                          // s x FI_TILE
+  double *Xs = acc + (size_t)Smax * FI_TILE; // Smax x KLD
+  double *Ut = Xs + (size_t)Smax * KLD;      // FI_KC x FXLD
+  (void)Mmax;
+  for (int c = tid; c < tw; c += FI_THREADS) tcol[c] = S.cols[tc0 + c0 + c];
+  for (int idx = tid; idx < s * FI_TILE; idx += FI_THREADS) {
+    const int t = idx / FI_TILE, c = idx - t * FI_TILE;
+    acc[idx] = c < tw ? Pm[(int64_t)t * W + c0 + c] : 0.0;
+  }
+  for (int64_t z = D.up_ptr[j]; z < D.up_ptr[j + 1]; ++z) {
+    const int v = D.src_v[z];
+    const int q0 = D.src_q0[z];
+    const int nq = D.src_q1[z] - q0;
+    const int vf = (int)S.first[v];
+    const int vs = (int)(S.first[v + 1] - vf);
+    const int64_t vc0 = S.colptr[v];
+    const int vW = (int)(S.colptr[v + 1] - vc0);
+    const int vnl = S.nl[v];
+    const double *vb = P.F + S.valoff[v];
+    const int pb0 = D.src_pb[z];
+    const int tb0 = D.src_tb[z];
+    const int m = vs - tb0;
+    const int qbase = vnl + vs + q0;
+    __syncthreads();
+    if (tid < nq) spos[tid] = lower_bound_i32(tcol, 0, tw, S.cols[vc0 + qbase + tid]);
     // Large contractions (target >= 32 rows, source block >= 16) run on the FP64
     // tensor cores: mma.sync.m8n8k4 f64 (DMMA), the 8x8 output tiles spread over
     // the 8 warps; fragments: A(8x4) one element per lane (row lane/4, col lane%4),
     // B(4x8) one element (row lane%4, col lane/4), C(8x8) two elements (row
     // lane/4, cols 2*(lane%4)+{0,1}).  Smaller ones use 4x4 FFMA register tiles.
-    const bool dmma = s >= 32 && m >= 16;
+    const bool dmma = true;
     const int warp = tid >> 5, lane = tid & 31, kq = lane & 3, lr = lane >> 2;
     const int nrb = (s + 7) >> 3, ncb = (nq + 7) >> 3, ntile = nrb * ncb;
     double d[8][2];
-    double c4[4][4];
 #pragma unroll
     for (int j2 = 0; j2 < 8; ++j2) d[j2][0] = d[j2][1] = 0.0;
-#pragma unroll
-    for (int x = 0; x < 4; ++x)
-#pragma unroll
-      for (int y = 0; y < 4; ++y) c4[x][y] = 0.0;
     for (int k0 = 0; k0 < m; k0 += FI_KC) {
       const int kc = min(FI_KC, m - k0);
       const int kc4 = (kc + 3) & ~3;
@@ -354,18 +437,6 @@ __global__ void __launch_bounds__(FI_THREADS) k_fi_upd(DevSym S, CallP P, FaninD
             }
           }
         }
-      } else {
-        for (int a = 0; a < kc; ++a) {
-          double xv[4], uv[4];
-#pragma unroll
-          for (int x = 0; x < 4; ++x) xv[x] = (tr + 16 * x < s) ? Xs[(tr + 16 * x) * KLD + a] : 0.0;
-#pragma unroll
-          for (int y = 0; y < 4; ++y) uv[y] = Ut[a * FXLD + tcl + 16 * y];
-#pragma unroll
-          for (int x = 0; x < 4; ++x)
-#pragma unroll
-            for (int y = 0; y < 4; ++y) c4[x][y] = fma(xv[x], uv[y], c4[x][y]);
-        }
       }
     }
     if (dmma) {
@@ -384,18 +455,6 @@ __global__ void __launch_bounds__(FI_THREADS) k_fi_upd(DevSym S, CallP P, FaninD
           }
         }
       }
-    } else {
-#pragma unroll
-      for (int x = 0; x < 4; ++x) {
-        const int t = tr + 16 * x;
-        if (t < s) {
-#pragma unroll
-          for (int y = 0; y < 4; ++y) {
-            const int c = tcl + 16 * y;
-            if (c < nq) acc[t * FI_TILE + spos[c]] -= c4[x][y];
-          }
-        }
-      }
     }
   }
   __syncthreads();
@@ -405,6 +464,8 @@ __global__ void __launch_bounds__(FI_THREADS) k_fi_upd(DevSym S, CallP P, FaninD
   }
 }
 
+// (k_fi_upd_mma: the same item loop with every contraction on DMMA; the host
+// routes items whose target has >= 32 rows to it.)
 size_t fi_upd_smem(int Smax, int Mmax) {
   (void)Mmax;
   return ((size_t)Smax * FI_TILE + (size_t)Smax * KLD + (size_t)FI_KC * FXLD) * sizeof(double);

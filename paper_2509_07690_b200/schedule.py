@@ -802,6 +802,7 @@ class FaninPlan:
     dep_pb: np.ndarray
     level_smax: np.ndarray     # max target rows among update items of a level
     level_mmax: np.ndarray     # max source rows of a level
+    lev_up_big: np.ndarray     # per level: first update item whose target has >= BIG_ROWS rows
 
     @property
     def nlevels(self):
@@ -835,6 +836,30 @@ def _fanin_levels(first, colptr, cols, nl, dptr, deps, node_of):
     return lev
 
 
+BIG_ROWS = 32
+
+
+def _split_items(out, rows, nlev):
+    """Within each level, order update items small-target first, big (>= BIG_ROWS rows)
+    after, so each group is a contiguous launch range (FFMA / DMMA kernels)."""
+    (lu_ptr, lu_nodes, pt_ptr, pt_node, pt_c0, pt_c1, xp_ptr, xp_edge, xp_tgt,
+     lev_up, up_t, up_c0, up_c1, up_ptr, src_k, src_q0, src_q1) = out
+    nitem = len(up_t)
+    lvl = np.repeat(np.arange(nlev), np.diff(lev_up))
+    big = (rows[up_t] >= BIG_ROWS).astype(np.int64)
+    order = np.lexsort((big, lvl))
+    cnt = np.diff(up_ptr)[order]
+    new_ptr = np.zeros(nitem + 1, np.int64)
+    np.cumsum(cnt, out=new_ptr[1:])
+    gather = np.repeat(up_ptr[:-1][order], cnt) + (np.arange(new_ptr[-1]) - np.repeat(new_ptr[:-1], cnt))
+    nsmall = np.bincount(lvl[big == 0], minlength=nlev) if nitem else np.zeros(nlev, np.int64)
+    split = lev_up[:-1] + nsmall
+    out = (lu_ptr, lu_nodes, pt_ptr, pt_node, pt_c0, pt_c1, xp_ptr, xp_edge, xp_tgt, lev_up,
+           up_t[order], up_c0[order], up_c1[order], new_ptr, src_k[gather], src_q0[gather],
+           src_q1[gather])
+    return out, split.astype(np.int64)
+
+
 def build_fanin_plan(sym, tw=FANIN_TILE, pw=PANEL_TILE):
     s = sym
     flev = _fanin_levels(s.node_first, s.colptr, s.cols, s.nl, s.dep_ptr, s.deps, s.node_of)
@@ -843,6 +868,7 @@ def build_fanin_plan(sym, tw=FANIN_TILE, pw=PANEL_TILE):
                       flev, nlev, tw, pw)
     dep_pb = _dep_block_pos(s.node_first, s.node_kind, s.colptr, s.cols, s.nl, s.dep_ptr, s.deps)
     rows = np.diff(s.node_first)
+    out, split = _split_items(out, rows, nlev)
     lu_ptr, lu_nodes = out[0], out[1]
     lev_up, up_t = out[9], out[10]
     smax = np.ones(nlev, np.int32)
@@ -854,7 +880,7 @@ def build_fanin_plan(sym, tw=FANIN_TILE, pw=PANEL_TILE):
         nodes = lu_nodes[lu_ptr[lv]:lu_ptr[lv + 1]]
         if len(nodes):
             mmax[lv] = int(rows[nodes].max())
-    return FaninPlan(*out, dep_pb, smax, mmax)
+    return FaninPlan(*out, dep_pb, smax, mmax, split)
 
 
 def fanin_source_records(sym, plan):
