@@ -215,7 +215,7 @@ int hy_batched_factor_values(hy_handle *h, int64_t b, double *d_out, uintptr_t s
 
 /* Tuning knobs: "staged" (0/1: stage each row's source values in shared memory
  * with cp.async in the batched pipeline kernel, default 0); "fanin_dmma" (0/1:
- * route update items of targets with >= 32 rows to the DMMA kernel, default 1). */
+ * route update items of targets with >= 32 rows to the DMMA kernel, default 0). */
 int hy_set_option(hy_handle *h, const char *name, int64_t value);
 
 /* Number of kernel launches issued by this handle since creation (bench evidence). */

@@ -184,7 +184,7 @@ struct hy_handle {
   std::vector<void *> fi_allocs;
   std::vector<int64_t> fi_lu, fi_pt, fi_xp, fi_up;   // per-level offsets
   std::vector<int64_t> fi_upbig;                     // per level: first DMMA-routed item
-  int fi_mma = 1;                                    // option "fanin_dmma"
+  int fi_mma = 0;                                    // option "fanin_dmma" (bitwise-equal results; slower here)
   std::vector<int32_t> fi_smax, fi_mmax;
   int sm_count = 148;
   // single-instance hub rows (ROWROW path): programs + per-level hub node lists
