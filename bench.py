@@ -292,6 +292,13 @@ def run_ours(args):
                          "parallel over instances), %.1f s" % (sample, cdt)}
 
     peak, peak_kind = _peaks()
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as fh:
+            tj = json.load(fh)
+        traffic = float(sum(v for k, v in tj.items() if k.startswith("k_"))) * B / N_INST
+    except Exception:
+        traffic = None
     bytes_per_inst = 8 * (A0.nnz + s.fill_nnz)
     achieved = B * bytes_per_inst / (fac_ms / 1e3) / 1e9
     if rank == 0:
@@ -308,7 +315,7 @@ def run_ours(args):
                        "l2": "inputs larger than L2 (values %.2f GB/step)" % (vals.nbytes * world / 1e9),
                        "parallelism": "shard%d" % world},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes per factor phase (ncu)",
                          "kernel": "k_bt_rows + k_bt_hub (all level launches of one refactorization pass, forward substitution fused)",
                          "algorithmic_bytes_per_instance": bytes_per_inst,
                          "factor_ms_per_step": fac_ms, "peak_source": peak_kind},
