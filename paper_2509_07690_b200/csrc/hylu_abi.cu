@@ -763,7 +763,7 @@ static int run_factor(hy_handle *h, const double *d_avals, double eps, const hy_
     k_anorm<<<296, 256, 0, st>>>(d_avals, h->S.scale, h->S.nnz, out->d_anorm);
     h->launches++;
   }
-  if (h->fanin_ok && h->S.mode >= 1) return run_fanin(h, P, st);
+  if (h->fanin_ok) return run_fanin(h, P, st);
   const Plan &pl = h->fplan;
   if (h->slab_ok) {
     h->slab_epoch++;

@@ -205,8 +205,11 @@ class DeviceContext:
         self.nnz = A.nnz
         from . import schedule as _sc
         self.wide_row = int(os.environ.get("HYLU_WIDE_ROW", _sc.WIDE_ROW))
-        self.path = "fanin" if (int(s.kernel_mode) >= 1 and os.environ.get("HYLU_PATH", "fanin") == "fanin") \
-            else "rows"
+        want = os.environ.get("HYLU_PATH", "auto")
+        if want == "auto":
+            self.path = "fanin" if int(s.kernel_mode) >= 1 else "rows"
+        else:
+            self.path = want
         if self.path == "fanin":
             self.upload_fanin_plan()
         else:

@@ -132,3 +132,18 @@ def test_single_path_hub_rows(name, monkeypatch):
     assert np.array_equal(f2.host_values(), f.host_values())
     x, _ = api.solve(p.A, f, b=p.b)
     assert np.linalg.norm(refmatrix.spmv(p.A, x) - p.b) / np.linalg.norm(p.b) <= RES_TOL
+
+
+@pytest.mark.parametrize("name", ["c1", "c0"])
+def test_rowrow_on_fanin_path(name, monkeypatch):
+    """ROWROW-mode analysis executed by the level fan-in kernels (supernode sources
+    applied as blocks: same values up to summation order)."""
+    monkeypatch.setenv("HYLU_PATH", "fanin")
+    p, an = _analysis(name, 0)
+    on = _oracle()
+    ref = on.factorize(an)
+    f = api.factorize_analysis(an)
+    assert np.array_equal(f.host_inner_perm(), ref.inner_perm)
+    assert _rel(f.host_values(), ref.values) <= LU_RTOL
+    x, _ = api.solve(p.A, f, b=p.b)
+    assert np.linalg.norm(refmatrix.spmv(p.A, x) - p.b) / np.linalg.norm(p.b) <= RES_TOL
