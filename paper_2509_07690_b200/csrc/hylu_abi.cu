@@ -501,7 +501,8 @@ int hy_upload_symbolic(hy_handle *h, const hy_symbolic_desc *d) {
           const int64_t lo = dir == 0 ? 0 : d->nl[u] + s, hi = dir == 0 ? d->nl[u] : W;
           slot0.push_back(slot);
           int32_t ns = 0;
-          for (int64_t c = lo; c < hi; c += CH) {
+          const bool direct = (hi - lo) * s <= 8192;   // small: the finish warp does it
+          for (int64_t c = lo; c < hi && !direct; c += CH) {
             chunks.push_back(SolveChunk{u, (int32_t)c, (int32_t)(c + CH < hi ? c + CH : hi), slot + ns});
             ++ns;
           }

@@ -623,6 +623,19 @@ __global__ void k_fwd_fin(DevSym S, const double *F, const int32_t *nodes, const
     for (int k = 0; k < an; ++k) acc -= scratch[(int64_t)(a0 + k) * 64 + lane + 32];
     mine1 = acc;
   }
+  if (an == 0 && L > 0) {
+    // small node: the warp computes the off-block dot products itself
+    const int32_t *cc = S.cols + S.colptr[u];
+    for (int t = 0; t < s; ++t) {
+      const double *row = Fu + (int64_t)t * W;
+      double acc = 0.0;
+      for (int q = lane; q < L; q += 32) acc += row[q] * y[cc[q]];
+      acc = warp_sum(acc);
+      if (lane == (t & 31)) {
+        if (t < 32) mine0 -= acc; else mine1 -= acc;
+      }
+    }
+  }
   for (int tt = 0; tt < s; ++tt) {
     const double ytt = __shfl_sync(HY_FULL, tt < 32 ? mine0 : mine1, tt & 31);
     const int t0 = lane, t1 = lane + 32;
@@ -656,6 +669,18 @@ __global__ void k_bwd_fin(DevSym S, const double *F, const int32_t *nodes, const
     double acc = y[r + lane + 32];
     for (int k = 0; k < an; ++k) acc -= scratch[(int64_t)(a0 + k) * 64 + lane + 32];
     mine1 = acc;
+  }
+  if (an == 0 && L + s < W) {
+    const int32_t *cc = S.cols + S.colptr[u];
+    for (int t = 0; t < s; ++t) {
+      const double *row = Fu + (int64_t)t * W;
+      double acc = 0.0;
+      for (int q = L + s + lane; q < W; q += 32) acc += row[q] * y[cc[q]];
+      acc = warp_sum(acc);
+      if (lane == (t & 31)) {
+        if (t < 32) mine0 -= acc; else mine1 -= acc;
+      }
+    }
   }
   for (int tt = s - 1; tt >= 0; --tt) {
     const double d = Fu[(int64_t)tt * W + L + tt];

@@ -206,10 +206,10 @@ class DeviceContext:
         from . import schedule as _sc
         self.wide_row = int(os.environ.get("HYLU_WIDE_ROW", _sc.WIDE_ROW))
         want = os.environ.get("HYLU_PATH", "auto")
-        if want == "auto":
-            self.path = "fanin" if int(s.kernel_mode) >= 1 else "rows"
-        else:
-            self.path = want
+        # level fan-in for every mode (supernode sources applied as blocks; in ROWROW
+        # mode this equals row-row up to summation order); the row
+        # path (row-row loop, hub pull rows, column slabs) stays selectable
+        self.path = "fanin" if want == "auto" else want
         if self.path == "fanin":
             self.upload_fanin_plan()
         else:
