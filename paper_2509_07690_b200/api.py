@@ -276,6 +276,49 @@ class BatchedRefactorizer:
         check(self.ctx.lib.hy_solve_batched(self.ctx.h, B, None, d_x.data_ptr(), sh))
         return d_x, d_npert
 
+    def run_host(self, h_vals, h_rhs, h_x, h_npert=None, chunks=4):
+        """Host buffers in, host buffers out, copies overlapped with compute.
+
+        The batch is cut into ``chunks`` contiguous slabs (multiples of 32
+        instances); chunk k's values/rhs go H2D on a copy stream while chunk k-1
+        is refactorized+solved on the compute stream and chunk k-2's solutions go
+        D2H on a third stream.  ``h_*`` should be pinned torch CPU tensors."""
+        import torch
+        B = h_vals.shape[0]
+        dev = self.ctx.device
+        per = ((B + chunks - 1) // chunks + 31) // 32 * 32
+        bounds = [(a, min(B, a + per)) for a in range(0, B, per)]
+        key = (B, per)
+        if getattr(self, "_host_key", None) != key:
+            self._host_key = key
+            self._streams = [torch.cuda.Stream(dev) for _ in range(3)]
+            self._dbufs = []
+            for a, b in bounds:
+                self._dbufs.append((torch.empty((b - a, self.ctx.nnz), dtype=torch.float64, device=dev),
+                                    torch.empty((b - a, self.ctx.n), dtype=torch.float64, device=dev),
+                                    torch.empty((b - a, self.ctx.n), dtype=torch.float64, device=dev),
+                                    torch.empty(b - a, dtype=torch.int32, device=dev)))
+        s_in, s_cmp, s_out = self._streams
+        cur = torch.cuda.current_stream(dev)
+        s_in.wait_stream(cur)
+        for (a, b), (dv, dr, dx, dn) in zip(bounds, self._dbufs):
+            with torch.cuda.stream(s_in):
+                dv.copy_(h_vals[a:b], non_blocking=True)
+                dr.copy_(h_rhs[a:b], non_blocking=True)
+                ev_in = torch.cuda.Event()
+                ev_in.record(s_in)
+            s_cmp.wait_event(ev_in)
+            self.run(dv, dr, dx, dn, s_cmp)
+            ev_c = torch.cuda.Event()
+            ev_c.record(s_cmp)
+            s_out.wait_event(ev_c)
+            with torch.cuda.stream(s_out):
+                h_x[a:b].copy_(dx, non_blocking=True)
+                if h_npert is not None:
+                    h_npert[a:b].copy_(dn, non_blocking=True)
+        cur.wait_stream(s_out)
+        return h_x, h_npert
+
     def factor_values(self, b, stream=None):
         import torch
         from .device import check
