@@ -313,6 +313,8 @@ __global__ void __launch_bounds__(HUB_THREADS) k_bt_hub(DevSym S, BatchP P, DevP
                                                         double *scratch, int max_slots, int *flags,
                                                         int epoch) {
   __shared__ double red[HUB_THREADS / 32][32];
+  constexpr int LVCAP = 512;
+  __shared__ int64_t s_wi[LVCAP + 1], s_sp[LVCAP + 1];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = HUB_THREADS / 32;
   const int task = blockIdx.x;
   const int u = nodes[task / G];
@@ -346,8 +348,21 @@ __global__ void __launch_bounds__(HUB_THREADS) k_bt_hub(DevSym S, BatchP P, DevP
     }
     __syncthreads();
     const int hr = hr0 + t;
-    for (int64_t lev = R.hrow_lev[hr]; lev < R.hrow_lev[hr + 1]; ++lev) {
-      for (int64_t it = R.lev_wi[lev] + warp; it < R.lev_wi[lev + 1]; it += nw) {
+    const int64_t lv0 = R.hrow_lev[hr], lv1 = R.hrow_lev[hr + 1];
+    // stage this row's level bounds in shared memory (one load instead of one per level)
+    const bool lsm = lv1 - lv0 <= LVCAP;
+    if (lsm)
+      for (int64_t q = threadIdx.x; q <= lv1 - lv0; q += HUB_THREADS) {
+        s_wi[q] = R.lev_wi[lv0 + q];
+        s_sp[q] = R.lev_sp[lv0 + q];
+      }
+    __syncthreads();
+    for (int64_t lev = lv0; lev < lv1; ++lev) {
+      const int64_t wi0 = lsm ? s_wi[lev - lv0] : R.lev_wi[lev];
+      const int64_t wi1 = lsm ? s_wi[lev - lv0 + 1] : R.lev_wi[lev + 1];
+      const int64_t sp0 = lsm ? s_sp[lev - lv0] : R.lev_sp[lev];
+      const int64_t sp1 = lsm ? s_sp[lev - lv0 + 1] : R.lev_sp[lev + 1];
+      for (int64_t it = wi0 + warp; it < wi1; it += nw) {
         const int p = R.wi_p[it];
         const int slot = R.wi_slot[it];
         const int64_t y1 = R.wi_y1[it];
@@ -376,9 +391,9 @@ __global__ void __launch_bounds__(HUB_THREADS) k_bt_hub(DevSym S, BatchP P, DevP
         else
           scr[(size_t)slot * 32] = acc;
       }
-      if (R.lev_sp[lev + 1] > R.lev_sp[lev]) {
+      if (sp1 > sp0) {
         __syncthreads();
-        for (int64_t k2 = R.lev_sp[lev] + warp; k2 < R.lev_sp[lev + 1]; k2 += nw) {
+        for (int64_t k2 = sp0 + warp; k2 < sp1; k2 += nw) {
           const int p = R.sp_p[k2];
           double acc = w[p * 32];
           const int s0 = R.sp_s0[k2], ns = R.sp_n[k2];
