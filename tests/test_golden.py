@@ -1,0 +1,62 @@
+"""Golden fixtures (tests/golden/make_golden.py): the reference's own matching/AMD
+outputs and oracle factors for small seeded configs.  CPU part: the host
+preprocessing on this machine reproduces them bit-exactly.  GPU part: the device
+factors match the golden oracle factors."""
+import os
+
+import numpy as np
+import pytest
+
+from paper_2509_07690_b200 import analysis
+from paper_2509_07690_b200._ref import SolverConfig, SparseMatrixCSR
+
+HERE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+NAMES = ["c0", "c1", "c2", "c3", "c4"]
+ORDER = {"c0": "amd", "c1": "amd", "c2": "nd", "c3": "nd", "c4": "amd"}
+
+
+def _load(name):
+    g = np.load(os.path.join(HERE, name + ".npz"))
+    n = len(g["row_ptr"]) - 1
+    A = SparseMatrixCSR(n, g["row_ptr"], g["col_idx"], g["values"])
+    an = analysis.analyze(A, SolverConfig(ordering=ORDER[name]))
+    return g, A, an
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_host_preprocessing_matches_golden(name):
+    g, A, an = _load(name)
+    assert np.array_equal(an.pivot_scale.row_perm, g["row_perm"])
+    assert np.array_equal(an.pivot_scale.dr, g["dr"]) and np.array_equal(an.pivot_scale.dc, g["dc"])
+    assert np.array_equal(an.ordering.perm, g["perm"])
+    s = an.symbolic
+    assert np.array_equal(s.node_first, g["node_first"]) and np.array_equal(s.cols, g["cols"])
+    assert s.flops == float(g["flops"]) and s.fill_nnz == int(g["fill_nnz"])
+    assert int(s.kernel_mode) == int(g["kernel_mode"])
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_oracle_matches_golden(name):
+    from oracle import numeric as on
+    g, A, an = _load(name)
+    f = on.factorize(an)
+    assert np.array_equal(f.inner_perm, g["inner_perm"])
+    assert np.array_equal(f.values, g["F"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", NAMES)
+def test_device_matches_golden(name):
+    from paper_2509_07690_b200 import api
+    g, A, an = _load(name)
+    f = api.factorize_analysis(an)
+    assert np.array_equal(f.host_inner_perm(), g["inner_perm"])
+    F = f.host_values()
+    assert np.abs(F - g["F"]).max() <= 1e-11 * max(1.0, np.abs(g["F"]).max())
+    x, _ = api.solve(A, f, b=g["b"])
+    assert np.abs(x - g["x"]).max() <= 1e-9 * max(1.0, np.abs(g["x"]).max())
+    if name == "c4":
+        X, _ = api.refactorize_solve_batched(g["batch_values"], f, g["batch_rhs"])
+        from oracle import numeric as on
+        Xo, _ = on.refactor_solve_batch(an, on.factorize(an), g["batch_values"], g["batch_rhs"])
+        assert np.abs(X - Xo).max() <= 1e-9 * np.abs(Xo).max()
