@@ -165,7 +165,7 @@ def factorize_analysis(an, values=None, opts=None, stream=None):
     ctx = _context(an, opts.device)
     vals = an.A.values if values is None else values
     d_vals = vals if isinstance(vals, torch.Tensor) else torch.from_numpy(
-        np.ascontiguousarray(vals, np.float64)).to(ctx.device)
+        np.array(vals, np.float64, copy=True)).to(ctx.device)
     bufs, desc = ctx.alloc_factors()
     from .device import check
     check(ctx.lib.hy_factorize(ctx.h, d_vals.data_ptr(), float(opts.perturbation_epsilon),

@@ -73,9 +73,15 @@ __global__ void k_fwd_fin(DevSym, const double *, const int32_t *, const int32_t
 __global__ void k_bwd_fin(DevSym, const double *, const int32_t *, const int32_t *, const int32_t *, int,
                           const double *, double *);
 __global__ void k_bwd(DevSym, const double *, const int32_t *, int, double *);
+struct TaskDesc {
+  int32_t u, g;
+  int64_t valoff;
+  int32_t r, s, W, L;
+  int64_t d0, d1;
+};
 template <bool STAGED>
-__global__ void k_bt_pipe(DevSym, BatchP, DevProg, const int2 *, int64_t, const double *, double *, int *, int *,
-                          int, int, int);
+__global__ void k_bt_pipe(DevSym, BatchP, DevProg, const TaskDesc *, int64_t, const double *, double *, int *,
+                          int *, int, int, int);
 __global__ void k_bt_hub(DevSym, BatchP, DevProg, const int32_t *, int, int, const double *, double *,
                          double *, int, int *, int);
 __global__ void k_batch_bhat(DevSym, const int32_t *, const double *, double *, int64_t);
@@ -129,6 +135,8 @@ struct hy_handle {
   double *d_solve_scratch = nullptr;
   int64_t stored = 0;
   bool uploaded = false;
+  // host copies of per-node data for descriptor building
+  std::vector<int64_t> h_first, h_colptr, h_valoff, h_dptr, h_nl;
   double *d_y = nullptr;          // single-solve workspace [n]
   double *d_bf = nullptr;         // batched factor workspace
   int64_t bf_cap = 0;             // doubles
@@ -158,7 +166,7 @@ struct hy_handle {
   // diagonal claim order per (segment, G): pair prefix sums, (level<<16|group), level offsets
   struct Seg {
     int l0, l1;
-    int2 *d_tasks = nullptr;   // (node, group) in diagonal claim order
+    TaskDesc *d_tasks = nullptr;   // task descriptors in diagonal claim order
     int64_t ntasks = 0;
   };
   std::vector<Seg> segs;
@@ -278,20 +286,33 @@ static int build_segments(hy_handle *h, int G) {
     sg.l0 = l;
     sg.l1 = l1;
     const int L = l1 - l;
-    std::vector<int2> tasks;
+    std::vector<TaskDesc> tasks;
     tasks.reserve((size_t)(h->bl_rptr[l1] - h->bl_rptr[l]) * G);
+    auto mk = [&](int32_t u, int32_t g) {
+      TaskDesc t;
+      t.u = u;
+      t.g = g;
+      t.valoff = h->h_valoff[u];
+      t.r = (int32_t)h->h_first[u];
+      t.s = (int32_t)(h->h_first[u + 1] - h->h_first[u]);
+      t.W = (int32_t)(h->h_colptr[u + 1] - h->h_colptr[u]);
+      t.L = (int32_t)h->h_nl[u];
+      t.d0 = h->h_dptr[u];
+      t.d1 = h->h_dptr[u + 1];
+      return t;
+    };
     const int sk = h->skew;
     for (int d = 0; d < sk * (G - 1) + L; ++d)
       for (int k = 0; k < L && k <= d; ++k) {
         if ((d - k) % sk) continue;
         const int g = (d - k) / sk;
         if (g >= G) continue;
-        for (int64_t q = h->bl_rptr[l + k]; q < h->bl_rptr[l + k + 1]; ++q) tasks.push_back(make_int2(rows[q], g));
+        for (int64_t q = h->bl_rptr[l + k]; q < h->bl_rptr[l + k + 1]; ++q) tasks.push_back(mk(rows[q], g));
       }
     sg.ntasks = (int64_t)tasks.size();
     if (sg.ntasks) {
-      CK(cudaMalloc((void **)&sg.d_tasks, sizeof(int2) * sg.ntasks));
-      CK(cudaMemcpy(sg.d_tasks, tasks.data(), sizeof(int2) * sg.ntasks, cudaMemcpyHostToDevice));
+      CK(cudaMalloc((void **)&sg.d_tasks, sizeof(TaskDesc) * sg.ntasks));
+      CK(cudaMemcpy(sg.d_tasks, tasks.data(), sizeof(TaskDesc) * sg.ntasks, cudaMemcpyHostToDevice));
     }
     h->segs.push_back(sg);
     l = l1;
@@ -452,6 +473,11 @@ int hy_upload_symbolic(hy_handle *h, const hy_symbolic_desc *d) {
   int64_t *p64;
   int32_t *p32;
   UP(&p64, d->node_first, nn + 1); S.first = p64;
+  h->h_first.assign(d->node_first, d->node_first + nn + 1);
+  h->h_colptr.assign(d->colptr, d->colptr + nn + 1);
+  h->h_valoff.assign(d->valoff, d->valoff + nn + 1);
+  h->h_dptr.assign(d->dep_ptr, d->dep_ptr + nn + 1);
+  h->h_nl.assign(d->nl, d->nl + nn);
   int8_t *p8;
   UP(&p8, d->node_kind, nn); S.kind = p8;
   UP(&p64, d->colptr, nn + 1); S.colptr = p64;

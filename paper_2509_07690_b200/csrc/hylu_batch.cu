@@ -248,9 +248,18 @@ size_t pipe_smem_bytes(bool staged) {
 // completion flags of the node's in-segment dependencies, run the task, then
 // publish its flag.  Claim order is topological and every claimed task is held by
 // a resident warp, so the earliest unfinished claimed task can always proceed.
+// Task descriptor (built on the host in claim order): everything a task needs
+// before its first data load, in one 48-byte record.
+struct TaskDesc {
+  int32_t u, g;
+  int64_t valoff;
+  int32_t r, s, W, L;
+  int64_t d0, d1;
+};
+
 template <bool STAGED>
 __global__ void __launch_bounds__(PIPE_WARPS * 32, STAGED ? 3 : 6)
-    k_bt_pipe(DevSym S, BatchP P, DevProg R, const int2 *tasks, int64_t total, const double *rhs,
+    k_bt_pipe(DevSym S, BatchP P, DevProg R, const TaskDesc *tasks, int64_t total, const double *rhs,
               double *Y, int *counter, int *flags, int epoch, int G, int nowait) {
   extern __shared__ __align__(16) double pipe_smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -259,32 +268,40 @@ __global__ void __launch_bounds__(PIPE_WARPS * 32, STAGED ? 3 : 6)
   double *stg_w = wsm_w + PIPE_WS * 32;
   int32_t *rlb_w = reinterpret_cast<int32_t *>(pipe_smem + (size_t)PIPE_WARPS * (PIPE_WS + SG) * 32) +
                    warp * SG;
+  long long t = 0;
+  if (lane == 0) t = (long long)atomicAdd(reinterpret_cast<unsigned long long *>(counter), 1ull);
+  t = __shfl_sync(HY_FULL, t, 0);
+  if (t >= total) return;
+  TaskDesc cur = tasks[t];
   for (;;) {
-    long long t = 0;
-    if (lane == 0) t = (long long)atomicAdd(reinterpret_cast<unsigned long long *>(counter), 1ull);
-    t = __shfl_sync(HY_FULL, t, 0);
-    if (t >= total) return;
-    const int2 tk = tasks[t];
-    const int u = tk.x, g = tk.y;
-    const longlong4 nr = R.node_rec[u];
+    // claim the next task now; its result is only needed after this task
+    long long tn = 0;
+    if (lane == 0) tn = (long long)atomicAdd(reinterpret_cast<unsigned long long *>(counter), 1ull);
     // lanes poll the dependency flags in parallel (acquire); the warp barrier then
     // orders every lane's subsequent loads after the producers' releases
-    const int64_t d0 = nr.y, d1 = S.dptr[u + 1];
-    for (int64_t k = d0 + lane; k < d1 && !nowait; k += 32) {
-      const int *f = flags + (int64_t)S.deps[k] * G + g;
+    for (int64_t k = cur.d0 + lane; k < cur.d1 && !nowait; k += 32) {
+      const int *f = flags + (int64_t)S.deps[k] * G + cur.g;
       while (ld_acquire(f) != epoch) __nanosleep(64);
     }
     __syncwarp();
-    bt_node<STAGED>(S, P, R, u, nr, g, rhs, Y, wsm_w, PIPE_WS, stg_w, rlb_w, lane);
+    const longlong4 nr = make_longlong4(cur.valoff, cur.d0, (int64_t)cur.r | ((int64_t)cur.s << 32),
+                                        (int64_t)cur.W | ((int64_t)cur.L << 32));
+    bt_node<STAGED>(S, P, R, cur.u, nr, cur.g, rhs, Y, wsm_w, PIPE_WS, stg_w, rlb_w, lane);
+    int *myflag = flags + (int64_t)cur.u * G + cur.g;
+    tn = __shfl_sync(HY_FULL, tn, 0);
+    TaskDesc nxt;
+    if (tn < total) nxt = tasks[tn];     // in flight while the fence drains this task's stores
     __threadfence();
     __syncwarp();
-    if (lane == 0) st_release(flags + (int64_t)u * G + g, epoch);
+    if (lane == 0) st_release(myflag, epoch);
+    if (tn >= total) return;
+    cur = nxt;
   }
 }
 
-template __global__ void k_bt_pipe<false>(DevSym, BatchP, DevProg, const int2 *, int64_t,
+template __global__ void k_bt_pipe<false>(DevSym, BatchP, DevProg, const TaskDesc *, int64_t,
                                           const double *, double *, int *, int *, int, int, int);
-template __global__ void k_bt_pipe<true>(DevSym, BatchP, DevProg, const int2 *, int64_t,
+template __global__ void k_bt_pipe<true>(DevSym, BatchP, DevProg, const TaskDesc *, int64_t,
                                          const double *, double *, int *, int *, int, int, int);
 
 // ---------------------------------------------------------------------------
