@@ -434,7 +434,7 @@ int hy_set_option(hy_handle *h, const char *name, int64_t value) {
     return HY_OK;
   }
   if (std::string(name) == "nowait_experiment") {
-    h->nowait = value != 0;
+    h->nowait = (int)value;   // bitmask: 1 no waits, 2 no steps, 4 no scatter, 8 no copy-out
     return HY_OK;
   }
   if (std::string(name) == "staged") {

@@ -177,7 +177,7 @@ template <bool STAGED>
 __device__ __forceinline__ void bt_node(const DevSym &S, const BatchP &P, const DevProg &R, int u,
                                         const longlong4 nr, int g, const double *rhs, double *Y,
                                         double *wsm0, int ws, double *stage, int32_t *relbuf,
-                                        int lane) {
+                                        int lane, int xmask) {
   const int64_t b = (int64_t)g * 32 + lane;
   const bool live = b < P.B;
   const int nlive = (int)(P.B - (int64_t)g * 32 < 32 ? P.B - (int64_t)g * 32 : 32);
@@ -207,12 +207,14 @@ __device__ __forceinline__ void bt_node(const DevSym &S, const BatchP &P, const 
     __syncwarp();
     // scatter: lanes over (instance, entry) pairs, instance-major, so a pass reads
     // the k contiguous entries of consecutive instances (few sectors per instance)
-    for (int idx = lane; idx < nlive * k; idx += 32) {
-      const int inst = idx / k, e = idx - inst * k;
-      w0[S.colpos[e0 + e] * 32 + inst] = Ab[(int64_t)inst * S.nnz + e0 + e] * S.scale[e0 + e];
-    }
+    if (!(xmask & 4))
+      for (int idx = lane; idx < nlive * k; idx += 32) {
+        const int inst = idx / k, e = idx - inst * k;
+        w0[S.colpos[e0 + e] * 32 + inst] = Ab[(int64_t)inst * S.nnz + e0 + e] * S.scale[e0 + e];
+      }
     __syncwarp();
-    if (STAGED) {
+    if (xmask & 2) {
+    } else if (STAGED) {
       if (inSm)
         yacc = run_staged(R, s0, s1, wsm0 + lane, gb, yb, yacc, stage, relbuf, lane);
       else
@@ -229,7 +231,7 @@ __device__ __forceinline__ void bt_node(const DevSym &S, const BatchP &P, const 
     w0[Lt * 32 + lane] = perturb(piv, thr, fired);
     if (fired && live) atomicAdd(&P.npert[b], 1);
     yb[(int64_t)i * 32] = yacc;
-    if (inSm)
+    if (inSm && !(xmask & 8))
       for (int q = 0; q < W; ++q) grow[q * 32 + lane] = w0[q * 32 + lane];
     __syncwarp();
   }
@@ -268,34 +270,25 @@ __global__ void __launch_bounds__(PIPE_WARPS * 32, STAGED ? 3 : 6)
   double *stg_w = wsm_w + PIPE_WS * 32;
   int32_t *rlb_w = reinterpret_cast<int32_t *>(pipe_smem + (size_t)PIPE_WARPS * (PIPE_WS + SG) * 32) +
                    warp * SG;
-  long long t = 0;
-  if (lane == 0) t = (long long)atomicAdd(reinterpret_cast<unsigned long long *>(counter), 1ull);
-  t = __shfl_sync(HY_FULL, t, 0);
-  if (t >= total) return;
-  TaskDesc cur = tasks[t];
   for (;;) {
-    // claim the next task now; its result is only needed after this task
-    long long tn = 0;
-    if (lane == 0) tn = (long long)atomicAdd(reinterpret_cast<unsigned long long *>(counter), 1ull);
+    long long t = 0;
+    if (lane == 0) t = (long long)atomicAdd(reinterpret_cast<unsigned long long *>(counter), 1ull);
+    t = __shfl_sync(HY_FULL, t, 0);
+    if (t >= total) return;
+    const TaskDesc cur = tasks[t];
     // lanes poll the dependency flags in parallel (acquire); the warp barrier then
     // orders every lane's subsequent loads after the producers' releases
-    for (int64_t k = cur.d0 + lane; k < cur.d1 && !nowait; k += 32) {
+    for (int64_t k = cur.d0 + lane; k < cur.d1 && !(nowait & 1); k += 32) {
       const int *f = flags + (int64_t)S.deps[k] * G + cur.g;
       while (ld_acquire(f) != epoch) __nanosleep(64);
     }
     __syncwarp();
     const longlong4 nr = make_longlong4(cur.valoff, cur.d0, (int64_t)cur.r | ((int64_t)cur.s << 32),
                                         (int64_t)cur.W | ((int64_t)cur.L << 32));
-    bt_node<STAGED>(S, P, R, cur.u, nr, cur.g, rhs, Y, wsm_w, PIPE_WS, stg_w, rlb_w, lane);
-    int *myflag = flags + (int64_t)cur.u * G + cur.g;
-    tn = __shfl_sync(HY_FULL, tn, 0);
-    TaskDesc nxt;
-    if (tn < total) nxt = tasks[tn];     // in flight while the fence drains this task's stores
+    bt_node<STAGED>(S, P, R, cur.u, nr, cur.g, rhs, Y, wsm_w, PIPE_WS, stg_w, rlb_w, lane, nowait);
     __threadfence();
     __syncwarp();
-    if (lane == 0) st_release(myflag, epoch);
-    if (tn >= total) return;
-    cur = nxt;
+    if (lane == 0) st_release(flags + (int64_t)cur.u * G + cur.g, epoch);
   }
 }
 
