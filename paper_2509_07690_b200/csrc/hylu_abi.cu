@@ -89,6 +89,8 @@ __global__ void k_batch_xout(DevSym, const double *, double *, int64_t);
 __global__ void k_batch_fwd(DevSym, const double *, int64_t, const int32_t *, int, int, double *);
 __global__ void k_batch_bwd(DevSym, const double *, int64_t, const int32_t *, int, int, double *);
 __global__ void k_batch_extract(const double *, int64_t, int64_t, double *);
+__global__ void k_bt_bwd(DevSym, const double *, int64_t, const int2 *, int64_t, const int64_t *, const int32_t *,
+                         int *, int *, int, int, double *);
 }  // namespace hy
 
 using namespace hy;
@@ -137,6 +139,18 @@ struct hy_handle {
   bool uploaded = false;
   // host copies of per-node data for descriptor building
   std::vector<int64_t> h_first, h_colptr, h_valoff, h_dptr, h_nl;
+  // backward-solve U dependencies + persistent bwd task list (per G)
+  int64_t *d_udp = nullptr;
+  int32_t *d_udeps = nullptr;
+  std::vector<int64_t> h_ulptr;
+  std::vector<int32_t> h_ulnodes;
+  int2 *d_bwd_tasks = nullptr;
+  int64_t bwd_ntasks = 0;
+  int bwd_G = -1;
+  int *d_bwd_flags = nullptr;
+  int64_t bwd_flags_cap = 0;
+  int bwd_persistent = 1;
+  int epoch_bwd = 0;
   double *d_y = nullptr;          // single-solve workspace [n]
   double *d_bf = nullptr;         // batched factor workspace
   int64_t bf_cap = 0;             // doubles
@@ -378,6 +392,7 @@ int hy_create(int device, hy_handle **out) {
   hy_handle *h = new hy_handle();
   h->device = device;
   h->sn_smem = sn_smem_bytes();
+  cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, device);
   cudaError_t e = cudaFuncSetAttribute(k_sn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)h->sn_smem);
   if (e != cudaSuccess) {
@@ -409,6 +424,8 @@ void hy_destroy(hy_handle *h) {
   if (h->d_bf) cudaFree(h->d_bf);
   if (h->d_scratch) cudaFree(h->d_scratch);
   if (h->d_flags) cudaFree(h->d_flags);
+  if (h->d_bwd_flags) cudaFree(h->d_bwd_flags);
+  if (h->d_bwd_tasks) cudaFree(h->d_bwd_tasks);
   free_segments(h);
   if (h->d_counters) cudaFree(h->d_counters);
   if (h->d_by) cudaFree(h->d_by);
@@ -422,6 +439,10 @@ int hy_set_option(hy_handle *h, const char *name, int64_t value) {
   if (!h || !name) return fail(HY_INVALID_ARGUMENT, "null handle/name");
   if (std::string(name) == "group_batch" && value >= 1) {
     h->gbatch = (int)value;
+    return HY_OK;
+  }
+  if (std::string(name) == "bwd_persistent") {
+    h->bwd_persistent = value != 0;
     return HY_OK;
   }
   if (std::string(name) == "fanin_dmma") {
@@ -545,6 +566,27 @@ int hy_upload_symbolic(hy_handle *h, const hy_symbolic_desc *d) {
     }
     const int64_t ns = (h->fsolve.nslots > h->bsolve.nslots ? h->fsolve.nslots : h->bsolve.nslots);
     UP(&h->d_solve_scratch, (const double *)nullptr, (ns > 0 ? ns : 1) * 64);
+  }
+  {
+    // U dependencies of each node: owners of its columns right of its block
+    std::vector<int64_t> udp(nn + 1, 0);
+    std::vector<int32_t> ud;
+    for (int64_t u = 0; u < nn; ++u) {
+      const int64_t s = d->node_first[u + 1] - d->node_first[u];
+      int32_t last = -1;
+      for (int64_t q = d->colptr[u] + d->nl[u] + s; q < d->colptr[u + 1]; ++q) {
+        const int32_t v = node_of[d->cols[q]];
+        if (v != last) {
+          ud.push_back(v);
+          last = v;
+        }
+      }
+      udp[u + 1] = (int64_t)ud.size();
+    }
+    UP(&h->d_udp, udp.data(), nn + 1);
+    UP(&h->d_udeps, ud.data(), ud.size());
+    h->h_ulptr.assign(d->ulevel_ptr, d->ulevel_ptr + d->nulevels + 1);
+    h->h_ulnodes.assign(d->ulevel_nodes, d->ulevel_nodes + d->ulevel_ptr[d->nulevels]);
   }
   {
     std::vector<int32_t> lev(nn, 0);
@@ -1009,12 +1051,12 @@ int hy_refactorize_batched(hy_handle *h, int64_t B, const double *d_vals, double
     h->epoch = 0;
   }
   const int nl = h->fplan.nlev;
-  if (h->counters_cap < nl + 1) {
+  if (h->counters_cap < nl + 2) {
     if (h->d_counters) CK(cudaFree(h->d_counters));
-    CK(cudaMalloc((void **)&h->d_counters, sizeof(long long) * (nl + 1)));
-    h->counters_cap = nl + 1;
+    CK(cudaMalloc((void **)&h->d_counters, sizeof(long long) * (nl + 2)));
+    h->counters_cap = nl + 2;
   }
-  CK(cudaMemsetAsync(h->d_counters, 0, sizeof(long long) * (nl + 1), st));
+  CK(cudaMemsetAsync(h->d_counters, 0, sizeof(long long) * (nl + 2), st));
   h->epoch++;
   if (h->pipe_blocks == 0) {
     int per_sm = 0, sms = 0;
@@ -1088,12 +1130,43 @@ int hy_solve_batched(hy_handle *h, int64_t B, const double *d_b, double *d_x, ui
   }
   }
   const Plan &bp = h->bplan;
-  for (int l = 0; l < bp.nlev; ++l) {
-    const int c = (int)(bp.aptr[l + 1] - bp.aptr[l]);
-    const int64_t tasks = (int64_t)c * G;
-    k_batch_bwd<<<(unsigned)((tasks + 3) / 4), 128, 0, st>>>(h->S, h->d_bf, h->stored,
-                                                           bp.d_all + bp.aptr[l], c, G, h->d_by);
+  if (h->bwd_persistent) {
+    if (h->bwd_G != G) {
+      std::vector<int2> tl;
+      const int L = (int)h->h_ulptr.size() - 1;
+      for (int d = 0; d < G + L - 1; ++d)
+        for (int k = (d - G + 1 > 0 ? d - G + 1 : 0); k <= (d < L - 1 ? d : L - 1); ++k)
+          for (int64_t q = h->h_ulptr[k]; q < h->h_ulptr[k + 1]; ++q) tl.push_back(make_int2(h->h_ulnodes[q], d - k));
+      if (h->d_bwd_tasks) CK(cudaFree(h->d_bwd_tasks));
+      h->d_bwd_tasks = nullptr;
+      h->bwd_ntasks = (int64_t)tl.size();
+      CK(cudaMalloc((void **)&h->d_bwd_tasks, sizeof(int2) * (tl.size() + 1)));
+      CK(cudaMemcpy(h->d_bwd_tasks, tl.data(), sizeof(int2) * tl.size(), cudaMemcpyHostToDevice));
+      h->bwd_G = G;
+    }
+    const int64_t nf = (int64_t)h->S.nn * G;
+    if (nf > h->bwd_flags_cap) {
+      if (h->d_bwd_flags) CK(cudaFree(h->d_bwd_flags));
+      CK(cudaMalloc((void **)&h->d_bwd_flags, sizeof(int) * nf));
+      CK(cudaMemset(h->d_bwd_flags, 0, sizeof(int) * nf));
+      h->bwd_flags_cap = nf;
+      h->epoch_bwd = 0;
+    }
+    h->epoch_bwd++;
+    int *ctr = (int *)((long long *)h->d_counters + h->counters_cap - 1);
+    CK(cudaMemsetAsync(ctr, 0, sizeof(long long), st));
+    k_bt_bwd<<<h->sm_count * 12, 128, 0, st>>>(h->S, h->d_bf, h->stored, h->d_bwd_tasks, h->bwd_ntasks,
+                                              h->d_udp, h->d_udeps, ctr, h->d_bwd_flags, h->epoch_bwd, G,
+                                              h->d_by);
     h->launches++;
+  } else {
+    for (int l = 0; l < bp.nlev; ++l) {
+      const int c = (int)(bp.aptr[l + 1] - bp.aptr[l]);
+      const int64_t tasks = (int64_t)c * G;
+      k_batch_bwd<<<(unsigned)((tasks + 3) / 4), 128, 0, st>>>(h->S, h->d_bf, h->stored,
+                                                             bp.d_all + bp.aptr[l], c, G, h->d_by);
+      h->launches++;
+    }
   }
   k_batch_xout<<<tg, 256, 0, st>>>(h->S, h->d_by, d_x, B);
   h->launches++;

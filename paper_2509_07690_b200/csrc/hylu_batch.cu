@@ -530,6 +530,59 @@ __global__ void __launch_bounds__(BW * 32) k_batch_bwd(DevSym S, const double *B
   }
 }
 
+// Persistent backward substitution: one warp per (node, group) task in diagonal
+// order over backward levels; a task waits for the nodes owning its columns right
+// of its block (U dependencies) and publishes its own completion flag.
+__global__ void __launch_bounds__(128) k_bt_bwd(DevSym S, const double *BF, int64_t stored,
+                                                const int2 *tasks, int64_t total, const int64_t *udp,
+                                                const int32_t *udeps, int *counter, int *flags, int epoch,
+                                                int G, double *Y) {
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    long long t = 0;
+    if (lane == 0) t = (long long)atomicAdd(reinterpret_cast<unsigned long long *>(counter), 1ull);
+    t = __shfl_sync(HY_FULL, t, 0);
+    if (t >= total) return;
+    const int2 tk = tasks[t];
+    const int u = tk.x, g = tk.y;
+    for (int64_t k = udp[u] + lane; k < udp[u + 1]; k += 32) {
+      const int *f = flags + (int64_t)udeps[k] * G + g;
+      while (ld_acquire(f) != epoch) __nanosleep(64);
+    }
+    __syncwarp();
+    const int r = (int)S.first[u];
+    const int s = (int)(S.first[u + 1] - r);
+    const int64_t c0 = S.colptr[u];
+    const int W = (int)(S.colptr[u + 1] - c0);
+    const int L = S.nl[u];
+    const double *gbase = BF + (int64_t)g * stored * 32 + lane;
+    double *y = Y + (int64_t)g * S.n * 32 + lane;
+    const int32_t *cc = S.cols + c0;
+    for (int t2 = s - 1; t2 >= 0; --t2) {
+      const double *row = gbase + (S.valoff[u] + (int64_t)t2 * W) * 32;
+      const int d = L + t2;
+      double acc = y[(int64_t)(r + t2) * 32];
+      int p = d + 1;
+      for (; p + 4 <= W; p += 4) {
+        const int k0 = cc[p], k1 = cc[p + 1], k2 = cc[p + 2], k3 = cc[p + 3];
+        const double a0 = row[(int64_t)p * 32], a1 = row[(int64_t)(p + 1) * 32];
+        const double a2 = row[(int64_t)(p + 2) * 32], a3 = row[(int64_t)(p + 3) * 32];
+        const double z0 = y[(int64_t)k0 * 32], z1 = y[(int64_t)k1 * 32];
+        const double z2 = y[(int64_t)k2 * 32], z3 = y[(int64_t)k3 * 32];
+        acc -= a0 * z0;
+        acc -= a1 * z1;
+        acc -= a2 * z2;
+        acc -= a3 * z3;
+      }
+      for (; p < W; ++p) acc -= row[(int64_t)p * 32] * y[(int64_t)cc[p] * 32];
+      y[(int64_t)(r + t2) * 32] = acc / row[(int64_t)d * 32];
+    }
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) st_release(flags + (int64_t)u * G + g, epoch);
+  }
+}
+
 // de-interleave one instance's factor values into node layout
 __global__ void k_batch_extract(const double *BF, int64_t stored, int64_t b, double *out) {
   const int64_t g = b / 32, lane = b % 32;
