@@ -59,6 +59,7 @@ __global__ void k_fi_upd(DevSym, CallP, FaninDev, int, int, int);
 __global__ void k_fi_upd_mma(DevSym, CallP, FaninDev, int, int, int);
 size_t fi_upd_smem(int, int);
 size_t pipe_smem_bytes(bool staged);
+size_t hub_smem_bytes();
 __global__ void k_bhat(DevSym, const int32_t *, const double *, double *);
 __global__ void k_xout(DevSym, const double *, double *);
 __global__ void k_fwd(DevSym, const double *, const int32_t *, int, double *);
@@ -149,7 +150,7 @@ struct hy_handle {
   int bwd_G = -1;
   int *d_bwd_flags = nullptr;
   int64_t bwd_flags_cap = 0;
-  int bwd_persistent = 1;
+  int bwd_persistent = 0;
   int epoch_bwd = 0;
   double *d_y = nullptr;          // single-solve workspace [n]
   double *d_bf = nullptr;         // batched factor workspace
@@ -399,6 +400,8 @@ int hy_create(int device, hy_handle **out) {
     delete h;
     return fail(HY_CUDA_ERROR, std::string("cudaFuncSetAttribute(k_sn): ") + cudaGetErrorString(e));
   }
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_bt_hub, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hub_smem_bytes());
   e = cudaFuncSetAttribute(k_bt_pipe<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)pipe_smem_bytes(true));
   if (e == cudaSuccess)
@@ -1087,7 +1090,7 @@ int hy_refactorize_batched(hy_handle *h, int64_t B, const double *d_vals, double
         CK(cudaMalloc((void **)&h->d_scratch, sizeof(double) * need));
         h->scratch_cap = need;
       }
-      k_bt_hub<<<(unsigned)(nh * G), 1024, 0, st>>>(h->S, P, h->prog, h->d_bl_hubs + h->bl_hptr[l], nh, G,
+      k_bt_hub<<<(unsigned)(nh * G), 1024, hub_smem_bytes(), st>>>(h->S, P, h->prog, h->d_bl_hubs + h->bl_hptr[l], nh, G,
                                                    d_b_fuse, h->d_by, h->d_scratch, h->max_slots,
                                                    h->d_flags, h->epoch);
       h->launches++;

@@ -17,6 +17,11 @@ namespace hy {
 
 constexpr int BW = 4;            // warps per block (bwd / fwd kernels)
 constexpr int HUB_THREADS = 1024;
+constexpr int HUB_CAPI = 2048;   // staged work items per level
+constexpr int HUB_CAPP = 8192;   // staged predecessor records per level
+size_t hub_smem_bytes() {
+  return (size_t)HUB_CAPP * (8 + 4) + (size_t)HUB_CAPI * (8 + 4 * 4);
+}
 
 // Apply the row-program steps [s0, s1) to the accumulator w (lane-offset pointer,
 // stride 32), software-pipelined: the next step's scalars, its U(j,j) and y_j are
@@ -325,6 +330,15 @@ __global__ void __launch_bounds__(HUB_THREADS) k_bt_hub(DevSym S, BatchP P, DevP
   __shared__ double red[HUB_THREADS / 32][32];
   constexpr int LVCAP = 512;
   __shared__ int64_t s_wi[LVCAP + 1], s_sp[LVCAP + 1];
+  // per-level staging of work-item metadata and predecessor lists (dynamic smem)
+  extern __shared__ __align__(16) unsigned char hub_dyn[];
+  int64_t *st_pu = reinterpret_cast<int64_t *>(hub_dyn);                 // [HUB_CAPP]
+  int64_t *st_kd = st_pu + HUB_CAPP;                                       // [HUB_CAPI]
+  int32_t *st_pp = reinterpret_cast<int32_t *>(st_kd + HUB_CAPI);         // [HUB_CAPP]
+  int32_t *st_p = st_pp + HUB_CAPP;                                        // [HUB_CAPI]
+  int32_t *st_sl = st_p + HUB_CAPI;
+  int32_t *st_y0 = st_sl + HUB_CAPI;
+  int32_t *st_y1 = st_y0 + HUB_CAPI;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = HUB_THREADS / 32;
   const int task = blockIdx.x;
   const int u = nodes[task / G];
@@ -372,6 +386,57 @@ __global__ void __launch_bounds__(HUB_THREADS) k_bt_hub(DevSym S, BatchP P, DevP
       const int64_t wi1 = lsm ? s_wi[lev - lv0 + 1] : R.lev_wi[lev + 1];
       const int64_t sp0 = lsm ? s_sp[lev - lv0] : R.lev_sp[lev];
       const int64_t sp1 = lsm ? s_sp[lev - lv0 + 1] : R.lev_sp[lev + 1];
+      const int64_t ni = wi1 - wi0;
+      const int64_t yb0 = ni ? R.wi_y0[wi0] : 0;
+      const int64_t np_ = ni ? R.wi_y1[wi1 - 1] - yb0 : 0;
+      const bool staged = ni <= HUB_CAPI && np_ <= HUB_CAPP;
+      if (staged) {
+        for (int64_t q = threadIdx.x; q < ni; q += HUB_THREADS) {
+          st_p[q] = R.wi_p[wi0 + q];
+          st_sl[q] = R.wi_slot[wi0 + q];
+          st_y0[q] = (int32_t)(R.wi_y0[wi0 + q] - yb0);
+          st_y1[q] = (int32_t)(R.wi_y1[wi0 + q] - yb0);
+          st_kd[q] = R.wi_kd[wi0 + q];
+        }
+        for (int64_t q = threadIdx.x; q < np_; q += HUB_THREADS) {
+          st_pp[q] = R.pred_p[yb0 + q];
+          st_pu[q] = R.pred_u[yb0 + q];
+        }
+        __syncthreads();
+        for (int64_t q = warp; q < ni; q += nw) {
+          const int p = st_p[q];
+          const int slot = st_sl[q];
+          const int y1 = st_y1[q];
+          int y = st_y0[q];
+          const int64_t kd = st_kd[q];
+          const double dv = kd >= 0 ? gb[kd * 32] : 1.0;
+          double acc = slot < 0 ? w[p * 32] : 0.0;
+          for (; y + 8 <= y1; y += 8) {
+            double lv[8], uv[8];
+#pragma unroll
+            for (int k2 = 0; k2 < 8; ++k2) {
+              lv[k2] = w[st_pp[y + k2] * 32];
+              uv[k2] = gb[st_pu[y + k2] * 32];
+            }
+#pragma unroll
+            for (int k2 = 0; k2 < 8; ++k2) acc -= lv[k2] * uv[k2];
+          }
+          for (; y < y1; ++y) acc -= w[st_pp[y] * 32] * gb[st_pu[y] * 32];
+          if (slot < 0) {
+            if (kd >= 0) {
+              acc = acc / dv;
+            } else if (kd == -2) {
+              bool fired;
+              const double piv = acc;
+              acc = perturb(piv, thr, fired);
+              if (fired && live) atomicAdd(&P.npert[b], 1);
+            }
+            w[p * 32] = acc;
+          } else {
+            scr[(size_t)slot * 32] = acc;
+          }
+        }
+      } else
       for (int64_t it = wi0 + warp; it < wi1; it += nw) {
         const int p = R.wi_p[it];
         const int slot = R.wi_slot[it];
