@@ -83,6 +83,7 @@ struct TaskDesc {
 template <bool STAGED>
 __global__ void k_bt_pipe(DevSym, BatchP, DevProg, const TaskDesc *, int64_t, const double *, double *, int *,
                           int *, int, int, int);
+__global__ void k_bt_lev0(DevSym, BatchP, DevProg, const int32_t *, int, int, const double *, double *, int *, int);
 __global__ void k_bt_hub(DevSym, BatchP, DevProg, const int32_t *, int, int, const double *, double *,
                          double *, int, int *, int);
 __global__ void k_batch_bhat(DevSym, const int32_t *, const double *, double *, int64_t);
@@ -151,6 +152,7 @@ struct hy_handle {
   int *d_bwd_flags = nullptr;
   int64_t bwd_flags_cap = 0;
   int bwd_persistent = 0;
+  int lev0_split = 1;
   int epoch_bwd = 0;
   double *d_y = nullptr;          // single-solve workspace [n]
   double *d_bf = nullptr;         // batched factor workspace
@@ -183,6 +185,7 @@ struct hy_handle {
     int l0, l1;
     TaskDesc *d_tasks = nullptr;   // task descriptors in diagonal claim order
     int64_t ntasks = 0;
+    bool lev0 = false;             // level 0 of this segment runs in k_bt_lev0
   };
   std::vector<Seg> segs;
   int segs_G = -1;
@@ -300,6 +303,8 @@ static int build_segments(hy_handle *h, int G) {
     hy_handle::Seg sg;
     sg.l0 = l;
     sg.l1 = l1;
+    sg.lev0 = (l == 0 && h->lev0_split && h->bl_hptr[1] == h->bl_hptr[0]);
+    const int lb = sg.lev0 ? 1 : 0;   // level 0 runs in k_bt_lev0
     const int L = l1 - l;
     std::vector<TaskDesc> tasks;
     tasks.reserve((size_t)(h->bl_rptr[l1] - h->bl_rptr[l]) * G);
@@ -318,7 +323,7 @@ static int build_segments(hy_handle *h, int G) {
     };
     const int sk = h->skew;
     for (int d = 0; d < sk * (G - 1) + L; ++d)
-      for (int k = 0; k < L && k <= d; ++k) {
+      for (int k = lb; k < L && k <= d; ++k) {
         if ((d - k) % sk) continue;
         const int g = (d - k) / sk;
         if (g >= G) continue;
@@ -402,6 +407,9 @@ int hy_create(int device, hy_handle **out) {
   }
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_bt_hub, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hub_smem_bytes());
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_bt_lev0, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)pipe_smem_bytes(false));
   e = cudaFuncSetAttribute(k_bt_pipe<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)pipe_smem_bytes(true));
   if (e == cudaSuccess)
@@ -442,6 +450,11 @@ int hy_set_option(hy_handle *h, const char *name, int64_t value) {
   if (!h || !name) return fail(HY_INVALID_ARGUMENT, "null handle/name");
   if (std::string(name) == "group_batch" && value >= 1) {
     h->gbatch = (int)value;
+    return HY_OK;
+  }
+  if (std::string(name) == "lev0_split") {
+    h->lev0_split = value != 0;
+    h->segs_G = -1;
     return HY_OK;
   }
   if (std::string(name) == "bwd_persistent") {
@@ -1093,6 +1106,14 @@ int hy_refactorize_batched(hy_handle *h, int64_t B, const double *d_vals, double
       k_bt_hub<<<(unsigned)(nh * G), 1024, hub_smem_bytes(), st>>>(h->S, P, h->prog, h->d_bl_hubs + h->bl_hptr[l], nh, G,
                                                    d_b_fuse, h->d_by, h->d_scratch, h->max_slots,
                                                    h->d_flags, h->epoch);
+      h->launches++;
+    }
+    if (sg.lev0) {
+      const int n0 = (int)(h->bl_rptr[1] - h->bl_rptr[0]);
+      const int64_t tasks0 = (int64_t)n0 * G;
+      const int grid0 = (int)((tasks0 + 3) / 4 < (int64_t)h->sm_count * 24 ? (tasks0 + 3) / 4 : h->sm_count * 24);
+      k_bt_lev0<<<grid0, 128, pipe_smem_bytes(false), st>>>(h->S, P, h->prog, h->d_bl_rows, n0, G, d_b_fuse,
+                                                            h->d_by, h->d_flags, h->epoch);
       h->launches++;
     }
     if (sg.ntasks) {

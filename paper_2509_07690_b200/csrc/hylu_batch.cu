@@ -297,6 +297,26 @@ __global__ void __launch_bounds__(PIPE_WARPS * 32, STAGED ? 3 : 6)
   }
 }
 
+// Level 0 of the batched factorization: no dependencies, so no claims, polls or
+// fences — one warp per (node, group); completion flags are plain stores (the
+// pipeline kernel that reads them is launched after this one on the same stream).
+__global__ void __launch_bounds__(PIPE_WARPS * 32, 6)
+    k_bt_lev0(DevSym S, BatchP P, DevProg R, const int32_t *nodes, int count, int G, const double *rhs,
+              double *Y, int *flags, int epoch) {
+  extern __shared__ __align__(16) double pipe_smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double *wsm_w = pipe_smem + (size_t)warp * PIPE_WS * 32;
+  const int64_t total = (int64_t)count * G;
+  for (int64_t t = (int64_t)blockIdx.x * PIPE_WARPS + warp; t < total;
+       t += (int64_t)gridDim.x * PIPE_WARPS) {
+    const int u = nodes[t / G];
+    const int g = (int)(t % G);
+    const longlong4 nr = R.node_rec[u];
+    bt_node<false>(S, P, R, u, nr, g, rhs, Y, wsm_w, PIPE_WS, nullptr, nullptr, lane, 0);
+    if (lane == 0) flags[(int64_t)u * G + g] = epoch;
+  }
+}
+
 template __global__ void k_bt_pipe<false>(DevSym, BatchP, DevProg, const TaskDesc *, int64_t,
                                           const double *, double *, int *, int *, int, int, int);
 template __global__ void k_bt_pipe<true>(DevSym, BatchP, DevProg, const TaskDesc *, int64_t,
