@@ -152,7 +152,7 @@ struct hy_handle {
   int *d_bwd_flags = nullptr;
   int64_t bwd_flags_cap = 0;
   int bwd_persistent = 0;
-  int lev0_split = 1;
+  int lev0_split = 0;
   int epoch_bwd = 0;
   double *d_y = nullptr;          // single-solve workspace [n]
   double *d_bf = nullptr;         // batched factor workspace
