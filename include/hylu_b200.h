@@ -151,6 +151,7 @@ typedef struct {
   const int32_t *level_smax, *level_mmax;                          /* [nlevels] */
   const int32_t *src_v, *src_pb, *src_tb;   /* [nsrc] source node, block position, first block row */
   const int64_t *lev_up_big;                /* [nlevels] first item routed to the DMMA kernel */
+  const int64_t *lev_up_reg;                /* [nlevels] first per-source item (before: packed) */
 } hy_fanin_plan;
 int hy_upload_fanin_plan(hy_handle *h, const hy_fanin_plan *plan);
 

@@ -57,6 +57,7 @@ __global__ void k_fi_panel(DevSym, CallP, FaninDev, int);
 __global__ void k_fi_x(DevSym, CallP, FaninDev, int);
 __global__ void k_fi_upd(DevSym, CallP, FaninDev, int, int, int);
 __global__ void k_fi_upd_mma(DevSym, CallP, FaninDev, int, int, int);
+__global__ void k_fi_upd_pk(DevSym, CallP, FaninDev, int, int, int);
 size_t fi_upd_smem(int, int);
 size_t pipe_smem_bytes(bool staged);
 size_t hub_smem_bytes();
@@ -210,6 +211,7 @@ struct hy_handle {
   std::vector<void *> fi_allocs;
   std::vector<int64_t> fi_lu, fi_pt, fi_xp, fi_up;   // per-level offsets
   std::vector<int64_t> fi_upbig;                     // per level: first DMMA-routed item
+  std::vector<int64_t> fi_upreg;                     // per level: first per-source item
   int fi_mma = 0;                                    // option "fanin_dmma" (bitwise-equal results; slower here)
   std::vector<int32_t> fi_smax, fi_mmax;
   int sm_count = 148;
@@ -705,6 +707,7 @@ int hy_upload_fanin_plan(hy_handle *h, const hy_fanin_plan *d) {
   h->fi_xp.assign(d->xp_ptr, d->xp_ptr + nl + 1);
   h->fi_up.assign(d->lev_up, d->lev_up + nl + 1);
   h->fi_upbig.assign(d->lev_up_big, d->lev_up_big + nl);
+  h->fi_upreg.assign(d->lev_up_reg, d->lev_up_reg + nl);
   h->fi_smax.assign(d->level_smax, d->level_smax + nl);
   h->fi_mmax.assign(d->level_mmax, d->level_mmax + nl);
   size_t mx = 0;
@@ -714,6 +717,7 @@ int hy_upload_fanin_plan(hy_handle *h, const hy_fanin_plan *d) {
   }
   CK(cudaFuncSetAttribute(k_fi_upd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx));
   CK(cudaFuncSetAttribute(k_fi_upd_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx));
+  CK(cudaFuncSetAttribute(k_fi_upd_pk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx));
   CK(cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, h->device));
   CK(cudaFuncSetAttribute(k_fi_panel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)(64 * 256 * sizeof(double))));
@@ -741,10 +745,16 @@ static int run_fanin(hy_handle *h, const CallP &P, cudaStream_t st) {
     if (nxp) { k_fi_x<<<nxp, 256, 2 * 64 * 65 * sizeof(double), st>>>(h->S, P, h->fi, (int)h->fi_xp[l]); h->launches++; }
     if (nup) {
       const size_t sm = fi_upd_smem(h->fi_smax[l], h->fi_mmax[l]);
+      const int reg = (int)h->fi_upreg[l];
       const int split = h->fi_mma ? (int)h->fi_upbig[l] : (int)h->fi_up[l + 1];
-      const int nsm = split - (int)h->fi_up[l], nbig = (int)h->fi_up[l + 1] - split;
+      const int npk = reg - (int)h->fi_up[l];
+      const int nsm = split - reg, nbig = (int)h->fi_up[l + 1] - split;
+      if (npk) {
+        k_fi_upd_pk<<<npk, 256, sm, st>>>(h->S, P, h->fi, (int)h->fi_up[l], h->fi_smax[l], h->fi_mmax[l]);
+        h->launches++;
+      }
       if (nsm) {
-        k_fi_upd<<<nsm, 256, sm, st>>>(h->S, P, h->fi, (int)h->fi_up[l], h->fi_smax[l], h->fi_mmax[l]);
+        k_fi_upd<<<nsm, 256, sm, st>>>(h->S, P, h->fi, reg, h->fi_smax[l], h->fi_mmax[l]);
         h->launches++;
       }
       if (nbig) {

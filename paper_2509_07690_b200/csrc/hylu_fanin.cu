@@ -268,13 +268,102 @@ constexpr int FI_TILE = 64;
 constexpr int FI_KC = 32;      // K (source rows) chunk staged per pass
 constexpr int KLD = FI_KC + 1;
 
+__global__ void __launch_bounds__(FI_THREADS) k_fi_upd(DevSym S, CallP P, FaninDev D, int base,
+                                                       int Smax, int Mmax) {
+  extern __shared__ __align__(16) double fs[];
+  __shared__ int tcol[FI_TILE];
+  __shared__ int spos[FI_TILE];
+  const int j = base + blockIdx.x;
+  const int T = D.up_t[j];
+  const int c0 = D.up_c0[j], c1 = D.up_c1[j];
+  const int tw = c1 - c0;
+  const int tid = threadIdx.x;
+  const int r = (int)S.first[T];
+  const int s = (int)(S.first[T + 1] - r);
+  const int64_t tc0 = S.colptr[T];
+  const int W = (int)(S.colptr[T + 1] - tc0);
+  double *Pm = P.F + S.valoff[T];
+  double *acc = fs;                          // s x FI_TILE
+  double *Xs = acc + (size_t)Smax * FI_TILE; // Smax x KLD
+  double *Ut = Xs + (size_t)Smax * KLD;      // FI_KC x FXLD
+  (void)Mmax;
+  for (int c = tid; c < tw; c += FI_THREADS) tcol[c] = S.cols[tc0 + c0 + c];
+  for (int idx = tid; idx < s * FI_TILE; idx += FI_THREADS) {
+    const int t = idx / FI_TILE, c = idx - t * FI_TILE;
+    acc[idx] = c < tw ? Pm[(int64_t)t * W + c0 + c] : 0.0;
+  }
+  const int tr = tid >> 4, tcl = tid & 15;
+  for (int64_t z = D.up_ptr[j]; z < D.up_ptr[j + 1]; ++z) {
+    const int v = D.src_v[z];
+    const int q0 = D.src_q0[z];
+    const int nq = D.src_q1[z] - q0;
+    const int vf = (int)S.first[v];
+    const int vs = (int)(S.first[v + 1] - vf);
+    const int64_t vc0 = S.colptr[v];
+    const int vW = (int)(S.colptr[v + 1] - vc0);
+    const int vnl = S.nl[v];
+    const double *vb = P.F + S.valoff[v];
+    const int pb0 = D.src_pb[z];
+    const int tb0 = D.src_tb[z];
+    const int m = vs - tb0;
+    const int qbase = vnl + vs + q0;
+    __syncthreads();
+    if (tid < nq) spos[tid] = lower_bound_i32(tcol, 0, tw, S.cols[vc0 + qbase + tid]);
+    double c4[4][4];
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) c4[x][y] = 0.0;
+    for (int k0 = 0; k0 < m; k0 += FI_KC) {
+      const int kc = min(FI_KC, m - k0);
+      if (k0) __syncthreads();
+      for (int idx = tid; idx < s * kc; idx += FI_THREADS) {
+        const int t = idx / kc, a = idx - t * kc;
+        Xs[t * KLD + a] = Pm[(int64_t)t * W + pb0 + k0 + a];
+      }
+      for (int idx = tid; idx < kc * FI_TILE; idx += FI_THREADS) {
+        const int a = idx >> 6, c = idx & 63;
+        Ut[a * FXLD + c] = c < nq ? vb[(int64_t)(tb0 + k0 + a) * vW + qbase + c] : 0.0;
+      }
+      __syncthreads();
+      for (int a = 0; a < kc; ++a) {
+        double xv[4], uv[4];
+#pragma unroll
+        for (int x = 0; x < 4; ++x) xv[x] = (tr + 16 * x < s) ? Xs[(tr + 16 * x) * KLD + a] : 0.0;
+#pragma unroll
+        for (int y = 0; y < 4; ++y) uv[y] = Ut[a * FXLD + tcl + 16 * y];
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y) c4[x][y] = fma(xv[x], uv[y], c4[x][y]);
+      }
+    }
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      const int t = tr + 16 * x;
+      if (t < s) {
+#pragma unroll
+        for (int y = 0; y < 4; ++y) {
+          const int c = tcl + 16 * y;
+          if (c < nq) acc[t * FI_TILE + spos[c]] -= c4[x][y];
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int idx = tid; idx < s * FI_TILE; idx += FI_THREADS) {
+    const int t = idx / FI_TILE, c = idx - t * FI_TILE;
+    if (c < tw) Pm[(int64_t)t * W + c0 + c] = acc[idx];
+  }
+}
+
 // Sources of an item are packed into K-slices of <= FI_KC source rows: each
 // slice's multiplier columns go to Xs and its U rows are scattered into the
 // tile's 64-column space of Ut (zeros elsewhere), so one register-tiled GEMM
 // handles many small sources per synchronisation round and the whole item is
 // accumulated in registers (K-aggregated over all of its sources) before the
 // tile is updated once.
-__global__ void __launch_bounds__(FI_THREADS) k_fi_upd(DevSym S, CallP P, FaninDev D, int base,
+__global__ void __launch_bounds__(FI_THREADS) k_fi_upd_pk(DevSym S, CallP P, FaninDev D, int base,
                                                        int Smax, int Mmax) {
   extern __shared__ __align__(16) double fs[];
   __shared__ int tcol[FI_TILE];
@@ -292,6 +381,7 @@ __global__ void __launch_bounds__(FI_THREADS) k_fi_upd(DevSym S, CallP P, FaninD
   __shared__ int64_t s_znext;
   __shared__ int s_anext;
   __shared__ int kmap[FI_KC];          // K row -> slice
+  __shared__ int pcache[FI_KC][FI_TILE];  // tile position of each slice column
   const int j = base + blockIdx.x;
   const int T = D.up_t[j];
   const int c0 = D.up_c0[j], c1 = D.up_c1[j];
@@ -382,16 +472,18 @@ __global__ void __launch_bounds__(FI_THREADS) k_fi_upd(DevSym S, CallP P, FaninD
       Xs[t * KLD + a] = Pm[(int64_t)t * W + sl_pb[q] + (a - sl_koff[q])];
     }
     for (int idx = tid; idx < kb * FI_TILE; idx += FI_THREADS) Ut[(idx >> 6) * FXLD + (idx & 63)] = 0.0;
+    for (int idx = tid; idx < nsl * FI_TILE; idx += FI_THREADS) {
+      const int q = idx >> 6, c = idx & 63;
+      if (c < sl_nq[q]) pcache[q][c] = lower_bound_i32(tcol, 0, tw, S.cols[sl_vc0[q] + sl_qoff[q] + c]);
+    }
     __syncthreads();
     // scatter each slice's U rows into the tile's column space
-    for (int q = 0; q < nsl; ++q) {
-      const int nq = sl_nq[q], m = sl_m[q];
-      for (int idx = tid; idx < nq * m; idx += FI_THREADS) {
-        const int c = idx % nq, a = idx / nq;
-        const int key = S.cols[sl_vc0[q] + sl_qoff[q] + c];
-        const int pos = lower_bound_i32(tcol, 0, tw, key);
-        Ut[(sl_koff[q] + a) * FXLD + pos] =
-            P.F[sl_vbase[q] + (int64_t)(sl_urow[q] + a) * sl_vW[q] + sl_qoff[q] + c];
+    for (int idx = tid; idx < kb * FI_TILE; idx += FI_THREADS) {
+      const int a = idx >> 6, c = idx & 63;
+      const int q = kmap[a];
+      if (c < sl_nq[q]) {
+        const int ar = a - sl_koff[q];
+        Ut[a * FXLD + pcache[q][c]] = P.F[sl_vbase[q] + (int64_t)(sl_urow[q] + ar) * sl_vW[q] + sl_qoff[q] + c];
       }
     }
     __syncthreads();

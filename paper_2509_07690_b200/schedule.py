@@ -803,6 +803,7 @@ class FaninPlan:
     level_smax: np.ndarray     # max target rows among update items of a level
     level_mmax: np.ndarray     # max source rows of a level
     lev_up_big: np.ndarray     # per level: first update item whose target has >= BIG_ROWS rows
+    lev_up_reg: np.ndarray     # per level: first item of the per-source (regular) group
 
     @property
     def nlevels(self):
@@ -839,25 +840,33 @@ def _fanin_levels(first, colptr, cols, nl, dptr, deps, node_of):
 BIG_ROWS = 32
 
 
-def _split_items(out, rows, nlev):
-    """Within each level, order update items small-target first, big (>= BIG_ROWS rows)
-    after, so each group is a contiguous launch range (FFMA / DMMA kernels)."""
+def _split_items(out, rows, nlev, src_rows):
+    """Within each level order the update items in three contiguous launch groups:
+    0 = many small sources (packed K-slice kernel), 1 = regular (per-source FFMA
+    kernel), 2 = target >= BIG_ROWS rows (DMMA-eligible; runs the FFMA kernel
+    unless DMMA routing is enabled)."""
     (lu_ptr, lu_nodes, pt_ptr, pt_node, pt_c0, pt_c1, xp_ptr, xp_edge, xp_tgt,
      lev_up, up_t, up_c0, up_c1, up_ptr, src_k, src_q0, src_q1) = out
     nitem = len(up_t)
     lvl = np.repeat(np.arange(nlev), np.diff(lev_up))
-    big = (rows[up_t] >= BIG_ROWS).astype(np.int64)
-    order = np.lexsort((big, lvl))
+    nsrc = np.diff(up_ptr)
+    msum = np.add.reduceat(src_rows, up_ptr[:-1]) if len(src_rows) else np.zeros(nitem)
+    packed = (nsrc >= 3) & (msum < 8 * nsrc)
+    big = (rows[up_t] >= BIG_ROWS) & ~packed
+    grp = np.where(packed, 0, np.where(big, 2, 1)).astype(np.int64)
+    order = np.lexsort((grp, lvl))
     cnt = np.diff(up_ptr)[order]
     new_ptr = np.zeros(nitem + 1, np.int64)
     np.cumsum(cnt, out=new_ptr[1:])
     gather = np.repeat(up_ptr[:-1][order], cnt) + (np.arange(new_ptr[-1]) - np.repeat(new_ptr[:-1], cnt))
-    nsmall = np.bincount(lvl[big == 0], minlength=nlev) if nitem else np.zeros(nlev, np.int64)
-    split = lev_up[:-1] + nsmall
+    n0 = np.bincount(lvl[grp == 0], minlength=nlev) if nitem else np.zeros(nlev, np.int64)
+    n1 = np.bincount(lvl[grp == 1], minlength=nlev) if nitem else np.zeros(nlev, np.int64)
+    reg = lev_up[:-1] + n0
+    split = reg + n1
     out = (lu_ptr, lu_nodes, pt_ptr, pt_node, pt_c0, pt_c1, xp_ptr, xp_edge, xp_tgt, lev_up,
            up_t[order], up_c0[order], up_c1[order], new_ptr, src_k[gather], src_q0[gather],
            src_q1[gather])
-    return out, split.astype(np.int64)
+    return out, split.astype(np.int64), reg.astype(np.int64)
 
 
 def build_fanin_plan(sym, tw=FANIN_TILE, pw=PANEL_TILE):
@@ -868,7 +877,14 @@ def build_fanin_plan(sym, tw=FANIN_TILE, pw=PANEL_TILE):
                       flev, nlev, tw, pw)
     dep_pb = _dep_block_pos(s.node_first, s.node_kind, s.colptr, s.cols, s.nl, s.dep_ptr, s.deps)
     rows = np.diff(s.node_first)
-    out, split = _split_items(out, rows, nlev)
+    # source rows per update-source record (rows of v from its first present block row)
+    up_ptr, up_t, src_k = out[13], out[10], out[14]
+    tgt = np.repeat(up_t.astype(np.int64), np.diff(up_ptr))
+    dk = s.dep_ptr[tgt] + src_k
+    v = s.deps[dk]
+    tb0 = s.cols[s.colptr[tgt] + dep_pb[dk]] - s.node_first[v]
+    src_rows = (rows[v] - tb0).astype(np.int64)
+    out, split, reg = _split_items(out, rows, nlev, src_rows)
     lu_ptr, lu_nodes = out[0], out[1]
     lev_up, up_t = out[9], out[10]
     smax = np.ones(nlev, np.int32)
@@ -880,7 +896,7 @@ def build_fanin_plan(sym, tw=FANIN_TILE, pw=PANEL_TILE):
         nodes = lu_nodes[lu_ptr[lv]:lu_ptr[lv + 1]]
         if len(nodes):
             mmax[lv] = int(rows[nodes].max())
-    return FaninPlan(*out, dep_pb, smax, mmax, split)
+    return FaninPlan(*out, dep_pb, smax, mmax, split, reg)
 
 
 def fanin_source_records(sym, plan):
