@@ -851,7 +851,10 @@ def _split_items(out, rows, nlev, src_rows):
     lvl = np.repeat(np.arange(nlev), np.diff(lev_up))
     nsrc = np.diff(up_ptr)
     msum = np.add.reduceat(src_rows, up_ptr[:-1]) if len(src_rows) else np.zeros(nitem)
-    packed = (nsrc >= 3) & (msum < 8 * nsrc)
+    import os
+    pm = float(os.environ.get("HYLU_PACK_M", "8"))
+    pn = int(os.environ.get("HYLU_PACK_N", "3"))
+    packed = (nsrc >= pn) & (msum < pm * nsrc)
     big = (rows[up_t] >= BIG_ROWS) & ~packed
     grp = np.where(packed, 0, np.where(big, 2, 1)).astype(np.int64)
     order = np.lexsort((grp, lvl))
