@@ -852,8 +852,8 @@ def _split_items(out, rows, nlev, src_rows):
     nsrc = np.diff(up_ptr)
     msum = np.add.reduceat(src_rows, up_ptr[:-1]) if len(src_rows) else np.zeros(nitem)
     import os
-    pm = float(os.environ.get("HYLU_PACK_M", "8"))
-    pn = int(os.environ.get("HYLU_PACK_N", "3"))
+    pm = float(os.environ.get("HYLU_PACK_M", "4"))
+    pn = int(os.environ.get("HYLU_PACK_N", "4"))
     packed = (nsrc >= pn) & (msum < pm * nsrc)
     big = (rows[up_t] >= BIG_ROWS) & ~packed
     grp = np.where(packed, 0, np.where(big, 2, 1)).astype(np.int64)
