@@ -58,6 +58,8 @@ __global__ void k_fi_x(DevSym, CallP, FaninDev, int);
 __global__ void k_fi_upd(DevSym, CallP, FaninDev, int, int, int);
 __global__ void k_fi_upd_mma(DevSym, CallP, FaninDev, int, int, int);
 __global__ void k_fi_upd_pk(DevSym, CallP, FaninDev, int, int, int);
+__global__ void k_fi_upd3(DevSym, CallP, FaninDev, int, int, int);
+size_t fi_upd3_smem(int);
 size_t fi_upd_smem(int, int);
 size_t pipe_smem_bytes(bool staged);
 size_t hub_smem_bytes();
@@ -212,6 +214,7 @@ struct hy_handle {
   std::vector<int64_t> fi_lu, fi_pt, fi_xp, fi_up;   // per-level offsets
   std::vector<int64_t> fi_upbig;                     // per level: first DMMA-routed item
   std::vector<int64_t> fi_upreg;                     // per level: first per-source item
+  int fi_v3 = 1;                                     // option "fanin_v3"
   int fi_mma = 0;                                    // option "fanin_dmma" (bitwise-equal results; slower here)
   std::vector<int32_t> fi_smax, fi_mmax;
   int sm_count = 148;
@@ -461,6 +464,10 @@ int hy_set_option(hy_handle *h, const char *name, int64_t value) {
   }
   if (std::string(name) == "bwd_persistent") {
     h->bwd_persistent = value != 0;
+    return HY_OK;
+  }
+  if (std::string(name) == "fanin_v3") {
+    h->fi_v3 = value != 0;
     return HY_OK;
   }
   if (std::string(name) == "fanin_dmma") {
@@ -718,6 +725,7 @@ int hy_upload_fanin_plan(hy_handle *h, const hy_fanin_plan *d) {
   CK(cudaFuncSetAttribute(k_fi_upd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx));
   CK(cudaFuncSetAttribute(k_fi_upd_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx));
   CK(cudaFuncSetAttribute(k_fi_upd_pk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx));
+  CK(cudaFuncSetAttribute(k_fi_upd3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fi_upd3_smem(64)));
   CK(cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, h->device));
   CK(cudaFuncSetAttribute(k_fi_panel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)(64 * 256 * sizeof(double))));
@@ -754,7 +762,11 @@ static int run_fanin(hy_handle *h, const CallP &P, cudaStream_t st) {
         h->launches++;
       }
       if (nsm) {
-        k_fi_upd<<<nsm, 256, sm, st>>>(h->S, P, h->fi, reg, h->fi_smax[l], h->fi_mmax[l]);
+        if (h->fi_v3)
+          k_fi_upd3<<<nsm, 256, fi_upd3_smem(h->fi_smax[l]), st>>>(h->S, P, h->fi, reg, h->fi_smax[l],
+                                                                   h->fi_mmax[l]);
+        else
+          k_fi_upd<<<nsm, 256, sm, st>>>(h->S, P, h->fi, reg, h->fi_smax[l], h->fi_mmax[l]);
         h->launches++;
       }
       if (nbig) {

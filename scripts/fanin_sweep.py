@@ -15,8 +15,9 @@ an = an_mod.analyze(p.A, SolverConfig(ordering=p.ordering))
 dv = torch.from_numpy(np.array(p.A.values)).cuda()
 f = api.factorize_analysis(an, dv)
 ctx = f._ctx
+opt = os.environ.get("SWEEP_OPT", "fanin_dmma")
 for v in (1, 0, 1):
-    ctx.set_option("fanin_dmma", v)
+    ctx.set_option(opt, v)
     ts = []
     for _ in range(3):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -26,5 +27,5 @@ for v in (1, 0, 1):
         torch.cuda.synchronize()
         ts.append(a.elapsed_time(b))
     err = float((g.values - f.values).abs().max())
-    print(name, "dmma", v, "factor ms %.1f" % min(ts), "GFLOP/s %.0f" % (an.symbolic.flops / min(ts) / 1e6),
+    print(name, opt, v, "factor ms %.1f" % min(ts), "GFLOP/s %.0f" % (an.symbolic.flops / min(ts) / 1e6),
           "maxdiff vs first %.2e" % err, flush=True)
