@@ -887,6 +887,15 @@ def build_fanin_plan(sym, tw=FANIN_TILE, pw=PANEL_TILE):
     v = s.deps[dk]
     tb0 = s.cols[s.colptr[tgt] + dep_pb[dk]] - s.node_first[v]
     src_rows = (rows[v] - tb0).astype(np.int64)
+    import os
+    cap_rows = int(os.environ.get("HYLU_MERGE_ROWS", "256"))
+    if cap_rows > 0:
+        cap_recs = int(os.environ.get("HYLU_MERGE_RECS", "64"))
+        (lev_up, up_t, up_c0, up_c1, up_ptr, src_k, src_q0, src_q1, src_rows) = _merge_items(
+            nlev, flev, s.node_first, s.colptr, s.cols, s.nl, s.dep_ptr, s.deps, s.node_of,
+            out[9], out[10], out[11], out[12], out[13], out[14], out[15], out[16], src_rows,
+            cap_rows, cap_recs)
+        out = out[:9] + (lev_up, up_t, up_c0, up_c1, up_ptr, src_k, src_q0, src_q1)
     out, split, reg = _split_items(out, rows, nlev, src_rows)
     lu_ptr, lu_nodes = out[0], out[1]
     lev_up, up_t = out[9], out[10]
@@ -914,3 +923,157 @@ def fanin_source_records(sym, plan):
     pb0 = plan.dep_pb[dk].astype(np.int32)
     tb0 = (s.cols[s.colptr[tgt] + pb0] - s.node_first[v]).astype(np.int32)
     return v, pb0, tb0
+
+
+# --------------------------------------------------------------------------- deadline merging
+@njit(cache=True)
+def _merge_items(nlev, flev, first, colptr, cols, nl, dptr, deps, node_of, lev_up, up_t, up_c0,
+                 up_c1, up_ptr, src_k, src_q0, src_q1, src_rows, cap_rows, cap_recs):
+    """Re-chunk each (target, tile)'s update records across levels.
+
+    Deadline D of a tile = the first level consuming it: the target's own level if
+    the tile reaches the block/panel, and the level of every source block owner
+    inside the tile (its multiplier block X is formed there).  Records (sorted by
+    source level, then dependency index) are packed into chunks of at most
+    cap_rows source rows / cap_recs records; a chunk runs at the level of its last
+    source (as early as possible), bumped to the next level if that tile already
+    has a chunk there (never beyond D-1, else merged)."""
+    nitem = len(up_t)
+    # group items by (target, tile) -> key order
+    keyT = up_t.astype(np.int64)
+    key = keyT * (1 << 20) + up_c0.astype(np.int64)
+    order = np.argsort(key, kind="mergesort")
+    out_lvl = []
+    out_t = []
+    out_c0 = []
+    out_c1 = []
+    out_ptr = [np.int64(0)]
+    o_k = []
+    o_q0 = []
+    o_q1 = []
+    o_rows = []
+    x = 0
+    item_level = np.empty(nitem, np.int64)
+    for lv in range(nlev):
+        for it in range(lev_up[lv], lev_up[lv + 1]):
+            item_level[it] = lv
+    while x < nitem:
+        it0 = order[x]
+        T = up_t[it0]
+        c0 = up_c0[it0]
+        x1 = x
+        while x1 < nitem and up_t[order[x1]] == T and up_c0[order[x1]] == c0:
+            x1 += 1
+        c1 = up_c1[it0]
+        # deadline
+        tc0 = colptr[T]
+        L = nl[T]
+        D = nlev
+        if c1 > L:
+            D = flev[T]
+        hiL = min(c1, L)
+        q = c0
+        while q < hiL:
+            w = node_of[cols[tc0 + q]]
+            if flev[w] < D:
+                D = flev[w]
+            q += 1
+        # gather records (items at increasing level; records already in dep order)
+        recs_lv = []
+        recs_z = []
+        for y in range(x, x1):
+            it = order[y]
+            for z in range(up_ptr[it], up_ptr[it + 1]):
+                recs_lv.append(item_level[it])
+                recs_z.append(z)
+        nr = len(recs_z)
+        ro = np.empty(nr, np.int64)
+        lvs = np.empty(nr, np.int64)
+        for a in range(nr):
+            lvs[a] = recs_lv[a]
+        idx = np.argsort(lvs, kind="mergesort")
+        for a in range(nr):
+            ro[a] = recs_z[idx[a]]
+        # part A: records whose source level is below the tile deadline are merged
+        # into capped chunks run as early as possible (never later than D-1);
+        # part B: the rest keep one chunk per source level (always valid).
+        last_level = -1
+        a = 0
+        nA = 0
+        while nA < nr and recs_lv[idx[nA]] <= D - 1:
+            nA += 1
+        while a < nr:
+            rows_sum = 0
+            b = a
+            if a < nA:
+                while b < nA and (b - a) < cap_recs and (rows_sum + src_rows[ro[b]] <= cap_rows or b == a):
+                    rows_sum += src_rows[ro[b]]
+                    b += 1
+                lvl = recs_lv[idx[b - 1]]
+                if lvl <= last_level:
+                    lvl = last_level + 1
+                if lvl > D - 1:
+                    lvl = D - 1
+            else:
+                lv0 = recs_lv[idx[a]]
+                while b < nr and recs_lv[idx[b]] == lv0:
+                    b += 1
+                lvl = lv0
+            if lvl <= last_level and len(out_t) > 0:
+                # same level as this tile's previous chunk: merge into it
+                for c in range(a, b):
+                    z = ro[c]
+                    o_k.append(src_k[z])
+                    o_q0.append(src_q0[z])
+                    o_q1.append(src_q1[z])
+                    o_rows.append(src_rows[z])
+                out_ptr[-1] = np.int64(len(o_k))
+                a = b
+                continue
+            out_lvl.append(lvl)
+            out_t.append(T)
+            out_c0.append(c0)
+            out_c1.append(c1)
+            for c in range(a, b):
+                z = ro[c]
+                o_k.append(src_k[z])
+                o_q0.append(src_q0[z])
+                o_q1.append(src_q1[z])
+                o_rows.append(src_rows[z])
+            out_ptr.append(np.int64(len(o_k)))
+            last_level = lvl
+            a = b
+        x = x1
+    n = len(out_t)
+    lv_arr = np.empty(n, np.int64)
+    for a in range(n):
+        lv_arr[a] = out_lvl[a]
+    perm = np.argsort(lv_arr, kind="mergesort")
+    new_lev = np.zeros(nlev + 1, np.int64)
+    for a in range(n):
+        new_lev[lv_arr[a] + 1] += 1
+    for l in range(nlev):
+        new_lev[l + 1] += new_lev[l]
+    nt = np.empty(n, np.int32)
+    nc0 = np.empty(n, np.int32)
+    nc1 = np.empty(n, np.int32)
+    nptr = np.zeros(n + 1, np.int64)
+    tot = len(o_k)
+    nk = np.empty(tot, np.int32)
+    nq0 = np.empty(tot, np.int32)
+    nq1 = np.empty(tot, np.int32)
+    nrw = np.empty(tot, np.int64)
+    pos = 0
+    for a in range(n):
+        it = perm[a]
+        nt[a] = out_t[it]
+        nc0[a] = out_c0[it]
+        nc1[a] = out_c1[it]
+        for z in range(out_ptr[it], out_ptr[it + 1]):
+            nk[pos] = o_k[z]
+            nq0[pos] = o_q0[z]
+            nq1[pos] = o_q1[z]
+            nrw[pos] = o_rows[z]
+            pos += 1
+        nptr[a + 1] = pos
+    return new_lev, nt, nc0, nc1, nptr, nk, nq0, nq1, nrw
