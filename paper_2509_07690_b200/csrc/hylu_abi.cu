@@ -214,7 +214,7 @@ struct hy_handle {
   std::vector<int64_t> fi_lu, fi_pt, fi_xp, fi_up;   // per-level offsets
   std::vector<int64_t> fi_upbig;                     // per level: first DMMA-routed item
   std::vector<int64_t> fi_upreg;                     // per level: first per-source item
-  int fi_v3 = 1;                                     // option "fanin_v3"
+  int fi_v3 = 0;                                     // option "fanin_v3" (slower; kept for experiments)
   int fi_mma = 0;                                    // option "fanin_dmma" (bitwise-equal results; slower here)
   std::vector<int32_t> fi_smax, fi_mmax;
   int sm_count = 148;
