@@ -888,7 +888,7 @@ def build_fanin_plan(sym, tw=FANIN_TILE, pw=PANEL_TILE):
     tb0 = s.cols[s.colptr[tgt] + dep_pb[dk]] - s.node_first[v]
     src_rows = (rows[v] - tb0).astype(np.int64)
     import os
-    cap_rows = int(os.environ.get("HYLU_MERGE_ROWS", "256"))
+    cap_rows = int(os.environ.get("HYLU_MERGE_ROWS", "0"))
     if cap_rows > 0:
         cap_recs = int(os.environ.get("HYLU_MERGE_RECS", "64"))
         (lev_up, up_t, up_c0, up_c1, up_ptr, src_k, src_q0, src_q1, src_rows) = _merge_items(
