@@ -86,6 +86,8 @@ struct TaskDesc {
 template <bool STAGED>
 __global__ void k_bt_pipe(DevSym, BatchP, DevProg, const TaskDesc *, int64_t, const double *, double *, int *,
                           int *, int, int, int);
+__global__ void k_bt_pipe2(DevSym, BatchP, DevProg, const TaskDesc *, int64_t, const double *, double *, int *,
+                           int *, int, int, int, int);
 __global__ void k_bt_lev0(DevSym, BatchP, DevProg, const int32_t *, int, int, const double *, double *, int *, int);
 __global__ void k_bt_hub(DevSym, BatchP, DevProg, const int32_t *, int, int, const double *, double *,
                          double *, int, int *, int);
@@ -182,6 +184,8 @@ struct hy_handle {
   int gbatch = 1 << 20;                    // unused (kept for hy_set_option compatibility)
   int staged = 0;                          // stage row sources with cp.async (option "staged")
   int nowait = 0;                          // timing experiment only: skip dependency waits
+  int pair = 1;                            // pipeline: one warp per (node, group pair)
+  int pipe_ws = 16;                        // pair-mode shared workspace columns per group
   int skew = 1;                            // diagonal claim order: group g+1 runs `skew` levels behind g
   // diagonal claim order per (segment, G): pair prefix sums, (level<<16|group), level offsets
   struct Seg {
@@ -327,12 +331,14 @@ static int build_segments(hy_handle *h, int G) {
       return t;
     };
     const int sk = h->skew;
-    for (int d = 0; d < sk * (G - 1) + L; ++d)
+    const int gs = h->pair ? 2 : 1;           // pair mode: tasks carry the even group of a pair
+    const int GT = (G + gs - 1) / gs;
+    for (int d = 0; d < sk * (GT - 1) + L; ++d)
       for (int k = lb; k < L && k <= d; ++k) {
         if ((d - k) % sk) continue;
         const int g = (d - k) / sk;
-        if (g >= G) continue;
-        for (int64_t q = h->bl_rptr[l + k]; q < h->bl_rptr[l + k + 1]; ++q) tasks.push_back(mk(rows[q], g));
+        if (g >= GT) continue;
+        for (int64_t q = h->bl_rptr[l + k]; q < h->bl_rptr[l + k + 1]; ++q) tasks.push_back(mk(rows[q], g * gs));
       }
     sg.ntasks = (int64_t)tasks.size();
     if (sg.ntasks) {
@@ -420,6 +426,8 @@ int hy_create(int device, hy_handle **out) {
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_bt_pipe<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)pipe_smem_bytes(false));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_bt_pipe2, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 2 * 64 * 32 * 8);
   if (e != cudaSuccess) {
     delete h;
     return fail(HY_CUDA_ERROR, std::string("cudaFuncSetAttribute(k_bt_pipe): ") + cudaGetErrorString(e));
@@ -481,6 +489,17 @@ int hy_set_option(hy_handle *h, const char *name, int64_t value) {
   }
   if (std::string(name) == "nowait_experiment") {
     h->nowait = (int)value;   // bitmask: 1 no waits, 2 no steps, 4 no scatter, 8 no copy-out
+    return HY_OK;
+  }
+  if (std::string(name) == "pair_groups") {
+    h->pair = value != 0;
+    h->segs_G = -1;
+    h->pipe_blocks = 0;
+    return HY_OK;
+  }
+  if (std::string(name) == "pipe_ws" && value >= 1 && value <= 64) {
+    h->pipe_ws = (int)value;
+    h->pipe_blocks = 0;
     return HY_OK;
   }
   if (std::string(name) == "staged") {
@@ -1043,7 +1062,7 @@ int hy_upload_row_programs(hy_handle *h, const hy_row_programs *d) {
 }
 
 static int batch_prepare(hy_handle *h, int64_t B) {
-  const int G = (int)((B + 31) / 32);
+  const int G = (int)((B + 63) / 64) * 2;   // even group count: pair mode's padding group
   const int64_t need = (int64_t)G * 32 * h->stored;
   if (need > h->bf_cap) {
     if (h->d_bf) CK(cudaFree(h->d_bf));
@@ -1098,7 +1117,10 @@ int hy_refactorize_batched(hy_handle *h, int64_t B, const double *d_vals, double
   h->epoch++;
   if (h->pipe_blocks == 0) {
     int per_sm = 0, sms = 0;
-    if (h->staged)
+    if (h->pair)
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bt_pipe2, 128,
+                                                       (size_t)4 * 2 * h->pipe_ws * 32 * 8));
+    else if (h->staged)
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bt_pipe<true>, 128, pipe_smem_bytes(true)));
     else
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bt_pipe<false>, 128,
@@ -1125,7 +1147,7 @@ int hy_refactorize_batched(hy_handle *h, int64_t B, const double *d_vals, double
         CK(cudaMalloc((void **)&h->d_scratch, sizeof(double) * need));
         h->scratch_cap = need;
       }
-      k_bt_hub<<<(unsigned)(nh * G), 1024, hub_smem_bytes(), st>>>(h->S, P, h->prog, h->d_bl_hubs + h->bl_hptr[l], nh, G,
+      k_bt_hub<<<(unsigned)(nh * G), 512, hub_smem_bytes(), st>>>(h->S, P, h->prog, h->d_bl_hubs + h->bl_hptr[l], nh, G,
                                                    d_b_fuse, h->d_by, h->d_scratch, h->max_slots,
                                                    h->d_flags, h->epoch);
       h->launches++;
@@ -1140,7 +1162,11 @@ int hy_refactorize_batched(hy_handle *h, int64_t B, const double *d_vals, double
     }
     if (sg.ntasks) {
       int *ctr = (int *)((long long *)h->d_counters + si);
-      if (h->staged)
+      if (h->pair)
+        k_bt_pipe2<<<h->pipe_blocks, 128, (size_t)4 * 2 * h->pipe_ws * 32 * 8, st>>>(
+            h->S, P, h->prog, sg.d_tasks, sg.ntasks, d_b_fuse, h->d_by, ctr, h->d_flags, h->epoch, G,
+            h->pipe_ws, h->nowait);
+      else if (h->staged)
         k_bt_pipe<true><<<h->pipe_blocks, 128, pipe_smem_bytes(true), st>>>(
             h->S, P, h->prog, sg.d_tasks, sg.ntasks, d_b_fuse, h->d_by, ctr, h->d_flags, h->epoch, G, h->nowait);
       else

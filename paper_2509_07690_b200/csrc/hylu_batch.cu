@@ -16,12 +16,11 @@
 namespace hy {
 
 constexpr int BW = 4;            // warps per block (bwd / fwd kernels)
-constexpr int HUB_THREADS = 1024;
-constexpr int HUB_CAPI = 2048;   // staged work items per level
-constexpr int HUB_CAPP = 8192;   // staged predecessor records per level
-size_t hub_smem_bytes() {
-  return (size_t)HUB_CAPP * (8 + 4) + (size_t)HUB_CAPI * (8 + 4 * 4);
-}
+constexpr int HUB_THREADS = 512;
+constexpr int HUB_CAPI = 1024;   // staged work items per level (per buffer)
+constexpr int HUB_CAPP = 4096;   // staged predecessor records per level (per buffer)
+constexpr size_t HUB_BUF = (size_t)HUB_CAPP * (8 + 4) + (size_t)HUB_CAPI * (8 * 3 + 4 * 2);
+size_t hub_smem_bytes() { return 2 * HUB_BUF; }
 
 // Apply the row-program steps [s0, s1) to the accumulator w (lane-offset pointer,
 // stride 32), software-pipelined: the next step's scalars, its U(j,j) and y_j are
@@ -55,23 +54,23 @@ __device__ __forceinline__ double run_steps(const DevProg &R, int64_t s0, int64_
     const double l = w[p * 32] / d;
     w[p * 32] = l;
     yacc -= l * yj;
-    int q = 0;
-    for (; q + 8 <= cnt; q += 8) {
+    // predicated 8-wide groups: every index and source load of the group is issued
+    // before its first shared-memory store (no scalar tail loop whose loads would
+    // each wait behind the previous store)
+    for (int q = 0; q < cnt; q += 8) {
       int t[8];
       double u[8], a[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        t[k] = rl[q + k];
-        u[k] = us[(q + k) * 32];
+        const bool ok = q + k < cnt;
+        t[k] = ok ? __ldg(rl + q + k) : 0;
+        u[k] = ok ? us[(q + k) * 32] : 0.0;
       }
 #pragma unroll
       for (int k = 0; k < 8; ++k) a[k] = w[t[k] * 32];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) w[t[k] * 32] = a[k] - l * u[k];
-    }
-    for (; q < cnt; ++q) {
-      const int tq = rl[q];
-      w[tq * 32] -= l * us[q * 32];
+      for (int k = 0; k < 8; ++k)
+        if (q + k < cnt) w[t[k] * 32] = a[k] - l * u[k];
     }
     p = pn; src = sn; cnt = cn; ro = rn; d = dn; yj = yn;
   }
@@ -85,6 +84,15 @@ __device__ __forceinline__ int ld_acquire(const int *p) {
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ int ld_relaxed(const int *p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(int *p, int v) {
+  asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ void st_release(int *p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -95,6 +103,13 @@ __device__ __forceinline__ void cp_async8(double *smem_dst, const double *gsrc) 
   const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gsrc) : "memory");
 }
+__device__ __forceinline__ void cp_async4(int32_t *smem_dst, const int32_t *gsrc) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
 }
@@ -317,6 +332,191 @@ __global__ void __launch_bounds__(PIPE_WARPS * 32, 6)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Pair mode: one warp runs the same node for two adjacent groups (g, g+1), lane =
+// instance g*32+lane and (g+1)*32+lane.  Every metadata load (task record, row
+// record, step program, rel lists) and every dependency poll now serves 64
+// instances, and each step has two independent FMA/load chains in flight.  The
+// value layout is unchanged (the allocation is padded to an even group count, so
+// the pair of the last odd group computes on padding: not live, no atomics).
+template <typename WPtr>
+__device__ __forceinline__ void run_steps2(const DevProg &R, int64_t s0, int64_t s1, WPtr wa,
+                                           WPtr wc, const double *ga, const double *gc,
+                                           const double *ya, const double *yc, double &acA,
+                                           double &acC) {
+  if (s0 >= s1) return;
+  int p = __ldg(R.st_p + s0);
+  int64_t src = __ldg(R.st_src + s0);
+  int cnt = __ldg(R.st_cnt + s0);
+  int64_t ro = __ldg(R.st_rel + s0);
+  int64_t j = __ldg(R.st_j + s0);
+  double da = __ldcg(ga + src * 32), dc = __ldcg(gc + src * 32);
+  double yja = __ldcg(ya + j * 32), yjc = __ldcg(yc + j * 32);
+  for (int64_t st = s0; st < s1; ++st) {
+    int pn = 0, cn = 0;
+    int64_t sn = 0, rn = 0;
+    double dna = 1.0, dnc = 1.0, yna = 0.0, ync = 0.0;
+    if (st + 1 < s1) {
+      pn = __ldg(R.st_p + st + 1);
+      sn = __ldg(R.st_src + st + 1);
+      cn = __ldg(R.st_cnt + st + 1);
+      rn = __ldg(R.st_rel + st + 1);
+      const int64_t jn = __ldg(R.st_j + st + 1);
+      dna = __ldcg(ga + sn * 32);
+      dnc = __ldcg(gc + sn * 32);
+      yna = __ldcg(ya + jn * 32);
+      ync = __ldcg(yc + jn * 32);
+    }
+    const int32_t *rl = R.rel + ro;
+    const double *ua = ga + (src + 1) * 32;
+    const double *uc = gc + (src + 1) * 32;
+    const double la = wa[p * 32] / da;
+    const double lc = wc[p * 32] / dc;
+    wa[p * 32] = la;
+    wc[p * 32] = lc;
+    acA -= la * yja;
+    acC -= lc * yjc;
+    for (int q = 0; q < cnt; q += 4) {
+      int t[4];
+      double xa[4], xc[4], va[4], vc[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const bool ok = q + k < cnt;
+        t[k] = ok ? __ldg(rl + q + k) : 0;
+        xa[k] = ok ? __ldcg(ua + (q + k) * 32) : 0.0;
+        xc[k] = ok ? __ldcg(uc + (q + k) * 32) : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        va[k] = wa[t[k] * 32];
+        vc[k] = wc[t[k] * 32];
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (q + k < cnt) {
+          wa[t[k] * 32] = va[k] - la * xa[k];
+          wc[t[k] * 32] = vc[k] - lc * xc[k];
+        }
+    }
+    p = pn; src = sn; cnt = cn; ro = rn; da = dna; dc = dnc; yja = yna; yjc = ync;
+  }
+}
+
+__device__ __forceinline__ void bt_node2(const DevSym &S, const BatchP &P, const DevProg &R,
+                                         const longlong4 nr, int g, const double *rhs, double *Y,
+                                         double *wsm0, int ws, int lane, int xmask) {
+  const int64_t ba = (int64_t)g * 32 + lane, bc = ba + 32;
+  const bool liveA = ba < P.B, liveC = bc < P.B;
+  const int64_t rem = P.B - (int64_t)g * 32;
+  const int nlive = (int)(rem < 64 ? rem : 64);   // live instances of the pair
+  const double thr = P.eps * P.anorm[0];
+  const int64_t vbase = nr.x;
+  const int r = (int)(nr.z & 0xffffffff);
+  const int s = (int)(nr.z >> 32);
+  const int W = (int)(nr.w & 0xffffffff);
+  const int L = (int)(nr.w >> 32);
+  double *ga0 = P.BF + (int64_t)g * P.stored * 32;
+  double *gc0 = ga0 + P.stored * 32;
+  double *ya = Y + (int64_t)g * S.n * 32 + lane;
+  double *yc = ya + (int64_t)S.n * 32;
+  const double *Ab = P.A + (int64_t)g * 32 * S.nnz;
+  longlong4 rr = R.row_rec[r];
+  for (int t = 0; t < s; ++t) {
+    const int i = r + t;
+    const int64_t s0 = rr.x, e0 = rr.y;
+    const int64_t s1 = s0 + (rr.z & 0xffffffff);
+    const int k = (int)(rr.z >> 32);
+    const int64_t a = rr.w;
+    if (t + 1 < s) rr = R.row_rec[i + 1];
+    const bool inSm = (s1 > s0) && W <= ws;
+    double *growA = ga0 + (vbase + (int64_t)t * W) * 32;
+    double *growC = gc0 + (vbase + (int64_t)t * W) * 32;
+    double *wA = inSm ? wsm0 : growA;
+    double *wC = inSm ? wsm0 + ws * 32 : growC;
+    double yaccA = (liveA && rhs) ? S.dr[a] * rhs[ba * S.n + a] : 0.0;
+    double yaccC = (liveC && rhs) ? S.dr[a] * rhs[bc * S.n + a] : 0.0;
+    for (int q = 0; q < W; ++q) {
+      wA[q * 32 + lane] = 0.0;
+      wC[q * 32 + lane] = 0.0;
+    }
+    __syncwarp();
+    // scatter in batches of 4 entries per lane: all loads of a batch are issued
+    // before its shared-memory stores
+    if (!(xmask & 4))
+      for (int base = 0; base < nlive * k; base += 128) {
+        int cp[4], in[4];
+        double av[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          const int idx = base + m * 32 + lane;
+          const bool ok = idx < nlive * k;
+          const int inst = ok ? idx / k : 0, e = ok ? idx - inst * k : 0;
+          in[m] = ok ? inst : -1;
+          cp[m] = ok ? __ldg(S.colpos + e0 + e) : 0;
+          av[m] = ok ? __ldg(Ab + (int64_t)inst * S.nnz + e0 + e) * __ldg(S.scale + e0 + e) : 0.0;
+        }
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+          if (in[m] >= 0) (in[m] < 32 ? wA : wC)[cp[m] * 32 + (in[m] & 31)] = av[m];
+      }
+    __syncwarp();
+    if (!(xmask & 2)) {
+      if (inSm)
+        run_steps2(R, s0, s1, wA + lane, wC + lane, ga0 + lane, gc0 + lane, ya, yc, yaccA, yaccC);
+      else
+        run_steps2(R, s0, s1, growA + lane, growC + lane, ga0 + lane, gc0 + lane, ya, yc, yaccA, yaccC);
+    }
+    const int Lt = L + t;
+    bool fa, fc;
+    wA[Lt * 32 + lane] = perturb(wA[Lt * 32 + lane], thr, fa);
+    wC[Lt * 32 + lane] = perturb(wC[Lt * 32 + lane], thr, fc);
+    if (fa && liveA) atomicAdd(&P.npert[ba], 1);
+    if (fc && liveC) atomicAdd(&P.npert[bc], 1);
+    ya[(int64_t)i * 32] = yaccA;
+    yc[(int64_t)i * 32] = yaccC;
+    if (inSm && !(xmask & 8))
+      for (int q = 0; q < W; ++q) {
+        growA[q * 32 + lane] = wA[q * 32 + lane];
+        growC[q * 32 + lane] = wC[q * 32 + lane];
+      }
+    __syncwarp();
+  }
+}
+
+// Pair-mode pipeline: task records carry the even group g of the pair; the warp
+// waits for both groups' dependency flags and publishes both.
+__global__ void __launch_bounds__(PIPE_WARPS * 32, 4)
+    k_bt_pipe2(DevSym S, BatchP P, DevProg R, const TaskDesc *tasks, int64_t total, const double *rhs,
+               double *Y, int *counter, int *flags, int epoch, int G, int ws, int nowait) {
+  extern __shared__ __align__(16) double pipe_smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double *wsm_w = pipe_smem + (size_t)warp * 2 * ws * 32;
+  for (;;) {
+    long long t = 0;
+    if (lane == 0) t = (long long)atomicAdd(reinterpret_cast<unsigned long long *>(counter), 1ull);
+    t = __shfl_sync(HY_FULL, t, 0);
+    if (t >= total) return;
+    const TaskDesc cur = tasks[t];
+    const int two = cur.g + 1 < G ? 2 : 1;
+    const int64_t nd = cur.d1 - cur.d0;
+    // relaxed polls (an acquire load would invalidate the SM's L1 on every poll);
+    // every value a task reads from another task is loaded L2-coherent (ld.cg)
+    // after the polls, and producers fence before publishing
+    for (int64_t k = lane; k < nd * two && !(nowait & 1); k += 32) {
+      const int64_t kk = k < nd ? k : k - nd;
+      const int *f = flags + (int64_t)__ldg(S.deps + cur.d0 + kk) * G + cur.g + (k < nd ? 0 : 1);
+      while (ld_relaxed(f) != epoch) __nanosleep(64);
+    }
+    __syncwarp();
+    const longlong4 nr = make_longlong4(cur.valoff, cur.d0, (int64_t)cur.r | ((int64_t)cur.s << 32),
+                                        (int64_t)cur.W | ((int64_t)cur.L << 32));
+    bt_node2(S, P, R, nr, cur.g, rhs, Y, wsm_w, ws, lane, nowait);
+    fence_acq_rel_gpu();
+    __syncwarp();
+    if (lane < two) st_relaxed(flags + (int64_t)cur.u * G + cur.g + lane, epoch);
+  }
+}
+
 template __global__ void k_bt_pipe<false>(DevSym, BatchP, DevProg, const TaskDesc *, int64_t,
                                           const double *, double *, int *, int *, int, int, int);
 template __global__ void k_bt_pipe<true>(DevSym, BatchP, DevProg, const TaskDesc *, int64_t,
@@ -349,16 +549,10 @@ __global__ void __launch_bounds__(HUB_THREADS) k_bt_hub(DevSym S, BatchP P, DevP
                                                         int epoch) {
   __shared__ double red[HUB_THREADS / 32][32];
   constexpr int LVCAP = 512;
-  __shared__ int64_t s_wi[LVCAP + 1], s_sp[LVCAP + 1];
-  // per-level staging of work-item metadata and predecessor lists (dynamic smem)
+  __shared__ int64_t s_wi[LVCAP + 1], s_sp[LVCAP + 1], s_y[LVCAP + 1];
+  // per-level staging of work-item metadata and predecessor lists, double-buffered:
+  // level l+1's records are copied (cp.async) while level l is processed
   extern __shared__ __align__(16) unsigned char hub_dyn[];
-  int64_t *st_pu = reinterpret_cast<int64_t *>(hub_dyn);                 // [HUB_CAPP]
-  int64_t *st_kd = st_pu + HUB_CAPP;                                       // [HUB_CAPI]
-  int32_t *st_pp = reinterpret_cast<int32_t *>(st_kd + HUB_CAPI);         // [HUB_CAPP]
-  int32_t *st_p = st_pp + HUB_CAPP;                                        // [HUB_CAPI]
-  int32_t *st_sl = st_p + HUB_CAPI;
-  int32_t *st_y0 = st_sl + HUB_CAPI;
-  int32_t *st_y1 = st_y0 + HUB_CAPI;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = HUB_THREADS / 32;
   const int task = blockIdx.x;
   const int u = nodes[task / G];
@@ -393,67 +587,126 @@ __global__ void __launch_bounds__(HUB_THREADS) k_bt_hub(DevSym S, BatchP P, DevP
     __syncthreads();
     const int hr = hr0 + t;
     const int64_t lv0 = R.hrow_lev[hr], lv1 = R.hrow_lev[hr + 1];
-    // stage this row's level bounds in shared memory (one load instead of one per level)
-    const bool lsm = lv1 - lv0 <= LVCAP;
-    if (lsm)
-      for (int64_t q = threadIdx.x; q <= lv1 - lv0; q += HUB_THREADS) {
+    // stage this row's level bounds and per-level predecessor offsets (the
+    // predecessor records of consecutive levels are contiguous)
+    const int nlv = (int)(lv1 - lv0);
+    const bool lsm = nlv <= LVCAP;
+    if (lsm) {
+      for (int q = threadIdx.x; q <= nlv; q += HUB_THREADS) {
         s_wi[q] = R.lev_wi[lv0 + q];
         s_sp[q] = R.lev_sp[lv0 + q];
       }
+      __syncthreads();
+      const int64_t wlast = s_wi[nlv];
+      for (int q = threadIdx.x; q <= nlv; q += HUB_THREADS)
+        s_y[q] = s_wi[q] < wlast ? R.wi_y0[s_wi[q]] : (wlast > s_wi[0] ? R.wi_y1[wlast - 1] : 0);
+    }
     __syncthreads();
+    auto buf = [&](int k, int64_t *&pu, int64_t *&kd, int64_t *&y0, int64_t *&y1, int32_t *&pp,
+                   int32_t *&pq, int32_t *&sl) {
+      unsigned char *bb = hub_dyn + (size_t)k * HUB_BUF;
+      pu = reinterpret_cast<int64_t *>(bb);
+      kd = pu + HUB_CAPP;
+      y0 = kd + HUB_CAPI;
+      y1 = y0 + HUB_CAPI;
+      pp = reinterpret_cast<int32_t *>(y1 + HUB_CAPI);
+      pq = pp + HUB_CAPP;
+      sl = pq + HUB_CAPI;
+    };
+    auto stageable = [&](int q) {
+      return lsm && s_wi[q + 1] - s_wi[q] <= HUB_CAPI && s_y[q + 1] - s_y[q] <= HUB_CAPP;
+    };
+    auto issue = [&](int q) {   // cp.async level lv0+q's records into buffer q&1
+      int64_t *pu, *kd, *y0, *y1;
+      int32_t *pp, *pq, *sl;
+      buf(q & 1, pu, kd, y0, y1, pp, pq, sl);
+      const int64_t wi0 = s_wi[q], ni = s_wi[q + 1] - wi0;
+      const int64_t yb0 = s_y[q], np_ = s_y[q + 1] - yb0;
+      for (int64_t k2 = threadIdx.x; k2 < ni; k2 += HUB_THREADS) {
+        cp_async4(pq + k2, R.wi_p + wi0 + k2);
+        cp_async4(sl + k2, R.wi_slot + wi0 + k2);
+        cp_async8(reinterpret_cast<double *>(y0 + k2), reinterpret_cast<const double *>(R.wi_y0 + wi0 + k2));
+        cp_async8(reinterpret_cast<double *>(y1 + k2), reinterpret_cast<const double *>(R.wi_y1 + wi0 + k2));
+        cp_async8(reinterpret_cast<double *>(kd + k2), reinterpret_cast<const double *>(R.wi_kd + wi0 + k2));
+      }
+      for (int64_t k2 = threadIdx.x; k2 < np_; k2 += HUB_THREADS) {
+        cp_async4(pp + k2, R.pred_p + yb0 + k2);
+        cp_async8(reinterpret_cast<double *>(pu + k2), reinterpret_cast<const double *>(R.pred_u + yb0 + k2));
+      }
+    };
+    if (nlv > 0 && stageable(0)) issue(0);
+    cp_async_commit();
     for (int64_t lev = lv0; lev < lv1; ++lev) {
-      const int64_t wi0 = lsm ? s_wi[lev - lv0] : R.lev_wi[lev];
-      const int64_t wi1 = lsm ? s_wi[lev - lv0 + 1] : R.lev_wi[lev + 1];
-      const int64_t sp0 = lsm ? s_sp[lev - lv0] : R.lev_sp[lev];
-      const int64_t sp1 = lsm ? s_sp[lev - lv0 + 1] : R.lev_sp[lev + 1];
+      const int q = (int)(lev - lv0);
+      if (lev + 1 < lv1 && stageable(q + 1)) issue(q + 1);
+      cp_async_commit();
+      cp_async_wait1();
+      __syncthreads();
+      const int64_t wi0 = lsm ? s_wi[q] : R.lev_wi[lev];
+      const int64_t wi1 = lsm ? s_wi[q + 1] : R.lev_wi[lev + 1];
+      const int64_t sp0 = lsm ? s_sp[q] : R.lev_sp[lev];
+      const int64_t sp1 = lsm ? s_sp[q + 1] : R.lev_sp[lev + 1];
       const int64_t ni = wi1 - wi0;
-      const int64_t yb0 = ni ? R.wi_y0[wi0] : 0;
-      const int64_t np_ = ni ? R.wi_y1[wi1 - 1] - yb0 : 0;
-      const bool staged = ni <= HUB_CAPI && np_ <= HUB_CAPP;
-      if (staged) {
-        for (int64_t q = threadIdx.x; q < ni; q += HUB_THREADS) {
-          st_p[q] = R.wi_p[wi0 + q];
-          st_sl[q] = R.wi_slot[wi0 + q];
-          st_y0[q] = (int32_t)(R.wi_y0[wi0 + q] - yb0);
-          st_y1[q] = (int32_t)(R.wi_y1[wi0 + q] - yb0);
-          st_kd[q] = R.wi_kd[wi0 + q];
-        }
-        for (int64_t q = threadIdx.x; q < np_; q += HUB_THREADS) {
-          st_pp[q] = R.pred_p[yb0 + q];
-          st_pu[q] = R.pred_u[yb0 + q];
-        }
-        __syncthreads();
-        for (int64_t q = warp; q < ni; q += nw) {
-          const int p = st_p[q];
-          const int slot = st_sl[q];
-          const int y1 = st_y1[q];
-          int y = st_y0[q];
-          const int64_t kd = st_kd[q];
-          const double dv = kd >= 0 ? gb[kd * 32] : 1.0;
-          double acc = slot < 0 ? w[p * 32] : 0.0;
-          for (; y + 8 <= y1; y += 8) {
-            double lv[8], uv[8];
+      if (stageable(q)) {
+        int64_t *st_pu, *st_kd, *st_y0, *st_y1;
+        int32_t *st_pp, *st_p, *st_sl;
+        buf(q & 1, st_pu, st_kd, st_y0, st_y1, st_pp, st_p, st_sl);
+        const int64_t yb0 = s_y[q];
+        // four items per warp at a time, four predecessors per item per round: up
+        // to 32 independent gathers in flight per warp
+        for (int64_t q0 = warp; q0 < ni; q0 += 4 * nw) {
+          int p[4], y[4], y1[4], slot[4];
+          int64_t kd[4];
+          double acc[4], dv[4];
 #pragma unroll
-            for (int k2 = 0; k2 < 8; ++k2) {
-              lv[k2] = w[st_pp[y + k2] * 32];
-              uv[k2] = gb[st_pu[y + k2] * 32];
-            }
-#pragma unroll
-            for (int k2 = 0; k2 < 8; ++k2) acc -= lv[k2] * uv[k2];
+          for (int jq = 0; jq < 4; ++jq) {
+            const int64_t qq = q0 + (int64_t)jq * nw;
+            const bool ok = qq < ni;
+            p[jq] = ok ? st_p[qq] : 0;
+            slot[jq] = ok ? st_sl[qq] : 0;
+            y[jq] = ok ? (int)(st_y0[qq] - yb0) : 0;
+            y1[jq] = ok ? (int)(st_y1[qq] - yb0) : 0;
+            kd[jq] = ok ? st_kd[qq] : -1;
+            dv[jq] = kd[jq] >= 0 ? gb[kd[jq] * 32] : 1.0;
+            acc[jq] = (ok && slot[jq] < 0) ? w[p[jq] * 32] : 0.0;
           }
-          for (; y < y1; ++y) acc -= w[st_pp[y] * 32] * gb[st_pu[y] * 32];
-          if (slot < 0) {
-            if (kd >= 0) {
-              acc = acc / dv;
-            } else if (kd == -2) {
-              bool fired;
-              const double piv = acc;
-              acc = perturb(piv, thr, fired);
-              if (fired && live) atomicAdd(&P.npert[b], 1);
+          int rem = 0;
+#pragma unroll
+          for (int jq = 0; jq < 4; ++jq) rem = max(rem, y1[jq] - y[jq]);
+          for (int step = 0; step < rem; step += 4) {
+            double lv[4][4], uv[4][4];
+#pragma unroll
+            for (int jq = 0; jq < 4; ++jq)
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const int yy = y[jq] + step + e;
+                const bool act = yy < y1[jq];
+                lv[jq][e] = act ? w[st_pp[yy] * 32] : 0.0;
+                uv[jq][e] = act ? gb[st_pu[yy] * 32] : 0.0;
+              }
+#pragma unroll
+            for (int jq = 0; jq < 4; ++jq)
+#pragma unroll
+              for (int e = 0; e < 4; ++e) acc[jq] -= lv[jq][e] * uv[jq][e];
+          }
+#pragma unroll
+          for (int jq = 0; jq < 4; ++jq) {
+            const int64_t qq = q0 + (int64_t)jq * nw;
+            if (qq >= ni) continue;
+            double a = acc[jq];
+            if (slot[jq] < 0) {
+              if (kd[jq] >= 0) {
+                a = a / dv[jq];
+              } else if (kd[jq] == -2) {
+                bool fired;
+                const double piv = a;
+                a = perturb(piv, thr, fired);
+                if (fired && live) atomicAdd(&P.npert[b], 1);
+              }
+              w[p[jq] * 32] = a;
+            } else {
+              scr[(size_t)slot[jq] * 32] = a;
             }
-            w[p * 32] = acc;
-          } else {
-            scr[(size_t)slot * 32] = acc;
           }
         }
       } else
@@ -498,6 +751,7 @@ __global__ void __launch_bounds__(HUB_THREADS) k_bt_hub(DevSym S, BatchP P, DevP
       }
       __syncthreads();
     }
+    cp_async_wait_all0();
     // forward substitution for row i: y_i = b̂_i − Σ_s l_s y_{j_s}
     double part = 0.0;
     for (int64_t st = R.row_ptr[i] + warp; st < R.row_ptr[i + 1]; st += nw)
@@ -610,8 +864,23 @@ __global__ void __launch_bounds__(BW * 32) k_batch_bwd(DevSym S, const double *B
     const double *row = gbase + (S.valoff[u] + (int64_t)t * W) * 32;
     const int d = L + t;
     double acc = y[(int64_t)(r + t) * 32];
-    for (int p = d + 1; p < W; ++p) acc -= row[(int64_t)p * 32] * y[(int64_t)cc[p] * 32];
-    y[(int64_t)(r + t) * 32] = acc / row[(int64_t)d * 32];
+    const double dg = row[(int64_t)d * 32];
+    // predicated 8-wide batches: all column indices, then all factor values and
+    // solution gathers of a batch are in flight together
+    for (int p0 = d + 1; p0 < W; p0 += 8) {
+      int k[8];
+      double a[8], z[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) k[e] = p0 + e < W ? __ldg(cc + p0 + e) : -1;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        a[e] = k[e] >= 0 ? row[(int64_t)(p0 + e) * 32] : 0.0;
+        z[e] = k[e] >= 0 ? y[(int64_t)k[e] * 32] : 0.0;
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc -= a[e] * z[e];
+    }
+    y[(int64_t)(r + t) * 32] = acc / dg;
   }
 }
 

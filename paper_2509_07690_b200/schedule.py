@@ -23,6 +23,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import os
+
 import numpy as np
 from numba import njit
 
@@ -327,7 +329,7 @@ class RowPrograms:
                    if isinstance(getattr(self, k), np.ndarray))
 
 
-HUB_CHUNK = 64
+HUB_CHUNK = int(os.environ.get("HYLU_HUB_CHUNK", "64"))
 
 
 def build_programs(an, inner_perm, hub_steps=HUB_STEPS, chunk=HUB_CHUNK, standalone_only=False):
