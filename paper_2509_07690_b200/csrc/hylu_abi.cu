@@ -87,7 +87,7 @@ template <bool STAGED>
 __global__ void k_bt_pipe(DevSym, BatchP, DevProg, const TaskDesc *, int64_t, const double *, double *, int *,
                           int *, int, int, int);
 __global__ void k_bt_pipe2(DevSym, BatchP, DevProg, const TaskDesc *, int64_t, const double *, double *, int *,
-                           int *, int, int, int, int);
+                           int *, int, int, int, int, int);
 __global__ void k_bt_lev0(DevSym, BatchP, DevProg, const int32_t *, int, int, const double *, double *, int *, int);
 __global__ void k_bt_hub(DevSym, BatchP, DevProg, const int32_t *, int, int, const double *, double *,
                          double *, int, int *, int);
@@ -185,6 +185,7 @@ struct hy_handle {
   int staged = 0;                          // stage row sources with cp.async (option "staged")
   int nowait = 0;                          // timing experiment only: skip dependency waits
   int pair = 1;                            // pipeline: one warp per (node, group pair)
+  int prefetch = 512;                      // pair mode: L2-prefetch the matrix values this many tasks ahead
   int pipe_ws = 16;                        // pair-mode shared workspace columns per group
   int skew = 1;                            // diagonal claim order: group g+1 runs `skew` levels behind g
   // diagonal claim order per (segment, G): pair prefix sums, (level<<16|group), level offsets
@@ -495,6 +496,10 @@ int hy_set_option(hy_handle *h, const char *name, int64_t value) {
     h->pair = value != 0;
     h->segs_G = -1;
     h->pipe_blocks = 0;
+    return HY_OK;
+  }
+  if (std::string(name) == "prefetch" && value >= 0) {
+    h->prefetch = (int)value;
     return HY_OK;
   }
   if (std::string(name) == "pipe_ws" && value >= 1 && value <= 64) {
@@ -1165,7 +1170,7 @@ int hy_refactorize_batched(hy_handle *h, int64_t B, const double *d_vals, double
       if (h->pair)
         k_bt_pipe2<<<h->pipe_blocks, 128, (size_t)4 * 2 * h->pipe_ws * 32 * 8, st>>>(
             h->S, P, h->prog, sg.d_tasks, sg.ntasks, d_b_fuse, h->d_by, ctr, h->d_flags, h->epoch, G,
-            h->pipe_ws, h->nowait);
+            h->pipe_ws, h->nowait, h->prefetch);
       else if (h->staged)
         k_bt_pipe<true><<<h->pipe_blocks, 128, pipe_smem_bytes(true), st>>>(
             h->S, P, h->prog, sg.d_tasks, sg.ntasks, d_b_fuse, h->d_by, ctr, h->d_flags, h->epoch, G, h->nowait);

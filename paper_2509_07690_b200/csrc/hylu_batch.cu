@@ -487,7 +487,7 @@ __device__ __forceinline__ void bt_node2(const DevSym &S, const BatchP &P, const
 // waits for both groups' dependency flags and publishes both.
 __global__ void __launch_bounds__(PIPE_WARPS * 32, 4)
     k_bt_pipe2(DevSym S, BatchP P, DevProg R, const TaskDesc *tasks, int64_t total, const double *rhs,
-               double *Y, int *counter, int *flags, int epoch, int G, int ws, int nowait) {
+               double *Y, int *counter, int *flags, int epoch, int G, int ws, int nowait, int pf) {
   extern __shared__ __align__(16) double pipe_smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double *wsm_w = pipe_smem + (size_t)warp * 2 * ws * 32;
@@ -497,6 +497,15 @@ __global__ void __launch_bounds__(PIPE_WARPS * 32, 4)
     t = __shfl_sync(HY_FULL, t, 0);
     if (t >= total) return;
     const TaskDesc cur = tasks[t];
+    // L2 prefetch of the matrix values of the task `pf` positions ahead in claim
+    // order (streamed from HBM; independent of every dependency): its descriptor
+    // loads now, its row record after the polls, the prefetches after this task
+    const int64_t tp = t + pf;
+    int pg = -1, pr = 0;
+    if (pf > 0 && tp < total) {
+      pg = __ldg(&tasks[tp].g);
+      pr = __ldg(&tasks[tp].r);
+    }
     const int two = cur.g + 1 < G ? 2 : 1;
     const int64_t nd = cur.d1 - cur.d0;
     // relaxed polls (an acquire load would invalidate the SM's L1 on every poll);
@@ -508,9 +517,24 @@ __global__ void __launch_bounds__(PIPE_WARPS * 32, 4)
       while (ld_relaxed(f) != epoch) __nanosleep(64);
     }
     __syncwarp();
+    int64_t pe0 = 0, pk = 0;
+    if (pg >= 0) {
+      pe0 = __ldg(&R.row_rec[pr].y);
+      pk = __ldg(&R.row_rec[pr].z) >> 32;
+    }
     const longlong4 nr = make_longlong4(cur.valoff, cur.d0, (int64_t)cur.r | ((int64_t)cur.s << 32),
                                         (int64_t)cur.W | ((int64_t)cur.L << 32));
     bt_node2(S, P, R, nr, cur.g, rhs, Y, wsm_w, ws, lane, nowait);
+    if (pg >= 0 && pk > 0)
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+        const int64_t bi = (int64_t)pg * 32 + m * 32 + lane;
+        if (bi < P.B) {
+          const double *a0 = P.A + bi * S.nnz + pe0;
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(a0));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(a0 + pk - 1));
+        }
+      }
     fence_acq_rel_gpu();
     __syncwarp();
     if (lane < two) st_relaxed(flags + (int64_t)cur.u * G + cur.g + lane, epoch);
@@ -570,10 +594,10 @@ __global__ void __launch_bounds__(HUB_THREADS) k_bt_hub(DevSym S, BatchP P, DevP
   const double *Ab = P.A + (int64_t)g * 32 * S.nnz;
   double *scr = scratch + (size_t)blockIdx.x * max_slots * 32 + lane;
   const int hr0 = R.hub_base[u];
+  // initialise every row of the node first: a (joint) node program may span rows
   for (int t = 0; t < s; ++t) {
     const int i = r + t;
     double *w0 = gb0 + (S.valoff[u] + (int64_t)t * W) * 32;
-    double *w = w0 + lane;
     for (int q = threadIdx.x; q < W * 32; q += HUB_THREADS) w0[q] = 0.0;
     __syncthreads();
     const int srow = S.kind[u] ? r + P.iperm[i] : r;
@@ -584,7 +608,15 @@ __global__ void __launch_bounds__(HUB_THREADS) k_bt_hub(DevSym S, BatchP P, DevP
       const int inst = idx / k, e = idx - inst * k;
       w0[S.colpos[e0 + e] * 32 + inst] = Ab[(int64_t)inst * S.nnz + e0 + e] * S.scale[e0 + e];
     }
-    __syncthreads();
+  }
+  __syncthreads();
+  for (int t = 0; t < s; ++t) {
+    const int i = r + t;
+    // positions are node-relative (t*W + p): every row's levels address the node base
+    double *w = gb0 + S.valoff[u] * 32 + lane;
+    double *w0 = gb0 + (S.valoff[u] + (int64_t)t * W) * 32;
+    const int srow = S.kind[u] ? r + P.iperm[i] : r;
+    const int64_t a = S.mrow_src[srow];
     const int hr = hr0 + t;
     const int64_t lv0 = R.hrow_lev[hr], lv1 = R.hrow_lev[hr + 1];
     // stage this row's level bounds and per-level predecessor offsets (the
@@ -755,7 +787,7 @@ __global__ void __launch_bounds__(HUB_THREADS) k_bt_hub(DevSym S, BatchP P, DevP
     // forward substitution for row i: y_i = b̂_i − Σ_s l_s y_{j_s}
     double part = 0.0;
     for (int64_t st = R.row_ptr[i] + warp; st < R.row_ptr[i + 1]; st += nw)
-      part += w[R.st_p[st] * 32] * yb[(int64_t)R.st_j[st] * 32];
+      part += w0[R.st_p[st] * 32 + lane] * yb[(int64_t)R.st_j[st] * 32];
     red[warp][lane] = part;
     __syncthreads();
     if (warp == 0) {

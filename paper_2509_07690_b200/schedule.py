@@ -286,6 +286,72 @@ def _chunks(hrow_lev, lev_ptr, hpp, ch):
     return lev_wi, wi_x, wi_y0, wi_y1, wi_slot, lev_sp, sp_x, sp_s0, sp_n, max_slots
 
 
+JOINT_HUB_ROWS = os.environ.get("HYLU_JOINT_HUB", "1") != "0"
+
+
+def _joint_hub_rows(hub_nodes, first, colptr, valoff, hrow_lev, lev_ptr, hpos, hdiv, hpp, pred_p,
+                    pred_u, merge=True):
+    """Merge the per-row pull programs of each hub supernode into one program.
+
+    Row t's levels below its first *cross level* (the first level with a
+    contribution or divisor taken from an earlier row of the same node) depend on
+    no other row of the node, so level q of all such rows runs as one joint level;
+    the remaining levels of each row follow row by row.  Positions (and multiplier
+    positions) become node-relative, t*W + p, so one level can span rows.  The whole
+    node program is attached to the node's first hub row (the other rows get empty
+    level ranges); every row is initialised before the node's first level runs.
+    Contribution order per position is unchanged, so the arithmetic is identical.
+    merge=False keeps the row-by-row level order (same node-relative form)."""
+    n_lev = [0]
+    pos, div, pp, pu, hppn = [], [], [], [], [0]
+    new_hrow = [0]
+    hr = 0
+    for u in hub_nodes:
+        r, s = int(first[u]), int(first[u + 1] - first[u])
+        W = int(colptr[u + 1] - colptr[u])
+        lo, hi = int(valoff[u]), int(valoff[u + 1])
+        levs = [list(range(int(hrow_lev[hr + t]), int(hrow_lev[hr + t + 1]))) for t in range(s)]
+        cut = []
+        for t in range(s):
+            c = len(levs[t])
+            if t > 0:
+                for q, l in enumerate(levs[t]):
+                    x0, x1 = int(lev_ptr[l]), int(lev_ptr[l + 1])
+                    d = hdiv[x0:x1]
+                    u_ = pred_u[hpp[x0]:hpp[x1]]
+                    if ((d >= lo) & (d < hi)).any() or ((u_ >= lo) & (u_ < hi)).any():
+                        c = q
+                        break
+            cut.append(c if merge else (len(levs[t]) if t == 0 else 0))
+        virt = []
+        for q in range(max(cut) if cut else 0):
+            seg = [(t, levs[t][q]) for t in range(s) if q < cut[t]]
+            if seg:
+                virt.append(seg)
+        for t in range(s):
+            for q in range(cut[t], len(levs[t])):
+                virt.append([(t, levs[t][q])])
+        for seg in virt:
+            cnt = 0
+            for t, l in seg:
+                x0, x1 = int(lev_ptr[l]), int(lev_ptr[l + 1])
+                pos.append(hpos[x0:x1].astype(np.int64) + t * W)
+                div.append(hdiv[x0:x1])
+                y0, y1 = int(hpp[x0]), int(hpp[x1])
+                pp.append(pred_p[y0:y1].astype(np.int64) + t * W)
+                pu.append(pred_u[y0:y1])
+                hppn.append(np.diff(hpp[x0:x1 + 1]))
+                cnt += x1 - x0
+            n_lev.append(n_lev[-1] + cnt)
+        new_hrow.append(new_hrow[-1] + len(virt))
+        new_hrow.extend([new_hrow[-1]] * (s - 1))
+        hr += s
+    cat = lambda xs, dt: np.concatenate(xs).astype(dt) if xs else np.zeros(0, dt)
+    hpp_new = np.concatenate([[0], np.cumsum(cat(hppn[1:], np.int64))]).astype(np.int64)
+    return (np.asarray(new_hrow, np.int64), np.asarray(n_lev, np.int64), cat(pos, np.int32),
+            cat(div, np.int64), hpp_new, cat(pp, np.int32), cat(pu, np.int64))
+
+
 @dataclass
 class RowPrograms:
     row_ptr: np.ndarray     # int64[n+1] steps of factor row i
@@ -344,6 +410,9 @@ def build_programs(an, inner_perm, hub_steps=HUB_STEPS, chunk=HUB_CHUNK, standal
         hrow_lev, lev_ptr, hpos, hdiv, hpp, pred_p, pred_u = _pull(
             s.n, s.node_first, s.colptr, s.nl, s.valoff, an.A.row_ptr, vm.mrow_src, vm.colpos,
             s.node_kind, ip, hub_nodes.astype(np.int64), row_ptr, st_p, st_src, st_cnt, st_rel, rel)
+        hrow_lev, lev_ptr, hpos, hdiv, hpp, pred_p, pred_u = _joint_hub_rows(
+            hub_nodes, s.node_first, s.colptr, s.valoff, hrow_lev, lev_ptr, hpos, hdiv, hpp,
+            pred_p, pred_u, JOINT_HUB_ROWS)
     else:
         hrow_lev = np.zeros(1, np.int64)
         lev_ptr = np.zeros(1, np.int64)

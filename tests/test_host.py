@@ -228,3 +228,71 @@ def test_fanin_plan_reproduces_oracle(name, mode):
     # the interpreter applies permutations to whole rows, like the device
     assert np.array_equal(ip, ref.inner_perm)
     assert np.abs(F - ref.values).max() <= 1e-11 * max(1.0, np.abs(ref.values).max())
+
+
+def test_joint_hub_programs_reproduce_oracle():
+    """Hub supernodes (several hub rows) through the joint pull programs: rows'
+    levels below their first cross-row level run together, the rest row by row."""
+    bp = gen.circuit_batch(2, 3000, 3, 400)
+    A = bp.A0
+    an = an_mod.analyze(A, SolverConfig(ordering="amd"))
+    f = on.factorize(an)
+    ref = on.factorize(an, prior=f)
+    prog = schedule.build_programs(an, f.inner_perm, hub_steps=40)
+    s = an.symbolic
+    multi = [u for u in prog.hub_nodes if s.node_first[u + 1] - s.node_first[u] > 1]
+    assert multi, "want a hub supernode with several rows"
+    # hub nodes read their sources' values: take every non-hub node from the oracle,
+    # run the hub programs, compare the hub ranges
+    F_all = ref.values.copy()
+    for u in prog.hub_nodes:
+        F_all[int(s.valoff[u]):int(s.valoff[u + 1])] = 0.0
+    F2 = _run_pull_with(an, prog, A.values, F_all)
+    for u in prog.hub_nodes:
+        a, b = int(s.valoff[u]), int(s.valoff[u + 1])
+        assert np.abs(F2[a:b] - ref.values[a:b]).max() <= 1e-12 * np.abs(ref.values).max()
+    # the joint form merged the rows' levels: fewer levels than row by row
+    schedule.JOINT_HUB_ROWS = False
+    try:
+        per_row = schedule.build_programs(an, f.inner_perm, hub_steps=40)
+    finally:
+        schedule.JOINT_HUB_ROWS = True
+    assert len(prog.lev_ptr) < len(per_row.lev_ptr)
+    F3 = _run_pull_with(an, per_row, A.values, F_all)
+    for u in prog.hub_nodes:
+        a, b = int(s.valoff[u]), int(s.valoff[u + 1])
+        assert np.array_equal(F2[a:b], F3[a:b])   # same arithmetic, bit for bit
+
+
+def _run_pull_with(an, prog, values, F):
+    s = an.symbolic
+    vm = an.vmap
+    F = F.copy()
+    thr = 1e-8 * on.anorm_kernel(an.A.values, vm.scale)
+    hr = 0
+    for u in prog.hub_nodes:
+        r = int(s.node_first[u])
+        nr = int(s.node_first[u + 1]) - r
+        W = int(s.colptr[u + 1] - s.colptr[u])
+        base = int(s.valoff[u])
+        for t in range(nr):
+            rec = prog.row_rec[r + t]
+            e0, k = int(rec[1]), int(rec[2] >> 32)
+            F[base + t * W: base + (t + 1) * W] = 0.0
+            F[base + t * W + vm.colpos[e0:e0 + k]] = values[e0:e0 + k] * vm.scale[e0:e0 + k]
+        for t in range(nr):
+            h = hr + t
+            for lev in range(prog.hrow_lev[h], prog.hrow_lev[h + 1]):
+                for x in range(prog.lev_ptr[lev], prog.lev_ptr[lev + 1]):
+                    p = base + int(prog.hpos[x])
+                    acc = F[p]
+                    for y in range(prog.hpp[x], prog.hpp[x + 1]):
+                        acc -= F[base + int(prog.pred_p[y])] * F[prog.pred_u[y]]
+                    kd = int(prog.hdiv[x])
+                    if kd >= 0:
+                        acc /= F[kd]
+                    elif kd == -2 and abs(acc) < thr:
+                        acc = thr if acc >= 0 else -thr
+                    F[p] = acc
+        hr += nr
+    return F
