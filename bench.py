@@ -344,7 +344,7 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=4096)
     ap.add_argument("--ref-sample", type=int, default=512)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--e2e-chunks", type=int, default=4)
+    ap.add_argument("--e2e-chunks", type=int, default=8)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":

@@ -276,7 +276,7 @@ class BatchedRefactorizer:
         check(self.ctx.lib.hy_solve_batched(self.ctx.h, B, None, d_x.data_ptr(), sh))
         return d_x, d_npert
 
-    def run_host(self, h_vals, h_rhs, h_x, h_npert=None, chunks=4):
+    def run_host(self, h_vals, h_rhs, h_x, h_npert=None, chunks=8):
         """Host buffers in, host buffers out, copies overlapped with compute.
 
         The batch is cut into ``chunks`` contiguous slabs (multiples of 32

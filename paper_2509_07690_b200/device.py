@@ -14,7 +14,8 @@ import numpy as np
 
 from ._ref import errors
 
-_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libhylu_b200.so")
+_LIB_PATH = os.environ.get("HYLU_LIB_PATH") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "lib", "libhylu_b200.so")
 _lib = None
 
 HY_CODES = {
