@@ -90,7 +90,7 @@ __global__ void k_bt_pipe2(DevSym, BatchP, DevProg, const TaskDesc *, int64_t, c
                            int *, int, int, int, int, int);
 __global__ void k_bt_lev0(DevSym, BatchP, DevProg, const int32_t *, int, int, const double *, double *, int *, int);
 __global__ void k_bt_hub(DevSym, BatchP, DevProg, const int32_t *, int, int, const double *, double *,
-                         double *, int, int *, int);
+                         double *, int, int *, int, int);
 __global__ void k_batch_bhat(DevSym, const int32_t *, const double *, double *, int64_t);
 __global__ void k_batch_xout(DevSym, const double *, double *, int64_t);
 __global__ void k_batch_fwd(DevSym, const double *, int64_t, const int32_t *, int, int, double *);
@@ -186,6 +186,7 @@ struct hy_handle {
   int nowait = 0;                          // timing experiment only: skip dependency waits
   int pair = 1;                            // pipeline: one warp per (node, group pair)
   int prefetch = 512;                      // pair mode: L2-prefetch the matrix values this many tasks ahead
+  int hub_df = 0;                          // hub kernel: dataflow phase for split-free leading levels
   int pipe_ws = 16;                        // pair-mode shared workspace columns per group
   int skew = 1;                            // diagonal claim order: group g+1 runs `skew` levels behind g
   // diagonal claim order per (segment, G): pair prefix sums, (level<<16|group), level offsets
@@ -496,6 +497,10 @@ int hy_set_option(hy_handle *h, const char *name, int64_t value) {
     h->pair = value != 0;
     h->segs_G = -1;
     h->pipe_blocks = 0;
+    return HY_OK;
+  }
+  if (std::string(name) == "hub_dataflow") {
+    h->hub_df = value != 0;
     return HY_OK;
   }
   if (std::string(name) == "prefetch" && value >= 0) {
@@ -1154,7 +1159,7 @@ int hy_refactorize_batched(hy_handle *h, int64_t B, const double *d_vals, double
       }
       k_bt_hub<<<(unsigned)(nh * G), 512, hub_smem_bytes(), st>>>(h->S, P, h->prog, h->d_bl_hubs + h->bl_hptr[l], nh, G,
                                                    d_b_fuse, h->d_by, h->d_scratch, h->max_slots,
-                                                   h->d_flags, h->epoch);
+                                                   h->d_flags, h->epoch, h->hub_df);
       h->launches++;
     }
     if (sg.lev0) {

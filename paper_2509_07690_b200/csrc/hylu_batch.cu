@@ -570,10 +570,11 @@ __global__ void __launch_bounds__(HUB_THREADS) k_bt_hub(DevSym S, BatchP P, DevP
                                                         const int32_t *nodes, int count, int G,
                                                         const double *rhs, double *Y,
                                                         double *scratch, int max_slots, int *flags,
-                                                        int epoch) {
+                                                        int epoch, int df) {
   __shared__ double red[HUB_THREADS / 32][32];
   constexpr int LVCAP = 512;
   __shared__ int64_t s_wi[LVCAP + 1], s_sp[LVCAP + 1], s_y[LVCAP + 1];
+  __shared__ int s_bt[LVCAP + 1];
   // per-level staging of work-item metadata and predecessor lists, double-buffered:
   // level l+1's records are copied (cp.async) while level l is processed
   extern __shared__ __align__(16) unsigned char hub_dyn[];
@@ -666,9 +667,130 @@ __global__ void __launch_bounds__(HUB_THREADS) k_bt_hub(DevSym S, BatchP P, DevP
         cp_async8(reinterpret_cast<double *>(pu + k2), reinterpret_cast<const double *>(R.pred_u + yb0 + k2));
       }
     };
-    if (nlv > 0 && stageable(0)) issue(0);
+    // ---- dataflow phase: the leading levels without split positions run without
+    // level barriers.  Batches of <= 4 same-level items are dealt to warps in level
+    // order; an item waits (shared-memory ready bits, one per node-relative
+    // position) for the positions it reads — its multipliers, and U values or
+    // divisors inside this node — then finalises its position and sets its bit.
+    // Every wait points to a strictly lower level, and each warp runs its batches
+    // in order, so the lowest unfinished batch can always proceed.
+    int qdf = 0;
+    const int64_t nbits = (int64_t)s * W;
+    if (df && lsm && nbits <= (int64_t)2 * HUB_BUF * 8)
+      while (qdf < nlv && s_sp[qdf + 1] == s_sp[qdf]) ++qdf;
+    if (qdf > 0) {
+      unsigned *rdy = reinterpret_cast<unsigned *>(hub_dyn);
+      volatile unsigned *vrdy = rdy;
+      const int nwords = (int)((nbits + 31) >> 5);
+      // positions no dataflow item writes (structural zeros of the union layout,
+      // A-only entries) are ready from the start
+      for (int q2 = threadIdx.x; q2 < nwords; q2 += HUB_THREADS) rdy[q2] = ~0u;
+      __syncthreads();
+      for (int64_t it = s_wi[0] + threadIdx.x; it < s_wi[qdf]; it += HUB_THREADS) {
+        const int pz = __ldg(R.wi_p + it);
+        atomicAnd(rdy + (pz >> 5), ~(1u << (pz & 31)));
+      }
+      if (threadIdx.x == 0) {
+        int acc = 0;
+        for (int q2 = 0; q2 < qdf; ++q2) {
+          s_bt[q2] = acc;
+          acc += (int)((s_wi[q2 + 1] - s_wi[q2] + 3) >> 2);
+        }
+        s_bt[qdf] = acc;
+      }
+      __syncthreads();
+      const int nbt = s_bt[qdf];
+      const int64_t nb = S.valoff[u], nbe = nb + nbits;
+      auto wait_pos = [&](int64_t pos) {
+        while (!((vrdy[pos >> 5] >> (pos & 31)) & 1u)) __nanosleep(20);
+      };
+      for (int k = warp; k < nbt; k += nw) {
+        int lo = 0, hi = qdf;
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (s_bt[mid] <= k) lo = mid; else hi = mid;
+        }
+        const int64_t i0 = s_wi[lo] + 4LL * (k - s_bt[lo]);
+        const int64_t iend = s_wi[lo + 1];
+        const int ni = (int)(i0 + 4 < iend ? 4 : iend - i0);
+        int p[4];
+        int64_t y[4], y1[4], kd[4];
+        double acc[4];
+#pragma unroll
+        for (int jq = 0; jq < 4; ++jq) {
+          const bool ok = jq < ni;
+          p[jq] = ok ? __ldg(R.wi_p + i0 + jq) : 0;
+          y[jq] = ok ? __ldg(R.wi_y0 + i0 + jq) : 0;
+          y1[jq] = ok ? __ldg(R.wi_y1 + i0 + jq) : 0;
+          kd[jq] = ok ? __ldg(R.wi_kd + i0 + jq) : -1;
+          acc[jq] = ok ? w[p[jq] * 32] : 0.0;
+        }
+        int64_t rem = 0;
+#pragma unroll
+        for (int jq = 0; jq < 4; ++jq) rem = max(rem, y1[jq] - y[jq]);
+        for (int64_t step = 0; step < rem; step += 2) {
+          int pp[4][2];
+          int64_t pu[4][2];
+#pragma unroll
+          for (int jq = 0; jq < 4; ++jq)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int64_t yy = y[jq] + step + e;
+              const bool act = yy < y1[jq];
+              pp[jq][e] = act ? __ldg(R.pred_p + yy) : -1;
+              pu[jq][e] = act ? __ldg(R.pred_u + yy) : -1;
+            }
+#pragma unroll
+          for (int jq = 0; jq < 4; ++jq)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              if (pp[jq][e] >= 0) wait_pos(pp[jq][e]);
+              if (pu[jq][e] >= nb && pu[jq][e] < nbe) wait_pos(pu[jq][e] - nb);
+            }
+          __threadfence_block();
+          double lv[4][2], uv[4][2];
+#pragma unroll
+          for (int jq = 0; jq < 4; ++jq)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              lv[jq][e] = pp[jq][e] >= 0 ? w[pp[jq][e] * 32] : 0.0;
+              uv[jq][e] = pp[jq][e] >= 0 ? gb[pu[jq][e] * 32] : 0.0;
+            }
+#pragma unroll
+          for (int jq = 0; jq < 4; ++jq)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) acc[jq] -= lv[jq][e] * uv[jq][e];
+        }
+#pragma unroll
+        for (int jq = 0; jq < 4; ++jq) {
+          if (jq >= ni) continue;
+          double a = acc[jq];
+          if (kd[jq] >= 0) {
+            if (kd[jq] >= nb && kd[jq] < nbe) {
+              wait_pos(kd[jq] - nb);
+              __threadfence_block();
+            }
+            a = a / gb[kd[jq] * 32];
+          } else if (kd[jq] == -2) {
+            bool fired;
+            const double piv = a;
+            a = perturb(piv, thr, fired);
+            if (fired && live) atomicAdd(&P.npert[b], 1);
+          }
+          w[p[jq] * 32] = a;
+        }
+        __threadfence_block();
+        __syncwarp();
+        if (lane == 0)
+#pragma unroll
+          for (int jq = 0; jq < 4; ++jq)
+            if (jq < ni) atomicOr(rdy + (p[jq] >> 5), 1u << (p[jq] & 31));
+      }
+      __syncthreads();
+    }
+    if (qdf < nlv && stageable(qdf)) issue(qdf);
     cp_async_commit();
-    for (int64_t lev = lv0; lev < lv1; ++lev) {
+    for (int64_t lev = lv0 + qdf; lev < lv1; ++lev) {
       const int q = (int)(lev - lv0);
       if (lev + 1 < lv1 && stageable(q + 1)) issue(q + 1);
       cp_async_commit();

@@ -166,6 +166,10 @@ class DeviceContext:
         h = ctypes.c_void_p()
         check(self.lib.hy_create(device, ctypes.byref(h)))
         self.h = h
+        # developer knobs: HYLU_OPTIONS="name=value,name=value" (hy_set_option)
+        for kv in filter(None, os.environ.get("HYLU_OPTIONS", "").split(",")):
+            k, v = kv.split("=")
+            self.set_option(k.strip(), int(v))
         s = analysis.symbolic
         A = analysis.A
         vm = analysis.vmap
