@@ -95,6 +95,7 @@ __global__ void k_batch_bhat(DevSym, const int32_t *, const double *, double *, 
 __global__ void k_batch_xout(DevSym, const double *, double *, int64_t);
 __global__ void k_batch_fwd(DevSym, const double *, int64_t, const int32_t *, int, int, double *);
 __global__ void k_batch_bwd(DevSym, const double *, int64_t, const int32_t *, int, int, double *);
+__global__ void k_batch_bwd2(DevSym, const double *, int64_t, const int32_t *, int, int, double *);
 __global__ void k_batch_extract(const double *, int64_t, int64_t, double *);
 __global__ void k_bt_bwd(DevSym, const double *, int64_t, const int2 *, int64_t, const int64_t *, const int32_t *,
                          int *, int *, int, int, double *);
@@ -186,6 +187,7 @@ struct hy_handle {
   int nowait = 0;                          // timing experiment only: skip dependency waits
   int pair = 1;                            // pipeline: one warp per (node, group pair)
   int prefetch = 512;                      // pair mode: L2-prefetch the matrix values this many tasks ahead
+  int bwd_pair = 1;                        // backward solve: one warp per (node, group pair)
   int hub_df = 0;                          // hub kernel: dataflow phase for split-free leading levels
   int pipe_ws = 16;                        // pair-mode shared workspace columns per group
   int skew = 1;                            // diagonal claim order: group g+1 runs `skew` levels behind g
@@ -497,6 +499,10 @@ int hy_set_option(hy_handle *h, const char *name, int64_t value) {
     h->pair = value != 0;
     h->segs_G = -1;
     h->pipe_blocks = 0;
+    return HY_OK;
+  }
+  if (std::string(name) == "bwd_pair") {
+    h->bwd_pair = value != 0;
     return HY_OK;
   }
   if (std::string(name) == "hub_dataflow") {
@@ -1244,9 +1250,16 @@ int hy_solve_batched(hy_handle *h, int64_t B, const double *d_b, double *d_x, ui
   } else {
     for (int l = 0; l < bp.nlev; ++l) {
       const int c = (int)(bp.aptr[l + 1] - bp.aptr[l]);
-      const int64_t tasks = (int64_t)c * G;
-      k_batch_bwd<<<(unsigned)((tasks + 3) / 4), 128, 0, st>>>(h->S, h->d_bf, h->stored,
-                                                             bp.d_all + bp.aptr[l], c, G, h->d_by);
+      if (h->bwd_pair) {
+        const int GP = (G + 1) / 2;
+        const int64_t tasks = (int64_t)c * GP;
+        k_batch_bwd2<<<(unsigned)((tasks + 3) / 4), 128, 0, st>>>(h->S, h->d_bf, h->stored,
+                                                                bp.d_all + bp.aptr[l], c, GP, h->d_by);
+      } else {
+        const int64_t tasks = (int64_t)c * G;
+        k_batch_bwd<<<(unsigned)((tasks + 3) / 4), 128, 0, st>>>(h->S, h->d_bf, h->stored,
+                                                               bp.d_all + bp.aptr[l], c, G, h->d_by);
+      }
       h->launches++;
     }
   }

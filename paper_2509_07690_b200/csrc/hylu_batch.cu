@@ -1038,6 +1038,55 @@ __global__ void __launch_bounds__(BW * 32) k_batch_bwd(DevSym S, const double *B
   }
 }
 
+// Pair mode backward substitution: one warp per (node, group pair); the padded
+// allocation makes the odd tail group's partner valid memory (never copied out).
+__global__ void __launch_bounds__(BW * 32) k_batch_bwd2(DevSym S, const double *BF, int64_t stored,
+                                                        const int32_t *nodes, int count, int GP,
+                                                        double *Y) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t task = (int64_t)blockIdx.x * BW + warp;
+  if (task >= (int64_t)count * GP) return;
+  const int u = nodes[task / GP];
+  const int g = 2 * (int)(task % GP);
+  const int r = (int)S.first[u];
+  const int s = (int)(S.first[u + 1] - r);
+  const int64_t c0 = S.colptr[u];
+  const int W = (int)(S.colptr[u + 1] - c0);
+  const int L = S.nl[u];
+  const double *ga = BF + (int64_t)g * stored * 32 + lane;
+  const double *gc = ga + stored * 32;
+  double *ya = Y + (int64_t)g * S.n * 32 + lane;
+  double *yc = ya + (int64_t)S.n * 32;
+  const int32_t *cc = S.cols + c0;
+  for (int t = s - 1; t >= 0; --t) {
+    const int64_t ro = (S.valoff[u] + (int64_t)t * W) * 32;
+    const int d = L + t;
+    double accA = ya[(int64_t)(r + t) * 32], accC = yc[(int64_t)(r + t) * 32];
+    const double dA = ga[ro + (int64_t)d * 32], dC = gc[ro + (int64_t)d * 32];
+    for (int p0 = d + 1; p0 < W; p0 += 4) {
+      int k[4];
+      double a[4], c[4], za[4], zc[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) k[e] = p0 + e < W ? __ldg(cc + p0 + e) : -1;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const bool ok = k[e] >= 0;
+        a[e] = ok ? ga[ro + (int64_t)(p0 + e) * 32] : 0.0;
+        c[e] = ok ? gc[ro + (int64_t)(p0 + e) * 32] : 0.0;
+        za[e] = ok ? ya[(int64_t)k[e] * 32] : 0.0;
+        zc[e] = ok ? yc[(int64_t)k[e] * 32] : 0.0;
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        accA -= a[e] * za[e];
+        accC -= c[e] * zc[e];
+      }
+    }
+    ya[(int64_t)(r + t) * 32] = accA / dA;
+    yc[(int64_t)(r + t) * 32] = accC / dC;
+  }
+}
+
 // Persistent backward substitution: one warp per (node, group) task in diagonal
 // order over backward levels; a task waits for the nodes owning its columns right
 // of its block (U dependencies) and publishes its own completion flag.
