@@ -152,6 +152,10 @@ typedef struct {
   const int32_t *src_v, *src_pb, *src_tb;   /* [nsrc] source node, block position, first block row */
   const int64_t *lev_up_big;                /* [nlevels] first item routed to the DMMA kernel */
   const int64_t *lev_up_reg;                /* [nlevels] first per-source item (before: packed) */
+  const int64_t *lev_up_rs;                 /* [nlevels] first per-source item run CTA-per-item
+                                               (before it, from lev_up_reg: warp-per-item) */
+  const int64_t *lev_xp_big;                /* [nlevels] first multiplier item run CTA-per-item
+                                               (before it: warp-per-item) */
 } hy_fanin_plan;
 int hy_upload_fanin_plan(hy_handle *h, const hy_fanin_plan *plan);
 

@@ -59,6 +59,8 @@ __global__ void k_fi_upd(DevSym, CallP, FaninDev, int, int, int);
 __global__ void k_fi_upd_mma(DevSym, CallP, FaninDev, int, int, int);
 __global__ void k_fi_upd_pk(DevSym, CallP, FaninDev, int, int, int);
 __global__ void k_fi_upd3(DevSym, CallP, FaninDev, int, int, int);
+__global__ void k_fi_x_w(DevSym, CallP, FaninDev, int, int);
+__global__ void k_fi_upd_w(DevSym, CallP, FaninDev, int, int);
 size_t fi_upd3_smem(int);
 size_t fi_upd_smem(int, int);
 size_t pipe_smem_bytes(bool staged);
@@ -222,6 +224,8 @@ struct hy_handle {
   std::vector<int64_t> fi_lu, fi_pt, fi_xp, fi_up;   // per-level offsets
   std::vector<int64_t> fi_upbig;                     // per level: first DMMA-routed item
   std::vector<int64_t> fi_upreg;                     // per level: first per-source item
+  std::vector<int64_t> fi_uprs;                      // per level: first CTA-per-item regular item
+  std::vector<int64_t> fi_xpbig;                     // per level: first CTA-per-item multiplier item
   int fi_v3 = 0;                                     // option "fanin_v3" (slower; kept for experiments)
   int fi_mma = 0;                                    // option "fanin_dmma" (bitwise-equal results; slower here)
   std::vector<int32_t> fi_smax, fi_mmax;
@@ -750,6 +754,8 @@ int hy_upload_fanin_plan(hy_handle *h, const hy_fanin_plan *d) {
   h->fi_up.assign(d->lev_up, d->lev_up + nl + 1);
   h->fi_upbig.assign(d->lev_up_big, d->lev_up_big + nl);
   h->fi_upreg.assign(d->lev_up_reg, d->lev_up_reg + nl);
+  h->fi_uprs.assign(d->lev_up_rs, d->lev_up_rs + nl);
+  h->fi_xpbig.assign(d->lev_xp_big, d->lev_xp_big + nl);
   h->fi_smax.assign(d->level_smax, d->level_smax + nl);
   h->fi_mmax.assign(d->level_mmax, d->level_mmax + nl);
   size_t mx = 0;
@@ -770,6 +776,9 @@ int hy_upload_fanin_plan(hy_handle *h, const hy_fanin_plan *d) {
   return HY_OK;
 }
 
+// below this many warp-eligible items a level's small items go to the CTA kernels
+constexpr int WARP_MIN_ITEMS = 256;
+
 static int run_fanin(hy_handle *h, const CallP &P, cudaStream_t st) {
   CK(cudaMemsetAsync(P.F, 0, sizeof(double) * h->stored, st));
   k_fi_scatter<<<(h->S.n * 32 + 255) / 256, 256, 0, st>>>(h->S, P);
@@ -785,23 +794,41 @@ static int run_fanin(hy_handle *h, const CallP &P, cudaStream_t st) {
       k_fi_panel<<<npt, 256, 64 * 256 * sizeof(double), st>>>(h->S, P, h->fi, (int)h->fi_pt[l]);
       h->launches++;
     }
-    if (nxp) { k_fi_x<<<nxp, 256, 2 * 64 * 65 * sizeof(double), st>>>(h->S, P, h->fi, (int)h->fi_xp[l]); h->launches++; }
+    if (nxp) {
+      // few small items: one CTA launch for the whole level (it handles any size)
+      const int xb = (int)h->fi_xpbig[l] - (int)h->fi_xp[l] < WARP_MIN_ITEMS ? (int)h->fi_xp[l] : (int)h->fi_xpbig[l];
+      const int nw = xb - (int)h->fi_xp[l], nc = (int)h->fi_xp[l + 1] - xb;
+      if (nw) {
+        k_fi_x_w<<<(nw + 7) / 8, 256, 0, st>>>(h->S, P, h->fi, (int)h->fi_xp[l], nw);
+        h->launches++;
+      }
+      if (nc) {
+        k_fi_x<<<nc, 256, 2 * 64 * 65 * sizeof(double), st>>>(h->S, P, h->fi, xb);
+        h->launches++;
+      }
+    }
     if (nup) {
       const size_t sm = fi_upd_smem(h->fi_smax[l], h->fi_mmax[l]);
       const int reg = (int)h->fi_upreg[l];
       const int split = h->fi_mma ? (int)h->fi_upbig[l] : (int)h->fi_up[l + 1];
       const int npk = reg - (int)h->fi_up[l];
-      const int nsm = split - reg, nbig = (int)h->fi_up[l + 1] - split;
+      const int nbig = (int)h->fi_up[l + 1] - split;
       if (npk) {
         k_fi_upd_pk<<<npk, 256, sm, st>>>(h->S, P, h->fi, (int)h->fi_up[l], h->fi_smax[l], h->fi_mmax[l]);
         h->launches++;
       }
-      if (nsm) {
+      const int rs = (int)h->fi_uprs[l] - reg < WARP_MIN_ITEMS ? reg : (int)h->fi_uprs[l];
+      if (rs > reg) {
+        k_fi_upd_w<<<(rs - reg + 7) / 8, 256, 0, st>>>(h->S, P, h->fi, reg, rs - reg);
+        h->launches++;
+      }
+      if (split > rs) {
+        const int nsm2 = split - rs;
         if (h->fi_v3)
-          k_fi_upd3<<<nsm, 256, fi_upd3_smem(h->fi_smax[l]), st>>>(h->S, P, h->fi, reg, h->fi_smax[l],
-                                                                   h->fi_mmax[l]);
+          k_fi_upd3<<<nsm2, 256, fi_upd3_smem(h->fi_smax[l]), st>>>(h->S, P, h->fi, rs, h->fi_smax[l],
+                                                                    h->fi_mmax[l]);
         else
-          k_fi_upd<<<nsm, 256, sm, st>>>(h->S, P, h->fi, reg, h->fi_smax[l], h->fi_mmax[l]);
+          k_fi_upd<<<nsm2, 256, sm, st>>>(h->S, P, h->fi, rs, h->fi_smax[l], h->fi_mmax[l]);
         h->launches++;
       }
       if (nbig) {

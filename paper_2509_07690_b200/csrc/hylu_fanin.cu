@@ -263,8 +263,119 @@ __global__ void __launch_bounds__(FI_THREADS) k_fi_x(DevSym S, CallP P, FaninDev
   }
 }
 
+// Warp-per-item multiplier blocks for small pairs (target <= 32 rows, <= 8 source
+// rows): lane = target row, the row's multipliers in registers; per element the
+// same operation sequence as k_fi_x (x_a = w_a / U_aa, then w_b -= x_a U_ab for
+// b > a, skipped when x_a == 0).
+constexpr int XW_M = 8;
+__global__ void __launch_bounds__(FI_THREADS) k_fi_x_w(DevSym S, CallP P, FaninDev D, int base, int count) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int jj = blockIdx.x * (FI_THREADS / 32) + warp;
+  if (jj >= count) return;
+  const int j = base + jj;
+  const int64_t dk = D.xp_edge[j];
+  const int T = D.xp_tgt[j];
+  const int v = S.deps[dk];
+  const int r = (int)S.first[T];
+  const int s = (int)(S.first[T + 1] - r);
+  const int64_t tc0 = S.colptr[T];
+  const int W = (int)(S.colptr[T + 1] - tc0);
+  const int vf = (int)S.first[v];
+  const int vs = (int)(S.first[v + 1] - vf);
+  const int vW = (int)(S.colptr[v + 1] - S.colptr[v]);
+  const int vnl = S.nl[v];
+  const double *ub = P.F + S.valoff[v] + (int64_t)0;
+  double *Pm = P.F + S.valoff[T];
+  const int pb0 = D.dep_pb[dk];
+  const int tb0 = S.cols[tc0 + pb0] - vf;
+  const int m = vs - tb0;
+  if (lane >= s) return;
+  double *row = Pm + (int64_t)lane * W + pb0;
+  double xr[XW_M];
+#pragma unroll
+  for (int a = 0; a < XW_M; ++a) xr[a] = a < m ? row[a] : 0.0;
+#pragma unroll
+  for (int a = 0; a < XW_M; ++a) {
+    if (a < m) {
+      const double *ua = ub + (int64_t)(tb0 + a) * vW + vnl + tb0;
+      const double x = xr[a] / ua[a];
+      xr[a] = x;
+      if (x != 0.0)
+#pragma unroll
+        for (int b2 = a + 1; b2 < XW_M; ++b2)
+          if (b2 < m) xr[b2] -= x * ua[b2];
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < XW_M; ++a)
+    if (a < m) row[a] = xr[a];
+}
+
+// Warp-per-item tile updates for small targets (<= 4 rows): lanes over the
+// source's columns in the tile; per source c = Σ_a X[t][a] U[a][q] (ascending a,
+// fused multiply-adds from zero), then the tile position of q gets -= c — the
+// per-element sequence of k_fi_upd.  The tile lives in a per-warp shared buffer.
+constexpr int UW_ROWS = 4;
+constexpr int UW_TILE = 64;   // == FI_TILE
+__global__ void __launch_bounds__(FI_THREADS) k_fi_upd_w(DevSym S, CallP P, FaninDev D, int base, int count) {
+  __shared__ double tile_s[FI_THREADS / 32][UW_ROWS * UW_TILE];
+  __shared__ int tcol_s[FI_THREADS / 32][UW_TILE];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int jj = blockIdx.x * (FI_THREADS / 32) + warp;
+  if (jj >= count) return;
+  const int j = base + jj;
+  const int T = D.up_t[j];
+  const int c0 = D.up_c0[j], c1 = D.up_c1[j];
+  const int tw = c1 - c0;
+  const int r = (int)S.first[T];
+  const int s = (int)(S.first[T + 1] - r);
+  const int64_t tc0 = S.colptr[T];
+  const int W = (int)(S.colptr[T + 1] - tc0);
+  double *Pm = P.F + S.valoff[T];
+  double *acc = tile_s[warp];
+  int *tcol = tcol_s[warp];
+  for (int c = lane; c < tw; c += 32) {
+    tcol[c] = S.cols[tc0 + c0 + c];
+    for (int t = 0; t < s; ++t) acc[t * UW_TILE + c] = Pm[(int64_t)t * W + c0 + c];
+  }
+  __syncwarp();
+  for (int64_t z = D.up_ptr[j]; z < D.up_ptr[j + 1]; ++z) {
+    const int v = D.src_v[z];
+    const int q0 = D.src_q0[z];
+    const int nq = D.src_q1[z] - q0;
+    const int vf = (int)S.first[v];
+    const int vs = (int)(S.first[v + 1] - vf);
+    const int64_t vc0 = S.colptr[v];
+    const int vW = (int)(S.colptr[v + 1] - vc0);
+    const double *vb = P.F + S.valoff[v];
+    const int pb0 = D.src_pb[z];
+    const int tb0 = D.src_tb[z];
+    const int m = vs - tb0;
+    const int qbase = S.nl[v] + vs + q0;
+    for (int q = lane; q < nq; q += 32) {
+      const int pos = lower_bound_i32(tcol, 0, tw, S.cols[vc0 + qbase + q]);
+      double c[UW_ROWS];
+#pragma unroll
+      for (int t = 0; t < UW_ROWS; ++t) c[t] = 0.0;
+      for (int a = 0; a < m; ++a) {
+        const double u = vb[(int64_t)(tb0 + a) * vW + qbase + q];
+#pragma unroll
+        for (int t = 0; t < UW_ROWS; ++t)
+          if (t < s) c[t] = fma(Pm[(int64_t)t * W + pb0 + a], u, c[t]);
+      }
+#pragma unroll
+      for (int t = 0; t < UW_ROWS; ++t)
+        if (t < s) acc[t * UW_TILE + pos] -= c[t];
+    }
+    __syncwarp();
+  }
+  for (int c = lane; c < tw; c += 32)
+    for (int t = 0; t < s; ++t) Pm[(int64_t)t * W + c0 + c] = acc[t * UW_TILE + c];
+}
+
 // ---------------------------------------------------------------------------- updates
 constexpr int FI_TILE = 64;
+static_assert(FI_TILE == UW_TILE, "warp update kernel assumes 64-column tiles");
 constexpr int FI_KC = 32;      // K (source rows) chunk staged per pass
 constexpr int KLD = FI_KC + 1;
 

@@ -98,6 +98,7 @@ class FaninPlanDesc(ctypes.Structure):
         ("dep_pb", ctypes.c_void_p), ("level_smax", ctypes.c_void_p), ("level_mmax", ctypes.c_void_p),
         ("src_v", ctypes.c_void_p), ("src_pb", ctypes.c_void_p), ("src_tb", ctypes.c_void_p),
         ("lev_up_big", ctypes.c_void_p), ("lev_up_reg", ctypes.c_void_p),
+        ("lev_up_rs", ctypes.c_void_p), ("lev_xp_big", ctypes.c_void_p),
     ]
 
 
@@ -242,7 +243,7 @@ class DeviceContext:
         arrs = {k: np.ascontiguousarray(getattr(plan, k)) for k in (
             "lu_ptr", "lu_nodes", "pt_ptr", "pt_node", "pt_c0", "pt_c1", "xp_ptr", "xp_edge", "xp_tgt",
             "lev_up", "up_t", "up_c0", "up_c1", "up_ptr", "src_k", "src_q0", "src_q1", "dep_pb",
-            "level_smax", "level_mmax", "lev_up_big", "lev_up_reg")}
+            "level_smax", "level_mmax", "lev_up_big", "lev_up_reg", "lev_up_rs", "lev_xp_big")}
         arrs["lu_nodes"] = arrs["lu_nodes"].astype(np.int32)
         sv, spb, stb = schedule.fanin_source_records(s, plan)
         arrs["src_v"], arrs["src_pb"], arrs["src_tb"] = sv, spb, stb

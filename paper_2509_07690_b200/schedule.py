@@ -875,6 +875,8 @@ class FaninPlan:
     level_mmax: np.ndarray     # max source rows of a level
     lev_up_big: np.ndarray     # per level: first update item whose target has >= BIG_ROWS rows
     lev_up_reg: np.ndarray     # per level: first item of the per-source (regular) group
+    lev_up_rs: np.ndarray      # per level: first regular item for the CTA kernel (before: warp kernel)
+    lev_xp_big: np.ndarray     # per level: first multiplier item for the CTA kernel (before: warp kernel)
 
     @property
     def nlevels(self):
@@ -909,12 +911,15 @@ def _fanin_levels(first, colptr, cols, nl, dptr, deps, node_of):
 
 
 BIG_ROWS = 32
+WARP_ROWS = 4          # update items with targets this small run warp-per-item
+XW_ROWS, XW_M = 32, 8  # multiplier blocks this small (target rows, source rows) too
 
 
 def _split_items(out, rows, nlev, src_rows):
-    """Within each level order the update items in three contiguous launch groups:
-    0 = many small sources (packed K-slice kernel), 1 = regular (per-source FFMA
-    kernel), 2 = target >= BIG_ROWS rows (DMMA-eligible; runs the FFMA kernel
+    """Within each level order the update items in four contiguous launch groups:
+    0 = many small sources (packed K-slice kernel), 1 = regular with a target of
+    <= WARP_ROWS rows (warp-per-item kernel), 2 = regular (per-source FFMA CTA
+    kernel), 3 = target >= BIG_ROWS rows (DMMA-eligible; runs the FFMA kernel
     unless DMMA routing is enabled)."""
     (lu_ptr, lu_nodes, pt_ptr, pt_node, pt_c0, pt_c1, xp_ptr, xp_edge, xp_tgt,
      lev_up, up_t, up_c0, up_c1, up_ptr, src_k, src_q0, src_q1) = out
@@ -927,20 +932,51 @@ def _split_items(out, rows, nlev, src_rows):
     pn = int(os.environ.get("HYLU_PACK_N", "4"))
     packed = (nsrc >= pn) & (msum < pm * nsrc)
     big = (rows[up_t] >= BIG_ROWS) & ~packed
-    grp = np.where(packed, 0, np.where(big, 2, 1)).astype(np.int64)
+    small = (rows[up_t] <= WARP_ROWS) & ~packed & ~big
+    grp = np.where(packed, 0, np.where(big, 3, np.where(small, 1, 2))).astype(np.int64)
     order = np.lexsort((grp, lvl))
     cnt = np.diff(up_ptr)[order]
     new_ptr = np.zeros(nitem + 1, np.int64)
     np.cumsum(cnt, out=new_ptr[1:])
     gather = np.repeat(up_ptr[:-1][order], cnt) + (np.arange(new_ptr[-1]) - np.repeat(new_ptr[:-1], cnt))
-    n0 = np.bincount(lvl[grp == 0], minlength=nlev) if nitem else np.zeros(nlev, np.int64)
-    n1 = np.bincount(lvl[grp == 1], minlength=nlev) if nitem else np.zeros(nlev, np.int64)
-    reg = lev_up[:-1] + n0
-    split = reg + n1
+    def cnt_of(k):
+        return np.bincount(lvl[grp == k], minlength=nlev) if nitem else np.zeros(nlev, np.int64)
+    reg = lev_up[:-1] + cnt_of(0)
+    rs = reg + cnt_of(1)
+    split = rs + cnt_of(2)
     out = (lu_ptr, lu_nodes, pt_ptr, pt_node, pt_c0, pt_c1, xp_ptr, xp_edge, xp_tgt, lev_up,
            up_t[order], up_c0[order], up_c1[order], new_ptr, src_k[gather], src_q0[gather],
            src_q1[gather])
-    return out, split.astype(np.int64), reg.astype(np.int64)
+    return out, split.astype(np.int64), reg.astype(np.int64), rs.astype(np.int64)
+
+
+def _split_xp(out, s, rows, nlev):
+    """Within each level put the small multiplier items (target <= XW_ROWS rows,
+    <= XW_M source rows) first: they run warp-per-item; the rest run CTA-per-item."""
+    out = list(out)
+    xp_ptr, xp_edge, xp_tgt = out[6], np.asarray(out[7], np.int64), np.asarray(out[8])
+    n = len(xp_tgt)
+    big = np.zeros(nlev, np.int64)
+    if n:
+        v = s.deps[xp_edge]
+        tb0 = s.cols[s.colptr[xp_tgt] + np.asarray(_dep_pb_cache(s))[xp_edge]] - s.node_first[v]
+        m = rows[v] - tb0
+        small = (rows[xp_tgt] <= XW_ROWS) & (m <= XW_M)
+        lvl = np.repeat(np.arange(nlev), np.diff(xp_ptr))
+        order = np.lexsort((~small, lvl))
+        out[7], out[8] = out[7][order], out[8][order]
+        big = xp_ptr[:-1] + np.bincount(lvl[small], minlength=nlev)
+    else:
+        big = np.asarray(xp_ptr[:-1], np.int64).copy()
+    return tuple(out), big.astype(np.int64)
+
+
+def _dep_pb_cache(s):
+    pb = getattr(s, "_dep_pb", None)
+    if pb is None:
+        pb = _dep_block_pos(s.node_first, s.node_kind, s.colptr, s.cols, s.nl, s.dep_ptr, s.deps)
+        s._dep_pb = pb
+    return pb
 
 
 def build_fanin_plan(sym, tw=FANIN_TILE, pw=PANEL_TILE):
@@ -949,7 +985,7 @@ def build_fanin_plan(sym, tw=FANIN_TILE, pw=PANEL_TILE):
     nlev = int(flev.max()) + 1
     out = _fanin_plan(s.node_first, s.node_kind, s.colptr, s.cols, s.nl, s.dep_ptr, s.deps,
                       flev, nlev, tw, pw)
-    dep_pb = _dep_block_pos(s.node_first, s.node_kind, s.colptr, s.cols, s.nl, s.dep_ptr, s.deps)
+    dep_pb = _dep_pb_cache(s)
     rows = np.diff(s.node_first)
     # source rows per update-source record (rows of v from its first present block row)
     up_ptr, up_t, src_k = out[13], out[10], out[14]
@@ -967,7 +1003,8 @@ def build_fanin_plan(sym, tw=FANIN_TILE, pw=PANEL_TILE):
             out[9], out[10], out[11], out[12], out[13], out[14], out[15], out[16], src_rows,
             cap_rows, cap_recs)
         out = out[:9] + (lev_up, up_t, up_c0, up_c1, up_ptr, src_k, src_q0, src_q1)
-    out, split, reg = _split_items(out, rows, nlev, src_rows)
+    out, split, reg, rs = _split_items(out, rows, nlev, src_rows)
+    out, xp_big = _split_xp(out, s, rows, nlev)
     lu_ptr, lu_nodes = out[0], out[1]
     lev_up, up_t = out[9], out[10]
     smax = np.ones(nlev, np.int32)
@@ -979,7 +1016,7 @@ def build_fanin_plan(sym, tw=FANIN_TILE, pw=PANEL_TILE):
         nodes = lu_nodes[lu_ptr[lv]:lu_ptr[lv + 1]]
         if len(nodes):
             mmax[lv] = int(rows[nodes].max())
-    return FaninPlan(*out, dep_pb, smax, mmax, split, reg)
+    return FaninPlan(*out, dep_pb, smax, mmax, split, reg, rs, xp_big)
 
 
 def fanin_source_records(sym, plan):
