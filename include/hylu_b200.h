@@ -156,6 +156,14 @@ typedef struct {
                                                (before it, from lev_up_reg: warp-per-item) */
   const int64_t *lev_xp_big;                /* [nlevels] first multiplier item run CTA-per-item
                                                (before it: warp-per-item) */
+  int64_t nhub;                             /* standalone rows computed by pull programs
+                                               (hy_upload_hub_programs) instead of fan-in updates */
+  const int64_t *lev_hub;                   /* [nlevels+1] offsets into hub_list */
+  const int32_t *hub_list;                  /* [nhub] those rows' nodes, by level */
+  int64_t nparts;                           /* split-K parts of heavy packed update items */
+  const int32_t *up_part;                   /* [nitems] part id or -1 */
+  const int32_t *part_first, *part_n;       /* [nparts] first part of the item, parts of the item */
+  const int64_t *part_off;                  /* [nparts] partial-tile offset (doubles) in the scratch */
 } hy_fanin_plan;
 int hy_upload_fanin_plan(hy_handle *h, const hy_fanin_plan *plan);
 

@@ -49,6 +49,12 @@ struct FaninDev {
   const int32_t *src_v;
   const int32_t *src_pb;
   const int32_t *src_tb;
+  const int32_t *up_part;    // layout shared with hylu_fanin.cu
+  const int32_t *part_first;
+  const int32_t *part_n;
+  const int64_t *part_off;
+  double *part_scr;
+  int *part_cnt;
 };
 __global__ void k_fi_scatter(DevSym, CallP);
 
@@ -226,6 +232,8 @@ struct hy_handle {
   std::vector<int64_t> fi_upreg;                     // per level: first per-source item
   std::vector<int64_t> fi_uprs;                      // per level: first CTA-per-item regular item
   std::vector<int64_t> fi_xpbig;                     // per level: first CTA-per-item multiplier item
+  std::vector<int64_t> fi_hub;                       // per level: offsets of pull-program rows
+  int32_t *d_fi_hubs = nullptr;
   int fi_v3 = 0;                                     // option "fanin_v3" (slower; kept for experiments)
   int fi_mma = 0;                                    // option "fanin_dmma" (bitwise-equal results; slower here)
   std::vector<int32_t> fi_smax, fi_mmax;
@@ -756,6 +764,29 @@ int hy_upload_fanin_plan(hy_handle *h, const hy_fanin_plan *d) {
   h->fi_upreg.assign(d->lev_up_reg, d->lev_up_reg + nl);
   h->fi_uprs.assign(d->lev_up_rs, d->lev_up_rs + nl);
   h->fi_xpbig.assign(d->lev_xp_big, d->lev_xp_big + nl);
+  D.up_part = nullptr; D.part_first = nullptr; D.part_n = nullptr; D.part_off = nullptr;
+  D.part_scr = nullptr; D.part_cnt = nullptr;
+  if (d->nparts > 0) {
+    const int64_t nitems = d->lev_up[nl];
+    UPF(&p32, d->up_part, nitems); D.up_part = p32;
+    UPF(&p32, d->part_first, d->nparts); D.part_first = p32;
+    UPF(&p32, d->part_n, d->nparts); D.part_n = p32;
+    UPF(&p64, d->part_off, d->nparts); D.part_off = p64;
+    // partial tiles: the last part's offset plus one full tile
+    const int64_t scr = d->part_off[d->nparts - 1] + 64 * 64;
+    CK(cudaMalloc((void **)&D.part_scr, sizeof(double) * scr));
+    h->fi_allocs.push_back(D.part_scr);
+    CK(cudaMalloc((void **)&D.part_cnt, sizeof(int) * d->nparts));
+    h->fi_allocs.push_back(D.part_cnt);
+    CK(cudaMemset(D.part_cnt, 0, sizeof(int) * d->nparts));
+  }
+  h->fi_hub.assign(nl + 1, 0);
+  h->d_fi_hubs = nullptr;
+  if (d->nhub > 0) {
+    if (!d->lev_hub || !d->hub_list) return fail(HY_INVALID_ARGUMENT, "pull rows without their lists");
+    h->fi_hub.assign(d->lev_hub, d->lev_hub + nl + 1);
+    UPF(&p32, d->hub_list, d->nhub); h->d_fi_hubs = p32;
+  }
   h->fi_smax.assign(d->level_smax, d->level_smax + nl);
   h->fi_mmax.assign(d->level_mmax, d->level_mmax + nl);
   size_t mx = 0;
@@ -789,6 +820,21 @@ static int run_fanin(hy_handle *h, const CallP &P, cudaStream_t st) {
     const int npt = (int)(h->fi_pt[l + 1] - h->fi_pt[l]);
     const int nxp = (int)(h->fi_xp[l + 1] - h->fi_xp[l]);
     const int nup = (int)(h->fi_up[l + 1] - h->fi_up[l]);
+    // pull-program rows of this level: every source is final, compute them whole
+    const int nph = (int)(h->fi_hub[l + 1] - h->fi_hub[l]);
+    if (nph) {
+      if (!h->hub1_ok) return fail(HY_INVALID_ARGUMENT, "fan-in plan has pull rows but no hub programs");
+      const int64_t need = (int64_t)nph * h->hub1_slots;
+      if (need > h->hub1_scratch_cap) {
+        if (h->d_hub1_scratch) CK(cudaFree(h->d_hub1_scratch));
+        h->d_hub1_scratch = nullptr;
+        CK(cudaMalloc((void **)&h->d_hub1_scratch, sizeof(double) * need));
+        h->hub1_scratch_cap = need;
+      }
+      k_hub1<<<nph, 1024, 0, st>>>(h->S, P, h->prog1, h->d_fi_hubs + h->fi_hub[l], h->d_hub1_scratch,
+                                   h->hub1_slots);
+      h->launches++;
+    }
     if (nlu) { k_fi_lu<<<nlu, 256, 0, st>>>(h->S, P, h->fi, (int)h->fi_lu[l]); h->launches++; }
     if (npt) {
       k_fi_panel<<<npt, 256, 64 * 256 * sizeof(double), st>>>(h->S, P, h->fi, (int)h->fi_pt[l]);

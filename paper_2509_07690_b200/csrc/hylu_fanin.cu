@@ -45,6 +45,12 @@ struct FaninDev {
   const int32_t *src_v;      // per source record: source node, block position, first block row
   const int32_t *src_pb;
   const int32_t *src_tb;
+  const int32_t *up_part;    // split-K: part id per item (-1: unsplit)
+  const int32_t *part_first;
+  const int32_t *part_n;
+  const int64_t *part_off;
+  double *part_scr;          // partial tiles
+  int *part_cnt;             // arrivals per split item (indexed by its first part id)
 };
 
 constexpr int FI_THREADS = 256;
@@ -612,18 +618,48 @@ __global__ void __launch_bounds__(FI_THREADS) k_fi_upd_pk(DevSym S, CallP P, Fan
     z = s_znext;
     a0 = s_anext;
   }
-  // one update of the tile: T[:, tile] -= accumulated product
+  const int part = D.up_part ? D.up_part[j] : -1;
+  if (part < 0) {
+    // one update of the tile: T[:, tile] -= accumulated product
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      const int t = tr + 16 * x;
+      if (t < s) {
+#pragma unroll
+        for (int y = 0; y < 4; ++y) {
+          const int c = tcl + 16 * y;
+          if (c < tw) Pm[(int64_t)t * W + c0 + c] -= c4[x][y];
+        }
+      }
+    }
+    return;
+  }
+  // split-K part: publish the partial tile; the last part of the item adds the
+  // partials in part order and updates the target once
+  double *mine = D.part_scr + D.part_off[part];
 #pragma unroll
   for (int x = 0; x < 4; ++x) {
     const int t = tr + 16 * x;
-    if (t < s) {
+    if (t < s)
 #pragma unroll
-      for (int y = 0; y < 4; ++y) {
-        const int c = tcl + 16 * y;
-        if (c < tw) Pm[(int64_t)t * W + c0 + c] -= c4[x][y];
-      }
-    }
+      for (int y = 0; y < 4; ++y) mine[t * FI_TILE + tcl + 16 * y] = c4[x][y];
   }
+  __threadfence();
+  __syncthreads();
+  __shared__ int s_last;
+  const int first = D.part_first[part], np = D.part_n[part];
+  if (tid == 0) s_last = atomicAdd(D.part_cnt + first, 1) == np - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int idx = tid; idx < s * FI_TILE; idx += FI_THREADS) {
+    const int t = idx / FI_TILE, c = idx - t * FI_TILE;
+    if (c >= tw) continue;
+    double sum = 0.0;
+    for (int k = 0; k < np; ++k) sum += __ldcg(D.part_scr + D.part_off[first + k] + t * FI_TILE + c);
+    Pm[(int64_t)t * W + c0 + c] -= sum;
+  }
+  if (tid == 0) D.part_cnt[first] = 0;
 }
 
 __global__ void __launch_bounds__(FI_THREADS) k_fi_upd_mma(DevSym S, CallP P, FaninDev D, int base,

@@ -99,6 +99,9 @@ class FaninPlanDesc(ctypes.Structure):
         ("src_v", ctypes.c_void_p), ("src_pb", ctypes.c_void_p), ("src_tb", ctypes.c_void_p),
         ("lev_up_big", ctypes.c_void_p), ("lev_up_reg", ctypes.c_void_p),
         ("lev_up_rs", ctypes.c_void_p), ("lev_xp_big", ctypes.c_void_p),
+        ("nhub", ctypes.c_int64), ("lev_hub", ctypes.c_void_p), ("hub_list", ctypes.c_void_p),
+        ("nparts", ctypes.c_int64), ("up_part", ctypes.c_void_p), ("part_first", ctypes.c_void_p),
+        ("part_n", ctypes.c_void_p), ("part_off", ctypes.c_void_p),
     ]
 
 
@@ -238,18 +241,34 @@ class DeviceContext:
         s = self.analysis.symbolic
         plan = getattr(s, "_fanin_plan", None)
         if plan is None:
-            plan = schedule.build_fanin_plan(s)
+            # standalone hub rows (thousands of row sources) run as pull programs
+            pull = None
+            if os.environ.get("HYLU_FANIN_PULL", "0") != "0":
+                hub = int(os.environ.get("HYLU_HUB_STEPS", schedule.HUB_STEPS))
+                progs = schedule.build_programs(self.analysis, np.zeros(self.n, np.int64), hub,
+                                                standalone_only=True)
+                if len(progs.hub_nodes):
+                    pull = np.zeros(s.nnodes, bool)
+                    pull[progs.hub_nodes] = True
+                    s._pull_programs = progs
+            plan = schedule.build_fanin_plan(s, pull=pull)
             s._fanin_plan = plan
+        progs = getattr(s, "_pull_programs", None)
+        if progs is not None and len(plan.hub_list):
+            self._desc_programs(progs, self.lib.hy_upload_hub_programs)
         arrs = {k: np.ascontiguousarray(getattr(plan, k)) for k in (
             "lu_ptr", "lu_nodes", "pt_ptr", "pt_node", "pt_c0", "pt_c1", "xp_ptr", "xp_edge", "xp_tgt",
             "lev_up", "up_t", "up_c0", "up_c1", "up_ptr", "src_k", "src_q0", "src_q1", "dep_pb",
-            "level_smax", "level_mmax", "lev_up_big", "lev_up_reg", "lev_up_rs", "lev_xp_big")}
+            "level_smax", "level_mmax", "lev_up_big", "lev_up_reg", "lev_up_rs", "lev_xp_big",
+            "lev_hub", "hub_list", "up_part", "part_first", "part_n", "part_off")}
         arrs["lu_nodes"] = arrs["lu_nodes"].astype(np.int32)
         sv, spb, stb = schedule.fanin_source_records(s, plan)
         arrs["src_v"], arrs["src_pb"], arrs["src_tb"] = sv, spb, stb
         arrs["xp_edge"] = arrs["xp_edge"].astype(np.int64)
         d = FaninPlanDesc()
         d.nlevels, d.nsrc, d.ndeps = plan.nlevels, len(plan.src_k), len(plan.dep_pb)
+        d.nhub = len(plan.hub_list)
+        d.nparts = len(plan.part_n)
         for k, v in arrs.items():
             setattr(d, k, v.ctypes.data if v.size else None)
         with self.torch.cuda.device(self.device):

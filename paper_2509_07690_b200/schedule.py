@@ -877,6 +877,12 @@ class FaninPlan:
     lev_up_reg: np.ndarray     # per level: first item of the per-source (regular) group
     lev_up_rs: np.ndarray      # per level: first regular item for the CTA kernel (before: warp kernel)
     lev_xp_big: np.ndarray     # per level: first multiplier item for the CTA kernel (before: warp kernel)
+    lev_hub: np.ndarray        # per level: offsets into hub_list
+    hub_list: np.ndarray       # pull-program rows by level (k_hub1)
+    up_part: np.ndarray        # per update item: split-K part id, -1 if unsplit
+    part_first: np.ndarray     # per part: first part id of its item's group
+    part_n: np.ndarray         # per part: parts in its group
+    part_off: np.ndarray       # per part: offset (doubles) of its partial tile in the scratch
 
     @property
     def nlevels(self):
@@ -950,6 +956,49 @@ def _split_items(out, rows, nlev, src_rows):
     return out, split.astype(np.int64), reg.astype(np.int64), rs.astype(np.int64)
 
 
+SPLIT_SRC = int(os.environ.get("HYLU_SPLIT_SRC", "48"))
+
+
+def _split_heavy(out, split, reg, rs, rows, nlev, cap=None):
+    """Split-K for packed update items (group 0) with more than `cap` sources: the
+    item becomes ceil(nsrc/cap) consecutive parts over contiguous source ranges.
+    Each part accumulates its partial product tile; the last part to finish adds
+    the partials in part order and updates the target once (deterministic).
+    Returns the plan, the shifted group offsets and the part tables."""
+    cap = SPLIT_SRC if cap is None else cap
+    out = list(out)
+    lev_up, up_t, up_c0, up_c1, up_ptr = out[9], out[10], out[11], out[12], out[13]
+    nitem = len(up_t)
+    nsrc = np.diff(up_ptr)
+    lvl = np.repeat(np.arange(nlev), np.diff(lev_up))
+    grp0 = np.arange(nitem) < reg[lvl] if nitem else np.zeros(0, bool)
+    heavy = grp0 & (nsrc > cap) if cap > 0 else np.zeros(nitem, bool)
+    npart = np.where(heavy, (nsrc + cap - 1) // max(cap, 1), 1).astype(np.int64)
+    empty = (np.full(0, -1, np.int32), np.zeros(0, np.int32), np.zeros(0, np.int32),
+             np.zeros(0, np.int64))
+    if not heavy.any():
+        return tuple(out), split, reg, rs, (np.full(nitem, -1, np.int32),) + empty[1:]
+    newstart = np.concatenate([[0], np.cumsum(npart)]).astype(np.int64)
+    tot = int(newstart[-1])
+    item_of = np.repeat(np.arange(nitem), npart)
+    k = np.arange(tot) - newstart[item_of]
+    out[10], out[11], out[12] = up_t[item_of], up_c0[item_of], up_c1[item_of]
+    starts = up_ptr[:-1][item_of] + k * cap
+    out[13] = np.concatenate([starts, [up_ptr[-1]]]).astype(np.int64)
+    out[9] = newstart[lev_up]
+    split, reg, rs = newstart[split], newstart[reg], newstart[rs]
+    # part tables
+    is_part = heavy[item_of]
+    nparts = int(is_part.sum())
+    up_part = np.full(tot, -1, np.int32)
+    up_part[is_part] = np.arange(nparts, dtype=np.int32)
+    part_n = npart[item_of][is_part].astype(np.int32)
+    part_first = (np.arange(nparts) - k[is_part]).astype(np.int32)
+    tile = rows[up_t[item_of][is_part]].astype(np.int64) * FANIN_TILE
+    part_off = np.concatenate([[0], np.cumsum(tile)[:-1]]).astype(np.int64)
+    return tuple(out), split, reg, rs, (up_part, part_first, part_n, part_off)
+
+
 def _split_xp(out, s, rows, nlev):
     """Within each level put the small multiplier items (target <= XW_ROWS rows,
     <= XW_M source rows) first: they run warp-per-item; the rest run CTA-per-item."""
@@ -979,12 +1028,48 @@ def _dep_pb_cache(s):
     return pb
 
 
-def build_fanin_plan(sym, tw=FANIN_TILE, pw=PANEL_TILE):
+def _drop_pull_targets(out, pull, nlev):
+    """Take the pull-program rows out of the fan-in plan as targets: no LU, tile,
+    multiplier-block or update item has them as target (they are computed whole
+    by their pull program at their level, once every source is final); they stay
+    sources of later nodes.  Returns the plan and the per-level pull-row lists."""
+    (lu_ptr, lu_nodes, pt_ptr, pt_node, pt_c0, pt_c1, xp_ptr, xp_edge, xp_tgt,
+     lev_up, up_t, up_c0, up_c1, up_ptr, src_k, src_q0, src_q1) = out
+
+    def keep_ptr(ptr, keep):
+        lvl = np.repeat(np.arange(nlev), np.diff(ptr))
+        cnt = np.bincount(lvl[keep], minlength=nlev)
+        return np.concatenate([[0], np.cumsum(cnt)]).astype(np.int64)
+
+    lu_nodes = np.asarray(lu_nodes)
+    k_lu = ~pull[lu_nodes]
+    lvl_lu = np.repeat(np.arange(nlev), np.diff(lu_ptr))
+    hub_list = lu_nodes[~k_lu].astype(np.int32)
+    lev_hub = np.concatenate([[0], np.cumsum(np.bincount(lvl_lu[~k_lu], minlength=nlev))]).astype(np.int64)
+    k_pt = ~pull[np.asarray(pt_node)]
+    k_xp = ~pull[np.asarray(xp_tgt)]
+    k_up = ~pull[np.asarray(up_t)]
+    nsrc = np.diff(up_ptr)
+    k_src = np.repeat(k_up, nsrc)
+    new_up_ptr = np.concatenate([[0], np.cumsum(nsrc[k_up])]).astype(np.int64)
+    out = (keep_ptr(lu_ptr, k_lu), lu_nodes[k_lu], keep_ptr(pt_ptr, k_pt), pt_node[k_pt], pt_c0[k_pt],
+           pt_c1[k_pt], keep_ptr(xp_ptr, k_xp), xp_edge[k_xp], xp_tgt[k_xp], keep_ptr(lev_up, k_up),
+           up_t[k_up], up_c0[k_up], up_c1[k_up], new_up_ptr, src_k[k_src], src_q0[k_src], src_q1[k_src])
+    return out, lev_hub, hub_list
+
+
+def build_fanin_plan(sym, tw=FANIN_TILE, pw=PANEL_TILE, pull=None):
+    """pull: optional bool[nnodes] — standalone rows computed by pull programs
+    (k_hub1) at their level instead of receiving fan-in updates."""
     s = sym
     flev = _fanin_levels(s.node_first, s.colptr, s.cols, s.nl, s.dep_ptr, s.deps, s.node_of)
     nlev = int(flev.max()) + 1
     out = _fanin_plan(s.node_first, s.node_kind, s.colptr, s.cols, s.nl, s.dep_ptr, s.deps,
                       flev, nlev, tw, pw)
+    if pull is not None and pull.any():
+        out, lev_hub, hub_list = _drop_pull_targets(out, np.asarray(pull, bool), nlev)
+    else:
+        lev_hub, hub_list = np.zeros(nlev + 1, np.int64), np.zeros(0, np.int32)
     dep_pb = _dep_pb_cache(s)
     rows = np.diff(s.node_first)
     # source rows per update-source record (rows of v from its first present block row)
@@ -1004,6 +1089,7 @@ def build_fanin_plan(sym, tw=FANIN_TILE, pw=PANEL_TILE):
             cap_rows, cap_recs)
         out = out[:9] + (lev_up, up_t, up_c0, up_c1, up_ptr, src_k, src_q0, src_q1)
     out, split, reg, rs = _split_items(out, rows, nlev, src_rows)
+    out, split, reg, rs, parts = _split_heavy(out, split, reg, rs, rows, nlev)
     out, xp_big = _split_xp(out, s, rows, nlev)
     lu_ptr, lu_nodes = out[0], out[1]
     lev_up, up_t = out[9], out[10]
@@ -1016,7 +1102,7 @@ def build_fanin_plan(sym, tw=FANIN_TILE, pw=PANEL_TILE):
         nodes = lu_nodes[lu_ptr[lv]:lu_ptr[lv + 1]]
         if len(nodes):
             mmax[lv] = int(rows[nodes].max())
-    return FaninPlan(*out, dep_pb, smax, mmax, split, reg, rs, xp_big)
+    return FaninPlan(*out, dep_pb, smax, mmax, split, reg, rs, xp_big, lev_hub, hub_list, *parts)
 
 
 def fanin_source_records(sym, plan):
