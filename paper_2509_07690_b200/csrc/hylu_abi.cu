@@ -772,8 +772,10 @@ int hy_upload_fanin_plan(hy_handle *h, const hy_fanin_plan *d) {
     UPF(&p32, d->part_first, d->nparts); D.part_first = p32;
     UPF(&p32, d->part_n, d->nparts); D.part_n = p32;
     UPF(&p64, d->part_off, d->nparts); D.part_off = p64;
-    // partial tiles: the last part's offset plus one full tile
-    const int64_t scr = d->part_off[d->nparts - 1] + 64 * 64;
+    // partial tiles (offsets restart per level): the largest offset plus one tile
+    int64_t scr = 0;
+    for (int64_t q = 0; q < d->nparts; ++q) scr = d->part_off[q] > scr ? d->part_off[q] : scr;
+    scr += 64 * 64;
     CK(cudaMalloc((void **)&D.part_scr, sizeof(double) * scr));
     h->fi_allocs.push_back(D.part_scr);
     CK(cudaMalloc((void **)&D.part_cnt, sizeof(int) * d->nparts));

@@ -956,7 +956,9 @@ def _split_items(out, rows, nlev, src_rows):
     return out, split.astype(np.int64), reg.astype(np.int64), rs.astype(np.int64)
 
 
-SPLIT_SRC = int(os.environ.get("HYLU_SPLIT_SRC", "48"))
+SPLIT_SRC = int(os.environ.get("HYLU_SPLIT_SRC", "8"))
+SPLIT_REL = float(os.environ.get("HYLU_SPLIT_REL", "4"))
+SPLIT_LEVEL_ITEMS = int(os.environ.get("HYLU_SPLIT_LEVEL_ITEMS", "8192"))  # packed items per level
 
 
 def _split_heavy(out, split, reg, rs, rows, nlev, cap=None):
@@ -972,7 +974,14 @@ def _split_heavy(out, split, reg, rs, rows, nlev, cap=None):
     nsrc = np.diff(up_ptr)
     lvl = np.repeat(np.arange(nlev), np.diff(lev_up))
     grp0 = np.arange(nitem) < reg[lvl] if nitem else np.zeros(0, bool)
-    heavy = grp0 & (nsrc > cap) if cap > 0 else np.zeros(nitem, bool)
+    # only outliers: items far above their level's mean source count set the
+    # level's critical path; splitting typical items just adds partial traffic
+    g0cnt = np.bincount(lvl[grp0], minlength=nlev)
+    g0sum = np.bincount(lvl[grp0], weights=nsrc[grp0], minlength=nlev)
+    mean = np.where(g0cnt > 0, g0sum / np.maximum(g0cnt, 1), 0.0)
+    outlier = nsrc > SPLIT_REL * mean[lvl] if nitem else np.zeros(0, bool)
+    narrow = (g0cnt < SPLIT_LEVEL_ITEMS)[lvl] if nitem else np.zeros(0, bool)
+    heavy = grp0 & narrow & outlier & (nsrc > cap) if cap > 0 else np.zeros(nitem, bool)
     npart = np.where(heavy, (nsrc + cap - 1) // max(cap, 1), 1).astype(np.int64)
     empty = (np.full(0, -1, np.int32), np.zeros(0, np.int32), np.zeros(0, np.int32),
              np.zeros(0, np.int64))
@@ -994,8 +1003,16 @@ def _split_heavy(out, split, reg, rs, rows, nlev, cap=None):
     up_part[is_part] = np.arange(nparts, dtype=np.int32)
     part_n = npart[item_of][is_part].astype(np.int32)
     part_first = (np.arange(nparts) - k[is_part]).astype(np.int32)
+    # partial tiles are live only within their level: offsets restart per level
     tile = rows[up_t[item_of][is_part]].astype(np.int64) * FANIN_TILE
-    part_off = np.concatenate([[0], np.cumsum(tile)[:-1]]).astype(np.int64)
+    plev = lvl[item_of][is_part]
+    csum = np.cumsum(tile) - tile
+    lev_base = np.zeros(nlev, np.int64)
+    if nparts:
+        first_in_lev = np.searchsorted(plev, np.arange(nlev))
+        has = first_in_lev < nparts
+        lev_base[has] = csum[first_in_lev[has]]
+    part_off = (csum - lev_base[plev]).astype(np.int64)
     return tuple(out), split, reg, rs, (up_part, part_first, part_n, part_off)
 
 
