@@ -385,6 +385,24 @@ static_assert(FI_TILE == UW_TILE, "warp update kernel assumes 64-column tiles");
 constexpr int FI_KC = 32;      // K (source rows) chunk staged per pass
 constexpr int KLD = FI_KC + 1;
 
+// k_fi_upd's register-tiled product over one staged K chunk: NX row groups and NY
+// column groups of 16 (the ones the source and target actually cover).
+template <int NX, int NY>
+__device__ __forceinline__ void fi_steps(const double *Xs, const double *Ut, int kc, int tr, int tcl,
+                                         int s, double (&c4)[4][4]) {
+  for (int a = 0; a < kc; ++a) {
+    double xv[NX], uv[NY];
+#pragma unroll
+    for (int x = 0; x < NX; ++x) xv[x] = (tr + 16 * x < s) ? Xs[(tr + 16 * x) * KLD + a] : 0.0;
+#pragma unroll
+    for (int y = 0; y < NY; ++y) uv[y] = Ut[a * FXLD + tcl + 16 * y];
+#pragma unroll
+    for (int x = 0; x < NX; ++x)
+#pragma unroll
+      for (int y = 0; y < NY; ++y) c4[x][y] = fma(xv[x], uv[y], c4[x][y]);
+  }
+}
+
 __global__ void __launch_bounds__(FI_THREADS) k_fi_upd(DevSym S, CallP P, FaninDev D, int base,
                                                        int Smax, int Mmax) {
   extern __shared__ __align__(16) double fs[];
@@ -431,6 +449,11 @@ __global__ void __launch_bounds__(FI_THREADS) k_fi_upd(DevSym S, CallP P, FaninD
     for (int x = 0; x < 4; ++x)
 #pragma unroll
       for (int y = 0; y < 4; ++y) c4[x][y] = 0.0;
+    // only the source's columns (nq) and the target's rows (s) are computed: the
+    // register tile shrinks to NX row groups x NY column groups of 16
+    const int ny = nq <= 16 ? 1 : (nq <= 32 ? 2 : 4);
+    const int nx = s <= 16 ? 1 : (s <= 32 ? 2 : 4);
+    const int cw = 16 * ny;
     for (int k0 = 0; k0 < m; k0 += FI_KC) {
       const int kc = min(FI_KC, m - k0);
       if (k0) __syncthreads();
@@ -438,21 +461,21 @@ __global__ void __launch_bounds__(FI_THREADS) k_fi_upd(DevSym S, CallP P, FaninD
         const int t = idx / kc, a = idx - t * kc;
         Xs[t * KLD + a] = Pm[(int64_t)t * W + pb0 + k0 + a];
       }
-      for (int idx = tid; idx < kc * FI_TILE; idx += FI_THREADS) {
-        const int a = idx >> 6, c = idx & 63;
+      for (int idx = tid; idx < kc * cw; idx += FI_THREADS) {
+        const int a = idx / cw, c = idx - a * cw;
         Ut[a * FXLD + c] = c < nq ? vb[(int64_t)(tb0 + k0 + a) * vW + qbase + c] : 0.0;
       }
       __syncthreads();
-      for (int a = 0; a < kc; ++a) {
-        double xv[4], uv[4];
-#pragma unroll
-        for (int x = 0; x < 4; ++x) xv[x] = (tr + 16 * x < s) ? Xs[(tr + 16 * x) * KLD + a] : 0.0;
-#pragma unroll
-        for (int y = 0; y < 4; ++y) uv[y] = Ut[a * FXLD + tcl + 16 * y];
-#pragma unroll
-        for (int x = 0; x < 4; ++x)
-#pragma unroll
-          for (int y = 0; y < 4; ++y) c4[x][y] = fma(xv[x], uv[y], c4[x][y]);
+      switch (nx * 8 + ny) {
+        case 9: fi_steps<1, 1>(Xs, Ut, kc, tr, tcl, s, c4); break;
+        case 10: fi_steps<1, 2>(Xs, Ut, kc, tr, tcl, s, c4); break;
+        case 12: fi_steps<1, 4>(Xs, Ut, kc, tr, tcl, s, c4); break;
+        case 17: fi_steps<2, 1>(Xs, Ut, kc, tr, tcl, s, c4); break;
+        case 18: fi_steps<2, 2>(Xs, Ut, kc, tr, tcl, s, c4); break;
+        case 20: fi_steps<2, 4>(Xs, Ut, kc, tr, tcl, s, c4); break;
+        case 33: fi_steps<4, 1>(Xs, Ut, kc, tr, tcl, s, c4); break;
+        case 34: fi_steps<4, 2>(Xs, Ut, kc, tr, tcl, s, c4); break;
+        default: fi_steps<4, 4>(Xs, Ut, kc, tr, tcl, s, c4); break;
       }
     }
 #pragma unroll
