@@ -764,6 +764,8 @@ int hy_upload_fanin_plan(hy_handle *h, const hy_fanin_plan *d) {
   h->fi_upreg.assign(d->lev_up_reg, d->lev_up_reg + nl);
   h->fi_uprs.assign(d->lev_up_rs, d->lev_up_rs + nl);
   h->fi_xpbig.assign(d->lev_xp_big, d->lev_xp_big + nl);
+  for (int64_t q = 0; q < d->pt_ptr[nl]; ++q)   // k_fi_panel: one thread per tile column
+    if (d->pt_c1[q] - d->pt_c0[q] > 256) return fail(HY_INVALID_ARGUMENT, "panel tile wider than 256");
   D.up_part = nullptr; D.part_first = nullptr; D.part_n = nullptr; D.part_off = nullptr;
   D.part_scr = nullptr; D.part_cnt = nullptr;
   if (d->nparts > 0) {

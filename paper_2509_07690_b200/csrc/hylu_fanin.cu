@@ -198,14 +198,14 @@ __global__ void __launch_bounds__(FI_THREADS) k_fi_panel(DevSym S, CallP P, Fani
   }
   __syncthreads();
   if (panel) {
-    for (int t = 0; t + 1 < s; ++t) {
-      const int rem = s - t - 1;
-      for (int idx = tid; idx < rem * tw; idx += FI_THREADS) {
-        const int q = t + 1 + idx / tw, c = idx % tw;
-        tl[q * tw + c] -= Lb[q * FXLD + t] * tl[t * tw + c];
+    // unit-lower TRSM, one thread per column (tw <= FI_THREADS): no barriers, the
+    // per-element update sequence (ascending t) is unchanged
+    if (tid < tw)
+      for (int t = 0; t + 1 < s; ++t) {
+        const double xt = tl[t * tw + tid];
+        for (int q = t + 1; q < s; ++q) tl[q * tw + tid] -= Lb[q * FXLD + t] * xt;
       }
-      __syncthreads();
-    }
+    __syncthreads();
   }
   for (int idx = tid; idx < s * tw; idx += FI_THREADS) {
     const int t = idx / tw, c = idx - t * tw;
