@@ -135,21 +135,27 @@ __global__ void __launch_bounds__(FI_THREADS) k_fi_lu(DevSym S, CallP P, FaninDe
         }
       }
     }
-    __syncthreads();
-    if (tid == 0) {
-      const double piv = B[t * FXLD + t];
-      bool fired;
-      B[t * FXLD + t] = perturb(piv, thr, fired);
-      log_pivot(P, r + t, piv, fired, thr);
+    // warp 0 (after its own pivot search and swap): perturb the pivot and scale
+    // the column, then one barrier; the rank-1 update runs column-per-thread
+    // (column tid&63, rows strided by 4), then the second barrier of the step
+    if (warp == 0) {
+      __syncwarp();
+      double pv = B[t * FXLD + t];
+      if (lane == 0) {
+        bool fired;
+        const double piv = pv;
+        pv = perturb(piv, thr, fired);
+        B[t * FXLD + t] = pv;
+        log_pivot(P, r + t, piv, fired, thr);
+      }
+      pv = __shfl_sync(HY_FULL, pv, 0);
+      for (int q = t + 1 + lane; q < s; q += 32) B[q * FXLD + t] /= pv;
     }
     __syncthreads();
-    const double pv = B[t * FXLD + t];
-    for (int q = t + 1 + tid; q < s; q += FI_THREADS) B[q * FXLD + t] /= pv;
-    __syncthreads();
-    const int rem = s - t - 1;
-    for (int idx = tid; idx < rem * rem; idx += FI_THREADS) {
-      const int q = t + 1 + idx / rem, c = t + 1 + idx % rem;
-      B[q * FXLD + c] -= B[q * FXLD + t] * B[t * FXLD + c];
+    const int c = tid & 63;
+    if (c > t && c < s) {
+      const double ut = B[t * FXLD + c];
+      for (int q = t + 1 + (tid >> 6); q < s; q += FI_THREADS / 64) B[q * FXLD + c] -= B[q * FXLD + t] * ut;
     }
     __syncthreads();
   }
