@@ -195,6 +195,7 @@ struct hy_handle {
   int nowait = 0;                          // timing experiment only: skip dependency waits
   int pair = 1;                            // pipeline: one warp per (node, group pair)
   int prefetch = 512;                      // pair mode: L2-prefetch the matrix values this many tasks ahead
+  int warp_min = 256;                      // fan-in: below this many small items per level, CTA kernels only
   int bwd_pair = 1;                        // backward solve: one warp per (node, group pair)
   int hub_df = 0;                          // hub kernel: dataflow phase for split-free leading levels
   int pipe_ws = 16;                        // pair-mode shared workspace columns per group
@@ -513,6 +514,10 @@ int hy_set_option(hy_handle *h, const char *name, int64_t value) {
     h->pipe_blocks = 0;
     return HY_OK;
   }
+  if (std::string(name) == "fanin_warp_min" && value >= 1) {
+    h->warp_min = (int)value;
+    return HY_OK;
+  }
   if (std::string(name) == "bwd_pair") {
     h->bwd_pair = value != 0;
     return HY_OK;
@@ -811,8 +816,6 @@ int hy_upload_fanin_plan(hy_handle *h, const hy_fanin_plan *d) {
   return HY_OK;
 }
 
-// below this many warp-eligible items a level's small items go to the CTA kernels
-constexpr int WARP_MIN_ITEMS = 256;
 
 static int run_fanin(hy_handle *h, const CallP &P, cudaStream_t st) {
   CK(cudaMemsetAsync(P.F, 0, sizeof(double) * h->stored, st));
@@ -846,7 +849,7 @@ static int run_fanin(hy_handle *h, const CallP &P, cudaStream_t st) {
     }
     if (nxp) {
       // few small items: one CTA launch for the whole level (it handles any size)
-      const int xb = (int)h->fi_xpbig[l] - (int)h->fi_xp[l] < WARP_MIN_ITEMS ? (int)h->fi_xp[l] : (int)h->fi_xpbig[l];
+      const int xb = (int)h->fi_xpbig[l] - (int)h->fi_xp[l] < h->warp_min ? (int)h->fi_xp[l] : (int)h->fi_xpbig[l];
       const int nw = xb - (int)h->fi_xp[l], nc = (int)h->fi_xp[l + 1] - xb;
       if (nw) {
         k_fi_x_w<<<(nw + 7) / 8, 256, 0, st>>>(h->S, P, h->fi, (int)h->fi_xp[l], nw);
@@ -867,7 +870,7 @@ static int run_fanin(hy_handle *h, const CallP &P, cudaStream_t st) {
         k_fi_upd_pk<<<npk, 256, sm, st>>>(h->S, P, h->fi, (int)h->fi_up[l], h->fi_smax[l], h->fi_mmax[l]);
         h->launches++;
       }
-      const int rs = (int)h->fi_uprs[l] - reg < WARP_MIN_ITEMS ? reg : (int)h->fi_uprs[l];
+      const int rs = (int)h->fi_uprs[l] - reg < h->warp_min ? reg : (int)h->fi_uprs[l];
       if (rs > reg) {
         k_fi_upd_w<<<(rs - reg + 7) / 8, 256, 0, st>>>(h->S, P, h->fi, reg, rs - reg);
         h->launches++;

@@ -147,3 +147,25 @@ def test_rowrow_on_fanin_path(name, monkeypatch):
     assert _rel(f.host_values(), ref.values) <= LU_RTOL
     x, _ = api.solve(p.A, f, b=p.b)
     assert np.linalg.norm(refmatrix.spmv(p.A, x) - p.b) / np.linalg.norm(p.b) <= RES_TOL
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c0"])
+def test_fanin_warp_kernels_and_split_k(name, monkeypatch):
+    """Every small multiplier block / small-target update on the warp-per-item
+    kernels (threshold forced to 1) and heavy packed items split-K at a low
+    threshold: factors still match the oracle."""
+    from paper_2509_07690_b200 import schedule
+    monkeypatch.setenv("HYLU_OPTIONS", "fanin_warp_min=1")
+    monkeypatch.setattr(schedule, "SPLIT_SRC", 2)
+    monkeypatch.setattr(schedule, "SPLIT_REL", 1.0)
+    p, an = _analysis(name, None)
+    plan = schedule.build_fanin_plan(an.symbolic)
+    an.symbolic._fanin_plan = plan
+    assert len(plan.part_n) > 0
+    on = _oracle()
+    ref = on.factorize(an)
+    f = api.factorize_analysis(an)
+    assert np.array_equal(f.host_inner_perm(), ref.inner_perm)
+    assert _rel(f.host_values(), ref.values) <= LU_RTOL
+    x, _ = api.solve(p.A, f, b=p.b)
+    assert np.linalg.norm(refmatrix.spmv(p.A, x) - p.b) / np.linalg.norm(p.b) <= RES_TOL
