@@ -600,6 +600,45 @@ __global__ void k_solve_part(DevSym S, const double *F, const SolveChunk *ch, in
 }
 
 // forward finish: y_t = y_t - sum(chunk partials) - sum_{tt<t} L[t][tt] y_tt
+// Off-block dot products of a small node's rows (columns [lo, hi) of each row)
+// against the solution vector, done by one warp: per 128-column block the gathered
+// solution values are loaded once (lanes over columns) and reused by every row;
+// two rows per step, each reduced across the warp and subtracted from the lane
+// that owns the row (row t lives on lane t&31, in mine0 for t < 32 else mine1).
+__device__ __forceinline__ void offblock_dots(const double *Fu, int W, const int32_t *cc,
+                                              const double *y, int lo, int hi, int s, int lane,
+                                              double &mine0, double &mine1) {
+  for (int q0 = lo; q0 < hi; q0 += 128) {
+    double yv[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int q = q0 + lane + 32 * k;
+      yv[k] = q < hi ? y[cc[q]] : 0.0;
+    }
+    for (int t = 0; t < s; t += 2) {
+      const double *ra = Fu + (int64_t)t * W;
+      const bool two = t + 1 < s;
+      double a = 0.0, b = 0.0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int q = q0 + lane + 32 * k;
+        if (q < hi) {
+          a += ra[q] * yv[k];
+          if (two) b += ra[W + q] * yv[k];
+        }
+      }
+      a = warp_sum(a);
+      b = warp_sum(b);
+      if (lane == (t & 31)) {
+        if (t < 32) mine0 -= a; else mine1 -= a;
+      }
+      if (two && lane == ((t + 1) & 31)) {
+        if (t + 1 < 32) mine0 -= b; else mine1 -= b;
+      }
+    }
+  }
+}
+
 __global__ void k_fwd_fin(DevSym S, const double *F, const int32_t *nodes, const int32_t *slot0,
                           const int32_t *nslot, int count, const double *scratch, double *y) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -623,19 +662,8 @@ __global__ void k_fwd_fin(DevSym S, const double *F, const int32_t *nodes, const
     for (int k = 0; k < an; ++k) acc -= scratch[(int64_t)(a0 + k) * 64 + lane + 32];
     mine1 = acc;
   }
-  if (an == 0 && L > 0) {
-    // small node: the warp computes the off-block dot products itself
-    const int32_t *cc = S.cols + S.colptr[u];
-    for (int t = 0; t < s; ++t) {
-      const double *row = Fu + (int64_t)t * W;
-      double acc = 0.0;
-      for (int q = lane; q < L; q += 32) acc += row[q] * y[cc[q]];
-      acc = warp_sum(acc);
-      if (lane == (t & 31)) {
-        if (t < 32) mine0 -= acc; else mine1 -= acc;
-      }
-    }
-  }
+  if (an == 0 && L > 0)   // small node: the warp computes the off-block dot products itself
+    offblock_dots(Fu, W, S.cols + S.colptr[u], y, 0, L, s, lane, mine0, mine1);
   for (int tt = 0; tt < s; ++tt) {
     const double ytt = __shfl_sync(HY_FULL, tt < 32 ? mine0 : mine1, tt & 31);
     const int t0 = lane, t1 = lane + 32;
@@ -670,18 +698,8 @@ __global__ void k_bwd_fin(DevSym S, const double *F, const int32_t *nodes, const
     for (int k = 0; k < an; ++k) acc -= scratch[(int64_t)(a0 + k) * 64 + lane + 32];
     mine1 = acc;
   }
-  if (an == 0 && L + s < W) {
-    const int32_t *cc = S.cols + S.colptr[u];
-    for (int t = 0; t < s; ++t) {
-      const double *row = Fu + (int64_t)t * W;
-      double acc = 0.0;
-      for (int q = L + s + lane; q < W; q += 32) acc += row[q] * y[cc[q]];
-      acc = warp_sum(acc);
-      if (lane == (t & 31)) {
-        if (t < 32) mine0 -= acc; else mine1 -= acc;
-      }
-    }
-  }
+  if (an == 0 && L + s < W)
+    offblock_dots(Fu, W, S.cols + S.colptr[u], y, L + s, W, s, lane, mine0, mine1);
   for (int tt = s - 1; tt >= 0; --tt) {
     const double d = Fu[(int64_t)tt * W + L + tt];
     if (lane == (tt & 31)) {
