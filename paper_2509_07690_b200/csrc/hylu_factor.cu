@@ -451,11 +451,26 @@ __global__ void k_fwd(DevSym S, const double *F, const int32_t *nodes, int count
     }
   }
   // in-block: y_t -= sum_{tt<t} L[t][tt] y_tt
-  for (int tt = 0; tt < s; ++tt) {
-    const double ytt = __shfl_sync(HY_FULL, tt < 32 ? mine0 : mine1, tt & 31);
-    const int t0 = lane, t1 = lane + 32;
-    if (t0 > tt && t0 < s) mine0 -= Fu[(int64_t)t0 * W + L + tt] * ytt;
-    if (t1 > tt && t1 < s) mine1 -= Fu[(int64_t)t1 * W + L + tt] * ytt;
+  // in-block unit-lower solve; each lane's block-row entries are loaded 8 columns
+  // at a time (all in flight together) instead of one dependent load per step
+  const int t0 = lane, t1 = lane + 32;
+  for (int b0 = 0; b0 < s; b0 += 8) {
+    double e0[8], e1[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int tt = b0 + k;
+      e0[k] = (tt < s && t0 > tt && t0 < s) ? Fu[(int64_t)t0 * W + L + tt] : 0.0;
+      e1[k] = (tt < s && t1 > tt && t1 < s) ? Fu[(int64_t)t1 * W + L + tt] : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int tt = b0 + k;
+      if (tt < s) {
+        const double ytt = __shfl_sync(HY_FULL, tt < 32 ? mine0 : mine1, tt & 31);
+        if (t0 > tt && t0 < s) mine0 -= e0[k] * ytt;
+        if (t1 > tt && t1 < s) mine1 -= e1[k] * ytt;
+      }
+    }
   }
   if (lane < s) y[r + lane] = mine0;
   if (lane + 32 < s) y[r + lane + 32] = mine1;
@@ -664,11 +679,26 @@ __global__ void k_fwd_fin(DevSym S, const double *F, const int32_t *nodes, const
   }
   if (an == 0 && L > 0)   // small node: the warp computes the off-block dot products itself
     offblock_dots(Fu, W, S.cols + S.colptr[u], y, 0, L, s, lane, mine0, mine1);
-  for (int tt = 0; tt < s; ++tt) {
-    const double ytt = __shfl_sync(HY_FULL, tt < 32 ? mine0 : mine1, tt & 31);
-    const int t0 = lane, t1 = lane + 32;
-    if (t0 > tt && t0 < s) mine0 -= Fu[(int64_t)t0 * W + L + tt] * ytt;
-    if (t1 > tt && t1 < s) mine1 -= Fu[(int64_t)t1 * W + L + tt] * ytt;
+  // in-block unit-lower solve; each lane's block-row entries are loaded 8 columns
+  // at a time (all in flight together) instead of one dependent load per step
+  const int t0 = lane, t1 = lane + 32;
+  for (int b0 = 0; b0 < s; b0 += 8) {
+    double e0[8], e1[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int tt = b0 + k;
+      e0[k] = (tt < s && t0 > tt && t0 < s) ? Fu[(int64_t)t0 * W + L + tt] : 0.0;
+      e1[k] = (tt < s && t1 > tt && t1 < s) ? Fu[(int64_t)t1 * W + L + tt] : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int tt = b0 + k;
+      if (tt < s) {
+        const double ytt = __shfl_sync(HY_FULL, tt < 32 ? mine0 : mine1, tt & 31);
+        if (t0 > tt && t0 < s) mine0 -= e0[k] * ytt;
+        if (t1 > tt && t1 < s) mine1 -= e1[k] * ytt;
+      }
+    }
   }
   if (lane < s) y[r + lane] = mine0;
   if (lane + 32 < s) y[r + lane + 32] = mine1;
@@ -700,15 +730,29 @@ __global__ void k_bwd_fin(DevSym S, const double *F, const int32_t *nodes, const
   }
   if (an == 0 && L + s < W)
     offblock_dots(Fu, W, S.cols + S.colptr[u], y, L + s, W, s, lane, mine0, mine1);
-  for (int tt = s - 1; tt >= 0; --tt) {
-    const double d = Fu[(int64_t)tt * W + L + tt];
-    if (lane == (tt & 31)) {
-      if (tt < 32) mine0 /= d; else mine1 /= d;
+  // in-block upper solve (descending), entries loaded 8 columns at a time; the
+  // diagonal entry of row tt is in its own lane's block (k = tt - b0)
+  const int t0 = lane, t1 = lane + 32;
+  for (int b0 = ((s - 1) / 8) * 8; b0 >= 0; b0 -= 8) {
+    double e0[8], e1[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int tt = b0 + k;
+      e0[k] = (tt < s && t0 <= tt) ? Fu[(int64_t)t0 * W + L + tt] : 0.0;
+      e1[k] = (tt < s && t1 <= tt) ? Fu[(int64_t)t1 * W + L + tt] : 0.0;
     }
-    const double ztt = __shfl_sync(HY_FULL, tt < 32 ? mine0 : mine1, tt & 31);
-    const int t0 = lane, t1 = lane + 32;
-    if (t0 < tt) mine0 -= Fu[(int64_t)t0 * W + L + tt] * ztt;
-    if (t1 < tt) mine1 -= Fu[(int64_t)t1 * W + L + tt] * ztt;
+#pragma unroll
+    for (int k = 7; k >= 0; --k) {
+      const int tt = b0 + k;
+      if (tt < s) {
+        if (lane == (tt & 31)) {
+          if (tt < 32) mine0 /= e0[k]; else mine1 /= e1[k];
+        }
+        const double ztt = __shfl_sync(HY_FULL, tt < 32 ? mine0 : mine1, tt & 31);
+        if (t0 < tt) mine0 -= e0[k] * ztt;
+        if (t1 < tt) mine1 -= e1[k] * ztt;
+      }
+    }
   }
   if (lane < s) y[r + lane] = mine0;
   if (lane + 32 < s) y[r + lane + 32] = mine1;
