@@ -606,7 +606,7 @@ int hy_upload_symbolic(hy_handle *h, const hy_symbolic_desc *d) {
   if (rc) return rc;
   {
     // chunked substitution plans (forward: L part [0, L); backward: panel [L+s, W))
-    const int CH = 512;
+    const int CH = 512;   // k_solve_part holds a chunk's gathered values in 16 registers per lane
     for (int dir = 0; dir < 2; ++dir) {
       const int64_t *lp = dir == 0 ? d->level_ptr : d->ulevel_ptr;
       const int32_t *ln = dir == 0 ? d->level_nodes : d->ulevel_nodes;

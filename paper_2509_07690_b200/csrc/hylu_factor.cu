@@ -605,12 +605,32 @@ __global__ void k_solve_part(DevSym S, const double *F, const SolveChunk *ch, in
   const double *Fu = F + S.valoff[u];
   const int32_t *cc = S.cols + cp;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int t = warp; t < s; t += nw) {
-    const double *row = Fu + (int64_t)t * W;
-    double acc = 0.0;
-    for (int q = c.c0 + lane; q < c.c1; q += 32) acc += row[q] * y[cc[q]];
-    acc = warp_sum(acc);
-    if (lane == 0) scratch[(int64_t)c.slot * 64 + t] = acc;
+  // the chunk's (<= 512) gathered solution values, once per warp (lanes over
+  // columns), reused by every row; two rows per reduction
+  double yv[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    const int q = c.c0 + lane + 32 * k;
+    yv[k] = q < c.c1 ? y[cc[q]] : 0.0;
+  }
+  for (int t = 2 * warp; t < s; t += 2 * nw) {
+    const double *ra = Fu + (int64_t)t * W;
+    const bool two = t + 1 < s;
+    double a = 0.0, b = 0.0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const int q = c.c0 + lane + 32 * k;
+      if (q < c.c1) {
+        a += ra[q] * yv[k];
+        if (two) b += ra[W + q] * yv[k];
+      }
+    }
+    a = warp_sum(a);
+    b = warp_sum(b);
+    if (lane == 0) {
+      scratch[(int64_t)c.slot * 64 + t] = a;
+      if (two) scratch[(int64_t)c.slot * 64 + t + 1] = b;
+    }
   }
 }
 
