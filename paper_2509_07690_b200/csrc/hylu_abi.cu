@@ -625,7 +625,8 @@ int hy_upload_symbolic(hy_handle *h, const hy_symbolic_desc *d) {
           const int64_t lo = dir == 0 ? 0 : d->nl[u] + s, hi = dir == 0 ? d->nl[u] : W;
           slot0.push_back(slot);
           int32_t ns = 0;
-          const bool direct = (hi - lo) * s <= 8192;   // small: the finish warp does it
+          // small: the finish warp does it (one warp walks at most 512 off-block columns)
+          const bool direct = (hi - lo) * s <= 8192 && hi - lo <= 512;
           for (int64_t c = lo; c < hi && !direct; c += CH) {
             chunks.push_back(SolveChunk{u, (int32_t)c, (int32_t)(c + CH < hi ? c + CH : hi), slot + ns});
             ++ns;
