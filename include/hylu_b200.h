@@ -11,6 +11,9 @@
  *   hy_refactorize                <- refactorize(A_new, prior, opts)
  *   hy_solve                      <- solve(A, factors, ps, ord, b) w/o refinement
  *                                    (forward/backward substitution)
+ *   hy_upload_matrix, hy_residual, hy_axpy
+ *                                 <- iterative_refinement's r = b - A x, backward_error
+ *                                    and x += d (matrix.py:258-310)
  *   hy_refactorize_solve_batched  <- B x [refactorize -> solve] sharing one symbolic
  *                                    (BASELINE config 4; SURVEY §3 call stack 3)
  *
@@ -112,6 +115,17 @@ int hy_refactorize(hy_handle *h, const double *d_avals, double eps, const hy_fac
                    hy_factors *out, uintptr_t stream);
 int hy_solve(hy_handle *h, const hy_factors *f, const double *d_b, double *d_x,
              uintptr_t stream);
+
+/* Iterative refinement on the device.  hy_upload_matrix: A's
+ * pattern in original coordinates (SparseMatrixCSR row_ptr / col_idx,
+ * matrix.py:30-66), once per analysis.  hy_residual: d_r = b - A x (d_r may be
+ * NULL) and *d_berr = max_i |b - Ax|_i / (|A||x| + |b|)_i with 0/0 = 0
+ * (backward_error, matrix.py:267-285, 303-310), bitwise the reference's row loops
+ * (index order, no fused multiply-add).  hy_axpy: x += dx elementwise. */
+int hy_upload_matrix(hy_handle *h, const int64_t *row_ptr, const int32_t *col_idx);
+int hy_residual(hy_handle *h, const double *d_avals, const double *d_x, const double *d_b,
+                double *d_r, double *d_berr, uintptr_t stream);
+int hy_axpy(hy_handle *h, double *d_x, const double *d_dx, uintptr_t stream);
 
 /* Column-slab plan for supernode targets (schedule.build_slab_plan): one CTA per
  * slab, slabs grouped by factorization level.  Optional: without it supernodes

@@ -23,7 +23,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import preprocess as _pp
-from ._ref import KernelMode, SolverConfig, errors, matrix as _refmatrix
+from ._ref import KernelMode, SolverConfig, errors
 from .analysis import Analysis, analyze, value_map
 from .symbolic import SymbolicStructure, symbolic_from_pattern
 
@@ -218,32 +218,77 @@ def substitute(factors, b, stream=None):
 
 def solve(A, factors, ps=None, order=None, b=None, threads=1, config=None):
     """SPEC.md:489-497 (+ automatic iterative_refinement when perturbation fired,
-    SPEC.md:499-507; residual and backward error in original coordinates)."""
+    SPEC.md:499-507, on the device: residual and backward error in original
+    coordinates, bitwise the reference's matrix.py row loops)."""
+    import torch
     b = np.ascontiguousarray(b, np.float64)
     if b.shape != (A.n,):
         raise errors.DimensionMismatch("b must have length %d" % A.n)
-    x = substitute(factors, b).cpu().numpy()
+    ctx = factors._ctx
+    d_b = torch.from_numpy(b.copy()).to(ctx.device)
+    d_x = substitute(factors, d_b)
     report = RefinementReport()
     if factors.perturbed:
-        cfg = config or SolverConfig()
-        errs = [_refmatrix.backward_error(A, x, b)]
-        it = 0
-        converged = errs[-1] <= cfg.refine_tolerance
-        while not converged and it < cfg.max_refine_iters:
-            r = b - _refmatrix.spmv(A, x)
-            xn = x + substitute(factors, r).cpu().numpy()
-            e = _refmatrix.backward_error(A, xn, b)
-            it += 1
-            if e > cfg.refine_stagnation_factor * errs[-1]:
-                if e < errs[-1]:
-                    x = xn
-                    errs.append(e)
-                break
-            x = xn
-            errs.append(e)
-            converged = e <= cfg.refine_tolerance
-        report = RefinementReport(it, errs, bool(converged))
-    return x, report
+        d_x, report = iterative_refinement(A, factors, d_b, d_x, config)
+    return d_x.cpu().numpy(), report
+
+
+def backward_error(A, factors, x, b):
+    """Componentwise backward error (matrix.py:303-310) computed on the device."""
+    import torch
+    from .device import check
+    ctx = factors._ctx
+    ctx.ensure_matrix(A)
+    dev = ctx.device
+    d_a = torch.from_numpy(np.array(A.values, np.float64, copy=True)).to(dev)
+    d_x = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.array(x, np.float64, copy=True)).to(dev)
+    d_b = b if isinstance(b, torch.Tensor) else torch.from_numpy(np.array(b, np.float64, copy=True)).to(dev)
+    berr = torch.zeros(1, dtype=torch.float64, device=dev)
+    check(ctx.lib.hy_residual(ctx.h, d_a.data_ptr(), d_x.data_ptr(), d_b.data_ptr(), None,
+                              berr.data_ptr(), ctx.stream_handle(None)))
+    return float(berr.item())
+
+
+def iterative_refinement(A, factors, d_b, d_x, config=None):
+    """SPEC.md:499-507 on the device: r = b - A x, stop at backward error <=
+    refine_tolerance, after max_refine_iters, or when the error fails to drop by
+    refine_stagnation_factor; else x += solve(r).  One fused residual/backward-error
+    pass per iteration; only the scalar backward error crosses to the host."""
+    import torch
+    from .device import check
+    cfg = config or SolverConfig()
+    ctx = factors._ctx
+    ctx.ensure_matrix(A)
+    dev = ctx.device
+    sh = ctx.stream_handle(None)
+    d_a = torch.from_numpy(np.array(A.values, np.float64, copy=True)).to(dev)
+    r = torch.empty_like(d_x)
+    berr = torch.zeros(1, dtype=torch.float64, device=dev)
+
+    def resid(x):
+        check(ctx.lib.hy_residual(ctx.h, d_a.data_ptr(), x.data_ptr(), d_b.data_ptr(), r.data_ptr(),
+                                  berr.data_ptr(), sh))
+        return float(berr.item())
+
+    x = d_x
+    errs = [resid(x)]
+    it = 0
+    converged = errs[-1] <= cfg.refine_tolerance
+    while not converged and it < cfg.max_refine_iters:
+        dx = substitute(factors, r)
+        xn = x.clone()
+        check(ctx.lib.hy_axpy(ctx.h, xn.data_ptr(), dx.data_ptr(), sh))
+        e = resid(xn)
+        it += 1
+        if e > cfg.refine_stagnation_factor * errs[-1]:
+            if e < errs[-1]:
+                x = xn
+                errs.append(e)
+            break
+        x = xn
+        errs.append(e)
+        converged = e <= cfg.refine_tolerance
+    return x, RefinementReport(it, errs, bool(converged))
 
 
 class BatchedRefactorizer:

@@ -57,6 +57,9 @@ struct FaninDev {
   int *part_cnt;
 };
 __global__ void k_fi_scatter(DevSym, CallP);
+__global__ void k_resid_berr(int, const int64_t *, const int32_t *, const double *, const double *,
+                             const double *, double *, unsigned long long *);
+__global__ void k_axpy1(int, double *, const double *);
 
 __global__ void k_fi_lu(DevSym, CallP, FaninDev, int);
 __global__ void k_fi_panel(DevSym, CallP, FaninDev, int);
@@ -235,6 +238,8 @@ struct hy_handle {
   std::vector<int64_t> fi_xpbig;                     // per level: first CTA-per-item multiplier item
   std::vector<int64_t> fi_hub;                       // per level: offsets of pull-program rows
   int32_t *d_fi_hubs = nullptr;
+  int64_t *d_arow = nullptr;   // A's pattern in original coordinates (refinement)
+  int32_t *d_acol = nullptr;
   int fi_v3 = 0;                                     // option "fanin_v3" (slower; kept for experiments)
   int fi_mma = 0;                                    // option "fanin_dmma" (bitwise-equal results; slower here)
   std::vector<int32_t> fi_smax, fi_mmax;
@@ -470,6 +475,8 @@ void hy_destroy(hy_handle *h) {
   free_segments(h);
   if (h->d_counters) cudaFree(h->d_counters);
   if (h->d_by) cudaFree(h->d_by);
+  if (h->d_arow) cudaFree(h->d_arow);
+  if (h->d_acol) cudaFree(h->d_acol);
   delete h;
 }
 
@@ -1045,6 +1052,50 @@ int hy_refactorize(hy_handle *h, const double *d_avals, double eps, const hy_fac
   if (!prior || !prior->d_inner_perm || !prior->d_anorm)
     return fail(HY_INVALID_ARGUMENT, "refactorize needs prior factors");
   return run_factor(h, d_avals, eps, prior, out, (cudaStream_t)stream);
+}
+
+
+int hy_upload_matrix(hy_handle *h, const int64_t *row_ptr, const int32_t *col_idx) {
+  if (!h || !h->uploaded || !row_ptr || !col_idx) return fail(HY_INVALID_ARGUMENT, "null handle/arrays");
+  const int64_t n = h->S.n;
+  if (row_ptr[0] != 0 || row_ptr[n] != h->S.nnz) return fail(HY_DIMENSION_MISMATCH, "row_ptr does not match nnz");
+  CK(cudaSetDevice(h->device));
+  if (h->d_arow) CK(cudaFree(h->d_arow));
+  if (h->d_acol) CK(cudaFree(h->d_acol));
+  h->d_arow = nullptr;
+  h->d_acol = nullptr;
+  CK(cudaMalloc((void **)&h->d_arow, sizeof(int64_t) * (n + 1)));
+  CK(cudaMalloc((void **)&h->d_acol, sizeof(int32_t) * (h->S.nnz > 0 ? h->S.nnz : 1)));
+  CK(cudaMemcpy(h->d_arow, row_ptr, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice));
+  if (h->S.nnz > 0)
+    CK(cudaMemcpy(h->d_acol, col_idx, sizeof(int32_t) * h->S.nnz, cudaMemcpyHostToDevice));
+  return HY_OK;
+}
+
+int hy_residual(hy_handle *h, const double *d_avals, const double *d_x, const double *d_b, double *d_r,
+                double *d_berr, uintptr_t stream) {
+  if (!h || !h->d_arow) return fail(HY_INVALID_ARGUMENT, "matrix pattern not uploaded");
+  if (!d_avals || !d_x || !d_b || !d_berr) return fail(HY_INVALID_ARGUMENT, "null buffer");
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaMemsetAsync(d_berr, 0, sizeof(double), st));
+  const int n = h->S.n;
+  const int grid = (n + 255) / 256 < h->sm_count * 8 ? (n + 255) / 256 : h->sm_count * 8;
+  k_resid_berr<<<grid > 0 ? grid : 1, 256, 0, st>>>(n, h->d_arow, h->d_acol, d_avals, d_x, d_b, d_r,
+                                                    reinterpret_cast<unsigned long long *>(d_berr));
+  h->launches++;
+  CK(cudaGetLastError());
+  return HY_OK;
+}
+
+int hy_axpy(hy_handle *h, double *d_x, const double *d_dx, uintptr_t stream) {
+  if (!h || !d_x || !d_dx) return fail(HY_INVALID_ARGUMENT, "null buffer");
+  CK(cudaSetDevice(h->device));
+  const int n = h->S.n;
+  k_axpy1<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(n, d_x, d_dx);
+  h->launches++;
+  CK(cudaGetLastError());
+  return HY_OK;
 }
 
 int hy_solve(hy_handle *h, const hy_factors *f, const double *d_b, double *d_x, uintptr_t stream) {

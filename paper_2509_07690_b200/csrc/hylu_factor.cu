@@ -778,4 +778,45 @@ __global__ void k_bwd_fin(DevSym S, const double *F, const int32_t *nodes, const
   if (lane + 32 < s) y[r + lane + 32] = mine1;
 }
 
+
+// ---------------------------------------------------------------------------
+// Residual and componentwise backward error in original coordinates
+// (matrix.py:258-285; "r = b − A·x ... full precision"): thread
+// per row, the row's entries in index order with separately rounded products and
+// sums (no fused multiply-add), exactly as the reference's row loops — so both
+// the residual and the backward error are bitwise the reference's for the same
+// x.  max over rows through an integer atomicMax on the (non-negative) bits.
+__global__ void k_resid_berr(int n, const int64_t *row_ptr, const int32_t *col_idx,
+                             const double *vals, const double *x, const double *b, double *r,
+                             unsigned long long *berr_bits) {
+  double worst = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double acc = 0.0, mag = 0.0;
+    for (int64_t t = row_ptr[i]; t < row_ptr[i + 1]; ++t) {
+      const double v = vals[t];
+      const double xa = x[col_idx[t]];
+      acc = __dadd_rn(acc, __dmul_rn(v, xa));
+      mag = __dadd_rn(mag, __dmul_rn(fabs(v), fabs(xa)));
+    }
+    const double bi = b[i];
+    if (r) r[i] = __dsub_rn(bi, acc);
+    const double num = fabs(__dsub_rn(bi, acc));
+    const double den = __dadd_rn(mag, fabs(bi));
+    if (den != 0.0) {
+      const double rel = __ddiv_rn(num, den);
+      if (rel > worst) worst = rel;
+    }
+  }
+  // warp max, then one atomic per warp (non-negative doubles order as their bits)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) worst = fmax(worst, __shfl_xor_sync(HY_FULL, worst, o));
+  if ((threadIdx.x & 31) == 0 && worst > 0.0)
+    atomicMax(berr_bits, (unsigned long long)__double_as_longlong(worst));
+}
+
+// x += dx (the refinement update, elementwise as numpy)
+__global__ void k_axpy1(int n, double *x, const double *dx) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    x[i] = __dadd_rn(x[i], dx[i]);
+}
 }  // namespace hy

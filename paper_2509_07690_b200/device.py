@@ -128,6 +128,9 @@ def library():
     lib.hy_refactorize.argtypes = [vp, vp, ctypes.c_double, ctypes.POINTER(FactorsDesc),
                                    ctypes.POINTER(FactorsDesc), u]
     lib.hy_solve.argtypes = [vp, ctypes.POINTER(FactorsDesc), vp, vp, u]
+    lib.hy_upload_matrix.argtypes = [vp, vp, vp]
+    lib.hy_residual.argtypes = [vp, vp, vp, vp, vp, vp, u]
+    lib.hy_axpy.argtypes = [vp, vp, vp, u]
     lib.hy_refactorize_solve_batched.argtypes = [vp, i64, vp, vp, vp, ctypes.c_double,
                                                  ctypes.POINTER(FactorsDesc), vp, u]
     lib.hy_refactorize_batched.argtypes = [vp, i64, vp, ctypes.c_double,
@@ -363,6 +366,21 @@ class DeviceContext:
             check(fn(self.h, ctypes.byref(d)))
         self._programs = getattr(self, "_programs", [])
         self._programs.append(arrs)
+
+    def ensure_matrix(self, A):
+        """Upload A's pattern (original coordinates) for device refinement, once.
+        The pattern must be the analysed one (SPEC.md:343 same-pattern contract)."""
+        if getattr(self, "_matrix_uploaded", False):
+            return
+        A0 = self.analysis.A
+        if A.n != A0.n or A.nnz != A0.nnz or not np.array_equal(A.row_ptr, A0.row_ptr) or \
+                not np.array_equal(A.col_idx, A0.col_idx):
+            raise errors.PatternMismatch("refinement matrix pattern differs from the analysed one")
+        rp = np.ascontiguousarray(A.row_ptr, np.int64)
+        ci = np.ascontiguousarray(A.col_idx, np.int32)
+        with self.torch.cuda.device(self.device):
+            check(self.lib.hy_upload_matrix(self.h, rp.ctypes.data, ci.ctypes.data))
+        self._matrix_uploaded = True
 
     def set_option(self, name, value):
         check(self.lib.hy_set_option(self.h, name.encode(), int(value)))

@@ -169,3 +169,66 @@ def test_fanin_warp_kernels_and_split_k(name, monkeypatch):
     assert _rel(f.host_values(), ref.values) <= LU_RTOL
     x, _ = api.solve(p.A, f, b=p.b)
     assert np.linalg.norm(refmatrix.spmv(p.A, x) - p.b) / np.linalg.norm(p.b) <= RES_TOL
+
+
+@pytest.mark.parametrize("name", ["c0", "c1", "c3"])
+def test_device_backward_error_is_the_references(name):
+    """hy_residual reproduces matrix.py's backward_error bit for bit."""
+    p, an = _analysis(name, None)
+    f = api.factorize_analysis(an)
+    x, _ = api.solve(p.A, f, b=p.b)
+    rng = np.random.default_rng(7)
+    for xx in (x, x * (1 + 1e-9 * rng.standard_normal(x.shape)), np.zeros_like(x)):
+        assert api.backward_error(p.A, f, xx, p.b) == refmatrix.backward_error(p.A, xx, p.b)
+
+
+def _perturbed_case():
+    """c0 small refactorized with the M diagonal of a few rows without L entries
+    (first pivots of their elimination) set to ~0: the prior pivoting and scaling
+    are reused, so those pivots are tiny, perturbation fires and the
+    solve refines."""
+    p, an = _analysis("c0", None)
+    f0 = api.factorize_analysis(an)
+    s = an.symbolic
+    ps, order = an.pivot_scale, an.ordering
+    rows = [int(s.node_first[u]) for u in range(s.nnodes)
+            if s.node_kind[u] == 0 and s.nl[u] == 0][:3]
+    assert rows
+    v = np.array(p.A.values)
+    rp, ci = p.A.row_ptr, p.A.col_idx
+    for k in rows:
+        c = int(order.perm[k])                       # column of M's pivot k
+        r = int(ps.row_perm[c])                      # original row matched to it
+        d = rp[r] + int(np.flatnonzero(ci[rp[r]:rp[r + 1]] == c)[0])
+        v[d] = 1e-300
+    A = p.A.with_values(v)
+    f = api.refactorize(A, f0)
+    return A, f, np.asarray(p.b)
+
+
+def test_device_refinement_matches_host_loop():
+    """The device refinement loop takes the same steps as the
+    host formulation with the reference's spmv / backward_error: same iteration
+    count, bitwise-equal backward errors and solution."""
+    A, f, b = _perturbed_case()
+    assert f.perturbed
+    x, rep = api.solve(A, f, b=b)
+    cfg = SolverConfig()
+    xh = api.substitute(f, b).cpu().numpy()
+    errs = [refmatrix.backward_error(A, xh, b)]
+    it, conv = 0, errs[-1] <= cfg.refine_tolerance
+    while not conv and it < cfg.max_refine_iters:
+        r = b - refmatrix.spmv(A, xh)
+        xn = xh + api.substitute(f, r).cpu().numpy()
+        e = refmatrix.backward_error(A, xn, b)
+        it += 1
+        if e > cfg.refine_stagnation_factor * errs[-1]:
+            if e < errs[-1]:
+                xh, errs = xn, errs + [e]
+            break
+        xh, errs = xn, errs + [e]
+        conv = e <= cfg.refine_tolerance
+    assert rep.iterations == it and rep.converged == conv
+    assert rep.backward_errors == errs
+    assert np.array_equal(x, xh)
+    assert rep.iterations >= 1
