@@ -93,6 +93,7 @@ struct TaskDesc {
   int64_t valoff;
   int32_t r, s, W, L;
   int64_t d0, d1;
+  longlong4 rr0;   // layout shared with hylu_batch.cu
 };
 template <bool STAGED>
 __global__ void k_bt_pipe(DevSym, BatchP, DevProg, const TaskDesc *, int64_t, const double *, double *, int *,
@@ -158,6 +159,7 @@ struct hy_handle {
   bool uploaded = false;
   // host copies of per-node data for descriptor building
   std::vector<int64_t> h_first, h_colptr, h_valoff, h_dptr, h_nl;
+  std::vector<longlong4> h_row_rec;   // batched row programs' row records (task descriptors)
   // backward-solve U dependencies + persistent bwd task list (per G)
   int64_t *d_udp = nullptr;
   int32_t *d_udeps = nullptr;
@@ -350,6 +352,7 @@ static int build_segments(hy_handle *h, int G) {
       t.L = (int32_t)h->h_nl[u];
       t.d0 = h->h_dptr[u];
       t.d1 = h->h_dptr[u + 1];
+      t.rr0 = h->h_row_rec[t.r];
       return t;
     };
     const int sk = h->skew;
@@ -1185,6 +1188,7 @@ int hy_upload_row_programs(hy_handle *h, const hy_row_programs *d) {
     longlong4 *q;
     UPP(&q, (const longlong4 *)d->node_rec, nn); R.node_rec = q;
     UPP(&q, (const longlong4 *)d->row_rec, n); R.row_rec = q;
+    h->h_row_rec.assign((const longlong4 *)d->row_rec, (const longlong4 *)d->row_rec + n);
   }
   h->segs_G = -1;
   h->max_slots = (int)d->max_slots;

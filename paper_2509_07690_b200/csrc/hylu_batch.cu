@@ -277,6 +277,7 @@ struct TaskDesc {
   int64_t valoff;
   int32_t r, s, W, L;
   int64_t d0, d1;
+  longlong4 rr0;   // row record of the node's first row (no dependent load for it)
 };
 
 template <bool STAGED>
@@ -402,9 +403,47 @@ __device__ __forceinline__ void run_steps2(const DevProg &R, int64_t s0, int64_t
   }
 }
 
+// Row initialisation of a pair task: zero the accumulators, scatter the row's
+// matrix values (lanes over (instance, entry) pairs, 4 per lane per batch, loads
+// before stores) and form b̂_i for both groups.  Needs no dependency: the pipeline
+// runs it for the first row before polling the task's dependency flags.
+__device__ __forceinline__ void row_init2(const DevSym &S, const BatchP &P, const longlong4 &rr, int W,
+                                          double *wA, double *wC, const double *Ab, int nlive, int lane,
+                                          int64_t ba, int64_t bc, bool liveA, bool liveC,
+                                          const double *rhs, int xmask, double &yA, double &yC) {
+  const int64_t e0 = rr.y, a = rr.w;
+  const int k = (int)(rr.z >> 32);
+  yA = (liveA && rhs) ? S.dr[a] * rhs[ba * S.n + a] : 0.0;
+  yC = (liveC && rhs) ? S.dr[a] * rhs[bc * S.n + a] : 0.0;
+  for (int q = 0; q < W; ++q) {
+    wA[q * 32 + lane] = 0.0;
+    wC[q * 32 + lane] = 0.0;
+  }
+  __syncwarp();
+  if (!(xmask & 4))
+    for (int base = 0; base < nlive * k; base += 128) {
+      int cp[4], in[4];
+      double av[4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const int idx = base + m * 32 + lane;
+        const bool ok = idx < nlive * k;
+        const int inst = ok ? idx / k : 0, e = ok ? idx - inst * k : 0;
+        in[m] = ok ? inst : -1;
+        cp[m] = ok ? __ldg(S.colpos + e0 + e) : 0;
+        av[m] = ok ? __ldg(Ab + (int64_t)inst * S.nnz + e0 + e) * __ldg(S.scale + e0 + e) : 0.0;
+      }
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+        if (in[m] >= 0) (in[m] < 32 ? wA : wC)[cp[m] * 32 + (in[m] & 31)] = av[m];
+    }
+  __syncwarp();
+}
+
 __device__ __forceinline__ void bt_node2(const DevSym &S, const BatchP &P, const DevProg &R,
                                          const longlong4 nr, int g, const double *rhs, double *Y,
-                                         double *wsm0, int ws, int lane, int xmask) {
+                                         double *wsm0, int ws, int lane, int xmask, longlong4 rr,
+                                         bool pre0, double y0A, double y0C) {
   const int64_t ba = (int64_t)g * 32 + lane, bc = ba + 32;
   const bool liveA = ba < P.B, liveC = bc < P.B;
   const int64_t rem = P.B - (int64_t)g * 32;
@@ -420,46 +459,19 @@ __device__ __forceinline__ void bt_node2(const DevSym &S, const BatchP &P, const
   double *ya = Y + (int64_t)g * S.n * 32 + lane;
   double *yc = ya + (int64_t)S.n * 32;
   const double *Ab = P.A + (int64_t)g * 32 * S.nnz;
-  longlong4 rr = R.row_rec[r];
   for (int t = 0; t < s; ++t) {
     const int i = r + t;
-    const int64_t s0 = rr.x, e0 = rr.y;
+    const int64_t s0 = rr.x;
     const int64_t s1 = s0 + (rr.z & 0xffffffff);
-    const int k = (int)(rr.z >> 32);
-    const int64_t a = rr.w;
-    if (t + 1 < s) rr = R.row_rec[i + 1];
     const bool inSm = (s1 > s0) && W <= ws;
     double *growA = ga0 + (vbase + (int64_t)t * W) * 32;
     double *growC = gc0 + (vbase + (int64_t)t * W) * 32;
     double *wA = inSm ? wsm0 : growA;
     double *wC = inSm ? wsm0 + ws * 32 : growC;
-    double yaccA = (liveA && rhs) ? S.dr[a] * rhs[ba * S.n + a] : 0.0;
-    double yaccC = (liveC && rhs) ? S.dr[a] * rhs[bc * S.n + a] : 0.0;
-    for (int q = 0; q < W; ++q) {
-      wA[q * 32 + lane] = 0.0;
-      wC[q * 32 + lane] = 0.0;
-    }
-    __syncwarp();
-    // scatter in batches of 4 entries per lane: all loads of a batch are issued
-    // before its shared-memory stores
-    if (!(xmask & 4))
-      for (int base = 0; base < nlive * k; base += 128) {
-        int cp[4], in[4];
-        double av[4];
-#pragma unroll
-        for (int m = 0; m < 4; ++m) {
-          const int idx = base + m * 32 + lane;
-          const bool ok = idx < nlive * k;
-          const int inst = ok ? idx / k : 0, e = ok ? idx - inst * k : 0;
-          in[m] = ok ? inst : -1;
-          cp[m] = ok ? __ldg(S.colpos + e0 + e) : 0;
-          av[m] = ok ? __ldg(Ab + (int64_t)inst * S.nnz + e0 + e) * __ldg(S.scale + e0 + e) : 0.0;
-        }
-#pragma unroll
-        for (int m = 0; m < 4; ++m)
-          if (in[m] >= 0) (in[m] < 32 ? wA : wC)[cp[m] * 32 + (in[m] & 31)] = av[m];
-      }
-    __syncwarp();
+    double yaccA = y0A, yaccC = y0C;
+    if (!(t == 0 && pre0))
+      row_init2(S, P, rr, W, wA, wC, Ab, nlive, lane, ba, bc, liveA, liveC, rhs, xmask, yaccA, yaccC);
+    if (t + 1 < s) rr = R.row_rec[i + 1];
     if (!(xmask & 2)) {
       if (inSm)
         run_steps2(R, s0, s1, wA + lane, wC + lane, ga0 + lane, gc0 + lane, ya, yc, yaccA, yaccC);
@@ -524,7 +536,7 @@ __global__ void __launch_bounds__(PIPE_WARPS * 32, 4)
     }
     const longlong4 nr = make_longlong4(cur.valoff, cur.d0, (int64_t)cur.r | ((int64_t)cur.s << 32),
                                         (int64_t)cur.W | ((int64_t)cur.L << 32));
-    bt_node2(S, P, R, nr, cur.g, rhs, Y, wsm_w, ws, lane, nowait);
+    bt_node2(S, P, R, nr, cur.g, rhs, Y, wsm_w, ws, lane, nowait, cur.rr0, false, 0.0, 0.0);
     if (pg >= 0 && pk > 0)
 #pragma unroll
       for (int m = 0; m < 2; ++m) {
