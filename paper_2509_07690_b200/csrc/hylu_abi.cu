@@ -94,6 +94,7 @@ struct TaskDesc {
   int32_t r, s, W, L;
   int64_t d0, d1;
   longlong4 rr0;   // layout shared with hylu_batch.cu
+  int32_t dep[4];
 };
 template <bool STAGED>
 __global__ void k_bt_pipe(DevSym, BatchP, DevProg, const TaskDesc *, int64_t, const double *, double *, int *,
@@ -160,6 +161,7 @@ struct hy_handle {
   // host copies of per-node data for descriptor building
   std::vector<int64_t> h_first, h_colptr, h_valoff, h_dptr, h_nl;
   std::vector<longlong4> h_row_rec;   // batched row programs' row records (task descriptors)
+  std::vector<int32_t> h_deps;        // dependency lists (task descriptors inline the first 4)
   // backward-solve U dependencies + persistent bwd task list (per G)
   int64_t *d_udp = nullptr;
   int32_t *d_udeps = nullptr;
@@ -353,6 +355,8 @@ static int build_segments(hy_handle *h, int G) {
       t.d0 = h->h_dptr[u];
       t.d1 = h->h_dptr[u + 1];
       t.rr0 = h->h_row_rec[t.r];
+      for (int k = 0; k < 4; ++k)
+        t.dep[k] = t.d0 + k < t.d1 ? h->h_deps[t.d0 + k] : -1;
       return t;
     };
     const int sk = h->skew;
@@ -585,6 +589,7 @@ int hy_upload_symbolic(hy_handle *h, const hy_symbolic_desc *d) {
   h->h_colptr.assign(d->colptr, d->colptr + nn + 1);
   h->h_valoff.assign(d->valoff, d->valoff + nn + 1);
   h->h_dptr.assign(d->dep_ptr, d->dep_ptr + nn + 1);
+  h->h_deps.assign(d->deps, d->deps + d->dep_ptr[nn]);
   h->h_nl.assign(d->nl, d->nl + nn);
   int8_t *p8;
   UP(&p8, d->node_kind, nn); S.kind = p8;

@@ -278,6 +278,7 @@ struct TaskDesc {
   int32_t r, s, W, L;
   int64_t d0, d1;
   longlong4 rr0;   // row record of the node's first row (no dependent load for it)
+  int32_t dep[4];  // the first (up to) 4 dependencies, inline (no dependent index load)
 };
 
 template <bool STAGED>
@@ -525,7 +526,9 @@ __global__ void __launch_bounds__(PIPE_WARPS * 32, 4)
     // after the polls, and producers fence before publishing
     for (int64_t k = lane; k < nd * two && !(nowait & 1); k += 32) {
       const int64_t kk = k < nd ? k : k - nd;
-      const int *f = flags + (int64_t)__ldg(S.deps + cur.d0 + kk) * G + cur.g + (k < nd ? 0 : 1);
+      const int dn = kk == 0 ? cur.dep[0] : kk == 1 ? cur.dep[1] : kk == 2 ? cur.dep[2] :
+                     kk == 3 ? cur.dep[3] : __ldg(S.deps + cur.d0 + kk);
+      const int *f = flags + (int64_t)dn * G + cur.g + (k < nd ? 0 : 1);
       while (ld_relaxed(f) != epoch) __nanosleep(64);
     }
     __syncwarp();
