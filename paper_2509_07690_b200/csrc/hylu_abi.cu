@@ -201,7 +201,7 @@ struct hy_handle {
   int staged = 0;                          // stage row sources with cp.async (option "staged")
   int nowait = 0;                          // timing experiment only: skip dependency waits
   int pair = 1;                            // pipeline: one warp per (node, group pair)
-  int prefetch = 512;                      // pair mode: L2-prefetch the matrix values this many tasks ahead
+  int prefetch = 0;                        // pair mode: L2-prefetch the matrix values this many tasks ahead
   int warp_min = 256;                      // fan-in: below this many small items per level, CTA kernels only
   int bwd_pair = 1;                        // backward solve: one warp per (node, group pair)
   int hub_df = 0;                          // hub kernel: dataflow phase for split-free leading levels

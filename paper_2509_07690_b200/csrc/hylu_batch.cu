@@ -421,23 +421,31 @@ __device__ __forceinline__ void row_init2(const DevSym &S, const BatchP &P, cons
     wC[q * 32 + lane] = 0.0;
   }
   __syncwarp();
-  if (!(xmask & 4))
-    for (int base = 0; base < nlive * k; base += 128) {
-      int cp[4], in[4];
-      double av[4];
+  // lane = instance: each lane reads its own instance's k contiguous values (the
+  // sectors are shared by consecutive entries, so DRAM efficiency matches a
+  // transposing scatter) and writes its own column; 4 entries per batch, loads first
+  if (!(xmask & 4)) {
+    const double *rA = Ab + (int64_t)lane * S.nnz + e0;
+    const double *rC = rA + (int64_t)32 * S.nnz;
+    for (int e = 0; e < k; e += 4) {
+      int cp[4];
+      double sc[4], va[4], vc[4];
 #pragma unroll
       for (int m = 0; m < 4; ++m) {
-        const int idx = base + m * 32 + lane;
-        const bool ok = idx < nlive * k;
-        const int inst = ok ? idx / k : 0, e = ok ? idx - inst * k : 0;
-        in[m] = ok ? inst : -1;
-        cp[m] = ok ? __ldg(S.colpos + e0 + e) : 0;
-        av[m] = ok ? __ldg(Ab + (int64_t)inst * S.nnz + e0 + e) * __ldg(S.scale + e0 + e) : 0.0;
+        const bool ok = e + m < k;
+        cp[m] = ok ? __ldg(S.colpos + e0 + e + m) : 0;
+        sc[m] = ok ? __ldg(S.scale + e0 + e + m) : 0.0;
+        va[m] = (ok && liveA) ? __ldg(rA + e + m) : 0.0;
+        vc[m] = (ok && liveC) ? __ldg(rC + e + m) : 0.0;
       }
 #pragma unroll
       for (int m = 0; m < 4; ++m)
-        if (in[m] >= 0) (in[m] < 32 ? wA : wC)[cp[m] * 32 + (in[m] & 31)] = av[m];
+        if (e + m < k) {
+          wA[cp[m] * 32 + lane] = va[m] * sc[m];
+          wC[cp[m] * 32 + lane] = vc[m] * sc[m];
+        }
     }
+  }
   __syncwarp();
 }
 
@@ -620,10 +628,10 @@ __global__ void __launch_bounds__(HUB_THREADS) k_bt_hub(DevSym S, BatchP P, DevP
     const int64_t a = S.mrow_src[srow];
     const int64_t e0 = S.a_ptr[a];
     const int k = (int)(S.a_ptr[a + 1] - e0);
-    for (int idx = threadIdx.x; idx < nlive * k; idx += HUB_THREADS) {
-      const int inst = idx / k, e = idx - inst * k;
-      w0[S.colpos[e0 + e] * 32 + inst] = Ab[(int64_t)inst * S.nnz + e0 + e] * S.scale[e0 + e];
-    }
+    // lane = instance, warps stride the entries: coalesced 256-byte stores
+    if (live)
+      for (int e = warp; e < k; e += nw)
+        w0[S.colpos[e0 + e] * 32 + lane] = Ab[(int64_t)lane * S.nnz + e0 + e] * S.scale[e0 + e];
   }
   __syncthreads();
   for (int t = 0; t < s; ++t) {
