@@ -341,6 +341,7 @@ __global__ void __launch_bounds__(PIPE_WARPS * 32, 6)
 // instances, and each step has two independent FMA/load chains in flight.  The
 // value layout is unchanged (the allocation is padded to an even group count, so
 // the pair of the last odd group computes on padding: not live, no atomics).
+constexpr int P2W = 4;   // update entries per batch in run_steps2 (all loads issued first)
 template <typename WPtr>
 __device__ __forceinline__ void run_steps2(const DevProg &R, int64_t s0, int64_t s1, WPtr wa,
                                            WPtr wc, const double *ga, const double *gc,
@@ -378,23 +379,24 @@ __device__ __forceinline__ void run_steps2(const DevProg &R, int64_t s0, int64_t
     wc[p * 32] = lc;
     acA -= la * yja;
     acC -= lc * yjc;
-    for (int q = 0; q < cnt; q += 4) {
-      int t[4];
-      double xa[4], xc[4], va[4], vc[4];
+    for (int q = 0; q < cnt; q += P2W) {
+      int t[P2W];
+      double xa[P2W], xc[P2W];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < P2W; ++k) {
         const bool ok = q + k < cnt;
         t[k] = ok ? __ldg(rl + q + k) : 0;
         xa[k] = ok ? __ldcg(ua + (q + k) * 32) : 0.0;
         xc[k] = ok ? __ldcg(uc + (q + k) * 32) : 0.0;
       }
+      double va[P2W], vc[P2W];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < P2W; ++k) {
         va[k] = wa[t[k] * 32];
         vc[k] = wc[t[k] * 32];
       }
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
+      for (int k = 0; k < P2W; ++k)
         if (q + k < cnt) {
           wa[t[k] * 32] = va[k] - la * xa[k];
           wc[t[k] * 32] = vc[k] - lc * xc[k];
