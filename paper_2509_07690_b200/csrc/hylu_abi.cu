@@ -105,10 +105,11 @@ __global__ void k_bt_lev0(DevSym, BatchP, DevProg, const int32_t *, int, int, co
 __global__ void k_bt_hub(DevSym, BatchP, DevProg, const int32_t *, int, int, const double *, double *,
                          double *, int, int *, int, int);
 __global__ void k_batch_bhat(DevSym, const int32_t *, const double *, double *, int64_t);
-__global__ void k_batch_xout(DevSym, const double *, double *, int64_t);
 __global__ void k_batch_fwd(DevSym, const double *, int64_t, const int32_t *, int, int, double *);
 __global__ void k_batch_bwd(DevSym, const double *, int64_t, const int32_t *, int, int, double *);
 __global__ void k_batch_bwd2(DevSym, const double *, int64_t, const int32_t *, int, int, double *);
+__global__ void k_batch_xout2(DevSym, const int32_t *, const double *, double *, int64_t);
+__global__ void k_perm_inverse(int, const int64_t *, int32_t *);
 __global__ void k_batch_extract(const double *, int64_t, int64_t, double *);
 __global__ void k_bt_bwd(DevSym, const double *, int64_t, const int2 *, int64_t, const int64_t *, const int32_t *,
                          int *, int *, int, int, double *);
@@ -242,6 +243,7 @@ struct hy_handle {
   std::vector<int64_t> fi_xpbig;                     // per level: first CTA-per-item multiplier item
   std::vector<int64_t> fi_hub;                       // per level: offsets of pull-program rows
   int32_t *d_fi_hubs = nullptr;
+  int32_t *d_pinv = nullptr;   // inverse column permutation (batched output order)
   int64_t *d_arow = nullptr;   // A's pattern in original coordinates (refinement)
   int32_t *d_acol = nullptr;
   int fi_v3 = 0;                                     // option "fanin_v3" (slower; kept for experiments)
@@ -483,6 +485,7 @@ void hy_destroy(hy_handle *h) {
   if (h->d_counters) cudaFree(h->d_counters);
   if (h->d_by) cudaFree(h->d_by);
   if (h->d_arow) cudaFree(h->d_arow);
+  if (h->d_pinv) cudaFree(h->d_pinv);
   if (h->d_acol) cudaFree(h->d_acol);
   delete h;
 }
@@ -1404,7 +1407,12 @@ int hy_solve_batched(hy_handle *h, int64_t B, const double *d_b, double *d_x, ui
       h->launches++;
     }
   }
-  k_batch_xout<<<tg, 256, 0, st>>>(h->S, h->d_by, d_x, B);
+  if (!h->d_pinv) {
+    CK(cudaMalloc((void **)&h->d_pinv, sizeof(int32_t) * h->S.n));
+    k_perm_inverse<<<(h->S.n + 255) / 256, 256, 0, st>>>(h->S.n, h->S.perm, h->d_pinv);
+    h->launches++;
+  }
+  k_batch_xout2<<<tg, 256, 0, st>>>(h->S, h->d_pinv, h->d_by, d_x, B);
   h->launches++;
   CK(cudaGetLastError());
   return HY_OK;

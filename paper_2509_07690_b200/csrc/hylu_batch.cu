@@ -977,26 +977,31 @@ __global__ void k_batch_bhat(DevSym S, const int32_t *iperm, const double *rhs, 
   }
 }
 
-// interleaved z [G][n][32] -> x [B][n]: x[perm[k]] = dc[perm[k]] z[k]
-__global__ void k_batch_xout(DevSym S, const double *Y, double *X, int64_t B) {
+// interleaved z [G][n][32] -> x [B][n] in output order: a tile of 32 consecutive
+// output columns c reads the 32 lines z[pinv[c]] (one 256-byte line each, lane =
+// instance) and writes 32 contiguous values per instance row.
+__global__ void k_batch_xout2(DevSym S, const int32_t *pinv, const double *Y, double *X, int64_t B) {
   __shared__ double tile[32][33];
   const int g = blockIdx.y;
-  const int k0 = blockIdx.x * 32;
+  const int c0 = blockIdx.x * 32;
   const int lane = threadIdx.x & 31, wy = threadIdx.x >> 5;
-  for (int kk = wy; kk < 32; kk += 8) {
-    const int k = k0 + kk;
-    tile[kk][lane] = k < S.n ? Y[((int64_t)g * S.n + k) * 32 + lane] : 0.0;
+  for (int cc = wy; cc < 32; cc += 8) {
+    const int c = c0 + cc;
+    tile[cc][lane] = c < S.n ? S.dc[c] * Y[((int64_t)g * S.n + pinv[c]) * 32 + lane] : 0.0;
   }
   __syncthreads();
   for (int ii = wy; ii < 32; ii += 8) {
     const int64_t b = (int64_t)g * 32 + ii;
-    const int k = k0 + lane;
-    if (k < S.n && b < B) {
-      const int64_t c = S.perm[k];
-      X[b * S.n + c] = S.dc[c] * tile[lane][ii];
-    }
+    const int c = c0 + lane;
+    if (c < S.n && b < B) X[b * S.n + c] = tile[lane][ii];
   }
 }
+
+__global__ void k_perm_inverse(int n, const int64_t *perm, int32_t *pinv) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+    pinv[perm[k]] = k;
+}
+
 
 // unfused forward substitution (when the batch was refactorized without a rhs)
 __global__ void __launch_bounds__(BW * 32) k_batch_fwd(DevSym S, const double *BF, int64_t stored,
