@@ -110,6 +110,8 @@ __global__ void k_batch_bwd(DevSym, const double *, int64_t, const int32_t *, in
 __global__ void k_batch_bwd2(DevSym, const double *, int64_t, const int32_t *, int, int, double *);
 __global__ void k_batch_xout2(DevSym, const int32_t *, const double *, double *, int64_t);
 __global__ void k_perm_inverse(int, const int64_t *, int32_t *);
+__global__ void k_row_of(DevSym, const int32_t *, int32_t *);
+__global__ void k_batch_bhat2(DevSym, const int32_t *, const double *, double *, int64_t);
 __global__ void k_batch_extract(const double *, int64_t, int64_t, double *);
 __global__ void k_bt_bwd(DevSym, const double *, int64_t, const int2 *, int64_t, const int64_t *, const int32_t *,
                          int *, int *, int, int, double *);
@@ -244,6 +246,7 @@ struct hy_handle {
   std::vector<int64_t> fi_hub;                       // per level: offsets of pull-program rows
   int32_t *d_fi_hubs = nullptr;
   int32_t *d_pinv = nullptr;   // inverse column permutation (batched output order)
+  int32_t *d_rowof = nullptr;  // factor row of each original row (batched b̂ in source order)
   int64_t *d_arow = nullptr;   // A's pattern in original coordinates (refinement)
   int32_t *d_acol = nullptr;
   int fi_v3 = 0;                                     // option "fanin_v3" (slower; kept for experiments)
@@ -486,6 +489,7 @@ void hy_destroy(hy_handle *h) {
   if (h->d_by) cudaFree(h->d_by);
   if (h->d_arow) cudaFree(h->d_arow);
   if (h->d_pinv) cudaFree(h->d_pinv);
+  if (h->d_rowof) cudaFree(h->d_rowof);
   if (h->d_acol) cudaFree(h->d_acol);
   delete h;
 }
@@ -1256,8 +1260,18 @@ int hy_refactorize_batched(hy_handle *h, int64_t B, const double *d_vals, double
   h->last_iperm = prior->d_inner_perm;
   CK(cudaMemsetAsync(d_npert, 0, sizeof(int32_t) * B, st));
   const int G = (int)((B + 31) / 32);
-  BatchP P{h->d_bf, d_vals, prior->d_inner_perm, prior->d_anorm, eps, d_npert, B, h->stored};
+  BatchP P{h->d_bf, d_vals, prior->d_inner_perm, prior->d_anorm, eps, d_npert, B, h->stored, 0};
   h->last_fused = d_b_fuse != nullptr;
+  if (d_b_fuse) {
+    // b̂ into Y first (coalesced transpose in source-row order); the row kernels then
+    // read one line per row instead of gathering one value per instance
+    if (!h->d_rowof) CK(cudaMalloc((void **)&h->d_rowof, sizeof(int32_t) * h->S.n));
+    k_row_of<<<(h->S.n + 255) / 256, 256, 0, st>>>(h->S, prior->d_inner_perm, h->d_rowof);
+    dim3 tg((h->S.n + 31) / 32, G);
+    k_batch_bhat2<<<tg, 256, 0, st>>>(h->S, h->d_rowof, d_b_fuse, h->d_by, B);
+    h->launches += 2;
+    P.ypre = 1;
+  }
   const int64_t nflags = (int64_t)h->S.nn * G;
   if (nflags > h->flags_cap) {
     if (h->d_flags) CK(cudaFree(h->d_flags));

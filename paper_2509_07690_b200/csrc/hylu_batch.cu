@@ -222,7 +222,7 @@ __device__ __forceinline__ void bt_node(const DevSym &S, const BatchP &P, const 
     const bool inSm = (s1 > s0) && W <= ws;
     double *grow = gb0 + (vbase + (int64_t)t * W) * 32;
     double *w0 = inSm ? wsm0 : grow;
-    double yacc = (live && rhs) ? S.dr[a] * rhs[b * S.n + a] : 0.0;
+    double yacc = P.ypre ? yb[(int64_t)i * 32] : (live && rhs) ? S.dr[a] * rhs[b * S.n + a] : 0.0;
     for (int q = 0; q < W; ++q) w0[q * 32 + lane] = 0.0;
     __syncwarp();
     // scatter: lanes over (instance, entry) pairs, instance-major, so a pass reads
@@ -413,11 +413,17 @@ __device__ __forceinline__ void run_steps2(const DevProg &R, int64_t s0, int64_t
 __device__ __forceinline__ void row_init2(const DevSym &S, const BatchP &P, const longlong4 &rr, int W,
                                           double *wA, double *wC, const double *Ab, int nlive, int lane,
                                           int64_t ba, int64_t bc, bool liveA, bool liveC,
-                                          const double *rhs, int xmask, double &yA, double &yC) {
+                                          const double *rhs, int xmask, double &yA, double &yC,
+                                          const double *yiA, const double *yiC) {
   const int64_t e0 = rr.y, a = rr.w;
   const int k = (int)(rr.z >> 32);
-  yA = (liveA && rhs) ? S.dr[a] * rhs[ba * S.n + a] : 0.0;
-  yC = (liveC && rhs) ? S.dr[a] * rhs[bc * S.n + a] : 0.0;
+  if (P.ypre) {   // b̂ prepared in Y by k_batch_bhat2 (one 256-byte line per row)
+    yA = *yiA;
+    yC = *yiC;
+  } else {
+    yA = (liveA && rhs) ? S.dr[a] * rhs[ba * S.n + a] : 0.0;
+    yC = (liveC && rhs) ? S.dr[a] * rhs[bc * S.n + a] : 0.0;
+  }
   for (int q = 0; q < W; ++q) {
     wA[q * 32 + lane] = 0.0;
     wC[q * 32 + lane] = 0.0;
@@ -481,7 +487,8 @@ __device__ __forceinline__ void bt_node2(const DevSym &S, const BatchP &P, const
     double *wC = inSm ? wsm0 + ws * 32 : growC;
     double yaccA = y0A, yaccC = y0C;
     if (!(t == 0 && pre0))
-      row_init2(S, P, rr, W, wA, wC, Ab, nlive, lane, ba, bc, liveA, liveC, rhs, xmask, yaccA, yaccC);
+      row_init2(S, P, rr, W, wA, wC, Ab, nlive, lane, ba, bc, liveA, liveC, rhs, xmask, yaccA, yaccC,
+                ya + (int64_t)i * 32, yc + (int64_t)i * 32);
     if (t + 1 < s) rr = R.row_rec[i + 1];
     if (!(xmask & 2)) {
       if (inSm)
@@ -938,7 +945,7 @@ __global__ void __launch_bounds__(HUB_THREADS) k_bt_hub(DevSym S, BatchP P, DevP
     red[warp][lane] = part;
     __syncthreads();
     if (warp == 0) {
-      double yacc = (live && rhs) ? S.dr[a] * rhs[b * S.n + a] : 0.0;
+      double yacc = P.ypre ? yb[(int64_t)i * 32] : (live && rhs) ? S.dr[a] * rhs[b * S.n + a] : 0.0;
       for (int k2 = 0; k2 < nw; ++k2) yacc -= red[k2][lane];
       yb[(int64_t)i * 32] = yacc;
     }
@@ -947,6 +954,37 @@ __global__ void __launch_bounds__(HUB_THREADS) k_bt_hub(DevSym S, BatchP P, DevP
   if (flags && threadIdx.x == 0) {
     __threadfence();
     st_release(flags + (int64_t)u * G + g, epoch);
+  }
+}
+
+// Factor row of every original row (the inverse of row i -> source row a, with the
+// prior inner_perm applied inside supernodes).
+__global__ void k_row_of(DevSym S, const int32_t *iperm, int32_t *rowof) {
+  for (int row = blockIdx.x * blockDim.x + threadIdx.x; row < S.n; row += gridDim.x * blockDim.x) {
+    const int u = S.node_of[row];
+    int src = row;
+    if (S.kind[u] == 1) src = (int)S.first[u] + iperm[row];
+    rowof[S.mrow_src[src]] = row;
+  }
+}
+
+// rhs [B][n] -> b̂ interleaved [G][n][32] in source-row order: a tile of 32
+// consecutive original rows reads 256 contiguous bytes per instance and writes one
+// full 256-byte line per row (b̂_i = dr[a] b[a], i = rowof[a]).
+__global__ void k_batch_bhat2(DevSym S, const int32_t *rowof, const double *rhs, double *Y, int64_t B) {
+  __shared__ double tile[32][33];
+  const int g = blockIdx.y;
+  const int a0 = blockIdx.x * 32;
+  const int lane = threadIdx.x & 31, wy = threadIdx.x >> 5;
+  for (int ii = wy; ii < 32; ii += 8) {
+    const int64_t b = (int64_t)g * 32 + ii;
+    const int a = a0 + lane;
+    tile[ii][lane] = (a < S.n && b < B) ? S.dr[a] * rhs[b * S.n + a] : 0.0;
+  }
+  __syncthreads();
+  for (int aa = wy; aa < 32; aa += 8) {
+    const int a = a0 + aa;
+    if (a < S.n) Y[((int64_t)g * S.n + rowof[a]) * 32 + lane] = tile[lane][aa];
   }
 }
 

@@ -53,6 +53,7 @@ struct BatchP {
   int32_t *npert;        // [B]
   int64_t B;
   int64_t stored;
+  int ypre;              // 1: Y already holds b̂ (interleaved, factor-row order)
 };
 
 // Row programs (schedule.py) resident on the device.
