@@ -4,6 +4,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <map>
 #include <vector>
 
 #include "hylu_b200.h"
@@ -219,6 +220,7 @@ struct hy_handle {
   };
   std::vector<Seg> segs;
   int segs_G = -1;
+  std::map<int, std::vector<Seg>> seg_cache;   // task lists per group count (chunked callers vary G)
   double *d_scratch = nullptr;             // hub partial sums
   int64_t scratch_cap = 0;
   int32_t *d_bl_rows = nullptr, *d_bl_hubs = nullptr;
@@ -323,14 +325,24 @@ static int upload_prog(hy_handle *h, T **dst, const T *src, int64_t count) {
   } while (0)
 
 static void free_segments(hy_handle *h) {
-  for (auto &sg : h->segs) cudaFree(sg.d_tasks);
+  for (auto &kv : h->seg_cache)
+    for (auto &sg : kv.second) cudaFree(sg.d_tasks);
+  h->seg_cache.clear();
   h->segs.clear();
+  h->segs_G = -1;
 }
 
 // Per hub-free level segment, the flat (node, group) task list in diagonal order:
 // group g at level l is listed with group g+1 at level l-1.
 static int build_segments(hy_handle *h, int G) {
-  free_segments(h);
+  auto hit = h->seg_cache.find(G);
+  if (hit != h->seg_cache.end()) {
+    h->segs = hit->second;
+    h->segs_G = G;
+    return HY_OK;
+  }
+  if (h->seg_cache.size() >= 8) free_segments(h);
+  h->segs.clear();
   const int nl = h->fplan.nlev;
   std::vector<int32_t> rows(h->bl_rptr[nl]);
   if (!rows.empty())
@@ -382,6 +394,7 @@ static int build_segments(hy_handle *h, int G) {
     h->segs.push_back(sg);
     l = l1;
   }
+  h->seg_cache[G] = h->segs;
   h->segs_G = G;
   return HY_OK;
 }
@@ -505,7 +518,7 @@ int hy_set_option(hy_handle *h, const char *name, int64_t value) {
   }
   if (std::string(name) == "lev0_split") {
     h->lev0_split = value != 0;
-    h->segs_G = -1;
+    free_segments(h);
     return HY_OK;
   }
   if (std::string(name) == "bwd_persistent") {
@@ -522,7 +535,7 @@ int hy_set_option(hy_handle *h, const char *name, int64_t value) {
   }
   if (std::string(name) == "diagonal_skew" && value >= 1) {
     h->skew = (int)value;
-    h->segs_G = -1;
+    free_segments(h);
     return HY_OK;
   }
   if (std::string(name) == "nowait_experiment") {
@@ -531,7 +544,7 @@ int hy_set_option(hy_handle *h, const char *name, int64_t value) {
   }
   if (std::string(name) == "pair_groups") {
     h->pair = value != 0;
-    h->segs_G = -1;
+    free_segments(h);
     h->pipe_blocks = 0;
     return HY_OK;
   }
@@ -1202,7 +1215,7 @@ int hy_upload_row_programs(hy_handle *h, const hy_row_programs *d) {
     UPP(&q, (const longlong4 *)d->row_rec, n); R.row_rec = q;
     h->h_row_rec.assign((const longlong4 *)d->row_rec, (const longlong4 *)d->row_rec + n);
   }
-  h->segs_G = -1;
+  free_segments(h);
   h->max_slots = (int)d->max_slots;
   h->level_ws.assign(d->level_ws, d->level_ws + h->fplan.nlev);
   // per level split: non-hub nodes / hub nodes
