@@ -396,6 +396,7 @@ constexpr int KLD = FI_KC + 1;
 template <int NX, int NY>
 __device__ __forceinline__ void fi_steps(const double *Xs, const double *Ut, int kc, int tr, int tcl,
                                          int s, double (&c4)[4][4]) {
+#pragma unroll 4
   for (int a = 0; a < kc; ++a) {
     double xv[NX], uv[NY];
 #pragma unroll
