@@ -52,7 +52,7 @@ def build_cuda(force=False, verbose=False):
     deps = srcs + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(INCLUDE, "*.h"))
     if force or _stale(out, deps):
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-               "-I", INCLUDE, "-o", out, *srcs]
+               "-I", INCLUDE, *os.environ.get("HYLU_NVCC_EXTRA", "").split(), "-o", out, *srcs]
         if verbose:
             cmd += ["-Xptxas", "-v"]
         log = _run(cmd)

@@ -75,6 +75,7 @@ size_t fi_upd3_smem(int);
 size_t fi_upd_smem(int, int);
 size_t pipe_smem_bytes(bool staged);
 size_t hub_smem_bytes();
+int hub_threads();
 __global__ void k_bhat(DevSym, const int32_t *, const double *, double *);
 __global__ void k_xout(DevSym, const double *, double *);
 __global__ void k_fwd(DevSym, const double *, const int32_t *, int, double *);
@@ -1334,7 +1335,7 @@ int hy_refactorize_batched(hy_handle *h, int64_t B, const double *d_vals, double
         CK(cudaMalloc((void **)&h->d_scratch, sizeof(double) * need));
         h->scratch_cap = need;
       }
-      k_bt_hub<<<(unsigned)(nh * G), 512, hub_smem_bytes(), st>>>(h->S, P, h->prog, h->d_bl_hubs + h->bl_hptr[l], nh, G,
+      k_bt_hub<<<(unsigned)(nh * G), hub_threads(), hub_smem_bytes(), st>>>(h->S, P, h->prog, h->d_bl_hubs + h->bl_hptr[l], nh, G,
                                                    d_b_fuse, h->d_by, h->d_scratch, h->max_slots,
                                                    h->d_flags, h->epoch, h->hub_df);
       h->launches++;

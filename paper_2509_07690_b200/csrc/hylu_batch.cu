@@ -16,7 +16,17 @@
 namespace hy {
 
 constexpr int BW = 4;            // warps per block (bwd / fwd kernels)
-constexpr int HUB_THREADS = 512;
+#ifndef HUB_THREADS_DEF
+#define HUB_THREADS_DEF 512
+#endif
+constexpr int HUB_THREADS = HUB_THREADS_DEF;
+int hub_threads() { return HUB_THREADS; }
+#ifndef HUB_I
+#define HUB_I 1     // work items per warp per round (staged hub levels; 1-8 measured, 1 best)
+#endif
+#ifndef HUB_P
+#define HUB_P 8     // predecessors per item per round
+#endif
 constexpr int HUB_CAPI = 1024;   // staged work items per level (per buffer)
 constexpr int HUB_CAPP = 4096;   // staged predecessor records per level (per buffer)
 constexpr size_t HUB_BUF = (size_t)HUB_CAPP * (8 + 4) + (size_t)HUB_CAPI * (8 * 3 + 4 * 2);
@@ -838,14 +848,14 @@ __global__ void __launch_bounds__(HUB_THREADS) k_bt_hub(DevSym S, BatchP P, DevP
         int32_t *st_pp, *st_p, *st_sl;
         buf(q & 1, st_pu, st_kd, st_y0, st_y1, st_pp, st_p, st_sl);
         const int64_t yb0 = s_y[q];
-        // four items per warp at a time, four predecessors per item per round: up
-        // to 32 independent gathers in flight per warp
-        for (int64_t q0 = warp; q0 < ni; q0 += 4 * nw) {
-          int p[4], y[4], y1[4], slot[4];
-          int64_t kd[4];
-          double acc[4], dv[4];
+        // HUB_I items per warp at a time, HUB_P predecessors per item per round:
+        // HUB_I x HUB_P x 2 independent gathers in flight per warp
+        for (int64_t q0 = warp; q0 < ni; q0 += HUB_I * nw) {
+          int p[HUB_I], y[HUB_I], y1[HUB_I], slot[HUB_I];
+          int64_t kd[HUB_I];
+          double acc[HUB_I], dv[HUB_I];
 #pragma unroll
-          for (int jq = 0; jq < 4; ++jq) {
+          for (int jq = 0; jq < HUB_I; ++jq) {
             const int64_t qq = q0 + (int64_t)jq * nw;
             const bool ok = qq < ni;
             p[jq] = ok ? st_p[qq] : 0;
@@ -858,25 +868,25 @@ __global__ void __launch_bounds__(HUB_THREADS) k_bt_hub(DevSym S, BatchP P, DevP
           }
           int rem = 0;
 #pragma unroll
-          for (int jq = 0; jq < 4; ++jq) rem = max(rem, y1[jq] - y[jq]);
-          for (int step = 0; step < rem; step += 4) {
-            double lv[4][4], uv[4][4];
+          for (int jq = 0; jq < HUB_I; ++jq) rem = max(rem, y1[jq] - y[jq]);
+          for (int step = 0; step < rem; step += HUB_P) {
+            double lv[HUB_I][HUB_P], uv[HUB_I][HUB_P];
 #pragma unroll
-            for (int jq = 0; jq < 4; ++jq)
+            for (int jq = 0; jq < HUB_I; ++jq)
 #pragma unroll
-              for (int e = 0; e < 4; ++e) {
+              for (int e = 0; e < HUB_P; ++e) {
                 const int yy = y[jq] + step + e;
                 const bool act = yy < y1[jq];
                 lv[jq][e] = act ? w[st_pp[yy] * 32] : 0.0;
                 uv[jq][e] = act ? gb[st_pu[yy] * 32] : 0.0;
               }
 #pragma unroll
-            for (int jq = 0; jq < 4; ++jq)
+            for (int jq = 0; jq < HUB_I; ++jq)
 #pragma unroll
-              for (int e = 0; e < 4; ++e) acc[jq] -= lv[jq][e] * uv[jq][e];
+              for (int e = 0; e < HUB_P; ++e) acc[jq] -= lv[jq][e] * uv[jq][e];
           }
 #pragma unroll
-          for (int jq = 0; jq < 4; ++jq) {
+          for (int jq = 0; jq < HUB_I; ++jq) {
             const int64_t qq = q0 + (int64_t)jq * nw;
             if (qq >= ni) continue;
             double a = acc[jq];
