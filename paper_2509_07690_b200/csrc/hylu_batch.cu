@@ -15,7 +15,10 @@
 
 namespace hy {
 
-constexpr int BW = 4;            // warps per block (bwd / fwd kernels)
+constexpr int BW = 4;
+#ifndef BWD_W
+#define BWD_W 2     // backward-solve entries per batch (k_batch_bwd2; 2-8 measured)
+#endif            // warps per block (bwd / fwd kernels)
 #ifndef HUB_THREADS_DEF
 #define HUB_THREADS_DEF 512
 #endif
@@ -1141,13 +1144,13 @@ __global__ void __launch_bounds__(BW * 32) k_batch_bwd2(DevSym S, const double *
     const int d = L + t;
     double accA = ya[(int64_t)(r + t) * 32], accC = yc[(int64_t)(r + t) * 32];
     const double dA = ga[ro + (int64_t)d * 32], dC = gc[ro + (int64_t)d * 32];
-    for (int p0 = d + 1; p0 < W; p0 += 4) {
-      int k[4];
-      double a[4], c[4], za[4], zc[4];
+    for (int p0 = d + 1; p0 < W; p0 += BWD_W) {
+      int k[BWD_W];
+      double a[BWD_W], c[BWD_W], za[BWD_W], zc[BWD_W];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) k[e] = p0 + e < W ? __ldg(cc + p0 + e) : -1;
+      for (int e = 0; e < BWD_W; ++e) k[e] = p0 + e < W ? __ldg(cc + p0 + e) : -1;
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
+      for (int e = 0; e < BWD_W; ++e) {
         const bool ok = k[e] >= 0;
         a[e] = ok ? ga[ro + (int64_t)(p0 + e) * 32] : 0.0;
         c[e] = ok ? gc[ro + (int64_t)(p0 + e) * 32] : 0.0;
@@ -1155,7 +1158,7 @@ __global__ void __launch_bounds__(BW * 32) k_batch_bwd2(DevSym S, const double *
         zc[e] = ok ? yc[(int64_t)k[e] * 32] : 0.0;
       }
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
+      for (int e = 0; e < BWD_W; ++e) {
         accA -= a[e] * za[e];
         accC -= c[e] * zc[e];
       }
