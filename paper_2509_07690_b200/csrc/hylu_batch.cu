@@ -354,7 +354,10 @@ __global__ void __launch_bounds__(PIPE_WARPS * 32, 6)
 // instances, and each step has two independent FMA/load chains in flight.  The
 // value layout is unchanged (the allocation is padded to an even group count, so
 // the pair of the last odd group computes on padding: not live, no atomics).
-constexpr int P2W = 4;   // update entries per batch in run_steps2 (all loads issued first)
+#ifndef P2W_DEF
+#define P2W_DEF 4
+#endif
+constexpr int P2W = P2W_DEF;   // update entries per batch in run_steps2 (all loads issued first)
 template <typename WPtr>
 __device__ __forceinline__ void run_steps2(const DevProg &R, int64_t s0, int64_t s1, WPtr wa,
                                            WPtr wc, const double *ga, const double *gc,
