@@ -321,20 +321,39 @@ class BatchedRefactorizer:
         check(self.ctx.lib.hy_solve_batched(self.ctx.h, B, None, d_x.data_ptr(), sh))
         return d_x, d_npert
 
-    def run_host(self, h_vals, h_rhs, h_x, h_npert=None, chunks=8):
+    def run_host(self, h_vals, h_rhs, h_x, h_npert=None, chunks=8, sizes=None, pipelined=False):
         """Host buffers in, host buffers out, copies overlapped with compute.
 
         The batch is cut into ``chunks`` contiguous slabs (multiples of 32
         instances); chunk k's values/rhs go H2D on a copy stream while chunk k-1
         is refactorized+solved on the compute stream and chunk k-2's solutions go
-        D2H on a third stream.  ``h_*`` should be pinned torch CPU tensors."""
+        D2H on a third stream.  ``h_*`` should be pinned torch CPU tensors.
+        ``sizes`` (optional) gives explicit chunk sizes instead.
+
+        ``pipelined=False``: the caller's current stream waits for the last D2H
+        (results are ready in stream order).  ``pipelined=True`` (streaming use):
+        the call returns without that wait, so the next call's H2D copies start
+        while this call's last chunks still compute — each chunk's device buffers
+        are reused only after their previous compute / D2H finished (per-chunk
+        events).  Call ``host_wait()`` before reading ``h_x``."""
         import torch
         B = h_vals.shape[0]
         dev = self.ctx.device
-        per = ((B + chunks - 1) // chunks + 31) // 32 * 32
-        bounds = [(a, min(B, a + per)) for a in range(0, B, per)]
-        key = (B, per)
+        if sizes is None:
+            per = ((B + chunks - 1) // chunks + 31) // 32 * 32
+            sizes = [min(per, B - a) for a in range(0, B, per)]
+        bounds, a = [], 0
+        for c in sizes:
+            if a >= B:
+                break
+            bounds.append((a, min(B, a + int(c))))
+            a += int(c)
+        if a < B:
+            bounds.append((a, B))
+        key = (B, tuple(bounds))
         if getattr(self, "_host_key", None) != key:
+            if getattr(self, "_host_key", None) is not None:
+                torch.cuda.synchronize(dev)
             self._host_key = key
             self._streams = [torch.cuda.Stream(dev) for _ in range(3)]
             self._dbufs = []
@@ -343,26 +362,43 @@ class BatchedRefactorizer:
                                     torch.empty((b - a, self.ctx.n), dtype=torch.float64, device=dev),
                                     torch.empty((b - a, self.ctx.n), dtype=torch.float64, device=dev),
                                     torch.empty(b - a, dtype=torch.int32, device=dev)))
+            self._ev_cmp = [None] * len(bounds)   # compute of chunk k done (dv/dr free)
+            self._ev_out = [None] * len(bounds)   # D2H of chunk k done (dx/dn free)
         s_in, s_cmp, s_out = self._streams
         cur = torch.cuda.current_stream(dev)
         s_in.wait_stream(cur)
-        for (a, b), (dv, dr, dx, dn) in zip(bounds, self._dbufs):
+        for k, ((a, b), (dv, dr, dx, dn)) in enumerate(zip(bounds, self._dbufs)):
             with torch.cuda.stream(s_in):
+                if self._ev_cmp[k] is not None:
+                    s_in.wait_event(self._ev_cmp[k])
                 dv.copy_(h_vals[a:b], non_blocking=True)
                 dr.copy_(h_rhs[a:b], non_blocking=True)
                 ev_in = torch.cuda.Event()
                 ev_in.record(s_in)
             s_cmp.wait_event(ev_in)
+            if self._ev_out[k] is not None:
+                s_cmp.wait_event(self._ev_out[k])
             self.run(dv, dr, dx, dn, s_cmp)
             ev_c = torch.cuda.Event()
             ev_c.record(s_cmp)
+            self._ev_cmp[k] = ev_c
             s_out.wait_event(ev_c)
             with torch.cuda.stream(s_out):
                 h_x[a:b].copy_(dx, non_blocking=True)
                 if h_npert is not None:
                     h_npert[a:b].copy_(dn, non_blocking=True)
-        cur.wait_stream(s_out)
+                ev_o = torch.cuda.Event()
+                ev_o.record(s_out)
+                self._ev_out[k] = ev_o
+        if not pipelined:
+            cur.wait_stream(s_out)
         return h_x, h_npert
+
+    def host_wait(self, stream=None):
+        """Make ``stream`` (default: current) wait for every pending run_host copy."""
+        import torch
+        if getattr(self, "_streams", None):
+            (stream or torch.cuda.current_stream(self.ctx.device)).wait_stream(self._streams[2])
 
     def factor_values(self, b, stream=None):
         import torch

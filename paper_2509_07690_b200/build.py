@@ -45,14 +45,15 @@ def build_metis(force=False):
     return out
 
 
-def build_cuda(force=False, verbose=False):
+def build_cuda(force=False, verbose=False, out=None, extra=None):
+    """extra: additional nvcc flags (default $HYLU_NVCC_EXTRA); out: variant path."""
     os.makedirs(LIBDIR, exist_ok=True)
-    out = os.path.join(LIBDIR, "libhylu_b200.so")
+    out = out or os.path.join(LIBDIR, "libhylu_b200.so")
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     deps = srcs + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(INCLUDE, "*.h"))
     if force or _stale(out, deps):
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-               "-I", INCLUDE, *os.environ.get("HYLU_NVCC_EXTRA", "").split(), "-o", out, *srcs]
+               "-I", INCLUDE, *(extra if extra is not None else os.environ.get("HYLU_NVCC_EXTRA", "")).split(), "-o", out, *srcs]
         if verbose:
             cmd += ["-Xptxas", "-v"]
         log = _run(cmd)

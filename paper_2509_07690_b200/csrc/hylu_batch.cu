@@ -358,6 +358,24 @@ __global__ void __launch_bounds__(PIPE_WARPS * 32, 6)
 #define P2W_DEF 4
 #endif
 constexpr int P2W = P2W_DEF;   // update entries per batch in run_steps2 (all loads issued first)
+#ifndef PFD_DEF
+#define PFD_DEF 0
+#endif
+constexpr int PFD = PFD_DEF;   // L2 prefetch distance (steps) of the source rows' U lines (0: off)
+
+// Lane q < cnt of step st requests line q of the step's source row U(j,>j) of both
+// groups into L2 (the lines of one source row are contiguous: one 256-byte line per
+// position).  Issued only after the task's dependency polls, so the values are final.
+__device__ __forceinline__ void pf_step(const DevProg &R, int64_t st, const double *ga, const double *gc) {
+  const int64_t src = __ldg(R.st_src + st);
+  const int cnt = __ldg(R.st_cnt + st);
+  const int lane = threadIdx.x & 31;
+  for (int q = lane; q < cnt; q += 32) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(ga + (src + 1 + q) * 32));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(gc + (src + 1 + q) * 32));
+  }
+}
+
 template <typename WPtr>
 __device__ __forceinline__ void run_steps2(const DevProg &R, int64_t s0, int64_t s1, WPtr wa,
                                            WPtr wc, const double *ga, const double *gc,
@@ -371,7 +389,14 @@ __device__ __forceinline__ void run_steps2(const DevProg &R, int64_t s0, int64_t
   int64_t j = __ldg(R.st_j + s0);
   double da = __ldcg(ga + src * 32), dc = __ldcg(gc + src * 32);
   double yja = __ldcg(ya + j * 32), yjc = __ldcg(yc + j * 32);
+  if (PFD > 0) {
+    // lane-0-relative group bases (wa/ga are lane-offset pointers)
+    const double *pa = ga - (threadIdx.x & 31), *pc = gc - (threadIdx.x & 31);
+    for (int64_t q = s0 + 1; q < s1 && q <= s0 + PFD; ++q) pf_step(R, q, pa, pc);
+  }
   for (int64_t st = s0; st < s1; ++st) {
+    if (PFD > 0 && st + PFD + 1 < s1)
+      pf_step(R, st + PFD + 1, ga - (threadIdx.x & 31), gc - (threadIdx.x & 31));
     int pn = 0, cn = 0;
     int64_t sn = 0, rn = 0;
     double dna = 1.0, dnc = 1.0, yna = 0.0, ync = 0.0;
