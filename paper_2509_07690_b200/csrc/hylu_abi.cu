@@ -73,6 +73,10 @@ __global__ void k_fi_x_w(DevSym, CallP, FaninDev, int, int);
 __global__ void k_fi_upd_w(DevSym, CallP, FaninDev, int, int);
 size_t fi_upd3_smem(int);
 size_t fi_upd_smem(int, int);
+size_t fi_upd_tc_smem(int);
+size_t fi_upd_kc_smem();
+__global__ void k_fi_upd_kc(DevSym, CallP, FaninDev, int);
+__global__ void k_fi_upd_tc(DevSym, CallP, FaninDev, int, int);
 size_t pipe_smem_bytes(bool staged);
 size_t hub_smem_bytes();
 int hub_threads();
@@ -254,6 +258,7 @@ struct hy_handle {
   int32_t *d_acol = nullptr;
   int fi_v3 = 0;                                     // option "fanin_v3" (slower; kept for experiments)
   int fi_mma = 0;                                    // option "fanin_dmma" (bitwise-equal results; slower here)
+  int fi_tc = 0;                                     // option "fanin_tc": DMMA update kernels (1/2: per-source k_fi_upd_tc for targets >= 32 rows / all regular items; 3/4: K-concatenated k_fi_upd_kc, same split)
   std::vector<int32_t> fi_smax, fi_mmax;
   int sm_count = 148;
   // single-instance hub rows (ROWROW path): programs + per-level hub node lists
@@ -528,6 +533,10 @@ int hy_set_option(hy_handle *h, const char *name, int64_t value) {
   }
   if (std::string(name) == "fanin_v3") {
     h->fi_v3 = value != 0;
+    return HY_OK;
+  }
+  if (std::string(name) == "fanin_tc" && value >= 0 && value <= 4) {
+    h->fi_tc = (int)value;
     return HY_OK;
   }
   if (std::string(name) == "fanin_dmma") {
@@ -842,6 +851,8 @@ int hy_upload_fanin_plan(hy_handle *h, const hy_fanin_plan *d) {
   }
   CK(cudaFuncSetAttribute(k_fi_upd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx));
   CK(cudaFuncSetAttribute(k_fi_upd_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx));
+  CK(cudaFuncSetAttribute(k_fi_upd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fi_upd_tc_smem(64)));
+  CK(cudaFuncSetAttribute(k_fi_upd_kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fi_upd_kc_smem()));
   CK(cudaFuncSetAttribute(k_fi_upd_pk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx));
   CK(cudaFuncSetAttribute(k_fi_upd3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fi_upd3_smem(64)));
   CK(cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, h->device));
@@ -900,7 +911,7 @@ static int run_fanin(hy_handle *h, const CallP &P, cudaStream_t st) {
     if (nup) {
       const size_t sm = fi_upd_smem(h->fi_smax[l], h->fi_mmax[l]);
       const int reg = (int)h->fi_upreg[l];
-      const int split = h->fi_mma ? (int)h->fi_upbig[l] : (int)h->fi_up[l + 1];
+      const int split = (h->fi_mma || h->fi_tc == 1 || h->fi_tc == 3) ? (int)h->fi_upbig[l] : (int)h->fi_up[l + 1];
       const int npk = reg - (int)h->fi_up[l];
       const int nbig = (int)h->fi_up[l + 1] - split;
       if (npk) {
@@ -912,7 +923,13 @@ static int run_fanin(hy_handle *h, const CallP &P, cudaStream_t st) {
         k_fi_upd_w<<<(rs - reg + 7) / 8, 256, 0, st>>>(h->S, P, h->fi, reg, rs - reg);
         h->launches++;
       }
-      if (split > rs) {
+      if (split > rs && h->fi_tc == 4) {
+        k_fi_upd_kc<<<split - rs, 256, fi_upd_kc_smem(), st>>>(h->S, P, h->fi, rs);
+        h->launches++;
+      } else if (split > rs && h->fi_tc == 2) {
+        k_fi_upd_tc<<<split - rs, 256, fi_upd_tc_smem(h->fi_smax[l]), st>>>(h->S, P, h->fi, rs, h->fi_smax[l]);
+        h->launches++;
+      } else if (split > rs) {
         const int nsm2 = split - rs;
         if (h->fi_v3)
           k_fi_upd3<<<nsm2, 256, fi_upd3_smem(h->fi_smax[l]), st>>>(h->S, P, h->fi, rs, h->fi_smax[l],
@@ -921,7 +938,13 @@ static int run_fanin(hy_handle *h, const CallP &P, cudaStream_t st) {
           k_fi_upd<<<nsm2, 256, sm, st>>>(h->S, P, h->fi, rs, h->fi_smax[l], h->fi_mmax[l]);
         h->launches++;
       }
-      if (nbig) {
+      if (nbig && h->fi_tc == 3) {
+        k_fi_upd_kc<<<nbig, 256, fi_upd_kc_smem(), st>>>(h->S, P, h->fi, split);
+        h->launches++;
+      } else if (nbig && h->fi_tc == 1) {
+        k_fi_upd_tc<<<nbig, 256, fi_upd_tc_smem(h->fi_smax[l]), st>>>(h->S, P, h->fi, split, h->fi_smax[l]);
+        h->launches++;
+      } else if (nbig) {
         k_fi_upd_mma<<<nbig, 256, sm, st>>>(h->S, P, h->fi, split, h->fi_smax[l], h->fi_mmax[l]);
         h->launches++;
       }

@@ -799,6 +799,291 @@ __global__ void __launch_bounds__(FI_THREADS) k_fi_upd_mma(DevSym S, CallP P, Fa
   }
 }
 
+// ---------------------------------------------------------------------------- updates, DMMA
+// k_fi_upd with every per-source contraction on the FP64 tensor cores
+// (mma.sync.aligned.m8n8k4 f64 -> SASS DMMA).  Warp tiles: 16 x 32 (4 x 2 warps
+// over the 64 x 64 output) when the source covers more than 32 tile columns, else
+// 8 x 32 (8 warps over the rows).  Each warp keeps its A fragments (one per 8-row
+// block) and B fragments (one per 8-column block) in registers per k-step of 4, so
+// a k-step costs 2 + 4 shared loads for 8 DMMAs (0.75 B/FMA vs 6 B/FMA for the 4x2
+// FFMA register tile).  Staging is warp-per-row (one 256-byte line per load), no
+// index divisions; the shared pitches (36 / 68 doubles) make the fragment loads
+// conflict-free.  Per output element DMMA applies its four products as chained
+// FMAs in k order, so the result equals k_fi_upd's bit for bit (tested).
+constexpr int TC_XLD = 36;
+constexpr int TC_ULD = 68;
+size_t fi_upd_tc_smem(int smax) {
+  return ((size_t)smax * FI_TILE + (size_t)smax * TC_XLD + (size_t)FI_KC * TC_ULD) * sizeof(double);
+}
+
+__device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(FI_THREADS, 3) k_fi_upd_tc(DevSym S, CallP P, FaninDev D, int base,
+                                                          int Smax) {
+  extern __shared__ __align__(16) double fs[];
+  __shared__ int tcol[FI_TILE];
+  __shared__ int spos[FI_TILE];
+  const int j = base + blockIdx.x;
+  const int T = D.up_t[j];
+  const int c0 = D.up_c0[j], c1 = D.up_c1[j];
+  const int tw = c1 - c0;
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31, kq = lane & 3, lr = lane >> 2;
+  const int r = (int)S.first[T];
+  const int s = (int)(S.first[T + 1] - r);
+  const int64_t tc0 = S.colptr[T];
+  const int W = (int)(S.colptr[T + 1] - tc0);
+  double *Pm = P.F + S.valoff[T];
+  double *acc = fs;                             // s x FI_TILE
+  double *Xs = acc + (size_t)Smax * FI_TILE;    // Smax x TC_XLD
+  double *Ut = Xs + (size_t)Smax * TC_XLD;      // FI_KC x TC_ULD
+  for (int c = tid; c < tw; c += FI_THREADS) tcol[c] = S.cols[tc0 + c0 + c];
+  for (int t = warp; t < s; t += FI_THREADS / 32) {
+    const double *src = Pm + (int64_t)t * W + c0;
+    acc[t * FI_TILE + lane] = lane < tw ? src[lane] : 0.0;
+    acc[t * FI_TILE + lane + 32] = lane + 32 < tw ? src[lane + 32] : 0.0;
+  }
+  for (int64_t z = D.up_ptr[j]; z < D.up_ptr[j + 1]; ++z) {
+    const int v = D.src_v[z];
+    const int q0 = D.src_q0[z];
+    const int nq = D.src_q1[z] - q0;
+    const int vf = (int)S.first[v];
+    const int vs = (int)(S.first[v + 1] - vf);
+    const int64_t vc0 = S.colptr[v];
+    const int vW = (int)(S.colptr[v + 1] - vc0);
+    const double *vb = P.F + S.valoff[v];
+    const int pb0 = D.src_pb[z];
+    const int tb0 = D.src_tb[z];
+    const int m = vs - tb0;
+    const int qbase = S.nl[v] + vs + q0;
+    const int ncw = (nq + 7) & ~7;
+    // warp tile
+    const bool wide = nq > 32;
+    const int wr0 = wide ? (warp >> 1) * 16 : warp * 8;
+    const int wc0 = wide ? (warp & 1) * 32 : 0;
+    const int nrb = wide ? 2 : 1;
+    double d[2][4][2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) d[a][b][0] = d[a][b][1] = 0.0;
+    bool ra[2], ca[4];
+#pragma unroll
+    for (int a = 0; a < 2; ++a) ra[a] = a < nrb && wr0 + 8 * a < s;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) ca[b] = wc0 + 8 * b < nq;
+    __syncthreads();
+    if (tid < nq) spos[tid] = lower_bound_i32(tcol, 0, tw, S.cols[vc0 + qbase + tid]);
+    for (int k0 = 0; k0 < m; k0 += FI_KC) {
+      const int kc = min(FI_KC, m - k0);
+      const int kc4 = (kc + 3) & ~3;
+      if (k0) __syncthreads();
+      for (int t = warp; t < s; t += FI_THREADS / 32)
+        if (lane < kc4) Xs[t * TC_XLD + lane] = lane < kc ? Pm[(int64_t)t * W + pb0 + k0 + lane] : 0.0;
+      for (int a = warp; a < kc4; a += FI_THREADS / 32) {
+        const double *urow = vb + (int64_t)(tb0 + k0 + a) * vW + qbase;
+        const bool ok = a < kc;
+        if (lane < ncw) Ut[a * TC_ULD + lane] = (ok && lane < nq) ? urow[lane] : 0.0;
+        if (lane + 32 < ncw) Ut[a * TC_ULD + lane + 32] = (ok && lane + 32 < nq) ? urow[lane + 32] : 0.0;
+      }
+      __syncthreads();
+      if (ra[0]) {
+        for (int k = 0; k < kc4; k += 4) {
+          double av[2], bv[4];
+#pragma unroll
+          for (int a = 0; a < 2; ++a) av[a] = ra[a] ? Xs[(wr0 + 8 * a + lr) * TC_XLD + k + kq] : 0.0;
+#pragma unroll
+          for (int b = 0; b < 4; ++b) bv[b] = ca[b] ? Ut[(k + kq) * TC_ULD + wc0 + 8 * b + lr] : 0.0;
+#pragma unroll
+          for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+              if (ra[a] && ca[b]) dmma884(d[a][b], av[a], bv[b]);
+        }
+      }
+    }
+    // scatter-subtract into the staged tile (row lr of each 8-row block, columns
+    // 2*kq, 2*kq+1 of each 8-column block)
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+      const int t = wr0 + 8 * a + lr;
+      if (!ra[a] || t >= s) continue;
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int c = wc0 + 8 * b + 2 * kq + e;
+          if (ca[b] && c < nq) acc[t * FI_TILE + spos[c]] -= d[a][b][e];
+        }
+    }
+  }
+  __syncthreads();
+  for (int t = warp; t < s; t += FI_THREADS / 32) {
+    double *dst = Pm + (int64_t)t * W + c0;
+    if (lane < tw) dst[lane] = acc[t * FI_TILE + lane];
+    if (lane + 32 < tw) dst[lane + 32] = acc[t * FI_TILE + lane + 32];
+  }
+}
+
+// ---------------------------------------------------------------------------- updates, K-concatenated DMMA
+// One CTA per update item (target T, 64-column tile).  The K dimension is the
+// concatenation of the item's sources' block rows, in chunks of <= FI_KC rows that
+// never straddle a source; each chunk's U rows are scattered into the tile's
+// 64-column space (cp.async with zero-fill for the columns the source does not
+// cover), so the whole item is ONE register-resident GEMM
+//     T[:, tile] -= X_item (s x K) * U_item (K x 64)
+// on DMMA (mma.sync.m8n8k4 f64), warp tile 16 x 32, A/B fragments loaded once per
+// k-step of 4 (2 + 4 shared loads per 8 DMMAs).  Chunk i+1 is in flight (cp.async,
+// double-buffered) while chunk i is multiplied; the source -> tile column maps of a
+// batch of sources are computed once up front (one parallel binary-search pass),
+// so no per-source round trip or barrier sits between the tensor-core steps.  The
+// target tile is read-modify-written once, straight from the accumulator
+// fragments.  Summation order per element: all sources' products chained in
+// ascending (source, row) order, then one subtraction — the packed kernel's order.
+constexpr int KC_XLD = 36;     // pitches == 4 (mod 16) doubles: conflict-free fragments
+constexpr int KC_ULD = 68;
+constexpr int KC_NSB = 16;     // sources per column-map batch
+size_t fi_upd_kc_smem() {
+  return (2 * ((size_t)64 * KC_XLD + (size_t)FI_KC * KC_ULD)) * sizeof(double) + (size_t)KC_NSB * 64;
+}
+
+__device__ __forceinline__ void kc_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void kc_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void kc_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void cp_async8z(double *smem_dst, const double *gsrc, bool ok) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  const int n = ok ? 8 : 0;   // src-size 0: the 8 bytes are zero-filled, nothing is read
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(gsrc), "r"(n) : "memory");
+}
+
+__global__ void __launch_bounds__(FI_THREADS, 3) k_fi_upd_kc(DevSym S, CallP P, FaninDev D, int base) {
+  extern __shared__ __align__(16) double fs[];
+  __shared__ int tcol[FI_TILE];
+  __shared__ int64_t s_vb[KC_NSB];
+  __shared__ int s_vW[KC_NSB], s_qb[KC_NSB], s_pb[KC_NSB], s_tb[KC_NSB], s_m[KC_NSB];
+  const int j = base + blockIdx.x;
+  const int T = D.up_t[j];
+  const int c0 = D.up_c0[j], c1 = D.up_c1[j];
+  const int tw = c1 - c0;
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31, kq = lane & 3, lr = lane >> 2;
+  const int r = (int)S.first[T];
+  const int s = (int)(S.first[T + 1] - r);
+  const int64_t tc0 = S.colptr[T];
+  const int W = (int)(S.colptr[T + 1] - tc0);
+  double *Pm = P.F + S.valoff[T];
+  constexpr int KC_BUF = 64 * KC_XLD + FI_KC * KC_ULD;   // one stage: X chunk, then U chunk
+  int8_t *inv = reinterpret_cast<int8_t *>(fs + 2 * KC_BUF);   // [KC_NSB][64]
+  for (int c = tid; c < tw; c += FI_THREADS) tcol[c] = S.cols[tc0 + c0 + c];
+  const int wr0 = (warp >> 1) * 16, wc0 = (warp & 1) * 32;
+  bool ra[2], ca[4];
+#pragma unroll
+  for (int a = 0; a < 2; ++a) ra[a] = wr0 + 8 * a < s;
+#pragma unroll
+  for (int b = 0; b < 4; ++b) ca[b] = wc0 + 8 * b < tw;
+  double d[2][4][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) d[a][b][0] = d[a][b][1] = 0.0;
+
+  const int64_t zb = D.up_ptr[j], ze = D.up_ptr[j + 1];
+  for (int64_t zb0 = zb; zb0 < ze; zb0 += KC_NSB) {
+    const int nsb = (int)(ze - zb0 < KC_NSB ? ze - zb0 : KC_NSB);
+    __syncthreads();   // previous batch's chunks are consumed; tcol visible
+    // per-source metadata and tile column maps for this batch
+    if (tid < nsb) {
+      const int64_t z = zb0 + tid;
+      const int v = D.src_v[z];
+      const int vs = (int)(S.first[v + 1] - S.first[v]);
+      const int tb0 = D.src_tb[z];
+      s_vb[tid] = S.valoff[v];
+      s_vW[tid] = (int)(S.colptr[v + 1] - S.colptr[v]);
+      s_qb[tid] = S.nl[v] + vs + D.src_q0[z];
+      s_pb[tid] = D.src_pb[z];
+      s_tb[tid] = tb0;
+      s_m[tid] = vs - tb0;
+    }
+    for (int q = tid; q < nsb * 64; q += FI_THREADS) inv[q] = -1;
+    __syncthreads();
+    for (int k = warp; k < nsb; k += FI_THREADS / 32) {
+      const int64_t z = zb0 + k;
+      const int v = D.src_v[z];
+      const int nq = D.src_q1[z] - D.src_q0[z];
+      const int64_t vc = S.colptr[v] + s_qb[k];
+      for (int c = lane; c < nq; c += 32) inv[k * 64 + lower_bound_i32(tcol, 0, tw, S.cols[vc + c])] = (int8_t)c;
+    }
+    __syncthreads();
+    // chunk sequence of the batch: (source k, rows [k0, k0 + kc))
+    auto issue = [&](int k, int k0, int buf) {
+      const int kc = min(FI_KC, s_m[k] - k0);
+      const double *xs = Pm + s_pb[k] + k0;
+      double *X = fs + buf * KC_BUF;
+      for (int t = warp; t < s; t += FI_THREADS / 32)
+        cp_async8z(X + t * KC_XLD + lane, xs + (int64_t)t * W + (lane < kc ? lane : 0), lane < kc);
+      const double *ub = P.F + s_vb[k] + (int64_t)(s_tb[k] + k0) * s_vW[k] + s_qb[k];
+      double *U = fs + buf * KC_BUF + 64 * KC_XLD;
+      const int i0 = inv[k * 64 + lane], i1 = inv[k * 64 + lane + 32];
+      for (int a = warp; a < FI_KC; a += FI_THREADS / 32) {
+        const double *ur = ub + (int64_t)(a < kc ? a : 0) * s_vW[k];
+        cp_async8z(U + a * KC_ULD + lane, ur + (i0 >= 0 ? i0 : 0), a < kc && i0 >= 0);
+        cp_async8z(U + a * KC_ULD + lane + 32, ur + (i1 >= 0 ? i1 : 0), a < kc && i1 >= 0);
+      }
+    };
+    int ck = 0, ck0 = 0, buf = 0;       // chunk being computed
+    issue(0, 0, 0);
+    kc_commit();
+    for (;;) {
+      // next chunk
+      int nk = ck, nk0 = ck0 + FI_KC;
+      if (nk0 >= s_m[nk]) { ++nk; nk0 = 0; }
+      const bool more = nk < nsb;
+      if (more) issue(nk, nk0, buf ^ 1);
+      kc_commit();
+      kc_wait1();
+      __syncthreads();
+      const int kc = min(FI_KC, s_m[ck] - ck0);
+      const int kc4 = (kc + 3) & ~3;
+      const double *X = fs + buf * KC_BUF, *U = X + 64 * KC_XLD;
+      if (ra[0])
+        for (int k = 0; k < kc4; k += 4) {
+          double av[2], bv[4];
+#pragma unroll
+          for (int a = 0; a < 2; ++a) av[a] = ra[a] ? X[(wr0 + 8 * a + lr) * KC_XLD + k + kq] : 0.0;
+#pragma unroll
+          for (int b = 0; b < 4; ++b) bv[b] = ca[b] ? U[(k + kq) * KC_ULD + wc0 + 8 * b + lr] : 0.0;
+#pragma unroll
+          for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+              if (ra[a] && ca[b]) dmma884(d[a][b], av[a], bv[b]);
+        }
+      __syncthreads();   // buffer `buf` free for the chunk after next
+      if (!more) break;
+      ck = nk; ck0 = nk0; buf ^= 1;
+    }
+  }
+  kc_wait0();
+  // T[:, tile] -= product (row lr of each 8-row block, columns 2*kq, 2*kq+1)
+#pragma unroll
+  for (int a = 0; a < 2; ++a) {
+    const int t = wr0 + 8 * a + lr;
+    if (!ra[a] || t >= s) continue;
+    double *prow = Pm + (int64_t)t * W + c0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = wc0 + 8 * b + 2 * kq + e;
+        if (ca[b] && c < tw) prow[c] -= d[a][b][e];
+      }
+  }
+}
+
 // ---------------------------------------------------------------------------- updates v3
 // Per item: the K dimension is the concatenation of its sources' block rows, cut
 // into chunks of <= FI_KC rows that never straddle a source.  Chunk c+1 is copied

@@ -16,7 +16,7 @@ dv = torch.from_numpy(np.array(p.A.values)).cuda()
 f = api.factorize_analysis(an, dv)
 ctx = f._ctx
 opt = os.environ.get("SWEEP_OPT", "fanin_dmma")
-for v in (1, 0, 1):
+for v in [int(x) for x in os.environ.get("SWEEP_VALS", "1,0,1").split(",")]:
     ctx.set_option(opt, v)
     ts = []
     for _ in range(3):
