@@ -258,7 +258,7 @@ struct hy_handle {
   int32_t *d_acol = nullptr;
   int fi_v3 = 0;                                     // option "fanin_v3" (slower; kept for experiments)
   int fi_mma = 0;                                    // option "fanin_dmma" (bitwise-equal results; slower here)
-  int fi_tc = 0;                                     // option "fanin_tc": DMMA update kernels (1/2: per-source k_fi_upd_tc for targets >= 32 rows / all regular items; 3/4: K-concatenated k_fi_upd_kc, same split)
+  int fi_tc = 4;                                     // option "fanin_tc": DMMA update kernels (1/2: per-source k_fi_upd_tc for targets >= 32 rows / all regular items; 3/4: K-concatenated k_fi_upd_kc, same split)
   std::vector<int32_t> fi_smax, fi_mmax;
   int sm_count = 148;
   // single-instance hub rows (ROWROW path): programs + per-level hub node lists

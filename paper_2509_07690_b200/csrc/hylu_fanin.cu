@@ -963,6 +963,9 @@ __device__ __forceinline__ void cp_async8z(double *smem_dst, const double *gsrc,
 __global__ void __launch_bounds__(FI_THREADS, 3) k_fi_upd_kc(DevSym S, CallP P, FaninDev D, int base) {
   extern __shared__ __align__(16) double fs[];
   __shared__ int tcol[FI_TILE];
+  __shared__ int8_t cidx[FI_TILE];     // tile column -> compact column (-1: untouched)
+  __shared__ int8_t ucol[FI_TILE];     // compact column -> tile column
+  __shared__ int s_nu;
   __shared__ int64_t s_vb[KC_NSB];
   __shared__ int s_vW[KC_NSB], s_qb[KC_NSB], s_pb[KC_NSB], s_tb[KC_NSB], s_m[KC_NSB];
   const int j = base + blockIdx.x;
@@ -977,25 +980,80 @@ __global__ void __launch_bounds__(FI_THREADS, 3) k_fi_upd_kc(DevSym S, CallP P, 
   const int W = (int)(S.colptr[T + 1] - tc0);
   double *Pm = P.F + S.valoff[T];
   constexpr int KC_BUF = 64 * KC_XLD + FI_KC * KC_ULD;   // one stage: X chunk, then U chunk
-  int8_t *inv = reinterpret_cast<int8_t *>(fs + 2 * KC_BUF);   // [KC_NSB][64]
+  int8_t *inv = reinterpret_cast<int8_t *>(fs + 2 * KC_BUF);   // [KC_NSB][64] source col -> compact col
+  const int64_t zb = D.up_ptr[j], ze = D.up_ptr[j + 1];
+  const bool compact = ze - zb <= KC_NSB;
   for (int c = tid; c < tw; c += FI_THREADS) tcol[c] = S.cols[tc0 + c0 + c];
-  const int wr0 = (warp >> 1) * 16, wc0 = (warp & 1) * 32;
+  if (tid < FI_TILE) cidx[tid] = compact ? -1 : (int8_t)tid;
+  __syncthreads();
+  if (compact) {
+    // tile columns any source touches -> compact column space [0, nu); the source
+    // column maps are written with compact indices (inv doubles as scratch for the
+    // tile positions first)
+    for (int k = warp; k < (int)(ze - zb); k += FI_THREADS / 32) {
+      const int64_t z = zb + k;
+      const int v = D.src_v[z];
+      const int nq = D.src_q1[z] - D.src_q0[z];
+      const int vs = (int)(S.first[v + 1] - S.first[v]);
+      const int64_t vc = S.colptr[v] + S.nl[v] + vs + D.src_q0[z];
+      for (int c = lane; c < 64; c += 32) {
+        int pos = -1;
+        if (c < nq) {
+          pos = lower_bound_i32(tcol, 0, tw, S.cols[vc + c]);
+          cidx[pos] = 1;
+        }
+        inv[k * 64 + c] = (int8_t)pos;
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {
+      const bool t0 = cidx[lane] == 1, t1 = cidx[lane + 32] == 1;
+      const unsigned m0 = __ballot_sync(HY_FULL, t0), m1 = __ballot_sync(HY_FULL, t1);
+      const int below = __popc(m0 & ((1u << lane) - 1));
+      const int i0 = below, i1 = __popc(m0) + __popc(m1 & ((1u << lane) - 1));
+      cidx[lane] = t0 ? (int8_t)i0 : -1;
+      cidx[lane + 32] = t1 ? (int8_t)i1 : -1;
+      if (t0) ucol[i0] = (int8_t)lane;
+      if (t1) ucol[i1] = (int8_t)(lane + 32);
+      if (lane == 0) s_nu = __popc(m0) + __popc(m1);
+    }
+    __syncthreads();
+    // inv[k][tile pos] -> inv[k][compact col] = source col
+    for (int k = warp; k < (int)(ze - zb); k += FI_THREADS / 32) {
+      const int p0 = inv[k * 64 + lane], p1 = inv[k * 64 + lane + 32];
+      __syncwarp();
+      inv[k * 64 + lane] = -1;
+      inv[k * 64 + lane + 32] = -1;
+      __syncwarp();
+      if (p0 >= 0) inv[k * 64 + cidx[p0]] = (int8_t)lane;
+      if (p1 >= 0) inv[k * 64 + cidx[p1]] = (int8_t)(lane + 32);
+    }
+  } else {
+    if (tid < FI_TILE) ucol[tid] = (int8_t)tid;
+    if (tid == 0) s_nu = tw;
+  }
+  __syncthreads();
+  const int nu = s_nu;
+  // warp tiles over the s x nu product: 8 x 32 (8 warps over the rows) when the
+  // item touches <= 32 columns, else 16 x 32 (4 x 2 warps)
+  const bool narrow = nu <= 32;
+  const int wr0 = narrow ? warp * 8 : (warp >> 1) * 16;
+  const int wc0 = narrow ? 0 : (warp & 1) * 32;
   bool ra[2], ca[4];
+  ra[0] = wr0 < s;
+  ra[1] = !narrow && wr0 + 8 < s;
 #pragma unroll
-  for (int a = 0; a < 2; ++a) ra[a] = wr0 + 8 * a < s;
-#pragma unroll
-  for (int b = 0; b < 4; ++b) ca[b] = wc0 + 8 * b < tw;
+  for (int b = 0; b < 4; ++b) ca[b] = wc0 + 8 * b < nu;
   double d[2][4][2];
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) d[a][b][0] = d[a][b][1] = 0.0;
 
-  const int64_t zb = D.up_ptr[j], ze = D.up_ptr[j + 1];
   for (int64_t zb0 = zb; zb0 < ze; zb0 += KC_NSB) {
     const int nsb = (int)(ze - zb0 < KC_NSB ? ze - zb0 : KC_NSB);
-    __syncthreads();   // previous batch's chunks are consumed; tcol visible
-    // per-source metadata and tile column maps for this batch
+    const bool last_batch = zb0 + KC_NSB >= ze;
+    if (zb0 != zb) __syncthreads();   // previous batch's chunks consumed
     if (tid < nsb) {
       const int64_t z = zb0 + tid;
       const int v = D.src_v[z];
@@ -1008,17 +1066,18 @@ __global__ void __launch_bounds__(FI_THREADS, 3) k_fi_upd_kc(DevSym S, CallP P, 
       s_tb[tid] = tb0;
       s_m[tid] = vs - tb0;
     }
-    for (int q = tid; q < nsb * 64; q += FI_THREADS) inv[q] = -1;
-    __syncthreads();
-    for (int k = warp; k < nsb; k += FI_THREADS / 32) {
-      const int64_t z = zb0 + k;
-      const int v = D.src_v[z];
-      const int nq = D.src_q1[z] - D.src_q0[z];
-      const int64_t vc = S.colptr[v] + s_qb[k];
-      for (int c = lane; c < nq; c += 32) inv[k * 64 + lower_bound_i32(tcol, 0, tw, S.cols[vc + c])] = (int8_t)c;
+    if (!compact) {
+      for (int q = tid; q < nsb * 64; q += FI_THREADS) inv[q] = -1;
+      __syncthreads();
+      for (int k = warp; k < nsb; k += FI_THREADS / 32) {
+        const int64_t z = zb0 + k;
+        const int v = D.src_v[z];
+        const int nq = D.src_q1[z] - D.src_q0[z];
+        const int64_t vc = S.colptr[v] + s_qb[k];
+        for (int c = lane; c < nq; c += 32) inv[k * 64 + lower_bound_i32(tcol, 0, tw, S.cols[vc + c])] = (int8_t)c;
+      }
     }
     __syncthreads();
-    // chunk sequence of the batch: (source k, rows [k0, k0 + kc))
     auto issue = [&](int k, int k0, int buf) {
       const int kc = min(FI_KC, s_m[k] - k0);
       const double *xs = Pm + s_pb[k] + k0;
@@ -1026,23 +1085,33 @@ __global__ void __launch_bounds__(FI_THREADS, 3) k_fi_upd_kc(DevSym S, CallP P, 
       for (int t = warp; t < s; t += FI_THREADS / 32)
         cp_async8z(X + t * KC_XLD + lane, xs + (int64_t)t * W + (lane < kc ? lane : 0), lane < kc);
       const double *ub = P.F + s_vb[k] + (int64_t)(s_tb[k] + k0) * s_vW[k] + s_qb[k];
-      double *U = fs + buf * KC_BUF + 64 * KC_XLD;
+      double *U = X + 64 * KC_XLD;
       const int i0 = inv[k * 64 + lane], i1 = inv[k * 64 + lane + 32];
+      const bool w1 = lane + 32 < nu;   // compact columns beyond nu are never read
       for (int a = warp; a < FI_KC; a += FI_THREADS / 32) {
         const double *ur = ub + (int64_t)(a < kc ? a : 0) * s_vW[k];
         cp_async8z(U + a * KC_ULD + lane, ur + (i0 >= 0 ? i0 : 0), a < kc && i0 >= 0);
-        cp_async8z(U + a * KC_ULD + lane + 32, ur + (i1 >= 0 ? i1 : 0), a < kc && i1 >= 0);
+        if (w1) cp_async8z(U + a * KC_ULD + lane + 32, ur + (i1 >= 0 ? i1 : 0), a < kc && i1 >= 0);
       }
     };
     int ck = 0, ck0 = 0, buf = 0;       // chunk being computed
     issue(0, 0, 0);
     kc_commit();
     for (;;) {
-      // next chunk
       int nk = ck, nk0 = ck0 + FI_KC;
       if (nk0 >= s_m[nk]) { ++nk; nk0 = 0; }
       const bool more = nk < nsb;
-      if (more) issue(nk, nk0, buf ^ 1);
+      if (more) {
+        issue(nk, nk0, buf ^ 1);
+      } else if (last_batch) {
+        // the target's touched tile values, into the free stage, for the epilogue
+        double *Tv = fs + (buf ^ 1) * KC_BUF;
+        for (int t = warp; t < s; t += FI_THREADS / 32) {
+          const double *prow = Pm + (int64_t)t * W + c0;
+          if (lane < nu) cp_async8z(Tv + t * 64 + lane, prow + ucol[lane], true);
+          if (lane + 32 < nu) cp_async8z(Tv + t * 64 + lane + 32, prow + ucol[lane + 32], true);
+        }
+      }
       kc_commit();
       kc_wait1();
       __syncthreads();
@@ -1062,25 +1131,29 @@ __global__ void __launch_bounds__(FI_THREADS, 3) k_fi_upd_kc(DevSym S, CallP P, 
             for (int b = 0; b < 4; ++b)
               if (ra[a] && ca[b]) dmma884(d[a][b], av[a], bv[b]);
         }
-      __syncthreads();   // buffer `buf` free for the chunk after next
       if (!more) break;
+      __syncthreads();   // buffer `buf` free for the chunk after next
       ck = nk; ck0 = nk0; buf ^= 1;
     }
-  }
-  kc_wait0();
-  // T[:, tile] -= product (row lr of each 8-row block, columns 2*kq, 2*kq+1)
+    if (last_batch) {
+      kc_wait0();
+      __syncthreads();
+      // T[:, tile] -= product (row lr of each 8-row block, compact columns 2*kq, 2*kq+1)
+      const double *Tv = fs + (buf ^ 1) * KC_BUF;
 #pragma unroll
-  for (int a = 0; a < 2; ++a) {
-    const int t = wr0 + 8 * a + lr;
-    if (!ra[a] || t >= s) continue;
-    double *prow = Pm + (int64_t)t * W + c0;
+      for (int a = 0; a < 2; ++a) {
+        const int t = wr0 + 8 * a + lr;
+        if (!ra[a] || t >= s) continue;
+        double *prow = Pm + (int64_t)t * W + c0;
 #pragma unroll
-    for (int b = 0; b < 4; ++b)
+        for (int b = 0; b < 4; ++b)
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int c = wc0 + 8 * b + 2 * kq + e;
-        if (ca[b] && c < tw) prow[c] -= d[a][b][e];
+          for (int e = 0; e < 2; ++e) {
+            const int c = wc0 + 8 * b + 2 * kq + e;
+            if (ca[b] && c < nu) prow[ucol[c]] = Tv[t * 64 + c] - d[a][b][e];
+          }
       }
+    }
   }
 }
 
