@@ -968,6 +968,7 @@ __global__ void __launch_bounds__(FI_THREADS, 3) k_fi_upd_kc(DevSym S, CallP P, 
   __shared__ int s_nu;
   __shared__ int64_t s_vb[KC_NSB];
   __shared__ int s_vW[KC_NSB], s_qb[KC_NSB], s_pb[KC_NSB], s_tb[KC_NSB], s_m[KC_NSB];
+  __shared__ unsigned s_bm[KC_NSB];   // 8-column blocks (compact space) a source touches
   const int j = base + blockIdx.x;
   const int T = D.up_t[j];
   const int c0 = D.up_c0[j], c1 = D.up_c1[j];
@@ -1078,6 +1079,22 @@ __global__ void __launch_bounds__(FI_THREADS, 3) k_fi_upd_kc(DevSym S, CallP P, 
       }
     }
     __syncthreads();
+    // per source: the compact 8-column blocks it has entries in (its other blocks of
+    // U are zero: those DMMAs are skipped, warp-uniformly)
+    for (int k = warp; k < nsb; k += FI_THREADS / 32) {
+      const unsigned m0 = __ballot_sync(HY_FULL, inv[k * 64 + lane] >= 0);
+      const unsigned m1 = __ballot_sync(HY_FULL, inv[k * 64 + lane + 32] >= 0);
+      if (lane == 0) {
+        unsigned bm = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          if ((m0 >> (8 * b)) & 0xffu) bm |= 1u << b;
+          if ((m1 >> (8 * b)) & 0xffu) bm |= 1u << (b + 4);
+        }
+        s_bm[k] = bm;
+      }
+    }
+    __syncthreads();
     auto issue = [&](int k, int k0, int buf) {
       const int kc = min(FI_KC, s_m[k] - k0);
       const double *xs = Pm + s_pb[k] + k0;
@@ -1118,18 +1135,22 @@ __global__ void __launch_bounds__(FI_THREADS, 3) k_fi_upd_kc(DevSym S, CallP P, 
       const int kc = min(FI_KC, s_m[ck] - ck0);
       const int kc4 = (kc + 3) & ~3;
       const double *X = fs + buf * KC_BUF, *U = X + 64 * KC_XLD;
-      if (ra[0])
+      const unsigned bm = s_bm[ck] >> (wc0 >> 3);
+      bool cb[4];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) cb[b] = ca[b] && ((bm >> b) & 1u);
+      if (ra[0] && (bm & 15u))
         for (int k = 0; k < kc4; k += 4) {
           double av[2], bv[4];
 #pragma unroll
           for (int a = 0; a < 2; ++a) av[a] = ra[a] ? X[(wr0 + 8 * a + lr) * KC_XLD + k + kq] : 0.0;
 #pragma unroll
-          for (int b = 0; b < 4; ++b) bv[b] = ca[b] ? U[(k + kq) * KC_ULD + wc0 + 8 * b + lr] : 0.0;
+          for (int b = 0; b < 4; ++b) bv[b] = cb[b] ? U[(k + kq) * KC_ULD + wc0 + 8 * b + lr] : 0.0;
 #pragma unroll
           for (int a = 0; a < 2; ++a)
 #pragma unroll
             for (int b = 0; b < 4; ++b)
-              if (ra[a] && ca[b]) dmma884(d[a][b], av[a], bv[b]);
+              if (ra[a] && cb[b]) dmma884(d[a][b], av[a], bv[b]);
         }
       if (!more) break;
       __syncthreads();   // buffer `buf` free for the chunk after next
