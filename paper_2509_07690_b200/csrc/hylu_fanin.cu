@@ -996,7 +996,18 @@ __global__ void __launch_bounds__(FI_THREADS, 3) k_fi_upd_kc(DevSym S, CallP P, 
       const int v = D.src_v[z];
       const int nq = D.src_q1[z] - D.src_q0[z];
       const int vs = (int)(S.first[v + 1] - S.first[v]);
-      const int64_t vc = S.colptr[v] + S.nl[v] + vs + D.src_q0[z];
+      const int64_t vcol = S.colptr[v];
+      const int qb = S.nl[v] + vs + D.src_q0[z];
+      const int64_t vc = vcol + qb;
+      if (lane == 0) {   // per-source metadata for the chunk loop (single batch)
+        const int tb0 = D.src_tb[z];
+        s_vb[k] = S.valoff[v];
+        s_vW[k] = (int)(S.colptr[v + 1] - vcol);
+        s_qb[k] = qb;
+        s_pb[k] = D.src_pb[z];
+        s_tb[k] = tb0;
+        s_m[k] = vs - tb0;
+      }
       for (int c = lane; c < 64; c += 32) {
         int pos = -1;
         if (c < nq) {
@@ -1028,6 +1039,19 @@ __global__ void __launch_bounds__(FI_THREADS, 3) k_fi_upd_kc(DevSym S, CallP P, 
       __syncwarp();
       if (p0 >= 0) inv[k * 64 + cidx[p0]] = (int8_t)lane;
       if (p1 >= 0) inv[k * 64 + cidx[p1]] = (int8_t)(lane + 32);
+      __syncwarp();
+      // compact 8-column blocks this source has entries in
+      const unsigned m0 = __ballot_sync(HY_FULL, inv[k * 64 + lane] >= 0);
+      const unsigned m1 = __ballot_sync(HY_FULL, inv[k * 64 + lane + 32] >= 0);
+      if (lane == 0) {
+        unsigned bm = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          if ((m0 >> (8 * b)) & 0xffu) bm |= 1u << b;
+          if ((m1 >> (8 * b)) & 0xffu) bm |= 1u << (b + 4);
+        }
+        s_bm[k] = bm;
+      }
     }
   } else {
     if (tid < FI_TILE) ucol[tid] = (int8_t)tid;
@@ -1055,7 +1079,7 @@ __global__ void __launch_bounds__(FI_THREADS, 3) k_fi_upd_kc(DevSym S, CallP P, 
     const int nsb = (int)(ze - zb0 < KC_NSB ? ze - zb0 : KC_NSB);
     const bool last_batch = zb0 + KC_NSB >= ze;
     if (zb0 != zb) __syncthreads();   // previous batch's chunks consumed
-    if (tid < nsb) {
+    if (!compact && tid < nsb) {
       const int64_t z = zb0 + tid;
       const int v = D.src_v[z];
       const int vs = (int)(S.first[v + 1] - S.first[v]);
@@ -1077,11 +1101,12 @@ __global__ void __launch_bounds__(FI_THREADS, 3) k_fi_upd_kc(DevSym S, CallP P, 
         const int64_t vc = S.colptr[v] + s_qb[k];
         for (int c = lane; c < nq; c += 32) inv[k * 64 + lower_bound_i32(tcol, 0, tw, S.cols[vc + c])] = (int8_t)c;
       }
+      __syncthreads();
     }
-    __syncthreads();
     // per source: the compact 8-column blocks it has entries in (its other blocks of
-    // U are zero: those DMMAs are skipped, warp-uniformly)
-    for (int k = warp; k < nsb; k += FI_THREADS / 32) {
+    // U are zero: those DMMAs are skipped, warp-uniformly); the compact path computed
+    // them with the column maps
+    for (int k = warp; k < nsb && !compact; k += FI_THREADS / 32) {
       const unsigned m0 = __ballot_sync(HY_FULL, inv[k * 64 + lane] >= 0);
       const unsigned m1 = __ballot_sync(HY_FULL, inv[k * 64 + lane + 32] >= 0);
       if (lane == 0) {
@@ -1094,7 +1119,7 @@ __global__ void __launch_bounds__(FI_THREADS, 3) k_fi_upd_kc(DevSym S, CallP P, 
         s_bm[k] = bm;
       }
     }
-    __syncthreads();
+    if (!compact) __syncthreads();   // (compact: published by the barrier after the maps)
     auto issue = [&](int k, int k0, int buf) {
       const int kc = min(FI_KC, s_m[k] - k0);
       const double *xs = Pm + s_pb[k] + k0;

@@ -261,3 +261,98 @@ def test_batched_host_buffers_match_device_path(pipelined):
     torch.cuda.synchronize()
     for k in range(3):
         assert np.array_equal(outs[k][1].numpy(), xs_dev[k])
+
+
+@pytest.mark.parametrize("name", ["c0", "c1"])
+def test_full_size_factor_matches_oracle(name):
+    """BASELINE configs at their full size (c0 n=4096, c1 n=200000): inner_perm equal,
+    L/U within 1e-11, refactorize on unchanged values bitwise equal, residual bound."""
+    p = gen.config(name)
+    an = an_mod.analyze(p.A, SolverConfig(ordering=p.ordering))
+    on = _oracle()
+    ref = on.factorize(an)
+    f = api.factorize_analysis(an)
+    assert np.array_equal(f.host_inner_perm(), ref.inner_perm)
+    assert _rel(f.host_values(), ref.values) <= LU_RTOL
+    f2 = api.refactorize(p.A, f)
+    assert np.array_equal(f2.host_values(), f.host_values())
+    x, _ = api.solve(p.A, f, b=p.b)
+    assert np.linalg.norm(refmatrix.spmv(p.A, x) - p.b) / np.linalg.norm(p.b) <= RES_TOL
+
+
+def test_batched_full_n_matches_oracle():
+    """c4 recipe at its full per-instance size (n = 20000, 3 hubs of 2000 entries) on
+    a 40-instance batch (a partial last group): factor values of sampled instances
+    within 1e-11 of the oracle's refactorize, solutions within 1e-9, perturbation
+    counts equal."""
+    import torch
+    bp = gen.circuit_batch(40)
+    an = an_mod.analyze(bp.A0, SolverConfig(ordering="amd"))
+    on = _oracle()
+    prior = api.factorize_analysis(an)
+    oprior = on.factorize(an)
+    br = api.BatchedRefactorizer(prior)
+    x, npert = br.run(torch.from_numpy(bp.values).cuda(), torch.from_numpy(bp.rhs).cuda())
+    Xo, npo = on.refactor_solve_batch(an, oprior, bp.values, bp.rhs)
+    assert _rel(x.cpu().numpy(), Xo) <= 1e-9
+    assert np.array_equal(npert.cpu().numpy(), npo)
+    for b in (0, 33, 39):
+        ref = on.factorize(an, bp.values[b], prior=oprior)
+        assert _rel(br.factor_values(b).cpu().numpy(), ref.values) <= LU_RTOL
+
+
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_update_kernel_variants(name):
+    """Sup-sup update kernels: the per-source DMMA kernel (fanin_tc=2) is bitwise equal
+    to the FFMA kernel (DMMA chains its four products per element in k order); the
+    default K-concatenated DMMA kernel (fanin_tc=4) differs only by summation order."""
+    p, an = _analysis(name)
+    on = _oracle()
+    ref = on.factorize(an)
+    f4 = api.factorize_analysis(an)
+    ctx = f4._ctx
+    try:
+        ctx.set_option("fanin_tc", 0)
+        f0 = api.factorize_analysis(an)
+        ctx.set_option("fanin_tc", 2)
+        f2 = api.factorize_analysis(an)
+    finally:
+        ctx.set_option("fanin_tc", 4)
+    v0, v2, v4 = f0.host_values(), f2.host_values(), f4.host_values()
+    assert np.array_equal(v2, v0)
+    assert _rel(v4, v0) <= 1e-12
+    assert _rel(v4, ref.values) <= LU_RTOL
+
+
+def test_api_errors_and_tiny_systems():
+    """Error convention (polylu.errors) and degenerate sizes through the device path."""
+    from paper_2509_07690_b200._ref import errors, SparseMatrixCSR
+    # n = 1
+    A1 = SparseMatrixCSR(1, np.array([0, 1]), np.array([0]), np.array([4.0]))
+    an1 = an_mod.analyze(A1, SolverConfig(ordering="amd"))
+    f1 = api.factorize_analysis(an1)
+    x1, _ = api.solve(A1, f1, b=np.array([2.0]))
+    assert abs(x1[0] - 0.5) <= 1e-15
+    # diagonal matrix: no fill, exact solve
+    n = 50
+    D = SparseMatrixCSR(n, np.arange(n + 1), np.arange(n), np.arange(1.0, n + 1))
+    anD = an_mod.analyze(D, SolverConfig(ordering="amd"))
+    fD = api.factorize_analysis(anD)
+    xD, _ = api.solve(D, fD, b=np.ones(n))
+    assert np.allclose(xD, 1.0 / np.arange(1.0, n + 1), rtol=0, atol=1e-15)
+    # refactorize with a different pattern -> PatternMismatch
+    p, an = _analysis("c0")
+    f = api.factorize_analysis(an)
+    A = p.A
+    rp, ci, va = np.asarray(A.row_ptr), np.asarray(A.col_idx), np.asarray(A.values)
+    drop = next(k for k in range(rp[0], rp[1]) if ci[k] != 0)      # an off-diagonal of row 0
+    keep = np.ones(len(ci), bool)
+    keep[drop] = False
+    rp2 = rp.copy()
+    rp2[1:] -= 1
+    bad = SparseMatrixCSR(A.n, rp2, ci[keep], va[keep])
+    with pytest.raises(errors.PatternMismatch):
+        api.refactorize(bad, f)
+    # rhs of the wrong length -> DimensionMismatch
+    with pytest.raises(errors.DimensionMismatch):
+        api.solve(A, f, b=np.ones(A.n + 1))
