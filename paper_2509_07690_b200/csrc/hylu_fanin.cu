@@ -944,11 +944,22 @@ __global__ void __launch_bounds__(FI_THREADS, 3) k_fi_upd_tc(DevSym S, CallP P, 
 // target tile is read-modify-written once, straight from the accumulator
 // fragments.  Summation order per element: all sources' products chained in
 // ascending (source, row) order, then one subtraction — the packed kernel's order.
-constexpr int KC_XLD = 36;     // pitches == 4 (mod 16) doubles: conflict-free fragments
+
 constexpr int KC_ULD = 68;
 constexpr int KC_NSB = 16;     // sources per column-map batch
+#ifndef KC_CHUNK_DEF
+#define KC_CHUNK_DEF 32
+#endif
+#ifndef KC_MINB_DEF
+#define KC_MINB_DEF 3
+#endif
+constexpr int KC_K = KC_CHUNK_DEF;   // K rows per chunk (<= 32: one lane per X column)
+constexpr int KC_XLD = KC_K + 4;     // pitches == 4 (mod 16) doubles: conflict-free fragments
+// one pipeline stage: an X chunk then a U chunk; it also holds the s x 64 target tile
+// prefetched for the epilogue
+constexpr int KC_STAGE = (64 * KC_XLD + KC_K * KC_ULD) > 64 * 64 ? (64 * KC_XLD + KC_K * KC_ULD) : 64 * 64;
 size_t fi_upd_kc_smem() {
-  return (2 * ((size_t)64 * KC_XLD + (size_t)FI_KC * KC_ULD)) * sizeof(double) + (size_t)KC_NSB * 64;
+  return 2 * (size_t)KC_STAGE * sizeof(double) + (size_t)KC_NSB * 64;
 }
 
 __device__ __forceinline__ void kc_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
@@ -960,7 +971,7 @@ __device__ __forceinline__ void cp_async8z(double *smem_dst, const double *gsrc,
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(gsrc), "r"(n) : "memory");
 }
 
-__global__ void __launch_bounds__(FI_THREADS, 3) k_fi_upd_kc(DevSym S, CallP P, FaninDev D, int base) {
+__global__ void __launch_bounds__(FI_THREADS, KC_MINB_DEF) k_fi_upd_kc(DevSym S, CallP P, FaninDev D, int base) {
   extern __shared__ __align__(16) double fs[];
   __shared__ int tcol[FI_TILE];
   __shared__ int8_t cidx[FI_TILE];     // tile column -> compact column (-1: untouched)
@@ -980,7 +991,7 @@ __global__ void __launch_bounds__(FI_THREADS, 3) k_fi_upd_kc(DevSym S, CallP P, 
   const int64_t tc0 = S.colptr[T];
   const int W = (int)(S.colptr[T + 1] - tc0);
   double *Pm = P.F + S.valoff[T];
-  constexpr int KC_BUF = 64 * KC_XLD + FI_KC * KC_ULD;   // one stage: X chunk, then U chunk
+  constexpr int KC_BUF = KC_STAGE;
   int8_t *inv = reinterpret_cast<int8_t *>(fs + 2 * KC_BUF);   // [KC_NSB][64] source col -> compact col
   const int64_t zb = D.up_ptr[j], ze = D.up_ptr[j + 1];
   const bool compact = ze - zb <= KC_NSB;
@@ -1121,16 +1132,17 @@ __global__ void __launch_bounds__(FI_THREADS, 3) k_fi_upd_kc(DevSym S, CallP P, 
     }
     if (!compact) __syncthreads();   // (compact: published by the barrier after the maps)
     auto issue = [&](int k, int k0, int buf) {
-      const int kc = min(FI_KC, s_m[k] - k0);
+      const int kc = min(KC_K, s_m[k] - k0);
       const double *xs = Pm + s_pb[k] + k0;
       double *X = fs + buf * KC_BUF;
-      for (int t = warp; t < s; t += FI_THREADS / 32)
-        cp_async8z(X + t * KC_XLD + lane, xs + (int64_t)t * W + (lane < kc ? lane : 0), lane < kc);
+      if (lane < KC_K)
+        for (int t = warp; t < s; t += FI_THREADS / 32)
+          cp_async8z(X + t * KC_XLD + lane, xs + (int64_t)t * W + (lane < kc ? lane : 0), lane < kc);
       const double *ub = P.F + s_vb[k] + (int64_t)(s_tb[k] + k0) * s_vW[k] + s_qb[k];
       double *U = X + 64 * KC_XLD;
       const int i0 = inv[k * 64 + lane], i1 = inv[k * 64 + lane + 32];
       const bool w1 = lane + 32 < nu;   // compact columns beyond nu are never read
-      for (int a = warp; a < FI_KC; a += FI_THREADS / 32) {
+      for (int a = warp; a < KC_K; a += FI_THREADS / 32) {
         const double *ur = ub + (int64_t)(a < kc ? a : 0) * s_vW[k];
         cp_async8z(U + a * KC_ULD + lane, ur + (i0 >= 0 ? i0 : 0), a < kc && i0 >= 0);
         if (w1) cp_async8z(U + a * KC_ULD + lane + 32, ur + (i1 >= 0 ? i1 : 0), a < kc && i1 >= 0);
@@ -1140,7 +1152,7 @@ __global__ void __launch_bounds__(FI_THREADS, 3) k_fi_upd_kc(DevSym S, CallP P, 
     issue(0, 0, 0);
     kc_commit();
     for (;;) {
-      int nk = ck, nk0 = ck0 + FI_KC;
+      int nk = ck, nk0 = ck0 + KC_K;
       if (nk0 >= s_m[nk]) { ++nk; nk0 = 0; }
       const bool more = nk < nsb;
       if (more) {
@@ -1157,7 +1169,7 @@ __global__ void __launch_bounds__(FI_THREADS, 3) k_fi_upd_kc(DevSym S, CallP P, 
       kc_commit();
       kc_wait1();
       __syncthreads();
-      const int kc = min(FI_KC, s_m[ck] - ck0);
+      const int kc = min(KC_K, s_m[ck] - ck0);
       const int kc4 = (kc + 3) & ~3;
       const double *X = fs + buf * KC_BUF, *U = X + 64 * KC_XLD;
       const unsigned bm = s_bm[ck] >> (wc0 >> 3);
