@@ -76,6 +76,7 @@ size_t fi_upd_smem(int, int);
 size_t fi_upd_tc_smem(int);
 size_t fi_upd_kc_smem();
 __global__ void k_fi_upd_kc(DevSym, CallP, FaninDev, int);
+__global__ void k_fi_upd_kcp(DevSym, CallP, FaninDev, int);
 __global__ void k_fi_upd_tc(DevSym, CallP, FaninDev, int, int);
 size_t pipe_smem_bytes(bool staged);
 size_t hub_smem_bytes();
@@ -258,7 +259,7 @@ struct hy_handle {
   int32_t *d_acol = nullptr;
   int fi_v3 = 0;                                     // option "fanin_v3" (slower; kept for experiments)
   int fi_mma = 0;                                    // option "fanin_dmma" (bitwise-equal results; slower here)
-  int fi_tc = 4;                                     // option "fanin_tc": DMMA update kernels (1/2: per-source k_fi_upd_tc for targets >= 32 rows / all regular items; 3/4: K-concatenated k_fi_upd_kc, same split)
+  int fi_tc = 5;                                     // option "fanin_tc": DMMA update kernels (1/2: per-source k_fi_upd_tc for targets >= 32 rows / all regular items; 3/4: K-concatenated k_fi_upd_kc, same split; 5 (default): k_fi_upd_kcp for the packed items too)
   std::vector<int32_t> fi_smax, fi_mmax;
   int sm_count = 148;
   // single-instance hub rows (ROWROW path): programs + per-level hub node lists
@@ -535,7 +536,7 @@ int hy_set_option(hy_handle *h, const char *name, int64_t value) {
     h->fi_v3 = value != 0;
     return HY_OK;
   }
-  if (std::string(name) == "fanin_tc" && value >= 0 && value <= 4) {
+  if (std::string(name) == "fanin_tc" && value >= 0 && value <= 5) {
     h->fi_tc = (int)value;
     return HY_OK;
   }
@@ -853,6 +854,7 @@ int hy_upload_fanin_plan(hy_handle *h, const hy_fanin_plan *d) {
   CK(cudaFuncSetAttribute(k_fi_upd_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx));
   CK(cudaFuncSetAttribute(k_fi_upd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fi_upd_tc_smem(64)));
   CK(cudaFuncSetAttribute(k_fi_upd_kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fi_upd_kc_smem()));
+  CK(cudaFuncSetAttribute(k_fi_upd_kcp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fi_upd_kc_smem()));
   CK(cudaFuncSetAttribute(k_fi_upd_pk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx));
   CK(cudaFuncSetAttribute(k_fi_upd3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fi_upd3_smem(64)));
   CK(cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, h->device));
@@ -914,7 +916,10 @@ static int run_fanin(hy_handle *h, const CallP &P, cudaStream_t st) {
       const int split = (h->fi_mma || h->fi_tc == 1 || h->fi_tc == 3) ? (int)h->fi_upbig[l] : (int)h->fi_up[l + 1];
       const int npk = reg - (int)h->fi_up[l];
       const int nbig = (int)h->fi_up[l + 1] - split;
-      if (npk) {
+      if (npk && h->fi_tc == 5) {
+        k_fi_upd_kcp<<<npk, 256, fi_upd_kc_smem(), st>>>(h->S, P, h->fi, (int)h->fi_up[l]);
+        h->launches++;
+      } else if (npk) {
         k_fi_upd_pk<<<npk, 256, sm, st>>>(h->S, P, h->fi, (int)h->fi_up[l], h->fi_smax[l], h->fi_mmax[l]);
         h->launches++;
       }
@@ -923,7 +928,7 @@ static int run_fanin(hy_handle *h, const CallP &P, cudaStream_t st) {
         k_fi_upd_w<<<(rs - reg + 7) / 8, 256, 0, st>>>(h->S, P, h->fi, reg, rs - reg);
         h->launches++;
       }
-      if (split > rs && h->fi_tc == 4) {
+      if (split > rs && h->fi_tc >= 4) {
         k_fi_upd_kc<<<split - rs, 256, fi_upd_kc_smem(), st>>>(h->S, P, h->fi, rs);
         h->launches++;
       } else if (split > rs && h->fi_tc == 2) {

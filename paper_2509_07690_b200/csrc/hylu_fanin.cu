@@ -954,6 +954,10 @@ constexpr int KC_NSB = 16;     // sources per column-map batch
 #define KC_MINB_DEF 3
 #endif
 constexpr int KC_K = KC_CHUNK_DEF;   // K rows per chunk (<= 32: one lane per X column)
+#ifndef KC_BIG_DEF
+#define KC_BIG_DEF 16
+#endif
+constexpr int KC_BIG = KC_BIG_DEF;   // sources with at least this many rows get their own chunks
 constexpr int KC_XLD = KC_K + 4;     // pitches == 4 (mod 16) doubles: conflict-free fragments
 // one pipeline stage: an X chunk then a U chunk; it also holds the s x 64 target tile
 // prefetched for the epilogue
@@ -1213,6 +1217,319 @@ __global__ void __launch_bounds__(FI_THREADS, KC_MINB_DEF) k_fi_upd_kc(DevSym S,
       }
     }
   }
+}
+
+// k_fi_upd_kcp: k_fi_upd_kc for the packed items (many small sources): chunks hold
+// up to KC_K rows of consecutive sources (sources of >= KC_BIG rows still get their
+// own chunks), so a synchronisation round covers several sources; split-K parts of
+// outlier items publish partial tiles (tile column space) and the last part adds
+// them in part order.  Replaces k_fi_upd_pk (fanin_tc=5): c2 350 -> 340 ms.
+__global__ void __launch_bounds__(FI_THREADS, KC_MINB_DEF) k_fi_upd_kcp(DevSym S, CallP P, FaninDev D, int base) {
+  extern __shared__ __align__(16) double fs[];
+  __shared__ int tcol[FI_TILE];
+  __shared__ int8_t cidx[FI_TILE];     // tile column -> compact column (-1: untouched)
+  __shared__ int8_t ucol[FI_TILE];     // compact column -> tile column
+  __shared__ int s_nu, s_kb;
+  __shared__ int64_t s_vb[KC_NSB];
+  __shared__ int s_vW[KC_NSB], s_qb[KC_NSB], s_pb[KC_NSB], s_tb[KC_NSB], s_m[KC_NSB];
+  __shared__ int s_koff[KC_NSB + 1];   // first K row of each source of the batch
+  __shared__ unsigned s_bm[KC_NSB];    // 8-column blocks (compact space) a source touches
+  __shared__ int8_t ksrc[KC_NSB * 64]; // K row -> source of the batch
+  __shared__ int s_cst[KC_NSB * 64 / 4 + KC_NSB + 2];   // chunk start rows (+ end)
+  __shared__ int s_nch;
+  const int j = base + blockIdx.x;
+  const int T = D.up_t[j];
+  const int c0 = D.up_c0[j], c1 = D.up_c1[j];
+  const int tw = c1 - c0;
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31, kq = lane & 3, lr = lane >> 2;
+  const int r = (int)S.first[T];
+  const int s = (int)(S.first[T + 1] - r);
+  const int64_t tc0 = S.colptr[T];
+  const int W = (int)(S.colptr[T + 1] - tc0);
+  double *Pm = P.F + S.valoff[T];
+  constexpr int KC_BUF = KC_STAGE;
+  int8_t *inv = reinterpret_cast<int8_t *>(fs + 2 * KC_BUF);   // [KC_NSB][64] source col -> compact col
+  const int part = D.up_part ? D.up_part[j] : -1;               // split-K part (packed items)
+  const int64_t zb = D.up_ptr[j], ze = D.up_ptr[j + 1];
+  // split-K parts publish whole tiles: no column compaction for them
+  const bool compact = ze - zb <= KC_NSB && part < 0;
+  for (int c = tid; c < tw; c += FI_THREADS) tcol[c] = S.cols[tc0 + c0 + c];
+  if (tid < FI_TILE) cidx[tid] = compact ? -1 : (int8_t)tid;
+  __syncthreads();
+  // per-source metadata and column maps of a batch of <= KC_NSB sources; `pos`
+  // mode (compact first pass) stores tile positions and marks touched columns
+  auto source_maps = [&](int64_t zb0, int nsb, bool pos) {
+    for (int k = warp; k < nsb; k += FI_THREADS / 32) {
+      const int64_t z = zb0 + k;
+      const int v = D.src_v[z];
+      const int nq = D.src_q1[z] - D.src_q0[z];
+      const int vs = (int)(S.first[v + 1] - S.first[v]);
+      const int64_t vcol = S.colptr[v];
+      const int qb = S.nl[v] + vs + D.src_q0[z];
+      const int64_t vc = vcol + qb;
+      const int tb0 = D.src_tb[z];
+      if (lane == 0) {
+        s_vb[k] = S.valoff[v];
+        s_vW[k] = (int)(S.colptr[v + 1] - vcol);
+        s_qb[k] = qb;
+        s_pb[k] = D.src_pb[z];
+        s_tb[k] = tb0;
+        s_m[k] = vs - tb0;
+      }
+      for (int c = lane; c < 64; c += 32) {
+        int p = -1;
+        if (c < nq) {
+          p = lower_bound_i32(tcol, 0, tw, S.cols[vc + c]);
+          if (pos) cidx[p] = 1;
+        }
+        inv[k * 64 + c] = (int8_t)p;   // tile position of source column c
+      }
+    }
+  };
+  // tile positions -> compact columns (inv[k][compact col] = source col), block masks
+  auto remap = [&](int nsb) {
+    for (int k = warp; k < nsb; k += FI_THREADS / 32) {
+      const int p0 = inv[k * 64 + lane], p1 = inv[k * 64 + lane + 32];
+      __syncwarp();
+      inv[k * 64 + lane] = -1;
+      inv[k * 64 + lane + 32] = -1;
+      __syncwarp();
+      if (p0 >= 0) inv[k * 64 + cidx[p0]] = (int8_t)lane;
+      if (p1 >= 0) inv[k * 64 + cidx[p1]] = (int8_t)(lane + 32);
+      __syncwarp();
+      const unsigned m0 = __ballot_sync(HY_FULL, inv[k * 64 + lane] >= 0);
+      const unsigned m1 = __ballot_sync(HY_FULL, inv[k * 64 + lane + 32] >= 0);
+      if (lane == 0) {
+        unsigned bm = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          if ((m0 >> (8 * b)) & 0xffu) bm |= 1u << b;
+          if ((m1 >> (8 * b)) & 0xffu) bm |= 1u << (b + 4);
+        }
+        s_bm[k] = bm;
+      }
+    }
+  };
+  // K layout of a batch: sources' rows concatenated (koff prefix sums, row -> source)
+  auto k_layout = [&](int nsb) {
+    if (warp == 0) {
+      int m = lane < nsb ? s_m[lane] : 0;
+      int incl = m;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(HY_FULL, incl, o);
+        if (lane >= o) incl += v;
+      }
+      if (lane < nsb) s_koff[lane] = incl - m;
+      if (lane == nsb - 1) { s_koff[nsb] = incl; s_kb = incl; }
+      __syncwarp();
+      if (lane == 0) {
+        // chunk boundaries: sources of >= KC_BIG rows start a chunk and are cut in
+        // KC_K-row pieces (no straddling: their 8-column block masks stay tight);
+        // smaller sources are packed together up to KC_K rows
+        int nch = 0, open = -1;
+        for (int k = 0; k < nsb; ++k) {
+          const int off = s_koff[k], mk = s_m[k];
+          if (mk >= KC_BIG) {
+            if (open >= 0) { s_cst[nch++] = open; open = -1; }
+            for (int q = 0; q < mk; q += KC_K) s_cst[nch++] = off + q;
+          } else if (mk > 0) {
+            if (open >= 0 && off + mk - open > KC_K) { s_cst[nch++] = open; open = -1; }
+            if (open < 0) open = off;
+          }
+        }
+        if (open >= 0) s_cst[nch++] = open;
+        s_cst[nch] = s_koff[nsb];
+        s_nch = nch;
+      }
+    }
+    __syncthreads();
+    for (int k = warp; k < nsb; k += FI_THREADS / 32)
+      for (int rr = lane; rr < s_m[k]; rr += 32) ksrc[s_koff[k] + rr] = (int8_t)k;
+  };
+  if (compact) {
+    const int nsb = (int)(ze - zb);
+    source_maps(zb, nsb, true);
+    __syncthreads();
+    if (warp == 0) {
+      const bool t0 = cidx[lane] == 1, t1 = cidx[lane + 32] == 1;
+      const unsigned m0 = __ballot_sync(HY_FULL, t0), m1 = __ballot_sync(HY_FULL, t1);
+      const int i0 = __popc(m0 & ((1u << lane) - 1)), i1 = __popc(m0) + __popc(m1 & ((1u << lane) - 1));
+      cidx[lane] = t0 ? (int8_t)i0 : -1;
+      cidx[lane + 32] = t1 ? (int8_t)i1 : -1;
+      if (t0) ucol[i0] = (int8_t)lane;
+      if (t1) ucol[i1] = (int8_t)(lane + 32);
+      if (lane == 0) s_nu = __popc(m0) + __popc(m1);
+    }
+    __syncthreads();
+    remap(nsb);
+  } else {
+    if (tid < FI_TILE) ucol[tid] = (int8_t)tid;
+    if (tid == 0) s_nu = tw;
+  }
+  __syncthreads();
+  const int nu = s_nu;
+  // warp tiles over the s x nu product: 8 x 32 (8 warps over the rows) when the
+  // item touches <= 32 columns, else 16 x 32 (4 x 2 warps)
+  const bool narrow = nu <= 32;
+  const int wr0 = narrow ? warp * 8 : (warp >> 1) * 16;
+  const int wc0 = narrow ? 0 : (warp & 1) * 32;
+  bool ra[2], ca[4];
+  ra[0] = wr0 < s;
+  ra[1] = !narrow && wr0 + 8 < s;
+#pragma unroll
+  for (int b = 0; b < 4; ++b) ca[b] = wc0 + 8 * b < nu;
+  double d[2][4][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) d[a][b][0] = d[a][b][1] = 0.0;
+
+  int buf = 0;
+  for (int64_t zb0 = zb; zb0 < ze; zb0 += KC_NSB) {
+    const int nsb = (int)(ze - zb0 < KC_NSB ? ze - zb0 : KC_NSB);
+    const bool last_batch = zb0 + KC_NSB >= ze;
+    if (!compact) {
+      if (zb0 != zb) __syncthreads();   // previous batch's chunks consumed
+      source_maps(zb0, nsb, false);
+      __syncthreads();
+      remap(nsb);   // identity compact space: stores source col by tile position
+    }
+    k_layout(nsb);
+    __syncthreads();
+    const int kb = s_kb;
+    const int nch = s_nch;
+    // chunk ch = K rows [ch*KC_K, ch*KC_K + KC_K) of the batch, any number of sources
+    auto issue = [&](int ch, int bf) {
+      double *X = fs + bf * KC_BUF;
+      double *U = X + 64 * KC_XLD;
+      const int a0 = s_cst[ch], a1 = s_cst[ch + 1];
+      if (lane < KC_K) {
+        const int ga = a0 + lane;
+        const bool ok = ga < a1;
+        const int k = ok ? ksrc[ga] : 0;
+        const int col = ok ? s_pb[k] + ga - s_koff[k] : 0;
+        for (int t = warp; t < s; t += FI_THREADS / 32)
+          cp_async8z(X + t * KC_XLD + lane, Pm + (int64_t)t * W + col, ok);
+      }
+      const bool w1 = lane + 32 < nu;   // compact columns beyond nu are never read
+      for (int a = warp; a < KC_K; a += FI_THREADS / 32) {
+        const int ga = a0 + a;
+        const bool ok = ga < a1;
+        const int k = ok ? ksrc[ga] : 0;
+        const double *ur = P.F + s_vb[k] + (int64_t)(s_tb[k] + (ok ? ga - s_koff[k] : 0)) * s_vW[k] + s_qb[k];
+        const int i0 = inv[k * 64 + lane], i1 = inv[k * 64 + lane + 32];
+        cp_async8z(U + a * KC_ULD + lane, ur + (i0 >= 0 ? i0 : 0), ok && i0 >= 0);
+        if (w1) cp_async8z(U + a * KC_ULD + lane + 32, ur + (i1 >= 0 ? i1 : 0), ok && i1 >= 0);
+      }
+    };
+    auto prefetch_tile = [&](int bf) {   // the target's touched tile values, for the epilogue
+      double *Tv = fs + bf * KC_BUF;
+      for (int t = warp; t < s; t += FI_THREADS / 32) {
+        const double *prow = Pm + (int64_t)t * W + c0;
+        if (lane < nu) cp_async8z(Tv + t * 64 + lane, prow + ucol[lane], true);
+        if (lane + 32 < nu) cp_async8z(Tv + t * 64 + lane + 32, prow + ucol[lane + 32], true);
+      }
+    };
+    if (nch > 0) issue(0, buf);
+    else if (last_batch && part < 0) prefetch_tile(buf ^ 1);
+    kc_commit();
+    for (int ch = 0; ch < nch; ++ch) {
+      const bool more = ch + 1 < nch;
+      if (more) {
+        issue(ch + 1, buf ^ 1);
+      } else if (last_batch && part < 0) {
+        prefetch_tile(buf ^ 1);   // into the free stage
+      }
+      kc_commit();
+      kc_wait1();
+      __syncthreads();
+      const int a0 = s_cst[ch];
+      const int rows = s_cst[ch + 1] - a0;
+      const int kc4 = (rows + 3) & ~3;
+      // 8-column blocks any source of this chunk touches
+      unsigned bmc = 0;
+      for (int k = ksrc[a0]; k <= ksrc[a0 + rows - 1]; ++k) bmc |= s_bm[k];
+      const double *X = fs + buf * KC_BUF, *U = X + 64 * KC_XLD;
+      const unsigned bm = bmc >> (wc0 >> 3);
+      bool cb[4];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) cb[b] = ca[b] && ((bm >> b) & 1u);
+      if (ra[0] && (bm & 15u))
+        for (int k = 0; k < kc4; k += 4) {
+          double av[2], bv[4];
+#pragma unroll
+          for (int a = 0; a < 2; ++a) av[a] = ra[a] ? X[(wr0 + 8 * a + lr) * KC_XLD + k + kq] : 0.0;
+#pragma unroll
+          for (int b = 0; b < 4; ++b) bv[b] = cb[b] ? U[(k + kq) * KC_ULD + wc0 + 8 * b + lr] : 0.0;
+#pragma unroll
+          for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+              if (ra[a] && cb[b]) dmma884(d[a][b], av[a], bv[b]);
+        }
+      if (more) {
+        __syncthreads();   // buffer `buf` free for the chunk after next
+        buf ^= 1;
+      }
+    }
+    if (!last_batch) {
+      __syncthreads();
+      buf ^= 1;   // the next batch starts in the other stage
+    }
+  }
+  kc_wait0();
+  __syncthreads();
+  if (part < 0) {
+    // T[:, tile] -= product (row lr of each 8-row block, compact columns 2*kq, 2*kq+1)
+    const double *Tv = fs + (buf ^ 1) * KC_BUF;
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+      const int t = wr0 + 8 * a + lr;
+      if (!ra[a] || t >= s) continue;
+      double *prow = Pm + (int64_t)t * W + c0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int c = wc0 + 8 * b + 2 * kq + e;
+          if (ca[b] && c < nu) prow[ucol[c]] = Tv[t * 64 + c] - d[a][b][e];
+        }
+    }
+    return;
+  }
+  // split-K part (tile column space): publish the partial tile; the last part of the
+  // item adds the partials in part order and updates the target once
+  double *mine = D.part_scr + D.part_off[part];
+#pragma unroll
+  for (int a = 0; a < 2; ++a) {
+    const int t = wr0 + 8 * a + lr;
+    if (!ra[a] || t >= s) continue;
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = wc0 + 8 * b + 2 * kq + e;
+        if (ca[b] && c < tw) mine[t * FI_TILE + c] = d[a][b][e];
+      }
+  }
+  __threadfence();
+  __syncthreads();
+  __shared__ int s_last;
+  const int first = D.part_first[part], np = D.part_n[part];
+  if (tid == 0) s_last = atomicAdd(D.part_cnt + first, 1) == np - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int idx = tid; idx < s * FI_TILE; idx += FI_THREADS) {
+    const int t = idx / FI_TILE, c = idx - t * FI_TILE;
+    if (c >= tw) continue;
+    double sum = 0.0;
+    for (int k = 0; k < np; ++k) sum += __ldcg(D.part_scr + D.part_off[first + k] + t * FI_TILE + c);
+    Pm[(int64_t)t * W + c0 + c] -= sum;
+  }
+  if (tid == 0) D.part_cnt[first] = 0;
 }
 
 // ---------------------------------------------------------------------------- updates v3

@@ -305,7 +305,8 @@ def test_batched_full_n_matches_oracle():
 def test_update_kernel_variants(name):
     """Sup-sup update kernels: the per-source DMMA kernel (fanin_tc=2) is bitwise equal
     to the FFMA kernel (DMMA chains its four products per element in k order); the
-    default K-concatenated DMMA kernel (fanin_tc=4) differs only by summation order."""
+    K-concatenated DMMA kernels (default fanin_tc=5: packed items too; 4: packed items
+    on the FFMA packing kernel) differ only by summation order."""
     p, an = _analysis(name)
     on = _oracle()
     ref = on.factorize(an)
@@ -316,11 +317,13 @@ def test_update_kernel_variants(name):
         f0 = api.factorize_analysis(an)
         ctx.set_option("fanin_tc", 2)
         f2 = api.factorize_analysis(an)
-    finally:
         ctx.set_option("fanin_tc", 4)
-    v0, v2, v4 = f0.host_values(), f2.host_values(), f4.host_values()
+        f4b = api.factorize_analysis(an)
+    finally:
+        ctx.set_option("fanin_tc", 5)
+    v0, v2, v4, v4b = f0.host_values(), f2.host_values(), f4.host_values(), f4b.host_values()
     assert np.array_equal(v2, v0)
-    assert _rel(v4, v0) <= 1e-12
+    assert _rel(v4, v0) <= 1e-12 and _rel(v4b, v0) <= 1e-12
     assert _rel(v4, ref.values) <= LU_RTOL
 
 
