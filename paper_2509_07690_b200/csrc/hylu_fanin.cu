@@ -169,6 +169,33 @@ __global__ void __launch_bounds__(FI_THREADS) k_fi_lu(DevSym S, CallP P, FaninDe
 // ---------------------------------------------------------------------------- panel
 // Tile of node v's columns [c0, c1) outside the block: apply the pivot row
 // permutation (factorize only) and, for panel tiles, the unit-lower TRSM.
+// Unit-lower TRSM of one panel column (thread `tid`), rows in register blocks of 16:
+// a block first takes the updates of every earlier (final) row from shared memory,
+// then its own triangle in registers.  Per element the updates are applied in
+// ascending t, as in the plain column loop.
+__device__ __forceinline__ void panel_trsm_col(double *tl, const double *Lb, int s, int tw, int tid) {
+  constexpr int RB = 16;
+  for (int q0 = 0; q0 < s; q0 += RB) {
+    double x[RB];
+#pragma unroll
+    for (int q = 0; q < RB; ++q) x[q] = q0 + q < s ? tl[(q0 + q) * tw + tid] : 0.0;
+    for (int t = 0; t < q0; ++t) {
+      const double xt = tl[t * tw + tid];
+#pragma unroll
+      for (int q = 0; q < RB; ++q) x[q] -= Lb[(q0 + q) * FXLD + t] * xt;
+    }
+#pragma unroll
+    for (int t = 0; t + 1 < RB; ++t) {
+      const double xt = x[t];
+#pragma unroll
+      for (int q = t + 1; q < RB; ++q) x[q] -= Lb[(q0 + q) * FXLD + q0 + t] * xt;
+    }
+#pragma unroll
+    for (int q = 0; q < RB; ++q)
+      if (q0 + q < s) tl[(q0 + q) * tw + tid] = x[q];
+  }
+}
+
 __global__ void __launch_bounds__(FI_THREADS) k_fi_panel(DevSym S, CallP P, FaninDev D, int base) {
   extern __shared__ __align__(16) double tl[];   // s x (c1-c0), stride PANEL
   __shared__ double Lb[64 * FXLD];
@@ -204,13 +231,11 @@ __global__ void __launch_bounds__(FI_THREADS) k_fi_panel(DevSym S, CallP P, Fani
   }
   __syncthreads();
   if (panel) {
-    // unit-lower TRSM, one thread per column (tw <= FI_THREADS): no barriers, the
-    // per-element update sequence (ascending t) is unchanged
-    if (tid < tw)
-      for (int t = 0; t + 1 < s; ++t) {
-        const double xt = tl[t * tw + tid];
-        for (int q = t + 1; q < s; ++q) tl[q * tw + tid] -= Lb[q * FXLD + t] * xt;
-      }
+    // unit-lower TRSM, one thread per column (tw <= FI_THREADS), the column held in
+    // registers (one shared broadcast load per FMA instead of a shared
+    // read-modify-write); no barriers, per-element update sequence (ascending t)
+    // unchanged
+    if (tid < tw) panel_trsm_col(tl, Lb, s, tw, tid);
     __syncthreads();
   }
   for (int idx = tid; idx < s * tw; idx += FI_THREADS) {
@@ -243,13 +268,22 @@ __global__ void __launch_bounds__(FI_THREADS) k_fi_x(DevSym S, CallP P, FaninDev
   const int pb0 = D.dep_pb[dk];
   const int tb0 = S.cols[tc0 + pb0] - vf;
   const int m = vs - tb0;
-  for (int idx = tid; idx < m * m; idx += FI_THREADS) {
-    const int a = idx / m, b2 = idx - a * m;
-    Ub[a * FXLD + b2] = b2 >= a ? vb[(int64_t)(tb0 + a) * vW + vnl + tb0 + b2] : 0.0;
+  // warp per row, lanes over columns (no index divisions); the diagonal's
+  // reciprocals are formed once, so the sequential loop multiplies instead of
+  // dividing (x_a = w_a * (1/U_aa): within one rounding of the division)
+  const int warp = tid >> 5;
+  __shared__ double rinv[64];
+  for (int a = warp; a < m; a += FI_THREADS / 32) {
+    const double *urow = vb + (int64_t)(tb0 + a) * vW + vnl + tb0;
+    for (int b2 = lane; b2 < m; b2 += 32) {
+      const double u = b2 >= a ? urow[b2] : 0.0;
+      Ub[a * FXLD + b2] = u;
+      if (b2 == a) rinv[a] = 1.0 / u;
+    }
   }
-  for (int idx = tid; idx < s * m; idx += FI_THREADS) {
-    const int t = idx / m, a = idx - t * m;
-    Xt[t * FXLD + a] = Pm[(int64_t)t * W + pb0 + a];
+  for (int t = warp; t < s; t += FI_THREADS / 32) {
+    const double *xs = Pm + (int64_t)t * W + pb0;
+    for (int a = lane; a < m; a += 32) Xt[t * FXLD + a] = xs[a];
   }
   __syncthreads();
   {
@@ -259,7 +293,7 @@ __global__ void __launch_bounds__(FI_THREADS) k_fi_x(DevSym S, CallP P, FaninDev
     for (int a = 0; a < m; ++a) {
       double x = 0.0;
       if (act && (a & 3) == qd) {
-        x = xr[a] / Ub[a * FXLD + a];
+        x = xr[a] * rinv[a];
         xr[a] = x;
       }
       x = __shfl_sync(HY_FULL, x, (lane & ~3) | (a & 3));
@@ -269,9 +303,9 @@ __global__ void __launch_bounds__(FI_THREADS) k_fi_x(DevSym S, CallP P, FaninDev
     }
   }
   __syncthreads();
-  for (int idx = tid; idx < s * m; idx += FI_THREADS) {
-    const int t = idx / m, a = idx - t * m;
-    Pm[(int64_t)t * W + pb0 + a] = Xt[t * FXLD + a];
+  for (int t = warp; t < s; t += FI_THREADS / 32) {
+    double *xd = Pm + (int64_t)t * W + pb0;
+    for (int a = lane; a < m; a += 32) xd[a] = Xt[t * FXLD + a];
   }
 }
 
