@@ -287,20 +287,35 @@ __global__ void __launch_bounds__(FI_THREADS) k_fi_x(DevSym S, CallP P, FaninDev
   }
   __syncthreads();
   {
+    // 4 threads per target row; thread qd holds the row's columns qd, qd+4, ... in
+    // registers (16 values), so the sequential loop has no shared read-modify-write
     const int t = tid >> 2, qd = tid & 3;
     double *xr = Xt + t * FXLD;
     const bool act = t < s;
-    for (int a = 0; a < m; ++a) {
-      double x = 0.0;
-      if (act && (a & 3) == qd) {
-        x = xr[a] * rinv[a];
-        xr[a] = x;
+    double xi[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) xi[i] = (act && qd + 4 * i < m) ? xr[qd + 4 * i] : 0.0;
+#pragma unroll
+    for (int a = 0; a < 64; ++a) {
+      if (a < m) {
+        double x = 0.0;
+        if ((a & 3) == qd) {
+          x = xi[a >> 2] * rinv[a];
+          xi[a >> 2] = x;
+        }
+        x = __shfl_sync(HY_FULL, x, (lane & ~3) | (a & 3));
+        if (x != 0.0) {
+#pragma unroll
+          for (int i = (a + 1) >> 2; i < 16; ++i) {
+            const int b2 = qd + 4 * i;
+            if (b2 > a && b2 < m) xi[i] -= x * Ub[a * FXLD + b2];
+          }
+        }
       }
-      x = __shfl_sync(HY_FULL, x, (lane & ~3) | (a & 3));
-      if (act && x != 0.0)
-        for (int b2 = a + 1 + ((qd - a - 1) & 3); b2 < m; b2 += 4) xr[b2] -= x * Ub[a * FXLD + b2];
-      __syncwarp();
     }
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (act && qd + 4 * i < m) xr[qd + 4 * i] = xi[i];
   }
   __syncthreads();
   for (int t = warp; t < s; t += FI_THREADS / 32) {
