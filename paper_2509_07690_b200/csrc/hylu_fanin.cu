@@ -995,7 +995,10 @@ __global__ void __launch_bounds__(FI_THREADS, 3) k_fi_upd_tc(DevSym S, CallP P, 
 // ascending (source, row) order, then one subtraction — the packed kernel's order.
 
 constexpr int KC_ULD = 68;
-constexpr int KC_NSB = 16;     // sources per column-map batch
+#ifndef KC_NSB_DEF
+#define KC_NSB_DEF 16
+#endif
+constexpr int KC_NSB = KC_NSB_DEF;     // sources per column-map batch (multi-batch path: > KC_NSB sources)
 #ifndef KC_CHUNK_DEF
 #define KC_CHUNK_DEF 32
 #endif
