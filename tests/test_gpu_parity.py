@@ -359,3 +359,28 @@ def test_api_errors_and_tiny_systems():
     # rhs of the wrong length -> DimensionMismatch
     with pytest.raises(errors.DimensionMismatch):
         api.solve(A, f, b=np.ones(A.n + 1))
+
+
+def test_single_call_batched_abi_matches_two_phase():
+    """hy_refactorize_solve_batched (one C call) equals refactorize_batched +
+    solve_batched bit for bit, including a batch of one instance."""
+    import torch
+    from paper_2509_07690_b200.device import check
+    bp = gen.circuit_batch(36, 1500, 2, 150)
+    an = an_mod.analyze(bp.A0, SolverConfig(ordering="amd"))
+    prior = api.factorize_analysis(an)
+    br = api.BatchedRefactorizer(prior)
+    ctx = br.ctx
+    for B in (36, 1):
+        dv = torch.from_numpy(bp.values[:B].copy()).cuda()
+        dr = torch.from_numpy(bp.rhs[:B].copy()).cuda()
+        x2, n2 = br.run(dv, dr)
+        x1 = torch.empty_like(x2)
+        n1 = torch.empty_like(n2)
+        check(ctx.lib.hy_refactorize_solve_batched(ctx.h, B, dv.data_ptr(), dr.data_ptr(), x1.data_ptr(),
+                                                   1e-8, prior._desc, n1.data_ptr(), ctx.stream_handle(None)))
+        torch.cuda.synchronize()
+        assert torch.equal(x1, x2) and torch.equal(n1, n2)
+        A = bp.A0.with_values(bp.values[0])
+        xh = x1[0].cpu().numpy()
+        assert np.linalg.norm(refmatrix.spmv(A, xh) - bp.rhs[0]) / np.linalg.norm(bp.rhs[0]) <= RES_TOL
