@@ -269,13 +269,16 @@ def convdiff3d(k=64, c=0.3, seed=SEEDS["c2"]):
 
 
 # --------------------------------------------------------------------------- c3
-def fem27(k=48, dof=3, seed=SEEDS["c3"]):
+def fem27(k=48, dof=3, seed=SEEDS["c3"], recipe="dominant"):
     """c3: 27-point node stencil (incl. self) on k^3 nodes, dof x dof blocks.
 
     "Dominant" reading of the recipe (recorded in DESIGN.md):
     per stored node pair (p, q) in CSR order, X~N(0,1) dof x dof, B = XᵀX/3;
     block = B + 81 I if p == q else -0.1 B; then every entry x (1+U[-0.05,0.05])
     (all X drawn first, then all U, then b~U[-1,1]).
+    ``recipe="literal"``: every block is XᵀX + 3I (BASELINE's text read literally),
+    then the same ±5% perturbation — not diagonally dominant, so static pivoting
+    moves most rows and the pivoted pattern is unsymmetric.
     """
     rng = np.random.default_rng(seed)
     nn = k ** 3
@@ -295,10 +298,13 @@ def fem27(k=48, dof=3, seed=SEEDS["c3"]):
     pr, pc = pr[order], pc[order]
     nb = len(pr)
     X = rng.normal(size=(nb, dof, dof))
-    B = np.einsum("bki,bkj->bij", X, X) / 3.0
     self_ = pr == pc
-    B[~self_] *= -0.1
-    B[self_] += 81.0 * np.eye(dof)
+    if recipe == "literal":
+        B = np.einsum("bki,bkj->bij", X, X) + 3.0 * np.eye(dof)
+    else:
+        B = np.einsum("bki,bkj->bij", X, X) / 3.0
+        B[~self_] *= -0.1
+        B[self_] += 81.0 * np.eye(dof)
     B *= 1.0 + rng.uniform(-0.05, 0.05, size=B.shape)
     # expand blocks to CSR: row 3p+a has, for each neighbour q ascending, cols 3q+0..dof-1
     n = nn * dof

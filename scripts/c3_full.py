@@ -12,8 +12,9 @@ from paper_2509_07690_b200 import api, generators as gen, analysis as an_mod  # 
 from paper_2509_07690_b200._ref import SolverConfig, matrix as refmatrix  # noqa: E402
 
 k = int(sys.argv[1]) if len(sys.argv) > 1 else 48
+recipe = sys.argv[2] if len(sys.argv) > 2 else "dominant"
 t0 = time.perf_counter()
-p = gen.fem27(k)
+p = gen.fem27(k, recipe=recipe)
 an = an_mod.analyze(p.A, SolverConfig(ordering="nd"))
 s = an.symbolic
 ta = time.perf_counter() - t0
@@ -43,7 +44,7 @@ tr, f2 = ev(lambda: api.refactorize(dv, f))
 ts, x = ev(lambda: api.substitute(f, db), 3)
 xh = x.cpu().numpy()
 res = float(np.linalg.norm(refmatrix.spmv(p.A, xh) - p.b) / np.linalg.norm(p.b))
-print(json.dumps(dict(config="c3_k%d" % k, n=s.n, nnz=p.A.nnz, fill=s.fill_nnz, flops=s.flops,
+print(json.dumps(dict(config="c3_k%d%s" % (k, "" if recipe == "dominant" else "_" + recipe), n=s.n, nnz=p.A.nnz, fill=s.fill_nnz, flops=s.flops,
                       stored=s.stored_values, levels=len(s.level_ptr) - 1, analyze_s=round(ta, 1),
                       first_factor_s=round(tfirst, 1), factor_ms=tf, refactor_ms=tr, solve_ms=ts,
                       gflops=s.flops / tf / 1e6, residual=res, npert=len(f.perturbed))), flush=True)
