@@ -1084,9 +1084,7 @@ static int run_factor(hy_handle *h, const double *d_avals, double eps, const hy_
                                      h->slab_mmax[l], h->slab_swmax[l], h->slab_accmax[l]);
       h->launches++;
       if (!P.refactor) {
-        int maxL = 1;
         dim3 g(ns, 4);
-        (void)maxL;
         k_lperm<<<g, 256, 0, st>>>(h->S, P, pl.d_sns + pl.sptr[l], ns);
         h->launches++;
       }

@@ -657,7 +657,6 @@ __global__ void __launch_bounds__(HUB_THREADS) k_bt_hub(DevSym S, BatchP P, DevP
   const int g = task % G;
   const int64_t b = (int64_t)g * 32 + lane;
   const bool live = b < P.B;
-  const int nlive = (int)(P.B - (int64_t)g * 32 < 32 ? P.B - (int64_t)g * 32 : 32);
   const double thr = P.eps * P.anorm[0];
   const int r = (int)S.first[u];
   const int s = (int)(S.first[u + 1] - r);

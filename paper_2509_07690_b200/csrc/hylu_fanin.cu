@@ -1281,7 +1281,7 @@ __global__ void __launch_bounds__(FI_THREADS, KC_MINB_DEF) k_fi_upd_kcp(DevSym S
   __shared__ int tcol[FI_TILE];
   __shared__ int8_t cidx[FI_TILE];     // tile column -> compact column (-1: untouched)
   __shared__ int8_t ucol[FI_TILE];     // compact column -> tile column
-  __shared__ int s_nu, s_kb;
+  __shared__ int s_nu;
   __shared__ int64_t s_vb[KC_NSB];
   __shared__ int s_vW[KC_NSB], s_qb[KC_NSB], s_pb[KC_NSB], s_tb[KC_NSB], s_m[KC_NSB];
   __shared__ int s_koff[KC_NSB + 1];   // first K row of each source of the batch
@@ -1374,7 +1374,7 @@ __global__ void __launch_bounds__(FI_THREADS, KC_MINB_DEF) k_fi_upd_kcp(DevSym S
         if (lane >= o) incl += v;
       }
       if (lane < nsb) s_koff[lane] = incl - m;
-      if (lane == nsb - 1) { s_koff[nsb] = incl; s_kb = incl; }
+      if (lane == nsb - 1) s_koff[nsb] = incl;
       __syncwarp();
       if (lane == 0) {
         // chunk boundaries: sources of >= KC_BIG rows start a chunk and are cut in
@@ -1450,9 +1450,8 @@ __global__ void __launch_bounds__(FI_THREADS, KC_MINB_DEF) k_fi_upd_kcp(DevSym S
     }
     k_layout(nsb);
     __syncthreads();
-    const int kb = s_kb;
     const int nch = s_nch;
-    // chunk ch = K rows [ch*KC_K, ch*KC_K + KC_K) of the batch, any number of sources
+    // chunk ch = K rows [s_cst[ch], s_cst[ch+1]) of the batch, any number of sources
     auto issue = [&](int ch, int bf) {
       double *X = fs + bf * KC_BUF;
       double *U = X + 64 * KC_XLD;
