@@ -296,3 +296,26 @@ def _run_pull_with(an, prog, values, F):
                     F[p] = acc
         hr += nr
     return F
+
+
+def test_chain_accelerated_symbolic_is_exact():
+    """The U-nesting-chain reach (symbolic._general_symbolic_chains, used for
+    unsymmetric patterns) returns exactly the plain Gilbert-Peierls row reach's L/U
+    patterns on unsymmetric, symmetric and random patterns."""
+    import numpy as np
+    import scipy.sparse as sp
+    from paper_2509_07690_b200 import generators as gen, analysis as an_mod, symbolic as sy
+    from paper_2509_07690_b200._ref import SolverConfig
+    pats = []
+    for p, order in [(gen.fem27(6, recipe="literal"), "nd"), (gen.config("c1", "small"), "amd"),
+                     (gen.config("c0", "small"), "amd")]:
+        s = an_mod.analyze(p.A, SolverConfig(ordering=order)).symbolic
+        pats.append((s.n, np.asarray(s.mp), np.asarray(s.mc)))
+    for t in range(4):
+        M = (sp.random(200, 200, density=0.01 + 0.015 * t, random_state=t, format="csr") + sp.eye(200)).tocsr()
+        M.sort_indices()
+        pats.append((200, M.indptr.astype(np.int64), M.indices.astype(np.int64)))
+    for n, mp, mc in pats:
+        a = sy._general_symbolic(n, mp, mc)
+        b = sy._general_symbolic_chains(n, mp, mc)
+        assert all(np.array_equal(x, y) for x, y in zip(a, b))
