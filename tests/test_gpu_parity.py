@@ -400,3 +400,32 @@ def test_c3_literal_recipe_matches_oracle():
     assert _rel(f.host_values(), ref.values) <= LU_RTOL
     x, _ = api.solve(p.A, f, b=p.b)
     assert np.linalg.norm(refmatrix.spmv(p.A, x) - p.b) / np.linalg.norm(p.b) <= RES_TOL
+
+
+def test_cli_solve_report(tmp_path):
+    """SPEC.md cli example: `solve --matrix lap.mtx --repeat K --report out.json` gives a
+    SolveReport JSON with K repeat entries and a small final backward error; the
+    identity example gives x = b with backward error 0."""
+    import json
+    from paper_2509_07690_b200 import cli
+    p = gen.config("c0", "small")
+    mtx = tmp_path / "lap.mtx"
+    A = p.A
+    rp, ci, va = np.asarray(A.row_ptr), np.asarray(A.col_idx), np.asarray(A.values)
+    lines = ["%%MatrixMarket matrix coordinate real general", "%d %d %d" % (A.n, A.n, A.nnz)]
+    for i in range(A.n):
+        for k in range(rp[i], rp[i + 1]):
+            lines.append("%d %d %r" % (i + 1, ci[k] + 1, float(va[k])))
+    mtx.write_text("\n".join(lines) + "\n")
+    out = tmp_path / "out.json"
+    assert cli.main(["--matrix", str(mtx), "--repeat", "3", "--perturb-values", "0.01",
+                     "--rhs", "random:3", "--report", str(out)]) == 0
+    r = json.loads(out.read_text())
+    assert len(r["repeat_times_seconds"]) == 3 and r["n"] == p.A.n
+    assert r["backward_error_final"] <= 1e-13
+    assert set(r["phase_times_seconds"]) == {"preprocess", "factorize", "solve"}
+    eye = tmp_path / "id2.mtx"
+    eye.write_text("%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 1.0\n2 2 1.0\n")
+    out2 = tmp_path / "id.json"
+    assert cli.main(["--matrix", str(eye), "--report", str(out2)]) == 0
+    assert json.loads(out2.read_text())["backward_error_final"] == 0.0

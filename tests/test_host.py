@@ -319,3 +319,25 @@ def test_chain_accelerated_symbolic_is_exact():
         a = sy._general_symbolic(n, mp, mc)
         b = sy._general_symbolic_chains(n, mp, mc)
         assert all(np.array_equal(x, y) for x, y in zip(a, b))
+
+
+def test_cli_usage_and_input_errors(tmp_path, capsys):
+    """SPEC.md cli: exit 2 on usage errors, exit 1 on solver/input errors (error class
+    and matrix name printed), generate_rhs modes."""
+    import numpy as np
+    import pytest
+    from paper_2509_07690_b200 import cli
+    from paper_2509_07690_b200._ref import errors
+    assert cli.main([]) == 2                                        # --matrix missing
+    bad = tmp_path / "bad.mtx"
+    bad.write_text("not a matrix market file\n")
+    assert cli.main(["--matrix", str(bad), "--set", "no_such_field=1"]) == 2
+    assert cli.main(["--matrix", str(bad), "--repeat", "-1"]) == 2
+    assert cli.main(["--matrix", str(bad)]) == 1
+    assert "ParseError" in capsys.readouterr().err
+    assert np.array_equal(cli.generate_rhs("ones", 3), np.ones(3))
+    assert np.array_equal(cli.generate_rhs("random:7", 4), cli.generate_rhs("random:7", 4))
+    f = tmp_path / "b.txt"
+    f.write_text("1 2\n")
+    with pytest.raises(errors.LengthMismatch):
+        cli.generate_rhs(str(f), 3)
