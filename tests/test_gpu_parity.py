@@ -429,3 +429,55 @@ def test_cli_solve_report(tmp_path):
     out2 = tmp_path / "id.json"
     assert cli.main(["--matrix", str(eye), "--report", str(out2)]) == 0
     assert json.loads(out2.read_text())["backward_error_final"] == 0.0
+
+
+def test_device_random_corpus_acceptance():
+    """SPEC acceptance 1-3 on the device path: random matrices n in [2, 64], density
+    in [0.05, 1] (condition <= 1e8): solve within 1e-8 of a dense solve, factors
+    within 1e-11 of the oracle's, and the three kernel modes agree within 1e-12."""
+    from paper_2509_07690_b200._ref import SparseMatrixCSR
+    on = _oracle()
+    done = 0
+    for seed in range(40):
+        rng = np.random.default_rng(5000 + seed)
+        n = int(rng.integers(2, 65))
+        dens = rng.uniform(0.05, 1.0)
+        D = np.where(rng.random((n, n)) < dens, rng.standard_normal((n, n)), 0.0)
+        D[np.arange(n), rng.permutation(n)] += rng.uniform(1, 2, n) * rng.choice([-1, 1], n)
+        if np.linalg.cond(D) > 1e8:
+            continue
+        A = SparseMatrixCSR.from_dense(D)
+        b = rng.uniform(-1, 1, n)
+        xd = np.linalg.solve(D, b)
+        vals = []
+        for mode in (0, 1, 2):
+            an = an_mod.analyze(A, SolverConfig(ordering="amd"), kernel_override=mode)
+            f = api.factorize_analysis(an)
+            ref = on.factorize(an)
+            assert np.array_equal(f.host_inner_perm(), ref.inner_perm)
+            assert _rel(f.host_values(), ref.values) <= LU_RTOL
+            x, _ = api.solve(A, f, b=b)
+            assert np.abs(x - xd).max() <= 1e-8 * max(1.0, np.abs(xd).max())
+            vals.append(f.host_values())
+        assert _rel(vals[1], vals[0]) <= 1e-12 and _rel(vals[2], vals[0]) <= 1e-12
+        done += 1
+    assert done >= 20
+
+
+def test_device_tridiagonal_and_laplacian_acceptance():
+    """SPEC acceptance 6/7 on the device: tridiagonal n = 100000 (zero fill, ROWROW,
+    backward error <= 1e-12) and the 250 x 250 5-point Laplacian (supernodal mode,
+    backward error <= 1e-12)."""
+    from paper_2509_07690_b200._ref import KernelMode
+    p = gen.tridiag(100000)
+    an = an_mod.analyze(p.A, SolverConfig(ordering="amd"))
+    assert an.symbolic.fill_nnz == p.A.nnz and an.symbolic.kernel_mode == KernelMode.ROWROW
+    f = api.factorize_analysis(an)
+    x, _ = api.solve(p.A, f, b=p.b)
+    assert refmatrix.backward_error(p.A, x, p.b) <= 1e-12
+    p = gen.lap2d(250)
+    an = an_mod.analyze(p.A, SolverConfig(ordering="amd"))
+    assert an.symbolic.kernel_mode in (KernelMode.SUPROW, KernelMode.SUPSUP)
+    f = api.factorize_analysis(an)
+    x, _ = api.solve(p.A, f, b=p.b)
+    assert refmatrix.backward_error(p.A, x, p.b) <= 1e-12
