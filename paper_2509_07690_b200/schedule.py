@@ -1136,6 +1136,21 @@ def fanin_source_records(sym, plan):
     return v, pb0, tb0
 
 
+def executed_update_flops(sym, plan):
+    """Flops the fan-in sup-sup / sup-row updates execute on the union-padded node
+    panels: Σ over update-source records of 2·s_T·m·nq (target rows × source block
+    rows × source columns in the tile).  SURVEY §8(d) asks for this beside the
+    algorithmic count (exact pre-union pattern) so the padding gap is visible."""
+    v, _, tb0 = fanin_source_records(sym, plan)
+    first = np.asarray(sym.node_first)
+    rows = np.diff(first)
+    cnt = np.diff(plan.up_ptr)
+    st = np.repeat(rows[plan.up_t], cnt).astype(np.float64)
+    m = (rows[v] - tb0).astype(np.float64)
+    nq = (plan.src_q1 - plan.src_q0).astype(np.float64)
+    return float(2.0 * np.sum(st * m * nq))
+
+
 # --------------------------------------------------------------------------- deadline merging
 @njit(cache=True)
 def _merge_items(nlev, flev, first, colptr, cols, nl, dptr, deps, node_of, lev_up, up_t, up_c0,

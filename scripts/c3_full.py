@@ -56,6 +56,9 @@ if res > 1e-10:
     extra = dict(refine_ms=a.elapsed_time(b2), refine_iters=rep.iterations,
                  backward_errors=[float(e) for e in rep.backward_errors],
                  residual_refined=float(np.linalg.norm(refmatrix.spmv(p.A, xrh) - p.b) / np.linalg.norm(p.b)))
+from paper_2509_07690_b200 import schedule  # noqa: E402
+ex = schedule.executed_update_flops(s, s._fanin_plan)
+extra.update(exec_update_flops=ex, exec_update_gflops=ex / tf / 1e6)
 print(json.dumps(dict(config="c3_k%d%s" % (k, "" if recipe == "dominant" else "_" + recipe), n=s.n, nnz=p.A.nnz, fill=s.fill_nnz, flops=s.flops,
                       stored=s.stored_values, levels=len(s.level_ptr) - 1, analyze_s=round(ta, 1),
                       first_factor_s=round(tfirst, 1), factor_ms=tf, refactor_ms=tr, solve_ms=ts,

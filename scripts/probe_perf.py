@@ -47,6 +47,11 @@ def single(name, p):
                nodes=s.nnodes, levels=len(s.level_ptr) - 1, stored=s.stored_values,
                analyze_s=round(ta, 2), factor_ms=tf, refactor_ms=tr, solve_ms=ts,
                gflops=s.flops / tf / 1e6, residual=res, npert=len(f.perturbed))
+    plan = getattr(s, "_fanin_plan", None)
+    if plan is not None:   # executed (union-padded) update flops, SURVEY §8(d)
+        from paper_2509_07690_b200 import schedule
+        ex = schedule.executed_update_flops(s, plan)
+        out.update(exec_update_flops=ex, exec_update_gflops=ex / tf / 1e6)
     print(json.dumps(out), flush=True)
 
 
