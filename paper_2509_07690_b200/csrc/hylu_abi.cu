@@ -259,6 +259,9 @@ struct hy_handle {
   int32_t *d_acol = nullptr;
   int fi_v3 = 0;                                     // option "fanin_v3" (slower; kept for experiments)
   int fi_mma = 0;                                    // option "fanin_dmma" (bitwise-equal results; slower here)
+  int fi_overlap = 1;                                // option "fanin_overlap": panel TRSM on a side stream, concurrent with the X blocks
+  cudaStream_t fi_side = nullptr;
+  cudaEvent_t fi_ev_lu = nullptr, fi_ev_pt = nullptr;
   int fi_tc = 5;                                     // option "fanin_tc": DMMA update kernels (1/2: per-source k_fi_upd_tc for targets >= 32 rows / all regular items; 3/4: K-concatenated k_fi_upd_kc, same split; 5 (default): k_fi_upd_kcp for the packed items too)
   std::vector<int32_t> fi_smax, fi_mmax;
   int sm_count = 148;
@@ -502,6 +505,9 @@ void hy_destroy(hy_handle *h) {
   if (h->d_bf) cudaFree(h->d_bf);
   if (h->d_scratch) cudaFree(h->d_scratch);
   if (h->d_flags) cudaFree(h->d_flags);
+  if (h->fi_side) cudaStreamDestroy(h->fi_side);
+  if (h->fi_ev_lu) cudaEventDestroy(h->fi_ev_lu);
+  if (h->fi_ev_pt) cudaEventDestroy(h->fi_ev_pt);
   if (h->d_bwd_flags) cudaFree(h->d_bwd_flags);
   if (h->d_bwd_tasks) cudaFree(h->d_bwd_tasks);
   free_segments(h);
@@ -534,6 +540,10 @@ int hy_set_option(hy_handle *h, const char *name, int64_t value) {
   }
   if (std::string(name) == "fanin_v3") {
     h->fi_v3 = value != 0;
+    return HY_OK;
+  }
+  if (std::string(name) == "fanin_overlap") {
+    h->fi_overlap = value != 0;
     return HY_OK;
   }
   if (std::string(name) == "fanin_tc" && value >= 0 && value <= 5) {
@@ -893,9 +903,24 @@ static int run_fanin(hy_handle *h, const CallP &P, cudaStream_t st) {
       h->launches++;
     }
     if (nlu) { k_fi_lu<<<nlu, 256, 0, st>>>(h->S, P, h->fi, (int)h->fi_lu[l]); h->launches++; }
+    // the panel TRSM of the level's nodes and the X blocks of their edges both need
+    // only the nodes' LU: with fanin_overlap the panel runs on a side stream while the
+    // X blocks run on `st`; the update kernels (which need both) wait for it
+    const bool side = h->fi_overlap && npt && nxp;
+    if (side) {
+      if (!h->fi_side) {
+        CK(cudaStreamCreateWithFlags(&h->fi_side, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&h->fi_ev_lu, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&h->fi_ev_pt, cudaEventDisableTiming));
+      }
+      CK(cudaEventRecord(h->fi_ev_lu, st));
+      CK(cudaStreamWaitEvent(h->fi_side, h->fi_ev_lu, 0));
+    }
     if (npt) {
-      k_fi_panel<<<npt, 256, 64 * 256 * sizeof(double), st>>>(h->S, P, h->fi, (int)h->fi_pt[l]);
+      k_fi_panel<<<npt, 256, 64 * 256 * sizeof(double), side ? h->fi_side : st>>>(h->S, P, h->fi,
+                                                                                  (int)h->fi_pt[l]);
       h->launches++;
+      if (side) CK(cudaEventRecord(h->fi_ev_pt, h->fi_side));
     }
     if (nxp) {
       // few small items: one CTA launch for the whole level (it handles any size)
@@ -910,6 +935,7 @@ static int run_fanin(hy_handle *h, const CallP &P, cudaStream_t st) {
         h->launches++;
       }
     }
+    if (side) CK(cudaStreamWaitEvent(st, h->fi_ev_pt, 0));
     if (nup) {
       const size_t sm = fi_upd_smem(h->fi_smax[l], h->fi_mmax[l]);
       const int reg = (int)h->fi_upreg[l];
