@@ -906,8 +906,11 @@ static int run_fanin(hy_handle *h, const CallP &P, cudaStream_t st) {
     // the panel TRSM of the level's nodes and the X blocks of their edges both need
     // only the nodes' LU: with fanin_overlap the panel runs on a side stream while the
     // X blocks run on `st`; the update kernels (which need both) wait for it
-    const bool side = h->fi_overlap && npt && nxp;
-    if (side) {
+    // Independent kernels of a phase run on two streams (fanin_overlap): after the
+    // LU, the panel TRSM (side) and the X blocks (st) need only the LU; after both,
+    // the packed-item updates (side) and the other update groups (st) touch disjoint
+    // target tiles.  Each phase joins back into `st`.
+    auto fork = [&]() -> int {
       if (!h->fi_side) {
         CK(cudaStreamCreateWithFlags(&h->fi_side, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&h->fi_ev_lu, cudaEventDisableTiming));
@@ -915,41 +918,62 @@ static int run_fanin(hy_handle *h, const CallP &P, cudaStream_t st) {
       }
       CK(cudaEventRecord(h->fi_ev_lu, st));
       CK(cudaStreamWaitEvent(h->fi_side, h->fi_ev_lu, 0));
+      return HY_OK;
+    };
+    auto join = [&]() -> int {
+      CK(cudaEventRecord(h->fi_ev_pt, h->fi_side));
+      CK(cudaStreamWaitEvent(st, h->fi_ev_pt, 0));
+      return HY_OK;
+    };
+    const int xb = nxp ? ((int)h->fi_xpbig[l] - (int)h->fi_xp[l] < h->warp_min ? (int)h->fi_xp[l]
+                                                                                : (int)h->fi_xpbig[l])
+                       : 0;
+    const int nw = nxp ? xb - (int)h->fi_xp[l] : 0, nc = nxp ? (int)h->fi_xp[l + 1] - xb : 0;
+    // phase A: panel on the side stream when anything else runs; else the warp X items
+    const bool sideA = h->fi_overlap && ((npt && (nw || nc)) || (!npt && nw && nc));
+    if (sideA) {
+      int rc = fork();
+      if (rc) return rc;
     }
+    cudaStream_t sp = sideA && npt ? h->fi_side : st;
+    cudaStream_t sw = sideA && !npt ? h->fi_side : st;
     if (npt) {
-      k_fi_panel<<<npt, 256, 64 * 256 * sizeof(double), side ? h->fi_side : st>>>(h->S, P, h->fi,
-                                                                                  (int)h->fi_pt[l]);
+      k_fi_panel<<<npt, 256, 64 * 256 * sizeof(double), sp>>>(h->S, P, h->fi, (int)h->fi_pt[l]);
       h->launches++;
-      if (side) CK(cudaEventRecord(h->fi_ev_pt, h->fi_side));
     }
-    if (nxp) {
-      // few small items: one CTA launch for the whole level (it handles any size)
-      const int xb = (int)h->fi_xpbig[l] - (int)h->fi_xp[l] < h->warp_min ? (int)h->fi_xp[l] : (int)h->fi_xpbig[l];
-      const int nw = xb - (int)h->fi_xp[l], nc = (int)h->fi_xp[l + 1] - xb;
-      if (nw) {
-        k_fi_x_w<<<(nw + 7) / 8, 256, 0, st>>>(h->S, P, h->fi, (int)h->fi_xp[l], nw);
-        h->launches++;
-      }
-      if (nc) {
-        k_fi_x<<<nc, 256, 2 * 64 * 65 * sizeof(double), st>>>(h->S, P, h->fi, xb);
-        h->launches++;
-      }
+    if (nw) {
+      k_fi_x_w<<<(nw + 7) / 8, 256, 0, sw>>>(h->S, P, h->fi, (int)h->fi_xp[l], nw);
+      h->launches++;
     }
-    if (side) CK(cudaStreamWaitEvent(st, h->fi_ev_pt, 0));
+    if (nc) {
+      k_fi_x<<<nc, 256, 2 * 64 * 65 * sizeof(double), st>>>(h->S, P, h->fi, xb);
+      h->launches++;
+    }
+    if (sideA) {
+      int rc = join();
+      if (rc) return rc;
+    }
     if (nup) {
       const size_t sm = fi_upd_smem(h->fi_smax[l], h->fi_mmax[l]);
       const int reg = (int)h->fi_upreg[l];
       const int split = (h->fi_mma || h->fi_tc == 1 || h->fi_tc == 3) ? (int)h->fi_upbig[l] : (int)h->fi_up[l + 1];
       const int npk = reg - (int)h->fi_up[l];
       const int nbig = (int)h->fi_up[l + 1] - split;
+      const int rs = (int)h->fi_uprs[l] - reg < h->warp_min ? reg : (int)h->fi_uprs[l];
+      // phase B: packed items on the side stream when other update groups exist
+      const bool sideB = h->fi_overlap && npk && (rs > reg || split > rs || nbig);
+      if (sideB) {
+        int rc = fork();
+        if (rc) return rc;
+      }
+      cudaStream_t sk = sideB ? h->fi_side : st;
       if (npk && h->fi_tc == 5) {
-        k_fi_upd_kcp<<<npk, 256, fi_upd_kc_smem(), st>>>(h->S, P, h->fi, (int)h->fi_up[l]);
+        k_fi_upd_kcp<<<npk, 256, fi_upd_kc_smem(), sk>>>(h->S, P, h->fi, (int)h->fi_up[l]);
         h->launches++;
       } else if (npk) {
-        k_fi_upd_pk<<<npk, 256, sm, st>>>(h->S, P, h->fi, (int)h->fi_up[l], h->fi_smax[l], h->fi_mmax[l]);
+        k_fi_upd_pk<<<npk, 256, sm, sk>>>(h->S, P, h->fi, (int)h->fi_up[l], h->fi_smax[l], h->fi_mmax[l]);
         h->launches++;
       }
-      const int rs = (int)h->fi_uprs[l] - reg < h->warp_min ? reg : (int)h->fi_uprs[l];
       if (rs > reg) {
         k_fi_upd_w<<<(rs - reg + 7) / 8, 256, 0, st>>>(h->S, P, h->fi, reg, rs - reg);
         h->launches++;
@@ -978,6 +1002,10 @@ static int run_fanin(hy_handle *h, const CallP &P, cudaStream_t st) {
       } else if (nbig) {
         k_fi_upd_mma<<<nbig, 256, sm, st>>>(h->S, P, h->fi, split, h->fi_smax[l], h->fi_mmax[l]);
         h->launches++;
+      }
+      if (sideB) {
+        int rc = join();
+        if (rc) return rc;
       }
     }
   }
