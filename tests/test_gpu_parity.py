@@ -481,3 +481,24 @@ def test_device_tridiagonal_and_laplacian_acceptance():
     f = api.factorize_analysis(an)
     x, _ = api.solve(p.A, f, b=p.b)
     assert refmatrix.backward_error(p.A, x, p.b) <= 1e-12
+
+
+def test_zero_pivot_without_perturbation_raises_numeric_breakdown():
+    """errors.NumericBreakdown (errors.py:60) only when perturbation is disabled
+    (perturbation_epsilon = 0) and a pivot is exactly zero."""
+    from paper_2509_07690_b200._ref import errors
+    p, an = _analysis("c0", None)
+    f0 = api.factorize_analysis(an)
+    s = an.symbolic
+    ps, order = an.pivot_scale, an.ordering
+    k = next(int(s.node_first[u]) for u in range(s.nnodes) if s.node_kind[u] == 0 and s.nl[u] == 0)
+    v = np.array(p.A.values)
+    rp, ci = p.A.row_ptr, p.A.col_idx
+    c = int(order.perm[k])
+    r = int(ps.row_perm[c])
+    v[rp[r] + int(np.flatnonzero(ci[rp[r]:rp[r + 1]] == c)[0])] = 0.0
+    A = p.A.with_values(v)
+    with pytest.raises(errors.NumericBreakdown):
+        api.refactorize(A, f0, api.FactorOptions(perturbation_epsilon=0.0))
+    f = api.refactorize(A, f0)                      # default eps: perturbed, no error
+    assert len(f.perturbed) >= 1
