@@ -585,6 +585,10 @@ int hy_set_option(hy_handle *h, const char *name, int64_t value) {
     h->prefetch = (int)value;
     return HY_OK;
   }
+  if (std::string(name) == "pipe_blocks" && value >= 0) {   // 0: occupancy-derived (default)
+    h->pipe_blocks = (int)value;
+    return HY_OK;
+  }
   if (std::string(name) == "pipe_ws" && value >= 1 && value <= 64) {
     h->pipe_ws = (int)value;
     h->pipe_blocks = 0;

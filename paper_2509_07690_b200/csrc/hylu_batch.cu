@@ -556,7 +556,10 @@ __device__ __forceinline__ void bt_node2(const DevSym &S, const BatchP &P, const
 
 // Pair-mode pipeline: task records carry the even group g of the pair; the warp
 // waits for both groups' dependency flags and publishes both.
-__global__ void __launch_bounds__(PIPE_WARPS * 32, 4)
+#ifndef PIPE_MINB_DEF
+#define PIPE_MINB_DEF 4
+#endif
+__global__ void __launch_bounds__(PIPE_WARPS * 32, PIPE_MINB_DEF)
     k_bt_pipe2(DevSym S, BatchP P, DevProg R, const TaskDesc *tasks, int64_t total, const double *rhs,
                double *Y, int *counter, int *flags, int epoch, int G, int ws, int nowait, int pf) {
   extern __shared__ __align__(16) double pipe_smem[];
