@@ -240,9 +240,17 @@ int hy_solve_batched(hy_handle *h, int64_t B, const double *d_b, double *d_x, ui
 /* Copy instance b's factor values from the last batched call into node layout. */
 int hy_batched_factor_values(hy_handle *h, int64_t b, double *d_out, uintptr_t stream);
 
-/* Tuning knobs: "staged" (0/1: stage each row's source values in shared memory
- * with cp.async in the batched pipeline kernel, default 0); "fanin_dmma" (0/1:
- * route update items of targets with >= 32 rows to the DMMA kernel, default 0). */
+/* Tuning knobs (developer options; defaults are the measured best):
+ *   "fanin_tc"      sup-sup / sup-row update kernels of the level fan-in: 0 FFMA per-source
+ *                   (k_fi_upd), 2 per-source DMMA (k_fi_upd_tc, bitwise equal to 0),
+ *                   4 K-concatenated DMMA (k_fi_upd_kc), 5 (default) = 4 plus the packed
+ *                   small-source items on k_fi_upd_kcp; 1 / 3 route only targets >= 32 rows
+ *   "fanin_overlap" 0/1 (default 1): independent kernels of a fan-in phase on two streams
+ *   "fanin_warp_min" items below which a level keeps its small items on the CTA kernels
+ *   "fanin_dmma"    0/1: legacy per-item DMMA kernel for targets >= 32 rows (default 0)
+ *   "staged"        0/1: cp.async staging of row sources in the non-pair batched kernel
+ *   "pipe_ws", "pipe_blocks", "prefetch", "diagonal_skew", "lev0_split", "hub_dataflow",
+ *   "bwd_persistent": batched-pipeline variants (see DESIGN.md measured dead ends). */
 int hy_set_option(hy_handle *h, const char *name, int64_t value);
 
 /* Number of kernel launches issued by this handle since creation (bench evidence). */
