@@ -180,6 +180,13 @@ typedef struct {
   const int64_t *part_off;                  /* [nparts] partial-tile offset (doubles) in the scratch */
 } hy_fanin_plan;
 int hy_upload_fanin_plan(hy_handle *h, const hy_fanin_plan *plan);
+/* Optional, after hy_upload_fanin_plan: per update-source record (nsrc records, plan
+ * order) the tile position of each of its columns (pos[poff[z] .. poff[z+1]), int8) and
+ * the source's value offset / width / first panel column / block height, so the
+ * K-concatenated update kernel skips the per-item binary searches. */
+int hy_upload_fanin_maps(hy_handle *h, int64_t nsrc, int64_t npos, const int64_t *poff,
+                         const int8_t *pos, const int64_t *vb, const int32_t *vW, const int32_t *qb,
+                         const int32_t *m);
 
 /* Row programs for the batched path (built on the host by schedule.py for a given
  * prior inner_perm).  Must be uploaded before the

@@ -56,6 +56,12 @@ struct FaninDev {
   const int64_t *part_off;
   double *part_scr;
   int *part_cnt;
+  const int64_t *src_poff;   // host-precomputed source maps (hy_upload_fanin_maps)
+  const int8_t *src_pos;
+  const int64_t *src_vb;
+  const int32_t *src_vW;
+  const int32_t *src_qb;
+  const int32_t *src_m;
 };
 __global__ void k_fi_scatter(DevSym, CallP);
 __global__ void k_resid_berr(int, const int64_t *, const int32_t *, const double *, const double *,
@@ -259,6 +265,7 @@ struct hy_handle {
   int32_t *d_acol = nullptr;
   int fi_v3 = 0;                                     // option "fanin_v3" (slower; kept for experiments)
   int fi_mma = 0;                                    // option "fanin_dmma" (bitwise-equal results; slower here)
+  int fi_maps = 1;                                   // option "fanin_maps": use host-precomputed source maps in k_fi_upd_kc
   int fi_overlap = 1;                                // option "fanin_overlap": panel TRSM on a side stream, concurrent with the X blocks
   cudaStream_t fi_side = nullptr;
   cudaEvent_t fi_ev_lu = nullptr, fi_ev_pt = nullptr;
@@ -542,6 +549,10 @@ int hy_set_option(hy_handle *h, const char *name, int64_t value) {
     h->fi_v3 = value != 0;
     return HY_OK;
   }
+  if (std::string(name) == "fanin_maps") {
+    h->fi_maps = value != 0;
+    return HY_OK;
+  }
   if (std::string(name) == "fanin_overlap") {
     h->fi_overlap = value != 0;
     return HY_OK;
@@ -803,6 +814,8 @@ int hy_upload_fanin_plan(hy_handle *h, const hy_fanin_plan *d) {
   h->fi_allocs.clear();
   const int64_t nl = d->nlevels;
   FaninDev &D = h->fi;
+  D.src_poff = nullptr; D.src_pos = nullptr; D.src_vb = nullptr;
+  D.src_vW = nullptr; D.src_qb = nullptr; D.src_m = nullptr;
   int32_t *p32;
   int64_t *p64;
   UPF(&p32, d->lu_nodes, d->lu_ptr[nl]); D.lu_nodes = p32;
@@ -983,7 +996,9 @@ static int run_fanin(hy_handle *h, const CallP &P, cudaStream_t st) {
         h->launches++;
       }
       if (split > rs && h->fi_tc >= 4) {
-        k_fi_upd_kc<<<split - rs, 256, fi_upd_kc_smem(), st>>>(h->S, P, h->fi, rs);
+        FaninDev Dk = h->fi;
+        if (!h->fi_maps) Dk.src_pos = nullptr;
+        k_fi_upd_kc<<<split - rs, 256, fi_upd_kc_smem(), st>>>(h->S, P, Dk, rs);
         h->launches++;
       } else if (split > rs && h->fi_tc == 2) {
         k_fi_upd_tc<<<split - rs, 256, fi_upd_tc_smem(h->fi_smax[l]), st>>>(h->S, P, h->fi, rs, h->fi_smax[l]);
@@ -1014,6 +1029,26 @@ static int run_fanin(hy_handle *h, const CallP &P, cudaStream_t st) {
     }
   }
   CK(cudaGetLastError());
+  return HY_OK;
+}
+
+int hy_upload_fanin_maps(hy_handle *h, int64_t nsrc, int64_t npos, const int64_t *poff,
+                         const int8_t *pos, const int64_t *vb, const int32_t *vW, const int32_t *qb,
+                         const int32_t *m) {
+  if (!h || !h->uploaded || !h->fanin_ok) return fail(HY_INVALID_ARGUMENT, "fan-in plan not uploaded");
+  if (nsrc < 0 || npos < 0 || (nsrc && (!poff || !vb || !vW || !qb || !m)) || (npos && !pos))
+    return fail(HY_INVALID_ARGUMENT, "null source-map arrays");
+  CK(cudaSetDevice(h->device));
+  FaninDev &D = h->fi;
+  int64_t *p64;
+  int32_t *p32;
+  int8_t *p8;
+  UPF(&p64, poff, nsrc + 1); D.src_poff = p64;
+  UPF(&p8, pos, npos); D.src_pos = p8;
+  UPF(&p64, vb, nsrc); D.src_vb = p64;
+  UPF(&p32, vW, nsrc); D.src_vW = p32;
+  UPF(&p32, qb, nsrc); D.src_qb = p32;
+  UPF(&p32, m, nsrc); D.src_m = p32;
   return HY_OK;
 }
 

@@ -51,6 +51,13 @@ struct FaninDev {
   const int64_t *part_off;
   double *part_scr;          // partial tiles
   int *part_cnt;             // arrivals per split item (indexed by its first part id)
+  // host-precomputed per source record (k_fi_upd_kc; null: derived on the device)
+  const int64_t *src_poff;   // [nsrc+1] offsets into src_pos
+  const int8_t *src_pos;     // tile position of each of the record's columns
+  const int64_t *src_vb;     // source node value offset
+  const int32_t *src_vW;     // source node width
+  const int32_t *src_qb;     // first panel column of the record in the source
+  const int32_t *src_m;      // source block rows from the first present one
 };
 
 constexpr int FI_THREADS = 256;
@@ -1060,8 +1067,30 @@ __global__ void __launch_bounds__(FI_THREADS, KC_MINB_DEF) k_fi_upd_kc(DevSym S,
     // tile positions first)
     for (int k = warp; k < (int)(ze - zb); k += FI_THREADS / 32) {
       const int64_t z = zb + k;
-      const int v = D.src_v[z];
       const int nq = D.src_q1[z] - D.src_q0[z];
+      if (D.src_pos) {
+        // host-precomputed: metadata and the tile position of every source column
+        // (one round of independent loads, no binary search)
+        if (lane == 0) {
+          s_vb[k] = D.src_vb[z];
+          s_vW[k] = D.src_vW[z];
+          s_qb[k] = D.src_qb[z];
+          s_pb[k] = D.src_pb[z];
+          s_tb[k] = D.src_tb[z];
+          s_m[k] = D.src_m[z];
+        }
+        const int8_t *pz = D.src_pos + D.src_poff[z];
+        for (int c = lane; c < 64; c += 32) {
+          int pos = -1;
+          if (c < nq) {
+            pos = pz[c];
+            cidx[pos] = 1;
+          }
+          inv[k * 64 + c] = (int8_t)pos;
+        }
+        continue;
+      }
+      const int v = D.src_v[z];
       const int vs = (int)(S.first[v + 1] - S.first[v]);
       const int64_t vcol = S.colptr[v];
       const int qb = S.nl[v] + vs + D.src_q0[z];

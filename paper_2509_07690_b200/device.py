@@ -141,6 +141,7 @@ def library():
     lib.hy_set_option.argtypes = [vp, ctypes.c_char_p, i64]
     lib.hy_upload_slab_plan.argtypes = [vp, ctypes.POINTER(SlabPlanDesc)]
     lib.hy_upload_fanin_plan.argtypes = [vp, ctypes.POINTER(FaninPlanDesc)]
+    lib.hy_upload_fanin_maps.argtypes = [vp, i64, i64, vp, vp, vp, vp, vp, vp]
     lib.hy_upload_hub_programs.argtypes = [vp, ctypes.POINTER(ProgramsDesc)]
     _lib = lib
     return lib
@@ -277,6 +278,18 @@ class DeviceContext:
         with self.torch.cuda.device(self.device):
             check(self.lib.hy_upload_fanin_plan(self.h, ctypes.byref(d)))
         self._fanin_arrays = arrs
+        if os.environ.get("HYLU_FANIN_MAPS", "1") != "0":
+            # per source record: tile positions of its columns + source metadata
+            # (k_fi_upd_kc skips its per-item binary searches); cached with the plan
+            maps = getattr(s, "_kc_maps", None)
+            if maps is None:
+                maps = schedule.kc_source_maps(s, plan)
+                s._kc_maps = maps
+            off, pos, vb, vW, qb, mm = maps
+            ptr = lambda a: a.ctypes.data if a.size else None  # noqa: E731
+            with self.torch.cuda.device(self.device):
+                check(self.lib.hy_upload_fanin_maps(self.h, len(vb), len(pos), ptr(off), ptr(pos), ptr(vb),
+                                                    ptr(vW), ptr(qb), ptr(mm)))
 
     def upload_slab_plan(self):
         from . import schedule

@@ -1136,6 +1136,58 @@ def fanin_source_records(sym, plan):
     return v, pb0, tb0
 
 
+@njit(cache=True)
+def _kc_maps(first, colptr, cols, nl, valoff, up_t, up_c0, up_c1, up_ptr, src_q0, src_q1, sv, stb):
+    nsrc = len(src_q0)
+    off = np.zeros(nsrc + 1, np.int64)
+    for z in range(nsrc):
+        off[z + 1] = off[z] + (src_q1[z] - src_q0[z])
+    pos = np.empty(off[nsrc], np.int8)
+    vb = np.empty(nsrc, np.int64)
+    vW = np.empty(nsrc, np.int32)
+    qb = np.empty(nsrc, np.int32)
+    mm = np.empty(nsrc, np.int32)
+    for it in range(len(up_t)):
+        T = up_t[it]
+        t0 = colptr[T] + up_c0[it]
+        t1 = colptr[T] + up_c1[it]
+        for z in range(up_ptr[it], up_ptr[it + 1]):
+            v = sv[z]
+            vs = first[v + 1] - first[v]
+            q = nl[v] + vs + src_q0[z]
+            vb[z] = valoff[v]
+            vW[z] = colptr[v + 1] - colptr[v]
+            qb[z] = q
+            mm[z] = vs - stb[z]
+            base = colptr[v] + q
+            lo = t0
+            for c in range(src_q1[z] - src_q0[z]):
+                key = cols[base + c]
+                # columns ascend: continue the search from the previous position
+                hi = t1
+                while lo < hi:
+                    mid = (lo + hi) >> 1
+                    if cols[mid] < key:
+                        lo = mid + 1
+                    else:
+                        hi = mid
+                pos[off[z] + c] = lo - t0
+    return off, pos, vb, vW, qb, mm
+
+
+def kc_source_maps(sym, plan):
+    """Per update-source record, host-precomputed for the K-concatenated DMMA kernel:
+    the tile position (0..63) of each of its nq columns (int8, records concatenated,
+    offsets int64) and the source's value offset / width / first panel column / block
+    height — the data the kernel otherwise derives per item with dependent loads and
+    binary searches."""
+    s = sym
+    sv, _, stb = fanin_source_records(s, plan)
+    return _kc_maps(np.asarray(s.node_first), np.asarray(s.colptr), np.asarray(s.cols), np.asarray(s.nl),
+                    np.asarray(s.valoff), plan.up_t, plan.up_c0, plan.up_c1, plan.up_ptr,
+                    plan.src_q0, plan.src_q1, sv, stb)
+
+
 def executed_update_flops(sym, plan):
     """Flops the fan-in sup-sup / sup-row updates execute on the union-padded node
     panels: Σ over update-source records of 2·s_T·m·nq (target rows × source block
