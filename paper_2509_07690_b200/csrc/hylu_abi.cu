@@ -985,7 +985,9 @@ static int run_fanin(hy_handle *h, const CallP &P, cudaStream_t st) {
       }
       cudaStream_t sk = sideB ? h->fi_side : st;
       if (npk && h->fi_tc == 5) {
-        k_fi_upd_kcp<<<npk, 256, fi_upd_kc_smem(), sk>>>(h->S, P, h->fi, (int)h->fi_up[l]);
+        FaninDev Dp = h->fi;
+        if (!h->fi_maps) Dp.src_pos = nullptr;
+        k_fi_upd_kcp<<<npk, 256, fi_upd_kc_smem(), sk>>>(h->S, P, Dp, (int)h->fi_up[l]);
         h->launches++;
       } else if (npk) {
         k_fi_upd_pk<<<npk, 256, sm, sk>>>(h->S, P, h->fi, (int)h->fi_up[l], h->fi_smax[l], h->fi_mmax[l]);

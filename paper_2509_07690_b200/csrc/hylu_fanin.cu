@@ -1343,8 +1343,28 @@ __global__ void __launch_bounds__(FI_THREADS, KC_MINB_DEF) k_fi_upd_kcp(DevSym S
   auto source_maps = [&](int64_t zb0, int nsb, bool pos) {
     for (int k = warp; k < nsb; k += FI_THREADS / 32) {
       const int64_t z = zb0 + k;
-      const int v = D.src_v[z];
       const int nq = D.src_q1[z] - D.src_q0[z];
+      if (D.src_pos) {   // host-precomputed maps (hy_upload_fanin_maps)
+        if (lane == 0) {
+          s_vb[k] = D.src_vb[z];
+          s_vW[k] = D.src_vW[z];
+          s_qb[k] = D.src_qb[z];
+          s_pb[k] = D.src_pb[z];
+          s_tb[k] = D.src_tb[z];
+          s_m[k] = D.src_m[z];
+        }
+        const int8_t *pz = D.src_pos + D.src_poff[z];
+        for (int c = lane; c < 64; c += 32) {
+          int p = -1;
+          if (c < nq) {
+            p = pz[c];
+            if (pos) cidx[p] = 1;
+          }
+          inv[k * 64 + c] = (int8_t)p;
+        }
+        continue;
+      }
+      const int v = D.src_v[z];
       const int vs = (int)(S.first[v + 1] - S.first[v]);
       const int64_t vcol = S.colptr[v];
       const int qb = S.nl[v] + vs + D.src_q0[z];
