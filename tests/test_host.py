@@ -341,3 +341,29 @@ def test_cli_usage_and_input_errors(tmp_path, capsys):
     f.write_text("1 2\n")
     with pytest.raises(errors.LengthMismatch):
         cli.generate_rhs(str(f), 3)
+
+
+def test_kc_source_maps_match_direct_search():
+    """schedule.kc_source_maps: every source column's tile position equals a direct
+    search of the target tile's columns, and the metadata matches the node arrays."""
+    import numpy as np
+    from paper_2509_07690_b200 import generators as gen, analysis as an_mod, schedule
+    from paper_2509_07690_b200._ref import SolverConfig
+    for name in ("c2", "c3", "c1"):
+        p = gen.config(name, "small")
+        s = an_mod.analyze(p.A, SolverConfig(ordering=p.ordering)).symbolic
+        plan = schedule.build_fanin_plan(s)
+        off, pos, vb, vW, qb, mm = schedule.kc_source_maps(s, plan)
+        sv, _, stb = schedule.fanin_source_records(s, plan)
+        cols, colptr = np.asarray(s.cols), np.asarray(s.colptr)
+        first, nl, valoff = np.asarray(s.node_first), np.asarray(s.nl), np.asarray(s.valoff)
+        for it in range(len(plan.up_t)):
+            T = plan.up_t[it]
+            tc = cols[colptr[T] + plan.up_c0[it]:colptr[T] + plan.up_c1[it]]
+            for z in range(plan.up_ptr[it], plan.up_ptr[it + 1]):
+                v = sv[z]
+                vs = first[v + 1] - first[v]
+                q = nl[v] + vs + plan.src_q0[z]
+                sc = cols[colptr[v] + q:colptr[v] + q + plan.src_q1[z] - plan.src_q0[z]]
+                assert np.array_equal(pos[off[z]:off[z + 1]], np.searchsorted(tc, sc))
+                assert (vb[z], vW[z], qb[z], mm[z]) == (valoff[v], colptr[v + 1] - colptr[v], q, vs - stb[z])
