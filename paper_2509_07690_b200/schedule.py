@@ -26,7 +26,7 @@ from dataclasses import dataclass
 import os
 
 import numpy as np
-from numba import njit
+from numba import njit, prange
 
 HUB_STEPS = 384
 
@@ -1136,7 +1136,7 @@ def fanin_source_records(sym, plan):
     return v, pb0, tb0
 
 
-@njit(cache=True)
+@njit(cache=True, parallel=True)
 def _kc_maps(first, colptr, cols, nl, valoff, up_t, up_c0, up_c1, up_ptr, src_q0, src_q1, sv, stb):
     nsrc = len(src_q0)
     off = np.zeros(nsrc + 1, np.int64)
@@ -1147,7 +1147,7 @@ def _kc_maps(first, colptr, cols, nl, valoff, up_t, up_c0, up_c1, up_ptr, src_q0
     vW = np.empty(nsrc, np.int32)
     qb = np.empty(nsrc, np.int32)
     mm = np.empty(nsrc, np.int32)
-    for it in range(len(up_t)):
+    for it in prange(len(up_t)):   # items own disjoint record ranges
         T = up_t[it]
         t0 = colptr[T] + up_c0[it]
         t1 = colptr[T] + up_c1[it]
