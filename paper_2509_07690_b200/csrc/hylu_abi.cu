@@ -994,7 +994,9 @@ static int run_fanin(hy_handle *h, const CallP &P, cudaStream_t st) {
         h->launches++;
       }
       if (rs > reg) {
-        k_fi_upd_w<<<(rs - reg + 7) / 8, 256, 0, st>>>(h->S, P, h->fi, reg, rs - reg);
+        FaninDev Dw = h->fi;
+        if (!h->fi_maps) Dw.src_pos = nullptr;
+        k_fi_upd_w<<<(rs - reg + 7) / 8, 256, 0, st>>>(h->S, P, Dw, reg, rs - reg);
         h->launches++;
       }
       if (split > rs && h->fi_tc >= 4) {

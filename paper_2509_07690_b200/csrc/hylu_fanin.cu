@@ -407,21 +407,32 @@ __global__ void __launch_bounds__(FI_THREADS) k_fi_upd_w(DevSym S, CallP P, Fani
     for (int t = 0; t < s; ++t) acc[t * UW_TILE + c] = Pm[(int64_t)t * W + c0 + c];
   }
   __syncwarp();
+  const bool maps = D.src_pos != nullptr;   // host-precomputed positions / metadata
   for (int64_t z = D.up_ptr[j]; z < D.up_ptr[j + 1]; ++z) {
-    const int v = D.src_v[z];
     const int q0 = D.src_q0[z];
     const int nq = D.src_q1[z] - q0;
-    const int vf = (int)S.first[v];
-    const int vs = (int)(S.first[v + 1] - vf);
-    const int64_t vc0 = S.colptr[v];
-    const int vW = (int)(S.colptr[v + 1] - vc0);
-    const double *vb = P.F + S.valoff[v];
     const int pb0 = D.src_pb[z];
     const int tb0 = D.src_tb[z];
-    const int m = vs - tb0;
-    const int qbase = S.nl[v] + vs + q0;
+    int vW, m, qbase;
+    int64_t vc0 = 0;
+    const double *vb;
+    if (maps) {
+      vW = D.src_vW[z];
+      m = D.src_m[z];
+      qbase = D.src_qb[z];
+      vb = P.F + D.src_vb[z];
+    } else {
+      const int v = D.src_v[z];
+      const int vs = (int)(S.first[v + 1] - S.first[v]);
+      vc0 = S.colptr[v];
+      vW = (int)(S.colptr[v + 1] - vc0);
+      vb = P.F + S.valoff[v];
+      m = vs - tb0;
+      qbase = S.nl[v] + vs + q0;
+    }
     for (int q = lane; q < nq; q += 32) {
-      const int pos = lower_bound_i32(tcol, 0, tw, S.cols[vc0 + qbase + q]);
+      const int pos = maps ? (int)D.src_pos[D.src_poff[z] + q]
+                           : lower_bound_i32(tcol, 0, tw, S.cols[vc0 + qbase + q]);
       double c[UW_ROWS];
 #pragma unroll
       for (int t = 0; t < UW_ROWS; ++t) c[t] = 0.0;
