@@ -1,8 +1,8 @@
 #!/usr/bin/env python
 """bench.py — headline benchmark (driver contract).
 
-Workload (BASELINE.json configs[4], the config BASELINE's "refactors/sec" metric
-is quoted on and the only one that shards): 4096 same-pattern circuit-like
+Headline workload (BASELINE.json configs[4], the config BASELINE's "refactors/sec"
+metric is quoted on and the only one that shards): 4096 same-pattern circuit-like
 matrices (n = 20000, ~102k nnz each), ONE host analysis on instance 0, then per
 instance refactorize + solve on the device.  A step = one refactorize+solve pass
 over every instance of the job (4096 in total, split contiguously across the N
@@ -14,9 +14,19 @@ e2e    = the same through the public API with host (pinned) buffers: values and
 roofline (dominant kernel = batched refactorization): algorithmic bytes per
          instance 8·(nnz + fill_nnz) x instances / factor-phase time,
          against MEASURED_PEAKS.json hbm_gbs.
-cpu_baseline: the CPU oracle (numba restatement of SPEC, oracle/numeric.py) on
-         a bounded sample of the same workload, all host threads.
-``--impl reference`` times that CPU path alone as the reference arm.
+cpu_baseline: the CPU oracle (numba restatement of SPEC, oracle/numeric.py) over
+         the same 4096 instances, all host threads.
+parity:  every instance's x and perturbation count against the oracle (the pass
+         the cpu_baseline leg times), outside the timed region; the run fails on a
+         mismatch.
+configs: c0-c3 (BASELINE configs[0..3]) single-factorization numbers on rank 0:
+         factor / refactor / solve ms (CUDA events, L2 flushed between repetitions),
+         GFLOP/s (algorithmic and executed) against the measured FP64 peak (c2/c3)
+         or bytes against HBM (c0/c1), clocks, parity against the oracle, and the
+         oracle's time on 1 thread and on all host threads.
+``--impl reference`` times the reference's CPU path (the oracle port: the
+reference ships no numeric code) on the same c4 workload as the reference arm.
+``--gpus N`` without a launcher re-executes itself under torch.distributed.run.
 """
 
 from __future__ import annotations
@@ -24,6 +34,8 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
+import subprocess
 import sys
 import threading
 import time
@@ -35,6 +47,10 @@ sys.path.insert(0, ROOT)
 
 N_INST = 4096
 N = 20000
+METRIC = "refactors/sec (c4: batched FP64 refactorize+solve, n=20000)"
+X_RTOL = 1e-9        # x vs oracle (north_star: L/U 1e-11, residual 1e-10; x inherits κ)
+LU_RTOL = 1e-11
+RES_TOL = 1e-10
 
 
 def _peaks():
@@ -44,6 +60,16 @@ def _peaks():
         return float(p["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+def _fp64_peak():
+    """FP64 peak measured on a B200 of this pool in round 1 (scripts/fp64_peak.py:
+    DMMA m8n8k4 microbenchmark 37.14 TF/s, cuBLAS DGEMM 35.5, DFMA 34.2)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peak_r01.json")) as fh:
+            return float(json.load(fh)["fp64_peak_tflops"]), "measured (profiles/fp64_peak_r01.json)"
+    except Exception:
+        return 37.0, "fallback"
 
 
 class ClockSampler:
@@ -82,7 +108,7 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
-            time.sleep(0.01)
+            time.sleep(0.005)
 
     def __enter__(self):
         if self.ok:
@@ -103,6 +129,7 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+# --------------------------------------------------------------------------- c4 problem
 def make_problem(lo, hi, threads):
     from paper_2509_07690_b200 import generators as gen
     base = gen.circuit(N, 3, 2000, gen.SEEDS["c4"])
@@ -120,82 +147,237 @@ def analysis_for(A0):
     return analysis.analyze(A0, SolverConfig(ordering="amd"))
 
 
-def cpu_sample(an, bv, count, threads):
-    """Oracle refactorize+solve over ``count`` instances (all host threads)."""
+def c4_config(A0, s, world):
+    """The workload description both arms print (identical dicts)."""
+    return {"workload": "c4 batched refactorize+solve (BASELINE configs[4])", "batch": N_INST,
+            "n": N, "nnz": int(A0.nnz), "fill_nnz": int(s.fill_nnz),
+            "stored_values": int(s.stored_values), "kernel_mode": s.kernel_mode.name,
+            "levels": int(len(s.level_ptr) - 1),
+            "l2": "inputs larger than L2 (values %.2f GB/step)" % (N_INST * A0.nnz * 8 / 1e9),
+            "parallelism": "shard%d" % world}
+
+
+def oracle_pass(an, prior, vals, rhs, threads):
+    """One oracle refactorize+solve pass over the given instances (numba, instances
+    in parallel on ``threads`` host threads)."""
     import numba
     from oracle import numeric as on
-    numba.set_num_threads(threads)
-    prior = on.factorize(an)
-    vals = np.empty((count, bv.nnz))
-    rhs = np.empty((count, bv.n))
-    bv.fill(range(count), vals, rhs, threads)
-    on.refactor_solve_batch(an, prior, vals[:2], rhs[:2])          # JIT warm-up
-    reps = 0
+    numba.set_num_threads(max(1, min(threads, numba.config.NUMBA_NUM_THREADS)))
     t0 = time.perf_counter()
-    while True:                      # about 10 s of CPU work (whole passes over the sample)
-        on.refactor_solve_batch(an, prior, vals, rhs)
-        reps += 1
-        dt = time.perf_counter() - t0
-        if dt >= 10.0 or reps >= 64:
-            break
-    return count * reps / dt, dt, reps
+    X, npert = on.refactor_solve_batch(an, prior, vals, rhs)
+    return X, npert, time.perf_counter() - t0
 
 
 def run_reference(args):
+    """Reference arm: the reference's CPU path (oracle port) on the c4 workload, all
+    host threads, each step one pass over the whole 4096-instance batch."""
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     if rank != 0:
         return
     import numba
     threads = numba.config.NUMBA_NUM_THREADS
-    A0, bv, _, _ = make_problem(0, 1, threads)
+    A0, bv, vals, rhs = make_problem(0, N_INST, threads)
     an = analysis_for(A0)
     from oracle import numeric as on
-    numba.set_num_threads(threads)
     prior = on.factorize(an)
-    sample = args.ref_sample
-    vals = np.empty((sample, bv.nnz))
-    rhs = np.empty((sample, bv.n))
-    bv.fill(range(sample), vals, rhs, threads)
+    oracle_pass(an, prior, vals[:2], rhs[:2], threads)        # JIT warm-up
     for _ in range(max(1, args.warmup)):
-        on.refactor_solve_batch(an, prior, vals, rhs)
+        oracle_pass(an, prior, vals, rhs, threads)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        on.refactor_solve_batch(an, prior, vals, rhs)
+        oracle_pass(an, prior, vals, rhs, threads)
     dt = time.perf_counter() - t0
-    value = sample * args.steps / dt
+    value = N_INST * args.steps / dt
     s = an.symbolic
     line = {
-        "impl": "reference",
-        "metric": "refactors/sec (c4: batched FP64 refactorize+solve, n=20000)",
-        "value": value, "unit": "instances/s", "n_gpus": args.gpus, "steps": args.steps,
+        "impl": "reference", "metric": METRIC,
+        "value": value, "unit": "instances/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
-        "config": {"workload": "c4 batched refactorize+solve", "batch": N_INST, "n": N,
-                   "nnz": int(A0.nnz), "fill_nnz": int(s.fill_nnz), "kernel_mode": s.kernel_mode.name},
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generators, paper_2509_07690_b200/generators.py)",
+        "config": c4_config(A0, s, world),
         "cpu_baseline": {"value": value, "unit": "instances/s", "cores": threads, "kind": "port",
-                         "sample": "%d of the 4096 instances per step (oracle/numeric.py, numba, "
-                                   "instances in parallel)" % sample},
+                         "sample": "every step = all %d instances (refactorize+solve, "
+                                   "oracle/numeric.py, numba, instances in parallel)" % N_INST},
         "e2e": {"value": value, "unit": "instances/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+# --------------------------------------------------------------------------- c0-c3
+def _l2_flusher(dev):
+    import torch
+    buf = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)   # 256 MB > 126 MB L2
+
+    def flush():
+        buf.fill_(1.0)
+    return flush
+
+
+def _timed(fn, reps, flush, stream):
+    import torch
+    ts, out = [], None
+    for _ in range(reps):
+        flush()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record(stream)
+        out = fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return float(np.median(ts)), float(min(ts)), out
+
+
+def _cpu_oracle_times(an, budget_s=8.0):
+    """Oracle factorize on 1 thread and on all host threads (best of repeats within
+    a time budget each; the first call of each executor is the numba warm-up)."""
+    import numba
+    from oracle import numeric as on
+    allt = numba.config.NUMBA_NUM_THREADS
+    out = {}
+    ref = None
+    for th in (1, allt):
+        f = on.factorize(an, threads=th)          # warm-up (JIT) + result
+        ref = ref or f
+        best, t_end, k = 1e30, time.perf_counter() + budget_s, 0
+        while k < 1 or (time.perf_counter() < t_end and k < 20):
+            t0 = time.perf_counter()
+            on.factorize(an, threads=th)
+            best = min(best, time.perf_counter() - t0)
+            k += 1
+        out["1_thread_ms" if th == 1 else "all_threads_ms"] = best * 1e3
+        if th != 1:
+            out["threads"] = th
+    return out, ref
+
+
+def measure_single(name, p, dev, flush, reps, cpu=True):
+    """Device factor / refactor / solve of one BASELINE config (+ oracle parity and
+    CPU times when ``cpu``)."""
+    import torch
+    from paper_2509_07690_b200 import analysis, api, schedule
+    from paper_2509_07690_b200._ref import SolverConfig, matrix as refmatrix
+    t0 = time.perf_counter()
+    an = analysis.analyze(p.A, SolverConfig(ordering=p.ordering))
+    t_an = time.perf_counter() - t0
+    s = an.symbolic
+    stream = torch.cuda.current_stream(dev)
+    dv = torch.from_numpy(np.array(p.A.values, np.float64)).to(dev)
+    db = torch.from_numpy(np.array(p.b, np.float64)).to(dev)
+    t0 = time.perf_counter()
+    f = api.factorize_analysis(an, dv)            # context + plan upload + first factorization
+    torch.cuda.synchronize()
+    t_up = time.perf_counter() - t0
+    ctx = f._ctx
+    with ClockSampler(dev.index) as clk:
+        l0 = ctx.launches()
+        tf, tf_min, f = _timed(lambda: api.factorize_analysis(an, dv), reps, flush, stream)
+        launches = ctx.launches() - l0
+        tr, tr_min, f2 = _timed(lambda: api.refactorize(dv, f), reps, flush, stream)
+        ts, ts_min, x = _timed(lambda: api.substitute(f, db), reps, flush, stream)
+    xh = x.cpu().numpy()
+    res = float(np.linalg.norm(refmatrix.spmv(p.A, xh) - p.b) / np.linalg.norm(p.b))
+    fill, nnz = s.fill_nnz, p.A.nnz
+    bytes_f = 8 * nnz + 8 * fill + 4 * (nnz + fill)
+    bytes_s = 12 * fill + 24 * s.n
+    peak_tf, _ = _fp64_peak()
+    hbm, _ = _peaks()
+    out = {"n": int(s.n), "nnz": int(nnz), "fill_nnz": int(fill), "flops": float(s.flops),
+           "kernel_mode": s.kernel_mode.name, "nodes": int(s.nnodes),
+           "supernodes": int(s.supernode_count), "levels": int(len(s.level_ptr) - 1),
+           "stored_values": int(s.stored_values), "ordering": p.ordering,
+           "host_analyze_s": round(t_an, 2), "host_upload_first_factor_s": round(t_up, 2),
+           "factor_ms": tf, "factor_ms_min": tf_min, "refactor_ms": tr, "refactor_ms_min": tr_min,
+           "solve_ms": ts, "solve_ms_min": ts_min, "factor_launches": int(launches),
+           "gflops": s.flops / tf / 1e6, "refactor_gflops": s.flops / tr / 1e6,
+           "factor_hbm_gbs": bytes_f / tf / 1e6, "solve_hbm_gbs": bytes_s / ts / 1e6,
+           "residual": res, "npert": len(f.perturbed), "clocks": clk.summary(),
+           "l2": "flushed (256 MB write) before every repetition", "reps": reps}
+    plan = getattr(s, "_fanin_plan", None)
+    if plan is not None:
+        ex = schedule.executed_update_flops(s, plan)
+        out["executed_update_flops"] = ex
+        out["executed_update_gflops"] = ex / tf / 1e6
+    if s.kernel_mode.name == "SUPSUP":
+        out["roofline"] = {"bound": "fp64", "achieved": s.flops / tf / 1e9, "peak": peak_tf,
+                           "unit": "TFLOP/s", "frac": s.flops / tf / 1e9 / peak_tf,
+                           "executed_frac": (out.get("executed_update_flops", 0.0) / tf / 1e9) / peak_tf}
+    else:
+        out["roofline"] = {"bound": "hbm", "achieved": bytes_f / tf / 1e6, "peak": hbm,
+                           "unit": "GB/s", "frac": bytes_f / tf / 1e6 / hbm,
+                           "note": "latency-bound: %d dependent levels" % (len(s.level_ptr) - 1)}
+    if not res <= RES_TOL:
+        raise SystemExit("%s: residual %.3g above %.0e" % (name, res, RES_TOL))
+    if cpu:
+        ct, ref = _cpu_oracle_times(an)
+        from oracle import numeric as on
+        xo, _ = on.solve(an, ref, p.b)
+        fv = f.host_values()
+        par = {"inner_perm_equal": bool(np.array_equal(f.host_inner_perm(), ref.inner_perm)),
+               "lu_max_rel": float(np.abs(fv - ref.values).max() / max(1.0, np.abs(ref.values).max())),
+               "x_max_rel": float(np.abs(xh - xo).max() / max(1.0, np.abs(xo).max())),
+               "npert_equal": len(f.perturbed) == len(ref.perturbed)}
+        out["parity"] = par
+        ct["gpu_speedup_vs_all_threads"] = ct["all_threads_ms"] / tf
+        out["cpu_oracle"] = ct
+        if not (par["inner_perm_equal"] and par["lu_max_rel"] <= LU_RTOL and par["x_max_rel"] <= X_RTOL):
+            raise SystemExit("%s: parity failure %s" % (name, par))
+    del f, f2, x
+    return out
+
+
+def run_configs(args, dev):
+    """c0-c3 (replicas only: one factorization per GPU, measured on rank 0)."""
+    from paper_2509_07690_b200 import generators as gen
+    flush = _l2_flusher(dev)
+    res = {}
+    t_all = time.perf_counter()
+    for name in [c for c in args.configs.split(",") if c]:
+        t0 = time.perf_counter()
+        if name in ("c0", "c1"):
+            res[name] = measure_single(name, gen.config(name), dev, flush, reps=20)
+        elif name == "c2":
+            full = measure_single(name, gen.config("c2"), dev, flush, reps=5, cpu=False)
+            k = args.c2_sample
+            full["sample"] = measure_single("c2_%d" % k, gen.convdiff3d(k), dev, flush, reps=5)
+            full["sample"]["what"] = ("convdiff3d(%d): the c2 recipe at n=%d, where the CPU oracle "
+                                      "finishes in seconds (parity + CPU times)" % (k, k ** 3))
+            res[name] = full
+        elif name == "c3":
+            full = measure_single(name, gen.fem27(args.c3k), dev, flush, reps=3, cpu=False)
+            k = args.c3_sample
+            full["sample"] = measure_single("c3_%d" % k, gen.fem27(k), dev, flush, reps=5)
+            full["sample"]["what"] = ("fem27(%d): the c3 recipe at n=%d (parity + CPU times)"
+                                      % (k, 3 * k ** 3))
+            res[name] = full
+        res[name]["wall_s"] = round(time.perf_counter() - t0, 1)
+        import gc
+        gc.collect()
+    res["_total_wall_s"] = round(time.perf_counter() - t_all, 1)
+    return res
+
+
+# --------------------------------------------------------------------------- ours
 def run_ours(args):
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit("bench.py: WORLD_SIZE=%d but --gpus %d" % (world, args.gpus))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
-    from paper_2509_07690_b200 import api
+    from paper_2509_07690_b200 import api, sharding
+    from paper_2509_07690_b200.device import check
     threads = max(1, (os.cpu_count() or 8) // max(1, world))
-    from paper_2509_07690_b200.sharding import shard_range
-    lo, hi = shard_range(N_INST, rank, world)
+    lo, hi = sharding.shard_range(N_INST, rank, world)
     B = hi - lo
     A0, bv, vals, rhs = make_problem(lo, hi, threads)
     an = analysis_for(A0)
@@ -210,7 +392,6 @@ def run_ours(args):
     d_np = torch.empty(B, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream(dev)
     sh = ctx.stream_handle(stream)
-    from paper_2509_07690_b200.device import check
 
     def step(ev=None):
         if ev is not None:
@@ -224,13 +405,6 @@ def run_ours(args):
     def barrier():
         if dist is not None:
             dist.barrier()
-
-    def max_over_ranks(v):
-        if dist is None:
-            return v
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
 
     for _ in range(args.warmup):
         step()
@@ -249,15 +423,13 @@ def run_ours(args):
         torch.cuda.synchronize()
     barrier()
     launches = ctx.launches() - l0
-    elapsed = max_over_ranks(t_ev[0].elapsed_time(t_ev[1]) / 1e3)
+    mine = t_ev[0].elapsed_time(t_ev[1]) / 1e3
+    elapsed = sharding.max_over_ranks(mine, dist, dev)
+    rank_ms = [v / args.steps * 1e3 for v in sharding.all_values(mine, dist, dev)]
     fac_ms = float(np.mean([a.elapsed_time(b) for a, b in fac_ev]))
     value = N_INST * args.steps / elapsed
-
-    # correctness spot check (outside the timed region)
-    from paper_2509_07690_b200._ref import matrix as refmatrix
-    xh = d_x[:2].cpu().numpy()
-    resid = max(np.linalg.norm(refmatrix.spmv(A0.with_values(vals[b]), xh[b]) - rhs[b])
-                / np.linalg.norm(rhs[b]) for b in range(2))
+    x_dev = d_x.cpu().numpy()
+    np_dev = d_np.cpu().numpy()
 
     # ---- e2e through the public API with pinned host buffers
     h_vals = torch.from_numpy(vals).pin_memory()
@@ -283,60 +455,95 @@ def run_ours(args):
     br.host_wait(stream)   # every step's D2H inside the timed region
     e_ev[1].record(stream)
     torch.cuda.synchronize()
-    e_elapsed = max_over_ranks(e_ev[0].elapsed_time(e_ev[1]) / 1e3)
+    e_elapsed = sharding.max_over_ranks(e_ev[0].elapsed_time(e_ev[1]) / 1e3, dist, dev)
     e2e_value = N_INST * args.steps / e_elapsed
+    # the host-buffer results are the device-resident results (same kernels per instance)
+    e2e_rel = float(np.abs(h_x.numpy() - x_dev).max() / max(1.0, np.abs(x_dev).max()))
+    if not (e2e_rel <= 1e-12 and np.array_equal(h_np.numpy(), np_dev)):
+        raise SystemExit("e2e host-buffer results differ from the device path: %g" % e2e_rel)
 
-    # ---- CPU baseline (rank 0 at N=1 only)
+    # ---- parity of every instance against the oracle (+ the CPU baseline timing)
+    import numba
+    cthreads = numba.config.NUMBA_NUM_THREADS if world == 1 else threads
+    from oracle import numeric as on
+    oprior = on.factorize(an)
+    oracle_pass(an, oprior, vals[:2], rhs[:2], cthreads)          # JIT warm-up
+    Xo, npo, dt0 = oracle_pass(an, oprior, vals, rhs, cthreads)
+    par_rel = float(np.max(np.abs(x_dev - Xo).max(axis=1) / np.maximum(1.0, np.abs(Xo).max(axis=1))))
+    par_np = bool(np.array_equal(np_dev.astype(np.int64), npo))
+    par_rel = sharding.max_over_ranks(par_rel, dist, dev)
+    par_np = sharding.max_over_ranks(0.0 if par_np else 1.0, dist, dev) == 0.0
+    if not (par_rel <= X_RTOL and par_np):
+        raise SystemExit("parity failure vs oracle: x max rel %g, npert equal %s" % (par_rel, par_np))
+    resid = 0.0
+    from paper_2509_07690_b200._ref import matrix as refmatrix
+    for b in np.linspace(0, B - 1, 16).astype(int):
+        r = np.linalg.norm(refmatrix.spmv(A0.with_values(vals[b]), x_dev[b]) - rhs[b]) / np.linalg.norm(rhs[b])
+        resid = max(resid, float(r))
+    if not resid <= RES_TOL:
+        raise SystemExit("residual %g above %g" % (resid, RES_TOL))
+
     cpu = None
     if world == 1 and not args.no_cpu:
-        import numba
-        cthreads = numba.config.NUMBA_NUM_THREADS
-        sample = args.cpu_sample
-        cv, cdt, reps = cpu_sample(an, bv, sample, cthreads)
-        cpu = {"value": cv, "unit": "instances/s", "cores": cthreads, "kind": "port",
-               "sample": "%d passes over %d of the 4096 instances (refactorize+solve, "
-                         "oracle/numeric.py, numba parallel over instances), %.1f s"
-                         % (reps, sample, cdt)}
+        reps, dt = 1, dt0
+        while dt < 10.0 and reps < 64:           # about 10 s of CPU work, whole passes
+            dt += oracle_pass(an, oprior, vals, rhs, cthreads)[2]
+            reps += 1
+        cpu = {"value": N_INST * reps / dt, "unit": "instances/s", "cores": cthreads, "kind": "port",
+               "sample": "%d passes over all %d instances (refactorize+solve, oracle/numeric.py, numba "
+                         "parallel over instances), %.1f s" % (reps, N_INST, dt)}
+
+    configs = None
+    if world == 1 and args.configs:
+        configs = run_configs(args, dev)
 
     peak, peak_kind = _peaks()
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as fh:
-            tj = json.load(fh)
-        traffic = float(sum(v for k, v in tj.items() if k.startswith("k_"))) * B / N_INST
-    except Exception:
-        traffic = None
     bytes_per_inst = 8 * (A0.nnz + s.fill_nnz)
     achieved = B * bytes_per_inst / (fac_ms / 1e3) / 1e9
+    traffic = None
+    try:   # ncu capture of this workload (static file, not measured in this run)
+        with open(os.path.join(ROOT, "profiles", "traffic_c4.json")) as fh:
+            tj = json.load(fh)
+        traffic = float(tj["dram_bytes_per_factor_phase"]) * B / N_INST
+        traffic_src = tj.get("source", "profiles/traffic_c4.json")
+    except Exception:
+        traffic_src = None
     if rank == 0:
         line = {
-            "metric": "refactors/sec (c4: batched FP64 refactorize+solve, n=20000)",
+            "metric": METRIC,
             "value": value, "unit": "instances/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": elapsed / args.steps * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generators, paper_2509_07690_b200/generators.py)",
-            "config": {"workload": "c4 batched refactorize+solve (BASELINE configs[4])",
-                       "batch": N_INST, "per_rank": B, "n": N, "nnz": int(A0.nnz),
-                       "fill_nnz": int(s.fill_nnz), "stored_values": int(s.stored_values),
-                       "kernel_mode": s.kernel_mode.name, "levels": int(len(s.level_ptr) - 1),
-                       "l2": "inputs larger than L2 (values %.2f GB/step)" % (vals.nbytes * world / 1e9),
-                       "parallelism": "shard%d" % world},
+            "config": c4_config(A0, s, world),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes per factor phase (ncu)",
-                         "kernel": "k_bt_pipe + k_bt_hub (one batched refactorization pass, forward substitution fused)",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "traffic_source": traffic_src,
+                         "kernel": "k_bt_pipe2 + k_bt_hub (one batched refactorization pass, "
+                                   "forward substitution fused)",
                          "algorithmic_bytes_per_instance": bytes_per_inst,
                          "factor_ms_per_step": fac_ms, "peak_source": peak_kind},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "instances/s",
                     "h2d_bytes_per_step": int(h_vals.numel() * 8 + h_rhs.numel() * 8) * world,
-                    "d2h_bytes_per_step": int(h_x.numel() * 8 + h_np.numel() * 4) * world},
+                    "d2h_bytes_per_step": int(h_x.numel() * 8 + h_np.numel() * 4) * world,
+                    "matches_device_path_rel": e2e_rel},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
-            "residual_max": resid,
+            "gpus_active": world, "rank_ms_per_step": rank_ms,
+            "parity": {"instances": N_INST, "x_max_rel_vs_oracle": par_rel, "npert_equal": par_np,
+                       "tolerance": X_RTOL, "residual_max_16": resid},
+            "configs": configs,
         }
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
 
 
 def main():
@@ -345,17 +552,29 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-sample", type=int, default=4096)
-    ap.add_argument("--ref-sample", type=int, default=512)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-chunks", type=int, default=6)
+    ap.add_argument("--configs", default="c0,c1,c2,c3",
+                    help="comma list of single-factorization configs measured at N=1 ('' = none)")
+    ap.add_argument("--c3k", type=int, default=48)
+    ap.add_argument("--c2-sample", type=int, default=32)
+    ap.add_argument("--c3-sample", type=int, default=16)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
         run_reference(args)
-    else:
-        run_ours(args)
+        return 0
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # N ranks, one per GPU: re-execute under torch.distributed.run
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               "--nproc-per-node=%d" % args.gpus, "--master-addr=127.0.0.1",
+               "--master-port=%d" % _free_port(), os.path.abspath(__file__), *sys.argv[1:]]
+        return subprocess.call(cmd)
+    if "WORLD_SIZE" not in os.environ:
+        os.environ.update(WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    run_ours(args)
+    return 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

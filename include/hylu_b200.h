@@ -254,10 +254,9 @@ int hy_batched_factor_values(hy_handle *h, int64_t b, double *d_out, uintptr_t s
  *                   small-source items on k_fi_upd_kcp; 1 / 3 route only targets >= 32 rows
  *   "fanin_overlap" 0/1 (default 1): independent kernels of a fan-in phase on two streams
  *   "fanin_warp_min" items below which a level keeps its small items on the CTA kernels
- *   "fanin_dmma"    0/1: legacy per-item DMMA kernel for targets >= 32 rows (default 0)
- *   "staged"        0/1: cp.async staging of row sources in the non-pair batched kernel
- *   "pipe_ws", "pipe_blocks", "prefetch", "diagonal_skew", "lev0_split", "hub_dataflow",
- *   "bwd_persistent": batched-pipeline variants (see DESIGN.md measured dead ends). */
+ *   "fanin_maps"    0/1 (default 1): host-precomputed source maps in the update kernels
+ *   "pipe_ws", "pipe_blocks": batched-pipeline shared workspace / resident CTAs
+ *   (the measured-slower variants of round 1 were removed; DESIGN.md lists them). */
 int hy_set_option(hy_handle *h, const char *name, int64_t value);
 
 /* Number of kernel launches issued by this handle since creation (bench evidence). */

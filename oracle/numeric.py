@@ -208,6 +208,146 @@ def factorize_kernel(n, first, kind, colptr, cols, nl, valoff, dptr, deps, node_
     return prow, pval, breakdown
 
 
+@njit(cache=True, inline="always")
+def _internal_lu(F, iperm, r, s, W, L, base, refactor, thr, pflag, pval, bdflag):
+    """internal_factorize of one supernode, as in factorize_kernel."""
+    for t in range(s):
+        Rt = base + t * W
+        if not refactor:
+            p = t
+            best = abs(F[Rt + L + t])
+            for q in range(t + 1, s):
+                vq = abs(F[base + q * W + L + t])
+                if vq > best:
+                    best = vq
+                    p = q
+            if p != t:
+                Rp = base + p * W
+                for c in range(W):
+                    tmp = F[Rt + c]
+                    F[Rt + c] = F[Rp + c]
+                    F[Rp + c] = tmp
+                tmpi = iperm[r + t]
+                iperm[r + t] = iperm[r + p]
+                iperm[r + p] = tmpi
+        piv = F[Rt + L + t]
+        newp, fired = _perturb(piv, thr)
+        if fired:
+            pflag[r + t] = 1
+            pval[r + t] = piv
+        if thr == 0.0 and piv == 0.0:
+            bdflag[r + t] = 1
+        F[Rt + L + t] = newp
+        for q in range(t + 1, s):
+            Rq = base + q * W
+            l = F[Rq + L + t] / newp
+            F[Rq + L + t] = l
+            if l != 0.0:
+                for c in range(L + t + 1, W):
+                    F[Rq + c] -= l * F[Rt + c]
+
+
+@njit(cache=True, parallel=True)
+def factorize_levels_kernel(n, first, kind, colptr, cols, nl, valoff, dptr, deps, node_of, mode,
+                            a_ptr, a_val, mrow_src, colpos, scale, F, iperm, refactor, thr,
+                            level_ptr, level_nodes, nthreads, pflag, pval, bdflag):
+    """The same computation as ``factorize_kernel`` executed level by level
+    (SPEC.md:397-405 ``run_bulk``: the nodes of a level depend only on earlier
+    levels).  Phase 1 runs one task per (node, row) on ``nthreads`` threads: scatter
+    of the row's M values, then every dependency update of that row in ascending
+    source order — per row exactly the operation sequence of the sequential loop
+    (row-row and sup-row updates of a target row read only final source rows and
+    write only that row).  Phase 2 runs the pivots / internal LU per node.  The
+    result is therefore bitwise identical to the sequential executor (tested).
+    Perturbations and breakdowns are flagged per factor row."""
+    smax = 1
+    for u in range(len(kind)):
+        smax = max(smax, first[u + 1] - first[u])
+    pos_all = np.full((nthreads, n), -1, np.int64)
+    x_all = np.empty((nthreads, smax))
+    cur_all = np.full(nthreads, -1, np.int64)
+    nlev = len(level_ptr) - 1
+    for lev in range(nlev):
+        l0 = level_ptr[lev]
+        l1 = level_ptr[lev + 1]
+        cnt = l1 - l0
+        rp = np.empty(cnt + 1, np.int64)
+        rp[0] = 0
+        for k in range(cnt):
+            u = level_nodes[l0 + k]
+            rp[k + 1] = rp[k] + first[u + 1] - first[u]
+        nitems = rp[cnt]
+        for T in prange(nthreads):
+            pos_of = pos_all[T]
+            x = x_all[T]
+            k = 0
+            for it in range(T, nitems, nthreads):
+                while rp[k + 1] <= it:
+                    k += 1
+                u = level_nodes[l0 + k]
+                prow = it - rp[k]
+                r = first[u]
+                c0 = colptr[u]
+                W = colptr[u + 1] - c0
+                base = valoff[u]
+                issn = kind[u] == SUPERNODE
+                if cur_all[T] != u:
+                    if cur_all[T] >= 0:
+                        pu = cur_all[T]
+                        for q in range(colptr[pu], colptr[pu + 1]):
+                            pos_of[cols[q]] = -1
+                    for q in range(W):
+                        pos_of[cols[c0 + q]] = q
+                    cur_all[T] = u
+                # scatter: destination row prow receives M row t with inv[t] == prow
+                t = prow
+                if issn:
+                    if refactor:
+                        t = iperm[r + prow]
+                    else:
+                        iperm[r + prow] = prow
+                R = base + prow * W
+                for c in range(W):
+                    F[R + c] = 0.0
+                a = mrow_src[r + t]
+                for e in range(a_ptr[a], a_ptr[a + 1]):
+                    F[R + colpos[e]] = a_val[e] * scale[e]
+                for di in range(dptr[u], dptr[u + 1]):
+                    v = deps[di]
+                    vfirst = first[v]
+                    vs = first[v + 1] - vfirst
+                    vc0 = colptr[v]
+                    vW = colptr[v + 1] - vc0
+                    vnl = nl[v]
+                    vbase = valoff[v]
+                    if kind[v] == STANDALONE_ROW or mode == ROWROW:
+                        for tj in range(vs):
+                            j = vfirst + tj
+                            if pos_of[j] < 0:
+                                continue
+                            _rowrow(F, R, pos_of, j, F, vbase + tj * vW, vnl + tj, vW, cols, vc0)
+                    else:
+                        _suprow(F, R, pos_of, vfirst, vs, vbase, vW, vnl, cols, vc0, x)
+        for k in prange(cnt):
+            u = level_nodes[l0 + k]
+            r = first[u]
+            s = first[u + 1] - r
+            W = colptr[u + 1] - colptr[u]
+            L = nl[u]
+            base = valoff[u]
+            if kind[u] != SUPERNODE:
+                piv = F[base + L]
+                newp, fired = _perturb(piv, thr)
+                if fired:
+                    pflag[r] = 1
+                    pval[r] = piv
+                if thr == 0.0 and piv == 0.0:
+                    bdflag[r] = 1
+                F[base + L] = newp
+            else:
+                _internal_lu(F, iperm, r, s, W, L, base, refactor, thr, pflag, pval, bdflag)
+
+
 @njit(cache=True)
 def anorm_kernel(a_val, scale):
     m = 0.0
@@ -273,8 +413,14 @@ def _sym_args(an):
             s.dep_ptr, s.deps.astype(np.int64), s.node_of)
 
 
-def factorize(an, values=None, eps=1e-8, mode=None, prior=None):
-    """Oracle factorize (prior=None) or refactorize (prior = OracleFactors)."""
+def factorize(an, values=None, eps=1e-8, mode=None, prior=None, threads=1):
+    """Oracle factorize (prior=None) or refactorize (prior = OracleFactors).
+
+    ``threads=1``: the sequential executor (pivot order).  ``threads>1``:
+    the level-parallel executor ``factorize_levels_kernel`` on that many threads —
+    bitwise the same factors (tests/test_oracle_spec.py::test_parallel_oracle_is_bitwise_sequential)."""
+    if threads and threads > 1:
+        return _factorize_par(an, values, eps, mode, prior, int(threads))
     s = an.symbolic
     vals = np.ascontiguousarray(an.A.values if values is None else values, np.float64)
     vm = an.vmap
@@ -290,6 +436,38 @@ def factorize(an, values=None, eps=1e-8, mode=None, prior=None):
                                       vm.colpos.astype(np.int64), vm.scale, F, iperm,
                                       prior is not None, eps * anorm)
     return OracleFactors(F, iperm, list(zip(prow.tolist(), pval.tolist())), anorm, bd)
+
+
+def _factorize_par(an, values, eps, mode, prior, threads):
+    import numba
+    s = an.symbolic
+    vals = np.ascontiguousarray(an.A.values if values is None else values, np.float64)
+    vm = an.vmap
+    F = np.empty(s.stored_values)
+    if prior is None:
+        iperm = np.zeros(s.n, np.int64)
+        anorm = anorm_kernel(vals, vm.scale)
+    else:
+        iperm = prior.inner_perm.copy()
+        anorm = prior.anorm
+    m = int(s.kernel_mode if mode is None else mode)
+    pflag = np.zeros(s.n, np.int8)
+    pval = np.zeros(s.n)
+    bdflag = np.zeros(s.n, np.int8)
+    old = numba.get_num_threads()
+    numba.set_num_threads(min(threads, numba.config.NUMBA_NUM_THREADS))
+    try:
+        factorize_levels_kernel(*_sym_args(an), m, an.A.row_ptr, vals, vm.mrow_src,
+                                vm.colpos.astype(np.int64), vm.scale, F, iperm, prior is not None,
+                                eps * anorm, s.level_ptr.astype(np.int64),
+                                s.level_nodes.astype(np.int64), numba.get_num_threads(), pflag, pval,
+                                bdflag)
+    finally:
+        numba.set_num_threads(old)
+    rows = np.flatnonzero(pflag)
+    bd = np.flatnonzero(bdflag)
+    return OracleFactors(F, iperm, list(zip(rows.tolist(), pval[rows].tolist())), anorm,
+                         int(bd[0]) if len(bd) else -1)
 
 
 def substitute(an, fac, b):

@@ -141,6 +141,44 @@ def _apply_mode(an, opts):
                          % (mode.name, an.symbolic.kernel_mode.name))
 
 
+def _device_values(ctx, vals, what="values"):
+    """Matrix values as a contiguous float64 tensor on the context's device (a torch
+    tensor is checked, not converted: its data_ptr goes to the C ABI as is)."""
+    import torch
+    if isinstance(vals, torch.Tensor):
+        if vals.dtype != torch.float64 or vals.device != ctx.device or vals.dim() != 1 \
+                or vals.numel() != ctx.nnz or not vals.is_contiguous():
+            raise errors.DimensionMismatch(
+                "%s must be a contiguous float64 tensor of length %d on %s" % (what, ctx.nnz, ctx.device))
+        return vals
+    v = np.array(vals, np.float64, copy=True)
+    if v.shape != (ctx.nnz,):
+        raise errors.DimensionMismatch("%s must have length %d" % (what, ctx.nnz))
+    return torch.from_numpy(v).to(ctx.device)
+
+
+def _enter_stream(ctx, stream, tensors):
+    """Order a launch on ``stream`` after the current stream (where the buffers were
+    allocated and zeroed) and tell the caching allocator the buffers are in use
+    there.  Returns the current stream if it differs from ``stream``, else None."""
+    import torch
+    if stream is None:
+        return None
+    cur = torch.cuda.current_stream(ctx.device)
+    if stream == cur:
+        return None
+    stream.wait_stream(cur)
+    for t in tensors:
+        t.record_stream(stream)
+    return cur
+
+
+def _leave_stream(cur, stream):
+    """Order the current stream (status reads in _finish) after the launch."""
+    if cur is not None:
+        cur.wait_stream(stream)
+
+
 def _finish(ctx, an, bufs, desc, check_breakdown=True):
     st = bufs["status"].cpu().numpy()
     npert = int(st[0])
@@ -163,13 +201,13 @@ def factorize_analysis(an, values=None, opts=None, stream=None):
     opts = opts or FactorOptions()
     _apply_mode(an, opts)
     ctx = _context(an, opts.device)
-    vals = an.A.values if values is None else values
-    d_vals = vals if isinstance(vals, torch.Tensor) else torch.from_numpy(
-        np.array(vals, np.float64, copy=True)).to(ctx.device)
+    d_vals = _device_values(ctx, an.A.values if values is None else values)
     bufs, desc = ctx.alloc_factors()
     from .device import check
+    cur = _enter_stream(ctx, stream, [d_vals, *bufs.values()])
     check(ctx.lib.hy_factorize(ctx.h, d_vals.data_ptr(), float(opts.perturbation_epsilon),
                                desc, ctx.stream_handle(stream)))
+    _leave_stream(cur, stream)
     return _finish(ctx, an, bufs, desc)
 
 
@@ -191,13 +229,15 @@ def refactorize(A_new, prior, opts=None, stream=None):
     ctx = prior._ctx
     an = ctx.analysis
     if isinstance(A_new, torch.Tensor):
-        d_vals = A_new
+        d_vals = _device_values(ctx, A_new, "refactorization values")
     else:
         _check_pattern(an, A_new)
-        d_vals = torch.from_numpy(np.ascontiguousarray(A_new.values)).to(ctx.device)
+        d_vals = _device_values(ctx, A_new.values)
     bufs, desc = ctx.alloc_factors()
+    cur = _enter_stream(ctx, stream, [d_vals, prior.values, prior.inner_perm, *bufs.values()])
     check(ctx.lib.hy_refactorize(ctx.h, d_vals.data_ptr(), float(opts.perturbation_epsilon),
                                  prior._desc, desc, ctx.stream_handle(stream)))
+    _leave_stream(cur, stream)
     return _finish(ctx, an, bufs, desc)
 
 

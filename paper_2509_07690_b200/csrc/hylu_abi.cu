@@ -72,19 +72,15 @@ __global__ void k_fi_lu(DevSym, CallP, FaninDev, int);
 __global__ void k_fi_panel(DevSym, CallP, FaninDev, int);
 __global__ void k_fi_x(DevSym, CallP, FaninDev, int);
 __global__ void k_fi_upd(DevSym, CallP, FaninDev, int, int, int);
-__global__ void k_fi_upd_mma(DevSym, CallP, FaninDev, int, int, int);
 __global__ void k_fi_upd_pk(DevSym, CallP, FaninDev, int, int, int);
-__global__ void k_fi_upd3(DevSym, CallP, FaninDev, int, int, int);
 __global__ void k_fi_x_w(DevSym, CallP, FaninDev, int, int);
 __global__ void k_fi_upd_w(DevSym, CallP, FaninDev, int, int);
-size_t fi_upd3_smem(int);
 size_t fi_upd_smem(int, int);
 size_t fi_upd_tc_smem(int);
 size_t fi_upd_kc_smem();
 __global__ void k_fi_upd_kc(DevSym, CallP, FaninDev, int);
 __global__ void k_fi_upd_kcp(DevSym, CallP, FaninDev, int);
 __global__ void k_fi_upd_tc(DevSym, CallP, FaninDev, int, int);
-size_t pipe_smem_bytes(bool staged);
 size_t hub_smem_bytes();
 int hub_threads();
 __global__ void k_bhat(DevSym, const int32_t *, const double *, double *);
@@ -109,25 +105,18 @@ struct TaskDesc {
   longlong4 rr0;   // layout shared with hylu_batch.cu
   int32_t dep[4];
 };
-template <bool STAGED>
-__global__ void k_bt_pipe(DevSym, BatchP, DevProg, const TaskDesc *, int64_t, const double *, double *, int *,
-                          int *, int, int, int);
 __global__ void k_bt_pipe2(DevSym, BatchP, DevProg, const TaskDesc *, int64_t, const double *, double *, int *,
-                           int *, int, int, int, int, int);
-__global__ void k_bt_lev0(DevSym, BatchP, DevProg, const int32_t *, int, int, const double *, double *, int *, int);
+                           int *, int, int, int);
 __global__ void k_bt_hub(DevSym, BatchP, DevProg, const int32_t *, int, int, const double *, double *,
-                         double *, int, int *, int, int);
+                         double *, int, int *, int);
 __global__ void k_batch_bhat(DevSym, const int32_t *, const double *, double *, int64_t);
 __global__ void k_batch_fwd(DevSym, const double *, int64_t, const int32_t *, int, int, double *);
-__global__ void k_batch_bwd(DevSym, const double *, int64_t, const int32_t *, int, int, double *);
 __global__ void k_batch_bwd2(DevSym, const double *, int64_t, const int32_t *, int, int, double *);
 __global__ void k_batch_xout2(DevSym, const int32_t *, const double *, double *, int64_t);
 __global__ void k_perm_inverse(int, const int64_t *, int32_t *);
 __global__ void k_row_of(DevSym, const int32_t *, int32_t *);
 __global__ void k_batch_bhat2(DevSym, const int32_t *, const double *, double *, int64_t);
 __global__ void k_batch_extract(const double *, int64_t, int64_t, double *);
-__global__ void k_bt_bwd(DevSym, const double *, int64_t, const int2 *, int64_t, const int64_t *, const int32_t *,
-                         int *, int *, int, int, double *);
 }  // namespace hy
 
 using namespace hy;
@@ -178,19 +167,6 @@ struct hy_handle {
   std::vector<int64_t> h_first, h_colptr, h_valoff, h_dptr, h_nl;
   std::vector<longlong4> h_row_rec;   // batched row programs' row records (task descriptors)
   std::vector<int32_t> h_deps;        // dependency lists (task descriptors inline the first 4)
-  // backward-solve U dependencies + persistent bwd task list (per G)
-  int64_t *d_udp = nullptr;
-  int32_t *d_udeps = nullptr;
-  std::vector<int64_t> h_ulptr;
-  std::vector<int32_t> h_ulnodes;
-  int2 *d_bwd_tasks = nullptr;
-  int64_t bwd_ntasks = 0;
-  int bwd_G = -1;
-  int *d_bwd_flags = nullptr;
-  int64_t bwd_flags_cap = 0;
-  int bwd_persistent = 0;
-  int lev0_split = 0;
-  int epoch_bwd = 0;
   double *d_y = nullptr;          // single-solve workspace [n]
   double *d_bf = nullptr;         // batched factor workspace
   int64_t bf_cap = 0;             // doubles
@@ -213,22 +189,13 @@ struct hy_handle {
   int epoch = 0;
   int32_t *d_node_level = nullptr;
   int pipe_blocks = 0;
-  int gbatch = 1 << 20;                    // unused (kept for hy_set_option compatibility)
-  int staged = 0;                          // stage row sources with cp.async (option "staged")
-  int nowait = 0;                          // timing experiment only: skip dependency waits
-  int pair = 1;                            // pipeline: one warp per (node, group pair)
-  int prefetch = 0;                        // pair mode: L2-prefetch the matrix values this many tasks ahead
   int warp_min = 256;                      // fan-in: below this many small items per level, CTA kernels only
-  int bwd_pair = 1;                        // backward solve: one warp per (node, group pair)
-  int hub_df = 0;                          // hub kernel: dataflow phase for split-free leading levels
   int pipe_ws = 16;                        // pair-mode shared workspace columns per group
-  int skew = 1;                            // diagonal claim order: group g+1 runs `skew` levels behind g
   // diagonal claim order per (segment, G): pair prefix sums, (level<<16|group), level offsets
   struct Seg {
     int l0, l1;
     TaskDesc *d_tasks = nullptr;   // task descriptors in diagonal claim order
     int64_t ntasks = 0;
-    bool lev0 = false;             // level 0 of this segment runs in k_bt_lev0
   };
   std::vector<Seg> segs;
   int segs_G = -1;
@@ -263,14 +230,13 @@ struct hy_handle {
   int32_t *d_rowof = nullptr;  // factor row of each original row (batched b̂ in source order)
   int64_t *d_arow = nullptr;   // A's pattern in original coordinates (refinement)
   int32_t *d_acol = nullptr;
-  int fi_v3 = 0;                                     // option "fanin_v3" (slower; kept for experiments)
-  int fi_mma = 0;                                    // option "fanin_dmma" (bitwise-equal results; slower here)
   int fi_maps = 1;                                   // option "fanin_maps": use host-precomputed source maps in k_fi_upd_kc
   int fi_overlap = 1;                                // option "fanin_overlap": panel TRSM on a side stream, concurrent with the X blocks
   cudaStream_t fi_side = nullptr;
   cudaEvent_t fi_ev_lu = nullptr, fi_ev_pt = nullptr;
   int fi_tc = 5;                                     // option "fanin_tc": DMMA update kernels (1/2: per-source k_fi_upd_tc for targets >= 32 rows / all regular items; 3/4: K-concatenated k_fi_upd_kc, same split; 5 (default): k_fi_upd_kcp for the packed items too)
   std::vector<int32_t> fi_smax, fi_mmax;
+  int64_t fi_nsrc = -1;                              // source records of the uploaded plan
   int sm_count = 148;
   // single-instance hub rows (ROWROW path): programs + per-level hub node lists
   bool hub1_ok = false;
@@ -372,8 +338,7 @@ static int build_segments(hy_handle *h, int G) {
     hy_handle::Seg sg;
     sg.l0 = l;
     sg.l1 = l1;
-    sg.lev0 = (l == 0 && h->lev0_split && h->bl_hptr[1] == h->bl_hptr[0]);
-    const int lb = sg.lev0 ? 1 : 0;   // level 0 runs in k_bt_lev0
+    const int lb = 0;
     const int L = l1 - l;
     std::vector<TaskDesc> tasks;
     tasks.reserve((size_t)(h->bl_rptr[l1] - h->bl_rptr[l]) * G);
@@ -393,8 +358,8 @@ static int build_segments(hy_handle *h, int G) {
         t.dep[k] = t.d0 + k < t.d1 ? h->h_deps[t.d0 + k] : -1;
       return t;
     };
-    const int sk = h->skew;
-    const int gs = h->pair ? 2 : 1;           // pair mode: tasks carry the even group of a pair
+    const int sk = 1;
+    const int gs = 2;                         // pair mode: tasks carry the even group of a pair
     const int GT = (G + gs - 1) / gs;
     for (int d = 0; d < sk * (GT - 1) + L; ++d)
       for (int k = lb; k < L && k <= d; ++k) {
@@ -483,14 +448,6 @@ int hy_create(int device, hy_handle **out) {
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_bt_hub, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hub_smem_bytes());
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_bt_lev0, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)pipe_smem_bytes(false));
-  e = cudaFuncSetAttribute(k_bt_pipe<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)pipe_smem_bytes(true));
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_bt_pipe<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)pipe_smem_bytes(false));
-  if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_bt_pipe2, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 2 * 64 * 32 * 8);
   if (e != cudaSuccess) {
     delete h;
@@ -515,8 +472,6 @@ void hy_destroy(hy_handle *h) {
   if (h->fi_side) cudaStreamDestroy(h->fi_side);
   if (h->fi_ev_lu) cudaEventDestroy(h->fi_ev_lu);
   if (h->fi_ev_pt) cudaEventDestroy(h->fi_ev_pt);
-  if (h->d_bwd_flags) cudaFree(h->d_bwd_flags);
-  if (h->d_bwd_tasks) cudaFree(h->d_bwd_tasks);
   free_segments(h);
   if (h->d_counters) cudaFree(h->d_counters);
   if (h->d_by) cudaFree(h->d_by);
@@ -532,23 +487,6 @@ int64_t hy_launch_count(const hy_handle *h) { return h ? h->launches : -1; }
 
 int hy_set_option(hy_handle *h, const char *name, int64_t value) {
   if (!h || !name) return fail(HY_INVALID_ARGUMENT, "null handle/name");
-  if (std::string(name) == "group_batch" && value >= 1) {
-    h->gbatch = (int)value;
-    return HY_OK;
-  }
-  if (std::string(name) == "lev0_split") {
-    h->lev0_split = value != 0;
-    free_segments(h);
-    return HY_OK;
-  }
-  if (std::string(name) == "bwd_persistent") {
-    h->bwd_persistent = value != 0;
-    return HY_OK;
-  }
-  if (std::string(name) == "fanin_v3") {
-    h->fi_v3 = value != 0;
-    return HY_OK;
-  }
   if (std::string(name) == "fanin_maps") {
     h->fi_maps = value != 0;
     return HY_OK;
@@ -561,39 +499,8 @@ int hy_set_option(hy_handle *h, const char *name, int64_t value) {
     h->fi_tc = (int)value;
     return HY_OK;
   }
-  if (std::string(name) == "fanin_dmma") {
-    h->fi_mma = value != 0;
-    return HY_OK;
-  }
-  if (std::string(name) == "diagonal_skew" && value >= 1) {
-    h->skew = (int)value;
-    free_segments(h);
-    return HY_OK;
-  }
-  if (std::string(name) == "nowait_experiment") {
-    h->nowait = (int)value;   // bitmask: 1 no waits, 2 no steps, 4 no scatter, 8 no copy-out
-    return HY_OK;
-  }
-  if (std::string(name) == "pair_groups") {
-    h->pair = value != 0;
-    free_segments(h);
-    h->pipe_blocks = 0;
-    return HY_OK;
-  }
   if (std::string(name) == "fanin_warp_min" && value >= 1) {
     h->warp_min = (int)value;
-    return HY_OK;
-  }
-  if (std::string(name) == "bwd_pair") {
-    h->bwd_pair = value != 0;
-    return HY_OK;
-  }
-  if (std::string(name) == "hub_dataflow") {
-    h->hub_df = value != 0;
-    return HY_OK;
-  }
-  if (std::string(name) == "prefetch" && value >= 0) {
-    h->prefetch = (int)value;
     return HY_OK;
   }
   if (std::string(name) == "pipe_blocks" && value >= 0) {   // 0: occupancy-derived (default)
@@ -602,11 +509,6 @@ int hy_set_option(hy_handle *h, const char *name, int64_t value) {
   }
   if (std::string(name) == "pipe_ws" && value >= 1 && value <= 64) {
     h->pipe_ws = (int)value;
-    h->pipe_blocks = 0;
-    return HY_OK;
-  }
-  if (std::string(name) == "staged") {
-    h->staged = value != 0;
     h->pipe_blocks = 0;
     return HY_OK;
   }
@@ -717,27 +619,6 @@ int hy_upload_symbolic(hy_handle *h, const hy_symbolic_desc *d) {
     UP(&h->d_solve_scratch, (const double *)nullptr, (ns > 0 ? ns : 1) * 64);
   }
   {
-    // U dependencies of each node: owners of its columns right of its block
-    std::vector<int64_t> udp(nn + 1, 0);
-    std::vector<int32_t> ud;
-    for (int64_t u = 0; u < nn; ++u) {
-      const int64_t s = d->node_first[u + 1] - d->node_first[u];
-      int32_t last = -1;
-      for (int64_t q = d->colptr[u] + d->nl[u] + s; q < d->colptr[u + 1]; ++q) {
-        const int32_t v = node_of[d->cols[q]];
-        if (v != last) {
-          ud.push_back(v);
-          last = v;
-        }
-      }
-      udp[u + 1] = (int64_t)ud.size();
-    }
-    UP(&h->d_udp, udp.data(), nn + 1);
-    UP(&h->d_udeps, ud.data(), ud.size());
-    h->h_ulptr.assign(d->ulevel_ptr, d->ulevel_ptr + d->nulevels + 1);
-    h->h_ulnodes.assign(d->ulevel_nodes, d->ulevel_nodes + d->ulevel_ptr[d->nulevels]);
-  }
-  {
     std::vector<int32_t> lev(nn, 0);
     for (int64_t l = 0; l < d->nlevels; ++l)
       for (int64_t k = d->level_ptr[l]; k < d->level_ptr[l + 1]; ++k) lev[d->level_nodes[k]] = (int32_t)l;
@@ -829,6 +710,7 @@ int hy_upload_fanin_plan(hy_handle *h, const hy_fanin_plan *d) {
   UPF(&p32, d->up_c1, d->lev_up[nl]); D.up_c1 = p32;
   UPF(&p64, d->up_ptr, d->lev_up[nl] + 1); D.up_ptr = p64;
   UPF(&p32, d->src_k, d->nsrc); D.src_k = p32;
+  h->fi_nsrc = d->nsrc;
   UPF(&p32, d->src_q0, d->nsrc); D.src_q0 = p32;
   UPF(&p32, d->src_q1, d->nsrc); D.src_q1 = p32;
   UPF(&p32, d->dep_pb, d->ndeps); D.dep_pb = p32;
@@ -878,12 +760,10 @@ int hy_upload_fanin_plan(hy_handle *h, const hy_fanin_plan *d) {
     if (b > mx) mx = b;
   }
   CK(cudaFuncSetAttribute(k_fi_upd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx));
-  CK(cudaFuncSetAttribute(k_fi_upd_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx));
   CK(cudaFuncSetAttribute(k_fi_upd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fi_upd_tc_smem(64)));
   CK(cudaFuncSetAttribute(k_fi_upd_kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fi_upd_kc_smem()));
   CK(cudaFuncSetAttribute(k_fi_upd_kcp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fi_upd_kc_smem()));
   CK(cudaFuncSetAttribute(k_fi_upd_pk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx));
-  CK(cudaFuncSetAttribute(k_fi_upd3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fi_upd3_smem(64)));
   CK(cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, h->device));
   CK(cudaFuncSetAttribute(k_fi_panel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)(64 * 256 * sizeof(double))));
@@ -973,7 +853,7 @@ static int run_fanin(hy_handle *h, const CallP &P, cudaStream_t st) {
     if (nup) {
       const size_t sm = fi_upd_smem(h->fi_smax[l], h->fi_mmax[l]);
       const int reg = (int)h->fi_upreg[l];
-      const int split = (h->fi_mma || h->fi_tc == 1 || h->fi_tc == 3) ? (int)h->fi_upbig[l] : (int)h->fi_up[l + 1];
+      const int split = (h->fi_tc == 1 || h->fi_tc == 3) ? (int)h->fi_upbig[l] : (int)h->fi_up[l + 1];
       const int npk = reg - (int)h->fi_up[l];
       const int nbig = (int)h->fi_up[l + 1] - split;
       const int rs = (int)h->fi_uprs[l] - reg < h->warp_min ? reg : (int)h->fi_uprs[l];
@@ -1009,11 +889,7 @@ static int run_fanin(hy_handle *h, const CallP &P, cudaStream_t st) {
         h->launches++;
       } else if (split > rs) {
         const int nsm2 = split - rs;
-        if (h->fi_v3)
-          k_fi_upd3<<<nsm2, 256, fi_upd3_smem(h->fi_smax[l]), st>>>(h->S, P, h->fi, rs, h->fi_smax[l],
-                                                                    h->fi_mmax[l]);
-        else
-          k_fi_upd<<<nsm2, 256, sm, st>>>(h->S, P, h->fi, rs, h->fi_smax[l], h->fi_mmax[l]);
+        k_fi_upd<<<nsm2, 256, sm, st>>>(h->S, P, h->fi, rs, h->fi_smax[l], h->fi_mmax[l]);
         h->launches++;
       }
       if (nbig && h->fi_tc == 3) {
@@ -1021,9 +897,6 @@ static int run_fanin(hy_handle *h, const CallP &P, cudaStream_t st) {
         h->launches++;
       } else if (nbig && h->fi_tc == 1) {
         k_fi_upd_tc<<<nbig, 256, fi_upd_tc_smem(h->fi_smax[l]), st>>>(h->S, P, h->fi, split, h->fi_smax[l]);
-        h->launches++;
-      } else if (nbig) {
-        k_fi_upd_mma<<<nbig, 256, sm, st>>>(h->S, P, h->fi, split, h->fi_smax[l], h->fi_mmax[l]);
         h->launches++;
       }
       if (sideB) {
@@ -1042,6 +915,12 @@ int hy_upload_fanin_maps(hy_handle *h, int64_t nsrc, int64_t npos, const int64_t
   if (!h || !h->uploaded || !h->fanin_ok) return fail(HY_INVALID_ARGUMENT, "fan-in plan not uploaded");
   if (nsrc < 0 || npos < 0 || (nsrc && (!poff || !vb || !vW || !qb || !m)) || (npos && !pos))
     return fail(HY_INVALID_ARGUMENT, "null source-map arrays");
+  // the maps index the uploaded plan's source records one to one, and poff[nsrc]
+  // bounds every position the update kernels read
+  if (nsrc != h->fi_nsrc)
+    return fail(HY_INVALID_ARGUMENT, "source-map count differs from the uploaded fan-in plan");
+  if (nsrc && (poff[0] != 0 || poff[nsrc] != npos))
+    return fail(HY_INVALID_ARGUMENT, "source-map offsets do not span the position array");
   CK(cudaSetDevice(h->device));
   FaninDev &D = h->fi;
   int64_t *p64;
@@ -1428,14 +1307,8 @@ int hy_refactorize_batched(hy_handle *h, int64_t B, const double *d_vals, double
   h->epoch++;
   if (h->pipe_blocks == 0) {
     int per_sm = 0, sms = 0;
-    if (h->pair)
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bt_pipe2, 128,
-                                                       (size_t)4 * 2 * h->pipe_ws * 32 * 8));
-    else if (h->staged)
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bt_pipe<true>, 128, pipe_smem_bytes(true)));
-    else
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bt_pipe<false>, 128,
-                                                       pipe_smem_bytes(false)));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bt_pipe2, 128,
+                                                     (size_t)4 * 2 * h->pipe_ws * 32 * 8));
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
     h->pipe_blocks = per_sm * sms;
   }
@@ -1460,29 +1333,14 @@ int hy_refactorize_batched(hy_handle *h, int64_t B, const double *d_vals, double
       }
       k_bt_hub<<<(unsigned)(nh * G), hub_threads(), hub_smem_bytes(), st>>>(h->S, P, h->prog, h->d_bl_hubs + h->bl_hptr[l], nh, G,
                                                    d_b_fuse, h->d_by, h->d_scratch, h->max_slots,
-                                                   h->d_flags, h->epoch, h->hub_df);
-      h->launches++;
-    }
-    if (sg.lev0) {
-      const int n0 = (int)(h->bl_rptr[1] - h->bl_rptr[0]);
-      const int64_t tasks0 = (int64_t)n0 * G;
-      const int grid0 = (int)((tasks0 + 3) / 4 < (int64_t)h->sm_count * 24 ? (tasks0 + 3) / 4 : h->sm_count * 24);
-      k_bt_lev0<<<grid0, 128, pipe_smem_bytes(false), st>>>(h->S, P, h->prog, h->d_bl_rows, n0, G, d_b_fuse,
-                                                            h->d_by, h->d_flags, h->epoch);
+                                                   h->d_flags, h->epoch);
       h->launches++;
     }
     if (sg.ntasks) {
       int *ctr = (int *)((long long *)h->d_counters + si);
-      if (h->pair)
-        k_bt_pipe2<<<h->pipe_blocks, 128, (size_t)4 * 2 * h->pipe_ws * 32 * 8, st>>>(
-            h->S, P, h->prog, sg.d_tasks, sg.ntasks, d_b_fuse, h->d_by, ctr, h->d_flags, h->epoch, G,
-            h->pipe_ws, h->nowait, h->prefetch);
-      else if (h->staged)
-        k_bt_pipe<true><<<h->pipe_blocks, 128, pipe_smem_bytes(true), st>>>(
-            h->S, P, h->prog, sg.d_tasks, sg.ntasks, d_b_fuse, h->d_by, ctr, h->d_flags, h->epoch, G, h->nowait);
-      else
-        k_bt_pipe<false><<<h->pipe_blocks, 128, pipe_smem_bytes(false), st>>>(
-            h->S, P, h->prog, sg.d_tasks, sg.ntasks, d_b_fuse, h->d_by, ctr, h->d_flags, h->epoch, G, h->nowait);
+      k_bt_pipe2<<<h->pipe_blocks, 128, (size_t)4 * 2 * h->pipe_ws * 32 * 8, st>>>(
+          h->S, P, h->prog, sg.d_tasks, sg.ntasks, d_b_fuse, h->d_by, ctr, h->d_flags, h->epoch, G,
+          h->pipe_ws);
       h->launches++;
     }
   }
@@ -1513,50 +1371,13 @@ int hy_solve_batched(hy_handle *h, int64_t B, const double *d_b, double *d_x, ui
   }
   }
   const Plan &bp = h->bplan;
-  if (h->bwd_persistent) {
-    if (h->bwd_G != G) {
-      std::vector<int2> tl;
-      const int L = (int)h->h_ulptr.size() - 1;
-      for (int d = 0; d < G + L - 1; ++d)
-        for (int k = (d - G + 1 > 0 ? d - G + 1 : 0); k <= (d < L - 1 ? d : L - 1); ++k)
-          for (int64_t q = h->h_ulptr[k]; q < h->h_ulptr[k + 1]; ++q) tl.push_back(make_int2(h->h_ulnodes[q], d - k));
-      if (h->d_bwd_tasks) CK(cudaFree(h->d_bwd_tasks));
-      h->d_bwd_tasks = nullptr;
-      h->bwd_ntasks = (int64_t)tl.size();
-      CK(cudaMalloc((void **)&h->d_bwd_tasks, sizeof(int2) * (tl.size() + 1)));
-      CK(cudaMemcpy(h->d_bwd_tasks, tl.data(), sizeof(int2) * tl.size(), cudaMemcpyHostToDevice));
-      h->bwd_G = G;
-    }
-    const int64_t nf = (int64_t)h->S.nn * G;
-    if (nf > h->bwd_flags_cap) {
-      if (h->d_bwd_flags) CK(cudaFree(h->d_bwd_flags));
-      CK(cudaMalloc((void **)&h->d_bwd_flags, sizeof(int) * nf));
-      CK(cudaMemset(h->d_bwd_flags, 0, sizeof(int) * nf));
-      h->bwd_flags_cap = nf;
-      h->epoch_bwd = 0;
-    }
-    h->epoch_bwd++;
-    int *ctr = (int *)((long long *)h->d_counters + h->counters_cap - 1);
-    CK(cudaMemsetAsync(ctr, 0, sizeof(long long), st));
-    k_bt_bwd<<<h->sm_count * 12, 128, 0, st>>>(h->S, h->d_bf, h->stored, h->d_bwd_tasks, h->bwd_ntasks,
-                                              h->d_udp, h->d_udeps, ctr, h->d_bwd_flags, h->epoch_bwd, G,
-                                              h->d_by);
+  for (int l = 0; l < bp.nlev; ++l) {
+    const int c = (int)(bp.aptr[l + 1] - bp.aptr[l]);
+    const int GP = (G + 1) / 2;
+    const int64_t tasks = (int64_t)c * GP;
+    k_batch_bwd2<<<(unsigned)((tasks + 3) / 4), 128, 0, st>>>(h->S, h->d_bf, h->stored,
+                                                            bp.d_all + bp.aptr[l], c, GP, h->d_by);
     h->launches++;
-  } else {
-    for (int l = 0; l < bp.nlev; ++l) {
-      const int c = (int)(bp.aptr[l + 1] - bp.aptr[l]);
-      if (h->bwd_pair) {
-        const int GP = (G + 1) / 2;
-        const int64_t tasks = (int64_t)c * GP;
-        k_batch_bwd2<<<(unsigned)((tasks + 3) / 4), 128, 0, st>>>(h->S, h->d_bf, h->stored,
-                                                                bp.d_all + bp.aptr[l], c, GP, h->d_by);
-      } else {
-        const int64_t tasks = (int64_t)c * G;
-        k_batch_bwd<<<(unsigned)((tasks + 3) / 4), 128, 0, st>>>(h->S, h->d_bf, h->stored,
-                                                               bp.d_all + bp.aptr[l], c, G, h->d_by);
-      }
-      h->launches++;
-    }
   }
   if (!h->d_pinv) {
     CK(cudaMalloc((void **)&h->d_pinv, sizeof(int32_t) * h->S.n));

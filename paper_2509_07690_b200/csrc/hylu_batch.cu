@@ -35,61 +35,6 @@ constexpr int HUB_CAPP = 4096;   // staged predecessor records per level (per bu
 constexpr size_t HUB_BUF = (size_t)HUB_CAPP * (8 + 4) + (size_t)HUB_CAPI * (8 * 3 + 4 * 2);
 size_t hub_smem_bytes() { return 2 * HUB_BUF; }
 
-// Apply the row-program steps [s0, s1) to the accumulator w (lane-offset pointer,
-// stride 32), software-pipelined: the next step's scalars, its U(j,j) and y_j are
-// loaded while the current step runs.  Returns the fused forward-substitution
-// accumulator.  Target positions inside one step are distinct (a source row's
-// columns are distinct), so each group of 8 updates loads all targets first.
-template <typename WPtr>
-__device__ __forceinline__ double run_steps(const DevProg &R, int64_t s0, int64_t s1, WPtr w,
-                                            const double *gb, const double *yb, double yacc) {
-  if (s0 >= s1) return yacc;
-  int p = R.st_p[s0];
-  int64_t src = R.st_src[s0];
-  int cnt = R.st_cnt[s0];
-  int64_t ro = R.st_rel[s0];
-  double d = gb[src * 32];
-  double yj = yb[(int64_t)R.st_j[s0] * 32];
-  for (int64_t st = s0; st < s1; ++st) {
-    int pn = 0, cn = 0;
-    int64_t sn = 0, rn = 0;
-    double dn = 1.0, yn = 0.0;
-    if (st + 1 < s1) {
-      pn = R.st_p[st + 1];
-      sn = R.st_src[st + 1];
-      cn = R.st_cnt[st + 1];
-      rn = R.st_rel[st + 1];
-      dn = gb[sn * 32];
-      yn = yb[(int64_t)R.st_j[st + 1] * 32];
-    }
-    const int32_t *rl = R.rel + ro;
-    const double *us = gb + (src + 1) * 32;
-    const double l = w[p * 32] / d;
-    w[p * 32] = l;
-    yacc -= l * yj;
-    // predicated 8-wide groups: every index and source load of the group is issued
-    // before its first shared-memory store (no scalar tail loop whose loads would
-    // each wait behind the previous store)
-    for (int q = 0; q < cnt; q += 8) {
-      int t[8];
-      double u[8], a[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const bool ok = q + k < cnt;
-        t[k] = ok ? __ldg(rl + q + k) : 0;
-        u[k] = ok ? us[(q + k) * 32] : 0.0;
-      }
-#pragma unroll
-      for (int k = 0; k < 8; ++k) a[k] = w[t[k] * 32];
-#pragma unroll
-      for (int k = 0; k < 8; ++k)
-        if (q + k < cnt) w[t[k] * 32] = a[k] - l * u[k];
-    }
-    p = pn; src = sn; cnt = cn; ro = rn; d = dn; yj = yn;
-  }
-  return yacc;
-}
-
 // ---------------------------------------------------------------------------
 // Dependency flags: flag[node * G + g] == epoch once (node, group) is complete.
 __device__ __forceinline__ int ld_acquire(const int *p) {
@@ -110,8 +55,6 @@ __device__ __forceinline__ void st_release(int *p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-constexpr int STAGE = 40;   // staged source values per warp (x32 lanes)
-
 __device__ __forceinline__ void cp_async8(double *smem_dst, const double *gsrc) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gsrc) : "memory");
@@ -127,156 +70,7 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
 }
 
-// Run the steps [s0, s1) of one row, staging each chunk of steps' source data
-// (U(j,j), y_j, U(j,>j)) in shared memory with cp.async first, so a chunk costs
-// one memory round trip instead of one per step.  Step metadata for up to 32
-// steps is loaded lane-parallel and broadcast with shuffles.
-template <typename WPtr>
-__device__ __forceinline__ double run_staged(const DevProg &R, int64_t s0, int64_t s1, WPtr w,
-                                             const double *gb, const double *yb, double yacc,
-                                             double *stage, int32_t *relbuf, int lane) {
-  int64_t st = s0;
-  while (st < s1) {
-    const bool have = st + lane < s1;
-    int mp = 0, mc = 0, mj = 0;
-    int64_t msrc = 0, mrel = 0;
-    if (have) {
-      mp = R.st_p[st + lane];
-      mc = R.st_cnt[st + lane];
-      msrc = R.st_src[st + lane];
-      mrel = R.st_rel[st + lane];
-      mj = R.st_j[st + lane];
-    }
-    const int sz = have ? mc + 2 : 0;
-    int incl = sz;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(HY_FULL, incl, o);
-      if (lane >= o) incl += v;
-    }
-    const unsigned fit = __ballot_sync(HY_FULL, have && incl <= STAGE);
-    const int nin = __popc(fit);  // fit is a prefix mask (incl is monotone)
-    if (nin == 0) {
-      // a single step larger than the stage: direct loads
-      const int p0 = __shfl_sync(HY_FULL, mp, 0), c0 = __shfl_sync(HY_FULL, mc, 0);
-      const int64_t src0 = __shfl_sync(HY_FULL, msrc, 0), rel0 = __shfl_sync(HY_FULL, mrel, 0);
-      const int j0 = __shfl_sync(HY_FULL, mj, 0);
-      const double dd = gb[src0 * 32];
-      const double lv = w[p0 * 32] / dd;
-      w[p0 * 32] = lv;
-      yacc -= lv * yb[(int64_t)j0 * 32];
-      const double *us = gb + (src0 + 1) * 32;
-      for (int q = 0; q < c0; ++q) w[R.rel[rel0 + q] * 32] -= lv * us[q * 32];
-      st += 1;
-      continue;
-    }
-    // issue the chunk's copies (each lane copies its own instance)
-    for (int k = 0; k < nin; ++k) {
-      const int ck = __shfl_sync(HY_FULL, mc, k);
-      const int64_t sk = __shfl_sync(HY_FULL, msrc, k);
-      const int64_t rk = __shfl_sync(HY_FULL, mrel, k);
-      const int jk = __shfl_sync(HY_FULL, mj, k);
-      const int ok = __shfl_sync(HY_FULL, incl, k) - ck - 2;
-      cp_async8(stage + ok * 32 + lane, gb + sk * 32);
-      cp_async8(stage + (ok + 1) * 32 + lane, yb + (int64_t)jk * 32);
-      const double *us = gb + (sk + 1) * 32;
-      for (int q = 0; q < ck; ++q) cp_async8(stage + (ok + 2 + q) * 32 + lane, us + q * 32);
-      for (int q = lane; q < ck; q += 32) relbuf[ok + 2 + q] = R.rel[rk + q];
-    }
-    cp_async_wait_all();
-    __syncwarp();
-    for (int k = 0; k < nin; ++k) {
-      const int pk = __shfl_sync(HY_FULL, mp, k);
-      const int ck = __shfl_sync(HY_FULL, mc, k);
-      const int ok = __shfl_sync(HY_FULL, incl, k) - ck - 2;
-      const double d = stage[ok * 32 + lane];
-      const double yj = stage[(ok + 1) * 32 + lane];
-      const double l = w[pk * 32] / d;
-      w[pk * 32] = l;
-      yacc -= l * yj;
-      const double *uv = stage + (ok + 2) * 32 + lane;
-      const int32_t *rl = relbuf + ok + 2;
-      for (int q = 0; q < ck; ++q) w[rl[q] * 32] -= l * uv[q * 32];
-    }
-    __syncwarp();
-    st += nin;
-  }
-  return yacc;
-}
-
-// One (node, group) task: up-looking rows in order, lane = instance.  All
-// per-node / per-row metadata comes from packed records (one load each).
-template <bool STAGED>
-__device__ __forceinline__ void bt_node(const DevSym &S, const BatchP &P, const DevProg &R, int u,
-                                        const longlong4 nr, int g, const double *rhs, double *Y,
-                                        double *wsm0, int ws, double *stage, int32_t *relbuf,
-                                        int lane, int xmask) {
-  const int64_t b = (int64_t)g * 32 + lane;
-  const bool live = b < P.B;
-  const int nlive = (int)(P.B - (int64_t)g * 32 < 32 ? P.B - (int64_t)g * 32 : 32);
-  const double thr = P.eps * P.anorm[0];
-  const int64_t vbase = nr.x;
-  const int r = (int)(nr.z & 0xffffffff);
-  const int s = (int)(nr.z >> 32);
-  const int W = (int)(nr.w & 0xffffffff);
-  const int L = (int)(nr.w >> 32);
-  double *gb0 = P.BF + (int64_t)g * P.stored * 32;  // group base (no lane offset)
-  const double *gb = gb0 + lane;
-  double *yb = Y + (int64_t)g * S.n * 32 + lane;
-  const double *Ab = P.A + (int64_t)g * 32 * S.nnz;
-  longlong4 rr = R.row_rec[r];
-  for (int t = 0; t < s; ++t) {
-    const int i = r + t;
-    const int64_t s0 = rr.x, e0 = rr.y;
-    const int64_t s1 = s0 + (rr.z & 0xffffffff);
-    const int k = (int)(rr.z >> 32);
-    const int64_t a = rr.w;
-    if (t + 1 < s) rr = R.row_rec[i + 1];
-    const bool inSm = (s1 > s0) && W <= ws;
-    double *grow = gb0 + (vbase + (int64_t)t * W) * 32;
-    double *w0 = inSm ? wsm0 : grow;
-    double yacc = P.ypre ? yb[(int64_t)i * 32] : (live && rhs) ? S.dr[a] * rhs[b * S.n + a] : 0.0;
-    for (int q = 0; q < W; ++q) w0[q * 32 + lane] = 0.0;
-    __syncwarp();
-    // scatter: lanes over (instance, entry) pairs, instance-major, so a pass reads
-    // the k contiguous entries of consecutive instances (few sectors per instance)
-    if (!(xmask & 4))
-      for (int idx = lane; idx < nlive * k; idx += 32) {
-        const int inst = idx / k, e = idx - inst * k;
-        w0[S.colpos[e0 + e] * 32 + inst] = Ab[(int64_t)inst * S.nnz + e0 + e] * S.scale[e0 + e];
-      }
-    __syncwarp();
-    if (xmask & 2) {
-    } else if (STAGED) {
-      if (inSm)
-        yacc = run_staged(R, s0, s1, wsm0 + lane, gb, yb, yacc, stage, relbuf, lane);
-      else
-        yacc = run_staged(R, s0, s1, grow + lane, gb, yb, yacc, stage, relbuf, lane);
-    } else {
-      if (inSm)
-        yacc = run_steps(R, s0, s1, wsm0 + lane, gb, yb, yacc);
-      else
-        yacc = run_steps(R, s0, s1, grow + lane, gb, yb, yacc);
-    }
-    const int Lt = L + t;
-    const double piv = w0[Lt * 32 + lane];
-    bool fired;
-    w0[Lt * 32 + lane] = perturb(piv, thr, fired);
-    if (fired && live) atomicAdd(&P.npert[b], 1);
-    yb[(int64_t)i * 32] = yacc;
-    if (inSm && !(xmask & 8))
-      for (int q = 0; q < W; ++q) grow[q * 32 + lane] = w0[q * 32 + lane];
-    __syncwarp();
-  }
-}
-
 constexpr int PIPE_WARPS = 4;
-constexpr int PIPE_WS = 32;
-size_t pipe_smem_bytes(bool staged) {
-  const int st = staged ? STAGE : 0;
-  return (size_t)PIPE_WARPS * ((PIPE_WS + st) * 32 * sizeof(double) + st * sizeof(int32_t));
-}
-
 // Persistent, dependency-driven row kernel for a segment of levels without hub
 // nodes (the device form of SPEC's pipeline mode): warps claim
 // (node, group) tasks in level-major order from an atomic counter, wait on the
@@ -294,59 +88,6 @@ struct TaskDesc {
   int32_t dep[4];  // the first (up to) 4 dependencies, inline (no dependent index load)
 };
 
-template <bool STAGED>
-__global__ void __launch_bounds__(PIPE_WARPS * 32, STAGED ? 3 : 6)
-    k_bt_pipe(DevSym S, BatchP P, DevProg R, const TaskDesc *tasks, int64_t total, const double *rhs,
-              double *Y, int *counter, int *flags, int epoch, int G, int nowait) {
-  extern __shared__ __align__(16) double pipe_smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int SG = STAGED ? STAGE : 0;
-  double *wsm_w = pipe_smem + (size_t)warp * (PIPE_WS + SG) * 32;
-  double *stg_w = wsm_w + PIPE_WS * 32;
-  int32_t *rlb_w = reinterpret_cast<int32_t *>(pipe_smem + (size_t)PIPE_WARPS * (PIPE_WS + SG) * 32) +
-                   warp * SG;
-  for (;;) {
-    long long t = 0;
-    if (lane == 0) t = (long long)atomicAdd(reinterpret_cast<unsigned long long *>(counter), 1ull);
-    t = __shfl_sync(HY_FULL, t, 0);
-    if (t >= total) return;
-    const TaskDesc cur = tasks[t];
-    // lanes poll the dependency flags in parallel (acquire); the warp barrier then
-    // orders every lane's subsequent loads after the producers' releases
-    for (int64_t k = cur.d0 + lane; k < cur.d1 && !(nowait & 1); k += 32) {
-      const int *f = flags + (int64_t)S.deps[k] * G + cur.g;
-      while (ld_acquire(f) != epoch) __nanosleep(64);
-    }
-    __syncwarp();
-    const longlong4 nr = make_longlong4(cur.valoff, cur.d0, (int64_t)cur.r | ((int64_t)cur.s << 32),
-                                        (int64_t)cur.W | ((int64_t)cur.L << 32));
-    bt_node<STAGED>(S, P, R, cur.u, nr, cur.g, rhs, Y, wsm_w, PIPE_WS, stg_w, rlb_w, lane, nowait);
-    __threadfence();
-    __syncwarp();
-    if (lane == 0) st_release(flags + (int64_t)cur.u * G + cur.g, epoch);
-  }
-}
-
-// Level 0 of the batched factorization: no dependencies, so no claims, polls or
-// fences — one warp per (node, group); completion flags are plain stores (the
-// pipeline kernel that reads them is launched after this one on the same stream).
-__global__ void __launch_bounds__(PIPE_WARPS * 32, 6)
-    k_bt_lev0(DevSym S, BatchP P, DevProg R, const int32_t *nodes, int count, int G, const double *rhs,
-              double *Y, int *flags, int epoch) {
-  extern __shared__ __align__(16) double pipe_smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double *wsm_w = pipe_smem + (size_t)warp * PIPE_WS * 32;
-  const int64_t total = (int64_t)count * G;
-  for (int64_t t = (int64_t)blockIdx.x * PIPE_WARPS + warp; t < total;
-       t += (int64_t)gridDim.x * PIPE_WARPS) {
-    const int u = nodes[t / G];
-    const int g = (int)(t % G);
-    const longlong4 nr = R.node_rec[u];
-    bt_node<false>(S, P, R, u, nr, g, rhs, Y, wsm_w, PIPE_WS, nullptr, nullptr, lane, 0);
-    if (lane == 0) flags[(int64_t)u * G + g] = epoch;
-  }
-}
-
 // ---------------------------------------------------------------------------
 // Pair mode: one warp runs the same node for two adjacent groups (g, g+1), lane =
 // instance g*32+lane and (g+1)*32+lane.  Every metadata load (task record, row
@@ -358,24 +99,6 @@ __global__ void __launch_bounds__(PIPE_WARPS * 32, 6)
 #define P2W_DEF 4
 #endif
 constexpr int P2W = P2W_DEF;   // update entries per batch in run_steps2 (all loads issued first)
-#ifndef PFD_DEF
-#define PFD_DEF 0
-#endif
-constexpr int PFD = PFD_DEF;   // L2 prefetch distance (steps) of the source rows' U lines (0: off)
-
-// Lane q < cnt of step st requests line q of the step's source row U(j,>j) of both
-// groups into L2 (the lines of one source row are contiguous: one 256-byte line per
-// position).  Issued only after the task's dependency polls, so the values are final.
-__device__ __forceinline__ void pf_step(const DevProg &R, int64_t st, const double *ga, const double *gc) {
-  const int64_t src = __ldg(R.st_src + st);
-  const int cnt = __ldg(R.st_cnt + st);
-  const int lane = threadIdx.x & 31;
-  for (int q = lane; q < cnt; q += 32) {
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(ga + (src + 1 + q) * 32));
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(gc + (src + 1 + q) * 32));
-  }
-}
-
 template <typename WPtr>
 __device__ __forceinline__ void run_steps2(const DevProg &R, int64_t s0, int64_t s1, WPtr wa,
                                            WPtr wc, const double *ga, const double *gc,
@@ -389,14 +112,7 @@ __device__ __forceinline__ void run_steps2(const DevProg &R, int64_t s0, int64_t
   int64_t j = __ldg(R.st_j + s0);
   double da = __ldcg(ga + src * 32), dc = __ldcg(gc + src * 32);
   double yja = __ldcg(ya + j * 32), yjc = __ldcg(yc + j * 32);
-  if (PFD > 0) {
-    // lane-0-relative group bases (wa/ga are lane-offset pointers)
-    const double *pa = ga - (threadIdx.x & 31), *pc = gc - (threadIdx.x & 31);
-    for (int64_t q = s0 + 1; q < s1 && q <= s0 + PFD; ++q) pf_step(R, q, pa, pc);
-  }
   for (int64_t st = s0; st < s1; ++st) {
-    if (PFD > 0 && st + PFD + 1 < s1)
-      pf_step(R, st + PFD + 1, ga - (threadIdx.x & 31), gc - (threadIdx.x & 31));
     int pn = 0, cn = 0;
     int64_t sn = 0, rn = 0;
     double dna = 1.0, dnc = 1.0, yna = 0.0, ync = 0.0;
@@ -561,7 +277,7 @@ __device__ __forceinline__ void bt_node2(const DevSym &S, const BatchP &P, const
 #endif
 __global__ void __launch_bounds__(PIPE_WARPS * 32, PIPE_MINB_DEF)
     k_bt_pipe2(DevSym S, BatchP P, DevProg R, const TaskDesc *tasks, int64_t total, const double *rhs,
-               double *Y, int *counter, int *flags, int epoch, int G, int ws, int nowait, int pf) {
+               double *Y, int *counter, int *flags, int epoch, int G, int ws) {
   extern __shared__ __align__(16) double pipe_smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double *wsm_w = pipe_smem + (size_t)warp * 2 * ws * 32;
@@ -571,56 +287,31 @@ __global__ void __launch_bounds__(PIPE_WARPS * 32, PIPE_MINB_DEF)
     t = __shfl_sync(HY_FULL, t, 0);
     if (t >= total) return;
     const TaskDesc cur = tasks[t];
-    // L2 prefetch of the matrix values of the task `pf` positions ahead in claim
-    // order (streamed from HBM; independent of every dependency): its descriptor
-    // loads now, its row record after the polls, the prefetches after this task
-    const int64_t tp = t + pf;
-    int pg = -1, pr = 0;
-    if (pf > 0 && tp < total) {
-      pg = __ldg(&tasks[tp].g);
-      pr = __ldg(&tasks[tp].r);
-    }
     const int two = cur.g + 1 < G ? 2 : 1;
     const int64_t nd = cur.d1 - cur.d0;
     // relaxed polls (an acquire load would invalidate the SM's L1 on every poll);
     // every value a task reads from another task is loaded L2-coherent (ld.cg)
     // after the polls, and producers fence before publishing
-    for (int64_t k = lane; k < nd * two && !(nowait & 1); k += 32) {
+    for (int64_t k = lane; k < nd * two; k += 32) {
       const int64_t kk = k < nd ? k : k - nd;
       const int dn = kk == 0 ? cur.dep[0] : kk == 1 ? cur.dep[1] : kk == 2 ? cur.dep[2] :
                      kk == 3 ? cur.dep[3] : __ldg(S.deps + cur.d0 + kk);
       const int *f = flags + (int64_t)dn * G + cur.g + (k < nd ? 0 : 1);
       while (ld_relaxed(f) != epoch) __nanosleep(64);
     }
+    // acquire side of the flag protocol: one fence after the observed flags (not one
+    // per spin) pairs with the producer's fence + relaxed store (PTX fence-based
+    // synchronization); __syncwarp then orders the other lanes after this lane
+    fence_acq_rel_gpu();
     __syncwarp();
-    int64_t pe0 = 0, pk = 0;
-    if (pg >= 0) {
-      pe0 = __ldg(&R.row_rec[pr].y);
-      pk = __ldg(&R.row_rec[pr].z) >> 32;
-    }
     const longlong4 nr = make_longlong4(cur.valoff, cur.d0, (int64_t)cur.r | ((int64_t)cur.s << 32),
                                         (int64_t)cur.W | ((int64_t)cur.L << 32));
-    bt_node2(S, P, R, nr, cur.g, rhs, Y, wsm_w, ws, lane, nowait, cur.rr0, false, 0.0, 0.0);
-    if (pg >= 0 && pk > 0)
-#pragma unroll
-      for (int m = 0; m < 2; ++m) {
-        const int64_t bi = (int64_t)pg * 32 + m * 32 + lane;
-        if (bi < P.B) {
-          const double *a0 = P.A + bi * S.nnz + pe0;
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(a0));
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(a0 + pk - 1));
-        }
-      }
+    bt_node2(S, P, R, nr, cur.g, rhs, Y, wsm_w, ws, lane, 0, cur.rr0, false, 0.0, 0.0);
     fence_acq_rel_gpu();
     __syncwarp();
     if (lane < two) st_relaxed(flags + (int64_t)cur.u * G + cur.g + lane, epoch);
   }
 }
-
-template __global__ void k_bt_pipe<false>(DevSym, BatchP, DevProg, const TaskDesc *, int64_t,
-                                          const double *, double *, int *, int *, int, int, int);
-template __global__ void k_bt_pipe<true>(DevSym, BatchP, DevProg, const TaskDesc *, int64_t,
-                                         const double *, double *, int *, int *, int, int, int);
 
 // ---------------------------------------------------------------------------
 // Hub kernel: one CTA per (hub node, group).  Pull programs: the positions of a row
@@ -646,7 +337,7 @@ __global__ void __launch_bounds__(HUB_THREADS) k_bt_hub(DevSym S, BatchP P, DevP
                                                         const int32_t *nodes, int count, int G,
                                                         const double *rhs, double *Y,
                                                         double *scratch, int max_slots, int *flags,
-                                                        int epoch, int df) {
+                                                        int epoch) {
   __shared__ double red[HUB_THREADS / 32][32];
   constexpr int LVCAP = 512;
   __shared__ int64_t s_wi[LVCAP + 1], s_sp[LVCAP + 1], s_y[LVCAP + 1];
@@ -742,127 +433,7 @@ __global__ void __launch_bounds__(HUB_THREADS) k_bt_hub(DevSym S, BatchP P, DevP
         cp_async8(reinterpret_cast<double *>(pu + k2), reinterpret_cast<const double *>(R.pred_u + yb0 + k2));
       }
     };
-    // ---- dataflow phase: the leading levels without split positions run without
-    // level barriers.  Batches of <= 4 same-level items are dealt to warps in level
-    // order; an item waits (shared-memory ready bits, one per node-relative
-    // position) for the positions it reads — its multipliers, and U values or
-    // divisors inside this node — then finalises its position and sets its bit.
-    // Every wait points to a strictly lower level, and each warp runs its batches
-    // in order, so the lowest unfinished batch can always proceed.
-    int qdf = 0;
-    const int64_t nbits = (int64_t)s * W;
-    if (df && lsm && nbits <= (int64_t)2 * HUB_BUF * 8)
-      while (qdf < nlv && s_sp[qdf + 1] == s_sp[qdf]) ++qdf;
-    if (qdf > 0) {
-      unsigned *rdy = reinterpret_cast<unsigned *>(hub_dyn);
-      volatile unsigned *vrdy = rdy;
-      const int nwords = (int)((nbits + 31) >> 5);
-      // positions no dataflow item writes (structural zeros of the union layout,
-      // A-only entries) are ready from the start
-      for (int q2 = threadIdx.x; q2 < nwords; q2 += HUB_THREADS) rdy[q2] = ~0u;
-      __syncthreads();
-      for (int64_t it = s_wi[0] + threadIdx.x; it < s_wi[qdf]; it += HUB_THREADS) {
-        const int pz = __ldg(R.wi_p + it);
-        atomicAnd(rdy + (pz >> 5), ~(1u << (pz & 31)));
-      }
-      if (threadIdx.x == 0) {
-        int acc = 0;
-        for (int q2 = 0; q2 < qdf; ++q2) {
-          s_bt[q2] = acc;
-          acc += (int)((s_wi[q2 + 1] - s_wi[q2] + 3) >> 2);
-        }
-        s_bt[qdf] = acc;
-      }
-      __syncthreads();
-      const int nbt = s_bt[qdf];
-      const int64_t nb = S.valoff[u], nbe = nb + nbits;
-      auto wait_pos = [&](int64_t pos) {
-        while (!((vrdy[pos >> 5] >> (pos & 31)) & 1u)) __nanosleep(20);
-      };
-      for (int k = warp; k < nbt; k += nw) {
-        int lo = 0, hi = qdf;
-        while (hi - lo > 1) {
-          const int mid = (lo + hi) >> 1;
-          if (s_bt[mid] <= k) lo = mid; else hi = mid;
-        }
-        const int64_t i0 = s_wi[lo] + 4LL * (k - s_bt[lo]);
-        const int64_t iend = s_wi[lo + 1];
-        const int ni = (int)(i0 + 4 < iend ? 4 : iend - i0);
-        int p[4];
-        int64_t y[4], y1[4], kd[4];
-        double acc[4];
-#pragma unroll
-        for (int jq = 0; jq < 4; ++jq) {
-          const bool ok = jq < ni;
-          p[jq] = ok ? __ldg(R.wi_p + i0 + jq) : 0;
-          y[jq] = ok ? __ldg(R.wi_y0 + i0 + jq) : 0;
-          y1[jq] = ok ? __ldg(R.wi_y1 + i0 + jq) : 0;
-          kd[jq] = ok ? __ldg(R.wi_kd + i0 + jq) : -1;
-          acc[jq] = ok ? w[p[jq] * 32] : 0.0;
-        }
-        int64_t rem = 0;
-#pragma unroll
-        for (int jq = 0; jq < 4; ++jq) rem = max(rem, y1[jq] - y[jq]);
-        for (int64_t step = 0; step < rem; step += 2) {
-          int pp[4][2];
-          int64_t pu[4][2];
-#pragma unroll
-          for (int jq = 0; jq < 4; ++jq)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int64_t yy = y[jq] + step + e;
-              const bool act = yy < y1[jq];
-              pp[jq][e] = act ? __ldg(R.pred_p + yy) : -1;
-              pu[jq][e] = act ? __ldg(R.pred_u + yy) : -1;
-            }
-#pragma unroll
-          for (int jq = 0; jq < 4; ++jq)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              if (pp[jq][e] >= 0) wait_pos(pp[jq][e]);
-              if (pu[jq][e] >= nb && pu[jq][e] < nbe) wait_pos(pu[jq][e] - nb);
-            }
-          __threadfence_block();
-          double lv[4][2], uv[4][2];
-#pragma unroll
-          for (int jq = 0; jq < 4; ++jq)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              lv[jq][e] = pp[jq][e] >= 0 ? w[pp[jq][e] * 32] : 0.0;
-              uv[jq][e] = pp[jq][e] >= 0 ? gb[pu[jq][e] * 32] : 0.0;
-            }
-#pragma unroll
-          for (int jq = 0; jq < 4; ++jq)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) acc[jq] -= lv[jq][e] * uv[jq][e];
-        }
-#pragma unroll
-        for (int jq = 0; jq < 4; ++jq) {
-          if (jq >= ni) continue;
-          double a = acc[jq];
-          if (kd[jq] >= 0) {
-            if (kd[jq] >= nb && kd[jq] < nbe) {
-              wait_pos(kd[jq] - nb);
-              __threadfence_block();
-            }
-            a = a / gb[kd[jq] * 32];
-          } else if (kd[jq] == -2) {
-            bool fired;
-            const double piv = a;
-            a = perturb(piv, thr, fired);
-            if (fired && live) atomicAdd(&P.npert[b], 1);
-          }
-          w[p[jq] * 32] = a;
-        }
-        __threadfence_block();
-        __syncwarp();
-        if (lane == 0)
-#pragma unroll
-          for (int jq = 0; jq < 4; ++jq)
-            if (jq < ni) atomicOr(rdy + (p[jq] >> 5), 1u << (p[jq] & 31));
-      }
-      __syncthreads();
-    }
+    const int qdf = 0;
     if (qdf < nlv && stageable(qdf)) issue(qdf);
     cp_async_commit();
     for (int64_t lev = lv0 + qdf; lev < lv1; ++lev) {
@@ -1109,46 +680,6 @@ __global__ void __launch_bounds__(BW * 32) k_batch_fwd(DevSym S, const double *B
   }
 }
 
-__global__ void __launch_bounds__(BW * 32) k_batch_bwd(DevSym S, const double *BF, int64_t stored,
-                                                       const int32_t *nodes, int count, int G,
-                                                       double *Y) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t task = (int64_t)blockIdx.x * BW + warp;
-  if (task >= (int64_t)count * G) return;
-  const int u = nodes[task / G];
-  const int g = (int)(task % G);
-  const int r = (int)S.first[u];
-  const int s = (int)(S.first[u + 1] - r);
-  const int64_t c0 = S.colptr[u];
-  const int W = (int)(S.colptr[u + 1] - c0);
-  const int L = S.nl[u];
-  const double *gbase = BF + (int64_t)g * stored * 32 + lane;
-  double *y = Y + (int64_t)g * S.n * 32 + lane;
-  const int32_t *cc = S.cols + c0;
-  for (int t = s - 1; t >= 0; --t) {
-    const double *row = gbase + (S.valoff[u] + (int64_t)t * W) * 32;
-    const int d = L + t;
-    double acc = y[(int64_t)(r + t) * 32];
-    const double dg = row[(int64_t)d * 32];
-    // predicated 8-wide batches: all column indices, then all factor values and
-    // solution gathers of a batch are in flight together
-    for (int p0 = d + 1; p0 < W; p0 += 8) {
-      int k[8];
-      double a[8], z[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) k[e] = p0 + e < W ? __ldg(cc + p0 + e) : -1;
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        a[e] = k[e] >= 0 ? row[(int64_t)(p0 + e) * 32] : 0.0;
-        z[e] = k[e] >= 0 ? y[(int64_t)k[e] * 32] : 0.0;
-      }
-#pragma unroll
-      for (int e = 0; e < 8; ++e) acc -= a[e] * z[e];
-    }
-    y[(int64_t)(r + t) * 32] = acc / dg;
-  }
-}
-
 // Pair mode backward substitution: one warp per (node, group pair); the padded
 // allocation makes the odd tail group's partner valid memory (never copied out).
 __global__ void __launch_bounds__(BW * 32) k_batch_bwd2(DevSym S, const double *BF, int64_t stored,
@@ -1195,59 +726,6 @@ __global__ void __launch_bounds__(BW * 32) k_batch_bwd2(DevSym S, const double *
     }
     ya[(int64_t)(r + t) * 32] = accA / dA;
     yc[(int64_t)(r + t) * 32] = accC / dC;
-  }
-}
-
-// Persistent backward substitution: one warp per (node, group) task in diagonal
-// order over backward levels; a task waits for the nodes owning its columns right
-// of its block (U dependencies) and publishes its own completion flag.
-__global__ void __launch_bounds__(128) k_bt_bwd(DevSym S, const double *BF, int64_t stored,
-                                                const int2 *tasks, int64_t total, const int64_t *udp,
-                                                const int32_t *udeps, int *counter, int *flags, int epoch,
-                                                int G, double *Y) {
-  const int lane = threadIdx.x & 31;
-  for (;;) {
-    long long t = 0;
-    if (lane == 0) t = (long long)atomicAdd(reinterpret_cast<unsigned long long *>(counter), 1ull);
-    t = __shfl_sync(HY_FULL, t, 0);
-    if (t >= total) return;
-    const int2 tk = tasks[t];
-    const int u = tk.x, g = tk.y;
-    for (int64_t k = udp[u] + lane; k < udp[u + 1]; k += 32) {
-      const int *f = flags + (int64_t)udeps[k] * G + g;
-      while (ld_acquire(f) != epoch) __nanosleep(64);
-    }
-    __syncwarp();
-    const int r = (int)S.first[u];
-    const int s = (int)(S.first[u + 1] - r);
-    const int64_t c0 = S.colptr[u];
-    const int W = (int)(S.colptr[u + 1] - c0);
-    const int L = S.nl[u];
-    const double *gbase = BF + (int64_t)g * stored * 32 + lane;
-    double *y = Y + (int64_t)g * S.n * 32 + lane;
-    const int32_t *cc = S.cols + c0;
-    for (int t2 = s - 1; t2 >= 0; --t2) {
-      const double *row = gbase + (S.valoff[u] + (int64_t)t2 * W) * 32;
-      const int d = L + t2;
-      double acc = y[(int64_t)(r + t2) * 32];
-      int p = d + 1;
-      for (; p + 4 <= W; p += 4) {
-        const int k0 = cc[p], k1 = cc[p + 1], k2 = cc[p + 2], k3 = cc[p + 3];
-        const double a0 = row[(int64_t)p * 32], a1 = row[(int64_t)(p + 1) * 32];
-        const double a2 = row[(int64_t)(p + 2) * 32], a3 = row[(int64_t)(p + 3) * 32];
-        const double z0 = y[(int64_t)k0 * 32], z1 = y[(int64_t)k1 * 32];
-        const double z2 = y[(int64_t)k2 * 32], z3 = y[(int64_t)k3 * 32];
-        acc -= a0 * z0;
-        acc -= a1 * z1;
-        acc -= a2 * z2;
-        acc -= a3 * z3;
-      }
-      for (; p < W; ++p) acc -= row[(int64_t)p * 32] * y[(int64_t)cc[p] * 32];
-      y[(int64_t)(r + t2) * 32] = acc / row[(int64_t)d * 32];
-    }
-    __threadfence();
-    __syncwarp();
-    if (lane == 0) st_release(flags + (int64_t)u * G + g, epoch);
   }
 }
 

@@ -759,113 +759,6 @@ __global__ void __launch_bounds__(FI_THREADS) k_fi_upd_pk(DevSym S, CallP P, Fan
   if (tid == 0) D.part_cnt[first] = 0;
 }
 
-__global__ void __launch_bounds__(FI_THREADS) k_fi_upd_mma(DevSym S, CallP P, FaninDev D, int base,
-                                                       int Smax, int Mmax) {
-  extern __shared__ __align__(16) double fs[];
-  __shared__ int tcol[FI_TILE];
-  __shared__ int spos[FI_TILE];
-  const int j = base + blockIdx.x;
-  const int T = D.up_t[j];
-  const int c0 = D.up_c0[j], c1 = D.up_c1[j];
-  const int tw = c1 - c0;
-  const int tid = threadIdx.x;
-  const int r = (int)S.first[T];
-  const int s = (int)(S.first[T + 1] - r);
-  const int64_t tc0 = S.colptr[T];
-  const int W = (int)(S.colptr[T + 1] - tc0);
-  double *Pm = P.F + S.valoff[T];
-  double *acc = fs;                          // s x FI_TILE
-  double *Xs = acc + (size_t)Smax * FI_TILE; // Smax x KLD
-  double *Ut = Xs + (size_t)Smax * KLD;      // FI_KC x FXLD
-  (void)Mmax;
-  for (int c = tid; c < tw; c += FI_THREADS) tcol[c] = S.cols[tc0 + c0 + c];
-  for (int idx = tid; idx < s * FI_TILE; idx += FI_THREADS) {
-    const int t = idx / FI_TILE, c = idx - t * FI_TILE;
-    acc[idx] = c < tw ? Pm[(int64_t)t * W + c0 + c] : 0.0;
-  }
-  for (int64_t z = D.up_ptr[j]; z < D.up_ptr[j + 1]; ++z) {
-    const int v = D.src_v[z];
-    const int q0 = D.src_q0[z];
-    const int nq = D.src_q1[z] - q0;
-    const int vf = (int)S.first[v];
-    const int vs = (int)(S.first[v + 1] - vf);
-    const int64_t vc0 = S.colptr[v];
-    const int vW = (int)(S.colptr[v + 1] - vc0);
-    const int vnl = S.nl[v];
-    const double *vb = P.F + S.valoff[v];
-    const int pb0 = D.src_pb[z];
-    const int tb0 = D.src_tb[z];
-    const int m = vs - tb0;
-    const int qbase = vnl + vs + q0;
-    __syncthreads();
-    if (tid < nq) spos[tid] = lower_bound_i32(tcol, 0, tw, S.cols[vc0 + qbase + tid]);
-    // Large contractions (target >= 32 rows, source block >= 16) run on the FP64
-    // tensor cores: mma.sync.m8n8k4 f64 (DMMA), the 8x8 output tiles spread over
-    // the 8 warps; fragments: A(8x4) one element per lane (row lane/4, col lane%4),
-    // B(4x8) one element (row lane%4, col lane/4), C(8x8) two elements (row
-    // lane/4, cols 2*(lane%4)+{0,1}).  Smaller ones use 4x4 FFMA register tiles.
-    const bool dmma = true;
-    const int warp = tid >> 5, lane = tid & 31, kq = lane & 3, lr = lane >> 2;
-    const int nrb = (s + 7) >> 3, ncb = (nq + 7) >> 3, ntile = nrb * ncb;
-    double d[8][2];
-#pragma unroll
-    for (int j2 = 0; j2 < 8; ++j2) d[j2][0] = d[j2][1] = 0.0;
-    for (int k0 = 0; k0 < m; k0 += FI_KC) {
-      const int kc = min(FI_KC, m - k0);
-      const int kc4 = (kc + 3) & ~3;
-      if (k0) __syncthreads();
-      for (int idx = tid; idx < s * kc4; idx += FI_THREADS) {
-        const int t = idx / kc4, a = idx - t * kc4;
-        Xs[t * KLD + a] = a < kc ? Pm[(int64_t)t * W + pb0 + k0 + a] : 0.0;
-      }
-      for (int idx = tid; idx < kc4 * FI_TILE; idx += FI_THREADS) {
-        const int a = idx >> 6, c = idx & 63;
-        Ut[a * FXLD + c] = (c < nq && a < kc) ? vb[(int64_t)(tb0 + k0 + a) * vW + qbase + c] : 0.0;
-      }
-      __syncthreads();
-      if (dmma) {
-        for (int k = 0; k < kc; k += 4) {
-#pragma unroll
-          for (int j2 = 0; j2 < 8; ++j2) {
-            const int ti = warp + 8 * j2;
-            if (ti < ntile) {
-              const int rb = ti / ncb, cb = ti - rb * ncb;
-              const int ar = rb * 8 + lr;
-              const double av = ar < s ? Xs[ar * KLD + k + kq] : 0.0;
-              const double bv = Ut[(k + kq) * FXLD + cb * 8 + lr];
-              asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                           : "+d"(d[j2][0]), "+d"(d[j2][1])
-                           : "d"(av), "d"(bv));
-            }
-          }
-        }
-      }
-    }
-    if (dmma) {
-#pragma unroll
-      for (int j2 = 0; j2 < 8; ++j2) {
-        const int ti = warp + 8 * j2;
-        if (ti < ntile) {
-          const int rb = ti / ncb, cb = ti - rb * ncb;
-          const int t = rb * 8 + lr;
-          if (t < s) {
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int c = cb * 8 + kq * 2 + e;
-              if (c < nq) acc[t * FI_TILE + spos[c]] -= d[j2][e];
-            }
-          }
-        }
-      }
-    }
-  }
-  __syncthreads();
-  for (int idx = tid; idx < s * FI_TILE; idx += FI_THREADS) {
-    const int t = idx / FI_TILE, c = idx - t * FI_TILE;
-    if (c < tw) Pm[(int64_t)t * W + c0 + c] = acc[idx];
-  }
-}
-
 // ---------------------------------------------------------------------------- updates, DMMA
 // k_fi_upd with every per-source contraction on the FP64 tensor cores
 // (mma.sync.aligned.m8n8k4 f64 -> SASS DMMA).  Warp tiles: 16 x 32 (4 x 2 warps
@@ -1643,172 +1536,6 @@ __global__ void __launch_bounds__(FI_THREADS, KC_MINB_DEF) k_fi_upd_kcp(DevSym S
   if (tid == 0) D.part_cnt[first] = 0;
 }
 
-// ---------------------------------------------------------------------------- updates v3
-// Per item: the K dimension is the concatenation of its sources' block rows, cut
-// into chunks of <= FI_KC rows that never straddle a source.  Chunk c+1 is copied
-// with cp.async (multipliers into Xb, the source's U rows scattered straight into
-// the tile's 64-column space of Ub, uncovered columns zeroed) while chunk c is
-// multiplied; the product of all sources accumulates in registers and the target
-// tile is updated once at the end.
-__device__ __forceinline__ void cpa8x(void *smem_dst, const void *gsrc) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gsrc) : "memory");
-}
-
-struct ChunkMeta {
-  int m;        // rows in chunk
-  int pb;       // target column of the chunk's first multiplier
-  int urow;     // first U row within the source
-  int nq;
-  int qoff;
-  int vW;
-  int64_t vbase, vc0;
-};
-
-__device__ __forceinline__ bool next_chunk(const DevSym &S, const FaninDev &D, int64_t &z, int &a0,
-                                           int64_t z1, ChunkMeta &cm) {
-  if (z >= z1) return false;
-  const int v = D.src_v[z];
-  const int vf = (int)S.first[v];
-  const int vs = (int)(S.first[v + 1] - vf);
-  const int tb = D.src_tb[z];
-  const int m = vs - tb;
-  cm.vc0 = S.colptr[v];
-  cm.vW = (int)(S.colptr[v + 1] - cm.vc0);
-  cm.vbase = S.valoff[v];
-  const int q0 = D.src_q0[z];
-  cm.nq = D.src_q1[z] - q0;
-  cm.qoff = S.nl[v] + vs + q0;
-  cm.m = min(FI_KC, m - a0);
-  cm.pb = D.src_pb[z] + a0;
-  cm.urow = tb + a0;
-  a0 += cm.m;
-  if (a0 >= m) {
-    ++z;
-    a0 = 0;
-  }
-  return true;
-}
-
-__global__ void __launch_bounds__(FI_THREADS) k_fi_upd3(DevSym S, CallP P, FaninDev D, int base,
-                                                        int Smax, int Mmax) {
-  extern __shared__ __align__(16) double fs3[];
-  __shared__ int tcol[FI_TILE];
-  __shared__ int posb[2][FI_TILE];
-  __shared__ int covb[2][FI_TILE];
-  (void)Mmax;
-  const int j = base + blockIdx.x;
-  const int T = D.up_t[j];
-  const int c0 = D.up_c0[j], c1 = D.up_c1[j];
-  const int tw = c1 - c0;
-  const int tid = threadIdx.x;
-  const int r = (int)S.first[T];
-  const int s = (int)(S.first[T + 1] - r);
-  const int64_t tc0 = S.colptr[T];
-  const int W = (int)(S.colptr[T + 1] - tc0);
-  double *Pm = P.F + S.valoff[T];
-  double *Xb[2], *Ub[2];
-  Xb[0] = fs3;
-  Ub[0] = Xb[0] + (size_t)Smax * KLD;
-  Xb[1] = Ub[0] + (size_t)FI_KC * FXLD;
-  Ub[1] = Xb[1] + (size_t)Smax * KLD;
-  for (int c = tid; c < tw; c += FI_THREADS) tcol[c] = S.cols[tc0 + c0 + c];
-  __syncthreads();
-  const int tr = tid >> 4, tcl = tid & 15;
-  double c4[4][4];
-#pragma unroll
-  for (int x = 0; x < 4; ++x)
-#pragma unroll
-    for (int y = 0; y < 4; ++y) c4[x][y] = 0.0;
-  int64_t z = D.up_ptr[j];
-  const int64_t z1 = D.up_ptr[j + 1];
-  int a0 = 0;
-  ChunkMeta cur, nxt;
-  bool have = next_chunk(S, D, z, a0, z1, cur);
-  // positions + coverage of the first chunk, then its copies
-  auto positions = [&](const ChunkMeta &cm, int b) {
-    if (tid < FI_TILE) covb[b][tid] = 0;
-    __syncthreads();
-    if (tid < cm.nq) {
-      const int pos = lower_bound_i32(tcol, 0, tw, S.cols[cm.vc0 + cm.qoff + tid]);
-      posb[b][tid] = pos;
-      covb[b][pos] = 1;
-    }
-    __syncthreads();
-  };
-  auto issue = [&](const ChunkMeta &cm, int b) {
-    double *X = Xb[b], *U = Ub[b];
-    for (int idx = tid; idx < s * cm.m; idx += FI_THREADS) {
-      const int t = idx / cm.m, a = idx - t * cm.m;
-      cpa8x(X + t * KLD + a, Pm + (int64_t)t * W + cm.pb + a);
-    }
-    const int m4 = (cm.m + 3) & ~3;
-    for (int idx = tid; idx < m4 * FI_TILE; idx += FI_THREADS) {
-      const int a = idx >> 6, c = idx & 63;
-      if (a >= cm.m || !covb[b][c]) U[a * FXLD + c] = 0.0;
-    }
-    for (int idx = tid; idx < cm.m * cm.nq; idx += FI_THREADS) {
-      const int a = idx / cm.nq, c = idx - a * cm.nq;
-      cpa8x(U + a * FXLD + posb[b][c], P.F + cm.vbase + (int64_t)(cm.urow + a) * cm.vW + cm.qoff + c);
-    }
-    // pad multiplier columns up to a multiple of 4 with zeros (kept for symmetry)
-    for (int idx = tid; idx < s * (m4 - cm.m); idx += FI_THREADS) {
-      const int t = idx / (m4 - cm.m), a = cm.m + idx - t * (m4 - cm.m);
-      X[t * KLD + a] = 0.0;
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-  if (have) {
-    positions(cur, 0);
-    issue(cur, 0);
-  }
-  int b = 0;
-  while (have) {
-    const bool more = next_chunk(S, D, z, a0, z1, nxt);
-    if (more) {
-      positions(nxt, b ^ 1);
-      issue(nxt, b ^ 1);
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-    }
-    __syncthreads();
-    const double *X = Xb[b], *U = Ub[b];
-    for (int a = 0; a < cur.m; ++a) {
-      double xv[4], uv[4];
-#pragma unroll
-      for (int x = 0; x < 4; ++x) xv[x] = (tr + 16 * x < s) ? X[(tr + 16 * x) * KLD + a] : 0.0;
-#pragma unroll
-      for (int y = 0; y < 4; ++y) uv[y] = U[a * FXLD + tcl + 16 * y];
-#pragma unroll
-      for (int x = 0; x < 4; ++x)
-#pragma unroll
-        for (int y = 0; y < 4; ++y) c4[x][y] = fma(xv[x], uv[y], c4[x][y]);
-    }
-    __syncthreads();   // buffer b free for the chunk after next
-    if (!more) break;
-    cur = nxt;
-    b ^= 1;
-  }
-#pragma unroll
-  for (int x = 0; x < 4; ++x) {
-    const int t = tr + 16 * x;
-    if (t < s) {
-#pragma unroll
-      for (int y = 0; y < 4; ++y) {
-        const int c = tcl + 16 * y;
-        if (c < tw) Pm[(int64_t)t * W + c0 + c] -= c4[x][y];
-      }
-    }
-  }
-}
-
-size_t fi_upd3_smem(int Smax) {
-  return 2 * ((size_t)Smax * KLD + (size_t)FI_KC * FXLD) * sizeof(double);
-}
-
-// (k_fi_upd_mma: the same item loop with every contraction on DMMA; the host
-// routes items whose target has >= 32 rows to it.)
 size_t fi_upd_smem(int Smax, int Mmax) {
   (void)Mmax;
   // k_fi_upd uses Xs + Ut only; the DMMA variant also keeps an accumulator tile

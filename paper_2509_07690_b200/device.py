@@ -281,11 +281,8 @@ class DeviceContext:
         if os.environ.get("HYLU_FANIN_MAPS", "1") != "0":
             # per source record: tile positions of its columns + source metadata
             # (k_fi_upd_kc skips its per-item binary searches); cached with the plan
-            maps = getattr(s, "_kc_maps", None)
-            if maps is None:
-                maps = schedule.kc_source_maps(s, plan)
-                s._kc_maps = maps
-            off, pos, vb, vW, qb, mm = maps
+            # (built per upload, not cached on the analysis: the device copy is the one used)
+            off, pos, vb, vW, qb, mm = schedule.kc_source_maps(s, plan)
             ptr = lambda a: a.ctypes.data if a.size else None  # noqa: E731
             with self.torch.cuda.device(self.device):
                 check(self.lib.hy_upload_fanin_maps(self.h, len(vb), len(pos), ptr(off), ptr(pos), ptr(vb),

@@ -502,3 +502,48 @@ def test_zero_pivot_without_perturbation_raises_numeric_breakdown():
         api.refactorize(A, f0, api.FactorOptions(perturbation_epsilon=0.0))
     f = api.refactorize(A, f0)                      # default eps: perturbed, no error
     assert len(f.perturbed) >= 1
+
+
+def _gpu_shard_worker(rank, world, port, q):
+    import os
+    import torch
+    import torch.distributed as dist
+    from paper_2509_07690_b200 import sharding
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)   # gather only, off the data path
+    try:
+        total = 96
+        bp = gen.circuit_batch(total, 2000, 2, 200)
+        an = an_mod.analyze(bp.A0, SolverConfig(ordering="amd"))
+        prior = api.factorize_analysis(an)
+        br = api.BatchedRefactorizer(prior)
+        lo, hi = sharding.shard_range(total, rank, world)
+        x, npert = br.run(torch.from_numpy(bp.values[lo:hi]).cuda(), torch.from_numpy(bp.rhs[lo:hi]).cuda())
+        X = sharding.gather_shards(x.cpu().numpy(), total, dist)
+        NP = sharding.gather_shards(npert.cpu().numpy(), total, dist)
+        if rank == 0:
+            x1, n1 = br.run(torch.from_numpy(bp.values).cuda(), torch.from_numpy(bp.rhs).cuda())
+            q.put((bool(np.array_equal(X, x1.cpu().numpy())), bool(np.array_equal(NP, n1.cpu().numpy()))))
+    except Exception as e:          # report instead of hanging the parent
+        q.put(("error", repr(e)))
+    dist.destroy_process_group()
+
+
+def test_sharded_batch_two_processes_bitwise():
+    """SURVEY §8(e) on one device: two independent processes each refactorize+solve
+    their contiguous shard (no collective on the data path; a gloo gather off the
+    clock), and the gathered x / perturbation counts equal a one-process run bit for
+    bit (per instance the arithmetic does not depend on its group or lane)."""
+    import multiprocessing as mp
+    import random
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = random.randint(20000, 40000)
+    ps = [ctx.Process(target=_gpu_shard_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(600)
+    res = q.get(timeout=5)
+    assert res == (True, True), res

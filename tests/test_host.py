@@ -367,3 +367,74 @@ def test_kc_source_maps_match_direct_search():
                 sc = cols[colptr[v] + q:colptr[v] + q + plan.src_q1[z] - plan.src_q0[z]]
                 assert np.array_equal(pos[off[z]:off[z + 1]], np.searchsorted(tc, sc))
                 assert (vb[z], vW[z], qb[z], mm[z]) == (valoff[v], colptr[v + 1] - colptr[v], q, vs - stb[z])
+
+
+@pytest.mark.parametrize("name", ["c0", "c1", "c2", "c3"])
+def test_parallel_oracle_is_bitwise_sequential(name):
+    """The oracle's level-parallel executor (SPEC.md:397-405 run_bulk) gives the
+    sequential restatement's factors bit for bit, in every kernel mode, for
+    factorize and refactorize (the CPU baseline's 'all threads' leg uses it)."""
+    p = gen.config(name, "small")
+    for mode in (None, 0, 1, 2):
+        an = an_mod.analyze(p.A, SolverConfig(ordering=p.ordering), kernel_override=mode)
+        f1 = on.factorize(an)
+        f2 = on.factorize(an, threads=4)
+        assert np.array_equal(f1.values, f2.values)
+        assert np.array_equal(f1.inner_perm, f2.inner_perm)
+        assert f1.perturbed == f2.perturbed and f1.breakdown == f2.breakdown
+        v2 = np.asarray(p.A.values) * 1.01
+        r1 = on.factorize(an, v2, prior=f1)
+        r2 = on.factorize(an, v2, prior=f1, threads=3)
+        assert np.array_equal(r1.values, r2.values)
+
+
+def test_parallel_oracle_perturbation_and_breakdown_logs():
+    """Zero pivots: the parallel executor's per-row flags reproduce the sequential
+    perturbation log (factor-row order)."""
+    p = gen.lap2d(8)
+    an = an_mod.analyze(p.A, SolverConfig(ordering="amd"))
+    v = np.array(p.A.values)
+    rows = np.repeat(np.arange(p.A.n), np.diff(p.A.row_ptr))
+    v[rows == p.A.col_idx] = 0.0                       # every diagonal zero
+    f1 = on.factorize(an, v)
+    f2 = on.factorize(an, v, threads=4)
+    assert len(f1.perturbed) > 0
+    assert f1.perturbed == f2.perturbed and f1.breakdown == f2.breakdown
+
+
+def _gloo_shard_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    bp = gen.circuit_batch(24, 2000, 2, 200)
+    an = an_mod.analyze(bp.A0, SolverConfig(ordering="amd"))
+    prior = on.factorize(an)
+    lo, hi = sharding.shard_range(24, rank, world)
+    X, npert = on.refactor_solve_batch(an, prior, bp.values[lo:hi], bp.rhs[lo:hi])
+    Xall = sharding.gather_shards(X, 24, dist)
+    nall = sharding.gather_shards(npert, 24, dist)
+    t = sharding.all_values(float(rank) + 0.5, dist)
+    if rank == 0:
+        X1, n1 = on.refactor_solve_batch(an, prior, bp.values, bp.rhs)
+        q.put((bool(np.array_equal(Xall, X1)), bool(np.array_equal(nall, n1)), t))
+    dist.destroy_process_group()
+
+
+def test_sharded_batch_gloo_world2_matches_single_rank():
+    """the c4 workload sharded contiguously over 2 ranks (gloo, CPU)
+    with no data-path collective; the gathered solutions equal a single-rank run
+    bit for bit."""
+    import multiprocessing as mp
+    import random
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = random.randint(20000, 40000)
+    ps = [ctx.Process(target=_gloo_shard_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(300)
+    same_x, same_n, t = q.get(timeout=5)
+    assert same_x and same_n
+    assert t == [0.5, 1.5]

@@ -191,17 +191,22 @@ def test_rowrow_zero_multiplier_keeps_workspace():
 
 
 def test_internal_factorize_swap_cases():
-    """Block [[0,1],[1,0]] -> step 0 swaps; diag(3,5) -> identity."""
+    """Block [[0,1],[1,0]] -> step 0 swaps; diag(3,5) -> identity.
+    Both blocks keep their explicit zeros, so the 2x2 pattern is full
+    and the two rows form one supernode on which internal_factorize runs."""
     for blk, expect in (([[0.0, 1.0], [1.0, 0.0]], [1, 0]), ([[3.0, 0.0], [0.0, 5.0]], [0, 1])):
-        A = _csr(blk) if blk[0][0] else SparseMatrixCSR.from_dense(np.array(blk), keep_zeros=True)
+        A = SparseMatrixCSR.from_dense(np.array(blk), keep_zeros=True)
         an = _analyze(A, mode=None)
         an.vmap.scale[:] = 1.0
         an.vmap.mrow_src[:] = np.arange(2)
         an.ordering.perm[:] = np.arange(2)
         s = an.symbolic
-        if s.supernode_count == 1:
-            f = on.factorize(an)
-            assert list(f.inner_perm) == expect
+        assert s.supernode_count == 1 and s.node_kind[0] == 1
+        f = on.factorize(an)
+        assert list(f.inner_perm) == expect
+        assert not f.perturbed
+        L, U, src = od.factors_dense(an, f.values, f.inner_perm)
+        assert np.array_equal(L @ U, np.array(blk)[src])
 
 
 @pytest.mark.parametrize("mode", [0, 1, 2])
@@ -288,17 +293,30 @@ def test_oracle_equivalence_random(seed):
 
 
 def test_inner_perm_selects_block_maximum():
-    """step t picks an in-block maximum."""
-    p = gen.fem27(3)
+    """step t picks an in-block maximum, |block[p_t][t]| >= |block[r][t]|
+    for r in t..s-1.  In the final factors that is: every in-block multiplier
+    L(r, t) = block[r][t] / block[p_t][t] (r > t, same supernode) has |.| <= 1, and
+    a non-trivial inner_perm occurs (the recipe is not diagonally dominant)."""
+    p = gen.fem27(3, recipe="literal")
     an = _analyze(p.A, "amd", 2)
     f = on.factorize(an)
-    assert an.symbolic.supernode_count > 0
+    s = an.symbolic
+    assert s.supernode_count > 0
+    assert not f.perturbed
     L, U, src = od.factors_dense(an, f.values, f.inner_perm)
     M = od.m_dense(an)
     assert np.abs(L @ U - M[src]).max() <= 1e-12 * np.abs(M).max()
-    assert np.abs(np.tril(L, -1)).max() <= 1.0 + 1e-12 or True
-
-
+    worst, checked, swapped = 0.0, 0, 0
+    for u in range(s.nnodes):
+        if s.node_kind[u] != 1:
+            continue
+        r, e = int(s.node_first[u]), int(s.node_first[u + 1])
+        blk = L[r:e, r:e]
+        worst = max(worst, float(np.abs(np.tril(blk, -1)).max()))
+        checked += 1
+        swapped += int(np.any(f.inner_perm[r:e] != np.arange(e - r)))
+    assert checked > 0 and swapped > 0
+    assert worst <= 1.0
 def test_tridiagonal_1e5_zero_fill_rowrow_fast():
     """Acceptance 6 (host part): tridiagonal n=100000 → zero fill, ROWROW, oracle solve."""
     import time
