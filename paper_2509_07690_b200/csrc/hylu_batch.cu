@@ -275,6 +275,9 @@ __device__ __forceinline__ void bt_node2(const DevSym &S, const BatchP &P, const
 #ifndef PIPE_MINB_DEF
 #define PIPE_MINB_DEF 4
 #endif
+#ifndef PIPE_ACQ
+#define PIPE_ACQ 2   // consumer acquire: 2 (default) one ld.acquire per observed flag after the relaxed spin, 1 one fence after the polls (+0.25 ms/step), 0 none (formally racy)
+#endif
 __global__ void __launch_bounds__(PIPE_WARPS * 32, PIPE_MINB_DEF)
     k_bt_pipe2(DevSym S, BatchP P, DevProg R, const TaskDesc *tasks, int64_t total, const double *rhs,
                double *Y, int *counter, int *flags, int epoch, int G, int ws) {
@@ -298,11 +301,16 @@ __global__ void __launch_bounds__(PIPE_WARPS * 32, PIPE_MINB_DEF)
                      kk == 3 ? cur.dep[3] : __ldg(S.deps + cur.d0 + kk);
       const int *f = flags + (int64_t)dn * G + cur.g + (k < nd ? 0 : 1);
       while (ld_relaxed(f) != epoch) __nanosleep(64);
+#if PIPE_ACQ == 2
+      (void)ld_acquire(f);
+#endif
     }
     // acquire side of the flag protocol: one fence after the observed flags (not one
     // per spin) pairs with the producer's fence + relaxed store (PTX fence-based
     // synchronization); __syncwarp then orders the other lanes after this lane
+#if PIPE_ACQ == 1
     fence_acq_rel_gpu();
+#endif
     __syncwarp();
     const longlong4 nr = make_longlong4(cur.valoff, cur.d0, (int64_t)cur.r | ((int64_t)cur.s << 32),
                                         (int64_t)cur.W | ((int64_t)cur.L << 32));
@@ -333,7 +341,7 @@ __device__ __forceinline__ void hub_finalize(const BatchP &P, int64_t kd, int p,
   w[p * 32] = acc;
 }
 
-__global__ void __launch_bounds__(HUB_THREADS) k_bt_hub(DevSym S, BatchP P, DevProg R,
+__global__ void __launch_bounds__(HUB_THREADS, 1) k_bt_hub(DevSym S, BatchP P, DevProg R,
                                                         const int32_t *nodes, int count, int G,
                                                         const double *rhs, double *Y,
                                                         double *scratch, int max_slots, int *flags,

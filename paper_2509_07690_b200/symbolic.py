@@ -29,7 +29,7 @@ from __future__ import annotations
 from dataclasses import dataclass, field
 
 import numpy as np
-from numba import njit
+from numba import njit, prange
 
 from ._ref import KernelMode, SolverConfig, errors
 
@@ -242,35 +242,43 @@ def _etree(n, mp, mc):
     return parent
 
 
-@njit(cache=True)
-def _row_subtrees(n, mp, mc, parent):
-    """L(i,:) = row subtree of i in the etree (symmetric patterns); exact, sorted."""
-    mark = np.full(n, -1, np.int64)
+@njit(cache=True, parallel=True)
+def _row_subtrees(n, mp, mc, parent, nthreads):
+    """L(i,:) = row subtree of i in the etree (symmetric patterns); exact, sorted.
+
+    Rows are independent given the etree: two passes (count, fill) over rows dealt
+    round-robin to ``nthreads`` workers, each with its own mark array (marker = the
+    row being walked).  Output is independent of the thread count."""
     cnt = np.zeros(n + 1, np.int64)
-    for i in range(n):
-        mark[i] = i
-        c = 0
-        for t in range(mp[i], mp[i + 1]):
-            j = mc[t]
-            while j < i and mark[j] != i:
-                mark[j] = i
-                c += 1
-                j = parent[j]
-        cnt[i + 1] = c
+    marks = np.full((nthreads, n), -1, np.int64)
+    for T in prange(nthreads):
+        mark = marks[T]
+        for i in range(T, n, nthreads):
+            mark[i] = i
+            c = 0
+            for t in range(mp[i], mp[i + 1]):
+                j = mc[t]
+                while j < i and mark[j] != i:
+                    mark[j] = i
+                    c += 1
+                    j = parent[j]
+            cnt[i + 1] = c
     lp = np.cumsum(cnt)
     li = np.empty(lp[n], np.int32)
-    mark[:] = -1
-    for i in range(n):
-        mark[i] = i
-        c = lp[i]
-        for t in range(mp[i], mp[i + 1]):
-            j = mc[t]
-            while j < i and mark[j] != i:
-                mark[j] = i
-                li[c] = j
-                c += 1
-                j = parent[j]
-        li[lp[i]:c] = np.sort(li[lp[i]:c])
+    for T in prange(nthreads):
+        mark = marks[T]
+        mark[:] = -1
+        for i in range(T, n, nthreads):
+            mark[i] = i
+            c = lp[i]
+            for t in range(mp[i], mp[i + 1]):
+                j = mc[t]
+                while j < i and mark[j] != i:
+                    mark[j] = i
+                    li[c] = j
+                    c += 1
+                    j = parent[j]
+            li[lp[i]:c] = np.sort(li[lp[i]:c])
     return lp, li
 
 
@@ -556,6 +564,11 @@ class SymbolicStructure:
         return [self.row_patterns(i)[1] for i in range(self.n)]
 
 
+def _host_threads():
+    import numba
+    return max(1, int(numba.config.NUMBA_NUM_THREADS))
+
+
 def symbolic_from_pattern(n, mp, mc, cfg=None, kernel_override=None, threads=1, method="auto"):
     """symbolic_factorize on the permuted pattern M.
 
@@ -571,7 +584,7 @@ def symbolic_from_pattern(n, mp, mc, cfg=None, kernel_override=None, threads=1, 
         method = "symmetric" if _pattern_symmetric(n, mp, mc) else "general"
     if method == "symmetric":
         parent = _etree(n, mp, mc)
-        lp, li = _row_subtrees(n, mp, mc, parent)
+        lp, li = _row_subtrees(n, mp, mc, parent, _host_threads())
         up, ui = _u_from_l(n, lp, li)
     else:
         lp, li, up, ui = _general_symbolic_chains(n, mp, mc)

@@ -60,3 +60,18 @@ def test_device_matches_golden(name):
         from oracle import numeric as on
         Xo, _ = on.refactor_solve_batch(an, on.factorize(an), g["batch_values"], g["batch_rhs"])
         assert np.abs(X - Xo).max() <= 1e-9 * np.abs(Xo).max()
+
+
+@pytest.mark.parametrize("name", ["c2_64", "c3_48"])
+def test_full_size_nd_permutation_is_pinned(name):
+    """The METIS ND permutation of the full-size c2 / c3 configs equals the committed
+    fixture (tests/golden/make_nd.py), so the full-size parity tests factor the
+    recorded ordering on every machine (ND parity is pinned here, not
+    by the reference, which has no ND)."""
+    from paper_2509_07690_b200 import generators as gen, preprocess as pp
+    z = np.load(os.path.join(HERE, "nd_%s.npz" % name))
+    p = gen.convdiff3d(64) if name == "c2_64" else gen.fem27(48)
+    assert p.A.n == int(z["n"]) and p.A.nnz == int(z["nnz"])
+    ps = pp.static_pivot(p.A)
+    ap, ai = pp.pivoted_sym_pattern(p.A, ps)
+    assert np.array_equal(pp.nd_order(ap, ai).perm, z["perm"].astype(np.int64))

