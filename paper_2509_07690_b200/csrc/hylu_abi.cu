@@ -13,8 +13,8 @@
 namespace hy {
 // kernels (hylu_factor.cu / hylu_batch.cu)
 __global__ void k_anorm(const double *, const double *, int64_t, double *);
-__global__ void k_rows(DevSym, CallP, const int32_t *, int);
-__global__ void k_sn(DevSym, CallP, const int32_t *);
+__global__ void k_rows(DevSym, const CallP *, const int32_t *, int);
+__global__ void k_sn(DevSym, const CallP *, const int32_t *);
 size_t sn_smem_bytes();
 struct SlabDev {
   const int32_t *sl_node;
@@ -28,9 +28,9 @@ struct SlabDev {
   const int8_t *it_own;
   const int32_t *dep_pb;
 };
-__global__ void k_slab(DevSym, CallP, SlabDev, int, int *, int *, int *, int, int, int, int, int);
-__global__ void k_lperm(DevSym, CallP, const int32_t *, int);
-__global__ void k_hub1(DevSym, CallP, DevProg, const int32_t *, double *, int);
+__global__ void k_slab(DevSym, const CallP *, SlabDev, int, int *, int *, int *, int, int, int, int, int);
+__global__ void k_lperm(DevSym, const CallP *, const int32_t *, int);
+__global__ void k_hub1(DevSym, const CallP *, DevProg, const int32_t *, double *, int);
 size_t slab_smem_bytes(int, int, int, int);
 struct FaninDev {
   const int32_t *lu_nodes;
@@ -63,24 +63,28 @@ struct FaninDev {
   const int32_t *src_qb;
   const int32_t *src_m;
 };
-__global__ void k_fi_scatter(DevSym, CallP);
+__global__ void k_fi_scatter(DevSym, const CallP *);
+__global__ void k_call_set(CallP *, CallP);
+__global__ void k_ptr_set(const double **, const double *);
+__global__ void k_call_prep(const CallP *, int, int64_t, int);
+__global__ void k_anorm_p(const CallP *, const double *, int64_t);
 __global__ void k_resid_berr(int, const int64_t *, const int32_t *, const double *, const double *,
                              const double *, double *, unsigned long long *);
 __global__ void k_axpy1(int, double *, const double *);
 
-__global__ void k_fi_lu(DevSym, CallP, FaninDev, int);
-__global__ void k_fi_panel(DevSym, CallP, FaninDev, int);
-__global__ void k_fi_x(DevSym, CallP, FaninDev, int);
-__global__ void k_fi_upd(DevSym, CallP, FaninDev, int, int, int);
-__global__ void k_fi_upd_pk(DevSym, CallP, FaninDev, int, int, int);
-__global__ void k_fi_x_w(DevSym, CallP, FaninDev, int, int);
-__global__ void k_fi_upd_w(DevSym, CallP, FaninDev, int, int);
+__global__ void k_fi_lu(DevSym, const CallP *, FaninDev, int);
+__global__ void k_fi_panel(DevSym, const CallP *, FaninDev, int);
+__global__ void k_fi_x(DevSym, const CallP *, FaninDev, int);
+__global__ void k_fi_upd(DevSym, const CallP *, FaninDev, int, int, int);
+__global__ void k_fi_upd_pk(DevSym, const CallP *, FaninDev, int, int, int);
+__global__ void k_fi_x_w(DevSym, const CallP *, FaninDev, int, int);
+__global__ void k_fi_upd_w(DevSym, const CallP *, FaninDev, int, int);
 size_t fi_upd_smem(int, int);
 size_t fi_upd_tc_smem(int);
 size_t fi_upd_kc_smem();
-__global__ void k_fi_upd_kc(DevSym, CallP, FaninDev, int);
-__global__ void k_fi_upd_kcp(DevSym, CallP, FaninDev, int);
-__global__ void k_fi_upd_tc(DevSym, CallP, FaninDev, int, int);
+__global__ void k_fi_upd_kc(DevSym, const CallP *, FaninDev, int);
+__global__ void k_fi_upd_kcp(DevSym, const CallP *, FaninDev, int);
+__global__ void k_fi_upd_tc(DevSym, const CallP *, FaninDev, int, int);
 size_t hub_smem_bytes();
 int hub_threads();
 __global__ void k_bhat(DevSym, const int32_t *, const double *, double *);
@@ -91,10 +95,10 @@ struct SolveChunk {
   int32_t c0, c1;
   int32_t slot;
 };
-__global__ void k_solve_part(DevSym, const double *, const SolveChunk *, int, const double *, double *, int);
-__global__ void k_fwd_fin(DevSym, const double *, const int32_t *, const int32_t *, const int32_t *, int,
+__global__ void k_solve_part(DevSym, const double *const *, const SolveChunk *, int, const double *, double *, int);
+__global__ void k_fwd_fin(DevSym, const double *const *, const int32_t *, const int32_t *, const int32_t *, int,
                           const double *, double *);
-__global__ void k_bwd_fin(DevSym, const double *, const int32_t *, const int32_t *, const int32_t *, int,
+__global__ void k_bwd_fin(DevSym, const double *const *, const int32_t *, const int32_t *, const int32_t *, int,
                           const double *, double *);
 __global__ void k_bwd(DevSym, const double *, const int32_t *, int, double *);
 struct TaskDesc {
@@ -237,6 +241,14 @@ struct hy_handle {
   int fi_tc = 5;                                     // option "fanin_tc": DMMA update kernels (1/2: per-source k_fi_upd_tc for targets >= 32 rows / all regular items; 3/4: K-concatenated k_fi_upd_kc, same split; 5 (default): k_fi_upd_kcp for the packed items too)
   std::vector<int32_t> fi_smax, fi_mmax;
   int64_t fi_nsrc = -1;                              // source records of the uploaded plan
+  CallP *d_callp = nullptr;                          // per-call parameters (device), see k_call_set
+  cudaStream_t cap_stream = nullptr;                 // graph capture stream
+  cudaGraphExec_t fi_exec = nullptr;                 // level fan-in graph (captured on first use)
+  cudaGraphExec_t sv_exec = nullptr;                 // substitution levels graph
+  int64_t sv_graph_launches = 0;
+  const double **d_fptr = nullptr;                   // factor values of the current solve (device slot)
+  int64_t fi_graph_launches = 0;                     // kernels per graph replay
+  int use_graphs = 1;                                // option "graphs"
   int sm_count = 148;
   // single-instance hub rows (ROWROW path): programs + per-level hub node lists
   bool hub1_ok = false;
@@ -251,6 +263,12 @@ struct hy_handle {
 };
 
 static void free_segments(hy_handle *h);
+static void drop_graph(hy_handle *h) {
+  if (h->fi_exec) cudaGraphExecDestroy(h->fi_exec);
+  if (h->sv_exec) cudaGraphExecDestroy(h->sv_exec);
+  h->fi_exec = nullptr;
+  h->sv_exec = nullptr;
+}
 
 template <class T>
 static int upload(hy_handle *h, T **dst, const T *src, int64_t count) {
@@ -469,6 +487,10 @@ void hy_destroy(hy_handle *h) {
   if (h->d_bf) cudaFree(h->d_bf);
   if (h->d_scratch) cudaFree(h->d_scratch);
   if (h->d_flags) cudaFree(h->d_flags);
+  drop_graph(h);
+  if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
+  if (h->d_callp) cudaFree(h->d_callp);
+  if (h->d_fptr) cudaFree(h->d_fptr);
   if (h->fi_side) cudaStreamDestroy(h->fi_side);
   if (h->fi_ev_lu) cudaEventDestroy(h->fi_ev_lu);
   if (h->fi_ev_pt) cudaEventDestroy(h->fi_ev_pt);
@@ -487,6 +509,11 @@ int64_t hy_launch_count(const hy_handle *h) { return h ? h->launches : -1; }
 
 int hy_set_option(hy_handle *h, const char *name, int64_t value) {
   if (!h || !name) return fail(HY_INVALID_ARGUMENT, "null handle/name");
+  drop_graph(h);   // every option can change the fan-in launch sequence
+  if (std::string(name) == "graphs") {
+    h->use_graphs = value != 0;
+    return HY_OK;
+  }
   if (std::string(name) == "fanin_maps") {
     h->fi_maps = value != 0;
     return HY_OK;
@@ -690,6 +717,7 @@ int hy_upload_slab_plan(hy_handle *h, const hy_slab_plan *d) {
 
 int hy_upload_fanin_plan(hy_handle *h, const hy_fanin_plan *d) {
   if (!h || !h->uploaded || !d) return fail(HY_INVALID_ARGUMENT, "symbolic not uploaded / null");
+  drop_graph(h);
   CK(cudaSetDevice(h->device));
   for (void *p : h->fi_allocs) cudaFree(p);
   h->fi_allocs.clear();
@@ -774,9 +802,8 @@ int hy_upload_fanin_plan(hy_handle *h, const hy_fanin_plan *d) {
 }
 
 
-static int run_fanin(hy_handle *h, const CallP &P, cudaStream_t st) {
-  CK(cudaMemsetAsync(P.F, 0, sizeof(double) * h->stored, st));
-  k_fi_scatter<<<(h->S.n * 32 + 255) / 256, 256, 0, st>>>(h->S, P);
+static int run_fanin(hy_handle *h, const CallP *Pd, cudaStream_t st) {
+  k_fi_scatter<<<(h->S.n * 32 + 255) / 256, 256, 0, st>>>(h->S, Pd);
   h->launches++;
   const int nfl = (int)h->fi_lu.size() - 1;
   for (int l = 0; l < nfl; ++l) {
@@ -795,11 +822,11 @@ static int run_fanin(hy_handle *h, const CallP &P, cudaStream_t st) {
         CK(cudaMalloc((void **)&h->d_hub1_scratch, sizeof(double) * need));
         h->hub1_scratch_cap = need;
       }
-      k_hub1<<<nph, 1024, 0, st>>>(h->S, P, h->prog1, h->d_fi_hubs + h->fi_hub[l], h->d_hub1_scratch,
+      k_hub1<<<nph, 1024, 0, st>>>(h->S, Pd, h->prog1, h->d_fi_hubs + h->fi_hub[l], h->d_hub1_scratch,
                                    h->hub1_slots);
       h->launches++;
     }
-    if (nlu) { k_fi_lu<<<nlu, 256, 0, st>>>(h->S, P, h->fi, (int)h->fi_lu[l]); h->launches++; }
+    if (nlu) { k_fi_lu<<<nlu, 256, 0, st>>>(h->S, Pd, h->fi, (int)h->fi_lu[l]); h->launches++; }
     // the panel TRSM of the level's nodes and the X blocks of their edges both need
     // only the nodes' LU: with fanin_overlap the panel runs on a side stream while the
     // X blocks run on `st`; the update kernels (which need both) wait for it
@@ -835,15 +862,15 @@ static int run_fanin(hy_handle *h, const CallP &P, cudaStream_t st) {
     cudaStream_t sp = sideA && npt ? h->fi_side : st;
     cudaStream_t sw = sideA && !npt ? h->fi_side : st;
     if (npt) {
-      k_fi_panel<<<npt, 256, 64 * 256 * sizeof(double), sp>>>(h->S, P, h->fi, (int)h->fi_pt[l]);
+      k_fi_panel<<<npt, 256, 64 * 256 * sizeof(double), sp>>>(h->S, Pd, h->fi, (int)h->fi_pt[l]);
       h->launches++;
     }
     if (nw) {
-      k_fi_x_w<<<(nw + 7) / 8, 256, 0, sw>>>(h->S, P, h->fi, (int)h->fi_xp[l], nw);
+      k_fi_x_w<<<(nw + 7) / 8, 256, 0, sw>>>(h->S, Pd, h->fi, (int)h->fi_xp[l], nw);
       h->launches++;
     }
     if (nc) {
-      k_fi_x<<<nc, 256, 2 * 64 * 65 * sizeof(double), st>>>(h->S, P, h->fi, xb);
+      k_fi_x<<<nc, 256, 2 * 64 * 65 * sizeof(double), st>>>(h->S, Pd, h->fi, xb);
       h->launches++;
     }
     if (sideA) {
@@ -867,36 +894,36 @@ static int run_fanin(hy_handle *h, const CallP &P, cudaStream_t st) {
       if (npk && h->fi_tc == 5) {
         FaninDev Dp = h->fi;
         if (!h->fi_maps) Dp.src_pos = nullptr;
-        k_fi_upd_kcp<<<npk, 256, fi_upd_kc_smem(), sk>>>(h->S, P, Dp, (int)h->fi_up[l]);
+        k_fi_upd_kcp<<<npk, 256, fi_upd_kc_smem(), sk>>>(h->S, Pd, Dp, (int)h->fi_up[l]);
         h->launches++;
       } else if (npk) {
-        k_fi_upd_pk<<<npk, 256, sm, sk>>>(h->S, P, h->fi, (int)h->fi_up[l], h->fi_smax[l], h->fi_mmax[l]);
+        k_fi_upd_pk<<<npk, 256, sm, sk>>>(h->S, Pd, h->fi, (int)h->fi_up[l], h->fi_smax[l], h->fi_mmax[l]);
         h->launches++;
       }
       if (rs > reg) {
         FaninDev Dw = h->fi;
         if (!h->fi_maps) Dw.src_pos = nullptr;
-        k_fi_upd_w<<<(rs - reg + 7) / 8, 256, 0, st>>>(h->S, P, Dw, reg, rs - reg);
+        k_fi_upd_w<<<(rs - reg + 7) / 8, 256, 0, st>>>(h->S, Pd, Dw, reg, rs - reg);
         h->launches++;
       }
       if (split > rs && h->fi_tc >= 4) {
         FaninDev Dk = h->fi;
         if (!h->fi_maps) Dk.src_pos = nullptr;
-        k_fi_upd_kc<<<split - rs, 256, fi_upd_kc_smem(), st>>>(h->S, P, Dk, rs);
+        k_fi_upd_kc<<<split - rs, 256, fi_upd_kc_smem(), st>>>(h->S, Pd, Dk, rs);
         h->launches++;
       } else if (split > rs && h->fi_tc == 2) {
-        k_fi_upd_tc<<<split - rs, 256, fi_upd_tc_smem(h->fi_smax[l]), st>>>(h->S, P, h->fi, rs, h->fi_smax[l]);
+        k_fi_upd_tc<<<split - rs, 256, fi_upd_tc_smem(h->fi_smax[l]), st>>>(h->S, Pd, h->fi, rs, h->fi_smax[l]);
         h->launches++;
       } else if (split > rs) {
         const int nsm2 = split - rs;
-        k_fi_upd<<<nsm2, 256, sm, st>>>(h->S, P, h->fi, rs, h->fi_smax[l], h->fi_mmax[l]);
+        k_fi_upd<<<nsm2, 256, sm, st>>>(h->S, Pd, h->fi, rs, h->fi_smax[l], h->fi_mmax[l]);
         h->launches++;
       }
       if (nbig && h->fi_tc == 3) {
-        k_fi_upd_kc<<<nbig, 256, fi_upd_kc_smem(), st>>>(h->S, P, h->fi, split);
+        k_fi_upd_kc<<<nbig, 256, fi_upd_kc_smem(), st>>>(h->S, Pd, h->fi, split);
         h->launches++;
       } else if (nbig && h->fi_tc == 1) {
-        k_fi_upd_tc<<<nbig, 256, fi_upd_tc_smem(h->fi_smax[l]), st>>>(h->S, P, h->fi, split, h->fi_smax[l]);
+        k_fi_upd_tc<<<nbig, 256, fi_upd_tc_smem(h->fi_smax[l]), st>>>(h->S, Pd, h->fi, split, h->fi_smax[l]);
         h->launches++;
       }
       if (sideB) {
@@ -913,6 +940,7 @@ int hy_upload_fanin_maps(hy_handle *h, int64_t nsrc, int64_t npos, const int64_t
                          const int8_t *pos, const int64_t *vb, const int32_t *vW, const int32_t *qb,
                          const int32_t *m) {
   if (!h || !h->uploaded || !h->fanin_ok) return fail(HY_INVALID_ARGUMENT, "fan-in plan not uploaded");
+  drop_graph(h);
   if (nsrc < 0 || npos < 0 || (nsrc && (!poff || !vb || !vW || !qb || !m)) || (npos && !pos))
     return fail(HY_INVALID_ARGUMENT, "null source-map arrays");
   // the maps index the uploaded plan's source records one to one, and poff[nsrc]
@@ -937,6 +965,7 @@ int hy_upload_fanin_maps(hy_handle *h, int64_t nsrc, int64_t npos, const int64_t
 
 int hy_upload_hub_programs(hy_handle *h, const hy_row_programs *d) {
   if (!h || !h->uploaded || !d) return fail(HY_INVALID_ARGUMENT, "symbolic not uploaded / null");
+  drop_graph(h);
   CK(cudaSetDevice(h->device));
   for (void *p : h->hub1_allocs) cudaFree(p);
   h->hub1_allocs.clear();
@@ -992,14 +1021,67 @@ int hy_upload_hub_programs(hy_handle *h, const hy_row_programs *d) {
   return HY_OK;
 }
 
+// Level fan-in as one CUDA graph per handle: the launch sequence depends only on the
+// uploaded plan and the options (all per-call pointers are read from the handle's
+// device-resident CallP), so it is captured once and replayed; an option change or
+// a new plan drops it.  Pull-row scratch is sized before capture (no allocation
+// inside a capture).
+
+static int fanin_scratch(hy_handle *h) {
+  int64_t need = 0;
+  for (size_t l = 0; l + 1 < h->fi_hub.size(); ++l)
+    need = std::max<int64_t>(need, (h->fi_hub[l + 1] - h->fi_hub[l]) * (int64_t)h->hub1_slots);
+  if (need > h->hub1_scratch_cap) {
+    if (h->d_hub1_scratch) CK(cudaFree(h->d_hub1_scratch));
+    h->d_hub1_scratch = nullptr;
+    CK(cudaMalloc((void **)&h->d_hub1_scratch, sizeof(double) * need));
+    h->hub1_scratch_cap = need;
+  }
+  return HY_OK;
+}
+
+static int run_fanin_graph(hy_handle *h, cudaStream_t st) {
+  if (!h->fi_exec) {
+    int rc = fanin_scratch(h);
+    if (rc) return rc;
+    if (!h->cap_stream) CK(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
+    if (!h->fi_side) {   // the fork/join stream and events exist before the capture starts
+      CK(cudaStreamCreateWithFlags(&h->fi_side, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&h->fi_ev_lu, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&h->fi_ev_pt, cudaEventDisableTiming));
+    }
+    const int64_t l0 = h->launches;
+    CK(cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal));
+    rc = run_fanin(h, h->d_callp, h->cap_stream);
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(h->cap_stream, &g);
+    h->fi_graph_launches = h->launches - l0;
+    h->launches = l0;
+    if (rc) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    if (e != cudaSuccess) return fail(HY_CUDA_ERROR, std::string("graph capture: ") + cudaGetErrorString(e));
+    e = cudaGraphInstantiate(&h->fi_exec, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) {
+      h->fi_exec = nullptr;
+      return fail(HY_CUDA_ERROR, std::string("graph instantiate: ") + cudaGetErrorString(e));
+    }
+  }
+  CK(cudaGraphLaunch(h->fi_exec, st));
+  h->launches += h->fi_graph_launches;
+  return HY_OK;
+}
+
 static int run_factor(hy_handle *h, const double *d_avals, double eps, const hy_factors *prior,
                       hy_factors *out, cudaStream_t st) {
   if (!h || !h->uploaded) return fail(HY_INVALID_ARGUMENT, "symbolic not uploaded");
   if (!d_avals || !out || !out->d_values || !out->d_inner_perm || !out->d_anorm || !out->d_status)
     return fail(HY_INVALID_ARGUMENT, "null buffer");
+  if (prior && (!prior->d_inner_perm || !prior->d_anorm)) return fail(HY_INVALID_ARGUMENT, "null prior buffer");
   if (eps < 0.0 || eps >= 1.0) return fail(HY_INVALID_ARGUMENT, "perturbation_epsilon outside [0,1)");
   CK(cudaSetDevice(h->device));
-  CK(cudaMemsetAsync(out->d_status, 0, 4 * sizeof(int32_t), st));
   CallP P{};
   P.F = out->d_values;
   P.A = d_avals;
@@ -1010,23 +1092,20 @@ static int run_factor(hy_handle *h, const double *d_avals, double eps, const hy_
   P.pert_rows = out->d_pert_rows;
   P.pert_vals = out->d_pert_vals;
   P.pert_cap = out->d_pert_rows && out->d_pert_vals ? out->pert_cap : 0;
-  if (prior) {
-    P.refactor = 1;
-    P.iperm_prior = prior->d_inner_perm;
-    if (prior->d_anorm != out->d_anorm)
-      CK(cudaMemcpyAsync(out->d_anorm, prior->d_anorm, sizeof(double), cudaMemcpyDeviceToDevice, st));
-    if (prior->d_inner_perm != out->d_inner_perm)
-      CK(cudaMemcpyAsync(out->d_inner_perm, prior->d_inner_perm, sizeof(int32_t) * h->S.n,
-                         cudaMemcpyDeviceToDevice, st));
-  } else {
-    P.refactor = 0;
-    P.iperm_prior = nullptr;
-    CK(cudaMemsetAsync(out->d_inner_perm, 0, sizeof(int32_t) * h->S.n, st));
-    CK(cudaMemsetAsync(out->d_anorm, 0, sizeof(double), st));
-    k_anorm<<<296, 256, 0, st>>>(d_avals, h->S.scale, h->S.nnz, out->d_anorm);
-    h->launches++;
-  }
-  if (h->fanin_ok) return run_fanin(h, P, st);
+  P.refactor = prior ? 1 : 0;
+  P.iperm_prior = prior ? prior->d_inner_perm : nullptr;
+  P.anorm_prior = prior ? prior->d_anorm : nullptr;
+  if (!h->d_callp) CK(cudaMalloc((void **)&h->d_callp, sizeof(CallP)));
+  const CallP *Pd = h->d_callp;
+  // stream-ordered: the previous call's kernels have read their CallP before this
+  // write runs (one stream per handle, include/hylu_b200.h)
+  k_call_set<<<1, 1, 0, st>>>(h->d_callp, P);
+  const int pb = (int)std::min<int64_t>(h->sm_count * 8, (h->stored / 2 + 255) / 256 + 1);
+  k_call_prep<<<h->fanin_ok ? pb : (h->S.n + 255) / 256 + 1, 256, 0, st>>>(Pd, (int)h->S.n, h->stored,
+                                                                         h->fanin_ok ? 1 : 0);
+  k_anorm_p<<<296, 256, 0, st>>>(Pd, h->S.scale, h->S.nnz);
+  h->launches += 3;
+  if (h->fanin_ok) return h->use_graphs ? run_fanin_graph(h, st) : run_fanin(h, Pd, st);
   const Plan &pl = h->fplan;
   if (h->slab_ok) {
     h->slab_epoch++;
@@ -1036,7 +1115,7 @@ static int run_factor(hy_handle *h, const double *d_avals, double eps, const hy_
     const int nr = (int)(pl.rptr[l + 1] - pl.rptr[l]);
     const int ns = (int)(pl.sptr[l + 1] - pl.sptr[l]);
     if (nr) {
-      k_rows<<<(nr + 3) / 4, 128, 0, st>>>(h->S, P, pl.d_rows + pl.rptr[l], nr);
+      k_rows<<<(nr + 3) / 4, 128, 0, st>>>(h->S, Pd, pl.d_rows + pl.rptr[l], nr);
       h->launches++;
     }
     const int nh1 = h->hub1_ok ? (int)(h->hub1_ptr[l + 1] - h->hub1_ptr[l]) : 0;
@@ -1048,24 +1127,24 @@ static int run_factor(hy_handle *h, const double *d_avals, double eps, const hy_
         CK(cudaMalloc((void **)&h->d_hub1_scratch, sizeof(double) * need));
         h->hub1_scratch_cap = need;
       }
-      k_hub1<<<nh1, 1024, 0, st>>>(h->S, P, h->prog1, h->d_hub1 + h->hub1_ptr[l], h->d_hub1_scratch,
+      k_hub1<<<nh1, 1024, 0, st>>>(h->S, Pd, h->prog1, h->d_hub1 + h->hub1_ptr[l], h->d_hub1_scratch,
                                    h->hub1_slots);
       h->launches++;
     }
     if (ns && h->slab_ok) {
       const int nsl = (int)(h->slab_lptr[l + 1] - h->slab_lptr[l]);
       const size_t smem = slab_smem_bytes(h->slab_smax[l], h->slab_mmax[l], h->slab_swmax[l], h->slab_accmax[l]);
-      k_slab<<<nsl, 256, smem, st>>>(h->S, P, h->slab, (int)h->slab_lptr[l], h->d_slab_counters + l,
+      k_slab<<<nsl, 256, smem, st>>>(h->S, Pd, h->slab, (int)h->slab_lptr[l], h->d_slab_counters + l,
                                      h->d_dep_flags, h->d_lu_flags, h->slab_epoch, h->slab_smax[l],
                                      h->slab_mmax[l], h->slab_swmax[l], h->slab_accmax[l]);
       h->launches++;
-      if (!P.refactor) {
+      if (!prior) {
         dim3 g(ns, 4);
-        k_lperm<<<g, 256, 0, st>>>(h->S, P, pl.d_sns + pl.sptr[l], ns);
+        k_lperm<<<g, 256, 0, st>>>(h->S, Pd, pl.d_sns + pl.sptr[l], ns);
         h->launches++;
       }
     } else if (ns) {
-      k_sn<<<ns, 256, h->sn_smem, st>>>(h->S, P, pl.d_sns + pl.sptr[l]);
+      k_sn<<<ns, 256, h->sn_smem, st>>>(h->S, Pd, pl.d_sns + pl.sptr[l]);
       h->launches++;
     }
   }
@@ -1129,14 +1208,10 @@ int hy_axpy(hy_handle *h, double *d_x, const double *d_dx, uintptr_t stream) {
   return HY_OK;
 }
 
-int hy_solve(hy_handle *h, const hy_factors *f, const double *d_b, double *d_x, uintptr_t stream) {
-  if (!h || !h->uploaded) return fail(HY_INVALID_ARGUMENT, "symbolic not uploaded");
-  if (!f || !f->d_values || !d_b || !d_x) return fail(HY_INVALID_ARGUMENT, "null buffer");
-  CK(cudaSetDevice(h->device));
-  cudaStream_t st = (cudaStream_t)stream;
-  const int n = h->S.n;
-  k_bhat<<<(n + 255) / 256, 256, 0, st>>>(h->S, f->d_inner_perm, d_b, h->d_y);
-  h->launches++;
+// Substitution levels as one CUDA graph per handle (captured on first use): the
+// level kernels read the factor-value pointer from the handle's device slot, which
+// k_ptr_set fills per call; b̂ and the output permutation run outside the graph.
+static int solve_levels(hy_handle *h, cudaStream_t st) {
   for (int dir = 0; dir < 2; ++dir) {
     const Plan &pl = dir == 0 ? h->fplan : h->bplan;
     const SolvePlan &sp = dir == 0 ? h->fsolve : h->bsolve;
@@ -1144,20 +1219,56 @@ int hy_solve(hy_handle *h, const hy_factors *f, const double *d_b, double *d_x, 
       const int c = (int)(pl.aptr[l + 1] - pl.aptr[l]);
       const int nch = (int)(sp.cptr[l + 1] - sp.cptr[l]);
       if (nch) {
-        k_solve_part<<<nch, 256, 0, st>>>(h->S, f->d_values, sp.d_chunks + sp.cptr[l], nch, h->d_y,
+        k_solve_part<<<nch, 256, 0, st>>>(h->S, h->d_fptr, sp.d_chunks + sp.cptr[l], nch, h->d_y,
                                          h->d_solve_scratch, dir == 0);
         h->launches++;
       }
       if (dir == 0)
-        k_fwd_fin<<<(c + 3) / 4, 128, 0, st>>>(h->S, f->d_values, pl.d_all + pl.aptr[l],
+        k_fwd_fin<<<(c + 3) / 4, 128, 0, st>>>(h->S, h->d_fptr, pl.d_all + pl.aptr[l],
                                                sp.d_slot0 + pl.aptr[l], sp.d_nslot + pl.aptr[l], c,
                                                h->d_solve_scratch, h->d_y);
       else
-        k_bwd_fin<<<(c + 3) / 4, 128, 0, st>>>(h->S, f->d_values, pl.d_all + pl.aptr[l],
+        k_bwd_fin<<<(c + 3) / 4, 128, 0, st>>>(h->S, h->d_fptr, pl.d_all + pl.aptr[l],
                                                sp.d_slot0 + pl.aptr[l], sp.d_nslot + pl.aptr[l], c,
                                                h->d_solve_scratch, h->d_y);
       h->launches++;
     }
+  }
+  return HY_OK;
+}
+
+int hy_solve(hy_handle *h, const hy_factors *f, const double *d_b, double *d_x, uintptr_t stream) {
+  if (!h || !h->uploaded) return fail(HY_INVALID_ARGUMENT, "symbolic not uploaded");
+  if (!f || !f->d_values || !f->d_inner_perm || !d_b || !d_x) return fail(HY_INVALID_ARGUMENT, "null buffer");
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n = h->S.n;
+  if (!h->d_fptr) CK(cudaMalloc((void **)&h->d_fptr, sizeof(double *)));
+  k_ptr_set<<<1, 1, 0, st>>>(h->d_fptr, f->d_values);
+  k_bhat<<<(n + 255) / 256, 256, 0, st>>>(h->S, f->d_inner_perm, d_b, h->d_y);
+  h->launches += 2;
+  if (h->use_graphs) {
+    if (!h->sv_exec) {
+      if (!h->cap_stream) CK(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
+      const int64_t l0 = h->launches;
+      CK(cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal));
+      solve_levels(h, h->cap_stream);
+      cudaGraph_t g = nullptr;
+      cudaError_t e = cudaStreamEndCapture(h->cap_stream, &g);
+      h->sv_graph_launches = h->launches - l0;
+      h->launches = l0;
+      if (e != cudaSuccess) return fail(HY_CUDA_ERROR, std::string("graph capture: ") + cudaGetErrorString(e));
+      e = cudaGraphInstantiate(&h->sv_exec, g, 0);
+      cudaGraphDestroy(g);
+      if (e != cudaSuccess) {
+        h->sv_exec = nullptr;
+        return fail(HY_CUDA_ERROR, std::string("graph instantiate: ") + cudaGetErrorString(e));
+      }
+    }
+    CK(cudaGraphLaunch(h->sv_exec, st));
+    h->launches += h->sv_graph_launches;
+  } else {
+    solve_levels(h, st);
   }
   k_xout<<<(n + 255) / 256, 256, 0, st>>>(h->S, h->d_y, d_x);
   h->launches++;

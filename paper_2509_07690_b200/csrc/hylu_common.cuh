@@ -35,6 +35,7 @@ struct CallP {
   int32_t *iperm;            // inner_perm [n] (written on factorize, read on refactorize)
   const int32_t *iperm_prior;
   const double *anorm;       // [1]
+  const double *anorm_prior; // [1] (refactorize: copied into anorm by k_call_prep)
   double eps;
   int refactor;
   int32_t *status;           // [4]

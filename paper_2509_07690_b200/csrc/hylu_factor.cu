@@ -28,6 +28,46 @@ __global__ void k_anorm(const double *__restrict__ A, const double *__restrict__
   if ((threadIdx.x & 31) == 0 && m > 0.0) atomic_max_nonneg(out, m);
 }
 
+// ============================================================================ per-call setup
+// The per-call parameters live in device memory (one CallP per handle) so that the
+// launch sequence of a factorization is a fixed CUDA graph: k_call_set writes the
+// call's CallP (stream-ordered, from its by-value argument), the graph's first
+// kernels clear / seed the outputs through it.
+__global__ void k_call_set(CallP *dst, CallP src) { *dst = src; }
+__global__ void k_ptr_set(const double **dst, const double *src) { *dst = src; }
+
+// status[0..3] = 0; factorize: inner_perm = 0, anorm = 0; refactorize: inner_perm =
+// prior inner_perm, anorm = prior anorm; zero_f: F[0:stored) = 0 (level fan-in).
+__global__ void k_call_prep(const CallP *__restrict__ Pd, int n, int64_t stored, int zero_f) {
+  const CallP P = *Pd;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+  if (tid < 4) P.status[tid] = 0;
+  if (tid == 0) *const_cast<double *>(P.anorm) = P.refactor ? *P.anorm_prior : 0.0;
+  for (int64_t i = tid; i < n; i += nth) P.iperm[i] = P.refactor ? P.iperm_prior[i] : 0;
+  if (zero_f && (reinterpret_cast<uintptr_t>(P.F) & 15)) {
+    for (int64_t i = tid; i < stored; i += nth) P.F[i] = 0.0;
+  } else if (zero_f) {
+    double2 *F2 = reinterpret_cast<double2 *>(P.F);
+    const int64_t h = stored >> 1;
+    for (int64_t i = tid; i < h; i += nth) F2[i] = make_double2(0.0, 0.0);
+    if ((stored & 1) && tid == 0) P.F[stored - 1] = 0.0;
+  }
+}
+
+// anorm = max |A·scale| (factorize only; refactorize keeps the prior anorm)
+__global__ void k_anorm_p(const CallP *__restrict__ Pd, const double *__restrict__ scale, int64_t nnz) {
+  if (Pd->refactor) return;
+  const double *A = Pd->A;
+  double m = 0.0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x)
+    m = fmax(m, fabs(A[e] * scale[e]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(HY_FULL, m, o));
+  if ((threadIdx.x & 31) == 0 && m > 0.0) atomic_max_nonneg(const_cast<double *>(Pd->anorm), m);
+}
+
 // ============================================================================ rows
 constexpr int RW_WARPS = 4;
 constexpr int CAPW = 512;
@@ -124,8 +164,9 @@ __device__ void row_task(const DevSym &S, const CallP &P, int u, RowSmem &sm, in
     for (int q = lane; q < W; q += 32) Fu[q] = w[q];
 }
 
-__global__ void __launch_bounds__(RW_WARPS * 32) k_rows(DevSym S, CallP P, const int32_t *nodes,
+__global__ void __launch_bounds__(RW_WARPS * 32) k_rows(DevSym S, const CallP *__restrict__ Pd, const int32_t *nodes,
                                                         int count) {
+  const CallP P = *Pd;
   __shared__ RowSmem sm[RW_WARPS];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int idx = blockIdx.x * RW_WARPS + warp;
@@ -163,7 +204,8 @@ __device__ __forceinline__ void map_cols(const int32_t *vc, int qa, int cnt, con
   }
 }
 
-__global__ void __launch_bounds__(SN_THREADS, 1) k_sn(DevSym S, CallP P, const int32_t *nodes) {
+__global__ void __launch_bounds__(SN_THREADS, 1) k_sn(DevSym S, const CallP *__restrict__ Pd, const int32_t *nodes) {
+  const CallP P = *Pd;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SnSmem &sm = *reinterpret_cast<SnSmem *>(smem_raw);
   const int u = nodes[blockIdx.x];
@@ -535,9 +577,10 @@ __device__ __forceinline__ void hub1_final(const CallP &P, int64_t kd, double *w
   w[p] = acc;
 }
 
-__global__ void __launch_bounds__(HUB1_THREADS) k_hub1(DevSym S, CallP P, DevProg R,
+__global__ void __launch_bounds__(HUB1_THREADS) k_hub1(DevSym S, const CallP *__restrict__ Pd, DevProg R,
                                                        const int32_t *nodes, double *scratch,
                                                        int max_slots) {
+  const CallP P = *Pd;
   const int u = nodes[blockIdx.x];
   const int tid = threadIdx.x;
   const int64_t i = S.first[u];
@@ -592,8 +635,9 @@ struct SolveChunk {
   int32_t slot;       // scratch slot (x 64 rows)
 };
 
-__global__ void k_solve_part(DevSym S, const double *F, const SolveChunk *ch, int count,
+__global__ void k_solve_part(DevSym S, const double *const *Fp, const SolveChunk *ch, int count,
                              const double *y, double *scratch, int fwd) {
+  const double *F = *Fp;   // factor values of this call (device-resident pointer: graph replay)
   const int j = blockIdx.x;
   if (j >= count) return;
   const SolveChunk c = ch[j];
@@ -674,8 +718,9 @@ __device__ __forceinline__ void offblock_dots(const double *Fu, int W, const int
   }
 }
 
-__global__ void k_fwd_fin(DevSym S, const double *F, const int32_t *nodes, const int32_t *slot0,
+__global__ void k_fwd_fin(DevSym S, const double *const *Fp, const int32_t *nodes, const int32_t *slot0,
                           const int32_t *nslot, int count, const double *scratch, double *y) {
+  const double *F = *Fp;   // factor values of this call (device-resident pointer: graph replay)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int idx = blockIdx.x * (blockDim.x >> 5) + warp;
   if (idx >= count) return;
@@ -725,8 +770,9 @@ __global__ void k_fwd_fin(DevSym S, const double *F, const int32_t *nodes, const
 }
 
 // backward finish: z_t = (y_t - sum(partials) - sum_{tt>t} U[t][tt] z_tt) / U[t][t]
-__global__ void k_bwd_fin(DevSym S, const double *F, const int32_t *nodes, const int32_t *slot0,
+__global__ void k_bwd_fin(DevSym S, const double *const *Fp, const int32_t *nodes, const int32_t *slot0,
                           const int32_t *nslot, int count, const double *scratch, double *y) {
+  const double *F = *Fp;   // factor values of this call (device-resident pointer: graph replay)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int idx = blockIdx.x * (blockDim.x >> 5) + warp;
   if (idx >= count) return;

@@ -65,7 +65,8 @@ constexpr int FXLD = 65;
 
 // ---------------------------------------------------------------------------- scatter
 // warp per M row: physical row = inverse of the prior inner_perm on refactorize
-__global__ void k_fi_scatter(DevSym S, CallP P) {
+__global__ void k_fi_scatter(DevSym S, const CallP *__restrict__ Pd) {
+  const CallP P = *Pd;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= S.n) return;
   const int i = warp;
@@ -88,7 +89,8 @@ __global__ void k_fi_scatter(DevSym S, CallP P) {
 }
 
 // ---------------------------------------------------------------------------- LU
-__global__ void __launch_bounds__(FI_THREADS) k_fi_lu(DevSym S, CallP P, FaninDev D, int base) {
+__global__ void __launch_bounds__(FI_THREADS) k_fi_lu(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base) {
+  const CallP P = *Pd;
   __shared__ double B[64 * FXLD];
   __shared__ int perm[64];
   const int u = D.lu_nodes[base + blockIdx.x];
@@ -203,7 +205,8 @@ __device__ __forceinline__ void panel_trsm_col(double *tl, const double *Lb, int
   }
 }
 
-__global__ void __launch_bounds__(FI_THREADS) k_fi_panel(DevSym S, CallP P, FaninDev D, int base) {
+__global__ void __launch_bounds__(FI_THREADS) k_fi_panel(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base) {
+  const CallP P = *Pd;
   extern __shared__ __align__(16) double tl[];   // s x (c1-c0), stride PANEL
   __shared__ double Lb[64 * FXLD];
   __shared__ int perm[64];
@@ -253,7 +256,8 @@ __global__ void __launch_bounds__(FI_THREADS) k_fi_panel(DevSym S, CallP P, Fani
 
 // ---------------------------------------------------------------------------- X blocks
 // X = T[:, pb0 .. pb0+m) · U_bb⁻¹ in place; 4 threads per target row.
-__global__ void __launch_bounds__(FI_THREADS) k_fi_x(DevSym S, CallP P, FaninDev D, int base) {
+__global__ void __launch_bounds__(FI_THREADS) k_fi_x(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base) {
+  const CallP P = *Pd;
   extern __shared__ __align__(16) double xsm[];
   double *Ub = xsm;
   double *Xt = xsm + 64 * FXLD;
@@ -336,7 +340,8 @@ __global__ void __launch_bounds__(FI_THREADS) k_fi_x(DevSym S, CallP P, FaninDev
 // same operation sequence as k_fi_x (x_a = w_a / U_aa, then w_b -= x_a U_ab for
 // b > a, skipped when x_a == 0).
 constexpr int XW_M = 8;
-__global__ void __launch_bounds__(FI_THREADS) k_fi_x_w(DevSym S, CallP P, FaninDev D, int base, int count) {
+__global__ void __launch_bounds__(FI_THREADS) k_fi_x_w(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base, int count) {
+  const CallP P = *Pd;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int jj = blockIdx.x * (FI_THREADS / 32) + warp;
   if (jj >= count) return;
@@ -385,7 +390,8 @@ __global__ void __launch_bounds__(FI_THREADS) k_fi_x_w(DevSym S, CallP P, FaninD
 // per-element sequence of k_fi_upd.  The tile lives in a per-warp shared buffer.
 constexpr int UW_ROWS = 4;
 constexpr int UW_TILE = 64;   // == FI_TILE
-__global__ void __launch_bounds__(FI_THREADS) k_fi_upd_w(DevSym S, CallP P, FaninDev D, int base, int count) {
+__global__ void __launch_bounds__(FI_THREADS) k_fi_upd_w(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base, int count) {
+  const CallP P = *Pd;
   __shared__ double tile_s[FI_THREADS / 32][UW_ROWS * UW_TILE];
   __shared__ int tcol_s[FI_THREADS / 32][UW_TILE];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -477,8 +483,9 @@ __device__ __forceinline__ void fi_steps(const double *Xs, const double *Ut, int
   }
 }
 
-__global__ void __launch_bounds__(FI_THREADS) k_fi_upd(DevSym S, CallP P, FaninDev D, int base,
+__global__ void __launch_bounds__(FI_THREADS) k_fi_upd(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base,
                                                        int Smax, int Mmax) {
+  const CallP P = *Pd;
   extern __shared__ __align__(16) double fs[];
   __shared__ int tcol[FI_TILE];
   __shared__ int spos[FI_TILE];
@@ -577,8 +584,9 @@ __global__ void __launch_bounds__(FI_THREADS) k_fi_upd(DevSym S, CallP P, FaninD
 // handles many small sources per synchronisation round and the whole item is
 // accumulated in registers (K-aggregated over all of its sources) before the
 // tile is updated once.
-__global__ void __launch_bounds__(FI_THREADS) k_fi_upd_pk(DevSym S, CallP P, FaninDev D, int base,
+__global__ void __launch_bounds__(FI_THREADS) k_fi_upd_pk(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base,
                                                        int Smax, int Mmax) {
+  const CallP P = *Pd;
   extern __shared__ __align__(16) double fs[];
   __shared__ int tcol[FI_TILE];
   // slice descriptors of the current batch (built by warp 0)
@@ -782,8 +790,9 @@ __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-__global__ void __launch_bounds__(FI_THREADS, 3) k_fi_upd_tc(DevSym S, CallP P, FaninDev D, int base,
+__global__ void __launch_bounds__(FI_THREADS, 3) k_fi_upd_tc(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base,
                                                           int Smax) {
+  const CallP P = *Pd;
   extern __shared__ __align__(16) double fs[];
   __shared__ int tcol[FI_TILE];
   __shared__ int spos[FI_TILE];
@@ -938,7 +947,8 @@ __device__ __forceinline__ void cp_async8z(double *smem_dst, const double *gsrc,
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(gsrc), "r"(n) : "memory");
 }
 
-__global__ void __launch_bounds__(FI_THREADS, KC_MINB_DEF) k_fi_upd_kc(DevSym S, CallP P, FaninDev D, int base) {
+__global__ void __launch_bounds__(FI_THREADS, KC_MINB_DEF) k_fi_upd_kc(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base) {
+  const CallP P = *Pd;
   extern __shared__ __align__(16) double fs[];
   __shared__ int tcol[FI_TILE];
   __shared__ int8_t cidx[FI_TILE];     // tile column -> compact column (-1: untouched)
@@ -1209,7 +1219,8 @@ __global__ void __launch_bounds__(FI_THREADS, KC_MINB_DEF) k_fi_upd_kc(DevSym S,
 // own chunks), so a synchronisation round covers several sources; split-K parts of
 // outlier items publish partial tiles (tile column space) and the last part adds
 // them in part order.  Replaces k_fi_upd_pk (fanin_tc=5): c2 350 -> 340 ms.
-__global__ void __launch_bounds__(FI_THREADS, KC_MINB_DEF) k_fi_upd_kcp(DevSym S, CallP P, FaninDev D, int base) {
+__global__ void __launch_bounds__(FI_THREADS, KC_MINB_DEF) k_fi_upd_kcp(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base) {
+  const CallP P = *Pd;
   extern __shared__ __align__(16) double fs[];
   __shared__ int tcol[FI_TILE];
   __shared__ int8_t cidx[FI_TILE];     // tile column -> compact column (-1: untouched)

@@ -49,8 +49,9 @@ __device__ __forceinline__ void st_rel(int *p, int v) {
 }
 
 __global__ void __launch_bounds__(SLAB_THREADS, 1)
-    k_slab(DevSym S, CallP P, SlabDev D, int slab_base, int *counter, int *dep_flags, int *lu_flags,
+    k_slab(DevSym S, const CallP *__restrict__ Pd, SlabDev D, int slab_base, int *counter, int *dep_flags, int *lu_flags,
            int epoch, int Smax, int Mmax, int SWmax, int ACCmax) {
+  const CallP P = *Pd;
   extern __shared__ __align__(16) double smd[];
   __shared__ int s_ticket;
   __shared__ int s_pinv[64];
@@ -324,7 +325,8 @@ __global__ void __launch_bounds__(SLAB_THREADS, 1)
 }
 
 // Apply each supernode's pivot permutation to its L-union columns (after the level).
-__global__ void k_lperm(DevSym S, CallP P, const int32_t *sns, int count) {
+__global__ void k_lperm(DevSym S, const CallP *__restrict__ Pd, const int32_t *sns, int count) {
+  const CallP P = *Pd;
   __shared__ double tile[64][65];
   __shared__ int perm[64];
   __shared__ int ident;
