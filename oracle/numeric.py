@@ -530,7 +530,12 @@ def batch_refactor_solve(n, first, kind, colptr, cols, nl, valoff, dptr, deps, n
                      rhs[b], X[b])
 
 
-def refactor_solve_batch(an, prior, values, rhs, mode=None):
+def refactor_solve_batch(an, prior, values, rhs, mode=None, refine_perturbed=True, cfg=None,
+                         reports=None):
+    """refactorize + solve per instance.  With
+    ``refine_perturbed`` every instance whose perturbation log is non-empty gets the
+    automatic iterative_refinement of SPEC.md:492,499-507 (``refine`` on that
+    instance's factors and matrix); ``reports`` (a dict) receives them."""
     s = an.symbolic
     B = values.shape[0]
     X = np.empty((B, s.n))
@@ -540,4 +545,13 @@ def refactor_solve_batch(an, prior, values, rhs, mode=None):
                          an.vmap.mrow_src, an.vmap.colpos.astype(np.int64), an.vmap.scale,
                          prior.inner_perm, 1e-8 * prior.anorm, an.pivot_scale.dr,
                          an.pivot_scale.dc, an.ordering.perm, np.ascontiguousarray(rhs), X, npert)
+    if refine_perturbed:
+        from paper_2509_07690_b200._ref import SolverConfig
+        cfg = cfg or an.config or SolverConfig()
+        for b in np.flatnonzero(npert > 0):
+            fac = factorize(an, values=values[b], mode=mode, prior=prior)
+            Ab = an.A.with_values(np.ascontiguousarray(values[b]))
+            X[b], rep = refine(an, fac, Ab, np.ascontiguousarray(rhs[b], np.float64), X[b].copy(), cfg)
+            if reports is not None:
+                reports[int(b)] = rep
     return X, npert

@@ -76,6 +76,13 @@ class NumericFactors:
     _bufs: dict = field(repr=False, default=None)
     _desc: object = field(repr=False, default=None)
     _ctx: object = field(repr=False, default=None)
+    kernel_mode: object = None   # the mode (maximum tier) this factorization ran with
+
+    def routing(self):
+        """Device dispatch of this factorization: see
+        ``schedule.device_routing``."""
+        from .schedule import device_routing
+        return device_routing(self.symbolic, self.kernel_mode)
 
     def host_values(self):
         return self.values.cpu().numpy()
@@ -130,15 +137,18 @@ def _check_pattern(an, A):
         raise errors.PatternMismatch("refactorization input pattern differs from the analyzed pattern")
 
 
-def _apply_mode(an, opts):
-    if opts.kernel_override is None:
-        return
+def _apply_mode(ctx, an, opts):
+    """FactorOptions.kernel_override ("an explicit user override always
+    wins"): the mode (maximum tier) of this call, set on the handle
+    before the launch; None = the analysis' kernel_mode.  Returns the mode."""
+    from .device import check
     mode = opts.kernel_override
-    mode = KernelMode.parse(mode) if isinstance(mode, str) else KernelMode(mode)
-    if mode != an.symbolic.kernel_mode:
-        raise ValueError("kernel_override must be fixed at analyze time "
-                         "(analyze(..., kernel_override=...)); got %s for a %s analysis"
-                         % (mode.name, an.symbolic.kernel_mode.name))
+    if mode is None:
+        mode = an.symbolic.kernel_mode
+    else:
+        mode = KernelMode.parse(mode) if isinstance(mode, str) else KernelMode(mode)
+    check(ctx.lib.hy_set_kernel_mode(ctx.h, int(mode)))
+    return mode
 
 
 def _device_values(ctx, vals, what="values"):
@@ -192,15 +202,15 @@ def _finish(ctx, an, bufs, desc, check_breakdown=True):
     pert = list(zip(rows[o].tolist(), vals[o].tolist()))
     anorm = float(bufs["anorm"].cpu().item())
     return NumericFactors(an.symbolic, bufs["values"], bufs["inner_perm"], anorm, pert,
-                          bufs, desc, ctx)
+                          bufs, desc, ctx, KernelMode(int(desc.kernel_mode)))
 
 
 def factorize_analysis(an, values=None, opts=None, stream=None):
     """factorize on an ``Analysis`` (values default to the analyzed A's)."""
     import torch
     opts = opts or FactorOptions()
-    _apply_mode(an, opts)
     ctx = _context(an, opts.device)
+    _apply_mode(ctx, an, opts)
     d_vals = _device_values(ctx, an.A.values if values is None else values)
     bufs, desc = ctx.alloc_factors()
     from .device import check
@@ -233,6 +243,10 @@ def refactorize(A_new, prior, opts=None, stream=None):
     else:
         _check_pattern(an, A_new)
         d_vals = _device_values(ctx, A_new.values)
+    if opts.kernel_override is None:
+        opts = FactorOptions(prior.kernel_mode, opts.perturbation_epsilon, opts.threads,
+                             opts.pivot_tolerance, opts.device)
+    _apply_mode(ctx, an, opts)
     bufs, desc = ctx.alloc_factors()
     cur = _enter_stream(ctx, stream, [d_vals, prior.values, prior.inner_perm, *bufs.values()])
     check(ctx.lib.hy_refactorize(ctx.h, d_vals.data_ptr(), float(opts.perturbation_epsilon),
@@ -344,7 +358,13 @@ class BatchedRefactorizer:
                                        HUB_STEPS if hub_steps is None else hub_steps)
         self.ctx.upload_programs(self.programs)
 
-    def run(self, d_vals, d_rhs, d_x=None, d_npert=None, stream=None):
+    def run(self, d_vals, d_rhs, d_x=None, d_npert=None, stream=None, refine=True, config=None):
+        """Refactorize + solve B instances (device buffers).  ``refine=True`` (SPEC.md:492:
+        refinement runs automatically when perturbation fired): waits for the batch,
+        and instances with a nonzero perturbation count get ``refine``; their reports
+        land in ``self.reports`` ({instance: RefinementReport}).  ``refine=False``
+        keeps the call asynchronous; the caller then checks ``d_npert`` and calls
+        ``refine`` before the next batched call on this handle."""
         import torch
         from .device import check
         B = d_vals.shape[0]
@@ -359,9 +379,92 @@ class BatchedRefactorizer:
             self.ctx.h, B, d_vals.data_ptr(), float(self.eps), self.prior._desc, d_npert.data_ptr(),
             d_rhs.data_ptr(), sh))
         check(self.ctx.lib.hy_solve_batched(self.ctx.h, B, None, d_x.data_ptr(), sh))
+        self.reports = {}
+        if refine:
+            self.reports = self.refine(d_vals, d_rhs, d_x, d_npert, config, stream)
         return d_x, d_npert
 
-    def run_host(self, h_vals, h_rhs, h_x, h_npert=None, chunks=8, sizes=None, pipelined=False):
+    def refine(self, d_vals, d_rhs, d_x, d_npert, config=None, stream=None):
+        """iterative_refinement for every instance of the batch just
+        factorized on this handle whose perturbation count is nonzero, on the device:
+        per iteration one masked batched residual + backward error pass
+        (``hy_residual_batched``, bitwise the reference's matrix.py loops per
+        instance), one batched substitution with the residuals as right-hand sides
+        (``hy_solve_batched``), one masked x + dx; per-instance stop rules as the
+        single-instance loop (tolerance, max iterations, stagnation).  Only the B
+        backward errors cross to the host per iteration.  Returns
+        {instance: RefinementReport}; ``d_x`` is updated in place."""
+        import torch
+        from .device import check
+        cfg = config or SolverConfig()
+        ctx = self.ctx
+        dev = ctx.device
+        B = d_vals.shape[0]
+        st = stream or torch.cuda.current_stream(dev)
+        st.synchronize()
+        npert = d_npert.cpu().numpy()
+        todo = np.flatnonzero(npert > 0)
+        if len(todo) == 0:
+            return {}
+        ctx.ensure_matrix(ctx.analysis.A)
+        sh = ctx.stream_handle(st)
+        lib = ctx.lib
+        with torch.cuda.stream(st):
+            r = torch.zeros_like(d_x)
+            dx = torch.zeros_like(d_x)
+            xn = torch.empty_like(d_x)
+            berr = torch.zeros(B, dtype=torch.float64, device=dev)
+            mask_h = np.zeros(B, np.int32)
+            mask = torch.zeros(B, dtype=torch.int32, device=dev)
+
+        def set_mask(idx):
+            mask_h[:] = 0
+            mask_h[idx] = 1
+            mask.copy_(torch.from_numpy(mask_h))
+
+        def resid(x):
+            check(lib.hy_residual_batched(ctx.h, B, d_vals.data_ptr(), x.data_ptr(), d_rhs.data_ptr(),
+                                          r.data_ptr(), berr.data_ptr(), mask.data_ptr(), sh))
+            return berr.cpu().numpy()
+
+        with torch.cuda.stream(st):
+            set_mask(todo)
+            e0 = resid(d_x)
+            errs = {int(b): [float(e0[b])] for b in todo}
+            iters = {int(b): 0 for b in todo}
+            conv = {int(b): bool(e0[b] <= cfg.refine_tolerance) for b in todo}
+            active = [int(b) for b in todo if not conv[int(b)]]
+            while active:
+                set_mask(active)
+                check(lib.hy_solve_batched(ctx.h, B, r.data_ptr(), dx.data_ptr(), sh))
+                check(lib.hy_axpy_batched(ctx.h, B, xn.data_ptr(), d_x.data_ptr(), dx.data_ptr(),
+                                          mask.data_ptr(), sh))
+                e = resid(xn)
+                accept, nxt = [], []
+                for b in active:
+                    eb, last = float(e[b]), errs[b][-1]
+                    iters[b] += 1
+                    if eb > cfg.refine_stagnation_factor * last:
+                        if eb < last:
+                            accept.append(b)
+                            errs[b].append(eb)
+                        continue
+                    accept.append(b)
+                    errs[b].append(eb)
+                    conv[b] = eb <= cfg.refine_tolerance
+                    if not conv[b] and iters[b] < cfg.max_refine_iters:
+                        nxt.append(b)
+                if accept:
+                    set_mask(accept)
+                    check(lib.hy_axpy_batched(ctx.h, B, d_x.data_ptr(), xn.data_ptr(), None,
+                                              mask.data_ptr(), sh))
+                # a continuing instance was accepted: r already holds b - A x_new
+                active = nxt
+            st.synchronize()
+        return {b: RefinementReport(iters[b], errs[b], bool(conv[b])) for b in errs}
+
+    def run_host(self, h_vals, h_rhs, h_x, h_npert=None, chunks=8, sizes=None, pipelined=False,
+                 refine=True):
         """Host buffers in, host buffers out, copies overlapped with compute.
 
         The batch is cut into ``chunks`` contiguous slabs (multiples of 32
@@ -375,7 +478,11 @@ class BatchedRefactorizer:
         the call returns without that wait, so the next call's H2D copies start
         while this call's last chunks still compute — each chunk's device buffers
         are reused only after their previous compute / D2H finished (per-chunk
-        events).  Call ``host_wait()`` before reading ``h_x``."""
+        events).  Call ``host_wait()`` before reading ``h_x``.
+
+        ``refine`` (needs ``h_npert``): perturbed instances are refined once the
+        copies are done — at the end of the call (``pipelined=False``) or in
+        ``host_wait()`` (``pipelined=True``); see ``_fixup_host``."""
         import torch
         B = h_vals.shape[0]
         dev = self.ctx.device
@@ -418,7 +525,7 @@ class BatchedRefactorizer:
             s_cmp.wait_event(ev_in)
             if self._ev_out[k] is not None:
                 s_cmp.wait_event(self._ev_out[k])
-            self.run(dv, dr, dx, dn, s_cmp)
+            self.run(dv, dr, dx, dn, s_cmp, refine=False)
             ev_c = torch.cuda.Event()
             ev_c.record(s_cmp)
             self._ev_cmp[k] = ev_c
@@ -430,13 +537,42 @@ class BatchedRefactorizer:
                 ev_o = torch.cuda.Event()
                 ev_o.record(s_out)
                 self._ev_out[k] = ev_o
+        self._pending = (h_vals, h_rhs, h_x, h_npert) if (refine and h_npert is not None) else None
         if not pipelined:
             cur.wait_stream(s_out)
+            self._fixup_host()
         return h_x, h_npert
 
-    def host_wait(self, stream=None):
-        """Make ``stream`` (default: current) wait for every pending run_host copy."""
+    def _fixup_host(self):
+        """Automatic refinement for run_host: once the copies are done,
+        instances whose perturbation count is nonzero are refactorized again as one
+        sub-batch on the device and refined (``run(..., refine=True)``); their
+        solutions replace the rows of ``h_x``.  Reports go to ``self.reports``."""
         import torch
+        pend, self._pending = getattr(self, "_pending", None), None
+        self.reports = {}
+        if pend is None:
+            return
+        h_vals, h_rhs, h_x, h_npert = pend
+        self._streams[2].synchronize()
+        idx = np.flatnonzero(h_npert.numpy() > 0)
+        if len(idx) == 0:
+            return
+        dev = self.ctx.device
+        ti = torch.from_numpy(idx)
+        dv = h_vals[ti].to(dev)
+        dr = h_rhs[ti].to(dev)
+        dx, _ = self.run(dv, dr)
+        h_x[ti] = dx.cpu()
+        self.reports = {int(idx[k]): rep for k, rep in self.reports.items()}
+
+    def host_wait(self, stream=None):
+        """Make ``stream`` (default: current) wait for every pending run_host copy.  If
+        the last run_host call asked for refinement (``h_npert`` given), this first
+        waits for its copies and refines the perturbed instances (``_fixup_host``)."""
+        import torch
+        if getattr(self, "_pending", None) is not None:
+            self._fixup_host()
         if getattr(self, "_streams", None):
             (stream or torch.cuda.current_stream(self.ctx.device)).wait_stream(self._streams[2])
 
@@ -451,12 +587,15 @@ class BatchedRefactorizer:
 
 def refactorize_solve_batched(values, prior, rhs, opts=None, hub_steps=None):
     """Host-facing batched call: values [B, nnz], rhs [B, n] (numpy or CUDA tensors)
-    → (x [B, n] numpy, perturbation counts [B])."""
+    → (x [B, n] numpy, perturbation counts [B]).  Perturbed instances are refined
+    automatically; their RefinementReports are left in
+    ``refactorize_solve_batched.last_reports`` ({instance: report})."""
     import torch
     opts = opts or FactorOptions()
     br = BatchedRefactorizer(prior, opts.perturbation_epsilon, hub_steps)
     dev = br.ctx.device
     dv = values if isinstance(values, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(values)).to(dev)
     dr = rhs if isinstance(rhs, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(rhs)).to(dev)
-    x, npert = br.run(dv, dr)
+    x, npert = br.run(dv, dr, refine=True)
+    refactorize_solve_batched.last_reports = br.reports
     return x.cpu().numpy(), npert.cpu().numpy()

@@ -46,6 +46,7 @@ class SolveReport:
     refinement_iterations: int = 0
     perturbation_count: int = 0
     threads: int = 1
+    device_routing: dict = field(default_factory=dict)   # B200 extension: schedule.device_routing
 
 
 def generate_rhs(mode, n):
@@ -179,7 +180,7 @@ def _run(args, cfg, name):
         repeat_times_seconds=repeats,
         backward_error_final=float(refmatrix.backward_error(A_last, x, b)),
         refinement_iterations=int(rep.iterations), perturbation_count=len(f_last.perturbed),
-        threads=int(args.threads))
+        threads=int(args.threads), device_routing=f_last.routing())
     text = json.dumps(asdict(report), indent=1)
     if args.report:
         with open(args.report, "w") as fh:

@@ -42,6 +42,8 @@ struct CallP {
   int64_t *pert_rows;
   double *pert_vals;
   int64_t pert_cap;
+  int chain;                 // 1: row-row operation order (ROWROW tier): each source row's
+                             // update subtracted from the running target value
 };
 
 // Per-call parameters (batched path).

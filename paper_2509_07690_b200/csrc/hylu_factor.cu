@@ -865,4 +865,47 @@ __global__ void k_axpy1(int n, double *x, const double *dx) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     x[i] = __dadd_rn(x[i], dx[i]);
 }
+
+// Batched k_resid_berr: blockIdx.y = instance (skipped when mask[b] == 0); values,
+// x, b, r row-major [B][nnz] / [B][n]; one backward error per instance.
+__global__ void k_resid_berr_b(int n, int64_t nnz, const int64_t *row_ptr, const int32_t *col_idx,
+                               const double *vals, const double *x, const double *b, double *r,
+                               unsigned long long *berr_bits, const int32_t *mask) {
+  const int64_t inst = blockIdx.y;
+  if (mask && !mask[inst]) return;
+  const double *v = vals + inst * nnz;
+  const double *xi = x + inst * n;
+  const double *bi_ = b + inst * n;
+  double worst = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double acc = 0.0, mag = 0.0;
+    for (int64_t t = row_ptr[i]; t < row_ptr[i + 1]; ++t) {
+      const double a = v[t];
+      const double xa = xi[col_idx[t]];
+      acc = __dadd_rn(acc, __dmul_rn(a, xa));
+      mag = __dadd_rn(mag, __dmul_rn(fabs(a), fabs(xa)));
+    }
+    const double bi = bi_[i];
+    if (r) r[inst * n + i] = __dsub_rn(bi, acc);
+    const double num = fabs(__dsub_rn(bi, acc));
+    const double den = __dadd_rn(mag, fabs(bi));
+    if (den != 0.0) {
+      const double rel = __ddiv_rn(num, den);
+      if (rel > worst) worst = rel;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) worst = fmax(worst, __shfl_xor_sync(HY_FULL, worst, o));
+  if ((threadIdx.x & 31) == 0 && worst > 0.0)
+    atomicMax(berr_bits + inst, (unsigned long long)__double_as_longlong(worst));
+}
+
+// y[b] = x[b] (+ dx[b]) for the instances with mask[b] != 0 (all when mask == NULL)
+__global__ void k_axpy_b(int n, double *y, const double *x, const double *dx, const int32_t *mask) {
+  const int64_t inst = blockIdx.y;
+  if (mask && !mask[inst]) return;
+  const int64_t o = inst * n;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    y[o + i] = dx ? __dadd_rn(x[o + i], dx[o + i]) : x[o + i];
+}
 }  // namespace hy

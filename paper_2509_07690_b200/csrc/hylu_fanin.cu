@@ -414,6 +414,7 @@ __global__ void __launch_bounds__(FI_THREADS) k_fi_upd_w(DevSym S, const CallP *
   }
   __syncwarp();
   const bool maps = D.src_pos != nullptr;   // host-precomputed positions / metadata
+  const bool chain = P.chain != 0;
   for (int64_t z = D.up_ptr[j]; z < D.up_ptr[j + 1]; ++z) {
     const int q0 = D.src_q0[z];
     const int nq = D.src_q1[z] - q0;
@@ -439,18 +440,23 @@ __global__ void __launch_bounds__(FI_THREADS) k_fi_upd_w(DevSym S, const CallP *
     for (int q = lane; q < nq; q += 32) {
       const int pos = maps ? (int)D.src_pos[D.src_poff[z] + q]
                            : lower_bound_i32(tcol, 0, tw, S.cols[vc0 + qbase + q]);
+      // sup-row order: c = sum_a x_a u_a, then one subtraction; row-row order (chain):
+      // the running target value minus each source row's product in turn
       double c[UW_ROWS];
 #pragma unroll
-      for (int t = 0; t < UW_ROWS; ++t) c[t] = 0.0;
+      for (int t = 0; t < UW_ROWS; ++t) c[t] = (chain && t < s) ? acc[t * UW_TILE + pos] : 0.0;
       for (int a = 0; a < m; ++a) {
         const double u = vb[(int64_t)(tb0 + a) * vW + qbase + q];
 #pragma unroll
         for (int t = 0; t < UW_ROWS; ++t)
-          if (t < s) c[t] = fma(Pm[(int64_t)t * W + pb0 + a], u, c[t]);
+          if (t < s) {
+            const double x = Pm[(int64_t)t * W + pb0 + a];
+            c[t] = fma(chain ? -x : x, u, c[t]);
+          }
       }
 #pragma unroll
       for (int t = 0; t < UW_ROWS; ++t)
-        if (t < s) acc[t * UW_TILE + pos] -= c[t];
+        if (t < s) acc[t * UW_TILE + pos] = chain ? c[t] : acc[t * UW_TILE + pos] - c[t];
     }
     __syncwarp();
   }
@@ -1079,11 +1085,21 @@ __global__ void __launch_bounds__(FI_THREADS, KC_MINB_DEF) k_fi_upd_kc(DevSym S,
   ra[1] = !narrow && wr0 + 8 < s;
 #pragma unroll
   for (int b = 0; b < 4; ++b) ca[b] = wc0 + 8 * b < nu;
+  // row-row order (chain): the accumulators start at the target's values and the
+  // multipliers enter negated, so DMMA's chained FMAs subtract every source row's
+  // product from the running value in (source, row) order; else they start at 0
+  // and the sum is subtracted once in the epilogue
+  const bool chain = P.chain != 0 && true;
   double d[2][4][2];
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) d[a][b][0] = d[a][b][1] = 0.0;
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int t = wr0 + 8 * a + lr, c = wc0 + 8 * b + 2 * kq + e;
+        d[a][b][e] = (chain && ra[a] && t < s && ca[b] && c < nu) ? Pm[(int64_t)t * W + c0 + ucol[c]] : 0.0;
+      }
 
   for (int64_t zb0 = zb; zb0 < ze; zb0 += KC_NSB) {
     const int nsb = (int)(ze - zb0 < KC_NSB ? ze - zb0 : KC_NSB);
@@ -1179,7 +1195,10 @@ __global__ void __launch_bounds__(FI_THREADS, KC_MINB_DEF) k_fi_upd_kc(DevSym S,
         for (int k = 0; k < kc4; k += 4) {
           double av[2], bv[4];
 #pragma unroll
-          for (int a = 0; a < 2; ++a) av[a] = ra[a] ? X[(wr0 + 8 * a + lr) * KC_XLD + k + kq] : 0.0;
+          for (int a = 0; a < 2; ++a) {
+            const double xv = ra[a] ? X[(wr0 + 8 * a + lr) * KC_XLD + k + kq] : 0.0;
+            av[a] = chain ? -xv : xv;
+          }
 #pragma unroll
           for (int b = 0; b < 4; ++b) bv[b] = cb[b] ? U[(k + kq) * KC_ULD + wc0 + 8 * b + lr] : 0.0;
 #pragma unroll
@@ -1207,7 +1226,7 @@ __global__ void __launch_bounds__(FI_THREADS, KC_MINB_DEF) k_fi_upd_kc(DevSym S,
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int c = wc0 + 8 * b + 2 * kq + e;
-            if (ca[b] && c < nu) prow[ucol[c]] = Tv[t * 64 + c] - d[a][b][e];
+            if (ca[b] && c < nu) prow[ucol[c]] = chain ? d[a][b][e] : Tv[t * 64 + c] - d[a][b][e];
           }
       }
     }
@@ -1396,11 +1415,21 @@ __global__ void __launch_bounds__(FI_THREADS, KC_MINB_DEF) k_fi_upd_kcp(DevSym S
   ra[1] = !narrow && wr0 + 8 < s;
 #pragma unroll
   for (int b = 0; b < 4; ++b) ca[b] = wc0 + 8 * b < nu;
+  // row-row order (chain): the accumulators start at the target's values and the
+  // multipliers enter negated, so DMMA's chained FMAs subtract every source row's
+  // product from the running value in (source, row) order; else they start at 0
+  // and the sum is subtracted once in the epilogue
+  const bool chain = P.chain != 0 && part < 0;
   double d[2][4][2];
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) d[a][b][0] = d[a][b][1] = 0.0;
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int t = wr0 + 8 * a + lr, c = wc0 + 8 * b + 2 * kq + e;
+        d[a][b][e] = (chain && ra[a] && t < s && ca[b] && c < nu) ? Pm[(int64_t)t * W + c0 + ucol[c]] : 0.0;
+      }
 
   int buf = 0;
   for (int64_t zb0 = zb; zb0 < ze; zb0 += KC_NSB) {
@@ -1475,7 +1504,10 @@ __global__ void __launch_bounds__(FI_THREADS, KC_MINB_DEF) k_fi_upd_kcp(DevSym S
         for (int k = 0; k < kc4; k += 4) {
           double av[2], bv[4];
 #pragma unroll
-          for (int a = 0; a < 2; ++a) av[a] = ra[a] ? X[(wr0 + 8 * a + lr) * KC_XLD + k + kq] : 0.0;
+          for (int a = 0; a < 2; ++a) {
+            const double xv = ra[a] ? X[(wr0 + 8 * a + lr) * KC_XLD + k + kq] : 0.0;
+            av[a] = chain ? -xv : xv;
+          }
 #pragma unroll
           for (int b = 0; b < 4; ++b) bv[b] = cb[b] ? U[(k + kq) * KC_ULD + wc0 + 8 * b + lr] : 0.0;
 #pragma unroll
@@ -1509,7 +1541,7 @@ __global__ void __launch_bounds__(FI_THREADS, KC_MINB_DEF) k_fi_upd_kcp(DevSym S
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int c = wc0 + 8 * b + 2 * kq + e;
-          if (ca[b] && c < nu) prow[ucol[c]] = Tv[t * 64 + c] - d[a][b][e];
+          if (ca[b] && c < nu) prow[ucol[c]] = chain ? d[a][b][e] : Tv[t * 64 + c] - d[a][b][e];
         }
     }
     return;

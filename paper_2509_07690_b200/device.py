@@ -50,7 +50,7 @@ class FactorsDesc(ctypes.Structure):
     _fields_ = [
         ("d_values", ctypes.c_void_p), ("d_inner_perm", ctypes.c_void_p), ("d_anorm", ctypes.c_void_p),
         ("d_status", ctypes.c_void_p), ("d_pert_rows", ctypes.c_void_p), ("d_pert_vals", ctypes.c_void_p),
-        ("pert_cap", ctypes.c_int64),
+        ("pert_cap", ctypes.c_int64), ("kernel_mode", ctypes.c_int32),
     ]
 
 
@@ -131,6 +131,9 @@ def library():
     lib.hy_upload_matrix.argtypes = [vp, vp, vp]
     lib.hy_residual.argtypes = [vp, vp, vp, vp, vp, vp, u]
     lib.hy_axpy.argtypes = [vp, vp, vp, u]
+    lib.hy_set_kernel_mode.argtypes = [vp, ctypes.c_int]
+    lib.hy_residual_batched.argtypes = [vp, i64, vp, vp, vp, vp, vp, vp, u]
+    lib.hy_axpy_batched.argtypes = [vp, i64, vp, vp, vp, vp, u]
     lib.hy_refactorize_solve_batched.argtypes = [vp, i64, vp, vp, vp, ctypes.c_double,
                                                  ctypes.POINTER(FactorsDesc), vp, u]
     lib.hy_refactorize_batched.argtypes = [vp, i64, vp, ctypes.c_double,
@@ -351,7 +354,7 @@ class DeviceContext:
         )
         desc = FactorsDesc(bufs["values"].data_ptr(), bufs["inner_perm"].data_ptr(),
                            bufs["anorm"].data_ptr(), bufs["status"].data_ptr(),
-                           bufs["pert_rows"].data_ptr(), bufs["pert_vals"].data_ptr(), pert_cap)
+                           bufs["pert_rows"].data_ptr(), bufs["pert_vals"].data_ptr(), pert_cap, -1)
         return bufs, desc
 
     def upload_programs(self, progs):

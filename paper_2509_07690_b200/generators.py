@@ -360,3 +360,27 @@ def config(name, scale="full"):
     if name == "c4":
         return circuit_batch(8, 2000, 2, 200) if small else circuit_batch()
     raise ValueError(name)
+
+
+def zero_first_pivot(an, values):
+    """Test helper ("new values placing 0 at a previously chosen pivot"):
+    zero, in ``values`` (one instance of ``an``'s pattern, modified in place), the A
+    entry that lands on the diagonal of the first factor row with an empty L row,
+    off-diagonal U entries and a later row depending on it (so A stays nonsingular),
+    making that row's pivot exactly 0 so perturbation fires.  Returns the A entry."""
+    s = an.symbolic
+    vm = an.vmap
+    A = an.A
+    used = np.zeros(s.nnodes, bool)
+    used[s.deps] = True
+    for i in range(s.n):
+        u = int(s.node_of[i])
+        if int(s.node_kind[u]) != 0 or int(s.nl[u]) != 0 or not used[u] or \
+                int(s.colptr[u + 1] - s.colptr[u]) < 2:
+            continue
+        a = int(vm.mrow_src[i])
+        for e in range(int(A.row_ptr[a]), int(A.row_ptr[a + 1])):
+            if int(vm.colpos[e]) == 0:          # standalone row, no L: diagonal at position 0
+                values[e] = 0.0
+                return e
+    raise ValueError("no standalone row with an empty L row")

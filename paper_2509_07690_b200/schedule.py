@@ -1355,3 +1355,60 @@ def _merge_items(nlev, flev, first, colptr, cols, nl, dptr, deps, node_of, lev_u
             pos += 1
         nptr[a + 1] = pos
     return new_lev, nt, nc0, nc1, nptr, nk, nq0, nq1, nrw
+
+
+# --------------------------------------------------------------------------- device dispatch
+TIER_NAMES = ("row-row", "sup-row", "sup-sup")
+
+
+def device_routing(sym, mode=None, warp_min=256):
+    """The device's kernel selection for one factorization,
+    written down so it can be reported (SolveReport) and tested.
+
+    * ``edges``: dependency edges (target u <- source v) by (target kind, source kind)
+      and the tier SPEC assigns them: min(kernel_mode, natural tier), natural =
+      row-row for a standalone source, sup-row for a supernode source into a
+      standalone target, sup-sup for supernode into supernode.
+    * ``update_order``: ROWROW mode runs every update in row-row operation order
+      (running target value minus each source row's product, source rows ascending:
+      the ``chain`` flag of the update kernels); SUPROW / SUPSUP apply supernode
+      sources as blocks (TRSM multiplier block, product summed then subtracted once)
+      — on supernode targets SUPROW and SUPSUP are the same arithmetic (oracle note 1).
+    * ``kernels``: launches of the level fan-in plan per kernel — multiplier blocks
+      (k_fi_x_w warp / k_fi_x CTA TRSM), update items (k_fi_upd_kcp packed DMMA,
+      k_fi_upd_w warp GEMV for targets of <= WARP_ROWS rows, k_fi_upd_kc DMMA GEMM),
+      split-K parts; the same grouping as run_fanin in csrc/hylu_abi.cu
+      (``warp_min`` = option fanin_warp_min)."""
+    from .symbolic import KernelMode
+    m = int(sym.kernel_mode if mode is None else mode)
+    kind = np.asarray(sym.node_kind)
+    tgt = np.repeat(np.arange(sym.nnodes), np.diff(sym.dep_ptr))
+    src = np.asarray(sym.deps)
+    tk, sk = kind[tgt], kind[src]
+    natural = np.where(sk == 0, 0, np.where(tk == 0, 1, 2))
+    tier = np.minimum(natural, m)
+    names = {(0, 0): "row<-row", (0, 1): "row<-sup", (1, 0): "sup<-row", (1, 1): "sup<-sup"}
+    edges = {nm: int(np.sum((tk == a) & (sk == b))) for (a, b), nm in names.items()}
+    tiers = {TIER_NAMES[t]: int(np.sum(tier == t)) for t in range(3)}
+    out = {"kernel_mode": KernelMode(m).name, "edges": edges, "edge_tiers": tiers,
+           "update_order": "row-row (chained)" if m == 0 else "block (summed, subtracted once)"}
+    plan = getattr(sym, "_fanin_plan", None)
+    if plan is not None:
+        k = {"k_fi_x_w": 0, "k_fi_x": 0, "k_fi_upd_kcp": 0, "k_fi_upd_w": 0, "k_fi_upd_kc": 0}
+        for lv in range(plan.nlevels):
+            xp0, xp1, xb = int(plan.xp_ptr[lv]), int(plan.xp_ptr[lv + 1]), int(plan.lev_xp_big[lv])
+            if xp1 > xp0:
+                xb = xp0 if xb - xp0 < warp_min else xb
+                k["k_fi_x_w"] += xb - xp0
+                k["k_fi_x"] += xp1 - xb
+            u0, u1 = int(plan.lev_up[lv]), int(plan.lev_up[lv + 1])
+            if u1 > u0:
+                reg, rs = int(plan.lev_up_reg[lv]), int(plan.lev_up_rs[lv])
+                rs = reg if rs - reg < warp_min else rs
+                k["k_fi_upd_kcp"] += reg - u0
+                k["k_fi_upd_w"] += rs - reg
+                k["k_fi_upd_kc"] += u1 - rs
+        k["split_k_parts"] = int(np.sum(np.asarray(plan.up_part) >= 0))
+        out["kernels"] = k
+        out["tensor_core_items"] = k["k_fi_upd_kcp"] + k["k_fi_upd_kc"]
+    return out

@@ -547,3 +547,97 @@ def test_sharded_batch_two_processes_bitwise():
         p.join(600)
     res = q.get(timeout=5)
     assert res == (True, True), res
+
+
+def _perturbed_batch():
+    bp = gen.circuit_batch(40, 1500, 2, 150)
+    an = an_mod.analyze(bp.A0, SolverConfig(ordering="amd"))
+    vals = bp.values.copy()
+    for b in (3, 33):                      # one in each group of 32
+        gen.zero_first_pivot(an, vals[b])
+    return bp, an, vals
+
+
+def test_batched_refinement_of_perturbed_instances():
+    """SPEC.md:492 on the batched path: instances whose pivots were perturbed are
+    refined on the device (masked batched residual / substitution / update) and
+    match the oracle's refined solutions; the others are untouched."""
+    import torch
+    bp, an, vals = _perturbed_batch()
+    on = _oracle()
+    prior = api.factorize_analysis(an)
+    oprior = on.factorize(an)
+    reps_o = {}
+    Xo, npo = on.refactor_solve_batch(an, oprior, vals, bp.rhs, reports=reps_o)
+    assert sorted(reps_o) == [3, 33]
+    X, npert = api.refactorize_solve_batched(vals, prior, bp.rhs)
+    reps = api.refactorize_solve_batched.last_reports
+    assert np.array_equal(npert, npo)
+    assert sorted(reps) == [3, 33]
+    for b in (3, 33):
+        assert reps[b].converged and reps[b].iterations >= 1
+        assert reps[b].backward_errors[-1] <= 1e-13
+        assert abs(reps[b].iterations - reps_o[b]["iterations"]) <= 1
+    assert _rel(X, Xo) <= 1e-9
+    # without refinement the perturbed instances are far off; the rest identical
+    br = api.BatchedRefactorizer(prior)
+    dv = torch.from_numpy(vals).cuda()
+    dr = torch.from_numpy(bp.rhs).cuda()
+    x0, _ = br.run(dv, dr, refine=False)
+    x0 = x0.cpu().numpy()
+    keep = [b for b in range(len(vals)) if b not in (3, 33)]
+    assert np.array_equal(x0[keep], X[keep])
+    A3 = bp.A0.with_values(vals[3])
+    assert refmatrix.backward_error(A3, x0[3], bp.rhs[3]) > 1e-13
+
+
+@pytest.mark.parametrize("pipelined", [False, True])
+def test_batched_host_buffers_refine_perturbed_instances(pipelined):
+    import torch
+    bp, an, vals = _perturbed_batch()
+    prior = api.factorize_analysis(an)
+    X, _ = api.refactorize_solve_batched(vals, prior, bp.rhs)
+    br = api.BatchedRefactorizer(prior)
+    h_vals = torch.from_numpy(vals).pin_memory()
+    h_rhs = torch.from_numpy(bp.rhs).pin_memory()
+    h_x = torch.empty(bp.rhs.shape, dtype=torch.float64).pin_memory()
+    h_np = torch.empty(len(vals), dtype=torch.int32).pin_memory()
+    br.run_host(h_vals, h_rhs, h_x, h_np, chunks=2, pipelined=pipelined)
+    br.host_wait()
+    torch.cuda.synchronize()
+    assert sorted(br.reports) == [3, 33]
+    assert _rel(h_x.numpy(), X) <= 1e-12
+
+
+@pytest.mark.parametrize("name", ["c0", "c2", "c3"])
+def test_kernel_override_at_factorize_routes_the_device(name):
+    """FactorOptions.kernel_override at factorize time sets the
+    device dispatch: ROWROW runs the row-row operation order,
+    SUPROW / SUPSUP the block order (bitwise the same on the device, as in the
+    oracle); every mode matches the oracle of that mode and the modes agree within
+    SPEC's 1e-12."""
+    from paper_2509_07690_b200._ref import KernelMode
+    p = gen.config(name, "small")
+    an = an_mod.analyze(p.A, SolverConfig(ordering=p.ordering))
+    on = _oracle()
+    fv = {}
+    for m in (2, 0, 1):
+        f = api.factorize_analysis(an, opts=api.FactorOptions(kernel_override=m))
+        assert int(f.kernel_mode) == m
+        ref = on.factorize(an, mode=m)
+        assert np.array_equal(f.host_inner_perm(), ref.inner_perm)
+        assert _rel(f.host_values(), ref.values) <= LU_RTOL
+        r = f.routing()
+        assert r["kernel_mode"] == KernelMode(m).name
+        assert r["update_order"].startswith("row-row") == (m == 0)
+        fv[m] = f.host_values()
+        # refactorize keeps the prior's mode: bitwise equal on unchanged values
+        f2 = api.refactorize(p.A, f)
+        assert int(f2.kernel_mode) == m and np.array_equal(f2.host_values(), fv[m])
+    assert np.array_equal(fv[1], fv[2])
+    assert an.symbolic.supernode_count > 0
+    assert not np.array_equal(fv[0], fv[2]), "ROWROW must run the row-row order"
+    assert _rel(fv[0], fv[2]) <= 1e-12
+    # the default (no override) is the analysis' mode
+    f = api.factorize_analysis(an)
+    assert f.kernel_mode == an.symbolic.kernel_mode

@@ -438,3 +438,55 @@ def test_sharded_batch_gloo_world2_matches_single_rank():
     same_x, same_n, t = q.get(timeout=5)
     assert same_x and same_n
     assert t == [0.5, 1.5]
+
+
+def test_oracle_batch_refines_perturbed_instances():
+    """a batch instance whose refactorization perturbs a pivot is refined
+    automatically (oracle side of the batched refinement parity)."""
+    bp = gen.circuit_batch(6, 1500, 2, 150)
+    an = an_mod.analyze(bp.A0, SolverConfig(ordering="amd"))
+    prior = on.factorize(an)
+    vals = bp.values.copy()
+    gen.zero_first_pivot(an, vals[3])
+    reps = {}
+    X, npert = on.refactor_solve_batch(an, prior, vals, bp.rhs, reports=reps)
+    assert npert[3] >= 1 and sorted(reps) == [b for b in range(6) if npert[b] > 0]
+    rep = reps[3]
+    assert rep["iterations"] >= 1 and rep["converged"]
+    assert rep["backward_errors"][-1] <= 1e-13
+    assert all(b <= a for a, b in zip(rep["backward_errors"], rep["backward_errors"][1:]))
+    from paper_2509_07690_b200._ref import matrix as refmatrix
+    A3 = bp.A0.with_values(vals[3])
+    assert refmatrix.backward_error(A3, X[3], bp.rhs[3]) <= 1e-13
+    X0, _ = on.refactor_solve_batch(an, prior, vals, bp.rhs, refine_perturbed=False)
+    assert refmatrix.backward_error(A3, X0[3], bp.rhs[3]) > 1e-13   # refinement did the work
+
+
+@pytest.mark.parametrize("name", ["c0", "c2"])
+def test_device_routing_table(name):
+    """The device dispatch written down: every dependency
+    edge gets tier min(kernel_mode, natural tier); ROWROW runs the row-row operation
+    order; the kernel counts cover every item of the fan-in plan."""
+    p = gen.config(name, "small")
+    an = an_mod.analyze(p.A, SolverConfig(ordering=p.ordering))
+    s = an.symbolic
+    plan = schedule.build_fanin_plan(s)
+    s._fanin_plan = plan
+    nd = int(s.dep_ptr[-1])
+    for m in (0, 1, 2):
+        r = schedule.device_routing(s, m)
+        assert sum(r["edges"].values()) == nd == sum(r["edge_tiers"].values())
+        assert r["kernel_mode"] == KernelMode(m).name
+        assert r["update_order"].startswith("row-row") == (m == 0)
+        t = r["edge_tiers"]
+        if m == 0:
+            assert t["sup-row"] == t["sup-sup"] == 0
+        if m == 1:
+            assert t["sup-sup"] == 0 and t["sup-row"] == r["edges"]["row<-sup"] + r["edges"]["sup<-sup"]
+        if m == 2:
+            assert t["row-row"] == r["edges"]["row<-row"] + r["edges"]["sup<-row"]
+            assert t["sup-sup"] == r["edges"]["sup<-sup"]
+        k = r["kernels"]
+        assert k["k_fi_upd_kcp"] + k["k_fi_upd_w"] + k["k_fi_upd_kc"] == len(plan.up_t)
+        assert k["k_fi_x_w"] + k["k_fi_x"] == len(plan.xp_edge)
+    assert r["edges"]["sup<-sup"] > 0 and r["tensor_core_items"] > 0
