@@ -99,6 +99,7 @@ typedef struct {
   int64_t *d_pert_rows;    /* [pert_cap] factor rows where perturbation fired */
   double *d_pert_vals;     /* [pert_cap] original pivot values */
   int64_t pert_cap;
+  int32_t kernel_mode;     /* out: the kernel mode (maximum tier) the call ran with */
 } hy_factors;
 
 int hy_create(int device, hy_handle **out);
@@ -115,6 +116,17 @@ int hy_refactorize(hy_handle *h, const double *d_avals, double eps, const hy_fac
                    hy_factors *out, uintptr_t stream);
 int hy_solve(hy_handle *h, const hy_factors *f, const double *d_b, double *d_x,
              uintptr_t stream);
+/* FactorOptions.kernel_override: the kernel mode of the following
+ * hy_factorize / hy_refactorize calls on this handle (-1 = the uploaded analysis'
+ * kernel_mode).  Device dispatch (DESIGN.md §3 "Kernel selection"):
+ * kernel_mode is the maximum tier.  ROWROW: every update runs in row-row operation
+ * order (the running target value minus each source row's product, source rows
+ * ascending — update_row_by_row) in every update kernel;
+ * SUPROW / SUPSUP: supernode sources act as blocks (multiplier block by TRSM, then
+ * the block product summed and subtracted once — update_row_by_sup / sup_by_sup,
+ * SPEC.md:300-318), the product on DMMA for multi-row targets (k_fi_upd_kc / kcp)
+ * and as a warp GEMV for targets of <= 4 rows (k_fi_upd_w). */
+int hy_set_kernel_mode(hy_handle *h, int mode);
 
 /* Iterative refinement on the device.  hy_upload_matrix: A's
  * pattern in original coordinates (SparseMatrixCSR row_ptr / col_idx,
@@ -126,6 +138,34 @@ int hy_upload_matrix(hy_handle *h, const int64_t *row_ptr, const int32_t *col_id
 int hy_residual(hy_handle *h, const double *d_avals, const double *d_x, const double *d_b,
                 double *d_r, double *d_berr, uintptr_t stream);
 int hy_axpy(hy_handle *h, double *d_x, const double *d_dx, uintptr_t stream);
+/* Partition-based substitution for many right-hand sides (Fig. 3;
+ * host side paper_2509_07690_b200/partition.py build_partition / device_launches).
+ * Launch lists per direction: rows of 6 int64 (kind, seq, lo, hi, item offset, item
+ * count); kind 0 = rectangular block (items: row-range pairs [r0, r1), one warp each;
+ * forward entries with column < lo, backward column >= hi), kind 1 = triangular
+ * level (items: nodes; entries with column in [lo, hi)); seq = 1: one warp walks the
+ * items in order.  hy_solve_multi: d_B / d_X [nrhs][n] row-major (x_j = A^-1 b_j with
+ * the factors' scaling and permutations, no refinement). */
+typedef struct {
+  int64_t nfwd, nbwd, nitems;
+  const int64_t *fwd;      /* [nfwd][6] */
+  const int64_t *bwd;      /* [nbwd][6] */
+  const int32_t *items;    /* [nitems] */
+} hy_partition_desc;
+int hy_upload_partition(hy_handle *h, const hy_partition_desc *d);
+int hy_solve_multi(hy_handle *h, const hy_factors *f, int64_t nrhs, const double *d_B, double *d_X,
+                   uintptr_t stream);
+
+/* Batched forms for the automatic refinement of perturbed batch instances
+ * (SPEC.md:492, 499-507): d_vals [B][nnz], d_x / d_b / d_r [B][n] row-major,
+ * d_berr [B] (one backward error per instance, same arithmetic as hy_residual);
+ * instances with d_mask[b] == 0 are skipped (d_mask NULL = all).
+ * hy_axpy_batched: d_y[b] = d_x[b] + d_dx[b] (d_dx NULL: a copy) where masked. */
+int hy_residual_batched(hy_handle *h, int64_t B, const double *d_vals, const double *d_x,
+                        const double *d_b, double *d_r, double *d_berr, const int32_t *d_mask,
+                        uintptr_t stream);
+int hy_axpy_batched(hy_handle *h, int64_t B, double *d_y, const double *d_x, const double *d_dx,
+                    const int32_t *d_mask, uintptr_t stream);
 
 /* Column-slab plan for supernode targets (schedule.build_slab_plan): one CTA per
  * slab, slabs grouped by factorization level.  Optional: without it supernodes

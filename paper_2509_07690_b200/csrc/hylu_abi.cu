@@ -71,6 +71,13 @@ __global__ void k_anorm_p(const CallP *, const double *, int64_t);
 __global__ void k_resid_berr(int, const int64_t *, const int32_t *, const double *, const double *,
                              const double *, double *, unsigned long long *);
 __global__ void k_axpy1(int, double *, const double *);
+__global__ void k_resid_berr_b(int, int64_t, const int64_t *, const int32_t *, const double *,
+                               const double *, const double *, double *, unsigned long long *,
+                               const int32_t *);
+__global__ void k_axpy_b(int, double *, const double *, const double *, const int32_t *);
+__global__ void k_msolve(DevSym, const double *, int, int, int, int, const int32_t *, int, int, double *, int);
+__global__ void k_mbhat(DevSym, const int32_t *, const double *, double *, int);
+__global__ void k_mxout(DevSym, const double *, double *, int);
 
 __global__ void k_fi_lu(DevSym, const CallP *, FaninDev, int);
 __global__ void k_fi_panel(DevSym, const CallP *, FaninDev, int);
@@ -249,6 +256,13 @@ struct hy_handle {
   const double **d_fptr = nullptr;                   // factor values of the current solve (device slot)
   int64_t fi_graph_launches = 0;                     // kernels per graph replay
   int use_graphs = 1;                                // option "graphs"
+  // partition-based multi-RHS solve (hy_upload_partition / hy_solve_multi)
+  std::vector<int64_t> ms_fwd, ms_bwd;               // [k][6] launch lists
+  int32_t *d_ms_items = nullptr;
+  double *d_my = nullptr;                            // Y [n][nrhs]
+  int64_t my_cap = 0;
+  int mode_an = 2;                                   // kernel_mode of the uploaded analysis
+  int kmode = -1;                                    // hy_set_kernel_mode (-1: mode_an)
   int sm_count = 148;
   // single-instance hub rows (ROWROW path): programs + per-level hub node lists
   bool hub1_ok = false;
@@ -501,6 +515,8 @@ void hy_destroy(hy_handle *h) {
   if (h->d_pinv) cudaFree(h->d_pinv);
   if (h->d_rowof) cudaFree(h->d_rowof);
   if (h->d_acol) cudaFree(h->d_acol);
+  if (h->d_ms_items) cudaFree(h->d_ms_items);
+  if (h->d_my) cudaFree(h->d_my);
   delete h;
 }
 
@@ -566,6 +582,8 @@ int hy_upload_symbolic(hy_handle *h, const hy_symbolic_desc *d) {
   S.n = (int32_t)n;
   S.nn = (int32_t)nn;
   S.mode = d->kernel_mode;
+  h->mode_an = d->kernel_mode;
+  h->kmode = -1;
   S.nnz = nnz;
   int64_t *p64;
   int32_t *p32;
@@ -1095,6 +1113,12 @@ static int run_factor(hy_handle *h, const double *d_avals, double eps, const hy_
   P.refactor = prior ? 1 : 0;
   P.iperm_prior = prior ? prior->d_inner_perm : nullptr;
   P.anorm_prior = prior ? prior->d_anorm : nullptr;
+  // SPEC dispatch: kernel_mode is the maximum tier; on the
+  // device the ROWROW tier is the row-row operation order in every update kernel
+  const int mode = h->kmode >= 0 ? h->kmode : h->mode_an;
+  P.chain = mode == HY_ROWROW;
+  h->S.mode = mode;                 // row path: per-(target, source) dispatch by mode
+  out->kernel_mode = mode;
   if (!h->d_callp) CK(cudaMalloc((void **)&h->d_callp, sizeof(CallP)));
   const CallP *Pd = h->d_callp;
   // stream-ordered: the previous call's kernels have read their CallP before this
@@ -1203,6 +1227,112 @@ int hy_axpy(hy_handle *h, double *d_x, const double *d_dx, uintptr_t stream) {
   CK(cudaSetDevice(h->device));
   const int n = h->S.n;
   k_axpy1<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(n, d_x, d_dx);
+  h->launches++;
+  CK(cudaGetLastError());
+  return HY_OK;
+}
+
+int hy_upload_partition(hy_handle *h, const hy_partition_desc *d) {
+  if (!h || !h->uploaded || !d) return fail(HY_INVALID_ARGUMENT, "symbolic not uploaded / null");
+  if (d->nfwd < 0 || d->nbwd < 0 || d->nitems < 0 || (d->nfwd && !d->fwd) || (d->nbwd && !d->bwd) ||
+      (d->nitems && !d->items))
+    return fail(HY_INVALID_ARGUMENT, "bad partition arrays");
+  for (int dir = 0; dir < 2; ++dir) {
+    const int64_t k = dir ? d->nbwd : d->nfwd;
+    const int64_t *L = dir ? d->bwd : d->fwd;
+    for (int64_t q = 0; q < k; ++q) {
+      const int64_t kind = L[6 * q], lo = L[6 * q + 2], hi = L[6 * q + 3], off = L[6 * q + 4],
+                    cnt = L[6 * q + 5];
+      const int64_t span = kind == 0 ? 2 * cnt : cnt;
+      if ((kind != 0 && kind != 1) || lo < 0 || hi > h->S.n || lo > hi || off < 0 || cnt < 0 ||
+          off + span > d->nitems)
+        return fail(HY_INVALID_ARGUMENT, "partition launch out of range");
+    }
+  }
+  CK(cudaSetDevice(h->device));
+  if (h->d_ms_items) CK(cudaFree(h->d_ms_items));
+  h->d_ms_items = nullptr;
+  if (d->nitems) {
+    CK(cudaMalloc((void **)&h->d_ms_items, sizeof(int32_t) * d->nitems));
+    CK(cudaMemcpy(h->d_ms_items, d->items, sizeof(int32_t) * d->nitems, cudaMemcpyHostToDevice));
+  }
+  h->ms_fwd.assign(d->fwd, d->fwd + 6 * d->nfwd);
+  h->ms_bwd.assign(d->bwd, d->bwd + 6 * d->nbwd);
+  return HY_OK;
+}
+
+int hy_solve_multi(hy_handle *h, const hy_factors *f, int64_t nrhs, const double *d_B, double *d_X,
+                   uintptr_t stream) {
+  if (!h || !h->uploaded) return fail(HY_INVALID_ARGUMENT, "symbolic not uploaded");
+  if (!f || !f->d_values || !f->d_inner_perm || !d_B || !d_X) return fail(HY_INVALID_ARGUMENT, "null buffer");
+  if (nrhs <= 0 || nrhs > (1 << 20)) return fail(HY_INVALID_ARGUMENT, "nrhs outside [1, 2^20]");
+  if (h->ms_fwd.empty() && h->ms_bwd.empty() && h->S.n > 0)
+    return fail(HY_INVALID_ARGUMENT, "solve partition not uploaded");
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t need = (int64_t)h->S.n * nrhs;
+  if (need > h->my_cap) {
+    if (h->d_my) CK(cudaFree(h->d_my));
+    h->d_my = nullptr;
+    CK(cudaMalloc((void **)&h->d_my, sizeof(double) * (need > 0 ? need : 1)));
+    h->my_cap = need;
+  }
+  const int gb = (int)std::min<int64_t>((need + 255) / 256 + 1, (int64_t)h->sm_count * 16);
+  k_mbhat<<<gb, 256, 0, st>>>(h->S, f->d_inner_perm, d_B, h->d_my, (int)nrhs);
+  h->launches++;
+  for (int dir = 0; dir < 2; ++dir) {
+    const std::vector<int64_t> &L = dir ? h->ms_bwd : h->ms_fwd;
+    for (size_t q = 0; q + 5 < L.size(); q += 6) {
+      const int kind = (int)L[q], seq = (int)L[q + 1], lo = (int)L[q + 2], hi = (int)L[q + 3];
+      const int cnt = (int)L[q + 5];
+      if (!cnt) continue;
+      const int blocks = seq ? 1 : (cnt + 3) / 4;
+      k_msolve<<<blocks, 128, 0, st>>>(h->S, f->d_values, kind, seq, lo, hi, h->d_ms_items + L[q + 4], cnt,
+                                       dir == 0, h->d_my, (int)nrhs);
+      h->launches++;
+    }
+  }
+  k_mxout<<<gb, 256, 0, st>>>(h->S, h->d_my, d_X, (int)nrhs);
+  h->launches++;
+  CK(cudaGetLastError());
+  return HY_OK;
+}
+
+int hy_set_kernel_mode(hy_handle *h, int mode) {
+  if (!h || !h->uploaded) return fail(HY_INVALID_ARGUMENT, "symbolic not uploaded");
+  if (mode < -1 || mode > 2) return fail(HY_INVALID_ARGUMENT, "kernel mode outside {-1, 0, 1, 2}");
+  h->kmode = mode;
+  return HY_OK;
+}
+
+int hy_residual_batched(hy_handle *h, int64_t B, const double *d_vals, const double *d_x,
+                        const double *d_b, double *d_r, double *d_berr, const int32_t *d_mask,
+                        uintptr_t stream) {
+  if (!h || !h->d_arow) return fail(HY_INVALID_ARGUMENT, "matrix pattern not uploaded");
+  if (B <= 0 || B > 65535 || !d_vals || !d_x || !d_b || !d_berr)
+    return fail(HY_INVALID_ARGUMENT, "null buffer or batch size outside [1, 65535]");
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaMemsetAsync(d_berr, 0, sizeof(double) * B, st));
+  const int n = h->S.n;
+  const int gx = (n + 255) / 256 < 64 ? (n + 255) / 256 : 64;
+  k_resid_berr_b<<<dim3(gx > 0 ? gx : 1, (unsigned)B), 256, 0, st>>>(
+      n, h->S.nnz, h->d_arow, h->d_acol, d_vals, d_x, d_b, d_r,
+      reinterpret_cast<unsigned long long *>(d_berr), d_mask);
+  h->launches++;
+  CK(cudaGetLastError());
+  return HY_OK;
+}
+
+int hy_axpy_batched(hy_handle *h, int64_t B, double *d_y, const double *d_x, const double *d_dx,
+                    const int32_t *d_mask, uintptr_t stream) {
+  if (!h || !d_y || !d_x) return fail(HY_INVALID_ARGUMENT, "null buffer");
+  if (B <= 0 || B > 65535) return fail(HY_INVALID_ARGUMENT, "batch size outside [1, 65535]");
+  CK(cudaSetDevice(h->device));
+  const int n = h->S.n;
+  const int gx = (n + 255) / 256 < 64 ? (n + 255) / 256 : 64;
+  k_axpy_b<<<dim3(gx > 0 ? gx : 1, (unsigned)B), 256, 0, (cudaStream_t)stream>>>(n, d_y, d_x, d_dx,
+                                                                                   d_mask);
   h->launches++;
   CK(cudaGetLastError());
   return HY_OK;
