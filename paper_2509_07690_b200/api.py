@@ -270,6 +270,47 @@ def substitute(factors, b, stream=None):
     return d_x
 
 
+def substitute_multi(factors, B, stream=None):
+    """Forward/backward substitution for many right-hand sides at once through the
+    partition-based device solve (Fig. 3; ``partition.py``): B is
+    [nrhs, n] (numpy or a CUDA float64 tensor), returns X [nrhs, n] on the device."""
+    import torch
+    from .device import check
+    ctx = factors._ctx
+    d_B = B if isinstance(B, torch.Tensor) else torch.from_numpy(
+        np.ascontiguousarray(B, np.float64)).to(ctx.device)
+    if d_B.dim() == 1:
+        d_B = d_B.reshape(1, -1)
+    if d_B.dim() != 2 or d_B.shape[1] != ctx.n or d_B.dtype != torch.float64 or d_B.device != ctx.device:
+        raise errors.DimensionMismatch("B must be a float64 [nrhs, %d] array" % ctx.n)
+    d_B = d_B.contiguous()
+    if getattr(ctx, "_partition", None) is None:   # else: the one ensure_partition uploaded
+        ctx.ensure_partition()
+    d_X = torch.empty_like(d_B)
+    check(ctx.lib.hy_solve_multi(ctx.h, factors._desc, d_B.shape[0], d_B.data_ptr(), d_X.data_ptr(),
+                                 ctx.stream_handle(stream)))
+    return d_X
+
+
+def solve_multi(A, factors, B, config=None):
+    """solve for the rows of B [nrhs, n] at once: partition-based
+    substitution, then the automatic refinement of SPEC.md:492 per right-hand side
+    when perturbation fired.  Returns (X [nrhs, n] numpy, [RefinementReport])."""
+    import torch
+    B = np.ascontiguousarray(B, np.float64)
+    if B.ndim != 2 or B.shape[1] != A.n:
+        raise errors.DimensionMismatch("B must have shape [nrhs, %d]" % A.n)
+    X = substitute_multi(factors, B)
+    reports = [RefinementReport() for _ in range(B.shape[0])]
+    if factors.perturbed:
+        ctx = factors._ctx
+        for j in range(B.shape[0]):
+            d_b = torch.from_numpy(B[j].copy()).to(ctx.device)
+            xj, reports[j] = iterative_refinement(A, factors, d_b, X[j].clone(), config)
+            X[j] = xj
+    return X.cpu().numpy(), reports
+
+
 def solve(A, factors, ps=None, order=None, b=None, threads=1, config=None):
     """SPEC.md:489-497 (+ automatic iterative_refinement when perturbation fired,
     SPEC.md:499-507, on the device: residual and backward error in original

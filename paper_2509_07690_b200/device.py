@@ -54,6 +54,11 @@ class FactorsDesc(ctypes.Structure):
     ]
 
 
+class PartitionDesc(ctypes.Structure):
+    _fields_ = [("nfwd", ctypes.c_int64), ("nbwd", ctypes.c_int64), ("nitems", ctypes.c_int64),
+                ("fwd", ctypes.c_void_p), ("bwd", ctypes.c_void_p), ("items", ctypes.c_void_p)]
+
+
 class ProgramsDesc(ctypes.Structure):
     _fields_ = [
         ("nsteps", ctypes.c_int64), ("nrel", ctypes.c_int64), ("nhubrows", ctypes.c_int64),
@@ -132,6 +137,8 @@ def library():
     lib.hy_residual.argtypes = [vp, vp, vp, vp, vp, vp, u]
     lib.hy_axpy.argtypes = [vp, vp, vp, u]
     lib.hy_set_kernel_mode.argtypes = [vp, ctypes.c_int]
+    lib.hy_upload_partition.argtypes = [vp, ctypes.POINTER(PartitionDesc)]
+    lib.hy_solve_multi.argtypes = [vp, ctypes.POINTER(FactorsDesc), i64, vp, vp, u]
     lib.hy_residual_batched.argtypes = [vp, i64, vp, vp, vp, vp, vp, vp, u]
     lib.hy_axpy_batched.argtypes = [vp, i64, vp, vp, vp, vp, u]
     lib.hy_refactorize_solve_batched.argtypes = [vp, i64, vp, vp, vp, ctypes.c_double,
@@ -394,6 +401,34 @@ class DeviceContext:
         with self.torch.cuda.device(self.device):
             check(self.lib.hy_upload_matrix(self.h, rp.ctypes.data, ci.ctypes.data))
         self._matrix_uploaded = True
+
+    def ensure_partition(self, threads=None, config=None):
+        """Build (partition.build_partition) and upload the multi-RHS solve partition,
+        cached per (threads, thresholds).  ``threads`` defaults to the device's
+        resident warps (SM count x 8) for the balanced row ranges; unless the config
+        sets ``seg_nnz_threshold``, segments hold >= 1/32 of the stored entries (each
+        segment costs launches on the device, not a thread barrier)."""
+        from . import partition as pt
+        if threads is None:
+            threads = self.torch.cuda.get_device_properties(self.device).multi_processor_count * 8
+        cfg = config or self.analysis.config
+        s = self.analysis.symbolic
+        if cfg.seg_nnz_threshold is None:
+            cfg = cfg.with_overrides(seg_nnz_threshold=max(4096, int(s.stored_values) // 32))
+        key = (int(threads), int(cfg.seg_nnz_threshold), int(cfg.small_tri_threshold),
+               int(cfg.bulk_width_factor))
+        if getattr(self, "_partition_key", None) == key:
+            return self._partition
+        part = pt.build_partition(s, threads, cfg)
+        fwd, bwd, items = pt.device_launches(s, part)
+        fwd, bwd = np.ascontiguousarray(fwd), np.ascontiguousarray(bwd)
+        items = np.ascontiguousarray(items)
+        d = PartitionDesc(len(fwd), len(bwd), len(items), fwd.ctypes.data if fwd.size else None,
+                          bwd.ctypes.data if bwd.size else None, items.ctypes.data if items.size else None)
+        with self.torch.cuda.device(self.device):
+            check(self.lib.hy_upload_partition(self.h, ctypes.byref(d)))
+        self._partition, self._partition_key = part, key
+        return part
 
     def set_option(self, name, value):
         check(self.lib.hy_set_option(self.h, name.encode(), int(value)))

@@ -641,3 +641,54 @@ def test_kernel_override_at_factorize_routes_the_device(name):
     # the default (no override) is the analysis' mode
     f = api.factorize_analysis(an)
     assert f.kernel_mode == an.symbolic.kernel_mode
+
+
+@pytest.mark.parametrize("name", ["c0", "c1", "c2", "c3"])
+@pytest.mark.parametrize("nrhs", [1, 37])
+def test_solve_multi_matches_oracle(name, nrhs):
+    """Partition-based multi-RHS substitution (Fig. 3) on the device
+    against the oracle's substitution on the same (device) factors, per right-hand
+    side, with a forced multi-segment partition."""
+    from oracle.numeric import OracleFactors
+    p = gen.config(name, "small")
+    an = an_mod.analyze(p.A, SolverConfig(ordering=p.ordering))
+    on = _oracle()
+    f = api.factorize_analysis(an)
+    ctx = f._ctx
+    part = ctx.ensure_partition(config=SolverConfig(seg_nnz_threshold=max(500, an.symbolic.stored_values // 12)))
+    assert part.seg_rows[-1] == an.symbolic.n and part.nsegments >= 2
+    rng = np.random.default_rng(11)
+    B = rng.uniform(-1, 1, (nrhs, p.A.n))
+    X = api.substitute_multi(f, B).cpu().numpy()
+    fo = OracleFactors(f.host_values(), f.host_inner_perm(), [], f.anorm)
+    for j in range(nrhs):
+        xo = on.substitute(an, fo, B[j])
+        assert _rel(X[j], xo) <= 1e-13
+    xs = api.substitute(f, B[0]).cpu().numpy()
+    assert _rel(X[0], xs) <= 1e-13
+    for j in range(min(nrhs, 3)):
+        res = np.linalg.norm(refmatrix.spmv(p.A, X[j]) - B[j]) / np.linalg.norm(B[j])
+        assert res <= RES_TOL
+
+
+def test_solve_multi_small_segments_and_refinement():
+    """Many small segments (sequential triangles, balanced rectangular ranges) and the
+    automatic refinement of solve_multi on a perturbed factorization."""
+    from paper_2509_07690_b200 import partition as pt
+    bp = gen.circuit_batch(2, 1500, 2, 150)
+    an = an_mod.analyze(bp.A0, SolverConfig(ordering="amd", seg_nnz_threshold=500))
+    vals = bp.values[1].copy()
+    gen.zero_first_pivot(an, vals)
+    A1 = bp.A0.with_values(vals)
+    f = api.factorize(A1, an.pivot_scale, an.ordering, an.symbolic)
+    assert f.perturbed
+    part = f._ctx.ensure_partition(config=an.config)
+    assert part.nsegments > 4 and part.sequential.any()
+    rng = np.random.default_rng(5)
+    B = rng.uniform(-1, 1, (4, 1500))
+    X, reps = api.solve_multi(A1, f, B)
+    for j in range(4):
+        assert reps[j].converged
+        assert refmatrix.backward_error(A1, X[j], B[j]) <= 1e-13
+        xj, _ = api.solve(A1, f, b=B[j])
+        assert _rel(X[j], xj) <= 1e-12
