@@ -89,8 +89,8 @@ __global__ void k_fi_upd_w(DevSym, const CallP *, FaninDev, int, int);
 size_t fi_upd_smem(int, int);
 size_t fi_upd_tc_smem(int);
 size_t fi_upd_kc_smem();
-__global__ void k_fi_upd_kc(DevSym, const CallP *, FaninDev, int);
-__global__ void k_fi_upd_kcp(DevSym, const CallP *, FaninDev, int);
+template <bool CHAIN> __global__ void k_fi_upd_kc(DevSym, const CallP *, FaninDev, int);
+template <bool CHAIN> __global__ void k_fi_upd_kcp(DevSym, const CallP *, FaninDev, int);
 __global__ void k_fi_upd_tc(DevSym, const CallP *, FaninDev, int, int);
 size_t hub_smem_bytes();
 int hub_threads();
@@ -263,6 +263,7 @@ struct hy_handle {
   int64_t my_cap = 0;
   int mode_an = 2;                                   // kernel_mode of the uploaded analysis
   int kmode = -1;                                    // hy_set_kernel_mode (-1: mode_an)
+  int fi_chain = -1;                                 // row-row order instantiations in the captured fan-in graph
   int sm_count = 148;
   // single-instance hub rows (ROWROW path): programs + per-level hub node lists
   bool hub1_ok = false;
@@ -807,8 +808,10 @@ int hy_upload_fanin_plan(hy_handle *h, const hy_fanin_plan *d) {
   }
   CK(cudaFuncSetAttribute(k_fi_upd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx));
   CK(cudaFuncSetAttribute(k_fi_upd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fi_upd_tc_smem(64)));
-  CK(cudaFuncSetAttribute(k_fi_upd_kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fi_upd_kc_smem()));
-  CK(cudaFuncSetAttribute(k_fi_upd_kcp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fi_upd_kc_smem()));
+  CK(cudaFuncSetAttribute(k_fi_upd_kc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fi_upd_kc_smem()));
+  CK(cudaFuncSetAttribute(k_fi_upd_kc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fi_upd_kc_smem()));
+  CK(cudaFuncSetAttribute(k_fi_upd_kcp<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fi_upd_kc_smem()));
+  CK(cudaFuncSetAttribute(k_fi_upd_kcp<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fi_upd_kc_smem()));
   CK(cudaFuncSetAttribute(k_fi_upd_pk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx));
   CK(cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, h->device));
   CK(cudaFuncSetAttribute(k_fi_panel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -912,7 +915,8 @@ static int run_fanin(hy_handle *h, const CallP *Pd, cudaStream_t st) {
       if (npk && h->fi_tc == 5) {
         FaninDev Dp = h->fi;
         if (!h->fi_maps) Dp.src_pos = nullptr;
-        k_fi_upd_kcp<<<npk, 256, fi_upd_kc_smem(), sk>>>(h->S, Pd, Dp, (int)h->fi_up[l]);
+        if (h->fi_chain) k_fi_upd_kcp<true><<<npk, 256, fi_upd_kc_smem(), sk>>>(h->S, Pd, Dp, (int)h->fi_up[l]);
+        else k_fi_upd_kcp<false><<<npk, 256, fi_upd_kc_smem(), sk>>>(h->S, Pd, Dp, (int)h->fi_up[l]);
         h->launches++;
       } else if (npk) {
         k_fi_upd_pk<<<npk, 256, sm, sk>>>(h->S, Pd, h->fi, (int)h->fi_up[l], h->fi_smax[l], h->fi_mmax[l]);
@@ -927,7 +931,8 @@ static int run_fanin(hy_handle *h, const CallP *Pd, cudaStream_t st) {
       if (split > rs && h->fi_tc >= 4) {
         FaninDev Dk = h->fi;
         if (!h->fi_maps) Dk.src_pos = nullptr;
-        k_fi_upd_kc<<<split - rs, 256, fi_upd_kc_smem(), st>>>(h->S, Pd, Dk, rs);
+        if (h->fi_chain) k_fi_upd_kc<true><<<split - rs, 256, fi_upd_kc_smem(), st>>>(h->S, Pd, Dk, rs);
+        else k_fi_upd_kc<false><<<split - rs, 256, fi_upd_kc_smem(), st>>>(h->S, Pd, Dk, rs);
         h->launches++;
       } else if (split > rs && h->fi_tc == 2) {
         k_fi_upd_tc<<<split - rs, 256, fi_upd_tc_smem(h->fi_smax[l]), st>>>(h->S, Pd, h->fi, rs, h->fi_smax[l]);
@@ -938,7 +943,8 @@ static int run_fanin(hy_handle *h, const CallP *Pd, cudaStream_t st) {
         h->launches++;
       }
       if (nbig && h->fi_tc == 3) {
-        k_fi_upd_kc<<<nbig, 256, fi_upd_kc_smem(), st>>>(h->S, Pd, h->fi, split);
+        if (h->fi_chain) k_fi_upd_kc<true><<<nbig, 256, fi_upd_kc_smem(), st>>>(h->S, Pd, h->fi, split);
+        else k_fi_upd_kc<false><<<nbig, 256, fi_upd_kc_smem(), st>>>(h->S, Pd, h->fi, split);
         h->launches++;
       } else if (nbig && h->fi_tc == 1) {
         k_fi_upd_tc<<<nbig, 256, fi_upd_tc_smem(h->fi_smax[l]), st>>>(h->S, Pd, h->fi, split, h->fi_smax[l]);
@@ -1117,6 +1123,10 @@ static int run_factor(hy_handle *h, const double *d_avals, double eps, const hy_
   // device the ROWROW tier is the row-row operation order in every update kernel
   const int mode = h->kmode >= 0 ? h->kmode : h->mode_an;
   P.chain = mode == HY_ROWROW;
+  if (h->fi_chain != P.chain) {     // the DMMA update kernels are instantiated per order
+    drop_graph(h);
+    h->fi_chain = P.chain;
+  }
   h->S.mode = mode;                 // row path: per-(target, source) dispatch by mode
   out->kernel_mode = mode;
   if (!h->d_callp) CK(cudaMalloc((void **)&h->d_callp, sizeof(CallP)));

@@ -953,6 +953,66 @@ __device__ __forceinline__ void cp_async8z(double *smem_dst, const double *gsrc,
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(gsrc), "r"(n) : "memory");
 }
 
+// DMMA without `volatile`: the compiler may schedule the fragment loads of the next
+// k-step across the MMAs
+__device__ __forceinline__ void dmma884s(double (&d)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(d[0]), "+d"(d[1])
+      : "d"(a), "d"(b));
+}
+
+// One staged K chunk of a warp's 16 (or 8) x 32 output tile.  Full tiles (every
+// 8-row and 8-column block live: the bulk of the c2/c3 work) run a predicate-free
+// loop; partial ones skip dead blocks warp-uniformly.  CHAIN negates the multipliers
+// (row-row operation order, see k_fi_upd_kc).
+template <bool CHAIN, int NA>
+__device__ __forceinline__ void kc_chunk_full(const double *X, const double *U, int kc4, int wr0, int wc0,
+                                              int lr, int kq, double (&d)[2][4][2]) {
+#pragma unroll 2
+  for (int k = 0; k < kc4; k += 4) {
+    double av[NA], bv[4];
+#pragma unroll
+    for (int a = 0; a < NA; ++a) {
+      av[a] = X[(wr0 + 8 * a + lr) * KC_XLD + k + kq];
+      if (CHAIN) av[a] = -av[a];
+    }
+#pragma unroll
+    for (int b = 0; b < 4; ++b) bv[b] = U[(k + kq) * KC_ULD + wc0 + 8 * b + lr];
+#pragma unroll
+    for (int a = 0; a < NA; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) dmma884s(d[a][b], av[a], bv[b]);
+  }
+}
+
+template <bool CHAIN>
+__device__ __forceinline__ void kc_chunk(const double *X, const double *U, int kc4, int wr0, int wc0, int lr,
+                                         int kq, const bool (&ra)[2], const bool (&cb)[4], unsigned bm,
+                                         double (&d)[2][4][2]) {
+  if (!ra[0] || !(bm & 15u)) return;
+  if (cb[0] && cb[1] && cb[2] && cb[3]) {
+    if (ra[1]) kc_chunk_full<CHAIN, 2>(X, U, kc4, wr0, wc0, lr, kq, d);
+    else kc_chunk_full<CHAIN, 1>(X, U, kc4, wr0, wc0, lr, kq, d);
+    return;
+  }
+  for (int k = 0; k < kc4; k += 4) {
+    double av[2], bv[4];
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+      av[a] = ra[a] ? X[(wr0 + 8 * a + lr) * KC_XLD + k + kq] : 0.0;
+      if (CHAIN) av[a] = -av[a];
+    }
+#pragma unroll
+    for (int b = 0; b < 4; ++b) bv[b] = cb[b] ? U[(k + kq) * KC_ULD + wc0 + 8 * b + lr] : 0.0;
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        if (ra[a] && cb[b]) dmma884s(d[a][b], av[a], bv[b]);
+  }
+}
+
+template <bool CHAIN>
 __global__ void __launch_bounds__(FI_THREADS, KC_MINB_DEF) k_fi_upd_kc(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base) {
   const CallP P = *Pd;
   extern __shared__ __align__(16) double fs[];
@@ -1089,7 +1149,7 @@ __global__ void __launch_bounds__(FI_THREADS, KC_MINB_DEF) k_fi_upd_kc(DevSym S,
   // multipliers enter negated, so DMMA's chained FMAs subtract every source row's
   // product from the running value in (source, row) order; else they start at 0
   // and the sum is subtracted once in the epilogue
-  const bool chain = P.chain != 0 && true;
+  const bool chain = CHAIN;
   double d[2][4][2];
 #pragma unroll
   for (int a = 0; a < 2; ++a)
@@ -1191,22 +1251,7 @@ __global__ void __launch_bounds__(FI_THREADS, KC_MINB_DEF) k_fi_upd_kc(DevSym S,
       bool cb[4];
 #pragma unroll
       for (int b = 0; b < 4; ++b) cb[b] = ca[b] && ((bm >> b) & 1u);
-      if (ra[0] && (bm & 15u))
-        for (int k = 0; k < kc4; k += 4) {
-          double av[2], bv[4];
-#pragma unroll
-          for (int a = 0; a < 2; ++a) {
-            const double xv = ra[a] ? X[(wr0 + 8 * a + lr) * KC_XLD + k + kq] : 0.0;
-            av[a] = chain ? -xv : xv;
-          }
-#pragma unroll
-          for (int b = 0; b < 4; ++b) bv[b] = cb[b] ? U[(k + kq) * KC_ULD + wc0 + 8 * b + lr] : 0.0;
-#pragma unroll
-          for (int a = 0; a < 2; ++a)
-#pragma unroll
-            for (int b = 0; b < 4; ++b)
-              if (ra[a] && cb[b]) dmma884(d[a][b], av[a], bv[b]);
-        }
+      kc_chunk<CHAIN>(X, U, kc4, wr0, wc0, lr, kq, ra, cb, bm, d);
       if (!more) break;
       __syncthreads();   // buffer `buf` free for the chunk after next
       ck = nk; ck0 = nk0; buf ^= 1;
@@ -1238,6 +1283,7 @@ __global__ void __launch_bounds__(FI_THREADS, KC_MINB_DEF) k_fi_upd_kc(DevSym S,
 // own chunks), so a synchronisation round covers several sources; split-K parts of
 // outlier items publish partial tiles (tile column space) and the last part adds
 // them in part order.  Replaces k_fi_upd_pk (fanin_tc=5): c2 350 -> 340 ms.
+template <bool CHAIN>
 __global__ void __launch_bounds__(FI_THREADS, KC_MINB_DEF) k_fi_upd_kcp(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base) {
   const CallP P = *Pd;
   extern __shared__ __align__(16) double fs[];
@@ -1419,7 +1465,7 @@ __global__ void __launch_bounds__(FI_THREADS, KC_MINB_DEF) k_fi_upd_kcp(DevSym S
   // multipliers enter negated, so DMMA's chained FMAs subtract every source row's
   // product from the running value in (source, row) order; else they start at 0
   // and the sum is subtracted once in the epilogue
-  const bool chain = P.chain != 0 && part < 0;
+  const bool chain = CHAIN && part < 0;
   double d[2][4][2];
 #pragma unroll
   for (int a = 0; a < 2; ++a)
@@ -1500,22 +1546,8 @@ __global__ void __launch_bounds__(FI_THREADS, KC_MINB_DEF) k_fi_upd_kcp(DevSym S
       bool cb[4];
 #pragma unroll
       for (int b = 0; b < 4; ++b) cb[b] = ca[b] && ((bm >> b) & 1u);
-      if (ra[0] && (bm & 15u))
-        for (int k = 0; k < kc4; k += 4) {
-          double av[2], bv[4];
-#pragma unroll
-          for (int a = 0; a < 2; ++a) {
-            const double xv = ra[a] ? X[(wr0 + 8 * a + lr) * KC_XLD + k + kq] : 0.0;
-            av[a] = chain ? -xv : xv;
-          }
-#pragma unroll
-          for (int b = 0; b < 4; ++b) bv[b] = cb[b] ? U[(k + kq) * KC_ULD + wc0 + 8 * b + lr] : 0.0;
-#pragma unroll
-          for (int a = 0; a < 2; ++a)
-#pragma unroll
-            for (int b = 0; b < 4; ++b)
-              if (ra[a] && cb[b]) dmma884(d[a][b], av[a], bv[b]);
-        }
+      if (chain) kc_chunk<true>(X, U, kc4, wr0, wc0, lr, kq, ra, cb, bm, d);   // split-K parts: sums
+      else kc_chunk<false>(X, U, kc4, wr0, wc0, lr, kq, ra, cb, bm, d);
       if (more) {
         __syncthreads();   // buffer `buf` free for the chunk after next
         buf ^= 1;
@@ -1578,6 +1610,11 @@ __global__ void __launch_bounds__(FI_THREADS, KC_MINB_DEF) k_fi_upd_kcp(DevSym S
   }
   if (tid == 0) D.part_cnt[first] = 0;
 }
+
+template __global__ void k_fi_upd_kc<false>(DevSym, const CallP *, FaninDev, int);
+template __global__ void k_fi_upd_kc<true>(DevSym, const CallP *, FaninDev, int);
+template __global__ void k_fi_upd_kcp<false>(DevSym, const CallP *, FaninDev, int);
+template __global__ void k_fi_upd_kcp<true>(DevSym, const CallP *, FaninDev, int);
 
 size_t fi_upd_smem(int Smax, int Mmax) {
   (void)Mmax;
