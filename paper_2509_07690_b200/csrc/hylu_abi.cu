@@ -62,8 +62,10 @@ struct FaninDev {
   const int32_t *src_vW;
   const int32_t *src_qb;
   const int32_t *src_m;
+  const ItemRec *up_rec;     // [items] packed prologue records (k_item_rec)
 };
 __global__ void k_fi_scatter(DevSym, const CallP *);
+__global__ void k_item_rec(DevSym, FaninDev, int64_t, ItemRec *);
 __global__ void k_call_set(CallP *, CallP);
 __global__ void k_ptr_set(const double **, const double *);
 __global__ void k_call_prep(const CallP *, int, int64_t, int);
@@ -764,6 +766,18 @@ int hy_upload_fanin_plan(hy_handle *h, const hy_fanin_plan *d) {
   UPF(&p32, d->src_v, d->nsrc); D.src_v = p32;
   UPF(&p32, d->src_pb, d->nsrc); D.src_pb = p32;
   UPF(&p32, d->src_tb, d->nsrc); D.src_tb = p32;
+  {   // packed item records for the update kernels' prologue
+    const int64_t ni = d->lev_up[nl];
+    ItemRec *rec = nullptr;
+    CK(cudaMalloc((void **)&rec, sizeof(ItemRec) * (ni > 0 ? ni : 1)));
+    h->fi_allocs.push_back(rec);
+    if (ni > 0) {
+      k_item_rec<<<(unsigned)std::min<int64_t>((ni + 255) / 256, 4096), 256>>>(h->S, D, ni, rec);
+      CK(cudaGetLastError());
+      CK(cudaDeviceSynchronize());
+    }
+    D.up_rec = rec;
+  }
   h->fi_lu.assign(d->lu_ptr, d->lu_ptr + nl + 1);
   h->fi_pt.assign(d->pt_ptr, d->pt_ptr + nl + 1);
   h->fi_xp.assign(d->xp_ptr, d->xp_ptr + nl + 1);

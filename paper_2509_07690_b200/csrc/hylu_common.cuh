@@ -28,6 +28,19 @@ struct DevSym {
   const int64_t *perm;      // [n]
 };
 
+// Fan-in update item (target node, 64-column tile) in one 32-byte record, built on
+// the device at plan upload (k_item_rec): the update kernels get everything their
+// prologue needs from one load instead of two dependent rounds (item -> node).
+struct __align__(16) ItemRec {
+  int64_t valoff;   // target node's value offset
+  int64_t zb;       // first source record
+  int32_t nz;       // source records
+  int32_t W;        // target width (row pitch)
+  int32_t c0;       // tile columns [c0, c0 + tw) of the target's column list
+  int16_t s;        // target rows (<= 64)
+  int16_t tw;       // tile width (<= 64)
+};
+
 // Per-call parameters (single-instance path).
 struct CallP {
   double *F;                 // factor values (node layout)

@@ -58,6 +58,7 @@ struct FaninDev {
   const int32_t *src_vW;     // source node width
   const int32_t *src_qb;     // first panel column of the record in the source
   const int32_t *src_m;      // source block rows from the first present one
+  const ItemRec *up_rec;     // [items] packed prologue records (k_item_rec)
 };
 
 constexpr int FI_THREADS = 256;
@@ -1024,21 +1025,22 @@ __global__ void __launch_bounds__(FI_THREADS, KC_MINB_DEF) k_fi_upd_kc(DevSym S,
   __shared__ int s_vW[KC_NSB], s_qb[KC_NSB], s_pb[KC_NSB], s_tb[KC_NSB], s_m[KC_NSB];
   __shared__ unsigned s_bm[KC_NSB];   // 8-column blocks (compact space) a source touches
   const int j = base + blockIdx.x;
-  const int T = D.up_t[j];
-  const int c0 = D.up_c0[j], c1 = D.up_c1[j];
-  const int tw = c1 - c0;
+  const ItemRec ir = D.up_rec[j];
+  const int c0 = ir.c0;
+  const int tw = ir.tw;
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31, kq = lane & 3, lr = lane >> 2;
-  const int r = (int)S.first[T];
-  const int s = (int)(S.first[T + 1] - r);
-  const int64_t tc0 = S.colptr[T];
-  const int W = (int)(S.colptr[T + 1] - tc0);
-  double *Pm = P.F + S.valoff[T];
+  const int s = ir.s;
+  const int W = ir.W;
+  double *Pm = P.F + ir.valoff;
   constexpr int KC_BUF = KC_STAGE;
   int8_t *inv = reinterpret_cast<int8_t *>(fs + 2 * KC_BUF);   // [KC_NSB][64] source col -> compact col
-  const int64_t zb = D.up_ptr[j], ze = D.up_ptr[j + 1];
+  const int64_t zb = ir.zb, ze = ir.zb + ir.nz;
   const bool compact = ze - zb <= KC_NSB;
-  for (int c = tid; c < tw; c += FI_THREADS) tcol[c] = S.cols[tc0 + c0 + c];
+  if (!D.src_pos || !compact) {   // the tile's column indices, for the column-map searches
+    const int64_t tc0 = S.colptr[D.up_t[j]];
+    for (int c = tid; c < tw; c += FI_THREADS) tcol[c] = S.cols[tc0 + c0 + c];
+  }
   if (tid < FI_TILE) cidx[tid] = compact ? -1 : (int8_t)tid;
   __syncthreads();
   if (compact) {
@@ -1299,23 +1301,24 @@ __global__ void __launch_bounds__(FI_THREADS, KC_MINB_DEF) k_fi_upd_kcp(DevSym S
   __shared__ int s_cst[KC_NSB * 64 / 4 + KC_NSB + 2];   // chunk start rows (+ end)
   __shared__ int s_nch;
   const int j = base + blockIdx.x;
-  const int T = D.up_t[j];
-  const int c0 = D.up_c0[j], c1 = D.up_c1[j];
-  const int tw = c1 - c0;
+  const ItemRec ir = D.up_rec[j];
+  const int c0 = ir.c0;
+  const int tw = ir.tw;
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31, kq = lane & 3, lr = lane >> 2;
-  const int r = (int)S.first[T];
-  const int s = (int)(S.first[T + 1] - r);
-  const int64_t tc0 = S.colptr[T];
-  const int W = (int)(S.colptr[T + 1] - tc0);
-  double *Pm = P.F + S.valoff[T];
+  const int s = ir.s;
+  const int W = ir.W;
+  double *Pm = P.F + ir.valoff;
   constexpr int KC_BUF = KC_STAGE;
   int8_t *inv = reinterpret_cast<int8_t *>(fs + 2 * KC_BUF);   // [KC_NSB][64] source col -> compact col
   const int part = D.up_part ? D.up_part[j] : -1;               // split-K part (packed items)
-  const int64_t zb = D.up_ptr[j], ze = D.up_ptr[j + 1];
+  const int64_t zb = ir.zb, ze = ir.zb + ir.nz;
   // split-K parts publish whole tiles: no column compaction for them
   const bool compact = ze - zb <= KC_NSB && part < 0;
-  for (int c = tid; c < tw; c += FI_THREADS) tcol[c] = S.cols[tc0 + c0 + c];
+  if (!D.src_pos || !compact) {   // the tile's column indices, for the column-map searches
+    const int64_t tc0 = S.colptr[D.up_t[j]];
+    for (int c = tid; c < tw; c += FI_THREADS) tcol[c] = S.cols[tc0 + c0 + c];
+  }
   if (tid < FI_TILE) cidx[tid] = compact ? -1 : (int8_t)tid;
   __syncthreads();
   // per-source metadata and column maps of a batch of <= KC_NSB sources; `pos`
@@ -1609,6 +1612,22 @@ __global__ void __launch_bounds__(FI_THREADS, KC_MINB_DEF) k_fi_upd_kcp(DevSym S
     Pm[(int64_t)t * W + c0 + c] -= sum;
   }
   if (tid == 0) D.part_cnt[first] = 0;
+}
+
+__global__ void k_item_rec(DevSym S, FaninDev D, int64_t nitems, ItemRec *out) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nitems;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int T = D.up_t[j];
+    ItemRec r;
+    r.valoff = S.valoff[T];
+    r.zb = D.up_ptr[j];
+    r.nz = (int32_t)(D.up_ptr[j + 1] - r.zb);
+    r.W = (int32_t)(S.colptr[T + 1] - S.colptr[T]);
+    r.s = (int16_t)(S.first[T + 1] - S.first[T]);
+    r.c0 = D.up_c0[j];
+    r.tw = (int16_t)(D.up_c1[j] - D.up_c0[j]);
+    out[j] = r;
+  }
 }
 
 template __global__ void k_fi_upd_kc<false>(DevSym, const CallP *, FaninDev, int);
