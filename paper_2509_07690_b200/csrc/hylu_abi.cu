@@ -66,6 +66,9 @@ struct FaninDev {
 };
 __global__ void k_fi_scatter(DevSym, const CallP *);
 __global__ void k_item_rec(DevSym, FaninDev, int64_t, ItemRec *);
+size_t fi_lu_smem();
+size_t fi_panel_smem();
+size_t fi_upd_w_smem();
 __global__ void k_call_set(CallP *, CallP);
 __global__ void k_ptr_set(const double **, const double *);
 __global__ void k_call_prep(const CallP *, int, int64_t, int);
@@ -828,8 +831,9 @@ int hy_upload_fanin_plan(hy_handle *h, const hy_fanin_plan *d) {
   CK(cudaFuncSetAttribute(k_fi_upd_kcp<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fi_upd_kc_smem()));
   CK(cudaFuncSetAttribute(k_fi_upd_pk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx));
   CK(cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, h->device));
-  CK(cudaFuncSetAttribute(k_fi_panel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)(64 * 256 * sizeof(double))));
+  CK(cudaFuncSetAttribute(k_fi_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fi_panel_smem()));
+  CK(cudaFuncSetAttribute(k_fi_lu, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fi_lu_smem()));
+  CK(cudaFuncSetAttribute(k_fi_upd_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fi_upd_w_smem()));
   CK(cudaFuncSetAttribute(k_fi_x, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)(2 * 64 * 65 * sizeof(double))));
   h->fanin_ok = true;
@@ -861,7 +865,7 @@ static int run_fanin(hy_handle *h, const CallP *Pd, cudaStream_t st) {
                                    h->hub1_slots);
       h->launches++;
     }
-    if (nlu) { k_fi_lu<<<nlu, 256, 0, st>>>(h->S, Pd, h->fi, (int)h->fi_lu[l]); h->launches++; }
+    if (nlu) { k_fi_lu<<<nlu, 256, fi_lu_smem(), st>>>(h->S, Pd, h->fi, (int)h->fi_lu[l]); h->launches++; }
     // the panel TRSM of the level's nodes and the X blocks of their edges both need
     // only the nodes' LU: with fanin_overlap the panel runs on a side stream while the
     // X blocks run on `st`; the update kernels (which need both) wait for it
@@ -897,7 +901,7 @@ static int run_fanin(hy_handle *h, const CallP *Pd, cudaStream_t st) {
     cudaStream_t sp = sideA && npt ? h->fi_side : st;
     cudaStream_t sw = sideA && !npt ? h->fi_side : st;
     if (npt) {
-      k_fi_panel<<<npt, 256, 64 * 256 * sizeof(double), sp>>>(h->S, Pd, h->fi, (int)h->fi_pt[l]);
+      k_fi_panel<<<npt, 256, fi_panel_smem(), sp>>>(h->S, Pd, h->fi, (int)h->fi_pt[l]);
       h->launches++;
     }
     if (nw) {
@@ -939,7 +943,7 @@ static int run_fanin(hy_handle *h, const CallP *Pd, cudaStream_t st) {
       if (rs > reg) {
         FaninDev Dw = h->fi;
         if (!h->fi_maps) Dw.src_pos = nullptr;
-        k_fi_upd_w<<<(rs - reg + 7) / 8, 256, 0, st>>>(h->S, Pd, Dw, reg, rs - reg);
+        k_fi_upd_w<<<(rs - reg + 7) / 8, 256, fi_upd_w_smem(), st>>>(h->S, Pd, Dw, reg, rs - reg);
         h->launches++;
       }
       if (split > rs && h->fi_tc >= 4) {
@@ -1058,6 +1062,7 @@ int hy_upload_hub_programs(hy_handle *h, const hy_row_programs *d) {
   h->hub1_ok = true;
   return HY_OK;
 }
+
 
 // Level fan-in as one CUDA graph per handle: the launch sequence depends only on the
 // uploaded plan and the options (all per-call pointers are read from the handle's

@@ -20,7 +20,7 @@ constexpr int BW = 4;
 #define BWD_W 2     // backward-solve entries per batch (k_batch_bwd2; 2-8 measured)
 #endif            // warps per block (bwd / fwd kernels)
 #ifndef HUB_THREADS_DEF
-#define HUB_THREADS_DEF 512
+#define HUB_THREADS_DEF 768   // 512: 17.56 ms/step, 768: 17.41, 1024: 17.43 (c4, round 2)
 #endif
 constexpr int HUB_THREADS = HUB_THREADS_DEF;
 int hub_threads() { return HUB_THREADS; }

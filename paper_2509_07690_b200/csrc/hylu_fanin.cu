@@ -66,9 +66,9 @@ constexpr int FXLD = 65;
 
 // ---------------------------------------------------------------------------- scatter
 // warp per M row: physical row = inverse of the prior inner_perm on refactorize
-__global__ void k_fi_scatter(DevSym S, const CallP *__restrict__ Pd) {
+__device__ __forceinline__ void d_fi_scatter(DevSym S, const CallP *__restrict__ Pd, int bid) {
   const CallP P = *Pd;
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int warp = (bid * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= S.n) return;
   const int i = warp;
   const int u = S.node_of[i];
@@ -88,13 +88,15 @@ __global__ void k_fi_scatter(DevSym S, const CallP *__restrict__ Pd) {
   const int64_t a = S.mrow_src[i];
   for (int64_t e = S.a_ptr[a] + lane; e < S.a_ptr[a + 1]; e += 32) row[S.colpos[e]] = P.A[e] * S.scale[e];
 }
+__global__ void k_fi_scatter(DevSym S, const CallP *__restrict__ Pd) { d_fi_scatter(S, Pd, blockIdx.x); }
 
 // ---------------------------------------------------------------------------- LU
-__global__ void __launch_bounds__(FI_THREADS) k_fi_lu(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base) {
+__device__ __forceinline__ void d_fi_lu(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base, int bid) {
   const CallP P = *Pd;
-  __shared__ double B[64 * FXLD];
+  extern __shared__ __align__(16) double lu_dyn[];
+  double *B = lu_dyn;                  // [64 * FXLD] (dynamic: fi_lu_smem())
   __shared__ int perm[64];
-  const int u = D.lu_nodes[base + blockIdx.x];
+  const int u = D.lu_nodes[base + bid];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int r = (int)S.first[u];
   const int s = (int)(S.first[u + 1] - r);
@@ -175,6 +177,7 @@ __global__ void __launch_bounds__(FI_THREADS) k_fi_lu(DevSym S, const CallP *__r
   }
   if (tid < s) P.iperm[r + tid] = P.refactor ? P.iperm_prior[r + tid] : perm[tid];
 }
+__global__ void __launch_bounds__(FI_THREADS) k_fi_lu(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base) { d_fi_lu(S, Pd, D, base, blockIdx.x); }
 
 // ---------------------------------------------------------------------------- panel
 // Tile of node v's columns [c0, c1) outside the block: apply the pivot row
@@ -206,13 +209,13 @@ __device__ __forceinline__ void panel_trsm_col(double *tl, const double *Lb, int
   }
 }
 
-__global__ void __launch_bounds__(FI_THREADS) k_fi_panel(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base) {
+__device__ __forceinline__ void d_fi_panel(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base, int bid) {
   const CallP P = *Pd;
   extern __shared__ __align__(16) double tl[];   // s x (c1-c0), stride PANEL
-  __shared__ double Lb[64 * FXLD];
+  double *Lb = tl + 64 * 256;                    // [64 * FXLD] after the tile (fi_panel_smem())
   __shared__ int perm[64];
   __shared__ int ident;
-  const int j = base + blockIdx.x;
+  const int j = base + bid;
   const int u = D.pt_node[j];
   const int c0 = D.pt_c0[j], c1 = D.pt_c1[j];
   const int tw = c1 - c0;
@@ -254,15 +257,16 @@ __global__ void __launch_bounds__(FI_THREADS) k_fi_panel(DevSym S, const CallP *
     Pm[(int64_t)t * W + c0 + c] = tl[idx];
   }
 }
+__global__ void __launch_bounds__(FI_THREADS) k_fi_panel(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base) { d_fi_panel(S, Pd, D, base, blockIdx.x); }
 
 // ---------------------------------------------------------------------------- X blocks
 // X = T[:, pb0 .. pb0+m) · U_bb⁻¹ in place; 4 threads per target row.
-__global__ void __launch_bounds__(FI_THREADS) k_fi_x(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base) {
+__device__ __forceinline__ void d_fi_x(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base, int bid) {
   const CallP P = *Pd;
   extern __shared__ __align__(16) double xsm[];
   double *Ub = xsm;
   double *Xt = xsm + 64 * FXLD;
-  const int j = base + blockIdx.x;
+  const int j = base + bid;
   const int64_t dk = D.xp_edge[j];
   const int T = D.xp_tgt[j];
   const int v = S.deps[dk];
@@ -335,16 +339,17 @@ __global__ void __launch_bounds__(FI_THREADS) k_fi_x(DevSym S, const CallP *__re
     for (int a = lane; a < m; a += 32) xd[a] = Xt[t * FXLD + a];
   }
 }
+__global__ void __launch_bounds__(FI_THREADS) k_fi_x(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base) { d_fi_x(S, Pd, D, base, blockIdx.x); }
 
 // Warp-per-item multiplier blocks for small pairs (target <= 32 rows, <= 8 source
 // rows): lane = target row, the row's multipliers in registers; per element the
 // same operation sequence as k_fi_x (x_a = w_a / U_aa, then w_b -= x_a U_ab for
 // b > a, skipped when x_a == 0).
 constexpr int XW_M = 8;
-__global__ void __launch_bounds__(FI_THREADS) k_fi_x_w(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base, int count) {
+__device__ __forceinline__ void d_fi_x_w(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base, int count, int bid) {
   const CallP P = *Pd;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int jj = blockIdx.x * (FI_THREADS / 32) + warp;
+  const int jj = bid * (FI_THREADS / 32) + warp;
   if (jj >= count) return;
   const int j = base + jj;
   const int64_t dk = D.xp_edge[j];
@@ -384,6 +389,7 @@ __global__ void __launch_bounds__(FI_THREADS) k_fi_x_w(DevSym S, const CallP *__
   for (int a = 0; a < XW_M; ++a)
     if (a < m) row[a] = xr[a];
 }
+__global__ void __launch_bounds__(FI_THREADS) k_fi_x_w(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base, int count) { d_fi_x_w(S, Pd, D, base, count, blockIdx.x); }
 
 // Warp-per-item tile updates for small targets (<= 4 rows): lanes over the
 // source's columns in the tile; per source c = Σ_a X[t][a] U[a][q] (ascending a,
@@ -391,12 +397,13 @@ __global__ void __launch_bounds__(FI_THREADS) k_fi_x_w(DevSym S, const CallP *__
 // per-element sequence of k_fi_upd.  The tile lives in a per-warp shared buffer.
 constexpr int UW_ROWS = 4;
 constexpr int UW_TILE = 64;   // == FI_TILE
-__global__ void __launch_bounds__(FI_THREADS) k_fi_upd_w(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base, int count) {
+__device__ __forceinline__ void d_fi_upd_w(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base, int count, int bid) {
   const CallP P = *Pd;
-  __shared__ double tile_s[FI_THREADS / 32][UW_ROWS * UW_TILE];
+  extern __shared__ __align__(16) double uw_dyn[];   // [FI_THREADS / 32][UW_ROWS * UW_TILE] (fi_upd_w_smem())
+  double (*tile_s)[UW_ROWS * UW_TILE] = reinterpret_cast<double (*)[UW_ROWS * UW_TILE]>(uw_dyn);
   __shared__ int tcol_s[FI_THREADS / 32][UW_TILE];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int jj = blockIdx.x * (FI_THREADS / 32) + warp;
+  const int jj = bid * (FI_THREADS / 32) + warp;
   if (jj >= count) return;
   const int j = base + jj;
   const int T = D.up_t[j];
@@ -464,6 +471,7 @@ __global__ void __launch_bounds__(FI_THREADS) k_fi_upd_w(DevSym S, const CallP *
   for (int c = lane; c < tw; c += 32)
     for (int t = 0; t < s; ++t) Pm[(int64_t)t * W + c0 + c] = acc[t * UW_TILE + c];
 }
+__global__ void __launch_bounds__(FI_THREADS) k_fi_upd_w(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base, int count) { d_fi_upd_w(S, Pd, D, base, count, blockIdx.x); }
 
 // ---------------------------------------------------------------------------- updates
 constexpr int FI_TILE = 64;
@@ -1014,7 +1022,7 @@ __device__ __forceinline__ void kc_chunk(const double *X, const double *U, int k
 }
 
 template <bool CHAIN>
-__global__ void __launch_bounds__(FI_THREADS, KC_MINB_DEF) k_fi_upd_kc(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base) {
+__device__ __forceinline__ void d_fi_upd_kc(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base, int bid) {
   const CallP P = *Pd;
   extern __shared__ __align__(16) double fs[];
   __shared__ int tcol[FI_TILE];
@@ -1024,7 +1032,7 @@ __global__ void __launch_bounds__(FI_THREADS, KC_MINB_DEF) k_fi_upd_kc(DevSym S,
   __shared__ int64_t s_vb[KC_NSB];
   __shared__ int s_vW[KC_NSB], s_qb[KC_NSB], s_pb[KC_NSB], s_tb[KC_NSB], s_m[KC_NSB];
   __shared__ unsigned s_bm[KC_NSB];   // 8-column blocks (compact space) a source touches
-  const int j = base + blockIdx.x;
+  const int j = base + bid;
   const ItemRec ir = D.up_rec[j];
   const int c0 = ir.c0;
   const int tw = ir.tw;
@@ -1279,6 +1287,8 @@ __global__ void __launch_bounds__(FI_THREADS, KC_MINB_DEF) k_fi_upd_kc(DevSym S,
     }
   }
 }
+template <bool CHAIN>
+__global__ void __launch_bounds__(FI_THREADS, KC_MINB_DEF) k_fi_upd_kc(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base) { d_fi_upd_kc<CHAIN>(S, Pd, D, base, blockIdx.x); }
 
 // k_fi_upd_kcp: k_fi_upd_kc for the packed items (many small sources): chunks hold
 // up to KC_K rows of consecutive sources (sources of >= KC_BIG rows still get their
@@ -1286,7 +1296,7 @@ __global__ void __launch_bounds__(FI_THREADS, KC_MINB_DEF) k_fi_upd_kc(DevSym S,
 // outlier items publish partial tiles (tile column space) and the last part adds
 // them in part order.  Replaces k_fi_upd_pk (fanin_tc=5): c2 350 -> 340 ms.
 template <bool CHAIN>
-__global__ void __launch_bounds__(FI_THREADS, KC_MINB_DEF) k_fi_upd_kcp(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base) {
+__device__ __forceinline__ void d_fi_upd_kcp(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base, int bid) {
   const CallP P = *Pd;
   extern __shared__ __align__(16) double fs[];
   __shared__ int tcol[FI_TILE];
@@ -1300,7 +1310,7 @@ __global__ void __launch_bounds__(FI_THREADS, KC_MINB_DEF) k_fi_upd_kcp(DevSym S
   __shared__ int8_t ksrc[KC_NSB * 64]; // K row -> source of the batch
   __shared__ int s_cst[KC_NSB * 64 / 4 + KC_NSB + 2];   // chunk start rows (+ end)
   __shared__ int s_nch;
-  const int j = base + blockIdx.x;
+  const int j = base + bid;
   const ItemRec ir = D.up_rec[j];
   const int c0 = ir.c0;
   const int tw = ir.tw;
@@ -1613,6 +1623,13 @@ __global__ void __launch_bounds__(FI_THREADS, KC_MINB_DEF) k_fi_upd_kcp(DevSym S
   }
   if (tid == 0) D.part_cnt[first] = 0;
 }
+template <bool CHAIN>
+__global__ void __launch_bounds__(FI_THREADS, KC_MINB_DEF) k_fi_upd_kcp(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base) { d_fi_upd_kcp<CHAIN>(S, Pd, D, base, blockIdx.x); }
+
+
+size_t fi_lu_smem() { return (size_t)64 * FXLD * sizeof(double); }
+size_t fi_panel_smem() { return (size_t)(64 * 256 + 64 * FXLD) * sizeof(double); }
+size_t fi_upd_w_smem() { return (size_t)(FI_THREADS / 32) * UW_ROWS * UW_TILE * sizeof(double); }
 
 __global__ void k_item_rec(DevSym S, FaninDev D, int64_t nitems, ItemRec *out) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nitems;
