@@ -113,14 +113,8 @@ __global__ void k_fwd_fin(DevSym, const double *const *, const int32_t *, const 
 __global__ void k_bwd_fin(DevSym, const double *const *, const int32_t *, const int32_t *, const int32_t *, int,
                           const double *, double *);
 __global__ void k_bwd(DevSym, const double *, const int32_t *, int, double *);
-struct TaskDesc {
-  int32_t u, g;
-  int64_t valoff;
-  int32_t r, s, W, L;
-  int64_t d0, d1;
-  longlong4 rr0;   // layout shared with hylu_batch.cu
-  int32_t dep[4];
-};
+
+size_t pipe_smem(int ws);
 __global__ void k_bt_pipe2(DevSym, BatchP, DevProg, const TaskDesc *, int64_t, const double *, double *, int *,
                            int *, int, int, int);
 __global__ void k_bt_hub(DevSym, BatchP, DevProg, const int32_t *, int, int, const double *, double *,
@@ -182,6 +176,8 @@ struct hy_handle {
   // host copies of per-node data for descriptor building
   std::vector<int64_t> h_first, h_colptr, h_valoff, h_dptr, h_nl;
   std::vector<longlong4> h_row_rec;   // batched row programs' row records (task descriptors)
+  struct Win { int64_t rel0, k0, nk, nrel; };
+  std::vector<Win> h_win;              // per node: program window (nk == 0: not staged)
   std::vector<int32_t> h_deps;        // dependency lists (task descriptors inline the first 4)
   double *d_y = nullptr;          // single-solve workspace [n]
   double *d_bf = nullptr;         // batched factor workspace
@@ -392,6 +388,12 @@ static int build_segments(hy_handle *h, int G) {
       t.d0 = h->h_dptr[u];
       t.d1 = h->h_dptr[u + 1];
       t.rr0 = h->h_row_rec[t.r];
+      const hy_handle::Win &w = h->h_win[u];
+      t.rel0 = w.rel0;
+      t.k0 = (int32_t)w.k0;
+      t.nk = (int32_t)w.nk;
+      t.nrel = (int32_t)w.nrel;
+      t.pad[0] = t.pad[1] = t.pad[2] = 0;
       for (int k = 0; k < 4; ++k)
         t.dep[k] = t.d0 + k < t.d1 ? h->h_deps[t.d0 + k] : -1;
       return t;
@@ -486,7 +488,7 @@ int hy_create(int device, hy_handle **out) {
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_bt_hub, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hub_smem_bytes());
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_bt_pipe2, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 2 * 64 * 32 * 8);
+    e = cudaFuncSetAttribute(k_bt_pipe2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pipe_smem(64));
   if (e != cudaSuccess) {
     delete h;
     return fail(HY_CUDA_ERROR, std::string("cudaFuncSetAttribute(k_bt_pipe): ") + cudaGetErrorString(e));
@@ -1452,7 +1454,40 @@ int hy_upload_row_programs(hy_handle *h, const hy_row_programs *d) {
   UPP(&p64, d->st_src, d->nsteps); R.st_src = p64;
   UPP(&p32, d->st_cnt, d->nsteps); R.st_cnt = p32;
   UPP(&p64, d->st_rel, d->nsteps); R.st_rel = p64;
-  UPP(&p32, d->rel, d->nrel); R.rel = p32;
+  {   // rel padded by 4 entries: the pipeline's aligned bulk copy of a window may read past the end
+    std::vector<int32_t> relp(d->rel, d->rel + d->nrel);
+    relp.resize(d->nrel + 4, 0);
+    UPP(&p32, relp.data(), d->nrel + 4); R.rel = p32;
+  }
+  {   // packed step records + per-node program windows (k_bt_pipe2 stages them in shared memory)
+    const int64_t ns = d->nsteps;
+    bool ok = h->stored < ((int64_t)1 << 31);
+    std::vector<StepRec> rec(ns + 1);
+    for (int64_t k = 0; k < ns && ok; ++k) {
+      rec[k].p = d->st_p[k];
+      rec[k].src = (int32_t)d->st_src[k];
+      rec[k].j = d->st_j[k];
+      if (d->st_cnt[k] > 32767) ok = false;
+      rec[k].cnt = (int16_t)d->st_cnt[k];
+      rec[k].rl = 0;
+    }
+    h->h_win.assign(nn, {0, 0, 0, 0});
+    for (int64_t u = 0; u < nn && ok; ++u) {
+      const int64_t k0 = d->row_ptr[h->h_first[u]], k1 = d->row_ptr[h->h_first[u + 1]];
+      if (k1 <= k0) continue;
+      const int64_t rel0 = d->st_rel[k0];
+      const int64_t nrel = d->st_rel[k1 - 1] + d->st_cnt[k1 - 1] - rel0;
+      if (k1 - k0 > PIPE_REC_CAP || nrel + 6 > PIPE_REL_CAP) continue;   // not stageable
+      for (int64_t k = k0; k < k1; ++k) rec[k].rl = (int16_t)(d->st_rel[k] - rel0);
+      h->h_win[u] = {rel0, k0, k1 - k0, nrel};
+    }
+    R.st_rec = nullptr;
+    if (ok) {
+      StepRec *q;
+      UPP(&q, rec.data(), ns + 1);
+      R.st_rec = q;
+    }
+  }
   std::vector<int32_t> hub_base(nn, -1);
   std::vector<int64_t> first(nn + 1);
   CK(cudaMemcpy(first.data(), h->S.first, sizeof(int64_t) * (nn + 1), cudaMemcpyDeviceToHost));
@@ -1578,7 +1613,7 @@ int hy_refactorize_batched(hy_handle *h, int64_t B, const double *d_vals, double
   if (h->pipe_blocks == 0) {
     int per_sm = 0, sms = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bt_pipe2, 128,
-                                                     (size_t)4 * 2 * h->pipe_ws * 32 * 8));
+                                                     pipe_smem(h->pipe_ws)));
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
     h->pipe_blocks = per_sm * sms;
   }
@@ -1608,7 +1643,7 @@ int hy_refactorize_batched(hy_handle *h, int64_t B, const double *d_vals, double
     }
     if (sg.ntasks) {
       int *ctr = (int *)((long long *)h->d_counters + si);
-      k_bt_pipe2<<<h->pipe_blocks, 128, (size_t)4 * 2 * h->pipe_ws * 32 * 8, st>>>(
+      k_bt_pipe2<<<h->pipe_blocks, 128, pipe_smem(h->pipe_ws), st>>>(
           h->S, P, h->prog, sg.d_tasks, sg.ntasks, d_b_fuse, h->d_by, ctr, h->d_flags, h->epoch, G,
           h->pipe_ws);
       h->launches++;

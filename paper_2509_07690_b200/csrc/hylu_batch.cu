@@ -79,14 +79,7 @@ constexpr int PIPE_WARPS = 4;
 // a resident warp, so the earliest unfinished claimed task can always proceed.
 // Task descriptor (built on the host in claim order): everything a task needs
 // before its first data load, in one 48-byte record.
-struct TaskDesc {
-  int32_t u, g;
-  int64_t valoff;
-  int32_t r, s, W, L;
-  int64_t d0, d1;
-  longlong4 rr0;   // row record of the node's first row (no dependent load for it)
-  int32_t dep[4];  // the first (up to) 4 dependencies, inline (no dependent index load)
-};
+
 
 // ---------------------------------------------------------------------------
 // Pair mode: one warp runs the same node for two adjacent groups (g, g+1), lane =
@@ -163,6 +156,64 @@ __device__ __forceinline__ void run_steps2(const DevProg &R, int64_t s0, int64_t
   }
 }
 
+// run_steps2 over a program window staged in shared memory (packed step records and
+// the window's target positions): the index loads of every step become shared loads.
+template <typename WPtr>
+__device__ __forceinline__ void run_steps2s(const StepRec *rec, const int32_t *relw, int s0, int s1, WPtr wa,
+                                            WPtr wc, const double *ga, const double *gc,
+                                            const double *ya, const double *yc, double &acA,
+                                            double &acC) {
+  if (s0 >= s1) return;
+  StepRec cr = rec[s0];
+  double da = __ldcg(ga + (int64_t)cr.src * 32), dc = __ldcg(gc + (int64_t)cr.src * 32);
+  double yja = __ldcg(ya + (int64_t)cr.j * 32), yjc = __ldcg(yc + (int64_t)cr.j * 32);
+  for (int st = s0; st < s1; ++st) {
+    StepRec nx = cr;
+    double dna = 1.0, dnc = 1.0, yna = 0.0, ync = 0.0;
+    if (st + 1 < s1) {
+      nx = rec[st + 1];
+      dna = __ldcg(ga + (int64_t)nx.src * 32);
+      dnc = __ldcg(gc + (int64_t)nx.src * 32);
+      yna = __ldcg(ya + (int64_t)nx.j * 32);
+      ync = __ldcg(yc + (int64_t)nx.j * 32);
+    }
+    const int p = cr.p, cnt = cr.cnt;
+    const int32_t *rl = relw + cr.rl;
+    const double *ua = ga + ((int64_t)cr.src + 1) * 32;
+    const double *uc = gc + ((int64_t)cr.src + 1) * 32;
+    const double la = wa[p * 32] / da;
+    const double lc = wc[p * 32] / dc;
+    wa[p * 32] = la;
+    wc[p * 32] = lc;
+    acA -= la * yja;
+    acC -= lc * yjc;
+    for (int q = 0; q < cnt; q += P2W) {
+      int t[P2W];
+      double xa[P2W], xc[P2W];
+#pragma unroll
+      for (int k = 0; k < P2W; ++k) {
+        const bool ok = q + k < cnt;
+        t[k] = ok ? rl[q + k] : 0;
+        xa[k] = ok ? __ldcg(ua + (q + k) * 32) : 0.0;
+        xc[k] = ok ? __ldcg(uc + (q + k) * 32) : 0.0;
+      }
+      double va[P2W], vc[P2W];
+#pragma unroll
+      for (int k = 0; k < P2W; ++k) {
+        va[k] = wa[t[k] * 32];
+        vc[k] = wc[t[k] * 32];
+      }
+#pragma unroll
+      for (int k = 0; k < P2W; ++k)
+        if (q + k < cnt) {
+          wa[t[k] * 32] = va[k] - la * xa[k];
+          wc[t[k] * 32] = vc[k] - lc * xc[k];
+        }
+    }
+    cr = nx; da = dna; dc = dnc; yja = yna; yjc = ync;
+  }
+}
+
 // Row initialisation of a pair task: zero the accumulators, scatter the row's
 // matrix values (lanes over (instance, entry) pairs, 4 per lane per batch, loads
 // before stores) and form b̂_i for both groups.  Needs no dependency: the pipeline
@@ -217,7 +268,9 @@ __device__ __forceinline__ void row_init2(const DevSym &S, const BatchP &P, cons
 __device__ __forceinline__ void bt_node2(const DevSym &S, const BatchP &P, const DevProg &R,
                                          const longlong4 nr, int g, const double *rhs, double *Y,
                                          double *wsm0, int ws, int lane, int xmask, longlong4 rr,
-                                         bool pre0, double y0A, double y0C) {
+                                         bool pre0, double y0A, double y0C,
+                                         const StepRec *srec = nullptr, const int32_t *srel = nullptr,
+                                         int64_t sk0 = 0) {
   const int64_t ba = (int64_t)g * 32 + lane, bc = ba + 32;
   const bool liveA = ba < P.B, liveC = bc < P.B;
   const int64_t rem = P.B - (int64_t)g * 32;
@@ -248,7 +301,14 @@ __device__ __forceinline__ void bt_node2(const DevSym &S, const BatchP &P, const
                 ya + (int64_t)i * 32, yc + (int64_t)i * 32);
     if (t + 1 < s) rr = R.row_rec[i + 1];
     if (!(xmask & 2)) {
-      if (inSm)
+      if (srec) {
+        if (inSm)
+          run_steps2s(srec, srel, (int)(s0 - sk0), (int)(s1 - sk0), wA + lane, wC + lane, ga0 + lane,
+                      gc0 + lane, ya, yc, yaccA, yaccC);
+        else
+          run_steps2s(srec, srel, (int)(s0 - sk0), (int)(s1 - sk0), growA + lane, growC + lane, ga0 + lane,
+                      gc0 + lane, ya, yc, yaccA, yaccC);
+      } else if (inSm)
         run_steps2(R, s0, s1, wA + lane, wC + lane, ga0 + lane, gc0 + lane, ya, yc, yaccA, yaccC);
       else
         run_steps2(R, s0, s1, growA + lane, growC + lane, ga0 + lane, gc0 + lane, ya, yc, yaccA, yaccC);
@@ -278,12 +338,50 @@ __device__ __forceinline__ void bt_node2(const DevSym &S, const BatchP &P, const
 #ifndef PIPE_ACQ
 #define PIPE_ACQ 2   // consumer acquire: 2 (default) one ld.acquire per observed flag after the relaxed spin, 1 one fence after the polls (+0.25 ms/step), 0 none (formally racy)
 #endif
+// Per-warp staging area after the 4 warps' accumulators: an mbarrier, the task's
+// step records and its rel window (bulk copies issued at claim, before the polls).
+constexpr int PIPE_STAGE = 16 + PIPE_REC_CAP * 16 + PIPE_REL_CAP * 4;
+size_t pipe_smem(int ws) { return (size_t)PIPE_WARPS * (2 * ws * 32 * 8 + PIPE_STAGE); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(d), "l"(src), "r"(bytes), "r"(b) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  unsigned done = 0;
+  while (!done)
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done) : "r"(a), "r"(phase) : "memory");
+}
+
 __global__ void __launch_bounds__(PIPE_WARPS * 32, PIPE_MINB_DEF)
     k_bt_pipe2(DevSym S, BatchP P, DevProg R, const TaskDesc *tasks, int64_t total, const double *rhs,
                double *Y, int *counter, int *flags, int epoch, int G, int ws) {
   extern __shared__ __align__(16) double pipe_smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double *wsm_w = pipe_smem + (size_t)warp * 2 * ws * 32;
+  unsigned char *stg = reinterpret_cast<unsigned char *>(pipe_smem + (size_t)PIPE_WARPS * 2 * ws * 32) +
+                       (size_t)warp * PIPE_STAGE;
+  uint64_t *mbar = reinterpret_cast<uint64_t *>(stg);
+  StepRec *srec = reinterpret_cast<StepRec *>(stg + 16);
+  int32_t *srel = reinterpret_cast<int32_t *>(stg + 16 + PIPE_REC_CAP * 16);
+  unsigned phase = 0;
+  if (R.st_rec && lane == 0) {
+    mbar_init(mbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
   for (;;) {
     long long t = 0;
     if (lane == 0) t = (long long)atomicAdd(reinterpret_cast<unsigned long long *>(counter), 1ull);
@@ -292,6 +390,20 @@ __global__ void __launch_bounds__(PIPE_WARPS * 32, PIPE_MINB_DEF)
     const TaskDesc cur = tasks[t];
     const int two = cur.g + 1 < G ? 2 : 1;
     const int64_t nd = cur.d1 - cur.d0;
+    // the task's program window into shared memory, in flight while the polls wait
+    const bool staged = R.st_rec != nullptr && cur.nk > 0;
+    int roff = 0;
+    if (staged && lane == 0) {
+      const int64_t a0 = (cur.rel0 * 4) & ~(int64_t)15;
+      const int64_t a1 = ((cur.rel0 + cur.nrel) * 4 + 15) & ~(int64_t)15;
+      const unsigned brec = (unsigned)cur.nk * 16u, brel = (unsigned)(a1 - a0);
+      // the previous task's generic reads of the buffers precede the async writes
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(mbar, brec + brel);
+      bulk_g2s(srec, R.st_rec + cur.k0, brec, mbar);
+      bulk_g2s(srel, reinterpret_cast<const char *>(R.rel) + a0, brel, mbar);
+    }
+    if (staged) roff = (int)(cur.rel0 & 3);
     // relaxed polls (an acquire load would invalidate the SM's L1 on every poll);
     // every value a task reads from another task is loaded L2-coherent (ld.cg)
     // after the polls, and producers fence before publishing
@@ -312,9 +424,14 @@ __global__ void __launch_bounds__(PIPE_WARPS * 32, PIPE_MINB_DEF)
     fence_acq_rel_gpu();
 #endif
     __syncwarp();
+    if (staged) {
+      mbar_wait(mbar, phase);
+      phase ^= 1u;
+    }
     const longlong4 nr = make_longlong4(cur.valoff, cur.d0, (int64_t)cur.r | ((int64_t)cur.s << 32),
                                         (int64_t)cur.W | ((int64_t)cur.L << 32));
-    bt_node2(S, P, R, nr, cur.g, rhs, Y, wsm_w, ws, lane, 0, cur.rr0, false, 0.0, 0.0);
+    bt_node2(S, P, R, nr, cur.g, rhs, Y, wsm_w, ws, lane, 0, cur.rr0, false, 0.0, 0.0,
+             staged ? srec : nullptr, srel + roff, cur.k0);
     fence_acq_rel_gpu();
     __syncwarp();
     if (lane < two) st_relaxed(flags + (int64_t)cur.u * G + cur.g + lane, epoch);

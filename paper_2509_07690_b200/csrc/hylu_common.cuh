@@ -73,7 +73,39 @@ struct BatchP {
 };
 
 // Row programs (schedule.py) resident on the device.
+// One step of a batched row program in 16 bytes (the SoA arrays below, packed): the
+// pipeline copies a task's steps into shared memory with one bulk copy.
+struct __align__(16) StepRec {
+  int32_t p;      // multiplier position in the target row
+  int32_t src;    // offset of U(j,j) in node storage
+  int32_t j;      // source row (forward-solve coupling)
+  int16_t cnt;    // U(j,>j) entries
+  int16_t rl;     // offset of the step's target positions in the task's rel window
+};
+
+#ifndef PIPE_REC_CAP
+#define PIPE_REC_CAP 96    // steps of a task's program window staged in shared memory
+#endif
+#ifndef PIPE_REL_CAP
+#define PIPE_REL_CAP 512   // rel entries of the window (+ 16-byte alignment slack)
+#endif
+
+// Batched pipeline task (node, group pair), built on the host in claim order.
+struct TaskDesc {
+  int32_t u, g;
+  int64_t valoff;
+  int32_t r, s, W, L;
+  int64_t d0, d1;
+  longlong4 rr0;   // row record of the node's first row (no dependent load for it)
+  int32_t dep[4];  // the first (up to) 4 dependencies, inline (no dependent index load)
+  int64_t rel0;    // first rel entry of the node's program window
+  int32_t k0, nk;  // the node's steps [k0, k0 + nk)
+  int32_t nrel;    // rel entries of the window (0: not stageable)
+  int32_t pad[3];
+};
+
 struct DevProg {
+  const StepRec *st_rec;    // [nsteps (+1 pad)] packed steps (nullptr: not built)
   const int64_t *row_ptr;   // [n+1]
   const int32_t *st_p;
   const int32_t *st_j;
