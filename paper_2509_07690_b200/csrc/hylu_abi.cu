@@ -183,6 +183,7 @@ struct hy_handle {
   double *d_bf = nullptr;         // batched factor workspace
   int64_t bf_cap = 0;             // doubles
   double *d_by = nullptr;         // batched solve workspace
+  double *d_bri = nullptr;        // batched pivot reciprocals [G][n][32]
   int64_t by_cap = 0;
   int64_t last_B = 0;
   const int32_t *last_iperm = nullptr;
@@ -202,7 +203,7 @@ struct hy_handle {
   int32_t *d_node_level = nullptr;
   int pipe_blocks = 0;
   int warp_min = 256;                      // fan-in: below this many small items per level, CTA kernels only
-  int pipe_ws = 16;                        // pair-mode shared workspace columns per group
+  int pipe_ws = 8;                         // pair-mode shared workspace columns per group (8: 16.42 ms/step, 12: 16.50, 16: 16.65 with the 160-step program windows)
   // diagonal claim order per (segment, G): pair prefix sums, (level<<16|group), level offsets
   struct Seg {
     int l0, l1;
@@ -519,6 +520,7 @@ void hy_destroy(hy_handle *h) {
   free_segments(h);
   if (h->d_counters) cudaFree(h->d_counters);
   if (h->d_by) cudaFree(h->d_by);
+  if (h->d_bri) cudaFree(h->d_bri);
   if (h->d_arow) cudaFree(h->d_arow);
   if (h->d_pinv) cudaFree(h->d_pinv);
   if (h->d_rowof) cudaFree(h->d_rowof);
@@ -1558,8 +1560,11 @@ static int batch_prepare(hy_handle *h, int64_t B) {
   const int64_t needy = (int64_t)G * 32 * h->S.n;
   if (needy > h->by_cap) {
     if (h->d_by) CK(cudaFree(h->d_by));
+    if (h->d_bri) CK(cudaFree(h->d_bri));
     h->d_by = nullptr;
+    h->d_bri = nullptr;
     CK(cudaMalloc((void **)&h->d_by, sizeof(double) * needy));
+    CK(cudaMalloc((void **)&h->d_bri, sizeof(double) * needy));
     h->by_cap = needy;
   }
   return HY_OK;
@@ -1581,7 +1586,8 @@ int hy_refactorize_batched(hy_handle *h, int64_t B, const double *d_vals, double
   h->last_iperm = prior->d_inner_perm;
   CK(cudaMemsetAsync(d_npert, 0, sizeof(int32_t) * B, st));
   const int G = (int)((B + 31) / 32);
-  BatchP P{h->d_bf, d_vals, prior->d_inner_perm, prior->d_anorm, eps, d_npert, B, h->stored, 0};
+  BatchP P{h->d_bf, d_vals, prior->d_inner_perm, prior->d_anorm, eps, d_npert, B, h->stored, 0,
+           h->d_bri};
   h->last_fused = d_b_fuse != nullptr;
   if (d_b_fuse) {
     // b̂ into Y first (coalesced transpose in source-row order); the row kernels then

@@ -88,6 +88,9 @@ constexpr int PIPE_WARPS = 4;
 // instances, and each step has two independent FMA/load chains in flight.  The
 // value layout is unchanged (the allocation is padded to an even group count, so
 // the pair of the last odd group computes on padding: not live, no atomics).
+#ifndef PIPE_RINV
+#define PIPE_RINV 1      // multipliers = value x stored reciprocal of the source pivot (else a division)
+#endif
 #ifndef P2W_DEF
 #define P2W_DEF 4
 #endif
@@ -96,14 +99,16 @@ template <typename WPtr>
 __device__ __forceinline__ void run_steps2(const DevProg &R, int64_t s0, int64_t s1, WPtr wa,
                                            WPtr wc, const double *ga, const double *gc,
                                            const double *ya, const double *yc, double &acA,
-                                           double &acC) {
+                                           double &acC, const double *ria, const double *ric) {
   if (s0 >= s1) return;
   int p = __ldg(R.st_p + s0);
   int64_t src = __ldg(R.st_src + s0);
   int cnt = __ldg(R.st_cnt + s0);
   int64_t ro = __ldg(R.st_rel + s0);
   int64_t j = __ldg(R.st_j + s0);
-  double da = __ldcg(ga + src * 32), dc = __ldcg(gc + src * 32);
+  // pivot of the source row: its reciprocal (one multiply per step) when available
+  double da = PIPE_RINV ? __ldcg(ria + j * 32) : __ldcg(ga + src * 32);
+  double dc = PIPE_RINV ? __ldcg(ric + j * 32) : __ldcg(gc + src * 32);
   double yja = __ldcg(ya + j * 32), yjc = __ldcg(yc + j * 32);
   for (int64_t st = s0; st < s1; ++st) {
     int pn = 0, cn = 0;
@@ -115,16 +120,16 @@ __device__ __forceinline__ void run_steps2(const DevProg &R, int64_t s0, int64_t
       cn = __ldg(R.st_cnt + st + 1);
       rn = __ldg(R.st_rel + st + 1);
       const int64_t jn = __ldg(R.st_j + st + 1);
-      dna = __ldcg(ga + sn * 32);
-      dnc = __ldcg(gc + sn * 32);
+      dna = PIPE_RINV ? __ldcg(ria + jn * 32) : __ldcg(ga + sn * 32);
+      dnc = PIPE_RINV ? __ldcg(ric + jn * 32) : __ldcg(gc + sn * 32);
       yna = __ldcg(ya + jn * 32);
       ync = __ldcg(yc + jn * 32);
     }
     const int32_t *rl = R.rel + ro;
     const double *ua = ga + (src + 1) * 32;
     const double *uc = gc + (src + 1) * 32;
-    const double la = wa[p * 32] / da;
-    const double lc = wc[p * 32] / dc;
+    const double la = PIPE_RINV ? wa[p * 32] * da : wa[p * 32] / da;
+    const double lc = PIPE_RINV ? wc[p * 32] * dc : wc[p * 32] / dc;
     wa[p * 32] = la;
     wc[p * 32] = lc;
     acA -= la * yja;
@@ -162,18 +167,19 @@ template <typename WPtr>
 __device__ __forceinline__ void run_steps2s(const StepRec *rec, const int32_t *relw, int s0, int s1, WPtr wa,
                                             WPtr wc, const double *ga, const double *gc,
                                             const double *ya, const double *yc, double &acA,
-                                            double &acC) {
+                                            double &acC, const double *ria, const double *ric) {
   if (s0 >= s1) return;
   StepRec cr = rec[s0];
-  double da = __ldcg(ga + (int64_t)cr.src * 32), dc = __ldcg(gc + (int64_t)cr.src * 32);
+  double da = PIPE_RINV ? __ldcg(ria + (int64_t)cr.j * 32) : __ldcg(ga + (int64_t)cr.src * 32);
+  double dc = PIPE_RINV ? __ldcg(ric + (int64_t)cr.j * 32) : __ldcg(gc + (int64_t)cr.src * 32);
   double yja = __ldcg(ya + (int64_t)cr.j * 32), yjc = __ldcg(yc + (int64_t)cr.j * 32);
   for (int st = s0; st < s1; ++st) {
     StepRec nx = cr;
     double dna = 1.0, dnc = 1.0, yna = 0.0, ync = 0.0;
     if (st + 1 < s1) {
       nx = rec[st + 1];
-      dna = __ldcg(ga + (int64_t)nx.src * 32);
-      dnc = __ldcg(gc + (int64_t)nx.src * 32);
+      dna = PIPE_RINV ? __ldcg(ria + (int64_t)nx.j * 32) : __ldcg(ga + (int64_t)nx.src * 32);
+      dnc = PIPE_RINV ? __ldcg(ric + (int64_t)nx.j * 32) : __ldcg(gc + (int64_t)nx.src * 32);
       yna = __ldcg(ya + (int64_t)nx.j * 32);
       ync = __ldcg(yc + (int64_t)nx.j * 32);
     }
@@ -181,8 +187,8 @@ __device__ __forceinline__ void run_steps2s(const StepRec *rec, const int32_t *r
     const int32_t *rl = relw + cr.rl;
     const double *ua = ga + ((int64_t)cr.src + 1) * 32;
     const double *uc = gc + ((int64_t)cr.src + 1) * 32;
-    const double la = wa[p * 32] / da;
-    const double lc = wc[p * 32] / dc;
+    const double la = PIPE_RINV ? wa[p * 32] * da : wa[p * 32] / da;
+    const double lc = PIPE_RINV ? wc[p * 32] * dc : wc[p * 32] / dc;
     wa[p * 32] = la;
     wc[p * 32] = lc;
     acA -= la * yja;
@@ -285,6 +291,8 @@ __device__ __forceinline__ void bt_node2(const DevSym &S, const BatchP &P, const
   double *gc0 = ga0 + P.stored * 32;
   double *ya = Y + (int64_t)g * S.n * 32 + lane;
   double *yc = ya + (int64_t)S.n * 32;
+  double *ria = P.RI + (int64_t)g * S.n * 32 + lane;   // P.RI is set whenever PIPE_RINV
+  double *ric = ria + (int64_t)S.n * 32;
   const double *Ab = P.A + (int64_t)g * 32 * S.nnz;
   for (int t = 0; t < s; ++t) {
     const int i = r + t;
@@ -304,14 +312,15 @@ __device__ __forceinline__ void bt_node2(const DevSym &S, const BatchP &P, const
       if (srec) {
         if (inSm)
           run_steps2s(srec, srel, (int)(s0 - sk0), (int)(s1 - sk0), wA + lane, wC + lane, ga0 + lane,
-                      gc0 + lane, ya, yc, yaccA, yaccC);
+                      gc0 + lane, ya, yc, yaccA, yaccC, ria, ric);
         else
           run_steps2s(srec, srel, (int)(s0 - sk0), (int)(s1 - sk0), growA + lane, growC + lane, ga0 + lane,
-                      gc0 + lane, ya, yc, yaccA, yaccC);
+                      gc0 + lane, ya, yc, yaccA, yaccC, ria, ric);
       } else if (inSm)
-        run_steps2(R, s0, s1, wA + lane, wC + lane, ga0 + lane, gc0 + lane, ya, yc, yaccA, yaccC);
+        run_steps2(R, s0, s1, wA + lane, wC + lane, ga0 + lane, gc0 + lane, ya, yc, yaccA, yaccC, ria, ric);
       else
-        run_steps2(R, s0, s1, growA + lane, growC + lane, ga0 + lane, gc0 + lane, ya, yc, yaccA, yaccC);
+        run_steps2(R, s0, s1, growA + lane, growC + lane, ga0 + lane, gc0 + lane, ya, yc, yaccA, yaccC, ria,
+                   ric);
     }
     const int Lt = L + t;
     bool fa, fc;
@@ -321,6 +330,10 @@ __device__ __forceinline__ void bt_node2(const DevSym &S, const BatchP &P, const
     if (fc && liveC) atomicAdd(&P.npert[bc], 1);
     ya[(int64_t)i * 32] = yaccA;
     yc[(int64_t)i * 32] = yaccC;
+    if (PIPE_RINV) {   // one division per row, off the consumers' step chains
+      ria[(int64_t)i * 32] = 1.0 / wA[Lt * 32 + lane];
+      ric[(int64_t)i * 32] = 1.0 / wC[Lt * 32 + lane];
+    }
     if (inSm && !(xmask & 8))
       for (int q = 0; q < W; ++q) {
         growA[q * 32 + lane] = wA[q * 32 + lane];
@@ -687,6 +700,7 @@ __global__ void __launch_bounds__(HUB_THREADS, 1) k_bt_hub(DevSym S, BatchP P, D
       double yacc = P.ypre ? yb[(int64_t)i * 32] : (live && rhs) ? S.dr[a] * rhs[b * S.n + a] : 0.0;
       for (int k2 = 0; k2 < nw; ++k2) yacc -= red[k2][lane];
       yb[(int64_t)i * 32] = yacc;
+      if (PIPE_RINV) P.RI[((int64_t)g * S.n + i) * 32 + lane] = 1.0 / w0[(int64_t)(S.nl[u] + t) * 32 + lane];
     }
     __syncthreads();
   }

@@ -70,6 +70,7 @@ struct BatchP {
   int64_t B;
   int64_t stored;
   int ypre;              // 1: Y already holds b̂ (interleaved, factor-row order)
+  double *RI;            // [G][n][32] reciprocal of each finished row's pivot (nullptr: divide)
 };
 
 // Row programs (schedule.py) resident on the device.
@@ -84,10 +85,10 @@ struct __align__(16) StepRec {
 };
 
 #ifndef PIPE_REC_CAP
-#define PIPE_REC_CAP 96    // steps of a task's program window staged in shared memory
+#define PIPE_REC_CAP 160   // steps of a task's program window staged in shared memory
 #endif
 #ifndef PIPE_REL_CAP
-#define PIPE_REL_CAP 512   // rel entries of the window (+ 16-byte alignment slack)
+#define PIPE_REL_CAP 1024  // rel entries of the window (+ 16-byte alignment slack)
 #endif
 
 // Batched pipeline task (node, group pair), built on the host in claim order.

@@ -1,3 +1,3 @@
-D=gpurun_out/r2k; mkdir -p $D
+D=gpurun_out/r2x; mkdir -p $D
 K=1 python scripts/batch_time.py > $D/plain.log 2>&1 && \
 K=1 timeout 1500 /usr/local/cuda/bin/ncu --set full --clock-control none --import-source on -k regex:k_bt_pipe2 -s 6 -c 1 -o $D/pipe python scripts/batch_time.py > $D/ncu.log 2>&1; echo "rc=$?" >> $D/ncu.log
