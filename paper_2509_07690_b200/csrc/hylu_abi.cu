@@ -203,7 +203,7 @@ struct hy_handle {
   int32_t *d_node_level = nullptr;
   int pipe_blocks = 0;
   int warp_min = 256;                      // fan-in: below this many small items per level, CTA kernels only
-  int pipe_ws = 8;                         // pair-mode shared workspace columns per group (8: 16.42 ms/step, 12: 16.50, 16: 16.65 with the 160-step program windows)
+  int pipe_ws = 6;                         // pair-mode shared workspace columns per group (c4 ms/step: 4: 15.50, 6: 15.48, 8: 15.64, 10: 15.64, 16: 16.65 before the reciprocals)
   // diagonal claim order per (segment, G): pair prefix sums, (level<<16|group), level offsets
   struct Seg {
     int l0, l1;
