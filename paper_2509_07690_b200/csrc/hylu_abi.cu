@@ -63,9 +63,11 @@ struct FaninDev {
   const int32_t *src_qb;
   const int32_t *src_m;
   const ItemRec *up_rec;     // [items] packed prologue records (k_item_rec)
+  const uint64_t *up_mask;   // [items] tile columns any source touches (k_item_mask; needs the maps)
 };
 __global__ void k_fi_scatter(DevSym, const CallP *);
 __global__ void k_item_rec(DevSym, FaninDev, int64_t, ItemRec *);
+__global__ void k_item_mask(FaninDev, int64_t, uint64_t *);
 size_t fi_lu_smem();
 size_t fi_panel_smem();
 size_t fi_upd_w_smem();
@@ -753,6 +755,7 @@ int hy_upload_fanin_plan(hy_handle *h, const hy_fanin_plan *d) {
   FaninDev &D = h->fi;
   D.src_poff = nullptr; D.src_pos = nullptr; D.src_vb = nullptr;
   D.src_vW = nullptr; D.src_qb = nullptr; D.src_m = nullptr;
+  D.up_mask = nullptr;
   int32_t *p32;
   int64_t *p64;
   UPF(&p32, d->lu_nodes, d->lu_ptr[nl]); D.lu_nodes = p32;
@@ -1006,6 +1009,18 @@ int hy_upload_fanin_maps(hy_handle *h, int64_t nsrc, int64_t npos, const int64_t
   UPF(&p32, vW, nsrc); D.src_vW = p32;
   UPF(&p32, qb, nsrc); D.src_qb = p32;
   UPF(&p32, m, nsrc); D.src_m = p32;
+  {   // per item: the tile columns any of its sources touches (compact column space)
+    const int64_t ni = h->fi_up.empty() ? 0 : h->fi_up.back();
+    uint64_t *mk = nullptr;
+    CK(cudaMalloc((void **)&mk, sizeof(uint64_t) * (ni > 0 ? ni : 1)));
+    h->fi_allocs.push_back(mk);
+    if (ni > 0) {
+      k_item_mask<<<(unsigned)std::min<int64_t>((ni + 255) / 256, 4096), 256>>>(D, ni, mk);
+      CK(cudaGetLastError());
+      CK(cudaDeviceSynchronize());
+    }
+    D.up_mask = mk;
+  }
   return HY_OK;
 }
 

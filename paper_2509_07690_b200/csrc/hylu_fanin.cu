@@ -59,6 +59,7 @@ struct FaninDev {
   const int32_t *src_qb;     // first panel column of the record in the source
   const int32_t *src_m;      // source block rows from the first present one
   const ItemRec *up_rec;     // [items] packed prologue records (k_item_rec)
+  const uint64_t *up_mask;   // [items] tile columns any source touches (k_item_mask; needs the maps)
 };
 
 constexpr int FI_THREADS = 256;
@@ -1049,6 +1050,41 @@ __device__ __forceinline__ void d_fi_upd_kc(DevSym S, const CallP *__restrict__ 
     const int64_t tc0 = S.colptr[D.up_t[j]];
     for (int c = tid; c < tw; c += FI_THREADS) tcol[c] = S.cols[tc0 + c0 + c];
   }
+  if (compact && D.src_pos && D.up_mask) {
+    // the item's touched tile columns are a precomputed 64-bit mask: a source
+    // column's compact index is the popcount of the mask below its tile position,
+    // so the maps and 8-column block masks are built in one pass, one barrier
+    const uint64_t mask = D.up_mask[j];
+    if (warp == 0) {
+      for (int c = lane; c < 64; c += 32)
+        if ((mask >> c) & 1ull) ucol[__popcll(mask & ((1ull << c) - 1ull))] = (int8_t)c;
+      if (lane == 0) s_nu = __popcll(mask);
+    }
+    for (int k = warp; k < (int)(ze - zb); k += FI_THREADS / 32) {
+      const int64_t z = zb + k;
+      const int nq = D.src_q1[z] - D.src_q0[z];
+      if (lane == 0) {
+        s_vb[k] = D.src_vb[z];
+        s_vW[k] = D.src_vW[z];
+        s_qb[k] = D.src_qb[z];
+        s_pb[k] = D.src_pb[z];
+        s_tb[k] = D.src_tb[z];
+        s_m[k] = D.src_m[z];
+      }
+      const int8_t *pz = D.src_pos + D.src_poff[z];
+      int cp0 = -1, cp1 = -1;
+      if (lane < nq) cp0 = __popcll(mask & ((1ull << pz[lane]) - 1ull));
+      if (lane + 32 < nq) cp1 = __popcll(mask & ((1ull << pz[lane + 32]) - 1ull));
+      inv[k * 64 + lane] = -1;
+      inv[k * 64 + lane + 32] = -1;
+      __syncwarp();
+      unsigned bits = 0;
+      if (cp0 >= 0) { inv[k * 64 + cp0] = (int8_t)lane; bits |= 1u << (cp0 >> 3); }
+      if (cp1 >= 0) { inv[k * 64 + cp1] = (int8_t)(lane + 32); bits |= 1u << (cp1 >> 3); }
+      bits = __reduce_or_sync(HY_FULL, bits);
+      if (lane == 0) s_bm[k] = bits;
+    }
+  } else {
   if (tid < FI_TILE) cidx[tid] = compact ? -1 : (int8_t)tid;
   __syncthreads();
   if (compact) {
@@ -1143,6 +1179,7 @@ __device__ __forceinline__ void d_fi_upd_kc(DevSym S, const CallP *__restrict__ 
     if (tid < FI_TILE) ucol[tid] = (int8_t)tid;
     if (tid == 0) s_nu = tw;
   }
+  }   // compact column space
   __syncthreads();
   const int nu = s_nu;
   // warp tiles over the s x nu product: 8 x 32 (8 warps over the rows) when the
@@ -1630,6 +1667,19 @@ __global__ void __launch_bounds__(FI_THREADS, KC_MINB_DEF) k_fi_upd_kcp(DevSym S
 size_t fi_lu_smem() { return (size_t)64 * FXLD * sizeof(double); }
 size_t fi_panel_smem() { return (size_t)(64 * 256 + 64 * FXLD) * sizeof(double); }
 size_t fi_upd_w_smem() { return (size_t)(FI_THREADS / 32) * UW_ROWS * UW_TILE * sizeof(double); }
+
+__global__ void k_item_mask(FaninDev D, int64_t nitems, uint64_t *out) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nitems;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t m = 0;
+    for (int64_t z = D.up_ptr[j]; z < D.up_ptr[j + 1]; ++z) {
+      const int8_t *pz = D.src_pos + D.src_poff[z];
+      const int nq = D.src_q1[z] - D.src_q0[z];
+      for (int c = 0; c < nq; ++c) m |= 1ull << pz[c];
+    }
+    out[j] = m;
+  }
+}
 
 __global__ void k_item_rec(DevSym S, FaninDev D, int64_t nitems, ItemRec *out) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nitems;
