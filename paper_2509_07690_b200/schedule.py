@@ -25,6 +25,7 @@ from dataclasses import dataclass
 
 import os
 
+import numba
 import numpy as np
 from numba import njit, prange
 
@@ -701,7 +702,7 @@ PANEL_TILE = 256         # columns per permutation / TRSM tile
 
 
 @njit(cache=True)
-def _fanin_plan(first, kind, colptr, cols, nl, dptr, deps, level, nlev, tw, pw):
+def _fanin_plan(first, kind, colptr, cols, nl, dptr, deps, level, nlev, tw, pw, updates=True):
     """Per level: LU nodes, perm/TRSM tiles, X pairs and update tiles.
 
     Update item = (target T, tile [c0, c1)) with its source list (dep index k, q0, q1):
@@ -770,7 +771,7 @@ def _fanin_plan(first, kind, colptr, cols, nl, dptr, deps, level, nlev, tw, pw):
     src_q1_l = []
     lev_up = np.zeros(nlev + 1, np.int64)
     tmp_tile = np.empty(0, np.int64)
-    for lv in range(nlev):
+    for lv in range(nlev if updates else 0):
         x = xp_ptr[lv]
         while x < xp_ptr[lv + 1]:
             u = xp_tgt[x]
@@ -849,6 +850,154 @@ def _fanin_plan(first, kind, colptr, cols, nl, dptr, deps, level, nlev, tw, pw):
         pt_c1[z] = pt_c1_l[z]
     return (lu_ptr, lu_nodes, pt_ptr, pt_node, pt_c0, pt_c1, xp_ptr, xp_edge.astype(np.int64), xp_tgt,
             lev_up, up_t, up_c0, up_c1, up_ptr, src_k, src_q0, src_q1)
+
+
+@njit(cache=True)
+def _tile_records(cols, first, colptr, nl, deps, dptr, xp_edge, x, x1, u, tw, out_t, out_k, out_q0, out_q1):
+    """Walk the beyond-block columns of the sources of edges x..x1 (all into target u)
+    tile by tile; fill the record arrays (if given, len > 0) and return the count."""
+    c0u = colptr[u]
+    W = colptr[u + 1] - c0u
+    n = 0
+    for e in range(x, x1):
+        k = xp_edge[e]
+        v = deps[k]
+        vs = first[v + 1] - first[v]
+        vc0 = colptr[v]
+        vW = colptr[v + 1] - vc0
+        pst = nl[v] + vs
+        q = pst
+        while q < vW:
+            pos = _lower_bound(cols, c0u, c0u + W, cols[vc0 + q]) - c0u
+            t = pos // tw
+            hi_id = cols[c0u + min(W, (t + 1) * tw) - 1]
+            qe = _lower_bound(cols, vc0 + q, vc0 + vW, hi_id + 1) - vc0
+            if len(out_t):
+                out_t[n] = t
+                out_k[n] = k - dptr[u]
+                out_q0[n] = q - pst
+                out_q1[n] = qe - pst
+            n += 1
+            q = qe
+    return n
+
+
+@njit(cache=True, parallel=True)
+def _fanin_updates_par(first, colptr, cols, nl, dptr, deps, xp_ptr, xp_edge, xp_tgt, nlev, tw, nth):
+    """The update items of _fanin_plan, built in parallel over (level, target) groups:
+    pass 1 counts each group's records and distinct tiles, pass 2 fills them at
+    prefix-sum offsets (records of a group counting-sorted by tile, edge order kept
+    within a tile) — the same arrays as the serial loop.  Per-thread scratch (no
+    allocation inside the parallel loops)."""
+    # groups: maximal runs of equal target within a level
+    ng = 0
+    for lv in range(nlev):
+        for x in range(xp_ptr[lv], xp_ptr[lv + 1]):
+            if x == xp_ptr[lv] or xp_tgt[x] != xp_tgt[x - 1]:
+                ng += 1
+    gs = np.empty(ng + 1, np.int64)
+    gl = np.empty(ng, np.int64)
+    g = 0
+    for lv in range(nlev):
+        for x in range(xp_ptr[lv], xp_ptr[lv + 1]):
+            if x == xp_ptr[lv] or xp_tgt[x] != xp_tgt[x - 1]:
+                gs[g] = x
+                gl[g] = lv
+                g += 1
+    gs[ng] = xp_ptr[nlev]
+    maxW = 0
+    for u in range(len(colptr) - 1):
+        maxW = max(maxW, colptr[u + 1] - colptr[u])
+    mt = (maxW + tw - 1) // tw + 1
+    stamp = np.zeros((nth, mt), np.int64)
+    nrec = np.zeros(ng, np.int64)
+    nitem = np.zeros(ng, np.int64)
+    e0 = np.zeros(0, np.int64)
+    e32 = np.zeros(0, np.int32)
+    for g in prange(ng):
+        th = numba.get_thread_id()
+        u = xp_tgt[gs[g]]
+        c0u = colptr[u]
+        W = colptr[u + 1] - c0u
+        n = 0
+        ni = 0
+        for e in range(gs[g], gs[g + 1]):
+            k = xp_edge[e]
+            v = deps[k]
+            vc0 = colptr[v]
+            vW = colptr[v + 1] - vc0
+            q = nl[v] + first[v + 1] - first[v]
+            while q < vW:
+                pos = _lower_bound(cols, c0u, c0u + W, cols[vc0 + q]) - c0u
+                t = pos // tw
+                hi_id = cols[c0u + min(W, (t + 1) * tw) - 1]
+                q = _lower_bound(cols, vc0 + q, vc0 + vW, hi_id + 1) - vc0
+                n += 1
+                if stamp[th, t] != g + 1:
+                    stamp[th, t] = g + 1
+                    ni += 1
+        nrec[g] = n
+        nitem[g] = ni
+    roff = np.zeros(ng + 1, np.int64)
+    ioff = np.zeros(ng + 1, np.int64)
+    maxn = 1
+    for g in range(ng):
+        roff[g + 1] = roff[g] + nrec[g]
+        ioff[g + 1] = ioff[g] + nitem[g]
+        maxn = max(maxn, nrec[g])
+    NI = ioff[ng]
+    NS = roff[ng]
+    up_t = np.empty(NI, np.int32)
+    up_c0 = np.empty(NI, np.int32)
+    up_c1 = np.empty(NI, np.int32)
+    up_ptr = np.empty(NI + 1, np.int64)
+    up_ptr[NI] = NS
+    src_k = np.empty(NS, np.int32)
+    src_q0 = np.empty(NS, np.int32)
+    src_q1 = np.empty(NS, np.int32)
+    srt = np.empty((nth, maxn), np.int64)
+    srk = np.empty((nth, maxn), np.int32)
+    sr0 = np.empty((nth, maxn), np.int32)
+    sr1 = np.empty((nth, maxn), np.int32)
+    scnt = np.empty((nth, mt + 1), np.int64)
+    for g in prange(ng):
+        th = numba.get_thread_id()
+        u = xp_tgt[gs[g]]
+        W = colptr[u + 1] - colptr[u]
+        ntile = (W + tw - 1) // tw
+        rt = srt[th]
+        rk = srk[th]
+        r0 = sr0[th]
+        r1 = sr1[th]
+        n = _tile_records(cols, first, colptr, nl, deps, dptr, xp_edge, gs[g], gs[g + 1], u, tw, rt, rk, r0, r1)
+        cnt = scnt[th]
+        for t in range(ntile + 1):
+            cnt[t] = 0
+        for z in range(n):
+            cnt[rt[z] + 1] += 1
+        for t in range(ntile):
+            cnt[t + 1] += cnt[t]
+        base = roff[g]
+        it = ioff[g]
+        for t in range(ntile):
+            if cnt[t + 1] > cnt[t]:
+                up_t[it] = u
+                up_c0[it] = t * tw
+                up_c1[it] = min(W, (t + 1) * tw)
+                up_ptr[it] = base + cnt[t]
+                it += 1
+        for z in range(n):          # stable counting sort by tile (cnt becomes the fill cursor)
+            d = base + cnt[rt[z]]
+            cnt[rt[z]] += 1
+            src_k[d] = rk[z]
+            src_q0[d] = r0[z]
+            src_q1[d] = r1[z]
+    lev_up = np.zeros(nlev + 1, np.int64)
+    for g in range(ng):
+        lev_up[gl[g] + 1] += nitem[g]
+    for lv in range(nlev):
+        lev_up[lv + 1] += lev_up[lv]
+    return lev_up, up_t, up_c0, up_c1, up_ptr, src_k, src_q0, src_q1
 
 
 @dataclass
@@ -1082,7 +1231,10 @@ def build_fanin_plan(sym, tw=FANIN_TILE, pw=PANEL_TILE, pull=None):
     flev = _fanin_levels(s.node_first, s.colptr, s.cols, s.nl, s.dep_ptr, s.deps, s.node_of)
     nlev = int(flev.max()) + 1
     out = _fanin_plan(s.node_first, s.node_kind, s.colptr, s.cols, s.nl, s.dep_ptr, s.deps,
-                      flev, nlev, tw, pw)
+                      flev, nlev, tw, pw, False)
+    # update items in parallel over (level, target) groups (the serial loop's arrays)
+    out = out[:9] + _fanin_updates_par(s.node_first, s.colptr, s.cols, s.nl, s.dep_ptr, s.deps,
+                                       out[6], out[7], out[8], nlev, tw, numba.get_num_threads())
     if pull is not None and pull.any():
         out, lev_hub, hub_list = _drop_pull_targets(out, np.asarray(pull, bool), nlev)
     else:

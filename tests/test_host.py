@@ -490,3 +490,20 @@ def test_device_routing_table(name):
         assert k["k_fi_upd_kcp"] + k["k_fi_upd_w"] + k["k_fi_upd_kc"] == len(plan.up_t)
         assert k["k_fi_x_w"] + k["k_fi_x"] == len(plan.xp_edge)
     assert r["edges"]["sup<-sup"] > 0 and r["tensor_core_items"] > 0
+
+
+@pytest.mark.parametrize("name", ["c0", "c1", "c2", "c3"])
+def test_parallel_fanin_updates_equal_serial(name):
+    """The update items built in parallel over (level, target) groups are the serial
+    plan loop's arrays, element for element."""
+    p = gen.config(name, "small")
+    an = an_mod.analyze(p.A, SolverConfig(ordering=p.ordering))
+    s = an.symbolic
+    flev = schedule._fanin_levels(s.node_first, s.colptr, s.cols, s.nl, s.dep_ptr, s.deps, s.node_of)
+    nlev = int(flev.max()) + 1
+    ser = schedule._fanin_plan(s.node_first, s.node_kind, s.colptr, s.cols, s.nl, s.dep_ptr, s.deps,
+                               flev, nlev, schedule.FANIN_TILE, schedule.PANEL_TILE)
+    par = schedule._fanin_updates_par(s.node_first, s.colptr, s.cols, s.nl, s.dep_ptr, s.deps,
+                                      ser[6], ser[7], ser[8], nlev, schedule.FANIN_TILE, 4)
+    for a, b in zip(ser[9:], par):
+        assert np.array_equal(np.asarray(a), np.asarray(b))
