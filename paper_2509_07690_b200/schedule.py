@@ -888,7 +888,8 @@ def _fanin_updates_par(first, colptr, cols, nl, dptr, deps, xp_ptr, xp_edge, xp_
     pass 1 counts each group's records and distinct tiles, pass 2 fills them at
     prefix-sum offsets (records of a group counting-sorted by tile, edge order kept
     within a tile) — the same arrays as the serial loop.  Per-thread scratch (no
-    allocation inside the parallel loops)."""
+    allocation inside the parallel loops); ``nth`` must cover every thread id of the
+    pool (numba.config.NUMBA_NUM_THREADS)."""
     # groups: maximal runs of equal target within a level
     ng = 0
     for lv in range(nlev):
@@ -1234,7 +1235,7 @@ def build_fanin_plan(sym, tw=FANIN_TILE, pw=PANEL_TILE, pull=None):
                       flev, nlev, tw, pw, False)
     # update items in parallel over (level, target) groups (the serial loop's arrays)
     out = out[:9] + _fanin_updates_par(s.node_first, s.colptr, s.cols, s.nl, s.dep_ptr, s.deps,
-                                       out[6], out[7], out[8], nlev, tw, numba.get_num_threads())
+                                       out[6], out[7], out[8], nlev, tw, numba.config.NUMBA_NUM_THREADS)
     if pull is not None and pull.any():
         out, lev_hub, hub_list = _drop_pull_targets(out, np.asarray(pull, bool), nlev)
     else:

@@ -5,6 +5,7 @@ import ctypes
 import os
 import re
 
+import numba
 import numpy as np
 import pytest
 
@@ -504,6 +505,7 @@ def test_parallel_fanin_updates_equal_serial(name):
     ser = schedule._fanin_plan(s.node_first, s.node_kind, s.colptr, s.cols, s.nl, s.dep_ptr, s.deps,
                                flev, nlev, schedule.FANIN_TILE, schedule.PANEL_TILE)
     par = schedule._fanin_updates_par(s.node_first, s.colptr, s.cols, s.nl, s.dep_ptr, s.deps,
-                                      ser[6], ser[7], ser[8], nlev, schedule.FANIN_TILE, 4)
+                                      ser[6], ser[7], ser[8], nlev, schedule.FANIN_TILE,
+                                      numba.config.NUMBA_NUM_THREADS)
     for a, b in zip(ser[9:], par):
         assert np.array_equal(np.asarray(a), np.asarray(b))
