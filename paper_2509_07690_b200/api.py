@@ -270,10 +270,29 @@ def substitute(factors, b, stream=None):
     return d_x
 
 
-def substitute_multi(factors, B, stream=None):
-    """Forward/backward substitution for many right-hand sides at once through the
-    partition-based device solve (Fig. 3; ``partition.py``): B is
-    [nrhs, n] (numpy or a CUDA float64 tensor), returns X [nrhs, n] on the device."""
+MULTI_WIDE_ROW = 2048     # stored entries: rows wider than this make the level solver the faster route
+
+
+def multi_rhs_method(factors):
+    """Route of ``substitute_multi``: "partition" (the Fig. 3 partition solve, warp per
+    row / balanced row range, lanes over the right-hand sides) unless the factors hold
+    rows wider than MULTI_WIDE_ROW stored entries (big supernodal panels, hub rows),
+    where one warp per row serialises thousands of entries and the chunked level solver
+    (``hy_solve``, off-block dot products split over warps) per right-hand side is
+    faster (c2: 32 right-hand sides 9.5 s partition vs 0.79 s level solves; c0: 10.9
+    ms vs 27.9 ms)."""
+    s = factors.symbolic
+    if getattr(s, "_max_row_width", None) is None:
+        s._max_row_width = int(np.diff(s.colptr).max()) if s.nnodes else 0
+    return "levels" if s._max_row_width > MULTI_WIDE_ROW else "partition"
+
+
+def substitute_multi(factors, B, stream=None, method="auto"):
+    """Forward/backward substitution for many right-hand sides at once.  ``method``:
+    "partition" — the partition-based device solve (SPEC.md:461-487, Fig. 3;
+    ``partition.py``, ``hy_solve_multi``); "levels" — the level-scheduled device solve
+    per right-hand side (``hy_solve``); "auto" — ``multi_rhs_method``.  B is [nrhs, n]
+    (numpy or a CUDA float64 tensor); returns X [nrhs, n] on the device."""
     import torch
     from .device import check
     ctx = factors._ctx
@@ -284,11 +303,19 @@ def substitute_multi(factors, B, stream=None):
     if d_B.dim() != 2 or d_B.shape[1] != ctx.n or d_B.dtype != torch.float64 or d_B.device != ctx.device:
         raise errors.DimensionMismatch("B must be a float64 [nrhs, %d] array" % ctx.n)
     d_B = d_B.contiguous()
+    d_X = torch.empty_like(d_B)
+    if method == "auto":
+        method = multi_rhs_method(factors)
+    sh = ctx.stream_handle(stream)
+    if method == "levels":
+        for j in range(d_B.shape[0]):
+            check(ctx.lib.hy_solve(ctx.h, factors._desc, d_B[j].data_ptr(), d_X[j].data_ptr(), sh))
+        return d_X
+    if method != "partition":
+        raise ValueError("method must be auto, partition or levels")
     if getattr(ctx, "_partition", None) is None:   # else: the one ensure_partition uploaded
         ctx.ensure_partition()
-    d_X = torch.empty_like(d_B)
-    check(ctx.lib.hy_solve_multi(ctx.h, factors._desc, d_B.shape[0], d_B.data_ptr(), d_X.data_ptr(),
-                                 ctx.stream_handle(stream)))
+    check(ctx.lib.hy_solve_multi(ctx.h, factors._desc, d_B.shape[0], d_B.data_ptr(), d_X.data_ptr(), sh))
     return d_X
 
 

@@ -644,8 +644,8 @@ def test_kernel_override_at_factorize_routes_the_device(name):
 
 
 @pytest.mark.parametrize("name", ["c0", "c1", "c2", "c3"])
-@pytest.mark.parametrize("nrhs", [1, 37])
-def test_solve_multi_matches_oracle(name, nrhs):
+@pytest.mark.parametrize("nrhs,method", [(1, "partition"), (37, "partition"), (5, "levels")])
+def test_solve_multi_matches_oracle(name, nrhs, method):
     """Partition-based multi-RHS substitution (Fig. 3) on the device
     against the oracle's substitution on the same (device) factors, per right-hand
     side, with a forced multi-segment partition."""
@@ -659,7 +659,7 @@ def test_solve_multi_matches_oracle(name, nrhs):
     assert part.seg_rows[-1] == an.symbolic.n and part.nsegments >= 2
     rng = np.random.default_rng(11)
     B = rng.uniform(-1, 1, (nrhs, p.A.n))
-    X = api.substitute_multi(f, B).cpu().numpy()
+    X = api.substitute_multi(f, B, method=method).cpu().numpy()
     fo = OracleFactors(f.host_values(), f.host_inner_perm(), [], f.anorm)
     for j in range(nrhs):
         xo = on.substitute(an, fo, B[j])
