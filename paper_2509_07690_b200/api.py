@@ -270,21 +270,27 @@ def substitute(factors, b, stream=None):
     return d_x
 
 
-MULTI_WIDE_ROW = 2048     # stored entries: rows wider than this make the level solver the faster route
+MULTI_WIDE_ROW = 2048     # stored entries of a "wide" row
+MULTI_WIDE_SHARE = 0.2    # share of stored entries in wide rows above which levels win
 
 
 def multi_rhs_method(factors):
-    """Route of ``substitute_multi``: "partition" (the Fig. 3 partition solve, warp per
-    row / balanced row range, lanes over the right-hand sides) unless the factors hold
-    rows wider than MULTI_WIDE_ROW stored entries (big supernodal panels, hub rows),
-    where one warp per row serialises thousands of entries and the chunked level solver
-    (``hy_solve``, off-block dot products split over warps) per right-hand side is
-    faster (c2: 32 right-hand sides 9.5 s partition vs 0.79 s level solves; c0: 10.9
-    ms vs 27.9 ms)."""
+    """Route of ``substitute_multi``: "partition" (the Fig. 3 partition solve: warp
+    per row / balanced row range, lanes over the right-hand sides) unless more than
+    MULTI_WIDE_SHARE of the stored entries sit in rows wider than MULTI_WIDE_ROW
+    (big supernodal panels), where one warp per row serialises thousands of entries
+    and the chunked level solver (``hy_solve``: off-block dot products split over
+    warps) per right-hand side is faster.  32 right-hand sides on one B200: c0 10.9 ms
+    partition vs 27.9 ms levels, c1 (5 wide hub rows, <5% of the entries) 18.3 vs
+    26.4 ms, c2 9.5 s vs 0.79 s."""
     s = factors.symbolic
-    if getattr(s, "_max_row_width", None) is None:
-        s._max_row_width = int(np.diff(s.colptr).max()) if s.nnodes else 0
-    return "levels" if s._max_row_width > MULTI_WIDE_ROW else "partition"
+    if getattr(s, "_wide_share", None) is None:
+        W = np.diff(s.colptr).astype(np.int64)
+        rows = np.diff(s.node_first).astype(np.int64)
+        wide = W > MULTI_WIDE_ROW
+        tot = float(np.sum(W * rows)) or 1.0
+        s._wide_share = float(np.sum((W * rows)[wide])) / tot
+    return "levels" if s._wide_share > MULTI_WIDE_SHARE else "partition"
 
 
 def substitute_multi(factors, B, stream=None, method="auto"):
