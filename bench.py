@@ -311,9 +311,8 @@ def measure_single(name, p, dev, flush, reps, cpu=True):
                            "vs_single_solves": ts * NR / tm, "residual_max": res_m,
                            "method": meth,
                            "segments": int(f._ctx._partition.nsegments) if meth == "partition" else None,
-                           "what": "32 right-hand sides through api.substitute_multi (partition-based "
-                                   "solve, or per-rhs level solves for factors with rows wider than "
-                                   "api.MULTI_WIDE_ROW) vs 32 single-rhs solves"},
+                           "what": "32 right-hand sides through api.substitute_multi (level-scheduled "
+                                   "multi-RHS solve, supernode panels on DMMA) vs 32 single-rhs solves"},
            "l2": "flushed (256 MB write) before every repetition", "reps": reps}
     plan = getattr(s, "_fanin_plan", None)
     if plan is not None:

@@ -270,34 +270,25 @@ def substitute(factors, b, stream=None):
     return d_x
 
 
-MULTI_WIDE_ROW = 2048     # stored entries of a "wide" row
-MULTI_WIDE_SHARE = 0.2    # share of stored entries in wide rows above which levels win
-
-
 def multi_rhs_method(factors):
-    """Route of ``substitute_multi``: "partition" (the Fig. 3 partition solve: warp
-    per row / balanced row range, lanes over the right-hand sides) unless more than
-    MULTI_WIDE_SHARE of the stored entries sit in rows wider than MULTI_WIDE_ROW
-    (big supernodal panels), where one warp per row serialises thousands of entries
-    and the chunked level solver (``hy_solve``: off-block dot products split over
-    warps) per right-hand side is faster.  32 right-hand sides on one B200: c0 10.9 ms
-    partition vs 27.9 ms levels, c1 (5 wide hub rows, <5% of the entries) 18.3 vs
-    26.4 ms, c2 9.5 s vs 0.79 s."""
-    s = factors.symbolic
-    if getattr(s, "_wide_share", None) is None:
-        W = np.diff(s.colptr).astype(np.int64)
-        rows = np.diff(s.node_first).astype(np.int64)
-        wide = W > MULTI_WIDE_ROW
-        tot = float(np.sum(W * rows)) or 1.0
-        s._wide_share = float(np.sum((W * rows)[wide])) / tot
-    return "levels" if s._wide_share > MULTI_WIDE_SHARE else "partition"
+    """Route of ``substitute_multi(method="auto")``: the level-scheduled multi-RHS
+    solve ("levels": warp per standalone row, CTA per wide row, CTA per supernode with
+    its off-block panel on DMMA).  Measured on one B200 with 32 right-hand sides
+    (``scripts/multi_rhs_probe.py``): c0 1.04 ms levels / 10.4 ms partition / 16.1 ms
+    as 32 single solves; c1 5.2 / 18.3 / 19.3 ms; c2 243 / 9521 / 785 ms; c3 (k=32)
+    145 / 6119 / 468 ms.  The partition solve of SPEC.md:461-487 ("partition") stays
+    selectable: it is the reference's method, and one warp per row range is the GPU
+    form of its per-thread row ranges."""
+    return "levels"
 
 
 def substitute_multi(factors, B, stream=None, method="auto"):
     """Forward/backward substitution for many right-hand sides at once.  ``method``:
     "partition" — the partition-based device solve (SPEC.md:461-487, Fig. 3;
-    ``partition.py``, ``hy_solve_multi``); "levels" — the level-scheduled device solve
-    per right-hand side (``hy_solve``); "auto" — ``multi_rhs_method``.  B is [nrhs, n]
+    ``partition.py``, ``hy_solve_multi``); "levels" — the level-scheduled multi-RHS
+    solve (``partition.device_launches_levels``: warp per standalone row, CTA per wide
+    row, CTA per supernode with its off-block panel on DMMA); "columns" — one
+    ``hy_solve`` per right-hand side; "auto" — ``multi_rhs_method``.  B is [nrhs, n]
     (numpy or a CUDA float64 tensor); returns X [nrhs, n] on the device."""
     import torch
     from .device import check
@@ -313,14 +304,17 @@ def substitute_multi(factors, B, stream=None, method="auto"):
     if method == "auto":
         method = multi_rhs_method(factors)
     sh = ctx.stream_handle(stream)
-    if method == "levels":
+    if method == "columns":
         for j in range(d_B.shape[0]):
             check(ctx.lib.hy_solve(ctx.h, factors._desc, d_B[j].data_ptr(), d_X[j].data_ptr(), sh))
         return d_X
-    if method != "partition":
-        raise ValueError("method must be auto, partition or levels")
-    if getattr(ctx, "_partition", None) is None:   # else: the one ensure_partition uploaded
-        ctx.ensure_partition()
+    if method == "levels":
+        ctx.ensure_partition(method="levels")
+    elif method == "partition":
+        if getattr(ctx, "_partition_key", ("levels",)) == ("levels",):   # else: the uploaded one
+            ctx.ensure_partition()
+    else:
+        raise ValueError("method must be auto, partition, levels or columns")
     check(ctx.lib.hy_solve_multi(ctx.h, factors._desc, d_B.shape[0], d_B.data_ptr(), d_X.data_ptr(), sh))
     return d_X
 

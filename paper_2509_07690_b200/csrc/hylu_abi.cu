@@ -84,6 +84,8 @@ __global__ void k_resid_berr_b(int, int64_t, const int64_t *, const int32_t *, c
 __global__ void k_axpy_b(int, double *, const double *, const double *, const int32_t *);
 __global__ void k_msolve(DevSym, const double *, int, int, int, int, const int32_t *, int, int, double *, int);
 __global__ void k_mbhat(DevSym, const int32_t *, const double *, double *, int);
+__global__ void k_msolve_long(DevSym, const double *, const int32_t *, int, double *, int);
+__global__ void k_msolve_sn(DevSym, const double *, const int32_t *, int, double *, int);
 __global__ void k_mxout(DevSym, const double *, double *, int);
 
 __global__ void k_fi_lu(DevSym, const CallP *, FaninDev, int);
@@ -1298,7 +1300,7 @@ int hy_upload_partition(hy_handle *h, const hy_partition_desc *d) {
       const int64_t kind = L[6 * q], lo = L[6 * q + 2], hi = L[6 * q + 3], off = L[6 * q + 4],
                     cnt = L[6 * q + 5];
       const int64_t span = kind == 0 ? 2 * cnt : cnt;
-      if ((kind != 0 && kind != 1) || lo < 0 || hi > h->S.n || lo > hi || off < 0 || cnt < 0 ||
+      if (kind < 0 || kind > 4 || kind == 2 || lo < 0 || hi > h->S.n || lo > hi || off < 0 || cnt < 0 ||
           off + span > d->nitems)
         return fail(HY_INVALID_ARGUMENT, "partition launch out of range");
     }
@@ -1340,6 +1342,17 @@ int hy_solve_multi(hy_handle *h, const hy_factors *f, int64_t nrhs, const double
       const int kind = (int)L[q], seq = (int)L[q + 1], lo = (int)L[q + 2], hi = (int)L[q + 3];
       const int cnt = (int)L[q + 5];
       if (!cnt) continue;
+      if (kind == 3 || kind == 4) {   // level form: CTA per wide row / per supernode
+        const dim3 g((unsigned)cnt, (unsigned)((nrhs + 31) / 32));
+        if (kind == 3)
+          k_msolve_long<<<g, 256, 0, st>>>(h->S, f->d_values, h->d_ms_items + L[q + 4], dir == 0, h->d_my,
+                                           (int)nrhs);
+        else
+          k_msolve_sn<<<g, 512, 0, st>>>(h->S, f->d_values, h->d_ms_items + L[q + 4], dir == 0, h->d_my,
+                                         (int)nrhs);
+        h->launches++;
+        continue;
+      }
       const int blocks = seq ? 1 : (cnt + 3) / 4;
       k_msolve<<<blocks, 128, 0, st>>>(h->S, f->d_values, kind, seq, lo, hi, h->d_ms_items + L[q + 4], cnt,
                                        dir == 0, h->d_my, (int)nrhs);

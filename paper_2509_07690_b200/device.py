@@ -402,25 +402,34 @@ class DeviceContext:
             check(self.lib.hy_upload_matrix(self.h, rp.ctypes.data, ci.ctypes.data))
         self._matrix_uploaded = True
 
-    def ensure_partition(self, threads=None, config=None):
-        """Build (partition.build_partition) and upload the multi-RHS solve partition,
-        cached per (threads, thresholds).  ``threads`` defaults to the device's
-        resident warps (SM count x 8) for the balanced row ranges; unless the config
-        sets ``seg_nnz_threshold``, segments hold >= 1/32 of the stored entries (each
-        segment costs launches on the device, not a thread barrier)."""
+    def ensure_partition(self, threads=None, config=None, method="partition"):
+        """Build and upload the launch lists of the multi-RHS solve, cached per method
+        and parameters.  ``method="partition"``: ``partition.build_partition`` (SPEC.md:
+        461-469) + ``device_launches``; ``threads`` defaults to the device's resident
+        warps (SM count x 8) for the balanced row ranges; unless the config sets
+        ``seg_nnz_threshold``, segments hold >= 1/32 of the stored entries (each segment
+        costs launches, not a thread barrier).  ``method="levels"``:
+        ``partition.device_launches_levels`` (supernode panels on DMMA)."""
         from . import partition as pt
-        if threads is None:
-            threads = self.torch.cuda.get_device_properties(self.device).multi_processor_count * 8
-        cfg = config or self.analysis.config
         s = self.analysis.symbolic
-        if cfg.seg_nnz_threshold is None:
-            cfg = cfg.with_overrides(seg_nnz_threshold=max(4096, int(s.stored_values) // 32))
-        key = (int(threads), int(cfg.seg_nnz_threshold), int(cfg.small_tri_threshold),
-               int(cfg.bulk_width_factor))
-        if getattr(self, "_partition_key", None) == key:
-            return self._partition
-        part = pt.build_partition(s, threads, cfg)
-        fwd, bwd, items = pt.device_launches(s, part)
+        if method == "levels":
+            key = ("levels",)
+            if getattr(self, "_partition_key", None) == key:
+                return self._partition
+            fwd, bwd, items = pt.device_launches_levels(s)
+            part = None
+        else:
+            if threads is None:
+                threads = self.torch.cuda.get_device_properties(self.device).multi_processor_count * 8
+            cfg = config or self.analysis.config
+            if cfg.seg_nnz_threshold is None:
+                cfg = cfg.with_overrides(seg_nnz_threshold=max(4096, int(s.stored_values) // 32))
+            key = (int(threads), int(cfg.seg_nnz_threshold), int(cfg.small_tri_threshold),
+                   int(cfg.bulk_width_factor))
+            if getattr(self, "_partition_key", None) == key:
+                return self._partition
+            part = pt.build_partition(s, threads, cfg)
+            fwd, bwd, items = pt.device_launches(s, part)
         fwd, bwd = np.ascontiguousarray(fwd), np.ascontiguousarray(bwd)
         items = np.ascontiguousarray(items)
         d = PartitionDesc(len(fwd), len(bwd), len(items), fwd.ctypes.data if fwd.size else None,

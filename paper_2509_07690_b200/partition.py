@@ -206,6 +206,43 @@ def device_launches(sym, part):
     return (np.asarray(fwd, np.int64).reshape(-1, 6), np.asarray(bwd, np.int64).reshape(-1, 6), it)
 
 
+def device_launches_levels(sym, long_row=64):
+    """Launch lists (same format as ``device_launches``) of the level-scheduled
+    multi-RHS substitution for supernodal factors: per forward level (``sym.level``)
+    and backward level (``sym.ulevel``) one launch per node class — standalone rows
+    with at most ``long_row`` off-diagonal entries in the direction (kind 1, warp per
+    row), wider standalone rows (kind 3, CTA per row, entries split over 8 warps),
+    supernodes (kind 4, CTA per supernode: off-block panel on DMMA, then the in-block
+    triangle); lo / hi = [0, n) (every entry)."""
+    s = sym
+    n = s.n
+    kind = np.asarray(s.node_kind)
+    W = np.diff(s.colptr)
+    items, fwd, bwd = [], [], []
+
+    def add(lst, k, arr):
+        if len(arr) == 0:
+            return
+        off = sum(len(a) for a in items)
+        items.append(np.asarray(arr, np.int32))
+        lst.append((k, 0, 0, n, off, len(arr)))
+
+    for lst, lev_ptr, lev_nodes, fwd_dir in ((fwd, s.level_ptr, s.level_nodes, True),
+                                           (bwd, s.ulevel_ptr, s.ulevel_nodes, False)):
+        for lv in range(len(lev_ptr) - 1):
+            nodes = np.asarray(lev_nodes[lev_ptr[lv]:lev_ptr[lv + 1]], np.int64)
+            if not len(nodes):
+                continue
+            sn = kind[nodes] == 1
+            width = np.asarray(s.nl)[nodes] if fwd_dir else W[nodes] - np.asarray(s.nl)[nodes] - 1
+            wide = (~sn) & (width > long_row)
+            add(lst, 1, nodes[(~sn) & ~wide])
+            add(lst, 3, nodes[wide])
+            add(lst, 4, nodes[sn])
+    it = np.concatenate(items).astype(np.int32) if items else np.zeros(0, np.int32)
+    return (np.asarray(fwd, np.int64).reshape(-1, 6), np.asarray(bwd, np.int64).reshape(-1, 6), it)
+
+
 def solve_cpu(sym, F, part, Y, direction_both=True):
     """CPU interpreter of the device launch lists (test infrastructure helper for the
     coverage property): applies the forward then backward substitution to the
