@@ -263,6 +263,7 @@ struct hy_handle {
   const double **d_fptr = nullptr;                   // factor values of the current solve (device slot)
   int64_t fi_graph_launches = 0;                     // kernels per graph replay
   int use_graphs = 1;                                // option "graphs"
+  int use_pdl = 1;                                   // option "pdl": programmatic dependent launch in the fan-in
   // partition-based multi-RHS solve (hy_upload_partition / hy_solve_multi)
   std::vector<int64_t> ms_fwd, ms_bwd;               // [k][6] launch lists
   int32_t *d_ms_items = nullptr;
@@ -474,6 +475,26 @@ static int upload_h1(hy_handle *h, T **dst, const T *src, int64_t count) {
     if (_r) return _r;                                     \
   } while (0)
 
+// Kernel launch with optional programmatic dependent launch (PDL, see pdl_wait): the
+// fan-in kernels wait for their predecessor inside, so their launch latency and CTA
+// scheduling overlap the predecessor's execution.
+template <typename... KArgs, typename... Args>
+static cudaError_t launchx(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                           bool pdl, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = pdl ? at : nullptr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+
 extern "C" {
 
 const char *hy_last_error(void) { return g_err.c_str(); }
@@ -541,6 +562,10 @@ int64_t hy_launch_count(const hy_handle *h) { return h ? h->launches : -1; }
 int hy_set_option(hy_handle *h, const char *name, int64_t value) {
   if (!h || !name) return fail(HY_INVALID_ARGUMENT, "null handle/name");
   drop_graph(h);   // every option can change the fan-in launch sequence
+  if (std::string(name) == "pdl") {
+    h->use_pdl = value != 0;
+    return HY_OK;
+  }
   if (std::string(name) == "graphs") {
     h->use_graphs = value != 0;
     return HY_OK;
@@ -857,7 +882,7 @@ int hy_upload_fanin_plan(hy_handle *h, const hy_fanin_plan *d) {
 
 
 static int run_fanin(hy_handle *h, const CallP *Pd, cudaStream_t st) {
-  k_fi_scatter<<<(h->S.n * 32 + 255) / 256, 256, 0, st>>>(h->S, Pd);
+  CK(launchx(k_fi_scatter, dim3((h->S.n * 32 + 255) / 256), dim3(256), 0, st, h->use_pdl, h->S, Pd));
   h->launches++;
   const int nfl = (int)h->fi_lu.size() - 1;
   for (int l = 0; l < nfl; ++l) {
@@ -865,6 +890,11 @@ static int run_fanin(hy_handle *h, const CallP *Pd, cudaStream_t st) {
     const int npt = (int)(h->fi_pt[l + 1] - h->fi_pt[l]);
     const int nxp = (int)(h->fi_xp[l + 1] - h->fi_xp[l]);
     const int nup = (int)(h->fi_up[l + 1] - h->fi_up[l]);
+    // PDL on latency-bound levels only: on a level with many CTAs the successor's
+    // early-resident CTAs would take slots from the predecessor's last waves
+    const int64_t lvmax = std::max<int64_t>(std::max<int64_t>(nlu, h->fi_pt[l + 1] - h->fi_pt[l]),
+                                            std::max<int64_t>(h->fi_xp[l + 1] - h->fi_xp[l], nup));
+    const bool pdl = h->use_pdl && lvmax <= 16 * (int64_t)h->sm_count;
     // pull-program rows of this level: every source is final, compute them whole
     const int nph = (int)(h->fi_hub[l + 1] - h->fi_hub[l]);
     if (nph) {
@@ -880,7 +910,10 @@ static int run_fanin(hy_handle *h, const CallP *Pd, cudaStream_t st) {
                                    h->hub1_slots);
       h->launches++;
     }
-    if (nlu) { k_fi_lu<<<nlu, 256, fi_lu_smem(), st>>>(h->S, Pd, h->fi, (int)h->fi_lu[l]); h->launches++; }
+    if (nlu) {
+      CK(launchx(k_fi_lu, dim3(nlu), dim3(256), fi_lu_smem(), st, pdl, h->S, Pd, h->fi, (int)h->fi_lu[l]));
+      h->launches++;
+    }
     // the panel TRSM of the level's nodes and the X blocks of their edges both need
     // only the nodes' LU: with fanin_overlap the panel runs on a side stream while the
     // X blocks run on `st`; the update kernels (which need both) wait for it
@@ -916,15 +949,17 @@ static int run_fanin(hy_handle *h, const CallP *Pd, cudaStream_t st) {
     cudaStream_t sp = sideA && npt ? h->fi_side : st;
     cudaStream_t sw = sideA && !npt ? h->fi_side : st;
     if (npt) {
-      k_fi_panel<<<npt, 256, fi_panel_smem(), sp>>>(h->S, Pd, h->fi, (int)h->fi_pt[l]);
+      CK(launchx(k_fi_panel, dim3(npt), dim3(256), fi_panel_smem(), sp, pdl && sp == st, h->S, Pd, h->fi,
+                 (int)h->fi_pt[l]));
       h->launches++;
     }
     if (nw) {
-      k_fi_x_w<<<(nw + 7) / 8, 256, 0, sw>>>(h->S, Pd, h->fi, (int)h->fi_xp[l], nw);
+      CK(launchx(k_fi_x_w, dim3((nw + 7) / 8), dim3(256), 0, sw, pdl && sw == st, h->S, Pd, h->fi,
+                 (int)h->fi_xp[l], nw));
       h->launches++;
     }
     if (nc) {
-      k_fi_x<<<nc, 256, 2 * 64 * 65 * sizeof(double), st>>>(h->S, Pd, h->fi, xb);
+      CK(launchx(k_fi_x, dim3(nc), dim3(256), 2 * 64 * 65 * sizeof(double), st, pdl, h->S, Pd, h->fi, xb));
       h->launches++;
     }
     if (sideA) {
@@ -948,8 +983,8 @@ static int run_fanin(hy_handle *h, const CallP *Pd, cudaStream_t st) {
       if (npk && h->fi_tc == 5) {
         FaninDev Dp = h->fi;
         if (!h->fi_maps) Dp.src_pos = nullptr;
-        if (h->fi_chain) k_fi_upd_kcp<true><<<npk, 256, fi_upd_kc_smem(), sk>>>(h->S, Pd, Dp, (int)h->fi_up[l]);
-        else k_fi_upd_kcp<false><<<npk, 256, fi_upd_kc_smem(), sk>>>(h->S, Pd, Dp, (int)h->fi_up[l]);
+        CK(launchx(h->fi_chain ? k_fi_upd_kcp<true> : k_fi_upd_kcp<false>, dim3(npk), dim3(256), fi_upd_kc_smem(),
+                   sk, pdl && sk == st, h->S, Pd, Dp, (int)h->fi_up[l]));
         h->launches++;
       } else if (npk) {
         k_fi_upd_pk<<<npk, 256, sm, sk>>>(h->S, Pd, h->fi, (int)h->fi_up[l], h->fi_smax[l], h->fi_mmax[l]);
@@ -958,14 +993,15 @@ static int run_fanin(hy_handle *h, const CallP *Pd, cudaStream_t st) {
       if (rs > reg) {
         FaninDev Dw = h->fi;
         if (!h->fi_maps) Dw.src_pos = nullptr;
-        k_fi_upd_w<<<(rs - reg + 7) / 8, 256, fi_upd_w_smem(), st>>>(h->S, Pd, Dw, reg, rs - reg);
+        CK(launchx(k_fi_upd_w, dim3((rs - reg + 7) / 8), dim3(256), fi_upd_w_smem(), st, pdl, h->S, Pd, Dw,
+                   reg, rs - reg));
         h->launches++;
       }
       if (split > rs && h->fi_tc >= 4) {
         FaninDev Dk = h->fi;
         if (!h->fi_maps) Dk.src_pos = nullptr;
-        if (h->fi_chain) k_fi_upd_kc<true><<<split - rs, 256, fi_upd_kc_smem(), st>>>(h->S, Pd, Dk, rs);
-        else k_fi_upd_kc<false><<<split - rs, 256, fi_upd_kc_smem(), st>>>(h->S, Pd, Dk, rs);
+        CK(launchx(h->fi_chain ? k_fi_upd_kc<true> : k_fi_upd_kc<false>, dim3(split - rs), dim3(256),
+                   fi_upd_kc_smem(), st, pdl, h->S, Pd, Dk, rs));
         h->launches++;
       } else if (split > rs && h->fi_tc == 2) {
         k_fi_upd_tc<<<split - rs, 256, fi_upd_tc_smem(h->fi_smax[l]), st>>>(h->S, Pd, h->fi, rs, h->fi_smax[l]);

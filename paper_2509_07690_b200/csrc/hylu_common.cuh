@@ -5,6 +5,13 @@
 
 #define HY_FULL 0xffffffffu
 
+// Programmatic dependent launch (PDL): a kernel launched with programmatic stream
+// serialization may start while its predecessor runs; it waits here until the
+// predecessor grid has completed (and its writes are visible), then lets its own
+// successor start launching.  Both are no-ops for a normally launched kernel.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 namespace hy {
 
 // Symbolic structure resident on the device (uploaded once by hy_upload_symbolic).

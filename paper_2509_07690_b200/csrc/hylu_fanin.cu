@@ -68,6 +68,8 @@ constexpr int FXLD = 65;
 // ---------------------------------------------------------------------------- scatter
 // warp per M row: physical row = inverse of the prior inner_perm on refactorize
 __device__ __forceinline__ void d_fi_scatter(DevSym S, const CallP *__restrict__ Pd, int bid) {
+  pdl_wait();
+  pdl_launch_dependents();
   const CallP P = *Pd;
   const int warp = (bid * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= S.n) return;
@@ -93,6 +95,8 @@ __global__ void k_fi_scatter(DevSym S, const CallP *__restrict__ Pd) { d_fi_scat
 
 // ---------------------------------------------------------------------------- LU
 __device__ __forceinline__ void d_fi_lu(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base, int bid) {
+  pdl_wait();
+  pdl_launch_dependents();
   const CallP P = *Pd;
   extern __shared__ __align__(16) double lu_dyn[];
   double *B = lu_dyn;                  // [64 * FXLD] (dynamic: fi_lu_smem())
@@ -211,6 +215,8 @@ __device__ __forceinline__ void panel_trsm_col(double *tl, const double *Lb, int
 }
 
 __device__ __forceinline__ void d_fi_panel(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base, int bid) {
+  pdl_wait();
+  pdl_launch_dependents();
   const CallP P = *Pd;
   extern __shared__ __align__(16) double tl[];   // s x (c1-c0), stride PANEL
   double *Lb = tl + 64 * 256;                    // [64 * FXLD] after the tile (fi_panel_smem())
@@ -263,6 +269,8 @@ __global__ void __launch_bounds__(FI_THREADS) k_fi_panel(DevSym S, const CallP *
 // ---------------------------------------------------------------------------- X blocks
 // X = T[:, pb0 .. pb0+m) · U_bb⁻¹ in place; 4 threads per target row.
 __device__ __forceinline__ void d_fi_x(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base, int bid) {
+  pdl_wait();
+  pdl_launch_dependents();
   const CallP P = *Pd;
   extern __shared__ __align__(16) double xsm[];
   double *Ub = xsm;
@@ -348,6 +356,8 @@ __global__ void __launch_bounds__(FI_THREADS) k_fi_x(DevSym S, const CallP *__re
 // b > a, skipped when x_a == 0).
 constexpr int XW_M = 8;
 __device__ __forceinline__ void d_fi_x_w(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base, int count, int bid) {
+  pdl_wait();
+  pdl_launch_dependents();
   const CallP P = *Pd;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int jj = bid * (FI_THREADS / 32) + warp;
@@ -399,6 +409,8 @@ __global__ void __launch_bounds__(FI_THREADS) k_fi_x_w(DevSym S, const CallP *__
 constexpr int UW_ROWS = 4;
 constexpr int UW_TILE = 64;   // == FI_TILE
 __device__ __forceinline__ void d_fi_upd_w(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base, int count, int bid) {
+  pdl_wait();
+  pdl_launch_dependents();
   const CallP P = *Pd;
   extern __shared__ __align__(16) double uw_dyn[];   // [FI_THREADS / 32][UW_ROWS * UW_TILE] (fi_upd_w_smem())
   double (*tile_s)[UW_ROWS * UW_TILE] = reinterpret_cast<double (*)[UW_ROWS * UW_TILE]>(uw_dyn);
@@ -1024,6 +1036,8 @@ __device__ __forceinline__ void kc_chunk(const double *X, const double *U, int k
 
 template <bool CHAIN>
 __device__ __forceinline__ void d_fi_upd_kc(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base, int bid) {
+  pdl_wait();
+  pdl_launch_dependents();
   const CallP P = *Pd;
   extern __shared__ __align__(16) double fs[];
   __shared__ int tcol[FI_TILE];
@@ -1334,6 +1348,8 @@ __global__ void __launch_bounds__(FI_THREADS, KC_MINB_DEF) k_fi_upd_kc(DevSym S,
 // them in part order.  Replaces k_fi_upd_pk (fanin_tc=5): c2 350 -> 340 ms.
 template <bool CHAIN>
 __device__ __forceinline__ void d_fi_upd_kcp(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base, int bid) {
+  pdl_wait();
+  pdl_launch_dependents();
   const CallP P = *Pd;
   extern __shared__ __align__(16) double fs[];
   __shared__ int tcol[FI_TILE];
