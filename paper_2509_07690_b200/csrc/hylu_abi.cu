@@ -1452,18 +1452,15 @@ static int solve_levels(hy_handle *h, cudaStream_t st) {
       const int c = (int)(pl.aptr[l + 1] - pl.aptr[l]);
       const int nch = (int)(sp.cptr[l + 1] - sp.cptr[l]);
       if (nch) {
-        k_solve_part<<<nch, 256, 0, st>>>(h->S, h->d_fptr, sp.d_chunks + sp.cptr[l], nch, h->d_y,
-                                         h->d_solve_scratch, dir == 0);
+        CK(launchx(k_solve_part, dim3(nch), dim3(256), 0, st, h->use_pdl, h->S, (const double *const *)h->d_fptr,
+                   (const SolveChunk *)(sp.d_chunks + sp.cptr[l]), nch, (const double *)h->d_y,
+                   h->d_solve_scratch, (int)(dir == 0)));
         h->launches++;
       }
-      if (dir == 0)
-        k_fwd_fin<<<(c + 3) / 4, 128, 0, st>>>(h->S, h->d_fptr, pl.d_all + pl.aptr[l],
-                                               sp.d_slot0 + pl.aptr[l], sp.d_nslot + pl.aptr[l], c,
-                                               h->d_solve_scratch, h->d_y);
-      else
-        k_bwd_fin<<<(c + 3) / 4, 128, 0, st>>>(h->S, h->d_fptr, pl.d_all + pl.aptr[l],
-                                               sp.d_slot0 + pl.aptr[l], sp.d_nslot + pl.aptr[l], c,
-                                               h->d_solve_scratch, h->d_y);
+      CK(launchx(dir == 0 ? k_fwd_fin : k_bwd_fin, dim3((c + 3) / 4), dim3(128), 0, st, h->use_pdl, h->S,
+                 (const double *const *)h->d_fptr, (const int32_t *)(pl.d_all + pl.aptr[l]),
+                 (const int32_t *)(sp.d_slot0 + pl.aptr[l]), (const int32_t *)(sp.d_nslot + pl.aptr[l]), c,
+                 (const double *)h->d_solve_scratch, h->d_y));
       h->launches++;
     }
   }
@@ -1756,8 +1753,8 @@ int hy_solve_batched(hy_handle *h, int64_t B, const double *d_b, double *d_x, ui
     const int c = (int)(bp.aptr[l + 1] - bp.aptr[l]);
     const int GP = (G + 1) / 2;
     const int64_t tasks = (int64_t)c * GP;
-    k_batch_bwd2<<<(unsigned)((tasks + 3) / 4), 128, 0, st>>>(h->S, h->d_bf, h->stored,
-                                                            bp.d_all + bp.aptr[l], c, GP, h->d_by);
+    CK(launchx(k_batch_bwd2, dim3((unsigned)((tasks + 3) / 4)), dim3(128), 0, st, h->use_pdl, h->S,
+               (const double *)h->d_bf, h->stored, (const int32_t *)(bp.d_all + bp.aptr[l]), c, GP, h->d_by));
     h->launches++;
   }
   if (!h->d_pinv) {

@@ -824,6 +824,8 @@ __global__ void __launch_bounds__(BW * 32) k_batch_fwd(DevSym S, const double *B
 __global__ void __launch_bounds__(BW * 32) k_batch_bwd2(DevSym S, const double *BF, int64_t stored,
                                                         const int32_t *nodes, int count, int GP,
                                                         double *Y) {
+  pdl_wait();
+  pdl_launch_dependents();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t task = (int64_t)blockIdx.x * BW + warp;
   if (task >= (int64_t)count * GP) return;

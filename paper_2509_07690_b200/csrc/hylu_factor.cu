@@ -637,6 +637,8 @@ struct SolveChunk {
 
 __global__ void k_solve_part(DevSym S, const double *const *Fp, const SolveChunk *ch, int count,
                              const double *y, double *scratch, int fwd) {
+  pdl_wait();
+  pdl_launch_dependents();
   const double *F = *Fp;   // factor values of this call (device-resident pointer: graph replay)
   const int j = blockIdx.x;
   if (j >= count) return;
@@ -720,6 +722,8 @@ __device__ __forceinline__ void offblock_dots(const double *Fu, int W, const int
 
 __global__ void k_fwd_fin(DevSym S, const double *const *Fp, const int32_t *nodes, const int32_t *slot0,
                           const int32_t *nslot, int count, const double *scratch, double *y) {
+  pdl_wait();
+  pdl_launch_dependents();
   const double *F = *Fp;   // factor values of this call (device-resident pointer: graph replay)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int idx = blockIdx.x * (blockDim.x >> 5) + warp;
@@ -772,6 +776,8 @@ __global__ void k_fwd_fin(DevSym S, const double *const *Fp, const int32_t *node
 // backward finish: z_t = (y_t - sum(partials) - sum_{tt>t} U[t][tt] z_tt) / U[t][t]
 __global__ void k_bwd_fin(DevSym S, const double *const *Fp, const int32_t *nodes, const int32_t *slot0,
                           const int32_t *nslot, int count, const double *scratch, double *y) {
+  pdl_wait();
+  pdl_launch_dependents();
   const double *F = *Fp;   // factor values of this call (device-resident pointer: graph replay)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int idx = blockIdx.x * (blockDim.x >> 5) + warp;
