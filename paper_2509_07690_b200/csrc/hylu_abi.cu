@@ -207,7 +207,6 @@ struct hy_handle {
   int32_t *d_node_level = nullptr;
   int pipe_blocks = 0;
   int warp_min = 256;                      // fan-in: below this many small items per level, CTA kernels only
-  int pipe_skew = 1;                       // option "pipe_skew" (claim-order slope)
   int pipe_ws = 6;                         // pair-mode shared workspace columns per group (c4 ms/step: 4: 15.50, 6: 15.48, 8: 15.64, 10: 15.64, 16: 16.65 before the reciprocals)
   // diagonal claim order per (segment, G): pair prefix sums, (level<<16|group), level offsets
   struct Seg {
@@ -405,7 +404,7 @@ static int build_segments(hy_handle *h, int G) {
         t.dep[k] = t.d0 + k < t.d1 ? h->h_deps[t.d0 + k] : -1;
       return t;
     };
-    const int sk = h->pipe_skew;   // diagonal slope: pair g's level k is claimed at d = k + sk*g
+    const int sk = 1;   // diagonal slope (2-4 measured slower)
     const int gs = 2;                         // pair mode: tasks carry the even group of a pair
     const int GT = (G + gs - 1) / gs;
     for (int d = 0; d < sk * (GT - 1) + L; ++d)
@@ -584,11 +583,6 @@ int hy_set_option(hy_handle *h, const char *name, int64_t value) {
   }
   if (std::string(name) == "fanin_warp_min" && value >= 1) {
     h->warp_min = (int)value;
-    return HY_OK;
-  }
-  if (std::string(name) == "pipe_skew" && value >= 1 && value <= 16) {
-    h->pipe_skew = (int)value;
-    free_segments(h);   // the claim order is baked into the cached task lists
     return HY_OK;
   }
   if (std::string(name) == "pipe_blocks" && value >= 0) {   // 0: occupancy-derived (default)

@@ -692,3 +692,45 @@ def test_solve_multi_small_segments_and_refinement():
         assert refmatrix.backward_error(A1, X[j], B[j]) <= 1e-13
         xj, _ = api.solve(A1, f, b=B[j])
         assert _rel(X[j], xj) <= 1e-12
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_launch_options_do_not_change_results(name):
+    """Launch-level options are scheduling only: factors and solutions are bitwise
+    equal with programmatic dependent launch, CUDA graphs and the two-stream phase
+    overlap switched off; the batched path likewise for PDL and the pair-workspace
+    width."""
+    import torch
+    p, an = _analysis(name)
+    f = api.factorize_analysis(an)
+    ctx = f._ctx
+    b = torch.from_numpy(np.asarray(p.b, np.float64)).cuda()
+    x = api.substitute(f, b)
+    try:
+        for opt in ("pdl", "graphs", "fanin_overlap"):
+            ctx.set_option(opt, 0)
+            g = api.factorize_analysis(an)
+            assert torch.equal(g.values, f.values), opt
+            assert torch.equal(api.substitute(g, b), x), opt
+            ctx.set_option(opt, 1)
+    finally:
+        for opt in ("pdl", "graphs", "fanin_overlap"):
+            ctx.set_option(opt, 1)
+    if name == "c1":
+        bp = gen.circuit_batch(70, 2000, 2, 200)
+        an4 = an_mod.analyze(bp.A0, SolverConfig(ordering="amd"))
+        prior = api.factorize_analysis(an4)
+        br = api.BatchedRefactorizer(prior)
+        dv = torch.from_numpy(bp.values).cuda()
+        dr = torch.from_numpy(bp.rhs).cuda()
+        x0, _ = br.run(dv, dr)
+        x0 = x0.clone()
+        c4 = br.ctx
+        try:
+            for opt, val in (("pdl", 0), ("pipe_ws", 16), ("pipe_ws", 2)):
+                c4.set_option(opt, val)
+                x1, _ = br.run(dv, dr)
+                assert torch.equal(x1, x0), (opt, val)
+        finally:
+            c4.set_option("pdl", 1)
+            c4.set_option("pipe_ws", 6)
