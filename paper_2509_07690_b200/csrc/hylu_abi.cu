@@ -207,6 +207,7 @@ struct hy_handle {
   int32_t *d_node_level = nullptr;
   int pipe_blocks = 0;
   int warp_min = 256;                      // fan-in: below this many small items per level, CTA kernels only
+  int pipe_order = 1;                      // claim order of the batched pipeline: 0 diagonal (level + pair), k >= 1: diagonal below level k-1... see build_segments
   int pipe_ws = 6;                         // pair-mode shared workspace columns per group (c4 ms/step: 4: 15.50, 6: 15.48, 8: 15.64, 10: 15.64, 16: 16.65 before the reciprocals)
   // diagonal claim order per (segment, G): pair prefix sums, (level<<16|group), level offsets
   struct Seg {
@@ -407,13 +408,21 @@ static int build_segments(hy_handle *h, int G) {
     const int sk = 1;   // diagonal slope (2-4 measured slower)
     const int gs = 2;                         // pair mode: tasks carry the even group of a pair
     const int GT = (G + gs - 1) / gs;
-    for (int d = 0; d < sk * (GT - 1) + L; ++d)
-      for (int k = lb; k < L && k <= d; ++k) {
+    // pipe_order = 0: diagonal over every level.  pipe_order = K >= 1: the levels
+    // below K-1 stay diagonal, the levels from K-1 up are claimed level by level
+    // across all pairs (K = 1: pure level-major), so every pair's narrow top levels
+    // run concurrently instead of the last pairs' chains forming a tail.
+    const int Ld = h->pipe_order == 0 ? L : std::min(L, h->pipe_order - 1);
+    for (int d = 0; d < sk * (GT - 1) + Ld; ++d)
+      for (int k = lb; k < Ld && k <= d; ++k) {
         if ((d - k) % sk) continue;
         const int g = (d - k) / sk;
         if (g >= GT) continue;
         for (int64_t q = h->bl_rptr[l + k]; q < h->bl_rptr[l + k + 1]; ++q) tasks.push_back(mk(rows[q], g * gs));
       }
+    for (int k = Ld; k < L; ++k)
+      for (int g = 0; g < GT; ++g)
+        for (int64_t q = h->bl_rptr[l + k]; q < h->bl_rptr[l + k + 1]; ++q) tasks.push_back(mk(rows[q], g * gs));
     sg.ntasks = (int64_t)tasks.size();
     if (sg.ntasks) {
       CK(cudaMalloc((void **)&sg.d_tasks, sizeof(TaskDesc) * sg.ntasks));
@@ -587,6 +596,11 @@ int hy_set_option(hy_handle *h, const char *name, int64_t value) {
   }
   if (std::string(name) == "pipe_blocks" && value >= 0) {   // 0: occupancy-derived (default)
     h->pipe_blocks = (int)value;
+    return HY_OK;
+  }
+  if (std::string(name) == "pipe_order" && value >= 0) {
+    h->pipe_order = (int)value;
+    free_segments(h);
     return HY_OK;
   }
   if (std::string(name) == "pipe_ws" && value >= 1 && value <= 64) {
@@ -1540,7 +1554,21 @@ int hy_upload_row_programs(hy_handle *h, const hy_row_programs *d) {
       if (k1 <= k0) continue;
       const int64_t rel0 = d->st_rel[k0];
       const int64_t nrel = d->st_rel[k1 - 1] + d->st_cnt[k1 - 1] - rel0;
-      if (k1 - k0 > PIPE_REC_CAP || nrel + 6 > PIPE_REL_CAP) continue;   // not stageable
+      if (k1 - k0 > PIPE_REC_CAP || nrel + 6 > PIPE_REL_CAP) {
+        // too large for one window: stage row by row when every row fits
+        bool rows_ok = true;
+        for (int64_t i = h->h_first[u]; i < h->h_first[u + 1] && rows_ok; ++i) {
+          const int64_t a = d->row_ptr[i], b = d->row_ptr[i + 1];
+          if (b > a && (b - a > PIPE_REC_CAP || d->st_rel[b - 1] + d->st_cnt[b - 1] - d->st_rel[a] + 6 > PIPE_REL_CAP))
+            rows_ok = false;
+        }
+        if (!rows_ok) continue;   // global step arrays
+        for (int64_t i = h->h_first[u]; i < h->h_first[u + 1]; ++i)
+          for (int64_t k = d->row_ptr[i]; k < d->row_ptr[i + 1]; ++k)
+            rec[k].rl = (int16_t)(d->st_rel[k] - d->st_rel[d->row_ptr[i]]);
+        h->h_win[u] = {0, 0, 0, -1};
+        continue;
+      }
       for (int64_t k = k0; k < k1; ++k) rec[k].rl = (int16_t)(d->st_rel[k] - rel0);
       h->h_win[u] = {rel0, k0, k1 - k0, nrel};
     }
@@ -1550,6 +1578,9 @@ int hy_upload_row_programs(hy_handle *h, const hy_row_programs *d) {
       UPP(&q, rec.data(), ns + 1);
       R.st_rec = q;
     }
+    std::vector<int64_t> row_rel(n + 1);
+    for (int64_t i = 0; i <= n; ++i) row_rel[i] = d->row_ptr[i] < ns ? d->st_rel[d->row_ptr[i]] : d->nrel;
+    UPP(&p64, row_rel.data(), n + 1); R.row_rel = p64;
   }
   std::vector<int32_t> hub_base(nn, -1);
   std::vector<int64_t> first(nn + 1);

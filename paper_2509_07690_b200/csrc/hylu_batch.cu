@@ -271,12 +271,36 @@ __device__ __forceinline__ void row_init2(const DevSym &S, const BatchP &P, cons
   __syncwarp();
 }
 
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(d), "l"(src), "r"(bytes), "r"(b) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  unsigned done = 0;
+  while (!done)
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done) : "r"(a), "r"(phase) : "memory");
+}
+
 __device__ __forceinline__ void bt_node2(const DevSym &S, const BatchP &P, const DevProg &R,
                                          const longlong4 nr, int g, const double *rhs, double *Y,
                                          double *wsm0, int ws, int lane, int xmask, longlong4 rr,
                                          bool pre0, double y0A, double y0C,
                                          const StepRec *srec = nullptr, const int32_t *srel = nullptr,
-                                         int64_t sk0 = 0) {
+                                         int64_t sk0 = 0, bool rowstage = false, uint64_t *mbar = nullptr,
+                                         unsigned *phase = nullptr, StepRec *srecbuf = nullptr,
+                                         int32_t *srelbuf = nullptr) {
   const int64_t ba = (int64_t)g * 32 + lane, bc = ba + 32;
   const bool liveA = ba < P.B, liveC = bc < P.B;
   const int64_t rem = P.B - (int64_t)g * 32;
@@ -304,10 +328,31 @@ __device__ __forceinline__ void bt_node2(const DevSym &S, const BatchP &P, const
     double *wA = inSm ? wsm0 : growA;
     double *wC = inSm ? wsm0 + ws * 32 : growC;
     double yaccA = y0A, yaccC = y0C;
+    // node too large for one program window: stage this row's window (its steps and
+    // their target positions) instead, in flight while the row is initialised
+    if (rowstage && s1 > s0) {
+      const int64_t rl0 = R.row_rel[i], rl1 = R.row_rel[i + 1];
+      if (lane == 0) {
+        const int64_t a0 = (rl0 * 4) & ~(int64_t)15;
+        const int64_t a1 = (rl1 * 4 + 15) & ~(int64_t)15;
+        const unsigned brec = (unsigned)(s1 - s0) * 16u, brel = (unsigned)(a1 - a0);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(mbar, brec + brel);
+        bulk_g2s(srecbuf, R.st_rec + s0, brec, mbar);
+        bulk_g2s(srelbuf, reinterpret_cast<const char *>(R.rel) + a0, brel, mbar);
+      }
+      srec = srecbuf;
+      srel = srelbuf + (int)(rl0 & 3);
+      sk0 = s0;
+    }
     if (!(t == 0 && pre0))
       row_init2(S, P, rr, W, wA, wC, Ab, nlive, lane, ba, bc, liveA, liveC, rhs, xmask, yaccA, yaccC,
                 ya + (int64_t)i * 32, yc + (int64_t)i * 32);
     if (t + 1 < s) rr = R.row_rec[i + 1];
+    if (rowstage && s1 > s0) {
+      mbar_wait(mbar, *phase);
+      *phase ^= 1u;
+    }
     if (!(xmask & 2)) {
       if (srec) {
         if (inSm)
@@ -356,27 +401,21 @@ __device__ __forceinline__ void bt_node2(const DevSym &S, const BatchP &P, const
 constexpr int PIPE_STAGE = 16 + PIPE_REC_CAP * 16 + PIPE_REL_CAP * 4;
 size_t pipe_smem(int ws) { return (size_t)PIPE_WARPS * (2 * ws * 32 * 8 + PIPE_STAGE); }
 
-__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
-  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+#ifdef HYLU_TRACE
+// Debug build only (-DHYLU_TRACE, scripts/pipe_trace.py): per task {claim, ready, end}
+// global timestamps and (node, group, SM id), written through hy_debug_pipe_trace's buffer.
+__device__ unsigned long long *g_pipe_trace = nullptr;
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
 }
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
-  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+__device__ __forceinline__ unsigned smid() {
+  unsigned s;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(s));
+  return s;
 }
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-               ::"r"(d), "l"(src), "r"(bytes), "r"(b) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
-  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
-  unsigned done = 0;
-  while (!done)
-    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                 : "=r"(done) : "r"(a), "r"(phase) : "memory");
-}
+#endif
 
 __global__ void __launch_bounds__(PIPE_WARPS * 32, PIPE_MINB_DEF)
     k_bt_pipe2(DevSym S, BatchP P, DevProg R, const TaskDesc *tasks, int64_t total, const double *rhs,
@@ -401,10 +440,18 @@ __global__ void __launch_bounds__(PIPE_WARPS * 32, PIPE_MINB_DEF)
     t = __shfl_sync(HY_FULL, t, 0);
     if (t >= total) return;
     const TaskDesc cur = tasks[t];
+#ifdef HYLU_TRACE
+    unsigned long long *tr = (g_pipe_trace && total > 1000) ? g_pipe_trace + 4 * t : nullptr;
+    if (tr && lane == 0) {
+      tr[0] = gtime();
+      tr[3] = ((unsigned long long)cur.u << 32) | ((unsigned long long)cur.g << 16) | smid();
+    }
+#endif
     const int two = cur.g + 1 < G ? 2 : 1;
     const int64_t nd = cur.d1 - cur.d0;
     // the task's program window into shared memory, in flight while the polls wait
     const bool staged = R.st_rec != nullptr && cur.nk > 0;
+    const bool rowstage = R.st_rec != nullptr && cur.nk == 0 && cur.nrel < 0;   // per-row windows
     int roff = 0;
     if (staged && lane == 0) {
       const int64_t a0 = (cur.rel0 * 4) & ~(int64_t)15;
@@ -441,15 +488,27 @@ __global__ void __launch_bounds__(PIPE_WARPS * 32, PIPE_MINB_DEF)
       mbar_wait(mbar, phase);
       phase ^= 1u;
     }
+#ifdef HYLU_TRACE
+    if (tr && lane == 0) tr[1] = gtime();
+#endif
     const longlong4 nr = make_longlong4(cur.valoff, cur.d0, (int64_t)cur.r | ((int64_t)cur.s << 32),
                                         (int64_t)cur.W | ((int64_t)cur.L << 32));
     bt_node2(S, P, R, nr, cur.g, rhs, Y, wsm_w, ws, lane, 0, cur.rr0, false, 0.0, 0.0,
-             staged ? srec : nullptr, srel + roff, cur.k0);
+             staged ? srec : nullptr, srel + roff, cur.k0, rowstage, mbar, &phase, srec, srel);
     fence_acq_rel_gpu();
     __syncwarp();
+#ifdef HYLU_TRACE
+    if (tr && lane == 0) tr[2] = gtime();
+#endif
     if (lane < two) st_relaxed(flags + (int64_t)cur.u * G + cur.g + lane, epoch);
   }
 }
+
+#ifdef HYLU_TRACE
+extern "C" int hy_debug_pipe_trace(unsigned long long *d_buf) {
+  return (int)cudaMemcpyToSymbol(g_pipe_trace, &d_buf, sizeof(d_buf));
+}
+#endif
 
 // ---------------------------------------------------------------------------
 // Hub kernel: one CTA per (hub node, group).  Pull programs: the positions of a row

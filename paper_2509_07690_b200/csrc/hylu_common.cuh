@@ -108,7 +108,7 @@ struct TaskDesc {
   int32_t dep[4];  // the first (up to) 4 dependencies, inline (no dependent index load)
   int64_t rel0;    // first rel entry of the node's program window
   int32_t k0, nk;  // the node's steps [k0, k0 + nk)
-  int32_t nrel;    // rel entries of the window (0: not stageable)
+  int32_t nrel;    // rel entries of the window (0: not stageable; -1 with nk == 0: staged row by row)
   int32_t pad[3];
 };
 
@@ -121,6 +121,7 @@ struct DevProg {
   const int32_t *st_cnt;
   const int64_t *st_rel;
   const int32_t *rel;
+  const int64_t *row_rel;   // [n+1] first rel entry of each row's steps (per-row program windows)
   const int32_t *hub_base;  // [nn] first hub-row index of a hub node, -1 otherwise
   const int64_t *hrow_lev;
   const int64_t *lev_ptr;

@@ -698,8 +698,8 @@ def test_solve_multi_small_segments_and_refinement():
 def test_launch_options_do_not_change_results(name):
     """Launch-level options are scheduling only: factors and solutions are bitwise
     equal with programmatic dependent launch, CUDA graphs and the two-stream phase
-    overlap switched off; the batched path likewise for PDL and the pair-workspace
-    width."""
+    overlap switched off; the batched path likewise for PDL, the pair-workspace
+    width and the pipeline's claim order (diagonal / level-major)."""
     import torch
     p, an = _analysis(name)
     f = api.factorize_analysis(an)
@@ -727,10 +727,11 @@ def test_launch_options_do_not_change_results(name):
         x0 = x0.clone()
         c4 = br.ctx
         try:
-            for opt, val in (("pdl", 0), ("pipe_ws", 16), ("pipe_ws", 2)):
+            for opt, val in (("pdl", 0), ("pipe_ws", 16), ("pipe_ws", 2), ("pipe_order", 0), ("pipe_order", 4)):
                 c4.set_option(opt, val)
                 x1, _ = br.run(dv, dr)
                 assert torch.equal(x1, x0), (opt, val)
         finally:
             c4.set_option("pdl", 1)
             c4.set_option("pipe_ws", 6)
+            c4.set_option("pipe_order", 1)
