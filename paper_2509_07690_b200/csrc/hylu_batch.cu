@@ -51,6 +51,10 @@ __device__ __forceinline__ void st_relaxed(int *p, int v) {
   asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+// one-sided fences: the release side is a MEMBAR without the L1 invalidation (CCTL.IVALL)
+// that fence.acq_rel appends; the acquire side is the invalidation alone
+__device__ __forceinline__ void fence_release_gpu() { asm volatile("fence.release.gpu;" ::: "memory"); }
+__device__ __forceinline__ void fence_acquire_gpu() { asm volatile("fence.acquire.gpu;" ::: "memory"); }
 __device__ __forceinline__ void st_release(int *p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -71,6 +75,21 @@ __device__ __forceinline__ void cp_async_wait_all() {
 }
 
 constexpr int PIPE_WARPS = 4;
+#ifdef HYLU_TRACE
+// phase cycle counters of a pipeline task (debug build, scripts/pipe_trace.py)
+struct TraceAcc {
+  long long init, mult, upd, fin;
+};
+#define TR_DECL , TraceAcc &tacc
+#define TR_ARG , tacc
+#define TR_T(x) const long long x = clock64();
+#define TR_ADD(f, a, b) tacc.f += (b) - (a);
+#else
+#define TR_DECL
+#define TR_ARG
+#define TR_T(x)
+#define TR_ADD(f, a, b)
+#endif
 // Persistent, dependency-driven row kernel for a segment of levels without hub
 // nodes (the device form of SPEC's pipeline mode): warps claim
 // (node, group) tasks in level-major order from an atomic counter, wait on the
@@ -167,7 +186,7 @@ template <typename WPtr>
 __device__ __forceinline__ void run_steps2s(const StepRec *rec, const int32_t *relw, int s0, int s1, WPtr wa,
                                             WPtr wc, const double *ga, const double *gc,
                                             const double *ya, const double *yc, double &acA,
-                                            double &acC, const double *ria, const double *ric) {
+                                            double &acC, const double *ria, const double *ric TR_DECL) {
   if (s0 >= s1) return;
   StepRec cr = rec[s0];
   double da = PIPE_RINV ? __ldcg(ria + (int64_t)cr.j * 32) : __ldcg(ga + (int64_t)cr.src * 32);
@@ -183,6 +202,7 @@ __device__ __forceinline__ void run_steps2s(const StepRec *rec, const int32_t *r
       yna = __ldcg(ya + (int64_t)nx.j * 32);
       ync = __ldcg(yc + (int64_t)nx.j * 32);
     }
+    TR_T(c0)
     const int p = cr.p, cnt = cr.cnt;
     const int32_t *rl = relw + cr.rl;
     const double *ua = ga + ((int64_t)cr.src + 1) * 32;
@@ -193,6 +213,8 @@ __device__ __forceinline__ void run_steps2s(const StepRec *rec, const int32_t *r
     wc[p * 32] = lc;
     acA -= la * yja;
     acC -= lc * yjc;
+    TR_T(c1)
+    TR_ADD(mult, c0, c1)
     for (int q = 0; q < cnt; q += P2W) {
       int t[P2W];
       double xa[P2W], xc[P2W];
@@ -216,10 +238,15 @@ __device__ __forceinline__ void run_steps2s(const StepRec *rec, const int32_t *r
           wc[t[k] * 32] = vc[k] - lc * xc[k];
         }
     }
+    TR_T(c2)
+    TR_ADD(upd, c1, c2)
     cr = nx; da = dna; dc = dnc; yja = yna; yjc = ync;
   }
 }
 
+#ifndef RI_W
+#define RI_W 8   // matrix entries per load batch of the row initialisation (c4 ms/step: 4: 14.79, 6: 14.79, 8: 14.75)
+#endif
 // Row initialisation of a pair task: zero the accumulators, scatter the row's
 // matrix values (lanes over (instance, entry) pairs, 4 per lane per batch, loads
 // before stores) and form b̂_i for both groups.  Needs no dependency: the pipeline
@@ -249,11 +276,11 @@ __device__ __forceinline__ void row_init2(const DevSym &S, const BatchP &P, cons
   if (!(xmask & 4)) {
     const double *rA = Ab + (int64_t)lane * S.nnz + e0;
     const double *rC = rA + (int64_t)32 * S.nnz;
-    for (int e = 0; e < k; e += 4) {
-      int cp[4];
-      double sc[4], va[4], vc[4];
+    for (int e = 0; e < k; e += RI_W) {
+      int cp[RI_W];
+      double sc[RI_W], va[RI_W], vc[RI_W];
 #pragma unroll
-      for (int m = 0; m < 4; ++m) {
+      for (int m = 0; m < RI_W; ++m) {
         const bool ok = e + m < k;
         cp[m] = ok ? __ldg(S.colpos + e0 + e + m) : 0;
         sc[m] = ok ? __ldg(S.scale + e0 + e + m) : 0.0;
@@ -261,7 +288,7 @@ __device__ __forceinline__ void row_init2(const DevSym &S, const BatchP &P, cons
         vc[m] = (ok && liveC) ? __ldg(rC + e + m) : 0.0;
       }
 #pragma unroll
-      for (int m = 0; m < 4; ++m)
+      for (int m = 0; m < RI_W; ++m)
         if (e + m < k) {
           wA[cp[m] * 32 + lane] = va[m] * sc[m];
           wC[cp[m] * 32 + lane] = vc[m] * sc[m];
@@ -297,10 +324,9 @@ __device__ __forceinline__ void bt_node2(const DevSym &S, const BatchP &P, const
                                          const longlong4 nr, int g, const double *rhs, double *Y,
                                          double *wsm0, int ws, int lane, int xmask, longlong4 rr,
                                          bool pre0, double y0A, double y0C,
-                                         const StepRec *srec = nullptr, const int32_t *srel = nullptr,
-                                         int64_t sk0 = 0, bool rowstage = false, uint64_t *mbar = nullptr,
-                                         unsigned *phase = nullptr, StepRec *srecbuf = nullptr,
-                                         int32_t *srelbuf = nullptr) {
+                                         const StepRec *srec, const int32_t *srel, int64_t sk0,
+                                         bool rowstage, uint64_t *mbar, unsigned *phase,
+                                         StepRec *srecbuf, int32_t *srelbuf TR_DECL) {
   const int64_t ba = (int64_t)g * 32 + lane, bc = ba + 32;
   const bool liveA = ba < P.B, liveC = bc < P.B;
   const int64_t rem = P.B - (int64_t)g * 32;
@@ -345,9 +371,12 @@ __device__ __forceinline__ void bt_node2(const DevSym &S, const BatchP &P, const
       srel = srelbuf + (int)(rl0 & 3);
       sk0 = s0;
     }
+    TR_T(b0)
     if (!(t == 0 && pre0))
       row_init2(S, P, rr, W, wA, wC, Ab, nlive, lane, ba, bc, liveA, liveC, rhs, xmask, yaccA, yaccC,
                 ya + (int64_t)i * 32, yc + (int64_t)i * 32);
+    TR_T(b1)
+    TR_ADD(init, b0, b1)
     if (t + 1 < s) rr = R.row_rec[i + 1];
     if (rowstage && s1 > s0) {
       mbar_wait(mbar, *phase);
@@ -357,16 +386,17 @@ __device__ __forceinline__ void bt_node2(const DevSym &S, const BatchP &P, const
       if (srec) {
         if (inSm)
           run_steps2s(srec, srel, (int)(s0 - sk0), (int)(s1 - sk0), wA + lane, wC + lane, ga0 + lane,
-                      gc0 + lane, ya, yc, yaccA, yaccC, ria, ric);
+                      gc0 + lane, ya, yc, yaccA, yaccC, ria, ric TR_ARG);
         else
           run_steps2s(srec, srel, (int)(s0 - sk0), (int)(s1 - sk0), growA + lane, growC + lane, ga0 + lane,
-                      gc0 + lane, ya, yc, yaccA, yaccC, ria, ric);
+                      gc0 + lane, ya, yc, yaccA, yaccC, ria, ric TR_ARG);
       } else if (inSm)
         run_steps2(R, s0, s1, wA + lane, wC + lane, ga0 + lane, gc0 + lane, ya, yc, yaccA, yaccC, ria, ric);
       else
         run_steps2(R, s0, s1, growA + lane, growC + lane, ga0 + lane, gc0 + lane, ya, yc, yaccA, yaccC, ria,
                    ric);
     }
+    TR_T(b2)
     const int Lt = L + t;
     bool fa, fc;
     wA[Lt * 32 + lane] = perturb(wA[Lt * 32 + lane], thr, fa);
@@ -385,6 +415,8 @@ __device__ __forceinline__ void bt_node2(const DevSym &S, const BatchP &P, const
         growC[q * 32 + lane] = wC[q * 32 + lane];
       }
     __syncwarp();
+    TR_T(b3)
+    TR_ADD(fin, b2, b3)
   }
 }
 
@@ -392,6 +424,9 @@ __device__ __forceinline__ void bt_node2(const DevSym &S, const BatchP &P, const
 // waits for both groups' dependency flags and publishes both.
 #ifndef PIPE_MINB_DEF
 #define PIPE_MINB_DEF 4
+#endif
+#ifndef PIPE_REL
+#define PIPE_REL 1   // producer fence: 1 fence.release (MEMBAR only), 0 fence.acq_rel (MEMBAR + L1 invalidation)
 #endif
 #ifndef PIPE_ACQ
 #define PIPE_ACQ 2   // consumer acquire: 2 (default) one ld.acquire per observed flag after the relaxed spin, 1 one fence after the polls (+0.25 ms/step), 0 none (formally racy)
@@ -441,7 +476,9 @@ __global__ void __launch_bounds__(PIPE_WARPS * 32, PIPE_MINB_DEF)
     if (t >= total) return;
     const TaskDesc cur = tasks[t];
 #ifdef HYLU_TRACE
-    unsigned long long *tr = (g_pipe_trace && total > 1000) ? g_pipe_trace + 4 * t : nullptr;
+    unsigned long long *tr = (g_pipe_trace && total > 1000) ? g_pipe_trace + 12 * t : nullptr;
+    TraceAcc tacc{0, 0, 0, 0};
+    const long long k0c = clock64();
     if (tr && lane == 0) {
       tr[0] = gtime();
       tr[3] = ((unsigned long long)cur.u << 32) | ((unsigned long long)cur.g << 16) | smid();
@@ -482,6 +519,8 @@ __global__ void __launch_bounds__(PIPE_WARPS * 32, PIPE_MINB_DEF)
     // synchronization); __syncwarp then orders the other lanes after this lane
 #if PIPE_ACQ == 1
     fence_acq_rel_gpu();
+#elif PIPE_ACQ == 3
+    if (nd > 0) fence_acquire_gpu();
 #endif
     __syncwarp();
     if (staged) {
@@ -489,16 +528,28 @@ __global__ void __launch_bounds__(PIPE_WARPS * 32, PIPE_MINB_DEF)
       phase ^= 1u;
     }
 #ifdef HYLU_TRACE
+    const long long k1c = clock64();
     if (tr && lane == 0) tr[1] = gtime();
 #endif
     const longlong4 nr = make_longlong4(cur.valoff, cur.d0, (int64_t)cur.r | ((int64_t)cur.s << 32),
                                         (int64_t)cur.W | ((int64_t)cur.L << 32));
     bt_node2(S, P, R, nr, cur.g, rhs, Y, wsm_w, ws, lane, 0, cur.rr0, false, 0.0, 0.0,
-             staged ? srec : nullptr, srel + roff, cur.k0, rowstage, mbar, &phase, srec, srel);
+             staged ? srec : nullptr, srel + roff, cur.k0, rowstage, mbar, &phase, srec, srel TR_ARG);
+#ifdef HYLU_TRACE
+    const long long k2c = clock64();
+#endif
+#if PIPE_REL == 1
+    fence_release_gpu();
+#else
     fence_acq_rel_gpu();
+#endif
     __syncwarp();
 #ifdef HYLU_TRACE
-    if (tr && lane == 0) tr[2] = gtime();
+    if (tr && lane == 0) {
+      tr[2] = gtime();
+      tr[4] = tacc.init; tr[5] = tacc.mult; tr[6] = tacc.upd; tr[7] = tacc.fin;
+      tr[8] = k1c - k0c; tr[9] = k2c - k1c; tr[10] = clock64() - k2c; tr[11] = 0;
+    }
 #endif
     if (lane < two) st_relaxed(flags + (int64_t)cur.u * G + cur.g + lane, epoch);
   }

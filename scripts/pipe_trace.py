@@ -32,14 +32,14 @@ for _ in range(3):
 torch.cuda.synchronize()
 lib = device.library()
 nt = s.nnodes * ((B + 63) // 64)
-buf = torch.zeros(nt * 4, dtype=torch.int64, device="cuda")
+buf = torch.zeros(nt * 12, dtype=torch.int64, device="cuda")
 lib.hy_debug_pipe_trace.argtypes = [ctypes.c_void_p]
 rc = lib.hy_debug_pipe_trace(ctypes.c_void_p(buf.data_ptr()))
 assert rc == 0, rc
 x, npert = br.run(dv, dr, refine=False)
 torch.cuda.synchronize()
 lib.hy_debug_pipe_trace(ctypes.c_void_p(0))
-t = buf.cpu().numpy().reshape(-1, 4)
+t = buf.cpu().numpy().reshape(-1, 12)
 t = t[t[:, 0] != 0]
 claim, ready, end, tag = t[:, 0], t[:, 1], t[:, 2], t[:, 3]
 u = tag >> 32
@@ -70,6 +70,24 @@ for l in range(int(lev.max()) + 1):
         l, m.sum(), wait[m].mean(), np.median(wait[m]), np.percentile(wait[m], 99), work[m].mean(),
         np.percentile(work[m], 99), st, cnt_node[u[m]].mean(), work[m].mean() / max(st, 1e-9),
         (claim[m].min() - t0) / 1e3, (claim[m].max() - t0) / 1e3))
+# phase cycle counters (SM clock): claim->deps ready, node body, fence; inside the body:
+# row init (A scatter), multiplier (pivot/target value arrives), update batches, row finalize
+cyc = t[:, 4:11].astype(np.float64)
+names = ["init", "mult", "upd", "fin", "claim+poll", "body", "fence"]
+tot = cyc[:, 4:7].sum()
+print("phase shares of task cycles: " + ", ".join("%s %.1f%%" % (n, 100 * cyc[:, k].sum() / tot) for k, n in enumerate(names)))
+nst = steps_node[u].astype(np.float64)
+nup = cnt_node[u]
+m = nst > 0
+print("per step: mult %.0f cyc, upd %.0f cyc (%.0f per update); per task: init %.0f, fin %.0f, claim+poll %.0f, fence %.0f" % (
+    cyc[m, 1].sum() / nst[m].sum(), cyc[m, 2].sum() / nst[m].sum(), cyc[m, 2].sum() / nup[m].sum(),
+    cyc[:, 0].mean(), cyc[:, 3].mean(), cyc[:, 4].mean(), cyc[:, 6].mean()))
+for lo, hi in [(0, 1), (1, 3), (3, 6), (6, 10), (10, 20), (20, 40)]:
+    mm = (lev >= lo) & (lev < hi)
+    ms = mm & m
+    print("levels %2d-%2d: tasks %7d  init %6.0f  fin %6.0f  claim+poll %6.0f  fence %6.0f | per step mult %5.0f upd %5.0f" % (
+        lo, hi - 1, mm.sum(), cyc[mm, 0].mean(), cyc[mm, 3].mean(), cyc[mm, 4].mean(), cyc[mm, 6].mean(),
+        cyc[ms, 1].sum() / max(1, nst[ms].sum()), cyc[ms, 2].sum() / max(1, nst[ms].sum())))
 # concurrency over time: tasks working / waiting in 100 buckets
 edges = np.linspace(0, span, 51)
 print("time_us  working  waiting")
