@@ -94,4 +94,5 @@ print("time_us  working  waiting")
 for a, b2 in zip(edges[:-1], edges[1:]):
     mid = t0 + (a + b2) / 2 * 1e3
     print("%8.0f %7d %7d" % ((a + b2) / 2, ((ready <= mid) & (end > mid)).sum(), ((claim <= mid) & (ready > mid)).sum()))
-np.save("gpurun_out/pipe_trace.npy", t)
+if os.environ.get("TRACE_SAVE"):
+    np.save("gpurun_out/pipe_trace.npy", t)
