@@ -296,6 +296,10 @@ int hy_batched_factor_values(hy_handle *h, int64_t b, double *d_out, uintptr_t s
  *   "fanin_warp_min" items below which a level keeps its small items on the CTA kernels
  *   "fanin_maps"    0/1 (default 1): host-precomputed source maps in the update kernels
  *   "pipe_ws", "pipe_blocks": batched-pipeline shared workspace / resident CTAs
+ *   "pipe_order"    claim order of the batched pipeline's (node, group pair) tasks: 1 (default)
+ *                   level-major (every pair at level k, then level k+1), 0 diagonal (pair g at
+ *                   level k with pair g+1 at level k-1), K >= 2 diagonal below level K-1 and
+ *                   level-major from there; scheduling only, results bitwise equal
  *   (the measured-slower variants of round 1 were removed; DESIGN.md lists them). */
 int hy_set_option(hy_handle *h, const char *name, int64_t value);
 

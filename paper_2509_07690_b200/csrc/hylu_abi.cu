@@ -125,6 +125,7 @@ __global__ void k_bt_hub(DevSym, BatchP, DevProg, const int32_t *, int, int, con
                          double *, int, int *, int);
 __global__ void k_batch_bhat(DevSym, const int32_t *, const double *, double *, int64_t);
 __global__ void k_batch_fwd(DevSym, const double *, int64_t, const int32_t *, int, int, double *);
+template <int BWDW>
 __global__ void k_batch_bwd2(DevSym, const double *, int64_t, const int32_t *, int, int, double *);
 __global__ void k_batch_xout2(DevSym, const int32_t *, const double *, double *, int64_t);
 __global__ void k_perm_inverse(int, const int64_t *, int32_t *);
@@ -207,12 +208,13 @@ struct hy_handle {
   int32_t *d_node_level = nullptr;
   int pipe_blocks = 0;
   int warp_min = 256;                      // fan-in: below this many small items per level, CTA kernels only
-  int pipe_order = 1;                      // claim order of the batched pipeline: 0 diagonal (level + pair), k >= 1: diagonal below level k-1... see build_segments
+  int64_t bwd_narrow = BWD_NARROW;         // batched backward solve: levels with at most this many tasks use BWD_WL-entry batches
+  int pipe_order = 1;                      // claim order of the batched pipeline: 1 level-major (default), 0 diagonal, K >= 2 diagonal below level K-1 (build_segments)
   int pipe_ws = 6;                         // pair-mode shared workspace columns per group (c4 ms/step: 4: 15.50, 6: 15.48, 8: 15.64, 10: 15.64, 16: 16.65 before the reciprocals)
-  // diagonal claim order per (segment, G): pair prefix sums, (level<<16|group), level offsets
+  // claim order per (segment, G)
   struct Seg {
     int l0, l1;
-    TaskDesc *d_tasks = nullptr;   // task descriptors in diagonal claim order
+    TaskDesc *d_tasks = nullptr;   // task descriptors in claim order
     int64_t ntasks = 0;
   };
   std::vector<Seg> segs;
@@ -356,8 +358,9 @@ static void free_segments(hy_handle *h) {
   h->segs_G = -1;
 }
 
-// Per hub-free level segment, the flat (node, group) task list in diagonal order:
-// group g at level l is listed with group g+1 at level l-1.
+// Per hub-free level segment, the flat (node, group pair) task list in claim order
+// (pipe_order: level-major by default; the diagonal lists pair g at level l with pair g+1
+// at level l-1).  Any order that lists a pair's levels ascending is deadlock-free.
 static int build_segments(hy_handle *h, int G) {
   auto hit = h->seg_cache.find(G);
   if (hit != h->seg_cache.end()) {
@@ -596,6 +599,10 @@ int hy_set_option(hy_handle *h, const char *name, int64_t value) {
   }
   if (std::string(name) == "pipe_blocks" && value >= 0) {   // 0: occupancy-derived (default)
     h->pipe_blocks = (int)value;
+    return HY_OK;
+  }
+  if (std::string(name) == "bwd_narrow" && value >= 0) {
+    h->bwd_narrow = value;
     return HY_OK;
   }
   if (std::string(name) == "pipe_order" && value >= 0) {
@@ -1716,7 +1723,7 @@ int hy_refactorize_batched(hy_handle *h, int64_t B, const double *d_vals, double
     h->pipe_blocks = per_sm * sms;
   }
   // segments: maximal level runs without hub nodes -> one persistent launch each
-  // (diagonal claim order); hub levels -> one CTA per (hub node, group), then the
+  // (claim order: build_segments); hub levels -> one CTA per (hub node, group), then the
   // level's non-hub nodes
   if (h->segs_G != G) {
     int rc2 = build_segments(h, G);
@@ -1778,7 +1785,9 @@ int hy_solve_batched(hy_handle *h, int64_t B, const double *d_b, double *d_x, ui
     const int c = (int)(bp.aptr[l + 1] - bp.aptr[l]);
     const int GP = (G + 1) / 2;
     const int64_t tasks = (int64_t)c * GP;
-    CK(launchx(k_batch_bwd2, dim3((unsigned)((tasks + 3) / 4)), dim3(128), 0, st, h->use_pdl, h->S,
+    // narrow levels are latency chains (wider load batches), wide levels throughput-bound
+    CK(launchx(tasks <= h->bwd_narrow ? k_batch_bwd2<BWD_WL> : k_batch_bwd2<BWD_W>,
+               dim3((unsigned)((tasks + 3) / 4)), dim3(128), 0, st, h->use_pdl, h->S,
                (const double *)h->d_bf, h->stored, (const int32_t *)(bp.d_all + bp.aptr[l]), c, GP, h->d_by));
     h->launches++;
   }

@@ -16,9 +16,7 @@
 namespace hy {
 
 constexpr int BW = 4;
-#ifndef BWD_W
-#define BWD_W 2     // backward-solve entries per batch (k_batch_bwd2; 2-8 measured)
-#endif            // warps per block (bwd / fwd kernels)
+// warps per block (bwd / fwd kernels); BWD_W / BWD_WL (hylu_common.cuh): backward-solve entries per batch
 #ifndef HUB_THREADS_DEF
 #define HUB_THREADS_DEF 768   // 512: 17.56 ms/step, 768: 17.41, 1024: 17.43 (c4, round 2)
 #endif
@@ -931,6 +929,7 @@ __global__ void __launch_bounds__(BW * 32) k_batch_fwd(DevSym S, const double *B
 
 // Pair mode backward substitution: one warp per (node, group pair); the padded
 // allocation makes the odd tail group's partner valid memory (never copied out).
+template <int BWDW>
 __global__ void __launch_bounds__(BW * 32) k_batch_bwd2(DevSym S, const double *BF, int64_t stored,
                                                         const int32_t *nodes, int count, int GP,
                                                         double *Y) {
@@ -956,13 +955,13 @@ __global__ void __launch_bounds__(BW * 32) k_batch_bwd2(DevSym S, const double *
     const int d = L + t;
     double accA = ya[(int64_t)(r + t) * 32], accC = yc[(int64_t)(r + t) * 32];
     const double dA = ga[ro + (int64_t)d * 32], dC = gc[ro + (int64_t)d * 32];
-    for (int p0 = d + 1; p0 < W; p0 += BWD_W) {
-      int k[BWD_W];
-      double a[BWD_W], c[BWD_W], za[BWD_W], zc[BWD_W];
+    for (int p0 = d + 1; p0 < W; p0 += BWDW) {
+      int k[BWDW];
+      double a[BWDW], c[BWDW], za[BWDW], zc[BWDW];
 #pragma unroll
-      for (int e = 0; e < BWD_W; ++e) k[e] = p0 + e < W ? __ldg(cc + p0 + e) : -1;
+      for (int e = 0; e < BWDW; ++e) k[e] = p0 + e < W ? __ldg(cc + p0 + e) : -1;
 #pragma unroll
-      for (int e = 0; e < BWD_W; ++e) {
+      for (int e = 0; e < BWDW; ++e) {
         const bool ok = k[e] >= 0;
         a[e] = ok ? ga[ro + (int64_t)(p0 + e) * 32] : 0.0;
         c[e] = ok ? gc[ro + (int64_t)(p0 + e) * 32] : 0.0;
@@ -970,7 +969,7 @@ __global__ void __launch_bounds__(BW * 32) k_batch_bwd2(DevSym S, const double *
         zc[e] = ok ? yc[(int64_t)k[e] * 32] : 0.0;
       }
 #pragma unroll
-      for (int e = 0; e < BWD_W; ++e) {
+      for (int e = 0; e < BWDW; ++e) {
         accA -= a[e] * za[e];
         accC -= c[e] * zc[e];
       }
@@ -979,6 +978,11 @@ __global__ void __launch_bounds__(BW * 32) k_batch_bwd2(DevSym S, const double *
     yc[(int64_t)(r + t) * 32] = accC / dC;
   }
 }
+
+// entries per batch: BWD_W (2) for the wide levels (throughput-bound, occupancy matters) and
+// BWD_WL for the narrow top levels, where a row's batches are a dependent chain of round trips
+template __global__ void k_batch_bwd2<BWD_W>(DevSym, const double *, int64_t, const int32_t *, int, int, double *);
+template __global__ void k_batch_bwd2<BWD_WL>(DevSym, const double *, int64_t, const int32_t *, int, int, double *);
 
 // de-interleave one instance's factor values into node layout
 __global__ void k_batch_extract(const double *BF, int64_t stored, int64_t b, double *out) {

@@ -91,6 +91,18 @@ struct __align__(16) StepRec {
   int16_t rl;     // offset of the step's target positions in the task's rel window
 };
 
+// Batched backward solve (k_batch_bwd2): entries per load batch on wide levels (throughput-bound:
+// 2-8 measured, 2 best) and on narrow levels, where a row's batches are a dependent chain
+#ifndef BWD_W
+#define BWD_W 2
+#endif
+#ifndef BWD_WL
+#define BWD_WL 8
+#endif
+#ifndef BWD_NARROW
+#define BWD_NARROW 4096   // (node, group pair) tasks per level up to which BWD_WL is used
+#endif
+
 #ifndef PIPE_REC_CAP
 #define PIPE_REC_CAP 160   // steps of a task's program window staged in shared memory
 #endif
