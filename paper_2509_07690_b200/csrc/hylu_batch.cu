@@ -438,6 +438,7 @@ size_t pipe_smem(int ws) { return (size_t)PIPE_WARPS * (2 * ws * 32 * 8 + PIPE_S
 // Debug build only (-DHYLU_TRACE, scripts/pipe_trace.py): per task {claim, ready, end}
 // global timestamps and (node, group, SM id), written through hy_debug_pipe_trace's buffer.
 __device__ unsigned long long *g_pipe_trace = nullptr;
+__device__ unsigned long long *g_hub_trace = nullptr;   // [0] record counter, then 8 words per hub CTA
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -557,6 +558,9 @@ __global__ void __launch_bounds__(PIPE_WARPS * 32, PIPE_MINB_DEF)
 extern "C" int hy_debug_pipe_trace(unsigned long long *d_buf) {
   return (int)cudaMemcpyToSymbol(g_pipe_trace, &d_buf, sizeof(d_buf));
 }
+extern "C" int hy_debug_hub_trace(unsigned long long *d_buf) {
+  return (int)cudaMemcpyToSymbol(g_hub_trace, &d_buf, sizeof(d_buf));
+}
 #endif
 
 // ---------------------------------------------------------------------------
@@ -607,24 +611,48 @@ __global__ void __launch_bounds__(HUB_THREADS, 1) k_bt_hub(DevSym S, BatchP P, D
   const double *Ab = P.A + (int64_t)g * 32 * S.nnz;
   double *scr = scratch + (size_t)blockIdx.x * max_slots * 32 + lane;
   const int hr0 = R.hub_base[u];
+#ifdef HYLU_TRACE
+  const long long h0 = clock64();
+  long long hlev = 0, hfwd = 0;
+#endif
   // initialise every row of the node first: a (joint) node program may span rows
   for (int t = 0; t < s; ++t) {
     const int i = r + t;
     double *w0 = gb0 + (S.valoff[u] + (int64_t)t * W) * 32;
-    for (int q = threadIdx.x; q < W * 32; q += HUB_THREADS) w0[q] = 0.0;
+    for (int q = threadIdx.x; q < W * 16; q += HUB_THREADS)   // 16-byte stores (rows are 256-byte aligned)
+      reinterpret_cast<double2 *>(w0)[q] = make_double2(0.0, 0.0);
     __syncthreads();
     const int srow = S.kind[u] ? r + P.iperm[i] : r;
     const int64_t a = S.mrow_src[srow];
     const int64_t e0 = S.a_ptr[a];
     const int k = (int)(S.a_ptr[a + 1] - e0);
     // lane = instance, warps stride the entries: coalesced 256-byte stores
+    // (4 consecutive entries per warp and iteration, loads before stores: one round trip
+    // per 4 entries, and a lane's 4 values share one 32-byte sector)
     if (live)
-      for (int e = warp; e < k; e += nw)
-        w0[S.colpos[e0 + e] * 32 + lane] = Ab[(int64_t)lane * S.nnz + e0 + e] * S.scale[e0 + e];
+      for (int e = warp * 4; e < k; e += nw * 4) {
+        int cp[4];
+        double v[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          const bool ok = e + m < k;
+          cp[m] = ok ? __ldg(S.colpos + e0 + e + m) : 0;
+          v[m] = ok ? __ldg(Ab + (int64_t)lane * S.nnz + e0 + e + m) * __ldg(S.scale + e0 + e + m) : 0.0;
+        }
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+          if (e + m < k) w0[cp[m] * 32 + lane] = v[m];
+      }
   }
   __syncthreads();
+#ifdef HYLU_TRACE
+  const long long h1 = clock64();
+#endif
   for (int t = 0; t < s; ++t) {
     const int i = r + t;
+#ifdef HYLU_TRACE
+    const long long r0c = clock64();
+#endif
     // positions are node-relative (t*W + p): every row's levels address the node base
     double *w = gb0 + S.valoff[u] * 32 + lane;
     double *w0 = gb0 + (S.valoff[u] + (int64_t)t * W) * 32;
@@ -798,6 +826,10 @@ __global__ void __launch_bounds__(HUB_THREADS, 1) k_bt_hub(DevSym S, BatchP P, D
       __syncthreads();
     }
     cp_async_wait_all0();
+#ifdef HYLU_TRACE
+    const long long r1c = clock64();
+    hlev += r1c - r0c;
+#endif
     // forward substitution for row i: y_i = b̂_i − Σ_s l_s y_{j_s}
     double part = 0.0;
     for (int64_t st = R.row_ptr[i] + warp; st < R.row_ptr[i + 1]; st += nw)
@@ -811,7 +843,17 @@ __global__ void __launch_bounds__(HUB_THREADS, 1) k_bt_hub(DevSym S, BatchP P, D
       if (PIPE_RINV) P.RI[((int64_t)g * S.n + i) * 32 + lane] = 1.0 / w0[(int64_t)(S.nl[u] + t) * 32 + lane];
     }
     __syncthreads();
+#ifdef HYLU_TRACE
+    hfwd += clock64() - r1c;
+#endif
   }
+#ifdef HYLU_TRACE
+  if (g_hub_trace && threadIdx.x == 0) {
+    const unsigned long long k = atomicAdd(g_hub_trace, 1ull);
+    unsigned long long *q = g_hub_trace + 1 + 8 * k;
+    q[0] = u; q[1] = g; q[2] = clock64() - h0; q[3] = h1 - h0; q[4] = hlev; q[5] = hfwd; q[6] = gtime(); q[7] = smid();
+  }
+#endif
   if (flags && threadIdx.x == 0) {
     __threadfence();
     st_release(flags + (int64_t)u * G + g, epoch);

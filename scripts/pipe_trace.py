@@ -33,12 +33,23 @@ torch.cuda.synchronize()
 lib = device.library()
 nt = s.nnodes * ((B + 63) // 64)
 buf = torch.zeros(nt * 12, dtype=torch.int64, device="cuda")
+hbuf = torch.zeros(1 + 8 * 4096, dtype=torch.int64, device="cuda")
+lib.hy_debug_hub_trace.argtypes = [ctypes.c_void_p]
+lib.hy_debug_hub_trace(ctypes.c_void_p(hbuf.data_ptr()))
 lib.hy_debug_pipe_trace.argtypes = [ctypes.c_void_p]
 rc = lib.hy_debug_pipe_trace(ctypes.c_void_p(buf.data_ptr()))
 assert rc == 0, rc
 x, npert = br.run(dv, dr, refine=False)
 torch.cuda.synchronize()
 lib.hy_debug_pipe_trace(ctypes.c_void_p(0))
+lib.hy_debug_hub_trace(ctypes.c_void_p(0))
+hb = hbuf.cpu().numpy()
+hrec = hb[1:1 + 8 * int(hb[0])].reshape(-1, 8)
+for hu in np.unique(hrec[:, 0]):
+    hm = hrec[:, 0] == hu
+    c = hrec[hm][:, 2:6].astype(np.float64) / 1.965e3   # us at 1965 MHz
+    print("hub node %d: %d CTAs  total %.0f us (max %.0f)  init %.0f  levels %.0f  fwd %.0f" % (
+        hu, hm.sum(), c[:, 0].mean(), c[:, 0].max(), c[:, 1].mean(), c[:, 2].mean(), c[:, 3].mean()))
 t = buf.cpu().numpy().reshape(-1, 12)
 t = t[t[:, 0] != 0]
 claim, ready, end, tag = t[:, 0], t[:, 1], t[:, 2], t[:, 3]
