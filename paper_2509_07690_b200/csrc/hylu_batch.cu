@@ -592,6 +592,7 @@ __global__ void __launch_bounds__(HUB_THREADS, 1) k_bt_hub(DevSym S, BatchP P, D
   constexpr int LVCAP = 512;
   __shared__ int64_t s_wi[LVCAP + 1], s_sp[LVCAP + 1], s_y[LVCAP + 1];
   __shared__ int s_bt[LVCAP + 1];
+  __shared__ int s_next;   // next unclaimed work item of the current level
   // per-level staging of work-item metadata and predecessor lists, double-buffered:
   // level l+1's records are copied (cp.async) while level l is processed
   extern __shared__ __align__(16) unsigned char hub_dyn[];
@@ -715,6 +716,7 @@ __global__ void __launch_bounds__(HUB_THREADS, 1) k_bt_hub(DevSym S, BatchP P, D
       if (lev + 1 < lv1 && stageable(q + 1)) issue(q + 1);
       cp_async_commit();
       cp_async_wait1();
+      if (threadIdx.x == 0) s_next = 0;   // every warp left the previous level's loop at its last barrier
       __syncthreads();
       const int64_t wi0 = lsm ? s_wi[q] : R.lev_wi[lev];
       const int64_t wi1 = lsm ? s_wi[q + 1] : R.lev_wi[lev + 1];
@@ -728,13 +730,18 @@ __global__ void __launch_bounds__(HUB_THREADS, 1) k_bt_hub(DevSym S, BatchP P, D
         const int64_t yb0 = s_y[q];
         // HUB_I items per warp at a time, HUB_P predecessors per item per round:
         // HUB_I x HUB_P x 2 independent gathers in flight per warp
-        for (int64_t q0 = warp; q0 < ni; q0 += HUB_I * nw) {
+        // warps claim the level's items one by one (the host lists them longest first)
+        for (;;) {
+          int64_t q0 = 0;
+          if (lane == 0) q0 = atomicAdd(&s_next, HUB_I);
+          q0 = __shfl_sync(HY_FULL, q0, 0);
+          if (q0 >= ni) break;
           int p[HUB_I], y[HUB_I], y1[HUB_I], slot[HUB_I];
           int64_t kd[HUB_I];
           double acc[HUB_I], dv[HUB_I];
 #pragma unroll
           for (int jq = 0; jq < HUB_I; ++jq) {
-            const int64_t qq = q0 + (int64_t)jq * nw;
+            const int64_t qq = q0 + jq;
             const bool ok = qq < ni;
             p[jq] = ok ? st_p[qq] : 0;
             slot[jq] = ok ? st_sl[qq] : 0;
@@ -765,7 +772,7 @@ __global__ void __launch_bounds__(HUB_THREADS, 1) k_bt_hub(DevSym S, BatchP P, D
           }
 #pragma unroll
           for (int jq = 0; jq < HUB_I; ++jq) {
-            const int64_t qq = q0 + (int64_t)jq * nw;
+            const int64_t qq = q0 + jq;
             if (qq >= ni) continue;
             double a = acc[jq];
             if (slot[jq] < 0) {

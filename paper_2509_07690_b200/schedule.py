@@ -287,6 +287,28 @@ def _chunks(hrow_lev, lev_ptr, hpp, ch):
     return lev_wi, wi_x, wi_y0, wi_y1, wi_slot, lev_sp, sp_x, sp_s0, sp_n, max_slots
 
 
+HUB_LPT = os.environ.get("HYLU_HUB_LPT", "1") != "0"   # probe switch: work items in generation order
+
+
+def _balance_items(hrow_lev, lev_wi, wi_x, wi_y0, wi_y1, wi_slot):
+    """Work items of an intra-row level in longest-first order (by gather rounds of 8 terms):
+    the hub kernel's warps claim a level's items one by one, so the order is its schedule
+    (longest-processing-time first).  The item holding a level's lowest pred offset stays
+    first and, in the last level of a hub row, the one holding the highest stays last: the
+    kernel takes a level's pred range from them.  Items are independent within a level (split
+    positions combine by slot), so the order changes no result."""
+    last_levels = set(int(v) - 1 for v in hrow_lev[1:])
+    perm = np.arange(len(wi_x))
+    for lev in range(len(lev_wi) - 1):
+        a, b = int(lev_wi[lev]), int(lev_wi[lev + 1])
+        hi = b - 1 if lev in last_levels else b
+        if hi - (a + 1) < 2:
+            continue
+        rounds = (wi_y1[a + 1:hi] - wi_y0[a + 1:hi] + 7) // 8
+        perm[a + 1:hi] = a + 1 + np.argsort(-rounds, kind="stable")
+    return wi_x[perm], wi_y0[perm], wi_y1[perm], wi_slot[perm]
+
+
 JOINT_HUB_ROWS = os.environ.get("HYLU_JOINT_HUB", "1") != "0"
 
 
@@ -424,6 +446,8 @@ def build_programs(an, inner_perm, hub_steps=HUB_STEPS, chunk=HUB_CHUNK, standal
         pred_u = np.zeros(0, np.int64)
     (lev_wi, wi_x, wi_y0, wi_y1, wi_slot, lev_sp, sp_x, sp_s0, sp_n,
      max_slots) = _chunks(hrow_lev, lev_ptr, hpp, chunk)
+    if HUB_LPT:
+        wi_x, wi_y0, wi_y1, wi_slot = _balance_items(hrow_lev, lev_wi, wi_x, wi_y0, wi_y1, wi_slot)
     W = np.diff(s.colptr)
     rows = np.diff(s.node_first)
     ndeps = np.diff(s.dep_ptr)
