@@ -26,7 +26,7 @@ int hub_threads() { return HUB_THREADS; }
 #define HUB_I 1     // work items per warp per round (staged hub levels; 1-8 measured, 1 best)
 #endif
 #ifndef HUB_P
-#define HUB_P 8     // predecessors per item per round
+#define HUB_P 12    // predecessors per item per round (c4 ms/step with longest-first items: 8: 14.33, 10: 14.79, 12: 14.23, 14: 14.33, 16: 14.45)
 #endif
 constexpr int HUB_CAPI = 1024;   // staged work items per level (per buffer)
 constexpr int HUB_CAPP = 4096;   // staged predecessor records per level (per buffer)
