@@ -592,7 +592,7 @@ __global__ void __launch_bounds__(HUB_THREADS, 1) k_bt_hub(DevSym S, BatchP P, D
   constexpr int LVCAP = 512;
   __shared__ int64_t s_wi[LVCAP + 1], s_sp[LVCAP + 1], s_y[LVCAP + 1];
   __shared__ int s_bt[LVCAP + 1];
-  __shared__ int s_next;   // next unclaimed work item of the current level
+  __shared__ int s_next[2];   // next unclaimed work item of the current / the next level
   // per-level staging of work-item metadata and predecessor lists, double-buffered:
   // level l+1's records are copied (cp.async) while level l is processed
   extern __shared__ __align__(16) unsigned char hub_dyn[];
@@ -708,16 +708,19 @@ __global__ void __launch_bounds__(HUB_THREADS, 1) k_bt_hub(DevSym S, BatchP P, D
         cp_async8(reinterpret_cast<double *>(pu + k2), reinterpret_cast<const double *>(R.pred_u + yb0 + k2));
       }
     };
-    const int qdf = 0;
-    if (qdf < nlv && stageable(qdf)) issue(qdf);
-    cp_async_commit();
-    for (int64_t lev = lv0 + qdf; lev < lv1; ++lev) {
+    // One barrier per level: level q+1's records are issued at the top of level q and
+    // awaited just before the barrier that ends level q, which so also publishes them
+    // (the claim counters alternate, so the next level's is reset a level ahead).
+    if (nlv > 0 && stageable(0)) issue(0);
+    cp_async_wait_all();
+    if (threadIdx.x == 0) s_next[0] = 0;
+    __syncthreads();
+    for (int64_t lev = lv0; lev < lv1; ++lev) {
       const int q = (int)(lev - lv0);
       if (lev + 1 < lv1 && stageable(q + 1)) issue(q + 1);
       cp_async_commit();
-      cp_async_wait1();
-      if (threadIdx.x == 0) s_next = 0;   // every warp left the previous level's loop at its last barrier
-      __syncthreads();
+      if (threadIdx.x == 0) s_next[(q + 1) & 1] = 0;
+      int *const nxt = &s_next[q & 1];
       const int64_t wi0 = lsm ? s_wi[q] : R.lev_wi[lev];
       const int64_t wi1 = lsm ? s_wi[q + 1] : R.lev_wi[lev + 1];
       const int64_t sp0 = lsm ? s_sp[q] : R.lev_sp[lev];
@@ -733,7 +736,7 @@ __global__ void __launch_bounds__(HUB_THREADS, 1) k_bt_hub(DevSym S, BatchP P, D
         // warps claim the level's items one by one (the host lists them longest first)
         for (;;) {
           int64_t q0 = 0;
-          if (lane == 0) q0 = atomicAdd(&s_next, HUB_I);
+          if (lane == 0) q0 = atomicAdd(nxt, HUB_I);
           q0 = __shfl_sync(HY_FULL, q0, 0);
           if (q0 >= ni) break;
           int p[HUB_I], y[HUB_I], y1[HUB_I], slot[HUB_I];
@@ -830,9 +833,9 @@ __global__ void __launch_bounds__(HUB_THREADS, 1) k_bt_hub(DevSym S, BatchP P, D
           hub_finalize(P, R.sp_kd[k2], p, acc, w, gb, thr, live, b);
         }
       }
+      cp_async_wait_all0();
       __syncthreads();
     }
-    cp_async_wait_all0();
 #ifdef HYLU_TRACE
     const long long r1c = clock64();
     hlev += r1c - r0c;
