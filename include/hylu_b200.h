@@ -296,6 +296,10 @@ int hy_batched_factor_values(hy_handle *h, int64_t b, double *d_out, uintptr_t s
  *   "fanin_warp_min" items below which a level keeps its small items on the CTA kernels
  *   "fanin_maps"    0/1 (default 1): host-precomputed source maps in the update kernels
  *   "pipe_ws", "pipe_blocks": batched-pipeline shared workspace / resident CTAs
+ *   "lu1_kernel"    0/1 (default 1): single-row nodes of a fan-in level perturb their pivot in a
+ *                   thread-per-node kernel (k_fi_lu1) instead of a CTA each
+ *   "bwd_narrow"    batched backward solve: levels with at most this many (node, group pair) tasks
+ *                   use 8-entry load batches (default 4096)
  *   "pipe_order"    claim order of the batched pipeline's (node, group pair) tasks: 1 (default)
  *                   level-major (every pair at level k, then level k+1), 0 diagonal (pair g at
  *                   level k with pair g+1 at level k-1), K >= 2 diagonal below level K-1 and

@@ -4,6 +4,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <algorithm>
 #include <map>
 #include <vector>
 
@@ -89,6 +90,7 @@ __global__ void k_msolve_sn(DevSym, const double *, const int32_t *, int, double
 __global__ void k_mxout(DevSym, const double *, double *, int);
 
 __global__ void k_fi_lu(DevSym, const CallP *, FaninDev, int);
+__global__ void k_fi_lu1(DevSym, const CallP *, FaninDev, int, int);
 __global__ void k_fi_panel(DevSym, const CallP *, FaninDev, int);
 __global__ void k_fi_x(DevSym, const CallP *, FaninDev, int);
 __global__ void k_fi_upd(DevSym, const CallP *, FaninDev, int, int, int);
@@ -209,6 +211,7 @@ struct hy_handle {
   int pipe_blocks = 0;
   int warp_min = 256;                      // fan-in: below this many small items per level, CTA kernels only
   int64_t bwd_narrow = BWD_NARROW;         // batched backward solve: levels with at most this many tasks use BWD_WL-entry batches
+  int lu1_kernel = 1;                      // fan-in: single-row nodes' pivot perturbation as a thread-per-node kernel
   int pipe_order = 1;                      // claim order of the batched pipeline: 1 level-major (default), 0 diagonal, K >= 2 diagonal below level K-1 (build_segments)
   int pipe_ws = 6;                         // pair-mode shared workspace columns per group (c4 ms/step: 4: 15.50, 6: 15.48, 8: 15.64, 10: 15.64, 16: 16.65 before the reciprocals)
   // claim order per (segment, G)
@@ -240,6 +243,7 @@ struct hy_handle {
   FaninDev fi{};
   std::vector<void *> fi_allocs;
   std::vector<int64_t> fi_lu, fi_pt, fi_xp, fi_up;   // per-level offsets
+  std::vector<int64_t> fi_lu1;                       // per level: single-row nodes at the head of its LU list
   std::vector<int64_t> fi_upbig;                     // per level: first DMMA-routed item
   std::vector<int64_t> fi_upreg;                     // per level: first per-source item
   std::vector<int64_t> fi_uprs;                      // per level: first CTA-per-item regular item
@@ -605,6 +609,10 @@ int hy_set_option(hy_handle *h, const char *name, int64_t value) {
     h->bwd_narrow = value;
     return HY_OK;
   }
+  if (std::string(name) == "lu1_kernel" && (value == 0 || value == 1)) {
+    h->lu1_kernel = (int)value;
+    return HY_OK;
+  }
   if (std::string(name) == "pipe_order" && value >= 0) {
     h->pipe_order = (int)value;
     free_segments(h);
@@ -806,7 +814,16 @@ int hy_upload_fanin_plan(hy_handle *h, const hy_fanin_plan *d) {
   D.up_mask = nullptr;
   int32_t *p32;
   int64_t *p64;
-  UPF(&p32, d->lu_nodes, d->lu_ptr[nl]); D.lu_nodes = p32;
+  {   // per level: single-row nodes first (thread per node, k_fi_lu1), then the supernodes (CTA each)
+    std::vector<int32_t> lun(d->lu_nodes, d->lu_nodes + d->lu_ptr[nl]);
+    h->fi_lu1.assign(nl, 0);
+    for (int64_t l = 0; l < nl; ++l) {
+      auto b = lun.begin() + d->lu_ptr[l], e = lun.begin() + d->lu_ptr[l + 1];
+      auto mid = std::stable_partition(b, e, [&](int32_t u) { return h->h_first[u + 1] - h->h_first[u] == 1; });
+      h->fi_lu1[l] = (int64_t)(mid - b);
+    }
+    UPF(&p32, lun.data(), d->lu_ptr[nl]); D.lu_nodes = p32;
+  }
   UPF(&p32, d->pt_node, d->pt_ptr[nl]); D.pt_node = p32;
   UPF(&p32, d->pt_c0, d->pt_ptr[nl]); D.pt_c0 = p32;
   UPF(&p32, d->pt_c1, d->pt_ptr[nl]); D.pt_c1 = p32;
@@ -925,8 +942,15 @@ static int run_fanin(hy_handle *h, const CallP *Pd, cudaStream_t st) {
                                    h->hub1_slots);
       h->launches++;
     }
-    if (nlu) {
-      CK(launchx(k_fi_lu, dim3(nlu), dim3(256), fi_lu_smem(), st, pdl, h->S, Pd, h->fi, (int)h->fi_lu[l]));
+    // single-row nodes: one thread each (their "LU" is the pivot perturbation); supernodes: a CTA each
+    const int nlu1 = h->lu1_kernel ? (int)h->fi_lu1[l] : 0;
+    if (nlu1) {
+      CK(launchx(k_fi_lu1, dim3((nlu1 + 255) / 256), dim3(256), 0, st, pdl, h->S, Pd, h->fi, (int)h->fi_lu[l], nlu1));
+      h->launches++;
+    }
+    if (nlu - nlu1) {
+      CK(launchx(k_fi_lu, dim3(nlu - nlu1), dim3(256), fi_lu_smem(), st, pdl, h->S, Pd, h->fi,
+                 (int)h->fi_lu[l] + nlu1));
       h->launches++;
     }
     // the panel TRSM of the level's nodes and the X blocks of their edges both need

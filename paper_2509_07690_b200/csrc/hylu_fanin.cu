@@ -184,6 +184,27 @@ __device__ __forceinline__ void d_fi_lu(DevSym S, const CallP *__restrict__ Pd, 
 }
 __global__ void __launch_bounds__(FI_THREADS) k_fi_lu(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base) { d_fi_lu(S, Pd, D, base, blockIdx.x); }
 
+// Single-row nodes of a level: their "LU" is the pivot perturbation (SPEC.md:320-328 with
+// s = 1), one thread per node instead of a CTA each (c1's first levels list 10^4-10^5 of them).
+__global__ void __launch_bounds__(256) k_fi_lu1(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base,
+                                                int count) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= count) return;
+  const CallP P = *Pd;
+  const int u = D.lu_nodes[base + k];
+  const int r = (int)S.first[u];
+  double *Pm = P.F + S.valoff[u];
+  const int L = S.nl[u];
+  const double thr = P.eps * P.anorm[0];
+  const double piv = Pm[L];
+  bool fired;
+  Pm[L] = perturb(piv, thr, fired);
+  log_pivot(P, r, piv, fired, thr);
+  P.iperm[r] = 0;
+}
+
 // ---------------------------------------------------------------------------- panel
 // Tile of node v's columns [c0, c1) outside the block: apply the pivot row
 // permutation (factorize only) and, for panel tiles, the unit-lower TRSM.

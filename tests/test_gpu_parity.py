@@ -697,8 +697,8 @@ def test_solve_multi_small_segments_and_refinement():
 @pytest.mark.parametrize("name", ["c1", "c2"])
 def test_launch_options_do_not_change_results(name):
     """Launch-level options are scheduling only: factors and solutions are bitwise
-    equal with programmatic dependent launch, CUDA graphs and the two-stream phase
-    overlap switched off; the batched path likewise for PDL, the pair-workspace
+    equal with programmatic dependent launch, CUDA graphs, the two-stream phase
+    overlap and the thread-per-node kernel for single-row nodes switched off; the batched path likewise for PDL, the pair-workspace
     width and the pipeline's claim order (diagonal / level-major)."""
     import torch
     p, an = _analysis(name)
@@ -707,14 +707,14 @@ def test_launch_options_do_not_change_results(name):
     b = torch.from_numpy(np.asarray(p.b, np.float64)).cuda()
     x = api.substitute(f, b)
     try:
-        for opt in ("pdl", "graphs", "fanin_overlap"):
+        for opt in ("pdl", "graphs", "fanin_overlap", "lu1_kernel"):
             ctx.set_option(opt, 0)
             g = api.factorize_analysis(an)
             assert torch.equal(g.values, f.values), opt
             assert torch.equal(api.substitute(g, b), x), opt
             ctx.set_option(opt, 1)
     finally:
-        for opt in ("pdl", "graphs", "fanin_overlap"):
+        for opt in ("pdl", "graphs", "fanin_overlap", "lu1_kernel"):
             ctx.set_option(opt, 1)
     if name == "c1":
         bp = gen.circuit_batch(70, 2000, 2, 200)
