@@ -65,9 +65,11 @@ struct FaninDev {
   const int32_t *src_m;
   const ItemRec *up_rec;     // [items] packed prologue records (k_item_rec)
   const uint64_t *up_mask;   // [items] tile columns any source touches (k_item_mask; needs the maps)
+  const XRec *xp_rec;        // [X items] packed records (k_x_rec)
 };
 __global__ void k_fi_scatter(DevSym, const CallP *);
 __global__ void k_item_rec(DevSym, FaninDev, int64_t, ItemRec *);
+__global__ void k_x_rec(DevSym, FaninDev, int64_t, XRec *);
 __global__ void k_item_mask(FaninDev, int64_t, uint64_t *);
 size_t fi_lu_smem();
 size_t fi_panel_smem();
@@ -852,6 +854,18 @@ int hy_upload_fanin_plan(hy_handle *h, const hy_fanin_plan *d) {
       CK(cudaDeviceSynchronize());
     }
     D.up_rec = rec;
+  }
+  {   // packed records of the multiplier-block (X) items
+    const int64_t nx = d->xp_ptr[nl];
+    XRec *xr = nullptr;
+    CK(cudaMalloc((void **)&xr, sizeof(XRec) * (nx > 0 ? nx : 1)));
+    h->fi_allocs.push_back(xr);
+    if (nx > 0) {
+      k_x_rec<<<(unsigned)std::min<int64_t>((nx + 255) / 256, 4096), 256>>>(h->S, D, nx, xr);
+      CK(cudaGetLastError());
+      CK(cudaDeviceSynchronize());
+    }
+    D.xp_rec = xr;
   }
   h->fi_lu.assign(d->lu_ptr, d->lu_ptr + nl + 1);
   h->fi_pt.assign(d->pt_ptr, d->pt_ptr + nl + 1);

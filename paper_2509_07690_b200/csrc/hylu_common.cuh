@@ -38,6 +38,16 @@ struct DevSym {
 // Fan-in update item (target node, 64-column tile) in one 32-byte record, built on
 // the device at plan upload (k_item_rec): the update kernels get everything their
 // prologue needs from one load instead of two dependent rounds (item -> node).
+// Multiplier-block (X) item of the level fan-in, packed once per plan upload (k_x_rec): what
+// k_fi_x / k_fi_x_w otherwise chase through four dependent metadata rounds per item.
+struct __align__(16) XRec {
+  int64_t t_off;   // target block: valoff[T] + pb0 (first panel column of the source in T)
+  int64_t u_off;   // source triangle: valoff[v] + tb0 * vW + nl[v] + tb0 (row/column tb0 of v's block)
+  int32_t W, vW;   // row widths of target and source
+  int16_t s, m;    // target rows, source block rows from the first present one
+  int32_t pad;
+};
+
 struct __align__(16) ItemRec {
   int64_t valoff;   // target node's value offset
   int64_t zb;       // first source record

@@ -60,6 +60,7 @@ struct FaninDev {
   const int32_t *src_m;      // source block rows from the first present one
   const ItemRec *up_rec;     // [items] packed prologue records (k_item_rec)
   const uint64_t *up_mask;   // [items] tile columns any source touches (k_item_mask; needs the maps)
+  const XRec *xp_rec;        // [X items] packed records (k_x_rec)
 };
 
 constexpr int FI_THREADS = 256;
@@ -296,31 +297,18 @@ __device__ __forceinline__ void d_fi_x(DevSym S, const CallP *__restrict__ Pd, F
   extern __shared__ __align__(16) double xsm[];
   double *Ub = xsm;
   double *Xt = xsm + 64 * FXLD;
-  const int j = base + bid;
-  const int64_t dk = D.xp_edge[j];
-  const int T = D.xp_tgt[j];
-  const int v = S.deps[dk];
+  const XRec xr0 = D.xp_rec[base + bid];
   const int tid = threadIdx.x, lane = tid & 31;
-  const int r = (int)S.first[T];
-  const int s = (int)(S.first[T + 1] - r);
-  const int64_t tc0 = S.colptr[T];
-  const int W = (int)(S.colptr[T + 1] - tc0);
-  const int vf = (int)S.first[v];
-  const int vs = (int)(S.first[v + 1] - vf);
-  const int vW = (int)(S.colptr[v + 1] - S.colptr[v]);
-  const int vnl = S.nl[v];
-  const double *vb = P.F + S.valoff[v];
-  double *Pm = P.F + S.valoff[T];
-  const int pb0 = D.dep_pb[dk];
-  const int tb0 = S.cols[tc0 + pb0] - vf;
-  const int m = vs - tb0;
+  const int s = xr0.s, W = xr0.W, vW = xr0.vW, m = xr0.m;
+  const double *vb = P.F + xr0.u_off;   // row a of the source triangle at vb + a * vW, from column tb0
+  double *Pm = P.F + xr0.t_off;         // target block (rows t at Pm + t * W)
   // warp per row, lanes over columns (no index divisions); the diagonal's
   // reciprocals are formed once, so the sequential loop multiplies instead of
   // dividing (x_a = w_a * (1/U_aa): within one rounding of the division)
   const int warp = tid >> 5;
   __shared__ double rinv[64];
   for (int a = warp; a < m; a += FI_THREADS / 32) {
-    const double *urow = vb + (int64_t)(tb0 + a) * vW + vnl + tb0;
+    const double *urow = vb + (int64_t)a * vW;
     for (int b2 = lane; b2 < m; b2 += 32) {
       const double u = b2 >= a ? urow[b2] : 0.0;
       Ub[a * FXLD + b2] = u;
@@ -328,7 +316,7 @@ __device__ __forceinline__ void d_fi_x(DevSym S, const CallP *__restrict__ Pd, F
     }
   }
   for (int t = warp; t < s; t += FI_THREADS / 32) {
-    const double *xs = Pm + (int64_t)t * W + pb0;
+    const double *xs = Pm + (int64_t)t * W;
     for (int a = lane; a < m; a += 32) Xt[t * FXLD + a] = xs[a];
   }
   __syncthreads();
@@ -365,7 +353,7 @@ __device__ __forceinline__ void d_fi_x(DevSym S, const CallP *__restrict__ Pd, F
   }
   __syncthreads();
   for (int t = warp; t < s; t += FI_THREADS / 32) {
-    double *xd = Pm + (int64_t)t * W + pb0;
+    double *xd = Pm + (int64_t)t * W;
     for (int a = lane; a < m; a += 32) xd[a] = Xt[t * FXLD + a];
   }
 }
@@ -383,32 +371,19 @@ __device__ __forceinline__ void d_fi_x_w(DevSym S, const CallP *__restrict__ Pd,
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int jj = bid * (FI_THREADS / 32) + warp;
   if (jj >= count) return;
-  const int j = base + jj;
-  const int64_t dk = D.xp_edge[j];
-  const int T = D.xp_tgt[j];
-  const int v = S.deps[dk];
-  const int r = (int)S.first[T];
-  const int s = (int)(S.first[T + 1] - r);
-  const int64_t tc0 = S.colptr[T];
-  const int W = (int)(S.colptr[T + 1] - tc0);
-  const int vf = (int)S.first[v];
-  const int vs = (int)(S.first[v + 1] - vf);
-  const int vW = (int)(S.colptr[v + 1] - S.colptr[v]);
-  const int vnl = S.nl[v];
-  const double *ub = P.F + S.valoff[v] + (int64_t)0;
-  double *Pm = P.F + S.valoff[T];
-  const int pb0 = D.dep_pb[dk];
-  const int tb0 = S.cols[tc0 + pb0] - vf;
-  const int m = vs - tb0;
+  const XRec xr0 = D.xp_rec[base + jj];
+  const int s = xr0.s, W = xr0.W, vW = xr0.vW, m = xr0.m;
+  const double *ub = P.F + xr0.u_off;   // row a of the source triangle at ub + a * vW, from column tb0
+  double *Pm = P.F + xr0.t_off;
   if (lane >= s) return;
-  double *row = Pm + (int64_t)lane * W + pb0;
+  double *row = Pm + (int64_t)lane * W;
   double xr[XW_M];
 #pragma unroll
   for (int a = 0; a < XW_M; ++a) xr[a] = a < m ? row[a] : 0.0;
 #pragma unroll
   for (int a = 0; a < XW_M; ++a) {
     if (a < m) {
-      const double *ua = ub + (int64_t)(tb0 + a) * vW + vnl + tb0;
+      const double *ua = ub + (int64_t)a * vW;
       const double x = xr[a] / ua[a];
       xr[a] = x;
       if (x != 0.0)
@@ -1715,6 +1690,29 @@ __global__ void k_item_mask(FaninDev D, int64_t nitems, uint64_t *out) {
       for (int c = 0; c < nq; ++c) m |= 1ull << pz[c];
     }
     out[j] = m;
+  }
+}
+
+__global__ void k_x_rec(DevSym S, FaninDev D, int64_t nitems, XRec *out) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nitems;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t dk = D.xp_edge[j];
+    const int T = D.xp_tgt[j];
+    const int v = S.deps[dk];
+    const int64_t tc0 = S.colptr[T];
+    const int vf = (int)S.first[v];
+    const int vW = (int)(S.colptr[v + 1] - S.colptr[v]);
+    const int pb0 = D.dep_pb[dk];
+    const int tb0 = S.cols[tc0 + pb0] - vf;
+    XRec r;
+    r.t_off = S.valoff[T] + pb0;
+    r.u_off = S.valoff[v] + (int64_t)tb0 * vW + S.nl[v] + tb0;
+    r.W = (int32_t)(S.colptr[T + 1] - tc0);
+    r.vW = vW;
+    r.s = (int16_t)(S.first[T + 1] - S.first[T]);
+    r.m = (int16_t)((int)(S.first[v + 1] - vf) - tb0);
+    r.pad = 0;
+    out[j] = r;
   }
 }
 
