@@ -66,10 +66,13 @@ struct FaninDev {
   const ItemRec *up_rec;     // [items] packed prologue records (k_item_rec)
   const uint64_t *up_mask;   // [items] tile columns any source touches (k_item_mask; needs the maps)
   const XRec *xp_rec;        // [X items] packed records (k_x_rec)
+  const NodeItemRec *lu_rec; // [LU items] / [panel items] packed records (k_node_rec)
+  const NodeItemRec *pt_rec;
 };
 __global__ void k_fi_scatter(DevSym, const CallP *);
 __global__ void k_item_rec(DevSym, FaninDev, int64_t, ItemRec *);
 __global__ void k_x_rec(DevSym, FaninDev, int64_t, XRec *);
+__global__ void k_node_rec(DevSym, const int32_t *, const int32_t *, const int32_t *, int64_t, NodeItemRec *);
 __global__ void k_item_mask(FaninDev, int64_t, uint64_t *);
 size_t fi_lu_smem();
 size_t fi_panel_smem();
@@ -866,6 +869,22 @@ int hy_upload_fanin_plan(hy_handle *h, const hy_fanin_plan *d) {
       CK(cudaDeviceSynchronize());
     }
     D.xp_rec = xr;
+  }
+  {   // packed records of the LU and panel items
+    const int64_t nlu = d->lu_ptr[nl], npt = d->pt_ptr[nl];
+    NodeItemRec *lr = nullptr, *pr = nullptr;
+    CK(cudaMalloc((void **)&lr, sizeof(NodeItemRec) * (nlu > 0 ? nlu : 1)));
+    h->fi_allocs.push_back(lr);
+    CK(cudaMalloc((void **)&pr, sizeof(NodeItemRec) * (npt > 0 ? npt : 1)));
+    h->fi_allocs.push_back(pr);
+    if (nlu > 0)
+      k_node_rec<<<(unsigned)std::min<int64_t>((nlu + 255) / 256, 4096), 256>>>(h->S, D.lu_nodes, nullptr, nullptr, nlu, lr);
+    if (npt > 0)
+      k_node_rec<<<(unsigned)std::min<int64_t>((npt + 255) / 256, 4096), 256>>>(h->S, D.pt_node, D.pt_c0, D.pt_c1, npt, pr);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    D.lu_rec = lr;
+    D.pt_rec = pr;
   }
   h->fi_lu.assign(d->lu_ptr, d->lu_ptr + nl + 1);
   h->fi_pt.assign(d->pt_ptr, d->pt_ptr + nl + 1);

@@ -48,6 +48,14 @@ struct __align__(16) XRec {
   int32_t pad;
 };
 
+// LU / panel item of the level fan-in, packed once per plan upload (k_node_rec): the node's
+// layout (and the panel tile's columns) in one 32-byte load instead of a dependent round.
+struct __align__(16) NodeItemRec {
+  int64_t valoff;
+  int32_t r, s, W, L;
+  int32_t c0, c1;   // panel tile columns (LU items: unused)
+};
+
 struct __align__(16) ItemRec {
   int64_t valoff;   // target node's value offset
   int64_t zb;       // first source record

@@ -61,6 +61,8 @@ struct FaninDev {
   const ItemRec *up_rec;     // [items] packed prologue records (k_item_rec)
   const uint64_t *up_mask;   // [items] tile columns any source touches (k_item_mask; needs the maps)
   const XRec *xp_rec;        // [X items] packed records (k_x_rec)
+  const NodeItemRec *lu_rec; // [LU items] / [panel items] packed records (k_node_rec)
+  const NodeItemRec *pt_rec;
 };
 
 constexpr int FI_THREADS = 256;
@@ -102,13 +104,10 @@ __device__ __forceinline__ void d_fi_lu(DevSym S, const CallP *__restrict__ Pd, 
   extern __shared__ __align__(16) double lu_dyn[];
   double *B = lu_dyn;                  // [64 * FXLD] (dynamic: fi_lu_smem())
   __shared__ int perm[64];
-  const int u = D.lu_nodes[base + bid];
+  const NodeItemRec nr = D.lu_rec[base + bid];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int r = (int)S.first[u];
-  const int s = (int)(S.first[u + 1] - r);
-  const int W = (int)(S.colptr[u + 1] - S.colptr[u]);
-  const int L = S.nl[u];
-  double *Pm = P.F + S.valoff[u];
+  const int r = nr.r, s = nr.s, W = nr.W, L = nr.L;
+  double *Pm = P.F + nr.valoff;
   const double thr = P.eps * P.anorm[0];
   if (s == 1) {
     if (tid == 0) {
@@ -194,10 +193,10 @@ __global__ void __launch_bounds__(256) k_fi_lu1(DevSym S, const CallP *__restric
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= count) return;
   const CallP P = *Pd;
-  const int u = D.lu_nodes[base + k];
-  const int r = (int)S.first[u];
-  double *Pm = P.F + S.valoff[u];
-  const int L = S.nl[u];
+  const NodeItemRec nr = D.lu_rec[base + k];
+  const int r = nr.r;
+  double *Pm = P.F + nr.valoff;
+  const int L = nr.L;
   const double thr = P.eps * P.anorm[0];
   const double piv = Pm[L];
   bool fired;
@@ -244,16 +243,12 @@ __device__ __forceinline__ void d_fi_panel(DevSym S, const CallP *__restrict__ P
   double *Lb = tl + 64 * 256;                    // [64 * FXLD] after the tile (fi_panel_smem())
   __shared__ int perm[64];
   __shared__ int ident;
-  const int j = base + bid;
-  const int u = D.pt_node[j];
-  const int c0 = D.pt_c0[j], c1 = D.pt_c1[j];
+  const NodeItemRec nr = D.pt_rec[base + bid];
+  const int c0 = nr.c0, c1 = nr.c1;
   const int tw = c1 - c0;
   const int tid = threadIdx.x;
-  const int r = (int)S.first[u];
-  const int s = (int)(S.first[u + 1] - r);
-  const int W = (int)(S.colptr[u + 1] - S.colptr[u]);
-  const int L = S.nl[u];
-  double *Pm = P.F + S.valoff[u];
+  const int r = nr.r, s = nr.s, W = nr.W, L = nr.L;
+  double *Pm = P.F + nr.valoff;
   const bool panel = c0 >= L + s;
   if (tid == 0) ident = 1;
   __syncthreads();
@@ -1690,6 +1685,23 @@ __global__ void k_item_mask(FaninDev D, int64_t nitems, uint64_t *out) {
       for (int c = 0; c < nq; ++c) m |= 1ull << pz[c];
     }
     out[j] = m;
+  }
+}
+
+__global__ void k_node_rec(DevSym S, const int32_t *nodes, const int32_t *c0, const int32_t *c1, int64_t nitems,
+                           NodeItemRec *out) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nitems;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int u = nodes[j];
+    NodeItemRec r;
+    r.valoff = S.valoff[u];
+    r.r = (int32_t)S.first[u];
+    r.s = (int32_t)(S.first[u + 1] - S.first[u]);
+    r.W = (int32_t)(S.colptr[u + 1] - S.colptr[u]);
+    r.L = S.nl[u];
+    r.c0 = c0 ? c0[j] : 0;
+    r.c1 = c1 ? c1[j] : 0;
+    out[j] = r;
   }
 }
 
