@@ -216,6 +216,7 @@ struct hy_handle {
   int pipe_blocks = 0;
   int warp_min = 256;                      // fan-in: below this many small items per level, CTA kernels only
   int64_t bwd_narrow = BWD_NARROW;         // batched backward solve: levels with at most this many tasks use BWD_WL-entry batches
+  int64_t lu1_min = 256;                   // ... for levels with at least this many single-row nodes
   int lu1_kernel = 1;                      // fan-in: single-row nodes' pivot perturbation as a thread-per-node kernel
   int pipe_order = 1;                      // claim order of the batched pipeline: 1 level-major (default), 0 diagonal, K >= 2 diagonal below level K-1 (build_segments)
   int pipe_ws = 6;                         // pair-mode shared workspace columns per group (c4 ms/step: 4: 15.50, 6: 15.48, 8: 15.64, 10: 15.64, 16: 16.65 before the reciprocals)
@@ -614,6 +615,10 @@ int hy_set_option(hy_handle *h, const char *name, int64_t value) {
     h->bwd_narrow = value;
     return HY_OK;
   }
+  if (std::string(name) == "lu1_min" && value >= 1) {
+    h->lu1_min = value;
+    return HY_OK;
+  }
   if (std::string(name) == "lu1_kernel" && (value == 0 || value == 1)) {
     h->lu1_kernel = (int)value;
     return HY_OK;
@@ -976,7 +981,8 @@ static int run_fanin(hy_handle *h, const CallP *Pd, cudaStream_t st) {
       h->launches++;
     }
     // single-row nodes: one thread each (their "LU" is the pivot perturbation); supernodes: a CTA each
-    const int nlu1 = h->lu1_kernel ? (int)h->fi_lu1[l] : 0;
+    // (a level with few of them keeps them in k_fi_lu's grid: one launch less on the chain)
+    const int nlu1 = h->lu1_kernel && h->fi_lu1[l] >= h->lu1_min ? (int)h->fi_lu1[l] : 0;
     if (nlu1) {
       CK(launchx(k_fi_lu1, dim3((nlu1 + 255) / 256), dim3(256), 0, st, pdl, h->S, Pd, h->fi, (int)h->fi_lu[l], nlu1));
       h->launches++;
