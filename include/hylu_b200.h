@@ -296,6 +296,8 @@ int hy_batched_factor_values(hy_handle *h, int64_t b, double *d_out, uintptr_t s
  *   "fanin_warp_min" items below which a level keeps its small items on the CTA kernels
  *   "fanin_maps"    0/1 (default 1): host-precomputed source maps in the update kernels
  *   "pipe_ws", "pipe_blocks": batched-pipeline shared workspace / resident CTAs
+ *   "refactor_panels" 0/1 (default 1): a refactorization launches only the panel tiles of the
+ *                   panel kernel (the L-part tiles only apply row swaps the prior inner_perm holds)
  *   "lu1_kernel"    0/1 (default 1): single-row nodes of a fan-in level perturb their pivot in a
  *                   thread-per-node kernel (k_fi_lu1) instead of a CTA each
  *   "bwd_narrow"    batched backward solve: levels with at most this many (node, group pair) tasks

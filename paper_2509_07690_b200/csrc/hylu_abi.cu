@@ -216,6 +216,7 @@ struct hy_handle {
   int pipe_blocks = 0;
   int warp_min = 256;                      // fan-in: below this many small items per level, CTA kernels only
   int64_t bwd_narrow = BWD_NARROW;         // batched backward solve: levels with at most this many tasks use BWD_WL-entry batches
+  int refactor_panels = 1;                 // refactorize launches only the panel tiles of k_fi_panel (the L-part tiles are no-ops there)
   int64_t lu1_min = 256;                   // ... for levels with at least this many single-row nodes
   int lu1_kernel = 1;                      // fan-in: single-row nodes' pivot perturbation as a thread-per-node kernel
   int pipe_order = 1;                      // claim order of the batched pipeline: 1 level-major (default), 0 diagonal, K >= 2 diagonal below level K-1 (build_segments)
@@ -250,6 +251,7 @@ struct hy_handle {
   std::vector<void *> fi_allocs;
   std::vector<int64_t> fi_lu, fi_pt, fi_xp, fi_up;   // per-level offsets
   std::vector<int64_t> fi_lu1;                       // per level: single-row nodes at the head of its LU list
+  std::vector<int64_t> fi_ptp;                       // per level: panel tiles at the head of its panel-item list
   std::vector<int64_t> fi_upbig;                     // per level: first DMMA-routed item
   std::vector<int64_t> fi_upreg;                     // per level: first per-source item
   std::vector<int64_t> fi_uprs;                      // per level: first CTA-per-item regular item
@@ -269,11 +271,12 @@ struct hy_handle {
   int64_t fi_nsrc = -1;                              // source records of the uploaded plan
   CallP *d_callp = nullptr;                          // per-call parameters (device), see k_call_set
   cudaStream_t cap_stream = nullptr;                 // graph capture stream
-  cudaGraphExec_t fi_exec = nullptr;                 // level fan-in graph (captured on first use)
+  cudaGraphExec_t fi_exec2[2] = {nullptr, nullptr};   // level fan-in graph per call kind (0 factorize, 1 refactorize; captured on first use)
+  int cur_refactor = 0;                              // kind of the call being launched (run_fanin)
   cudaGraphExec_t sv_exec = nullptr;                 // substitution levels graph
   int64_t sv_graph_launches = 0;
   const double **d_fptr = nullptr;                   // factor values of the current solve (device slot)
-  int64_t fi_graph_launches = 0;                     // kernels per graph replay
+  int64_t fi_graph_launches2[2] = {0, 0};            // kernels per graph replay
   int use_graphs = 1;                                // option "graphs"
   int use_pdl = 1;                                   // option "pdl": programmatic dependent launch in the fan-in
   // partition-based multi-RHS solve (hy_upload_partition / hy_solve_multi)
@@ -299,9 +302,11 @@ struct hy_handle {
 
 static void free_segments(hy_handle *h);
 static void drop_graph(hy_handle *h) {
-  if (h->fi_exec) cudaGraphExecDestroy(h->fi_exec);
+  for (int k = 0; k < 2; ++k) {
+    if (h->fi_exec2[k]) cudaGraphExecDestroy(h->fi_exec2[k]);
+    h->fi_exec2[k] = nullptr;
+  }
   if (h->sv_exec) cudaGraphExecDestroy(h->sv_exec);
-  h->fi_exec = nullptr;
   h->sv_exec = nullptr;
 }
 
@@ -615,6 +620,10 @@ int hy_set_option(hy_handle *h, const char *name, int64_t value) {
     h->bwd_narrow = value;
     return HY_OK;
   }
+  if (std::string(name) == "refactor_panels" && (value == 0 || value == 1)) {
+    h->refactor_panels = (int)value;
+    return HY_OK;
+  }
   if (std::string(name) == "lu1_min" && value >= 1) {
     h->lu1_min = value;
     return HY_OK;
@@ -834,9 +843,29 @@ int hy_upload_fanin_plan(hy_handle *h, const hy_fanin_plan *d) {
     }
     UPF(&p32, lun.data(), d->lu_ptr[nl]); D.lu_nodes = p32;
   }
-  UPF(&p32, d->pt_node, d->pt_ptr[nl]); D.pt_node = p32;
-  UPF(&p32, d->pt_c0, d->pt_ptr[nl]); D.pt_c0 = p32;
-  UPF(&p32, d->pt_c1, d->pt_ptr[nl]); D.pt_c1 = p32;
+  {   // per level: the panel tiles (right of the block) first, then the L-part tiles, which only
+      // apply the block's row swaps: a refactorization (prior inner_perm pre-applied) skips them
+    const int64_t npt = d->pt_ptr[nl];
+    std::vector<int32_t> idx(npt), pn(npt), pc0(npt), pc1(npt);
+    for (int64_t q = 0; q < npt; ++q) idx[q] = (int32_t)q;
+    h->fi_ptp.assign(nl, 0);
+    for (int64_t l = 0; l < nl; ++l) {
+      auto b = idx.begin() + d->pt_ptr[l], e = idx.begin() + d->pt_ptr[l + 1];
+      auto mid = std::stable_partition(b, e, [&](int32_t q) {
+        const int32_t u = d->pt_node[q];
+        return d->pt_c0[q] >= h->h_nl[u] + (h->h_first[u + 1] - h->h_first[u]);
+      });
+      h->fi_ptp[l] = (int64_t)(mid - b);
+    }
+    for (int64_t q = 0; q < npt; ++q) {
+      pn[q] = d->pt_node[idx[q]];
+      pc0[q] = d->pt_c0[idx[q]];
+      pc1[q] = d->pt_c1[idx[q]];
+    }
+    UPF(&p32, pn.data(), npt); D.pt_node = p32;
+    UPF(&p32, pc0.data(), npt); D.pt_c0 = p32;
+    UPF(&p32, pc1.data(), npt); D.pt_c1 = p32;
+  }
   UPF(&p64, d->xp_edge, d->xp_ptr[nl]); D.xp_edge = p64;
   UPF(&p32, d->xp_tgt, d->xp_ptr[nl]); D.xp_tgt = p32;
   UPF(&p32, d->up_t, d->lev_up[nl]); D.up_t = p32;
@@ -957,7 +986,7 @@ static int run_fanin(hy_handle *h, const CallP *Pd, cudaStream_t st) {
   const int nfl = (int)h->fi_lu.size() - 1;
   for (int l = 0; l < nfl; ++l) {
     const int nlu = (int)(h->fi_lu[l + 1] - h->fi_lu[l]);
-    const int npt = (int)(h->fi_pt[l + 1] - h->fi_pt[l]);
+    const int npt = h->cur_refactor && h->refactor_panels ? (int)h->fi_ptp[l] : (int)(h->fi_pt[l + 1] - h->fi_pt[l]);
     const int nxp = (int)(h->fi_xp[l + 1] - h->fi_xp[l]);
     const int nup = (int)(h->fi_up[l + 1] - h->fi_up[l]);
     // PDL on latency-bound levels only: on a level with many CTAs the successor's
@@ -1225,7 +1254,9 @@ static int fanin_scratch(hy_handle *h) {
 }
 
 static int run_fanin_graph(hy_handle *h, cudaStream_t st) {
-  if (!h->fi_exec) {
+  cudaGraphExec_t &fi_exec = h->fi_exec2[h->cur_refactor];
+  int64_t &fi_graph_launches = h->fi_graph_launches2[h->cur_refactor];
+  if (!fi_exec) {
     int rc = fanin_scratch(h);
     if (rc) return rc;
     if (!h->cap_stream) CK(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
@@ -1239,22 +1270,22 @@ static int run_fanin_graph(hy_handle *h, cudaStream_t st) {
     rc = run_fanin(h, h->d_callp, h->cap_stream);
     cudaGraph_t g = nullptr;
     cudaError_t e = cudaStreamEndCapture(h->cap_stream, &g);
-    h->fi_graph_launches = h->launches - l0;
+    fi_graph_launches = h->launches - l0;
     h->launches = l0;
     if (rc) {
       if (g) cudaGraphDestroy(g);
       return rc;
     }
     if (e != cudaSuccess) return fail(HY_CUDA_ERROR, std::string("graph capture: ") + cudaGetErrorString(e));
-    e = cudaGraphInstantiate(&h->fi_exec, g, 0);
+    e = cudaGraphInstantiate(&fi_exec, g, 0);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) {
-      h->fi_exec = nullptr;
+      fi_exec = nullptr;
       return fail(HY_CUDA_ERROR, std::string("graph instantiate: ") + cudaGetErrorString(e));
     }
   }
-  CK(cudaGraphLaunch(h->fi_exec, st));
-  h->launches += h->fi_graph_launches;
+  CK(cudaGraphLaunch(fi_exec, st));
+  h->launches += fi_graph_launches;
   return HY_OK;
 }
 
@@ -1299,6 +1330,7 @@ static int run_factor(hy_handle *h, const double *d_avals, double eps, const hy_
                                                                          h->fanin_ok ? 1 : 0);
   k_anorm_p<<<296, 256, 0, st>>>(Pd, h->S.scale, h->S.nnz);
   h->launches += 3;
+  h->cur_refactor = prior ? 1 : 0;
   if (h->fanin_ok) return h->use_graphs ? run_fanin_graph(h, st) : run_fanin(h, Pd, st);
   const Plan &pl = h->fplan;
   if (h->slab_ok) {

@@ -713,6 +713,12 @@ def test_launch_options_do_not_change_results(name):
             assert torch.equal(g.values, f.values), opt
             assert torch.equal(api.substitute(g, b), x), opt
             ctx.set_option(opt, 1)
+        # refactorize with and without the L-part panel tiles (no-ops there): bitwise equal
+        r1 = api.refactorize(p.A, f)
+        ctx.set_option("refactor_panels", 0)
+        r0 = api.refactorize(p.A, f)
+        ctx.set_option("refactor_panels", 1)
+        assert torch.equal(r0.values, r1.values) and torch.equal(r1.values, f.values)
     finally:
         for opt in ("pdl", "graphs", "fanin_overlap", "lu1_kernel"):
             ctx.set_option(opt, 1)
