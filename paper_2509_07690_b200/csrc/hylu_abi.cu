@@ -119,10 +119,9 @@ struct SolveChunk {
   int32_t slot;
 };
 __global__ void k_solve_part(DevSym, const double *const *, const SolveChunk *, int, const double *, double *, int);
-__global__ void k_fwd_fin(DevSym, const double *const *, const int32_t *, const int32_t *, const int32_t *, int,
-                          const double *, double *);
-__global__ void k_bwd_fin(DevSym, const double *const *, const int32_t *, const int32_t *, const int32_t *, int,
-                          const double *, double *);
+__global__ void k_fwd_fin(DevSym, const double *const *, const SolveRec *, int, const double *, double *);
+__global__ void k_bwd_fin(DevSym, const double *const *, const SolveRec *, int, const double *, double *);
+__global__ void k_solve_rec(DevSym, const int32_t *, const int32_t *, const int32_t *, int64_t, SolveRec *);
 __global__ void k_bwd(DevSym, const double *, const int32_t *, int, double *);
 
 size_t pipe_smem(int ws);
@@ -173,6 +172,7 @@ struct SolvePlan {
   std::vector<int64_t> cptr;         // [nlev+1] chunk offsets
   SolveChunk *d_chunks = nullptr;
   int32_t *d_slot0 = nullptr, *d_nslot = nullptr;  // per node in level order
+  SolveRec *d_rec = nullptr;                       // packed per-node records (k_solve_rec)
   int64_t nslots = 0;
 };
 
@@ -746,6 +746,13 @@ int hy_upload_symbolic(hy_handle *h, const hy_symbolic_desc *d) {
       UP(&sp.d_chunks, chunks.data(), chunks.size());
       UP(&sp.d_slot0, slot0.data(), slot0.size());
       UP(&sp.d_nslot, nslot.data(), nslot.size());
+      UP(&sp.d_rec, (const SolveRec *)nullptr, (int64_t)std::max<size_t>(slot0.size(), 1));
+      if (!slot0.empty()) {
+        k_solve_rec<<<(unsigned)std::min<int64_t>(((int64_t)slot0.size() + 255) / 256, 4096), 256>>>(
+            h->S, (dir == 0 ? h->fplan : h->bplan).d_all, sp.d_slot0, sp.d_nslot, (int64_t)slot0.size(), sp.d_rec);
+        CK(cudaGetLastError());
+        CK(cudaDeviceSynchronize());
+      }
     }
     const int64_t ns = (h->fsolve.nslots > h->bsolve.nslots ? h->fsolve.nslots : h->bsolve.nslots);
     UP(&h->d_solve_scratch, (const double *)nullptr, (ns > 0 ? ns : 1) * 64);
@@ -1568,8 +1575,7 @@ static int solve_levels(hy_handle *h, cudaStream_t st) {
         h->launches++;
       }
       CK(launchx(dir == 0 ? k_fwd_fin : k_bwd_fin, dim3((c + 3) / 4), dim3(128), 0, st, h->use_pdl, h->S,
-                 (const double *const *)h->d_fptr, (const int32_t *)(pl.d_all + pl.aptr[l]),
-                 (const int32_t *)(sp.d_slot0 + pl.aptr[l]), (const int32_t *)(sp.d_nslot + pl.aptr[l]), c,
+                 (const double *const *)h->d_fptr, (const SolveRec *)(sp.d_rec + pl.aptr[l]), c,
                  (const double *)h->d_solve_scratch, h->d_y));
       h->launches++;
     }

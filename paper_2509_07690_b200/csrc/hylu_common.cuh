@@ -56,6 +56,15 @@ struct __align__(16) NodeItemRec {
   int32_t c0, c1;   // panel tile columns (LU items: unused)
 };
 
+// Node of a substitution level, packed once per symbolic upload (k_solve_rec): layout,
+// column list and partial-sum slots in one record instead of a dependent metadata round.
+struct __align__(16) SolveRec {
+  int64_t valoff, col0;   // factor values / first entry of the node's column list
+  int32_t r, s, W, L;
+  int32_t slot0, nslot;   // partial sums of the level's chunk kernel
+  int32_t pad[2];
+};
+
 struct __align__(16) ItemRec {
   int64_t valoff;   // target node's value offset
   int64_t zb;       // first source record

@@ -720,21 +720,18 @@ __device__ __forceinline__ void offblock_dots(const double *Fu, int W, const int
   }
 }
 
-__global__ void k_fwd_fin(DevSym S, const double *const *Fp, const int32_t *nodes, const int32_t *slot0,
-                          const int32_t *nslot, int count, const double *scratch, double *y) {
+__global__ void k_fwd_fin(DevSym S, const double *const *Fp, const SolveRec *recs, int count,
+                          const double *scratch, double *y) {
   pdl_wait();
   pdl_launch_dependents();
   const double *F = *Fp;   // factor values of this call (device-resident pointer: graph replay)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int idx = blockIdx.x * (blockDim.x >> 5) + warp;
   if (idx >= count) return;
-  const int u = nodes[idx];
-  const int r = (int)S.first[u];
-  const int s = (int)(S.first[u + 1] - r);
-  const int W = (int)(S.colptr[u + 1] - S.colptr[u]);
-  const int L = S.nl[u];
-  const double *Fu = F + S.valoff[u];
-  const int a0 = slot0[idx], an = nslot[idx];
+  const SolveRec sr = recs[idx];
+  const int r = sr.r, s = sr.s, W = sr.W, L = sr.L;
+  const double *Fu = F + sr.valoff;
+  const int a0 = sr.slot0, an = sr.nslot;
   double mine0 = 0.0, mine1 = 0.0;
   if (lane < s) {
     double acc = y[r + lane];
@@ -747,7 +744,7 @@ __global__ void k_fwd_fin(DevSym S, const double *const *Fp, const int32_t *node
     mine1 = acc;
   }
   if (an == 0 && L > 0)   // small node: the warp computes the off-block dot products itself
-    offblock_dots(Fu, W, S.cols + S.colptr[u], y, 0, L, s, lane, mine0, mine1);
+    offblock_dots(Fu, W, S.cols + sr.col0, y, 0, L, s, lane, mine0, mine1);
   // in-block unit-lower solve; each lane's block-row entries are loaded 8 columns
   // at a time (all in flight together) instead of one dependent load per step
   const int t0 = lane, t1 = lane + 32;
@@ -773,22 +770,37 @@ __global__ void k_fwd_fin(DevSym S, const double *const *Fp, const int32_t *node
   if (lane + 32 < s) y[r + lane + 32] = mine1;
 }
 
+__global__ void k_solve_rec(DevSym S, const int32_t *nodes, const int32_t *slot0, const int32_t *nslot, int64_t count,
+                            SolveRec *out) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < count; j += (int64_t)gridDim.x * blockDim.x) {
+    const int u = nodes[j];
+    SolveRec r;
+    r.valoff = S.valoff[u];
+    r.col0 = S.colptr[u];
+    r.r = (int32_t)S.first[u];
+    r.s = (int32_t)(S.first[u + 1] - S.first[u]);
+    r.W = (int32_t)(S.colptr[u + 1] - S.colptr[u]);
+    r.L = S.nl[u];
+    r.slot0 = slot0[j];
+    r.nslot = nslot[j];
+    r.pad[0] = r.pad[1] = 0;
+    out[j] = r;
+  }
+}
+
 // backward finish: z_t = (y_t - sum(partials) - sum_{tt>t} U[t][tt] z_tt) / U[t][t]
-__global__ void k_bwd_fin(DevSym S, const double *const *Fp, const int32_t *nodes, const int32_t *slot0,
-                          const int32_t *nslot, int count, const double *scratch, double *y) {
+__global__ void k_bwd_fin(DevSym S, const double *const *Fp, const SolveRec *recs, int count,
+                          const double *scratch, double *y) {
   pdl_wait();
   pdl_launch_dependents();
   const double *F = *Fp;   // factor values of this call (device-resident pointer: graph replay)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int idx = blockIdx.x * (blockDim.x >> 5) + warp;
   if (idx >= count) return;
-  const int u = nodes[idx];
-  const int r = (int)S.first[u];
-  const int s = (int)(S.first[u + 1] - r);
-  const int W = (int)(S.colptr[u + 1] - S.colptr[u]);
-  const int L = S.nl[u];
-  const double *Fu = F + S.valoff[u];
-  const int a0 = slot0[idx], an = nslot[idx];
+  const SolveRec sr = recs[idx];
+  const int r = sr.r, s = sr.s, W = sr.W, L = sr.L;
+  const double *Fu = F + sr.valoff;
+  const int a0 = sr.slot0, an = sr.nslot;
   double mine0 = 0.0, mine1 = 0.0;
   if (lane < s) {
     double acc = y[r + lane];
@@ -801,7 +813,7 @@ __global__ void k_bwd_fin(DevSym S, const double *const *Fp, const int32_t *node
     mine1 = acc;
   }
   if (an == 0 && L + s < W)
-    offblock_dots(Fu, W, S.cols + S.colptr[u], y, L + s, W, s, lane, mine0, mine1);
+    offblock_dots(Fu, W, S.cols + sr.col0, y, L + s, W, s, lane, mine0, mine1);
   // in-block upper solve (descending), entries loaded 8 columns at a time; the
   // diagonal entry of row tt is in its own lane's block (k = tt - b0)
   const int t0 = lane, t1 = lane + 32;
