@@ -391,7 +391,10 @@ __device__ __forceinline__ void d_fi_x_w(DevSym S, const CallP *__restrict__ Pd,
   for (int a = 0; a < XW_M; ++a)
     if (a < m) row[a] = xr[a];
 }
-__global__ void __launch_bounds__(FI_THREADS) k_fi_x_w(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base, int count) { d_fi_x_w(S, Pd, D, base, count, blockIdx.x); }
+#ifndef XW_MINB
+#define XW_MINB 6   // 40 registers: 48 resident warps/SM for the warp-per-item X kernel (c1 -1 %)
+#endif
+__global__ void __launch_bounds__(FI_THREADS, XW_MINB) k_fi_x_w(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base, int count) { d_fi_x_w(S, Pd, D, base, count, blockIdx.x); }
 
 // Warp-per-item tile updates for small targets (<= 4 rows): lanes over the
 // source's columns in the tile; per source c = Σ_a X[t][a] U[a][q] (ascending a,
@@ -475,7 +478,10 @@ __device__ __forceinline__ void d_fi_upd_w(DevSym S, const CallP *__restrict__ P
   for (int c = lane; c < tw; c += 32)
     for (int t = 0; t < s; ++t) Pm[(int64_t)t * W + c0 + c] = acc[t * UW_TILE + c];
 }
-__global__ void __launch_bounds__(FI_THREADS) k_fi_upd_w(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base, int count) { d_fi_upd_w(S, Pd, D, base, count, blockIdx.x); }
+#ifndef UPDW_MINB
+#define UPDW_MINB 5   // 48 registers: 40 resident warps/SM for the warp-per-item update kernel (c1 3.67 -> 3.58 ms; 6 / 8 spill and are slower)
+#endif
+__global__ void __launch_bounds__(FI_THREADS, UPDW_MINB) k_fi_upd_w(DevSym S, const CallP *__restrict__ Pd, FaninDev D, int base, int count) { d_fi_upd_w(S, Pd, D, base, count, blockIdx.x); }
 
 // ---------------------------------------------------------------------------- updates
 constexpr int FI_TILE = 64;
