@@ -981,8 +981,11 @@ __global__ void __launch_bounds__(BW * 32) k_batch_fwd(DevSym S, const double *B
 
 // Pair mode backward substitution: one warp per (node, group pair); the padded
 // allocation makes the odd tail group's partner valid memory (never copied out).
+#ifndef BWD_MINB
+#define BWD_MINB 10   // 48 registers for the 2-entry form: more resident warps on the wide (throughput-bound) levels (c4 14.45 -> 14.19 ms; 12: 14.30, 16: 14.41)
+#endif
 template <int BWDW>
-__global__ void __launch_bounds__(BW * 32) k_batch_bwd2(DevSym S, const double *BF, int64_t stored,
+__global__ void __launch_bounds__(BW * 32, BWDW <= 2 ? BWD_MINB : 1) k_batch_bwd2(DevSym S, const double *BF, int64_t stored,
                                                         const int32_t *nodes, int count, int GP,
                                                         double *Y) {
   pdl_wait();
