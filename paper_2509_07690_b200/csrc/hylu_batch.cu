@@ -18,7 +18,7 @@ namespace hy {
 constexpr int BW = 4;
 // warps per block (bwd / fwd kernels); BWD_W / BWD_WL (hylu_common.cuh): backward-solve entries per batch
 #ifndef HUB_THREADS_DEF
-#define HUB_THREADS_DEF 768   // 512: 17.56 ms/step, 768: 17.41, 1024: 17.43 (c4, round 2)
+#define HUB_THREADS_DEF 768   // c4 ms/step, round-2 final kernels: 512: 14.37, 640: 14.29, 768: 14.14-14.17, 1024: 14.75
 #endif
 constexpr int HUB_THREADS = HUB_THREADS_DEF;
 int hub_threads() { return HUB_THREADS; }
@@ -982,7 +982,7 @@ __global__ void __launch_bounds__(BW * 32) k_batch_fwd(DevSym S, const double *B
 // Pair mode backward substitution: one warp per (node, group pair); the padded
 // allocation makes the odd tail group's partner valid memory (never copied out).
 #ifndef BWD_MINB
-#define BWD_MINB 10   // 48 registers for the 2-entry form: more resident warps on the wide (throughput-bound) levels (c4 14.45 -> 14.19 ms; 12: 14.30, 16: 14.41)
+#define BWD_MINB 10   // 48 registers for the 2-entry form: more resident warps on the wide (throughput-bound) levels (c4 14.45 -> 14.19 ms; 12: 14.30, 16: 14.41; re-swept at the end: 8: 14.68, 9: 14.16, 10: 14.14-14.17, 11: 14.26)
 #endif
 template <int BWDW>
 __global__ void __launch_bounds__(BW * 32, BWDW <= 2 ? BWD_MINB : 1) k_batch_bwd2(DevSym S, const double *BF, int64_t stored,
