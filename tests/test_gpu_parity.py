@@ -741,3 +741,28 @@ def test_launch_options_do_not_change_results(name):
             c4.set_option("pdl", 1)
             c4.set_option("pipe_ws", 6)
             c4.set_option("pipe_order", 1)
+
+
+def test_batched_edge_sizes_match_oracle():
+    """Ragged batches: one instance, one short of a group, exactly one group pair, one past
+    it — each against the oracle on the same instances; an empty batch and mismatched
+    shapes are rejected (ABI: batch size outside [1, 65535])."""
+    from paper_2509_07690_b200._ref import errors
+    from paper_2509_07690_b200.device import DeviceError
+    bp = gen.circuit_batch(65, 1500, 2, 150)
+    an = an_mod.analyze(bp.A0, SolverConfig(ordering="amd"))
+    on = _oracle()
+    prior = api.factorize_analysis(an)
+    oprior = on.factorize(an)
+    Xo, npo = on.refactor_solve_batch(an, oprior, bp.values, bp.rhs)
+    for B in (1, 31, 64, 65):
+        X, npert = api.refactorize_solve_batched(bp.values[:B], prior, bp.rhs[:B])
+        assert X.shape == (B, bp.A0.n)
+        assert _rel(X, Xo[:B]) <= 1e-9
+        assert np.array_equal(npert, npo[:B])
+    with pytest.raises(DeviceError):
+        api.refactorize_solve_batched(bp.values[:0], prior, bp.rhs[:0])
+    with pytest.raises(errors.DimensionMismatch):
+        api.refactorize_solve_batched(bp.values[:4], prior, bp.rhs[:3])
+    with pytest.raises(errors.DimensionMismatch):
+        api.refactorize_solve_batched(bp.values[:4, :-1], prior, bp.rhs[:4])
