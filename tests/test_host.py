@@ -151,6 +151,15 @@ def test_c_abi_library_exports_every_header_symbol():
         assert hasattr(lib, nm), nm
 
 
+def test_integration_doc_names_every_header_symbol():
+    """INTEGRATION.md (the reference-side binding) covers the whole C ABI."""
+    hdr = open(os.path.join(ROOT, "include", "hylu_b200.h")).read()
+    doc = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    names = set(re.findall(r"\b(hy_[a-z_]+)\s*\(", hdr))
+    missing = sorted(nm for nm in names if nm not in doc)
+    assert not missing, missing
+
+
 def _run_fanin_cpu(an, plan):
     """CPU interpreter of the level fan-in plan (the device kernels' arithmetic)."""
     s = an.symbolic
