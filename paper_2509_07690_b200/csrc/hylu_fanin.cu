@@ -940,6 +940,9 @@ __global__ void __launch_bounds__(FI_THREADS, 3) k_fi_upd_tc(DevSym S, const Cal
 // ascending (source, row) order, then one subtraction — the packed kernel's order.
 
 constexpr int KC_ULD = 68;
+// Tile knobs, re-swept on the round-2 final kernels (factor ms, c2 / c3 k=32; defaults 286.9 / 107.3):
+// KC_MINB 2: 324.5 / 118.1, 4: 315.2 / 115.8 (spills); KC_CHUNK 16: 297.0 / 115.0; KC_BIG 8: 288.1 / 107.4,
+// 32: 286.9 / 107.2; KC_NSB 8: 289.5 / 107.7, 32: 288.6 / 107.6 (profiles/r02_kc_knob_sweep_final.txt).
 #ifndef KC_NSB_DEF
 #define KC_NSB_DEF 16
 #endif
