@@ -32,7 +32,8 @@ def timed(fn, reps=5):
 
 def single(name, p):
     t0 = time.perf_counter()
-    an = an_mod.analyze(p.A, SolverConfig(ordering=p.ordering))
+    cap = int(os.environ.get("PROBE_SUPCAP", 64))   # SolverConfig.max_supernode_rows (SPEC default 64)
+    an = an_mod.analyze(p.A, SolverConfig(ordering=p.ordering, max_supernode_rows=cap))
     ta = time.perf_counter() - t0
     s = an.symbolic
     dv = torch.from_numpy(np.array(p.A.values)).cuda()
